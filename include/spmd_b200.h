@@ -1,0 +1,195 @@
+/*
+ * spmd_b200.h -- C ABI of the B200-native GSPMD partitioned-execution hot path.
+ *
+ * The reference (minispmd, pure Python/NumPy) executes a partitioned program
+ * with `evaluate_spmd` (minispmd/simulator.py:393-426), dispatching every
+ * instruction to `evaluate_instruction` (simulator.py:157-301) and every
+ * collective to `_collective` (simulator.py:333-390).  This library replaces
+ * both: one entry point per instruction family, plain pointers and sizes, no
+ * torch types.  A ctypes binding of exactly these symbols is what a
+ * maintainer would add to the reference.
+ *
+ * Conventions
+ *  - Every tensor is dense row-major and *partition-stacked*: the buffer holds
+ *    `nparts` consecutive per-partition tensors of shape dims[0..rank).  With
+ *    one process per GPU nparts == 1 and the partition id is the rank; on one
+ *    GPU simulating an N-device mesh nparts == N (reference lockstep
+ *    semantics, simulator.py:412-425).
+ *  - Scalars consumed per partition (pad value, reduce init, dynamic-slice
+ *    start indices) are rank-0 tensors, i.e. `nparts` values.
+ *  - All calls are asynchronous on the caller's `cudaStream_t` (passed as
+ *    void*).  Status codes are returned synchronously for argument errors;
+ *    device-side faults (integer divide by zero, simulator.py:63-69) set a
+ *    device error word read back by spmd_check_device_errors().
+ *  - The library never frees caller memory.
+ */
+#ifndef SPMD_B200_H_
+#define SPMD_B200_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SPMD_MAX_RANK 8
+#define SPMD_MAX_PARTS 64
+
+/* IR dtypes (reference ir.py:19-23 plus BF16). */
+typedef enum {
+  SPMD_F32 = 0, SPMD_S32 = 1, SPMD_U32 = 2, SPMD_PRED = 3, SPMD_BF16 = 4
+} spmd_dtype;
+
+/* Status codes.  The Python shim maps them onto the reference's exception
+ * classes (simulator.py:33-42, sharding.py:27-58, partitioner.py:44-53). */
+typedef enum {
+  SPMD_OK = 0,
+  SPMD_ERR_INVALID = 1,      /* bad argument                     -> EvalError */
+  SPMD_ERR_SHAPE = 2,        /* inconsistent shapes              -> EvalError */
+  SPMD_ERR_SUBGROUP = 3,     /* groups/pairs do not partition    -> SubgroupMismatch */
+  SPMD_ERR_DIV_ZERO = 4,     /* integer division by zero         -> DivideByZero */
+  SPMD_ERR_CUDA = 5,
+  SPMD_ERR_NCCL = 6,
+  SPMD_ERR_UNSUPPORTED = 7
+} spmd_status;
+
+typedef struct {
+  void* data;
+  int32_t dtype;   /* spmd_dtype */
+  int32_t rank;    /* per-partition rank, <= SPMD_MAX_RANK */
+  int64_t dims[SPMD_MAX_RANK];
+} spmd_tensor;
+
+/* Opcodes of the elementwise families (values of ir.Op order). */
+typedef enum { SPMD_NEGATE = 0, SPMD_EXP = 1, SPMD_RELU = 2 } spmd_unary_op;
+typedef enum {
+  SPMD_ADD = 0, SPMD_MULTIPLY = 1, SPMD_MAXIMUM = 2, SPMD_SUBTRACT = 3,
+  SPMD_DIVIDE = 4, SPMD_COMPARE = 5
+} spmd_binary_op;
+typedef enum { SPMD_EQ = 0, SPMD_NE = 1, SPMD_LT = 2, SPMD_LE = 3, SPMD_GT = 4, SPMD_GE = 5 } spmd_cmp;
+typedef enum { SPMD_SUM = 0, SPMD_MAX = 1, SPMD_MIN = 2, SPMD_PROD = 3 } spmd_reduce_kind;
+
+/* ---- library ------------------------------------------------------------ */
+const char* spmd_version(void);
+const char* spmd_status_string(int status);
+const char* spmd_last_error(void);
+/* Reads and clears the device error word; returns SPMD_ERR_DIV_ZERO if an
+ * integer division by zero happened since the last call. Synchronises stream. */
+int spmd_check_device_errors(void* stream);
+/* Number of kernels this library has launched (for launch accounting). */
+int64_t spmd_launch_count(void);
+
+/* ---- sources (simulator.py:161-172) ---------------------------------------- */
+int spmd_iota(spmd_tensor out, int axis, int64_t nparts, void* stream);
+int spmd_partition_id(spmd_tensor out, int64_t nparts, int32_t first_id, void* stream);
+/* Broadcast one host literal (rank `lit.rank`, `lit.data` on the HOST) to all
+ * partitions of `out`. */
+int spmd_constant(spmd_tensor lit_host, spmd_tensor out, int64_t nparts, void* stream);
+
+/* ---- elementwise (simulator.py:173-198) ------------------------------------ */
+int spmd_unary(int op, spmd_tensor in, spmd_tensor out, int64_t nparts, void* stream);
+int spmd_binary(int op, int cmp, spmd_tensor a, spmd_tensor b, spmd_tensor out,
+                int64_t nparts, void* stream);
+int spmd_select(spmd_tensor pred, spmd_tensor on_true, spmd_tensor on_false,
+                spmd_tensor out, int64_t nparts, void* stream);
+/* dtype conversion (host I/O helper; not an IR op). */
+int spmd_convert(spmd_tensor in, spmd_tensor out, int64_t nparts, void* stream);
+
+/* ---- data movement (simulator.py:199-241, 278-300) ------------------------- */
+int spmd_broadcast(spmd_tensor in, spmd_tensor out, const int32_t* broadcast_dims,
+                   int64_t nparts, void* stream);
+int spmd_transpose(spmd_tensor in, spmd_tensor out, const int32_t* perm,
+                   int64_t nparts, void* stream);
+int spmd_reverse(spmd_tensor in, spmd_tensor out, const int32_t* dims, int ndims,
+                 int64_t nparts, void* stream);
+int spmd_pad(spmd_tensor in, spmd_tensor value, spmd_tensor out, const int64_t* low,
+             const int64_t* high, const int64_t* interior, int64_t nparts, void* stream);
+int spmd_slice(spmd_tensor in, spmd_tensor out, const int64_t* starts,
+               const int64_t* strides, int64_t nparts, void* stream);
+/* Start indices are clamped to [0, dim - size] (XLA semantics, simulator.py:227). */
+int spmd_dynamic_slice(spmd_tensor in, const spmd_tensor* starts, spmd_tensor out,
+                       int64_t nparts, void* stream);
+int spmd_dynamic_update_slice(spmd_tensor in, spmd_tensor update,
+                              const spmd_tensor* starts, spmd_tensor out,
+                              int64_t nparts, void* stream);
+int spmd_concat(const spmd_tensor* ins, int n, int axis, spmd_tensor out,
+                int64_t nparts, void* stream);
+int spmd_rotate(spmd_tensor in, spmd_tensor out, int dim, int64_t amount,
+                int64_t nparts, void* stream);
+int spmd_shift(spmd_tensor in, spmd_tensor fill, spmd_tensor out, int dim,
+               int64_t amount, int64_t nparts, void* stream);
+
+/* ---- reductions (simulator.py:242-257) ------------------------------------- */
+int spmd_reduce(spmd_tensor in, spmd_tensor init, spmd_tensor out, const int32_t* dims,
+                int ndims, int kind, int64_t nparts, void* stream);
+
+/* ---- contractions (simulator.py:258-277) ------------------------------------
+ * Generalised dot: out[batch, lhs_free, rhs_free] = sum_k lhs*rhs.  BF16 runs on
+ * tcgen05 tensor cores (fp32 TMEM accumulation); F32 accumulates in fp64 and
+ * integers in int64 (as the reference), rounding once. */
+typedef struct {
+  int32_t n_batch, n_contract;
+  int32_t lhs_batch[SPMD_MAX_RANK], rhs_batch[SPMD_MAX_RANK];
+  int32_t lhs_contracting[SPMD_MAX_RANK], rhs_contracting[SPMD_MAX_RANK];
+  int32_t epilogue;      /* 0 none, 1 relu (fused; executor-level fusion) */
+} spmd_dot_dims;
+int spmd_dot(spmd_tensor lhs, spmd_tensor rhs, spmd_tensor out, const spmd_dot_dims* dd,
+             int64_t nparts, void* stream);
+
+typedef struct {
+  int32_t lhs_batch, lhs_feature, rhs_in_feature, rhs_out_feature, out_batch, out_feature;
+  int32_t n_spatial;
+  int32_t lhs_spatial[SPMD_MAX_RANK], rhs_spatial[SPMD_MAX_RANK], out_spatial[SPMD_MAX_RANK];
+  int32_t size[SPMD_MAX_RANK], stride[SPMD_MAX_RANK], pad_low[SPMD_MAX_RANK],
+          pad_high[SPMD_MAX_RANK], base_dilation[SPMD_MAX_RANK], window_dilation[SPMD_MAX_RANK];
+} spmd_conv_dims;
+int spmd_convolution(spmd_tensor lhs, spmd_tensor rhs, spmd_tensor out,
+                     const spmd_conv_dims* cd, int64_t nparts, void* stream);
+
+/* ---- fused kernels selected by the executor (same semantics as the op chain) */
+/* Row softmax over the last dim: out = exp(x - max) / sum(exp(x - max)). */
+int spmd_softmax_lastdim(spmd_tensor in, spmd_tensor out, int64_t nparts, void* stream);
+
+/* ---- loopback collectives: all partitions resident on this GPU ---------------
+ * (simulator.py:333-390 semantics; groups is a flat [ngroups*gsize] table in
+ * group order; reductions fold serially in group order, so integer and float
+ * results are bit-identical to the reference). */
+int spmd_local_all_gather(spmd_tensor in, spmd_tensor out, int dim, const int32_t* groups,
+                          int ngroups, int gsize, int64_t nparts, void* stream);
+int spmd_local_all_reduce(spmd_tensor in, spmd_tensor out, int kind, const int32_t* groups,
+                          int ngroups, int gsize, int64_t nparts, void* stream);
+int spmd_local_reduce_scatter(spmd_tensor in, spmd_tensor out, int dim, int kind,
+                              const int32_t* groups, int ngroups, int gsize,
+                              int64_t nparts, void* stream);
+int spmd_local_all_to_all(spmd_tensor in, spmd_tensor out, int split_dim, int concat_dim,
+                          const int32_t* groups, int ngroups, int gsize, int64_t nparts,
+                          void* stream);
+/* pairs: flat [npairs*2] (source, target); non-targets receive zeros. */
+int spmd_local_collective_permute(spmd_tensor in, spmd_tensor out, const int32_t* pairs,
+                                  int npairs, int64_t nparts, void* stream);
+
+/* ---- NCCL collectives: one process per GPU over NVLink/NVSwitch -------------- */
+typedef struct spmd_comm spmd_comm;
+int spmd_comm_id_bytes(void);
+int spmd_comm_get_unique_id(void* id_out);
+int spmd_comm_init(spmd_comm** comm, int nranks, int rank, const void* unique_id);
+int spmd_comm_destroy(spmd_comm* comm);
+/* Scratch used for pack/unpack of non-leading-dim collectives (device memory
+ * owned by the caller, >= 2x the largest collective buffer). */
+int spmd_comm_set_workspace(spmd_comm* comm, void* ptr, int64_t bytes);
+int spmd_all_gather(spmd_comm* comm, spmd_tensor in, spmd_tensor out, int dim,
+                    const int32_t* groups, int ngroups, int gsize, void* stream);
+int spmd_all_reduce(spmd_comm* comm, spmd_tensor in, spmd_tensor out, int kind,
+                    const int32_t* groups, int ngroups, int gsize, void* stream);
+int spmd_reduce_scatter(spmd_comm* comm, spmd_tensor in, spmd_tensor out, int dim, int kind,
+                        const int32_t* groups, int ngroups, int gsize, void* stream);
+int spmd_all_to_all(spmd_comm* comm, spmd_tensor in, spmd_tensor out, int split_dim,
+                    int concat_dim, const int32_t* groups, int ngroups, int gsize,
+                    void* stream);
+int spmd_collective_permute(spmd_comm* comm, spmd_tensor in, spmd_tensor out,
+                            const int32_t* pairs, int npairs, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SPMD_B200_H_ */

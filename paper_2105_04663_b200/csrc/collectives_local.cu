@@ -1,0 +1,248 @@
+// Loopback collectives: all partitions of a simulated mesh resident on ONE
+// GPU (partition-stacked buffers).  Exact reference semantics
+// (simulator.py:333-390): all-gather concatenates in subgroup order;
+// all-reduce / reduce-scatter fold serially in subgroup order (so float
+// results are bit-identical to the reference, not just within tolerance);
+// all-to-all splits evenly and concatenates in group order; collective-permute
+// zero-fills non-targets.  NCCL refuses two ranks on one GPU, so this is the
+// comm backend for single-GPU parity runs -- still GPU-only.
+#include "common.cuh"
+
+#include <string.h>
+
+namespace spmd {
+
+struct GroupTab {
+  int P, gsize;
+  int8_t gid[SPMD_MAX_PARTS];
+  int8_t gpos[SPMD_MAX_PARTS];
+  int8_t members[SPMD_MAX_PARTS];   // [ngroups][gsize]
+};
+
+static int make_groups(const int32_t* groups, int ngroups, int gsize, int64_t nparts,
+                       GroupTab& g) {
+  if (nparts > SPMD_MAX_PARTS || ngroups * gsize != nparts) {
+    set_error("subgroups do not partition the devices");
+    return SPMD_ERR_SUBGROUP;
+  }
+  memset(&g, -1, sizeof(g));
+  g.P = (int)nparts;
+  g.gsize = gsize;
+  for (int i = 0; i < ngroups * gsize; ++i) {
+    int d = groups[i];
+    if (d < 0 || d >= nparts || g.gid[d] != -1) {
+      set_error("subgroups do not partition the devices");
+      return SPMD_ERR_SUBGROUP;
+    }
+    g.gid[d] = (int8_t)(i / gsize);
+    g.gpos[d] = (int8_t)(i % gsize);
+    g.members[i] = (int8_t)d;
+  }
+  return SPMD_OK;
+}
+
+struct View {
+  int rank;
+  int64_t d[SPMD_MAX_RANK];
+};
+
+static View view_of(const spmd_tensor& t) {
+  View v;
+  v.rank = t.rank;
+  for (int i = 0; i < SPMD_MAX_RANK; ++i) v.d[i] = i < t.rank ? t.dims[i] : 1;
+  return v;
+}
+
+__device__ __forceinline__ void unravel_v(int64_t r, const View& v, int64_t* c) {
+  for (int i = v.rank - 1; i >= 0; --i) {
+    c[i] = r % v.d[i];
+    r /= v.d[i];
+  }
+}
+__device__ __forceinline__ int64_t ravel_v(const int64_t* c, const View& v) {
+  int64_t o = 0;
+  for (int i = 0; i < v.rank; ++i) o = o * v.d[i] + c[i];
+  return o;
+}
+
+enum { K_AG = 0, K_A2A = 1, K_CP = 2 };
+
+struct MoveArgs {
+  int kind;
+  View in, out, piece;
+  int dim, split, concat;
+  int8_t src_of[SPMD_MAX_PARTS];   // collective-permute: source partition or -1
+};
+
+template <typename T>
+__global__ void local_move_kernel(const T* __restrict__ in, T* __restrict__ out, MoveArgs a,
+                                  GroupTab g, int64_t n_out, int64_t n_in) {
+  const int64_t total = n_out * g.P;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    int p = (int)(idx / n_out);
+    int64_t r = idx - (int64_t)p * n_out;
+    int64_t c[SPMD_MAX_RANK];
+    unravel_v(r, a.out, c);
+    int src;
+    if (a.kind == K_CP) {
+      src = a.src_of[p];
+      if (src < 0) {
+        out[idx] = T(0);
+        continue;
+      }
+    } else if (a.kind == K_AG) {
+      int64_t nd = a.in.d[a.dim];
+      int j = (int)(c[a.dim] / nd);
+      c[a.dim] -= j * nd;
+      src = g.members[g.gid[p] * g.gsize + j];
+    } else {   // all-to-all
+      int64_t pc = a.piece.d[a.concat];
+      int j = (int)(c[a.concat] / pc);
+      c[a.concat] -= j * pc;
+      c[a.split] += (int64_t)g.gpos[p] * a.piece.d[a.split];
+      src = g.members[g.gid[p] * g.gsize + j];
+    }
+    out[idx] = in[(int64_t)src * n_in + ravel_v(c, a.in)];
+  }
+}
+
+template <typename T>
+__global__ void local_reduce_kernel(const T* __restrict__ in, T* __restrict__ out, View vin,
+                                    View vout, int dim, int scatter, int kind, GroupTab g,
+                                    int64_t n_out, int64_t n_in) {
+  typedef typename Compute<T>::type C;
+  const int64_t total = n_out * g.P;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    int p = (int)(idx / n_out);
+    int64_t r = idx - (int64_t)p * n_out;
+    int64_t c[SPMD_MAX_RANK];
+    unravel_v(r, vout, c);
+    if (scatter) c[dim] += (int64_t)g.gpos[p] * vout.d[dim];
+    int64_t off = ravel_v(c, vin);
+    const int8_t* mem = g.members + g.gid[p] * g.gsize;
+    C acc = ld<T>(in[(int64_t)mem[0] * n_in + off]);
+    for (int j = 1; j < g.gsize; ++j)   // serial fold in group order
+      acc = combine<C>(kind, acc, ld<T>(in[(int64_t)mem[j] * n_in + off]));
+    out[idx] = st<T>(acc);
+  }
+}
+
+template <typename T>
+static int launch_move(const spmd_tensor& in, const spmd_tensor& out, MoveArgs& a, GroupTab& g,
+                       cudaStream_t s) {
+  int64_t n_out = numel(out), n_in = numel(in);
+  if (n_out * g.P == 0) return SPMD_OK;
+  local_move_kernel<T><<<grid_for(n_out * g.P, 256, 2), 256, 0, s>>>((const T*)in.data,
+                                                                     (T*)out.data, a, g, n_out,
+                                                                     n_in);
+  return launched(s);
+}
+
+}  // namespace spmd
+
+using namespace spmd;
+
+extern "C" int spmd_local_all_gather(spmd_tensor in, spmd_tensor out, int dim,
+                                     const int32_t* groups, int ngroups, int gsize,
+                                     int64_t nparts, void* stream) {
+  SPMD_CHECK_ARG(in.dtype == out.dtype && dim >= 0 && dim < in.rank, "all-gather mismatch");
+  SPMD_CHECK_ARG(out.dims[dim] == in.dims[dim] * gsize, "all-gather output shape mismatch");
+  GroupTab g;
+  int rc = make_groups(groups, ngroups, gsize, nparts, g);
+  if (rc) return rc;
+  MoveArgs a;
+  memset(&a, 0, sizeof(a));
+  a.kind = K_AG;
+  a.in = view_of(in);
+  a.out = view_of(out);
+  a.dim = dim;
+  SPMD_DISPATCH_BYTES(in.dtype, T, return launch_move<T>(in, out, a, g, as_stream(stream)));
+  return SPMD_OK;
+}
+
+extern "C" int spmd_local_all_to_all(spmd_tensor in, spmd_tensor out, int split_dim,
+                                     int concat_dim, const int32_t* groups, int ngroups,
+                                     int gsize, int64_t nparts, void* stream) {
+  SPMD_CHECK_ARG(in.dtype == out.dtype, "all-to-all dtype mismatch");
+  SPMD_CHECK_ARG(in.dims[split_dim] % gsize == 0, "all-to-all split dim not divisible");
+  GroupTab g;
+  int rc = make_groups(groups, ngroups, gsize, nparts, g);
+  if (rc) return rc;
+  MoveArgs a;
+  memset(&a, 0, sizeof(a));
+  a.kind = K_A2A;
+  a.in = view_of(in);
+  a.out = view_of(out);
+  a.piece = a.in;
+  a.piece.d[split_dim] /= gsize;
+  a.split = split_dim;
+  a.concat = concat_dim;
+  SPMD_DISPATCH_BYTES(in.dtype, T, return launch_move<T>(in, out, a, g, as_stream(stream)));
+  return SPMD_OK;
+}
+
+extern "C" int spmd_local_collective_permute(spmd_tensor in, spmd_tensor out,
+                                             const int32_t* pairs, int npairs, int64_t nparts,
+                                             void* stream) {
+  SPMD_CHECK_ARG(in.dtype == out.dtype && numel(in) == numel(out), "permute mismatch");
+  SPMD_CHECK_ARG(nparts <= SPMD_MAX_PARTS, "too many partitions");
+  MoveArgs a;
+  memset(&a, 0, sizeof(a));
+  memset(a.src_of, -1, sizeof(a.src_of));
+  bool src_seen[SPMD_MAX_PARTS] = {false};
+  for (int i = 0; i < npairs; ++i) {
+    int sdev = pairs[2 * i], tdev = pairs[2 * i + 1];
+    if (sdev < 0 || sdev >= nparts || tdev < 0 || tdev >= nparts || a.src_of[tdev] != -1 ||
+        src_seen[sdev]) {
+      set_error("collective-permute pairs must have distinct sources and distinct targets");
+      return SPMD_ERR_SUBGROUP;
+    }
+    a.src_of[tdev] = (int8_t)sdev;
+    src_seen[sdev] = true;
+  }
+  a.kind = K_CP;
+  a.in = view_of(in);
+  a.out = view_of(out);
+  GroupTab g;
+  memset(&g, 0, sizeof(g));
+  g.P = (int)nparts;
+  g.gsize = 1;
+  SPMD_DISPATCH_BYTES(in.dtype, T, return launch_move<T>(in, out, a, g, as_stream(stream)));
+  return SPMD_OK;
+}
+
+static int local_reduce(spmd_tensor in, spmd_tensor out, int dim, int scatter, int kind,
+                        const int32_t* groups, int ngroups, int gsize, int64_t nparts,
+                        void* stream) {
+  SPMD_CHECK_ARG(in.dtype == out.dtype, "reduction dtype mismatch");
+  SPMD_CHECK_ARG(kind >= 0 && kind <= 3, "bad reduce kind");
+  GroupTab g;
+  int rc = make_groups(groups, ngroups, gsize, nparts, g);
+  if (rc) return rc;
+  int64_t n_out = numel(out), n_in = numel(in);
+  if (n_out * nparts == 0) return SPMD_OK;
+  cudaStream_t s = as_stream(stream);
+  View vin = view_of(in), vout = view_of(out);
+  SPMD_DISPATCH(in.dtype, T,
+                local_reduce_kernel<T><<<grid_for(n_out * nparts, 256, 2), 256, 0, s>>>(
+                    (const T*)in.data, (T*)out.data, vin, vout, dim, scatter, kind, g, n_out,
+                    n_in));
+  return launched(s);
+}
+
+extern "C" int spmd_local_all_reduce(spmd_tensor in, spmd_tensor out, int kind,
+                                     const int32_t* groups, int ngroups, int gsize,
+                                     int64_t nparts, void* stream) {
+  SPMD_CHECK_ARG(numel(in) == numel(out), "all-reduce shape mismatch");
+  return local_reduce(in, out, 0, 0, kind, groups, ngroups, gsize, nparts, stream);
+}
+
+extern "C" int spmd_local_reduce_scatter(spmd_tensor in, spmd_tensor out, int dim, int kind,
+                                         const int32_t* groups, int ngroups, int gsize,
+                                         int64_t nparts, void* stream) {
+  SPMD_CHECK_ARG(dim >= 0 && dim < in.rank && in.dims[dim] == out.dims[dim] * gsize,
+                 "reduce-scatter shape mismatch");
+  return local_reduce(in, out, dim, 1, kind, groups, ngroups, gsize, nparts, stream);
+}

@@ -1,0 +1,207 @@
+// Shared helpers for the sm_100a kernels behind include/spmd_b200.h.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include <stdint.h>
+#include <atomic>
+#include <string>
+
+#include "../../include/spmd_b200.h"
+
+namespace spmd {
+
+// ---------------------------------------------------------------------------
+// status / error plumbing
+// ---------------------------------------------------------------------------
+void set_error(const std::string& msg);
+extern std::atomic<int64_t> g_launches;
+// Device error word (cudaMalloc'd int on the current device): bit 0 =
+// integer division by zero.  Kernels that can fault receive it as a pointer.
+int* device_error_word();
+
+#define SPMD_CHECK_ARG(cond, msg)                  \
+  do {                                             \
+    if (!(cond)) {                                 \
+      ::spmd::set_error(msg);                      \
+      return SPMD_ERR_INVALID;                     \
+    }                                              \
+  } while (0)
+
+#define SPMD_CUDA_TRY(expr)                                                 \
+  do {                                                                      \
+    cudaError_t _e = (expr);                                                \
+    if (_e != cudaSuccess) {                                                \
+      ::spmd::set_error(std::string(#expr) + ": " + cudaGetErrorString(_e)); \
+      return SPMD_ERR_CUDA;                                                 \
+    }                                                                       \
+  } while (0)
+
+inline int launched(cudaStream_t s) {
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    set_error(std::string("kernel launch: ") + cudaGetErrorString(e));
+    return SPMD_ERR_CUDA;
+  }
+  (void)s;
+  return SPMD_OK;
+}
+
+inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// ---------------------------------------------------------------------------
+// shapes
+// ---------------------------------------------------------------------------
+inline int64_t numel(const spmd_tensor& t) {
+  int64_t n = 1;
+  for (int i = 0; i < t.rank; ++i) n *= t.dims[i];
+  return n;
+}
+
+inline int elem_size(int dtype) {
+  switch (dtype) {
+    case SPMD_F32: case SPMD_S32: case SPMD_U32: return 4;
+    case SPMD_PRED: return 1;
+    case SPMD_BF16: return 2;
+  }
+  return 0;
+}
+
+struct Shape8 {
+  int rank;
+  int64_t d[SPMD_MAX_RANK];
+};
+
+inline Shape8 shape_of(const spmd_tensor& t) {
+  Shape8 s;
+  s.rank = t.rank;
+  for (int i = 0; i < SPMD_MAX_RANK; ++i) s.d[i] = i < t.rank ? t.dims[i] : 1;
+  return s;
+}
+
+inline void row_strides(const Shape8& s, int64_t* st) {
+  int64_t acc = 1;
+  for (int i = s.rank - 1; i >= 0; --i) {
+    st[i] = acc;
+    acc *= s.d[i];
+  }
+}
+
+// Grid for a grid-stride loop over n work items.
+inline unsigned grid_for(int64_t n, int block, int per_thread = 1) {
+  int64_t b = (n + (int64_t)block * per_thread - 1) / ((int64_t)block * per_thread);
+  if (b < 1) b = 1;
+  const int64_t cap = 148LL * 32;   // 148 SMs x enough resident blocks
+  return (unsigned)(b < cap ? b : cap);
+}
+
+// ---------------------------------------------------------------------------
+// element types
+// ---------------------------------------------------------------------------
+typedef __nv_bfloat16 bf16;
+
+template <typename T> struct Compute { typedef T type; };
+template <> struct Compute<bf16> { typedef float type; };
+
+template <typename T> __device__ __forceinline__ typename Compute<T>::type ld(const T& v) { return v; }
+template <> __device__ __forceinline__ float ld<bf16>(const bf16& v) { return __bfloat162float(v); }
+
+template <typename T> __device__ __forceinline__ T st(typename Compute<T>::type v) { return v; }
+template <> __device__ __forceinline__ bf16 st<bf16>(float v) { return __float2bfloat16_rn(v); }
+
+#define SPMD_DISPATCH(DT, T, ...)                                  \
+  switch (DT) {                                                    \
+    case SPMD_F32: { typedef float T; __VA_ARGS__; break; }        \
+    case SPMD_S32: { typedef int32_t T; __VA_ARGS__; break; }      \
+    case SPMD_U32: { typedef uint32_t T; __VA_ARGS__; break; }     \
+    case SPMD_PRED: { typedef uint8_t T; __VA_ARGS__; break; }     \
+    case SPMD_BF16: { typedef bf16 T; __VA_ARGS__; break; }        \
+    default: set_error("bad dtype"); return SPMD_ERR_INVALID;     \
+  }
+
+// Dispatch on element byte size only (pure data movement).
+#define SPMD_DISPATCH_BYTES(DT, T, ...)                            \
+  switch (elem_size(DT)) {                                         \
+    case 4: { typedef uint32_t T; __VA_ARGS__; break; }            \
+    case 2: { typedef uint16_t T; __VA_ARGS__; break; }            \
+    case 1: { typedef uint8_t T; __VA_ARGS__; break; }             \
+    default: set_error("bad dtype"); return SPMD_ERR_INVALID;     \
+  }
+
+// NaN-propagating max/min (numpy semantics).
+template <typename T> __device__ __forceinline__ T vmax(T a, T b) { return a > b ? a : b; }
+template <typename T> __device__ __forceinline__ T vmin(T a, T b) { return a < b ? a : b; }
+template <> __device__ __forceinline__ float vmax<float>(float a, float b) {
+  return (a > b || a != a) ? a : b;
+}
+template <> __device__ __forceinline__ float vmin<float>(float a, float b) {
+  return (a < b || a != a) ? a : b;
+}
+
+// Wrapping integer arithmetic (numpy int32 semantics).
+template <typename T> __device__ __forceinline__ T wadd(T a, T b) { return a + b; }
+template <typename T> __device__ __forceinline__ T wsub(T a, T b) { return a - b; }
+template <typename T> __device__ __forceinline__ T wmul(T a, T b) { return a * b; }
+template <> __device__ __forceinline__ int32_t wadd<int32_t>(int32_t a, int32_t b) {
+  return (int32_t)((uint32_t)a + (uint32_t)b);
+}
+template <> __device__ __forceinline__ int32_t wsub<int32_t>(int32_t a, int32_t b) {
+  return (int32_t)((uint32_t)a - (uint32_t)b);
+}
+template <> __device__ __forceinline__ int32_t wmul<int32_t>(int32_t a, int32_t b) {
+  return (int32_t)((uint32_t)a * (uint32_t)b);
+}
+template <> __device__ __forceinline__ uint8_t wadd<uint8_t>(uint8_t a, uint8_t b) { return a | b; }
+template <> __device__ __forceinline__ uint8_t wmul<uint8_t>(uint8_t a, uint8_t b) { return a & b; }
+template <> __device__ __forceinline__ uint8_t wsub<uint8_t>(uint8_t a, uint8_t b) { return a ^ b; }
+
+// Reduction combiner.
+template <typename C>
+__device__ __forceinline__ C combine(int kind, C a, C b) {
+  switch (kind) {
+    case SPMD_SUM: return wadd<C>(a, b);
+    case SPMD_MAX: return vmax<C>(a, b);
+    case SPMD_MIN: return vmin<C>(a, b);
+    default: return wmul<C>(a, b);
+  }
+}
+
+// Unravel a linear index into coordinates (row-major).
+template <typename I>
+__device__ __forceinline__ void unravel(I idx, const Shape8& s, I* c) {
+#pragma unroll
+  for (int i = SPMD_MAX_RANK - 1; i >= 0; --i) {
+    if (i < s.rank) {
+      I di = (I)s.d[i];
+      c[i] = idx % di;
+      idx /= di;
+    } else {
+      c[i] = 0;
+    }
+  }
+}
+
+// Affine strided copy between two views (datamove.cu).
+struct CopyArgs {
+  int rank;
+  int64_t shape[SPMD_MAX_RANK];
+  int64_t sst[SPMD_MAX_RANK];
+  int64_t dst[SPMD_MAX_RANK];
+  int64_t sbase, dbase;        // element offsets
+  int64_t spart, dpart;        // per-partition element strides
+  int64_t n;                   // elements per partition
+  // dynamic (per-partition) base: base += clamp(start[d][p], 0, dmax[d]) * dmul[d]
+  int ndyn;
+  const int32_t* dyn_start[SPMD_MAX_RANK];
+  int64_t dyn_max[SPMD_MAX_RANK];
+  int64_t dyn_mul[SPMD_MAX_RANK];
+  int dyn_on_dst;
+};
+
+int launch_copy(const void* src, void* dst, int dtype, CopyArgs a, int64_t nparts,
+                cudaStream_t s);
+int launch_fill(void* out, const void* value, int dtype, int64_t n, int64_t nparts,
+                cudaStream_t s);
+
+}  // namespace spmd

@@ -1,0 +1,365 @@
+// Data-movement ops (reference simulator.py:199-241, 278-300): broadcast,
+// transpose, reverse, pad, slice, dynamic-slice, dynamic-update-slice, concat,
+// rotate, shift.
+//
+// Every one of them is an *affine* copy between two strided views
+//   dst[dbase(p) + sum_d c_d * dstride_d] = src[sbase(p) + sum_d c_d * sstride_d]
+// (negative strides for reverse, stride*(interior+1) for pad, a per-partition
+// clamped base for dynamic slices), optionally preceded by a per-partition
+// scalar fill.  The host side merges dims that are contiguous in both views
+// and drops unit dims, so most copies run with 1-3 dims of index math; when
+// the innermost dim is unit-stride on both sides and 16-byte aligned the
+// kernel moves 16 bytes per thread.  Pure HBM-bound work.
+#include "common.cuh"
+
+#include <string.h>
+
+namespace spmd {
+
+
+template <typename T, typename I, int V>
+__global__ void strided_copy_kernel(const T* __restrict__ src, T* __restrict__ dst, CopyArgs a,
+                                    int64_t nparts) {
+  const I per = (I)(a.n / V);
+  const I total = per * (I)nparts;
+  for (I idx = blockIdx.x * (I)blockDim.x + threadIdx.x; idx < total;
+       idx += (I)gridDim.x * blockDim.x) {
+    I p = idx / per;
+    I r = (idx - p * per) * V;
+    int64_t so = a.sbase + (int64_t)p * a.spart;
+    int64_t d0 = a.dbase + (int64_t)p * a.dpart;
+#pragma unroll
+    for (int k = SPMD_MAX_RANK - 1; k >= 0; --k) {
+      if (k < a.rank) {
+        I dk = (I)a.shape[k];
+        I c = r % dk;
+        r /= dk;
+        so += (int64_t)c * a.sst[k];
+        d0 += (int64_t)c * a.dst[k];
+      }
+    }
+    if (a.ndyn) {
+      int64_t off = 0;
+      for (int k = 0; k < a.ndyn; ++k) {
+        int64_t s0 = a.dyn_start[k][p];
+        s0 = s0 < 0 ? 0 : (s0 > a.dyn_max[k] ? a.dyn_max[k] : s0);
+        off += s0 * a.dyn_mul[k];
+      }
+      if (a.dyn_on_dst) d0 += off; else so += off;
+    }
+    if (V == 1) {
+      dst[d0] = src[so];
+    } else {
+      *reinterpret_cast<uint4*>(dst + d0) = *reinterpret_cast<const uint4*>(src + so);
+    }
+  }
+}
+
+template <typename T>
+__global__ void fill_kernel(T* __restrict__ out, const T* __restrict__ value, int64_t n,
+                            int64_t nparts) {
+  const int64_t total = n * nparts;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = value[i / n];
+}
+
+// Merge dims contiguous in both views; drop unit dims.
+static void canonicalize(CopyArgs& a) {
+  int64_t sh[SPMD_MAX_RANK], ss[SPMD_MAX_RANK], ds[SPMD_MAX_RANK];
+  int r = 0;
+  for (int k = 0; k < a.rank; ++k) {
+    if (a.shape[k] == 1) continue;
+    if (r > 0 && ss[r - 1] == a.sst[k] * a.shape[k] && ds[r - 1] == a.dst[k] * a.shape[k]) {
+      sh[r - 1] *= a.shape[k];
+      ss[r - 1] = a.sst[k];
+      ds[r - 1] = a.dst[k];
+      continue;
+    }
+    sh[r] = a.shape[k];
+    ss[r] = a.sst[k];
+    ds[r] = a.dst[k];
+    ++r;
+  }
+  a.rank = r;
+  for (int k = 0; k < r; ++k) {
+    a.shape[k] = sh[k];
+    a.sst[k] = ss[k];
+    a.dst[k] = ds[k];
+  }
+}
+
+int launch_copy(const void* src, void* dst, int dtype, CopyArgs a, int64_t nparts,
+                cudaStream_t s) {
+  a.n = 1;
+  for (int k = 0; k < a.rank; ++k) a.n *= a.shape[k];
+  if (a.n == 0 || nparts == 0) return SPMD_OK;
+  canonicalize(a);
+  const int es = elem_size(dtype);
+  // 16-byte vector path: innermost dim unit-stride on both sides, all offsets
+  // and strides multiples of the vector width, pointers aligned.
+  const int V = 16 / es;
+  bool vec = a.rank >= 1 && a.sst[a.rank - 1] == 1 && a.dst[a.rank - 1] == 1 &&
+             a.shape[a.rank - 1] % V == 0 && a.ndyn == 0 &&
+             (reinterpret_cast<uintptr_t>(src) & 15) == 0 &&
+             (reinterpret_cast<uintptr_t>(dst) & 15) == 0 && a.sbase % V == 0 &&
+             a.dbase % V == 0 && a.spart % V == 0 && a.dpart % V == 0;
+  for (int k = 0; vec && k < a.rank - 1; ++k) vec = a.sst[k] % V == 0 && a.dst[k] % V == 0;
+  // The kernel walks groups of V consecutive last-dim elements (element-unit
+  // index math is unchanged; each group is contiguous on both sides).
+  const int64_t work = (vec ? a.n / V : a.n) * nparts;
+  const bool small = a.n * nparts < (int64_t)1 << 31;
+  SPMD_DISPATCH_BYTES(dtype, T, {
+    if (vec) {
+      if (small)
+        strided_copy_kernel<T, uint32_t, 16 / sizeof(T)><<<grid_for(work, 256), 256, 0, s>>>(
+            (const T*)src, (T*)dst, a, nparts);
+      else
+        strided_copy_kernel<T, uint64_t, 16 / sizeof(T)><<<grid_for(work, 256), 256, 0, s>>>(
+            (const T*)src, (T*)dst, a, nparts);
+    } else {
+      if (small)
+        strided_copy_kernel<T, uint32_t, 1><<<grid_for(work, 256, 2), 256, 0, s>>>(
+            (const T*)src, (T*)dst, a, nparts);
+      else
+        strided_copy_kernel<T, uint64_t, 1><<<grid_for(work, 256, 2), 256, 0, s>>>(
+            (const T*)src, (T*)dst, a, nparts);
+    }
+  });
+  return launched(s);
+}
+
+int launch_fill(void* out, const void* value, int dtype, int64_t n, int64_t nparts,
+                cudaStream_t s) {
+  if (n == 0 || nparts == 0) return SPMD_OK;
+  SPMD_DISPATCH_BYTES(dtype, T,
+                      fill_kernel<T><<<grid_for(n * nparts, 256, 4), 256, 0, s>>>(
+                          (T*)out, (const T*)value, n, nparts));
+  return launched(s);
+}
+
+static CopyArgs base_args(const spmd_tensor& shape_src) {
+  CopyArgs a;
+  memset(&a, 0, sizeof(a));
+  a.rank = shape_src.rank;
+  for (int k = 0; k < a.rank; ++k) a.shape[k] = shape_src.dims[k];
+  return a;
+}
+
+static void contiguous_strides(const spmd_tensor& t, int64_t* st) {
+  int64_t acc = 1;
+  for (int k = t.rank - 1; k >= 0; --k) {
+    st[k] = acc;
+    acc *= t.dims[k];
+  }
+}
+
+}  // namespace spmd
+
+using namespace spmd;
+
+extern "C" int spmd_broadcast(spmd_tensor in, spmd_tensor out, const int32_t* bdims,
+                              int64_t nparts, void* stream) {
+  SPMD_CHECK_ARG(in.dtype == out.dtype, "broadcast dtype mismatch");
+  int64_t ist[SPMD_MAX_RANK];
+  contiguous_strides(in, ist);
+  CopyArgs a = base_args(out);
+  contiguous_strides(out, a.dst);
+  for (int k = 0; k < out.rank; ++k) a.sst[k] = 0;
+  for (int i = 0; i < in.rank; ++i) {
+    SPMD_CHECK_ARG(bdims[i] >= 0 && bdims[i] < out.rank && out.dims[bdims[i]] == in.dims[i],
+                   "broadcast dims mismatch");
+    a.sst[bdims[i]] = ist[i];
+  }
+  a.spart = numel(in);
+  a.dpart = numel(out);
+  return launch_copy(in.data, out.data, out.dtype, a, nparts, as_stream(stream));
+}
+
+extern "C" int spmd_transpose(spmd_tensor in, spmd_tensor out, const int32_t* perm,
+                              int64_t nparts, void* stream) {
+  SPMD_CHECK_ARG(in.dtype == out.dtype && in.rank == out.rank, "transpose mismatch");
+  int64_t ist[SPMD_MAX_RANK];
+  contiguous_strides(in, ist);
+  CopyArgs a = base_args(out);
+  contiguous_strides(out, a.dst);
+  for (int j = 0; j < out.rank; ++j) {
+    SPMD_CHECK_ARG(out.dims[j] == in.dims[perm[j]], "transpose dims mismatch");
+    a.sst[j] = ist[perm[j]];
+  }
+  a.spart = a.dpart = numel(in);
+  return launch_copy(in.data, out.data, out.dtype, a, nparts, as_stream(stream));
+}
+
+extern "C" int spmd_reverse(spmd_tensor in, spmd_tensor out, const int32_t* dims, int ndims,
+                            int64_t nparts, void* stream) {
+  SPMD_CHECK_ARG(in.dtype == out.dtype && numel(in) == numel(out), "reverse mismatch");
+  CopyArgs a = base_args(out);
+  contiguous_strides(in, a.sst);
+  contiguous_strides(out, a.dst);
+  for (int i = 0; i < ndims; ++i) {
+    int d = dims[i];
+    SPMD_CHECK_ARG(d >= 0 && d < in.rank, "reverse dim out of range");
+    if (in.dims[d] == 0) continue;
+    a.sbase += (in.dims[d] - 1) * a.sst[d];
+    a.sst[d] = -a.sst[d];
+  }
+  a.spart = a.dpart = numel(in);
+  return launch_copy(in.data, out.data, out.dtype, a, nparts, as_stream(stream));
+}
+
+extern "C" int spmd_pad(spmd_tensor in, spmd_tensor value, spmd_tensor out, const int64_t* low,
+                        const int64_t* high, const int64_t* interior, int64_t nparts,
+                        void* stream) {
+  SPMD_CHECK_ARG(in.dtype == out.dtype && value.dtype == in.dtype && value.rank == 0,
+                 "pad dtype mismatch");
+  cudaStream_t s = as_stream(stream);
+  int rc = launch_fill(out.data, value.data, out.dtype, numel(out), nparts, s);
+  if (rc) return rc;
+  CopyArgs a = base_args(in);
+  contiguous_strides(in, a.sst);
+  int64_t ost[SPMD_MAX_RANK];
+  contiguous_strides(out, ost);
+  for (int k = 0; k < in.rank; ++k) {
+    SPMD_CHECK_ARG(low[k] >= 0 && high[k] >= 0 && interior[k] >= 0, "negative padding");
+    int64_t n = in.dims[k];
+    SPMD_CHECK_ARG(out.dims[k] == n + (n > 0 ? n - 1 : 0) * interior[k] + low[k] + high[k],
+                   "pad output shape mismatch");
+    a.dst[k] = ost[k] * (interior[k] + 1);
+    a.dbase += low[k] * ost[k];
+  }
+  a.spart = numel(in);
+  a.dpart = numel(out);
+  return launch_copy(in.data, out.data, out.dtype, a, nparts, s);
+}
+
+extern "C" int spmd_slice(spmd_tensor in, spmd_tensor out, const int64_t* starts,
+                          const int64_t* strides, int64_t nparts, void* stream) {
+  SPMD_CHECK_ARG(in.dtype == out.dtype && in.rank == out.rank, "slice mismatch");
+  int64_t ist[SPMD_MAX_RANK];
+  contiguous_strides(in, ist);
+  CopyArgs a = base_args(out);
+  contiguous_strides(out, a.dst);
+  for (int k = 0; k < in.rank; ++k) {
+    SPMD_CHECK_ARG(strides[k] >= 1, "slice stride must be >= 1");
+    a.sst[k] = ist[k] * strides[k];
+    a.sbase += starts[k] * ist[k];
+  }
+  a.spart = numel(in);
+  a.dpart = numel(out);
+  return launch_copy(in.data, out.data, out.dtype, a, nparts, as_stream(stream));
+}
+
+extern "C" int spmd_dynamic_slice(spmd_tensor in, const spmd_tensor* starts, spmd_tensor out,
+                                  int64_t nparts, void* stream) {
+  SPMD_CHECK_ARG(in.dtype == out.dtype && in.rank == out.rank, "dynamic-slice mismatch");
+  CopyArgs a = base_args(out);
+  contiguous_strides(in, a.sst);
+  contiguous_strides(out, a.dst);
+  for (int k = 0; k < in.rank; ++k) {
+    SPMD_CHECK_ARG(starts[k].dtype == SPMD_S32 || starts[k].dtype == SPMD_U32,
+                   "dynamic-slice index must be s32/u32");
+    SPMD_CHECK_ARG(out.dims[k] <= in.dims[k], "dynamic-slice size exceeds operand");
+    a.dyn_start[a.ndyn] = (const int32_t*)starts[k].data;
+    a.dyn_max[a.ndyn] = in.dims[k] - out.dims[k];
+    a.dyn_mul[a.ndyn] = a.sst[k];
+    a.ndyn++;
+  }
+  a.spart = numel(in);
+  a.dpart = numel(out);
+  return launch_copy(in.data, out.data, out.dtype, a, nparts, as_stream(stream));
+}
+
+extern "C" int spmd_dynamic_update_slice(spmd_tensor in, spmd_tensor upd, const spmd_tensor* starts,
+                                         spmd_tensor out, int64_t nparts, void* stream) {
+  SPMD_CHECK_ARG(in.dtype == out.dtype && upd.dtype == in.dtype && in.rank == upd.rank,
+                 "dynamic-update-slice mismatch");
+  cudaStream_t s = as_stream(stream);
+  if (out.data != in.data)
+    SPMD_CUDA_TRY(cudaMemcpyAsync(out.data, in.data,
+                                  (size_t)numel(in) * nparts * elem_size(in.dtype),
+                                  cudaMemcpyDeviceToDevice, s));
+  CopyArgs a = base_args(upd);
+  contiguous_strides(upd, a.sst);
+  contiguous_strides(out, a.dst);
+  a.dyn_on_dst = 1;
+  for (int k = 0; k < in.rank; ++k) {
+    SPMD_CHECK_ARG(upd.dims[k] <= in.dims[k], "update larger than operand");
+    a.dyn_start[a.ndyn] = (const int32_t*)starts[k].data;
+    a.dyn_max[a.ndyn] = in.dims[k] - upd.dims[k];
+    a.dyn_mul[a.ndyn] = a.dst[k];
+    a.ndyn++;
+  }
+  a.spart = numel(upd);
+  a.dpart = numel(out);
+  return launch_copy(upd.data, out.data, out.dtype, a, nparts, s);
+}
+
+extern "C" int spmd_concat(const spmd_tensor* ins, int n, int axis, spmd_tensor out,
+                           int64_t nparts, void* stream) {
+  cudaStream_t s = as_stream(stream);
+  int64_t off = 0;
+  int64_t ost[SPMD_MAX_RANK];
+  contiguous_strides(out, ost);
+  for (int i = 0; i < n; ++i) {
+    const spmd_tensor& t = ins[i];
+    SPMD_CHECK_ARG(t.dtype == out.dtype && t.rank == out.rank, "concat mismatch");
+    CopyArgs a = base_args(t);
+    contiguous_strides(t, a.sst);
+    for (int k = 0; k < t.rank; ++k) a.dst[k] = ost[k];
+    a.dbase = off * ost[axis];
+    a.spart = numel(t);
+    a.dpart = numel(out);
+    int rc = launch_copy(t.data, out.data, out.dtype, a, nparts, s);
+    if (rc) return rc;
+    off += t.dims[axis];
+  }
+  SPMD_CHECK_ARG(off == out.dims[axis], "concat output size mismatch");
+  return SPMD_OK;
+}
+
+extern "C" int spmd_rotate(spmd_tensor in, spmd_tensor out, int dim, int64_t amount,
+                           int64_t nparts, void* stream) {
+  // out[o] = in[(o + amount) mod n]  (np.roll(x, -amount), simulator.py:278-279)
+  SPMD_CHECK_ARG(in.dtype == out.dtype && dim >= 0 && dim < in.rank, "rotate mismatch");
+  cudaStream_t s = as_stream(stream);
+  int64_t n = in.dims[dim];
+  if (n == 0) return SPMD_OK;
+  int64_t k = ((amount % n) + n) % n;
+  int64_t st[SPMD_MAX_RANK];
+  contiguous_strides(in, st);
+  for (int piece = 0; piece < 2; ++piece) {
+    int64_t len = piece == 0 ? n - k : k;
+    if (len == 0) continue;
+    CopyArgs a = base_args(in);
+    a.shape[dim] = len;
+    for (int d = 0; d < in.rank; ++d) a.sst[d] = a.dst[d] = st[d];
+    a.sbase = (piece == 0 ? k : 0) * st[dim];
+    a.dbase = (piece == 0 ? 0 : n - k) * st[dim];
+    a.spart = a.dpart = numel(in);
+    int rc = launch_copy(in.data, out.data, out.dtype, a, nparts, s);
+    if (rc) return rc;
+  }
+  return SPMD_OK;
+}
+
+extern "C" int spmd_shift(spmd_tensor in, spmd_tensor fill, spmd_tensor out, int dim,
+                          int64_t amount, int64_t nparts, void* stream) {
+  SPMD_CHECK_ARG(in.dtype == out.dtype && fill.dtype == in.dtype && dim >= 0 && dim < in.rank,
+                 "shift mismatch");
+  cudaStream_t s = as_stream(stream);
+  int rc = launch_fill(out.data, fill.data, out.dtype, numel(out), nparts, s);
+  if (rc) return rc;
+  int64_t n = in.dims[dim];
+  int64_t k = amount >= 0 ? amount : -amount;
+  if (k >= n) return SPMD_OK;
+  int64_t st[SPMD_MAX_RANK];
+  contiguous_strides(in, st);
+  CopyArgs a = base_args(in);
+  a.shape[dim] = n - k;
+  for (int d = 0; d < in.rank; ++d) a.sst[d] = a.dst[d] = st[d];
+  if (amount >= 0) a.dbase = amount * st[dim];
+  else a.sbase = k * st[dim];
+  a.spart = a.dpart = numel(in);
+  return launch_copy(in.data, out.data, out.dtype, a, nparts, s);
+}

@@ -1,0 +1,550 @@
+// BF16 generalised dot on 5th-gen tensor cores (sm_100a): TMA -> swizzled
+// smem ring -> tcgen05.mma (fp32 accumulators in TMEM) -> tcgen05.ld epilogue.
+//
+// Replaces the reference's float64 einsum (simulator.py:258-275) for BF16.
+// out[b, m, n] = sum_k A[b, m, k] * B[b, n, k] where A/B are views of the
+// Dot operands: batch dims (<= 3, incl. the partition stack) and one merged
+// M / N / K dim each.  Each operand may be K-major (K contiguous) or MN-major
+// (M or N contiguous) -- both are native UMMA smem layouts, so weights stored
+// [K, N] (x @ W) and activations stored [.., K] feed the tensor cores without
+// any transpose pass.
+//
+// Kernel structure (persistent, one CTA per SM, 256 threads):
+//   warp 0      TMA producer: kStages-deep ring of (A, B) tiles, mbarrier
+//               expect-tx completion.
+//   warp 1      MMA issuer: one elected thread issues BK/16 tcgen05.mma per
+//               stage into a double-buffered TMEM accumulator (2 x BN cols),
+//               tcgen05.commit frees smem stages / signals the epilogue.
+//   warp 2      TMEM allocator (alloc/relinquish/dealloc).
+//   warps 4-7   epilogue: tcgen05.ld 32x32b -> fp32 regs -> (relu) -> bf16 ->
+//               global; overlaps the next tile's MMAs via the second buffer.
+// Tile 128 x BN x 64, BN in {128, 256}; SWIZZLE_128B everywhere.
+#include "common.cuh"
+
+#include <cuda.h>
+#include <string.h>
+
+namespace spmd {
+
+// ---------------------------------------------------------------------------
+// PTX wrappers
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  uint32_t addr = smem_u32(bar);
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(addr),
+      "r"(phase)
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_load_5d(void* dst, const CUtensorMap* map, uint64_t* bar,
+                                            int c0, int c1, int c2, int c3, int c4) {
+  asm volatile(
+      "cp.async.bulk.tensor.5d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6, %7}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3),
+      "r"(c4)
+      : "memory");
+}
+
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+
+__device__ __forceinline__ void tc_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   smem_u32(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ void tc_mma(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc,
+                                       uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate));
+}
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, "
+      "%12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, "
+      "%30, %31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]),
+        "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),
+        "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+// UMMA shared-memory descriptor, SWIZZLE_128B, version 1 (Blackwell).
+//   K-major : rows of 128 B (64 bf16 of K), 8-row atoms 1024 B apart (SBO).
+//   MN-major: rows of 128 B (64 bf16 of M/N) per K index, 8-K-row atoms
+//             1024 B apart (SBO), 64-wide M/N chunks `lbo` bytes apart (LBO).
+__device__ __forceinline__ uint64_t make_desc(uint32_t saddr, uint32_t lbo_bytes,
+                                              uint32_t sbo_bytes) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)((lbo_bytes >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)((sbo_bytes >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)1 << 46;   // version = 1
+  d |= (uint64_t)2 << 61;   // SWIZZLE_128B
+  return d;
+}
+
+// Instruction descriptor: kind::f16, bf16 x bf16 -> f32, M=128, N=BN.
+__host__ __device__ constexpr uint32_t make_idesc(int M, int N, int a_mn, int b_mn) {
+  return (1u << 4)                      // D format f32
+         | (1u << 7)                    // A bf16
+         | (1u << 10)                   // B bf16
+         | ((uint32_t)a_mn << 15)       // A major (0 K, 1 MN)
+         | ((uint32_t)b_mn << 16)       // B major
+         | ((uint32_t)(N >> 3) << 17)   // N / 8
+         | ((uint32_t)(M >> 4) << 24);  // M / 16
+}
+
+constexpr int BM = 128;
+constexpr int BK = 64;
+constexpr int EPI_WARP0 = 4;
+
+struct GemmShape {
+  int M, N, K;
+  int nb[3];            // batch extents (innermost first in tensor-map order)
+  int mt, nt;           // tile counts
+  int64_t tiles;
+  int64_t out_batch_stride;   // elements between consecutive flat batches
+  int a_mn, b_mn;
+  int relu;
+};
+
+template <int BN, int STAGES>
+struct Smem {
+  static constexpr int A_BYTES = BM * BK * 2;
+  static constexpr int B_BYTES = BN * BK * 2;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int BAR_OFF = STAGES * STAGE_BYTES;
+  static constexpr int TOTAL = BAR_OFF + 256 + 1024;   // + barriers + align slack
+};
+
+__device__ __forceinline__ void tile_coords(const GemmShape& g, int64_t t, int& b, int& m, int& n) {
+  const int64_t per = (int64_t)g.mt * g.nt;
+  b = (int)(t / per);
+  int r = (int)(t - (int64_t)b * per);
+  // Grouped rasterisation: 8 M-tiles sweep the N-tiles together (L2 reuse).
+  const int G = 8;
+  int group = r / (G * g.nt);
+  int first = group * G;
+  int gs = g.mt - first < G ? g.mt - first : G;
+  int rr = r - group * G * g.nt;
+  m = first + rr % gs;
+  n = rr / gs;
+}
+
+template <int BN, int STAGES>
+__global__ void __launch_bounds__(256, 1)
+    gemm_bf16_tcgen05(const __grid_constant__ CUtensorMap map_a,
+                      const __grid_constant__ CUtensorMap map_b, bf16* __restrict__ out,
+                      GemmShape g) {
+  typedef Smem<BN, STAGES> L;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint64_t* full = (uint64_t*)(smem + L::BAR_OFF);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 4);   // one arrival per epilogue warp
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                     smem_u32(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const int kblocks = (g.K + BK - 1) / BK;
+
+  if (warp == 0 && lane == 0) {
+    // ---------------- TMA producer ----------------
+    int s = 0;
+    uint32_t ph = 0;
+    for (int64_t t = blockIdx.x; t < g.tiles; t += gridDim.x) {
+      int b, m, n;
+      tile_coords(g, t, b, m, n);
+      const int b0 = b % g.nb[0], b1 = (b / g.nb[0]) % g.nb[1], b2 = b / (g.nb[0] * g.nb[1]);
+      for (int kb = 0; kb < kblocks; ++kb) {
+        mbar_wait(&empty[s], ph ^ 1);
+        uint8_t* sa = smem + s * L::STAGE_BYTES;
+        uint8_t* sb = sa + L::A_BYTES;
+        mbar_expect_tx(&full[s], L::STAGE_BYTES);
+        const int k0 = kb * BK;
+        if (!g.a_mn) {
+          tma_load_5d(sa, &map_a, &full[s], k0, m * BM, b0, b1, b2);
+        } else {
+#pragma unroll
+          for (int c = 0; c < BM / 64; ++c)
+            tma_load_5d(sa + c * (BK * 128), &map_a, &full[s], m * BM + c * 64, k0, b0, b1, b2);
+        }
+        if (!g.b_mn) {
+          tma_load_5d(sb, &map_b, &full[s], k0, n * BN, b0, b1, b2);
+        } else {
+#pragma unroll
+          for (int c = 0; c < BN / 64; ++c)
+            tma_load_5d(sb + c * (BK * 128), &map_b, &full[s], n * BN + c * 64, k0, b0, b1, b2);
+        }
+        if (++s == STAGES) {
+          s = 0;
+          ph ^= 1;
+        }
+      }
+    }
+  } else if (warp == 1 && lane == 0) {
+    // ---------------- MMA issuer ----------------
+    const uint32_t idesc = make_idesc(BM, BN, g.a_mn, g.b_mn);
+    int s = 0;
+    uint32_t ph = 0;
+    int acc = 0;
+    uint32_t acc_ph = 0;
+    for (int64_t t = blockIdx.x; t < g.tiles; t += gridDim.x) {
+      mbar_wait(&tempty[acc], acc_ph ^ 1);
+      tc_fence_after();
+      const uint32_t d_tmem = tmem + acc * BN;
+      for (int kb = 0; kb < kblocks; ++kb) {
+        mbar_wait(&full[s], ph);
+        tc_fence_after();
+        const uint32_t sa = smem_u32(smem + s * L::STAGE_BYTES);
+        const uint32_t sb = sa + L::A_BYTES;
+#pragma unroll
+        for (int k = 0; k < BK / 16; ++k) {
+          // K advance of 16 elements: +32 B inside a K-major 128 B row, or
+          // +2 atoms (16 K-rows x 128 B) in an MN-major tile.
+          const uint64_t ad = g.a_mn ? make_desc(sa + k * 2048, BK * 128, 1024)
+                                     : make_desc(sa + k * 32, 16, 1024);
+          const uint64_t bd = g.b_mn ? make_desc(sb + k * 2048, BK * 128, 1024)
+                                     : make_desc(sb + k * 32, 16, 1024);
+          tc_mma(d_tmem, ad, bd, idesc, (kb | k) != 0);
+        }
+        tc_commit(&empty[s]);
+        if (++s == STAGES) {
+          s = 0;
+          ph ^= 1;
+        }
+      }
+      tc_commit(&tfull[acc]);
+      if (++acc == 2) {
+        acc = 0;
+        acc_ph ^= 1;
+      }
+    }
+  } else if (warp >= EPI_WARP0) {
+    // ---------------- epilogue ----------------
+    const int ew = warp - EPI_WARP0;          // == warp % 4 -> TMEM lanes 32*ew..
+    int acc = 0;
+    uint32_t acc_ph = 0;
+    for (int64_t t = blockIdx.x; t < g.tiles; t += gridDim.x) {
+      int b, m, n;
+      tile_coords(g, t, b, m, n);
+      mbar_wait(&tfull[acc], acc_ph);
+      tc_fence_after();
+      const int row = m * BM + ew * 32 + lane;
+      bf16* orow = out + (int64_t)b * g.out_batch_stride + (int64_t)row * g.N;
+#pragma unroll 1
+      for (int c0 = 0; c0 < BN; c0 += 32) {
+        uint32_t r[32];
+        tmem_ld32(tmem + ((uint32_t)(ew * 32) << 16) + acc * BN + c0, r);
+        const int col = n * BN + c0;
+        if (row < g.M && col < g.N) {
+          __align__(16) bf16 v[32];
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            float f = __uint_as_float(r[j]);
+            if (g.relu) f = f > 0.f ? f : 0.f;
+            v[j] = __float2bfloat16_rn(f);
+          }
+          if (col + 32 <= g.N && (g.N & 7) == 0) {
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+              *reinterpret_cast<uint4*>(orow + col + 8 * j) = reinterpret_cast<uint4*>(v)[j];
+          } else {
+            for (int j = 0; j < 32 && col + j < g.N; ++j) orow[col + j] = v[j];
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
+      if (++acc == 2) {
+        acc = 0;
+        acc_ph ^= 1;
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+  }
+}
+
+// ---------------------------------------------------------------------------
+// host side: operand views -> tensor maps
+// ---------------------------------------------------------------------------
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (EncodeTiledFn)p;
+  }
+  return fn;
+}
+
+// One operand: dims (inner, outer, b0, b1, b2) with element strides.
+struct OperandView {
+  int64_t size[5];
+  int64_t stride[5];   // elements; stride[0] must be 1
+};
+
+static bool encode(CUtensorMap* map, void* base, const OperandView& v, int box_inner,
+                   int box_outer) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[5], strides[4];
+  cuuint32_t box[5] = {(cuuint32_t)box_inner, (cuuint32_t)box_outer, 1, 1, 1};
+  cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+  for (int i = 0; i < 5; ++i) dims[i] = (cuuint64_t)v.size[i];
+  for (int i = 1; i < 5; ++i) {
+    strides[i - 1] = (cuuint64_t)(v.stride[i] * 2);
+    if (strides[i - 1] % 16 != 0 || strides[i - 1] >= ((cuuint64_t)1 << 40)) return false;
+  }
+  if ((reinterpret_cast<uintptr_t>(base) & 15) != 0) return false;
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, base, dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+struct DimRef {
+  int64_t size;
+  int64_t st;
+};
+
+// Merge a list of (size, stride) dims (outer->inner order) into one dim.
+static bool merge_dims(const DimRef* d, int n, DimRef* out) {
+  int64_t size = 1, st = 0;
+  bool first = true;
+  for (int i = n - 1; i >= 0; --i) {
+    if (d[i].size == 1) continue;
+    if (first) {
+      size = d[i].size;
+      st = d[i].st;
+      first = false;
+    } else {
+      if (d[i].st != st * size) return false;
+      size *= d[i].size;
+    }
+  }
+  out->size = size;
+  out->st = first ? 1 : st;
+  return true;
+}
+
+template <int BN, int STAGES>
+static int launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, bf16* out, GemmShape g,
+                       cudaStream_t s) {
+  typedef Smem<BN, STAGES> L;
+  static bool configured = false;
+  if (!configured) {
+    SPMD_CUDA_TRY(cudaFuncSetAttribute(gemm_bf16_tcgen05<BN, STAGES>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, L::TOTAL));
+    configured = true;
+  }
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  int64_t grid = g.tiles < sms ? g.tiles : sms;
+  gemm_bf16_tcgen05<BN, STAGES><<<(unsigned)grid, 256, L::TOTAL, s>>>(ma, mb, out, g);
+  return launched(s);
+}
+
+int dot_tcgen05(const spmd_tensor& lhs, const spmd_tensor& rhs, const spmd_tensor& out,
+                const spmd_dot_dims& dd, int64_t nparts, cudaStream_t s) {
+  if (lhs.dtype != SPMD_BF16) return SPMD_ERR_UNSUPPORTED;
+  int64_t ls[SPMD_MAX_RANK], rs[SPMD_MAX_RANK];
+  {
+    int64_t a = 1;
+    for (int k = lhs.rank - 1; k >= 0; --k) ls[k] = a, a *= lhs.dims[k];
+    a = 1;
+    for (int k = rhs.rank - 1; k >= 0; --k) rs[k] = a, a *= rhs.dims[k];
+  }
+  bool lu[SPMD_MAX_RANK] = {false}, ru[SPMD_MAX_RANK] = {false};
+  DimRef lb[SPMD_MAX_RANK + 1], rb[SPMD_MAX_RANK + 1], lk[SPMD_MAX_RANK], rk[SPMD_MAX_RANK];
+  DimRef lm[SPMD_MAX_RANK], rn[SPMD_MAX_RANK];
+  int nb = 0, nk = 0, nm = 0, nn = 0;
+  int64_t Bsz = 1;
+  for (int i = 0; i < dd.n_batch; ++i) {
+    int l = dd.lhs_batch[i], r = dd.rhs_batch[i];
+    lu[l] = ru[r] = true;
+    if (lhs.dims[l] == 1) continue;
+    lb[nb] = {lhs.dims[l], ls[l]};
+    rb[nb++] = {rhs.dims[r], rs[r]};
+    Bsz *= lhs.dims[l];
+  }
+  for (int i = 0; i < dd.n_contract; ++i) {
+    int l = dd.lhs_contracting[i], r = dd.rhs_contracting[i];
+    lu[l] = ru[r] = true;
+    lk[nk] = {lhs.dims[l], ls[l]};
+    rk[nk++] = {rhs.dims[r], rs[r]};
+  }
+  for (int d = 0; d < lhs.rank; ++d)
+    if (!lu[d]) lm[nm++] = {lhs.dims[d], ls[d]};
+  for (int d = 0; d < rhs.rank; ++d)
+    if (!ru[d]) rn[nn++] = {rhs.dims[d], rs[d]};
+  DimRef M, N, K, K2;
+  if (!merge_dims(lm, nm, &M) || !merge_dims(rn, nn, &N) || !merge_dims(lk, nk, &K) ||
+      !merge_dims(rk, nk, &K2))
+    return SPMD_ERR_UNSUPPORTED;
+  if (K.size != K2.size || M.size * N.size * Bsz != numel(out)) return SPMD_ERR_UNSUPPORTED;
+  // Partition stack as an extra (outermost) batch dim.
+  if (nparts > 1) {
+    // shift batch dims to make room for the partition dim at the front
+    for (int i = nb; i > 0; --i) lb[i] = lb[i - 1], rb[i] = rb[i - 1];
+    lb[0] = {nparts, numel(lhs)};
+    rb[0] = {nparts, numel(rhs)};
+    ++nb;
+  }
+  if (nb > 3) return SPMD_ERR_UNSUPPORTED;
+  if (M.size < 64 || N.size < 64 || K.size < 16) return SPMD_ERR_UNSUPPORTED;
+  const int a_mn = M.st == 1 && K.st != 1;
+  const int b_mn = N.st == 1 && K2.st != 1 ? 1 : 0;
+  if (!a_mn && K.st != 1) return SPMD_ERR_UNSUPPORTED;
+  const int b_k = K2.st == 1;
+  if (!b_mn && !b_k) return SPMD_ERR_UNSUPPORTED;
+
+  GemmShape g;
+  memset(&g, 0, sizeof(g));
+  g.M = (int)M.size;
+  g.N = (int)N.size;
+  g.K = (int)K.size;
+  g.a_mn = a_mn;
+  g.b_mn = b_mn;
+  g.relu = dd.epilogue == 1;
+  // tensor-map batch dims: innermost first
+  OperandView va, vb;
+  for (int i = 0; i < 3; ++i) {
+    int src = nb - 1 - i;   // innermost batch dim first
+    va.size[2 + i] = src >= 0 ? lb[src].size : 1;
+    va.stride[2 + i] = src >= 0 ? lb[src].st : 1;
+    vb.size[2 + i] = src >= 0 ? rb[src].size : 1;
+    vb.stride[2 + i] = src >= 0 ? rb[src].st : 1;
+    g.nb[i] = (int)(src >= 0 ? lb[src].size : 1);
+  }
+  // give unit dims a harmless stride (tensor maps need 16B multiples)
+  for (int i = 2; i < 5; ++i) {
+    if (va.size[i] == 1) va.stride[i] = va.stride[i - 1] ? 8 : 8;
+    if (vb.size[i] == 1) vb.stride[i] = 8;
+  }
+  if (!a_mn) {
+    va.size[0] = K.size, va.stride[0] = 1, va.size[1] = M.size, va.stride[1] = M.st;
+  } else {
+    va.size[0] = M.size, va.stride[0] = 1, va.size[1] = K.size, va.stride[1] = K.st;
+  }
+  if (!b_mn) {
+    vb.size[0] = K2.size, vb.stride[0] = 1, vb.size[1] = N.size, vb.stride[1] = N.st;
+  } else {
+    vb.size[0] = N.size, vb.stride[0] = 1, vb.size[1] = K2.size, vb.stride[1] = K2.st;
+  }
+  const int BNsel = N.size >= 256 ? 256 : 128;
+  CUtensorMap ma, mb;
+  bool ok = a_mn ? encode(&ma, lhs.data, va, 64, BK) : encode(&ma, lhs.data, va, BK, BM);
+  ok = ok && (b_mn ? encode(&mb, rhs.data, vb, 64, BK) : encode(&mb, rhs.data, vb, BK, BNsel));
+  if (!ok) return SPMD_ERR_UNSUPPORTED;
+  g.mt = (g.M + BM - 1) / BM;
+  g.nt = (g.N + BNsel - 1) / BNsel;
+  g.tiles = (int64_t)g.mt * g.nt * g.nb[0] * g.nb[1] * g.nb[2];
+  g.out_batch_stride = (int64_t)g.M * g.N;
+  if (BNsel == 256) return launch_gemm<256, 4>(ma, mb, (bf16*)out.data, g, s);
+  return launch_gemm<128, 6>(ma, mb, (bf16*)out.data, g, s);
+}
+
+}  // namespace spmd
+
+// Direct entry point for benchmarking the GEMM alone: C[M,N] = A[M,K] . B[K,N]
+// (row-major, A K-major, B MN-major), all bf16.
+extern "C" int spmd_gemm_bf16(const void* a, const void* b, void* c, int64_t M, int64_t N,
+                              int64_t K, int relu, void* stream) {
+  spmd_tensor ta, tb, tc;
+  memset(&ta, 0, sizeof(ta));
+  memset(&tb, 0, sizeof(tb));
+  memset(&tc, 0, sizeof(tc));
+  ta.data = const_cast<void*>(a), ta.dtype = SPMD_BF16, ta.rank = 2, ta.dims[0] = M, ta.dims[1] = K;
+  tb.data = const_cast<void*>(b), tb.dtype = SPMD_BF16, tb.rank = 2, tb.dims[0] = K, tb.dims[1] = N;
+  tc.data = c, tc.dtype = SPMD_BF16, tc.rank = 2, tc.dims[0] = M, tc.dims[1] = N;
+  spmd_dot_dims dd;
+  memset(&dd, 0, sizeof(dd));
+  dd.n_contract = 1;
+  dd.lhs_contracting[0] = 1;
+  dd.rhs_contracting[0] = 0;
+  dd.epilogue = relu;
+  return spmd::dot_tcgen05(ta, tb, tc, dd, 1, spmd::as_stream(stream));
+}

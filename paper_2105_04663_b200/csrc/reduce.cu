@@ -1,0 +1,225 @@
+// Reductions (reference simulator.py:242-257) and the fused row softmax.
+//
+// out[kept] = init (+) reduce_{reduced dims} in[...]; integer reductions wrap
+// exactly like numpy; float reductions accumulate in fp32 (bf16 in fp32).
+// Two schedules, both coalesced:
+//  * the innermost input dim is reduced -> one warp per output element,
+//    lanes stride along the contiguous run, shuffle tree at the end;
+//  * the innermost input dim is kept -> one thread per output element,
+//    threads of a warp read adjacent addresses at every reduction step.
+#include "common.cuh"
+
+#include <string.h>
+
+namespace spmd {
+
+struct ReduceArgs {
+  int nk, nr;                        // kept / reduced dim counts
+  int64_t kshape[SPMD_MAX_RANK], kst[SPMD_MAX_RANK];
+  int64_t rshape[SPMD_MAX_RANK], rst[SPMD_MAX_RANK];
+  int64_t nout, nred, in_part;       // per-partition sizes
+  int kind;
+};
+
+template <typename I>
+__device__ __forceinline__ int64_t offset_of(I idx, int n, const int64_t* shape,
+                                             const int64_t* st) {
+  int64_t off = 0;
+#pragma unroll
+  for (int k = SPMD_MAX_RANK - 1; k >= 0; --k) {
+    if (k < n) {
+      I d = (I)shape[k];
+      off += (int64_t)(idx % d) * st[k];
+      idx /= d;
+    }
+  }
+  return off;
+}
+
+template <typename C>
+__device__ __forceinline__ C identity(int kind);
+template <> __device__ __forceinline__ float identity<float>(int kind) {
+  return kind == SPMD_SUM ? 0.f : kind == SPMD_PROD ? 1.f : kind == SPMD_MAX ? -INFINITY : INFINITY;
+}
+template <> __device__ __forceinline__ int32_t identity<int32_t>(int kind) {
+  return kind == SPMD_SUM ? 0 : kind == SPMD_PROD ? 1 : kind == SPMD_MAX ? INT32_MIN : INT32_MAX;
+}
+template <> __device__ __forceinline__ uint32_t identity<uint32_t>(int kind) {
+  return kind == SPMD_SUM ? 0u : kind == SPMD_PROD ? 1u : kind == SPMD_MAX ? 0u : 0xffffffffu;
+}
+template <> __device__ __forceinline__ uint8_t identity<uint8_t>(int kind) {
+  return kind == SPMD_SUM ? 0 : kind == SPMD_PROD ? 1 : kind == SPMD_MAX ? 0 : 1;
+}
+
+template <typename T>
+__device__ __forceinline__ typename Compute<T>::type shfl_combine(int kind,
+                                                                  typename Compute<T>::type v) {
+  typedef typename Compute<T>::type C;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    C w = __shfl_xor_sync(0xffffffffu, v, o);
+    v = combine<C>(kind, v, w);
+  }
+  return v;
+}
+
+template <typename T>
+__global__ void reduce_warp_kernel(const T* __restrict__ in, const T* __restrict__ init,
+                                   T* __restrict__ out, ReduceArgs a, int64_t nparts) {
+  typedef typename Compute<T>::type C;
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const int64_t total = a.nout * nparts;
+  for (int64_t w = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); w < total;
+       w += warps) {
+    int64_t p = w / a.nout, o = w - p * a.nout;
+    const T* base = in + p * a.in_part + offset_of<int64_t>(o, a.nk, a.kshape, a.kst);
+    C acc = identity<C>(a.kind);
+    for (int64_t r = lane; r < a.nred; r += 32)
+      acc = combine<C>(a.kind, acc, ld<T>(base[offset_of<int64_t>(r, a.nr, a.rshape, a.rst)]));
+    acc = shfl_combine<T>(a.kind, acc);
+    if (lane == 0) out[w] = st<T>(combine<C>(a.kind, acc, ld<T>(init[p])));
+  }
+}
+
+template <typename T>
+__global__ void reduce_thread_kernel(const T* __restrict__ in, const T* __restrict__ init,
+                                     T* __restrict__ out, ReduceArgs a, int64_t nparts) {
+  typedef typename Compute<T>::type C;
+  const int64_t total = a.nout * nparts;
+  for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < total;
+       w += (int64_t)gridDim.x * blockDim.x) {
+    int64_t p = w / a.nout, o = w - p * a.nout;
+    const T* base = in + p * a.in_part + offset_of<int64_t>(o, a.nk, a.kshape, a.kst);
+    C acc = identity<C>(a.kind);
+    for (int64_t r = 0; r < a.nred; ++r)
+      acc = combine<C>(a.kind, acc, ld<T>(base[offset_of<int64_t>(r, a.nr, a.rshape, a.rst)]));
+    out[w] = st<T>(combine<C>(a.kind, acc, ld<T>(init[p])));
+  }
+}
+
+// Row softmax over a contiguous last dim of length L: one warp per row, the
+// row held in registers when L <= 32*32, else three streaming passes.
+template <typename T, int PER_LANE>
+__global__ void softmax_rows_kernel(const T* __restrict__ in, T* __restrict__ out, int64_t rows,
+                                    int64_t L) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t row = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); row < rows;
+       row += warps) {
+    const T* x = in + row * L;
+    T* y = out + row * L;
+    float m = -INFINITY;
+    if (PER_LANE > 0) {
+      float v[PER_LANE > 0 ? PER_LANE : 1];
+#pragma unroll
+      for (int j = 0; j < PER_LANE; ++j) {
+        int64_t c = lane + 32 * j;
+        v[j] = c < L ? ld<T>(x[c]) : -INFINITY;
+        m = vmax<float>(m, v[j]);
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) m = vmax<float>(m, __shfl_xor_sync(0xffffffffu, m, o));
+      float s = 0.f;
+#pragma unroll
+      for (int j = 0; j < PER_LANE; ++j) {
+        int64_t c = lane + 32 * j;
+        v[j] = c < L ? expf(v[j] - m) : 0.f;
+        s += v[j];
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+#pragma unroll
+      for (int j = 0; j < PER_LANE; ++j) {
+        int64_t c = lane + 32 * j;
+        if (c < L) y[c] = st<T>(v[j] / s);
+      }
+    } else {
+      for (int64_t c = lane; c < L; c += 32) m = vmax<float>(m, ld<T>(x[c]));
+      for (int o = 16; o > 0; o >>= 1) m = vmax<float>(m, __shfl_xor_sync(0xffffffffu, m, o));
+      float s = 0.f;
+      for (int64_t c = lane; c < L; c += 32) s += expf(ld<T>(x[c]) - m);
+      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+      for (int64_t c = lane; c < L; c += 32) y[c] = st<T>(expf(ld<T>(x[c]) - m) / s);
+    }
+  }
+}
+
+}  // namespace spmd
+
+using namespace spmd;
+
+extern "C" int spmd_reduce(spmd_tensor in, spmd_tensor init, spmd_tensor out, const int32_t* dims,
+                           int ndims, int kind, int64_t nparts, void* stream) {
+  SPMD_CHECK_ARG(in.dtype == out.dtype && init.dtype == in.dtype && init.rank == 0,
+                 "reduce dtype mismatch");
+  SPMD_CHECK_ARG(kind >= 0 && kind <= 3, "bad reduce kind");
+  bool red[SPMD_MAX_RANK] = {false};
+  for (int i = 0; i < ndims; ++i) {
+    SPMD_CHECK_ARG(dims[i] >= 0 && dims[i] < in.rank, "reduce dim out of range");
+    red[dims[i]] = true;
+  }
+  ReduceArgs a;
+  memset(&a, 0, sizeof(a));
+  a.kind = kind;
+  int64_t st_[SPMD_MAX_RANK];
+  int64_t acc = 1;
+  for (int k = in.rank - 1; k >= 0; --k) {
+    st_[k] = acc;
+    acc *= in.dims[k];
+  }
+  a.in_part = acc;
+  a.nout = a.nred = 1;
+  for (int k = 0; k < in.rank; ++k) {
+    if (red[k]) {
+      a.rshape[a.nr] = in.dims[k];
+      a.rst[a.nr++] = st_[k];
+      a.nred *= in.dims[k];
+    } else {
+      a.kshape[a.nk] = in.dims[k];
+      a.kst[a.nk++] = st_[k];
+      a.nout *= in.dims[k];
+    }
+  }
+  SPMD_CHECK_ARG(a.nout == numel(out), "reduce output shape mismatch");
+  if (a.nout * nparts == 0) return SPMD_OK;
+  cudaStream_t s = as_stream(stream);
+  const bool inner_reduced = in.rank > 0 && red[in.rank - 1];
+  SPMD_DISPATCH(in.dtype, T, {
+    if (inner_reduced || a.nout * nparts < 148 * 64) {
+      int64_t warps = a.nout * nparts;
+      reduce_warp_kernel<T><<<grid_for(warps * 32, 256), 256, 0, s>>>(
+          (const T*)in.data, (const T*)init.data, (T*)out.data, a, nparts);
+    } else {
+      reduce_thread_kernel<T><<<grid_for(a.nout * nparts, 256), 256, 0, s>>>(
+          (const T*)in.data, (const T*)init.data, (T*)out.data, a, nparts);
+    }
+  });
+  return launched(s);
+}
+
+extern "C" int spmd_softmax_lastdim(spmd_tensor in, spmd_tensor out, int64_t nparts,
+                                    void* stream) {
+  SPMD_CHECK_ARG(in.dtype == out.dtype && (in.dtype == SPMD_F32 || in.dtype == SPMD_BF16) &&
+                     in.rank >= 1 && numel(in) == numel(out),
+                 "softmax expects f32/bf16 with rank >= 1");
+  int64_t L = in.dims[in.rank - 1];
+  int64_t rows = L ? numel(in) / L * nparts : 0;
+  if (rows == 0) return SPMD_OK;
+  cudaStream_t s = as_stream(stream);
+  unsigned grid = grid_for(rows * 32, 256);
+#define SOFTMAX_LAUNCH(T)                                                                        \
+  if (L <= 32 * 8)                                                                               \
+    softmax_rows_kernel<T, 8><<<grid, 256, 0, s>>>((const T*)in.data, (T*)out.data, rows, L);   \
+  else if (L <= 32 * 32)                                                                         \
+    softmax_rows_kernel<T, 32><<<grid, 256, 0, s>>>((const T*)in.data, (T*)out.data, rows, L);  \
+  else                                                                                           \
+    softmax_rows_kernel<T, 0><<<grid, 256, 0, s>>>((const T*)in.data, (T*)out.data, rows, L);
+  if (in.dtype == SPMD_F32) {
+    SOFTMAX_LAUNCH(float)
+  } else {
+    SOFTMAX_LAUNCH(bf16)
+  }
+#undef SOFTMAX_LAUNCH
+  return launched(s);
+}

@@ -1,0 +1,773 @@
+"""B200 executor for partitioned SPMD programs.
+
+Replaces the reference's lockstep NumPy interpreter ``evaluate_spmd``
+(``minispmd/simulator.py:393-426``): every instruction of the per-device
+program is dispatched to one C-ABI entry point (``include/spmd_b200.h``),
+which launches hand-written sm_100a kernels on the current CUDA stream;
+collectives go to NCCL (one process per GPU) or, when one GPU simulates the
+whole mesh, to loopback kernels with the reference's exact semantics.
+
+Values live on the device *partition-stacked*: a per-device value of shape
+``dims`` is a tensor ``[P, *dims]`` where ``P`` is the number of partitions
+this process executes (``P = N`` for a simulated mesh on one GPU, ``P = 1``
+with one process per GPU).  Reshape is a free view of that layout.
+
+Executor-level fusions (``fuse=True``, default off for bit-level parity
+runs) replace op chains by single kernels with identical semantics:
+  * reduce-max / broadcast / subtract / exp / reduce-sum / broadcast /
+    divide over the last dim  ->  one row-softmax kernel;
+  * dot followed only by relu ->  relu in the GEMM epilogue.
+
+Public functions ``evaluate_single`` / ``evaluate_spmd`` /
+``verify_equivalence`` keep the reference signatures
+(``simulator.py:304, 393, 438``) and raise the reference's exception classes.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import dataclasses
+from typing import Mapping, Optional, Sequence
+
+import numpy as np
+
+from . import _capi as C
+from .ir import (COLLECTIVES, ELEMENTWISE_BINARY, ELEMENTWISE_UNARY,
+                 CompareDirection, DType, Graph, Instruction, Op, ReduceKind,
+                 Shape, np_dtype)
+
+
+class EvalError(Exception):
+    pass
+
+
+class DivideByZero(EvalError):
+    pass
+
+
+class SubgroupMismatch(EvalError):
+    pass
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def torch_dtype(dt: DType):
+    t = _torch()
+    return {DType.F32: t.float32, DType.S32: t.int32, DType.U32: t.int32,
+            DType.PRED: t.uint8, DType.BF16: t.bfloat16}[dt]
+
+
+_UNARY = {Op.NEGATE: 0, Op.EXP: 1, Op.RELU: 2}
+_BINARY = {Op.ADD: 0, Op.MULTIPLY: 1, Op.MAXIMUM: 2, Op.SUBTRACT: 3,
+           Op.DIVIDE: 4, Op.COMPARE: 5}
+_CMP = {CompareDirection.EQ: 0, CompareDirection.NE: 1, CompareDirection.LT: 2,
+        CompareDirection.LE: 3, CompareDirection.GT: 4, CompareDirection.GE: 5}
+_KIND = {ReduceKind.SUM: 0, ReduceKind.MAX: 1, ReduceKind.MIN: 2, ReduceKind.PROD: 3}
+
+
+def desc(t, shape: Shape) -> C.SpmdTensor:
+    """Descriptor of a partition-stacked tensor holding per-partition ``shape``."""
+    d = C.SpmdTensor()
+    d.data = t.data_ptr()
+    d.dtype = C.DTYPE_CODE[shape.dtype]
+    d.rank = shape.rank
+    for i, n in enumerate(shape.dims):
+        d.dims[i] = n
+    return d
+
+
+def _groups_arg(subgroups):
+    flat = [d for g in subgroups for d in g]
+    sizes = {len(g) for g in subgroups}
+    if len(sizes) != 1:
+        raise SubgroupMismatch(f"subgroups {subgroups} have unequal sizes")
+    return C.i32_array(flat), len(subgroups), sizes.pop()
+
+
+class NcclComm:
+    """Per-process NCCL communicator (world + cached subgroup splits)."""
+
+    def __init__(self, rank: int, world: int, unique_id: Optional[bytes] = None):
+        lib = C.lib()
+        self.rank, self.world = rank, world
+        n = lib.spmd_comm_id_bytes()
+        if unique_id is None:
+            buf = ctypes.create_string_buffer(n)
+            C.check(lib.spmd_comm_get_unique_id(buf), "spmd_comm_get_unique_id")
+            unique_id = buf.raw
+        self.unique_id = unique_id
+        self.handle = ctypes.c_void_p()
+        idbuf = ctypes.create_string_buffer(unique_id, n)
+        C.check(lib.spmd_comm_init(ctypes.byref(self.handle), world, rank, idbuf),
+                "spmd_comm_init")
+        self._ws = None
+
+    @staticmethod
+    def from_torch_distributed():
+        """Create with the rank/world of ``torch.distributed`` (unique id
+        broadcast through its store)."""
+        torch = _torch()
+        import torch.distributed as dist
+        rank, world = dist.get_rank(), dist.get_world_size()
+        obj = [NcclComm._new_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        return NcclComm(rank, world, obj[0])
+
+    @staticmethod
+    def _new_id() -> bytes:
+        lib = C.lib()
+        buf = ctypes.create_string_buffer(lib.spmd_comm_id_bytes())
+        C.check(lib.spmd_comm_get_unique_id(buf), "spmd_comm_get_unique_id")
+        return buf.raw
+
+    def ensure_workspace(self, nbytes: int, device) -> None:
+        torch = _torch()
+        if self._ws is None or self._ws.numel() < nbytes:
+            self._ws = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=device)
+            C.check(C.lib().spmd_comm_set_workspace(self.handle, self._ws.data_ptr(),
+                                                    self._ws.numel()),
+                    "spmd_comm_set_workspace")
+
+    def close(self):
+        if self.handle:
+            C.lib().spmd_comm_destroy(self.handle)
+            self.handle = ctypes.c_void_p()
+
+
+@dataclasses.dataclass
+class _Step:
+    ins: Instruction
+    fn: object              # callable(env, stream) -> tensor
+    frees: tuple = ()
+
+
+class Executor:
+    """Compiled per-process runner of one SpmdProgram."""
+
+    def __init__(self, program, nparts: Optional[int] = None, device=None,
+                 comm: Optional[NcclComm] = None, partition_base: int = 0,
+                 fuse: bool = False):
+        torch = _torch()
+        self.lib = C.lib()
+        self.program = program
+        self.graph: Graph = program.graph
+        self.P = int(nparts if nparts is not None else program.num_partitions)
+        self.comm = comm
+        self.base = partition_base
+        self.device = torch.device(device) if device is not None else \
+            torch.device("cuda", torch.cuda.current_device())
+        self.by_id = self.graph.by_id
+        self.params = self.graph.parameters
+        self.fuse = fuse
+        self._consts: dict[str, object] = {}
+        self._fused_skip: set[str] = set()
+        self._fused: dict[str, object] = {}
+        if fuse:
+            self._plan_fusions()
+        self.steps = self._compile()
+        if comm is not None:
+            comm.ensure_workspace(self._workspace_bytes(), self.device)
+
+    # ------------------------------------------------------------------
+    def _shape(self, vid: str) -> Shape:
+        return self.by_id[vid].shape
+
+    def _alloc(self, shape: Shape):
+        torch = _torch()
+        return torch.empty((self.P,) + shape.dims, dtype=torch_dtype(shape.dtype),
+                           device=self.device)
+
+    def _workspace_bytes(self) -> int:
+        need = 0
+        for ins in self.graph.instructions:
+            if ins.opcode in COLLECTIVES and ins.opcode != Op.COLLECTIVE_PERMUTE:
+                src = self._shape(ins.operands[0])
+                n = max(src.num_elements, ins.shape.num_elements)
+                need = max(need, 2 * n * ins.shape.dtype.itemsize)
+        return need
+
+    # ------------------------------------------------------------------
+    # fusion planning
+    # ------------------------------------------------------------------
+    def _users(self):
+        users: dict[str, list[str]] = {}
+        for ins in self.graph.instructions:
+            for o in ins.operands:
+                users.setdefault(o, []).append(ins.id)
+        return users
+
+    def _plan_fusions(self):
+        users = self._users()
+        outs = set(self.graph.outputs)
+        by = self.by_id
+
+        def only_user(vid, op):
+            u = users.get(vid, [])
+            return len(u) == 1 and by[u[0]].opcode == op and vid not in outs
+
+        def const_value(vid):
+            c = by[vid]
+            if c.opcode != Op.CONSTANT:
+                return None
+            lit = np.asarray(c.attrs["literal"])
+            return float(lit) if lit.size == 1 else None
+
+        for ins in self.graph.instructions:
+            # softmax: e=exp(x - bcast(max(x))); e / bcast(sum(e))
+            if ins.opcode == Op.REDUCE and ins.attrs["kind"] == ReduceKind.MAX \
+                    and ins.shape.dtype.is_float:
+                x = ins.operands[0]
+                xs = self._shape(x)
+                if tuple(ins.attrs["dims"]) != (xs.rank - 1,) or const_value(ins.operands[1]) != -np.inf:
+                    continue
+                if not only_user(ins.id, Op.BROADCAST):
+                    continue
+                mxb = by[users[ins.id][0]]
+                if tuple(mxb.attrs["broadcast_dims"]) != tuple(range(xs.rank - 1)):
+                    continue
+                if not only_user(mxb.id, Op.SUBTRACT):
+                    continue
+                sub = by[users[mxb.id][0]]
+                if sub.operands != (x, mxb.id) or not only_user(sub.id, Op.EXP):
+                    continue
+                e = by[users[sub.id][0]]
+                eu = users.get(e.id, [])
+                if len(eu) != 2 or e.id in outs:
+                    continue
+                red = [by[u] for u in eu if by[u].opcode == Op.REDUCE]
+                div = [by[u] for u in eu if by[u].opcode == Op.DIVIDE]
+                if len(red) != 1 or len(div) != 1:
+                    continue
+                red, div = red[0], div[0]
+                if red.attrs["kind"] != ReduceKind.SUM or tuple(red.attrs["dims"]) != (xs.rank - 1,) \
+                        or red.operands[0] != e.id or const_value(red.operands[1]) != 0.0:
+                    continue
+                if not only_user(red.id, Op.BROADCAST):
+                    continue
+                denb = by[users[red.id][0]]
+                if tuple(denb.attrs["broadcast_dims"]) != tuple(range(xs.rank - 1)):
+                    continue
+                if div.operands != (e.id, denb.id) or len(users.get(denb.id, [])) != 1:
+                    continue
+                for vid in (ins.id, mxb.id, sub.id, e.id, red.id, denb.id):
+                    self._fused_skip.add(vid)
+                self._fused[div.id] = ("softmax", x)
+            # dot -> relu epilogue
+            if ins.opcode == Op.DOT and only_user(ins.id, Op.RELU) and ins.shape.dtype == DType.BF16:
+                relu = by[users[ins.id][0]]
+                self._fused_skip.add(ins.id)
+                self._fused[relu.id] = ("dot_relu", ins)
+
+    # ------------------------------------------------------------------
+    # compilation: one closure per instruction
+    # ------------------------------------------------------------------
+    def _compile(self) -> list[_Step]:
+        last_use: dict[str, int] = {}
+        instrs = [i for i in self.graph.instructions if i.id not in self._fused_skip]
+        for k, ins in enumerate(instrs):
+            for o in self._operands_of(ins):
+                last_use[o] = k
+        keep = set(self.graph.outputs)
+        steps = []
+        for k, ins in enumerate(instrs):
+            fn = self._make_step(ins)
+            frees = tuple(o for o in set(self._operands_of(ins))
+                          if last_use.get(o) == k and o not in keep)
+            steps.append(_Step(ins, fn, frees))
+        return steps
+
+    def _operands_of(self, ins: Instruction):
+        f = self._fused.get(ins.id)
+        if f is None:
+            return ins.operands
+        if f[0] == "softmax":
+            return (f[1],)
+        return f[1].operands
+
+    def _make_step(self, ins: Instruction):
+        lib = self.lib
+        op = ins.opcode
+        P = self.P
+        shp = ins.shape
+        f = self._fused.get(ins.id)
+        if f is not None and f[0] == "softmax":
+            x = f[1]
+            xs = self._shape(x)
+
+            def run(env, s):
+                out = self._alloc(shp)
+                C.check(lib.spmd_softmax_lastdim(desc(env[x], xs), desc(out, shp), P, s),
+                        "spmd_softmax_lastdim")
+                return out
+            return run
+        if f is not None and f[0] == "dot_relu":
+            return self._dot_step(f[1], shp, epilogue=1)
+
+        if op == Op.PARAMETER:
+            idx = [p.id for p in self.params].index(ins.id)
+            return lambda env, s: env["__inputs__"][idx]
+        if op == Op.CONSTANT:
+            return lambda env, s: self._constant(ins)
+        if op == Op.IOTA:
+            axis = ins.attrs["iota_dimension"]
+
+            def run(env, s):
+                out = self._alloc(shp)
+                C.check(lib.spmd_iota(desc(out, shp), axis, P, s), "spmd_iota")
+                return out
+            return run
+        if op == Op.PARTITION_ID:
+            base = self.base
+
+            def run(env, s):
+                out = self._alloc(shp)
+                C.check(lib.spmd_partition_id(desc(out, shp), P, base, s), "spmd_partition_id")
+                return out
+            return run
+        if op in ELEMENTWISE_UNARY:
+            code = _UNARY[op]
+            a = ins.operands[0]
+
+            def run(env, s):
+                out = self._alloc(shp)
+                C.check(lib.spmd_unary(code, desc(env[a], shp), desc(out, shp), P, s), op.value)
+                return out
+            return run
+        if op in ELEMENTWISE_BINARY:
+            code = _BINARY[op]
+            cmp = _CMP[ins.attrs["direction"]] if op == Op.COMPARE else 0
+            a, b = ins.operands
+            ish = self._shape(a)
+
+            def run(env, s):
+                out = self._alloc(shp)
+                C.check(lib.spmd_binary(code, cmp, desc(env[a], ish), desc(env[b], ish),
+                                        desc(out, shp), P, s), op.value)
+                return out
+            return run
+        if op == Op.SELECT:
+            p_, a, b = ins.operands
+            psh = self._shape(p_)
+
+            def run(env, s):
+                out = self._alloc(shp)
+                C.check(lib.spmd_select(desc(env[p_], psh), desc(env[a], shp),
+                                        desc(env[b], shp), desc(out, shp), P, s), "select")
+                return out
+            return run
+        if op == Op.BROADCAST:
+            a = ins.operands[0]
+            ash = self._shape(a)
+            bd = C.i32_array(ins.attrs["broadcast_dims"])
+
+            def run(env, s):
+                out = self._alloc(shp)
+                C.check(lib.spmd_broadcast(desc(env[a], ash), desc(out, shp), bd, P, s),
+                        "broadcast")
+                return out
+            return run
+        if op == Op.RESHAPE:
+            a = ins.operands[0]
+            return lambda env, s: env[a].reshape((P,) + shp.dims)
+        if op == Op.TRANSPOSE:
+            a = ins.operands[0]
+            ash = self._shape(a)
+            perm = C.i32_array(ins.attrs["permutation"])
+
+            def run(env, s):
+                out = self._alloc(shp)
+                C.check(lib.spmd_transpose(desc(env[a], ash), desc(out, shp), perm, P, s),
+                        "transpose")
+                return out
+            return run
+        if op == Op.REVERSE:
+            a = ins.operands[0]
+            dims = list(ins.attrs["dims"])
+            arr = C.i32_array(dims)
+
+            def run(env, s):
+                out = self._alloc(shp)
+                C.check(lib.spmd_reverse(desc(env[a], shp), desc(out, shp), arr, len(dims), P, s),
+                        "reverse")
+                return out
+            return run
+        if op == Op.PAD:
+            a, v = ins.operands
+            ash, vsh = self._shape(a), self._shape(v)
+            lo, hi, it = (C.i64_array(ins.attrs[k]) for k in ("low", "high", "interior"))
+
+            def run(env, s):
+                out = self._alloc(shp)
+                C.check(lib.spmd_pad(desc(env[a], ash), desc(env[v], vsh), desc(out, shp),
+                                     lo, hi, it, P, s), "pad")
+                return out
+            return run
+        if op == Op.SLICE:
+            a = ins.operands[0]
+            ash = self._shape(a)
+            st, sd = C.i64_array(ins.attrs["starts"]), C.i64_array(ins.attrs["strides"])
+
+            def run(env, s):
+                out = self._alloc(shp)
+                C.check(lib.spmd_slice(desc(env[a], ash), desc(out, shp), st, sd, P, s), "slice")
+                return out
+            return run
+        if op in (Op.DYNAMIC_SLICE, Op.DYNAMIC_UPDATE_SLICE):
+            a = ins.operands[0]
+            ash = self._shape(a)
+            upd = ins.operands[1] if op == Op.DYNAMIC_UPDATE_SLICE else None
+            first = 2 if upd else 1
+            starts = ins.operands[first:]
+            ssh = [self._shape(x) for x in starts]
+            ush = self._shape(upd) if upd else None
+
+            def run(env, s):
+                out = self._alloc(shp)
+                arr = (C.SpmdTensor * max(1, len(starts)))(
+                    *[desc(env[x], sh) for x, sh in zip(starts, ssh)])
+                if upd is None:
+                    C.check(lib.spmd_dynamic_slice(desc(env[a], ash), arr, desc(out, shp), P, s),
+                            "dynamic-slice")
+                else:
+                    C.check(lib.spmd_dynamic_update_slice(desc(env[a], ash), desc(env[upd], ush),
+                                                          arr, desc(out, shp), P, s),
+                            "dynamic-update-slice")
+                return out
+            return run
+        if op == Op.CONCAT:
+            ops = ins.operands
+            shs = [self._shape(x) for x in ops]
+            axis = ins.attrs["dim"]
+
+            def run(env, s):
+                out = self._alloc(shp)
+                arr = (C.SpmdTensor * max(1, len(ops)))(
+                    *[desc(env[x], sh) for x, sh in zip(ops, shs)])
+                C.check(lib.spmd_concat(arr, len(ops), axis, desc(out, shp), P, s), "concat")
+                return out
+            return run
+        if op == Op.REDUCE:
+            a, init = ins.operands
+            ash, ish = self._shape(a), self._shape(init)
+            dims = list(ins.attrs["dims"])
+            arr = C.i32_array(dims)
+            kind = _KIND[ins.attrs["kind"]]
+
+            def run(env, s):
+                out = self._alloc(shp)
+                C.check(lib.spmd_reduce(desc(env[a], ash), desc(env[init], ish), desc(out, shp),
+                                        arr, len(dims), kind, P, s), "reduce")
+                return out
+            return run
+        if op == Op.DOT:
+            return self._dot_step(ins, shp, epilogue=0)
+        if op == Op.CONVOLUTION:
+            return self._conv_step(ins)
+        if op == Op.ROTATE:
+            a = ins.operands[0]
+            dim, amt = ins.attrs["dim"], ins.attrs["amount"]
+
+            def run(env, s):
+                out = self._alloc(shp)
+                C.check(lib.spmd_rotate(desc(env[a], shp), desc(out, shp), dim, amt, P, s),
+                        "rotate")
+                return out
+            return run
+        if op == Op.SHIFT:
+            a, fill = ins.operands
+            fsh = self._shape(fill)
+            dim, amt = ins.attrs["dim"], ins.attrs["amount"]
+
+            def run(env, s):
+                out = self._alloc(shp)
+                C.check(lib.spmd_shift(desc(env[a], shp), desc(env[fill], fsh), desc(out, shp),
+                                       dim, amt, P, s), "shift")
+                return out
+            return run
+        if op in COLLECTIVES:
+            return self._collective_step(ins)
+        raise EvalError(f"cannot evaluate opcode {op.value}")
+
+    def _dot_step(self, ins, shp, epilogue):
+        lib, P = self.lib, self.P
+        a, b = ins.operands
+        ash, bsh = self._shape(a), self._shape(b)
+        dd = C.SpmdDotDims()
+        at = ins.attrs
+        dd.n_batch = len(at["lhs_batch"])
+        dd.n_contract = len(at["lhs_contracting"])
+        for i, (x, y) in enumerate(zip(at["lhs_batch"], at["rhs_batch"])):
+            dd.lhs_batch[i], dd.rhs_batch[i] = x, y
+        for i, (x, y) in enumerate(zip(at["lhs_contracting"], at["rhs_contracting"])):
+            dd.lhs_contracting[i], dd.rhs_contracting[i] = x, y
+        dd.epilogue = epilogue
+        ref = ctypes.byref(dd)
+
+        def run(env, s):
+            out = self._alloc(shp)
+            C.check(lib.spmd_dot(desc(env[a], ash), desc(env[b], bsh), desc(out, shp), ref, P, s),
+                    "dot")
+            return out
+        return run
+
+    def _conv_step(self, ins):
+        lib, P = self.lib, self.P
+        a, b = ins.operands
+        ash, bsh, shp = self._shape(a), self._shape(b), ins.shape
+        cd = ins.attrs["conv_dims"]
+        win = ins.attrs["window"]
+        c = C.SpmdConvDims()
+        c.lhs_batch, c.lhs_feature = cd.lhs_batch, cd.lhs_feature
+        c.rhs_in_feature, c.rhs_out_feature = cd.rhs_in_feature, cd.rhs_out_feature
+        c.out_batch, c.out_feature = cd.out_batch, cd.out_feature
+        c.n_spatial = len(cd.lhs_spatial)
+        for i, w in enumerate(win):
+            c.lhs_spatial[i], c.rhs_spatial[i] = cd.lhs_spatial[i], cd.rhs_spatial[i]
+            c.out_spatial[i] = cd.out_spatial[i]
+            c.size[i], c.stride[i] = w.size, w.stride
+            c.pad_low[i], c.pad_high[i] = w.padding_low, w.padding_high
+            c.base_dilation[i], c.window_dilation[i] = w.base_dilation, w.window_dilation
+        ref = ctypes.byref(c)
+
+        def run(env, s):
+            out = self._alloc(shp)
+            C.check(lib.spmd_convolution(desc(env[a], ash), desc(env[b], bsh), desc(out, shp),
+                                         ref, P, s), "convolution")
+            return out
+        return run
+
+    def _collective_step(self, ins):
+        lib, P = self.lib, self.P
+        op, shp = ins.opcode, ins.shape
+        a = ins.operands[0]
+        ash = self._shape(a)
+        at = ins.attrs
+        comm = self.comm
+        if op == Op.COLLECTIVE_PERMUTE:
+            flat = [x for pr in at["pairs"] for x in pr]
+            pairs = C.i32_array(flat)
+            npairs = len(at["pairs"])
+
+            def run(env, s):
+                out = self._alloc(shp)
+                if comm is None:
+                    C.check(lib.spmd_local_collective_permute(desc(env[a], ash), desc(out, shp),
+                                                              pairs, npairs, P, s),
+                            "collective-permute")
+                else:
+                    C.check(lib.spmd_collective_permute(comm.handle, desc(env[a], ash),
+                                                        desc(out, shp), pairs, npairs, s),
+                            "collective-permute")
+                return out
+            return run
+        groups, ng, gs = _groups_arg(at["subgroups"])
+        if comm is None and ng * gs != P:
+            raise SubgroupMismatch(f"subgroups {at['subgroups']} do not partition "
+                                   f"{P} devices")
+
+        def run(env, s):
+            out = self._alloc(shp)
+            x, y = desc(env[a], ash), desc(out, shp)
+            if op == Op.ALL_GATHER:
+                rc = lib.spmd_local_all_gather(x, y, at["dim"], groups, ng, gs, P, s) \
+                    if comm is None else \
+                    lib.spmd_all_gather(comm.handle, x, y, at["dim"], groups, ng, gs, s)
+            elif op == Op.ALL_REDUCE:
+                k = _KIND[at["kind"]]
+                rc = lib.spmd_local_all_reduce(x, y, k, groups, ng, gs, P, s) \
+                    if comm is None else \
+                    lib.spmd_all_reduce(comm.handle, x, y, k, groups, ng, gs, s)
+            elif op == Op.REDUCE_SCATTER:
+                k = _KIND[at["kind"]]
+                rc = lib.spmd_local_reduce_scatter(x, y, at["dim"], k, groups, ng, gs, P, s) \
+                    if comm is None else \
+                    lib.spmd_reduce_scatter(comm.handle, x, y, at["dim"], k, groups, ng, gs, s)
+            else:
+                rc = lib.spmd_local_all_to_all(x, y, at["split_dim"], at["concat_dim"], groups,
+                                               ng, gs, P, s) \
+                    if comm is None else \
+                    lib.spmd_all_to_all(comm.handle, x, y, at["split_dim"], at["concat_dim"],
+                                        groups, ng, gs, s)
+            C.check(rc, op.value)
+            return out
+        return run
+
+    def _constant(self, ins: Instruction):
+        t = self._consts.get(ins.id)
+        if t is None:
+            t = upload_stacked([np.asarray(ins.attrs["literal"])] * self.P, ins.shape,
+                               self.device, self.lib)
+            self._consts[ins.id] = t
+        return t
+
+    # ------------------------------------------------------------------
+    def run(self, inputs: Sequence, stream=None, keep: Optional[set] = None) -> list:
+        """Execute on stacked device inputs ``[P, *param_dims]``; returns the
+        stacked device outputs.  ``keep``: extra value ids to retain
+        (returned via ``self.last_env``)."""
+        torch = _torch()
+        s = stream if stream is not None else torch.cuda.current_stream(self.device).cuda_stream
+        if len(inputs) != len(self.params):
+            raise EvalError(f"expected {len(self.params)} inputs, got {len(inputs)}")
+        env = {"__inputs__": list(inputs)}
+        keep = keep or set()
+        for step in self.steps:
+            env[step.ins.id] = step.fn(env, s)
+            for vid in step.frees:
+                if vid not in keep:
+                    env.pop(vid, None)
+        self.last_env = env if keep else None
+        return [env[o] for o in self.graph.outputs]
+
+    def check_errors(self, stream=None) -> None:
+        torch = _torch()
+        s = stream if stream is not None else torch.cuda.current_stream(self.device).cuda_stream
+        C.check(self.lib.spmd_check_device_errors(s), "device")
+
+
+# ---------------------------------------------------------------------------
+# host <-> device
+# ---------------------------------------------------------------------------
+
+def upload_stacked(arrays: Sequence[np.ndarray], shape: Shape, device, lib=None):
+    """Stack per-partition host arrays into one device tensor ``[P, *dims]``."""
+    torch = _torch()
+    lib = lib or C.lib()
+    P = len(arrays)
+    if shape.dtype == DType.BF16:
+        host = np.stack([np.asarray(a, dtype=np.float32).reshape(shape.dims) for a in arrays])
+        f32 = torch.from_numpy(np.ascontiguousarray(host)).to(device)
+        out = torch.empty((P,) + shape.dims, dtype=torch.bfloat16, device=device)
+        s = torch.cuda.current_stream(device).cuda_stream
+        C.check(lib.spmd_convert(desc(f32, Shape(shape.dims, DType.F32)), desc(out, shape), P, s),
+                "convert")
+        return out
+    host = np.stack([np.asarray(a, dtype=np_dtype(shape.dtype)).reshape(shape.dims)
+                     for a in arrays])
+    if shape.dtype == DType.U32:
+        host = host.view(np.int32)
+    elif shape.dtype == DType.PRED:
+        host = host.astype(np.uint8)
+    return torch.from_numpy(np.ascontiguousarray(host)).to(device)
+
+
+def download_stacked(t, shape: Shape, lib=None) -> list[np.ndarray]:
+    """Device ``[P, *dims]`` -> list of per-partition host arrays (bf16 as
+    float32)."""
+    torch = _torch()
+    lib = lib or C.lib()
+    if shape.dtype == DType.BF16:
+        f32 = torch.empty(t.shape, dtype=torch.float32, device=t.device)
+        s = torch.cuda.current_stream(t.device).cuda_stream
+        C.check(lib.spmd_convert(desc(t, shape), desc(f32, Shape(shape.dims, DType.F32)),
+                                 t.shape[0], s), "convert")
+        host = f32.cpu().numpy()
+    else:
+        host = t.cpu().numpy()
+        if shape.dtype == DType.U32:
+            host = host.view(np.uint32)
+        elif shape.dtype == DType.PRED:
+            host = host.astype(np.bool_)
+    return [host[p] for p in range(host.shape[0])]
+
+
+# ---------------------------------------------------------------------------
+# reference-compatible entry points
+# ---------------------------------------------------------------------------
+
+def evaluate_spmd(program, per_device_inputs: Mapping[int, Sequence[np.ndarray]],
+                  fuse: bool = False, device=None) -> dict[int, list[np.ndarray]]:
+    """Lockstep-equivalent evaluation of ``program`` on a simulated mesh of
+    ``program.num_partitions`` partitions stacked on one B200
+    (reference ``simulator.py:393-426``)."""
+    torch = _torch()
+    dev = torch.device(device) if device is not None else torch.device("cuda", 0)
+    n = program.num_partitions
+    ex = Executor(program, nparts=n, device=dev, fuse=fuse)
+    params = program.graph.parameters
+    for d in range(n):
+        if len(per_device_inputs[d]) != len(params):
+            raise EvalError(f"device {d}: expected {len(params)} inputs")
+    stacked = [upload_stacked([per_device_inputs[d][k] for d in range(n)], p.shape, dev)
+               for k, p in enumerate(params)]
+    with torch.cuda.device(dev):
+        outs = ex.run(stacked)
+        ex.check_errors()
+    host = [download_stacked(o, program.graph.instr(oid).shape)
+            for o, oid in zip(outs, program.graph.outputs)]
+    return {d: [h[d] for h in host] for d in range(n)}
+
+
+def evaluate_single(graph: Graph, inputs: Sequence[np.ndarray], fuse: bool = False,
+                    device=None) -> list[np.ndarray]:
+    """Single-device evaluation of an unpartitioned graph on one B200
+    (reference ``simulator.py:304-319``; rejects SPMD-only opcodes)."""
+    from .partitioner import SpmdProgram
+    for ins in graph.instructions:
+        if ins.opcode in COLLECTIVES or ins.opcode == Op.PARTITION_ID:
+            raise EvalError(f"{ins.id}: {ins.opcode.value} is SPMD-only")
+    if len(inputs) != len(graph.parameters):
+        raise EvalError(f"expected {len(graph.parameters)} inputs, got {len(inputs)}")
+    prog = SpmdProgram(graph, 1, {}, (), ())
+    return evaluate_spmd(prog, {0: list(inputs)}, fuse=fuse, device=device)[0]
+
+
+@dataclasses.dataclass
+class EquivalenceReport:
+    passed: bool
+    max_abs_error: float
+    max_rel_error: float
+    collective_counts: dict[str, int]
+    details: list[str] = dataclasses.field(default_factory=list)
+
+
+def verify_equivalence(graph: Graph, annotated_graph: Graph, num_devices: int,
+                       inputs: Sequence[np.ndarray], tolerance: float = 1e-4,
+                       pad_value=0, plan: str = "reference",
+                       fuse: bool = False) -> EquivalenceReport:
+    """Partition, run on the B200 (simulated mesh), reassemble, and compare
+    with the single-device B200 run (reference ``simulator.py:438-490``;
+    metric: max|err| / max(max|expected|, 1) <= tolerance; ints exact)."""
+    from .partitioner import partition
+    from .sharding import assemble_data, shard_data
+    expected = evaluate_single(graph, inputs, fuse=fuse)
+    program = partition(annotated_graph, num_devices, plan=plan)
+    devices = list(range(num_devices))
+    per_dev: dict[int, list] = {d: [] for d in devices}
+    for p, val in zip(annotated_graph.parameters, inputs):
+        arr = np.asarray(val, dtype=np_dtype(p.shape.dtype)).reshape(p.shape.dims)
+        shards = shard_data(arr, p.sharding, pad_value=pad_value, devices=devices)
+        for d in devices:
+            per_dev[d].append(shards[d])
+    results = evaluate_spmd(program, per_dev, fuse=fuse)
+    max_abs = max_rel = 0.0
+    passed = True
+    details = []
+    for i, oid in enumerate(graph.outputs):
+        shape = graph.instr(oid).shape
+        actual = assemble_data({d: results[d][i] for d in devices},
+                               program.output_shardings[i], shape,
+                               rtol=max(tolerance, 1e-6))
+        exp = expected[i]
+        if shape.dtype.is_float:
+            a64, e64 = np.asarray(actual, np.float64), np.asarray(exp, np.float64)
+            err = float(np.max(np.abs(a64 - e64))) if e64.size else 0.0
+            scale = float(np.max(np.abs(e64))) if e64.size else 0.0
+            rel = err / max(scale, 1.0)
+            max_abs, max_rel = max(max_abs, err), max(max_rel, rel)
+            if rel > tolerance:       # NaN compares false, as in the reference
+                passed = False
+                details.append(f"output {oid}: rel error {rel} > {tolerance}")
+        elif not np.array_equal(actual, exp):
+            passed = False
+            diff = np.max(np.abs(actual.astype(np.int64) - exp.astype(np.int64)))
+            max_abs = max(max_abs, float(diff))
+            details.append(f"output {oid}: integer mismatch")
+    counts: dict[str, int] = {}
+    for ins in program.graph.instructions:
+        if ins.opcode in COLLECTIVES:
+            counts[ins.opcode.value] = counts.get(ins.opcode.value, 0) + 1
+    return EquivalenceReport(passed, max_abs, max_rel, counts, details)
