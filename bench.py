@@ -1,0 +1,372 @@
+#!/usr/bin/env python
+"""Benchmark: 2-D (data x model) sharded Transformer layer (BASELINE configs[1])
+through the B200 partitioned-execution path.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...        (N > 1)
+
+Workload (config C2, paper Table-2 dims): M=8192, H=65536,
+N=128 heads, D=256, S=1024, global batch B=16, bf16, synthetic random data
+generated on the device.  Mesh per GPU count: 1 (1,1), 2 (1,2), 4 (2,2),
+8 (2,4) as (X=data, Y=model); annotations per PAPER.md:679.  One step =
+one forward pass of the layer: propagate -> partition (fast plan, done once)
+-> per-rank executor (tcgen05 GEMMs, fused softmax, NCCL collectives).
+Total work is fixed as N grows ("scaling": "strong").
+
+`value` = aggregate layer TFLOP/s over all GPUs (algorithmic FLOPs
+2T(3MND+NDM+2MH)+4BNS^2D per step / step time, max over ranks);
+`tflops_per_gpu` and `mfu` are the per-GPU views of the same number.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "sharded Transformer layer TFLOP/s/GPU & MFU at 1/2/4/8 B200; reshard GB/s"
+MESHES = {1: (1, 1), 2: (1, 2), 4: (2, 2), 8: (2, 4)}
+PAPER = dict(B=16, S=1024, M=8192, N=128, D=256, H=65536)
+SPEC_BF16_TFLOPS = 2250.0
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return p.get("bf16_tflops", 1590.0), p.get("bf16_tflops_sustained", 1400.0), \
+            p.get("hbm_gbs", 6650.0), "measured"
+    except Exception:
+        return 1590.0, 1400.0, 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.proc = None
+        self.lines: list[str] = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        sm.sort()
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def _dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def _cpu_baseline(mesh, steps=1):
+    """Reference executor restated on the CPU (oracle port, single-threaded
+    float64 einsum like the reference) on a bounded sample of the C2 graph:
+    same annotations/mesh, dims M=1024 N=16 D=64 H=8192 B=1 S=256."""
+    import numpy as np
+    from oracle import evaluator as O
+    from paper_2105_04663_b200 import partition, propagate
+    from paper_2105_04663_b200.ir import DType
+    from paper_2105_04663_b200.sharding import shard_data
+    from paper_2105_04663_b200.workloads import transformer_flops, transformer_layer
+    dims = dict(B=max(1, mesh[0]), S=256, M=1024, N=16, D=64, H=8192)
+    g, ins = transformer_layer(mesh, dtype=DType.F32, seed=1, **dims)
+    ann, _ = propagate(g)
+    n = mesh[0] * mesh[1]
+    prog = partition(ann, n)
+    devices = list(range(n))
+    per = {d: [] for d in devices}
+    for p, x in zip(ann.parameters, ins):
+        sh = shard_data(x, p.sharding, devices=devices)
+        for d in devices:
+            per[d].append(sh[d])
+    best = None
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        O.evaluate_spmd(prog, per)
+        dt = time.perf_counter() - t0
+        best = dt if best is None else min(best, dt)
+    flops = transformer_flops(**dims)
+    cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+    sample = ("oracle evaluate_spmd of the C2 layer graph, mesh %s, B=%d S=256 M=1024 N=16 "
+              "D=64 H=8192 f32 (%.3g FLOP/step)" % (mesh, dims["B"], flops))
+    return flops / best / 1e12, best, cores, sample
+
+
+def run_reference(args):
+    rank, world, _ = _dist_env()
+    if rank != 0:
+        return 0
+    mesh = MESHES[args.gpus]
+    vals = []
+    for i in range(args.warmup + args.steps):
+        v, t, cores, sample = _cpu_baseline(mesh)
+        if i >= args.warmup:
+            vals.append((v, t))
+    v = sorted(x[0] for x in vals)[len(vals) // 2]
+    t = sorted(x[1] for x in vals)[len(vals) // 2]
+    line = {"metric": METRIC, "impl": "reference", "value": v, "unit": "TFLOP/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": "C2 transformer layer (bounded CPU sample)",
+                       "mesh": list(mesh), "parallelism": "dp%dxmp%d" % mesh},
+            "cpu_baseline": {"value": v, "unit": "TFLOP/s", "cores": cores, "kind": "port",
+                             "sample": sample},
+            "e2e": {"value": v, "unit": "TFLOP/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def _rand_like_shard(shape, device, scale, seed):
+    import torch
+    gen = torch.Generator(device=device)
+    gen.manual_seed(seed)
+    t = torch.randn((1,) + tuple(shape.dims), generator=gen, device=device,
+                    dtype=torch.float32)
+    return (t * scale).to(torch.bfloat16)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--scale", type=float, default=1.0,
+                    help="shrink B (testing only; the reported config is the paper's)")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    from paper_2105_04663_b200 import _capi as C
+    from paper_2105_04663_b200 import collective_stats, partition, propagate
+    from paper_2105_04663_b200.executor import Executor, NcclComm
+    from paper_2105_04663_b200.ir import DType, Op
+    from paper_2105_04663_b200.workloads import transformer_flops, transformer_layer
+
+    rank, world, local = _dist_env()
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    mesh = MESHES[world]
+    dims = dict(PAPER)
+    if args.scale != 1.0:
+        dims["B"] = max(mesh[0], int(dims["B"] * args.scale))
+    g, _ = transformer_layer(mesh, dtype=DType.BF16, with_inputs=False, **dims)
+    ann, _ = propagate(g)
+    prog = partition(ann, world, plan="fast")
+    comm = NcclComm.from_torch_distributed() if world > 1 else None
+    ex = Executor(prog, nparts=1, device=dev, comm=comm, partition_base=rank, fuse=True)
+    flops = transformer_flops(**dims)
+
+    # Synthetic local shards, generated on the device (weights ~ N(0, 1/fan_in)).
+    fan = {"x": 1, "wq": dims["M"], "wk": dims["M"], "wv": dims["M"],
+           "wo": dims["N"] * dims["D"], "wi": dims["M"], "wt": dims["H"]}
+    src_params = {p.attrs["index"]: p.id for p in ann.parameters}
+    inputs = []
+    for p in prog.graph.parameters:
+        name = src_params[p.attrs["index"]]
+        inputs.append(_rand_like_shard(p.shape, dev, 1.0 / np.sqrt(fan[name]),
+                                       seed=1000 * rank + p.attrs["index"]))
+    stream = torch.cuda.current_stream(dev)
+
+    def barrier():
+        if world > 1:
+            dist.barrier(device_ids=[local])
+
+    def step(x_inputs):
+        return ex.run(x_inputs)
+
+    for _ in range(args.warmup):
+        step(inputs)
+    torch.cuda.synchronize()
+    ex.check_errors()
+    barrier()
+
+    sampler = ClockSampler(local)
+    sampler.start()
+    launches0 = C.lib().spmd_launch_count()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    torch.cuda.synchronize()
+    ev0.record(stream)
+    for _ in range(args.steps):
+        out = step(inputs)
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    launches = C.lib().spmd_launch_count() - launches0
+    clocks = sampler.stop()
+    ms = ev0.elapsed_time(ev1) / args.steps
+    t = torch.tensor([ms], device=dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    value = flops / (ms * 1e-3) / 1e12
+
+    # ---- e2e: host (pinned) activation in, host result out, every step ----
+    e2e = None
+    if not args.no_e2e:
+        x_host = torch.empty(inputs[0].shape, dtype=torch.bfloat16, pin_memory=True)
+        x_host.copy_(inputs[0].cpu())
+        out_host = torch.empty(out[0].shape, dtype=torch.bfloat16, pin_memory=True)
+        dev_inputs = list(inputs)
+        x_dev = torch.empty_like(inputs[0])
+        dev_inputs[0] = x_dev
+        for _ in range(2):
+            x_dev.copy_(x_host, non_blocking=True)
+            o = step(dev_inputs)
+            out_host.copy_(o[0], non_blocking=True)
+        torch.cuda.synchronize()
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            x_dev.copy_(x_host, non_blocking=True)
+            o = step(dev_inputs)
+            out_host.copy_(o[0], non_blocking=True)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        ems = e0.elapsed_time(e1) / args.steps
+        t = torch.tensor([ems], device=dev, dtype=torch.float64)
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ems = float(t.item())
+        e2e = {"value": flops / (ems * 1e-3) / 1e12, "unit": "TFLOP/s",
+               "ms_per_step": ems,
+               "h2d_bytes_per_step": int(x_host.numel() * 2 * world),
+               "d2h_bytes_per_step": int(out_host.numel() * 2 * world)}
+
+    # ---- roofline of the dominant kernel: the largest tcgen05 GEMM ----
+    burst, sustained, hbm, peak_src = _peaks()
+    dots = [i for i in prog.graph.instructions if i.opcode == Op.DOT]
+    from paper_2105_04663_b200.ir import dot_dim_lists
+
+    def dot_flops(ins):
+        a = prog.graph.instr(ins.operands[0]).shape
+        bsh = prog.graph.instr(ins.operands[1]).shape
+        lb, rb, lc, rc, lf, rf = dot_dim_lists(ins.attrs, a.rank, bsh.rank)
+        k = int(np.prod([a.dims[d] for d in lc]))
+        return 2.0 * ins.shape.num_elements * k
+
+    top = max(dots, key=dot_flops)
+    top_step = next(s for s in ex.steps if s.ins.id == top.id)
+    env = {"__inputs__": inputs}
+    # materialise the operands of the top GEMM once
+    keep = set(top.operands)
+    ex.run(inputs, keep=keep)
+    env.update({k: v for k, v in ex.last_env.items() if k in keep})
+    for _ in range(3):
+        top_step.fn(env, stream.cuda_stream)
+    torch.cuda.synchronize()
+    k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    reps = 20
+    k0.record(stream)
+    for _ in range(reps):
+        top_step.fn(env, stream.cuda_stream)
+    k1.record(stream)
+    torch.cuda.synchronize()
+    kms = k0.elapsed_time(k1) / reps
+    achieved = dot_flops(top) / (kms * 1e-3) / 1e12
+    gemm_share = None
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        v, tcpu, cores, sample = _cpu_baseline(mesh)
+        cpu = {"value": v, "unit": "TFLOP/s", "cores": cores, "kind": "port",
+               "sample": sample, "seconds_per_sample": tcpu}
+
+    stats = collective_stats(prog)
+    if rank == 0:
+        per_gpu = value / world
+        line = {
+            "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "bf16", "data": "synthetic",
+            "config": {"workload": "C2 transformer layer (attention+FFN), paper dims",
+                       "model_dims": dims, "global_batch": dims["B"], "seq_len": dims["S"],
+                       "mesh": list(mesh), "parallelism": "dp%dxmp%d" % mesh,
+                       "plan": "fast", "l2": "inputs larger than L2 (weights+activations)",
+                       "collectives_per_step": stats["counts"]},
+            "tflops_per_gpu": per_gpu,
+            "mfu": {"vs_spec_2250": per_gpu / SPEC_BF16_TFLOPS,
+                    "vs_measured_sustained": per_gpu / sustained},
+            "roofline": {"bound": "tensor", "kernel": "gemm_bf16_tcgen05 (%s)" % top.id,
+                         "achieved": achieved, "peak": burst, "unit": "TFLOP/s",
+                         "frac": achieved / burst, "peak_source": peak_src + " burst",
+                         "traffic": None, "ms_per_launch": kms,
+                         "flops_per_launch": dot_flops(top)},
+            "e2e": e2e, "gpu_launches": int(launches), "clocks": clocks,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())
