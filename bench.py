@@ -311,7 +311,9 @@ def main():
         return 2.0 * ins.shape.num_elements * k
 
     top = max(dots, key=dot_flops)
-    top_step = next(s for s in ex.steps if s.ins.id == top.id)
+    top_step = next(s for s in ex.steps if s.ins.id == top.id or
+                    (ex._fused.get(s.ins.id) or (None, None))[1] is top)
+    print(f"[bench] step {ms:.2f} ms  ({value:.1f} TFLOP/s aggregate)", file=sys.stderr)
     env = {"__inputs__": inputs}
     # materialise the operands of the top GEMM once
     keep = set(top.operands)
