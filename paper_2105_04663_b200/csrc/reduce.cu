@@ -145,6 +145,80 @@ __global__ void softmax_rows_kernel(const T* __restrict__ in, T* __restrict__ ou
   }
 }
 
+// Vectorised row softmax for contiguous rows with L % 8 == 0 and
+// L <= 256 * CH: each lane owns CH 16-byte chunks (8 bf16 each) of its row,
+// the row never leaves registers, exp is ex2.approx on log2e-prescaled
+// inputs and the normalisation is one reciprocal.  One HBM read + one write
+// per element.
+__device__ __forceinline__ float fast_exp2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+template <int CH>
+__global__ void __launch_bounds__(256, 4)
+    softmax_rows_bf16_vec(const bf16* __restrict__ in, bf16* __restrict__ out, int64_t rows,
+                          int L) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const float LOG2E = 1.4426950408889634f;
+  for (int64_t row = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); row < rows;
+       row += warps) {
+    const uint4* x = reinterpret_cast<const uint4*>(in + row * L);
+    uint4* y = reinterpret_cast<uint4*>(out + row * L);
+    const int nch = L >> 3;
+    uint4 raw[CH];
+#pragma unroll
+    for (int i = 0; i < CH; ++i) {
+      int c = lane + 32 * i;
+      raw[i] = c < nch ? __ldcs(x + c) : make_uint4(0xff80ff80u, 0xff80ff80u, 0xff80ff80u,
+                                                      0xff80ff80u);   // -inf
+    }
+    float m = -INFINITY;
+#pragma unroll
+    for (int i = 0; i < CH; ++i) {
+      const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&raw[i]);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        float2 f = __bfloat1622float2(h[j]);
+        m = vmax<float>(m, vmax<float>(f.x, f.y));
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = vmax<float>(m, __shfl_xor_sync(0xffffffffu, m, o));
+    const float mb = (m == -INFINITY) ? 0.f : m * LOG2E;
+    float v[CH][8];
+    float s = 0.f;
+#pragma unroll
+    for (int i = 0; i < CH; ++i) {
+      const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&raw[i]);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        float2 f = __bfloat1622float2(h[j]);
+        v[i][2 * j] = fast_exp2(fmaf(f.x, LOG2E, -mb));
+        v[i][2 * j + 1] = fast_exp2(fmaf(f.y, LOG2E, -mb));
+        s += v[i][2 * j] + v[i][2 * j + 1];
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    const float r = 1.f / s;
+#pragma unroll
+    for (int i = 0; i < CH; ++i) {
+      int c = lane + 32 * i;
+      if (c < nch) {
+        uint4 o4;
+        __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&o4);
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          h[j] = __floats2bfloat162_rn(v[i][2 * j] * r, v[i][2 * j + 1] * r);
+        __stcs(y + c, o4);
+      }
+    }
+  }
+}
+
 }  // namespace spmd
 
 using namespace spmd;
@@ -208,6 +282,20 @@ extern "C" int spmd_softmax_lastdim(spmd_tensor in, spmd_tensor out, int64_t npa
   if (rows == 0) return SPMD_OK;
   cudaStream_t s = as_stream(stream);
   unsigned grid = grid_for(rows * 32, 256);
+  if (in.dtype == SPMD_BF16 && L % 8 == 0 && L <= 256 * 4 &&
+      (reinterpret_cast<uintptr_t>(in.data) & 15) == 0 &&
+      (reinterpret_cast<uintptr_t>(out.data) & 15) == 0) {
+    if (L <= 256)
+      softmax_rows_bf16_vec<1><<<grid, 256, 0, s>>>((const bf16*)in.data, (bf16*)out.data, rows,
+                                                    (int)L);
+    else if (L <= 512)
+      softmax_rows_bf16_vec<2><<<grid, 256, 0, s>>>((const bf16*)in.data, (bf16*)out.data, rows,
+                                                    (int)L);
+    else
+      softmax_rows_bf16_vec<4><<<grid, 256, 0, s>>>((const bf16*)in.data, (bf16*)out.data, rows,
+                                                    (int)L);
+    return launched(s);
+  }
 #define SOFTMAX_LAUNCH(T)                                                                        \
   if (L <= 32 * 8)                                                                               \
     softmax_rows_kernel<T, 8><<<grid, 256, 0, s>>>((const T*)in.data, (T*)out.data, rows, L);   \

@@ -1,0 +1,96 @@
+"""Micro-benchmarks of the hot kernels at the C2 (paper-dims, 1 GPU) shapes.
+
+    python scripts/kernel_bench.py [gemm|softmax|all]
+
+Times each kernel with CUDA events on the launching stream after warm-up and
+prints one JSON line per case (TFLOP/s or GB/s).
+"""
+
+import ctypes
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+from paper_2105_04663_b200 import _capi as C  # noqa: E402
+from paper_2105_04663_b200.executor import desc  # noqa: E402
+from paper_2105_04663_b200.ir import DType, Op, Shape, infer_shape  # noqa: E402
+
+
+def timeit(fn, reps=10, warm=3):
+    s = torch.cuda.current_stream()
+    for _ in range(warm):
+        fn()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(s)
+    for _ in range(reps):
+        fn()
+    e1.record(s)
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / reps
+
+
+def dot_case(name, lshape, rshape, lb, rb, lc, rc):
+    lib = C.lib()
+    lsh, rsh = Shape(lshape, DType.BF16), Shape(rshape, DType.BF16)
+    attrs = {"lhs_batch": lb, "rhs_batch": rb, "lhs_contracting": lc, "rhs_contracting": rc}
+    osh = infer_shape(Op.DOT, [lsh, rsh], attrs)
+    a = torch.randn((1,) + lshape, device="cuda", dtype=torch.bfloat16)
+    b = torch.randn((1,) + rshape, device="cuda", dtype=torch.bfloat16) * 0.01
+    o = torch.empty((1,) + osh.dims, device="cuda", dtype=torch.bfloat16)
+    dd = C.SpmdDotDims()
+    dd.n_batch, dd.n_contract = len(lb), len(lc)
+    for i, (x, y) in enumerate(zip(lb, rb)):
+        dd.lhs_batch[i], dd.rhs_batch[i] = x, y
+    for i, (x, y) in enumerate(zip(lc, rc)):
+        dd.lhs_contracting[i], dd.rhs_contracting[i] = x, y
+    da, db, do = desc(a, lsh), desc(b, rsh), desc(o, osh)
+    st = torch.cuda.current_stream().cuda_stream
+
+    def fn():
+        C.check(lib.spmd_dot(da, db, do, ctypes.byref(dd), 1, st), "dot")
+    ms = timeit(fn)
+    k = 1
+    for d in lc:
+        k *= lshape[d]
+    flops = 2.0 * osh.num_elements * k
+    print(json.dumps({"kernel": "gemm_bf16_tcgen05", "case": name, "ms": ms,
+                      "tflops": flops / ms / 1e9}), flush=True)
+
+
+def gemms():
+    B, S, M, N, D, H = 16, 1024, 8192, 128, 256, 65536
+    dot_case("qkv x[B,S,M].w[M,N,D]", (B, S, M), (M, N, D), (), (), (2,), (0,))
+    dot_case("logits q.k", (B, S, N, D), (B, S, N, D), (0, 2), (0, 2), (3,), (3,))
+    dot_case("ctx p.v", (B, N, S, S), (B, S, N, D), (0, 1), (0, 2), (3,), (1,))
+    dot_case("out ctx_t.wo", (B, S, N, D), (N, D, M), (), (), (2, 3), (0, 1))
+    dot_case("ffn_in res.wi", (B, S, M), (M, H), (), (), (2,), (0,))
+    dot_case("ffn_out act.wt", (B, S, H), (H, M), (), (), (2,), (0,))
+    dot_case("square 8192", (8192, 8192), (8192, 8192), (), (), (1,), (0,))
+
+
+def softmax():
+    lib = C.lib()
+    shp = Shape((16, 128, 1024, 1024), DType.BF16)
+    x = torch.randn((1,) + shp.dims, device="cuda", dtype=torch.bfloat16)
+    y = torch.empty_like(x)
+    st = torch.cuda.current_stream().cuda_stream
+    dx, dy = desc(x, shp), desc(y, shp)
+    ms = timeit(lambda: C.check(lib.spmd_softmax_lastdim(dx, dy, 1, st), "softmax"))
+    ref = torch.softmax(x[0, 0, 0].float(), -1)
+    err = (y[0, 0, 0].float() - ref).abs().max().item()
+    print(json.dumps({"kernel": "softmax_rows_bf16_vec", "ms": ms,
+                      "gbs": 2 * x.numel() * 2 / ms / 1e6, "max_err": err}), flush=True)
+
+
+if __name__ == "__main__":
+    what = sys.argv[1] if len(sys.argv) > 1 else "all"
+    if what in ("softmax", "all"):
+        softmax()
+    if what in ("gemm", "all"):
+        gemms()
