@@ -335,6 +335,244 @@ __global__ void __launch_bounds__(256, 1)
 }
 
 // ---------------------------------------------------------------------------
+// 2-CTA variant (cta_group::2): a CTA pair computes a 256 x 256 tile with
+// UMMA M=256.  Each CTA stages its 128-row half of A and its 128-row half
+// of B (N split) in its own smem; the leader CTA issues the MMAs, which read
+// both CTAs' smem and write each CTA's own TMEM half.  Per-SM smem operand
+// traffic halves versus the 1-CTA kernel -- the condition for feeding the
+// tensor cores at full rate.
+//   * TMA: .cta_group::2 loads complete on the LEADER's full barrier (peer
+//     bit masked); the leader arms it with both CTAs' bytes.
+//   * MMA commit multicasts to both CTAs' empty / tmem-full barriers.
+//   * Epilogue warps of both CTAs release the leader's tmem-empty barrier
+//     with remote (mapa) arrives.
+// ---------------------------------------------------------------------------
+constexpr uint32_t PEER_MASK = 0xFEFFFFFFu;
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::
+                   : "memory");
+}
+
+__device__ __forceinline__ void tma_load_5d_2sm(void* dst, const CUtensorMap* map, uint64_t* bar,
+                                                int c0, int c1, int c2, int c3, int c4) {
+  asm volatile(
+      "cp.async.bulk.tensor.5d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6, %7}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar) & PEER_MASK), "r"(c0), "r"(c1),
+      "r"(c2), "r"(c3), "r"(c4)
+      : "memory");
+}
+
+__device__ __forceinline__ void tc_commit_2sm_mc(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], %1;" ::"r"(smem_u32(bar)),
+      "h"((uint16_t)3)
+      : "memory");
+}
+
+__device__ __forceinline__ void tc_mma_2sm(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc,
+                                           uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate));
+}
+
+__device__ __forceinline__ void mbar_arrive_leader(uint64_t* bar) {
+  asm volatile(
+      "{\n.reg .b32 ra;\n"
+      "mapa.shared::cluster.u32 ra, %0, 0;\n"
+      "mbarrier.arrive.shared::cluster.b64 _, [ra];\n}" ::"r"(smem_u32(bar))
+      : "memory");
+}
+
+constexpr int BM2 = 256, BN2 = 256, HALF = 128;
+
+template <int STAGES>
+struct Smem2 {
+  static constexpr int A_BYTES = HALF * BK * 2;
+  static constexpr int B_BYTES = HALF * BK * 2;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int BAR_OFF = STAGES * STAGE_BYTES;
+  static constexpr int TOTAL = BAR_OFF + 256 + 1024;
+};
+
+template <int STAGES>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
+    gemm_bf16_tcgen05_2sm(const __grid_constant__ CUtensorMap map_a,
+                          const __grid_constant__ CUtensorMap map_b, bf16* __restrict__ out,
+                          GemmShape g) {
+  typedef Smem2<STAGES> L;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint64_t* full = (uint64_t*)(smem + L::BAR_OFF);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_rank();
+  const bool leader = rank == 0;
+  const int64_t cluster = blockIdx.x >> 1, nclusters = gridDim.x >> 1;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 8);   // 4 epilogue warps x 2 CTAs
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                     smem_u32(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const int kblocks = (g.K + BK - 1) / BK;
+
+  if (warp == 0 && lane == 0) {
+    // ---------------- TMA producer (both CTAs) ----------------
+    int s = 0;
+    uint32_t ph = 0;
+    for (int64_t t = cluster; t < g.tiles; t += nclusters) {
+      int b, m, n;
+      tile_coords(g, t, b, m, n);
+      const int b0 = b % g.nb[0], b1 = (b / g.nb[0]) % g.nb[1], b2 = b / (g.nb[0] * g.nb[1]);
+      const int mrow = m * BM2 + rank * HALF, nrow = n * BN2 + rank * HALF;
+      for (int kb = 0; kb < kblocks; ++kb) {
+        mbar_wait(&empty[s], ph ^ 1);
+        uint8_t* sa = smem + s * L::STAGE_BYTES;
+        uint8_t* sb = sa + L::A_BYTES;
+        if (leader) mbar_expect_tx(&full[s], 2 * L::STAGE_BYTES);
+        const int k0 = kb * BK;
+        if (!g.a_mn) {
+          tma_load_5d_2sm(sa, &map_a, &full[s], k0, mrow, b0, b1, b2);
+        } else {
+#pragma unroll
+          for (int c = 0; c < HALF / 64; ++c)
+            tma_load_5d_2sm(sa + c * (BK * 128), &map_a, &full[s], mrow + c * 64, k0, b0, b1, b2);
+        }
+        if (!g.b_mn) {
+          tma_load_5d_2sm(sb, &map_b, &full[s], k0, nrow, b0, b1, b2);
+        } else {
+#pragma unroll
+          for (int c = 0; c < HALF / 64; ++c)
+            tma_load_5d_2sm(sb + c * (BK * 128), &map_b, &full[s], nrow + c * 64, k0, b0, b1, b2);
+        }
+        if (++s == STAGES) {
+          s = 0;
+          ph ^= 1;
+        }
+      }
+    }
+  } else if (warp == 1 && lane == 0 && leader) {
+    // ---------------- MMA issuer (leader CTA only) ----------------
+    const uint32_t idesc = make_idesc(BM2, BN2, g.a_mn, g.b_mn);
+    int s = 0;
+    uint32_t ph = 0;
+    int acc = 0;
+    uint32_t acc_ph = 0;
+    for (int64_t t = cluster; t < g.tiles; t += nclusters) {
+      mbar_wait(&tempty[acc], acc_ph ^ 1);
+      tc_fence_after();
+      const uint32_t d_tmem = tmem + acc * BN2;
+      for (int kb = 0; kb < kblocks; ++kb) {
+        mbar_wait(&full[s], ph);
+        tc_fence_after();
+        const uint32_t sa = smem_u32(smem + s * L::STAGE_BYTES);
+        const uint32_t sb = sa + L::A_BYTES;
+#pragma unroll
+        for (int k = 0; k < BK / 16; ++k) {
+          const uint64_t ad = g.a_mn ? make_desc(sa + k * 2048, BK * 128, 1024)
+                                     : make_desc(sa + k * 32, 16, 1024);
+          const uint64_t bd = g.b_mn ? make_desc(sb + k * 2048, BK * 128, 1024)
+                                     : make_desc(sb + k * 32, 16, 1024);
+          tc_mma_2sm(d_tmem, ad, bd, idesc, (kb | k) != 0);
+        }
+        tc_commit_2sm_mc(&empty[s]);
+        if (++s == STAGES) {
+          s = 0;
+          ph ^= 1;
+        }
+      }
+      tc_commit_2sm_mc(&tfull[acc]);
+      if (++acc == 2) {
+        acc = 0;
+        acc_ph ^= 1;
+      }
+    }
+  } else if (warp >= EPI_WARP0) {
+    // ---------------- epilogue (both CTAs, own TMEM half) ----------------
+    const int ew = warp - EPI_WARP0;
+    int acc = 0;
+    uint32_t acc_ph = 0;
+    for (int64_t t = cluster; t < g.tiles; t += nclusters) {
+      int b, m, n;
+      tile_coords(g, t, b, m, n);
+      mbar_wait(&tfull[acc], acc_ph);
+      tc_fence_after();
+      const int row = m * BM2 + rank * HALF + ew * 32 + lane;
+      bf16* orow = out + (int64_t)b * g.out_batch_stride + (int64_t)row * g.N;
+#pragma unroll 1
+      for (int c0 = 0; c0 < BN2; c0 += 32) {
+        uint32_t r[32];
+        tmem_ld32(tmem + ((uint32_t)(ew * 32) << 16) + acc * BN2 + c0, r);
+        const int col = n * BN2 + c0;
+        if (row < g.M && col < g.N) {
+          __align__(16) bf16 v[32];
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            float f = __uint_as_float(r[j]);
+            if (g.relu) f = f > 0.f ? f : 0.f;
+            v[j] = __float2bfloat16_rn(f);
+          }
+          if (col + 32 <= g.N && (g.N & 7) == 0) {
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+              *reinterpret_cast<uint4*>(orow + col + 8 * j) = reinterpret_cast<uint4*>(v)[j];
+          } else {
+            for (int j = 0; j < 32 && col + j < g.N; ++j) orow[col + j] = v[j];
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_leader(&tempty[acc]);
+      if (++acc == 2) {
+        acc = 0;
+        acc_ph ^= 1;
+      }
+    }
+  }
+  tc_fence_before();
+  cluster_sync();
+  if (warp == 2) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+  }
+}
+
+// ---------------------------------------------------------------------------
 // host side: operand views -> tensor maps
 // ---------------------------------------------------------------------------
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
@@ -427,6 +665,37 @@ static int launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, bf16* out, 
   return launched(s);
 }
 
+template <int STAGES>
+static int launch_gemm_2sm(const CUtensorMap& ma, const CUtensorMap& mb, bf16* out, GemmShape g,
+                           cudaStream_t s) {
+  typedef Smem2<STAGES> L;
+  static bool configured = false;
+  if (!configured) {
+    SPMD_CUDA_TRY(cudaFuncSetAttribute(gemm_bf16_tcgen05_2sm<STAGES>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, L::TOTAL));
+    configured = true;
+  }
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  int64_t clusters = g.tiles < sms / 2 ? g.tiles : sms / 2;
+  gemm_bf16_tcgen05_2sm<STAGES><<<(unsigned)(2 * clusters), 256, L::TOTAL, s>>>(ma, mb, out, g);
+  return launched(s);
+}
+
+static int gemm_mode() {
+  static int mode = -1;
+  if (mode < 0) {
+    const char* e = getenv("SPMD_GEMM_MODE");
+    mode = (e && strcmp(e, "1sm") == 0) ? 1 : 2;
+  }
+  return mode;
+}
+
 int dot_tcgen05(const spmd_tensor& lhs, const spmd_tensor& rhs, const spmd_tensor& out,
                 const spmd_dot_dims& dd, int64_t nparts, cudaStream_t s) {
   if (lhs.dtype != SPMD_BF16) return SPMD_ERR_UNSUPPORTED;
@@ -514,8 +783,19 @@ int dot_tcgen05(const spmd_tensor& lhs, const spmd_tensor& rhs, const spmd_tenso
   } else {
     vb.size[0] = N.size, vb.stride[0] = 1, vb.size[1] = K2.size, vb.stride[1] = K2.st;
   }
-  const int BNsel = N.size >= 256 ? 256 : 128;
+  g.out_batch_stride = (int64_t)g.M * g.N;
   CUtensorMap ma, mb;
+  if (gemm_mode() == 2 && M.size >= 256 && N.size >= 256) {
+    // 2-CTA path: per-CTA boxes are 128 rows of A and 128 rows of B.
+    bool ok2 = a_mn ? encode(&ma, lhs.data, va, 64, BK) : encode(&ma, lhs.data, va, BK, HALF);
+    ok2 = ok2 && (b_mn ? encode(&mb, rhs.data, vb, 64, BK) : encode(&mb, rhs.data, vb, BK, HALF));
+    if (!ok2) return SPMD_ERR_UNSUPPORTED;
+    g.mt = (g.M + BM2 - 1) / BM2;
+    g.nt = (g.N + BN2 - 1) / BN2;
+    g.tiles = (int64_t)g.mt * g.nt * g.nb[0] * g.nb[1] * g.nb[2];
+    return launch_gemm_2sm<6>(ma, mb, (bf16*)out.data, g, s);
+  }
+  const int BNsel = N.size >= 256 ? 256 : 128;
   bool ok = a_mn ? encode(&ma, lhs.data, va, 64, BK) : encode(&ma, lhs.data, va, BK, BM);
   ok = ok && (b_mn ? encode(&mb, rhs.data, vb, 64, BK) : encode(&mb, rhs.data, vb, BK, BNsel));
   if (!ok) return SPMD_ERR_UNSUPPORTED;
