@@ -142,6 +142,8 @@ class _Step:
     ins: Instruction
     fn: object              # callable(env, stream) -> tensor
     frees: tuple = ()
+    ops: tuple = ()         # value ids read
+    coll: bool = False      # runs on the comm stream when overlapping
 
 
 class Executor:
@@ -149,9 +151,12 @@ class Executor:
 
     def __init__(self, program, nparts: Optional[int] = None, device=None,
                  comm: Optional[NcclComm] = None, partition_base: int = 0,
-                 fuse: bool = False):
+                 fuse: bool = False, overlap: Optional[bool] = None):
         torch = _torch()
         self.lib = C.lib()
+        # Collectives on a dedicated stream, hoisted to issue as soon as
+        # their operands exist (weight all-gathers prefetch under GEMMs).
+        self.overlap = (comm is not None) if overlap is None else overlap
         self.program = program
         self.graph: Graph = program.graph
         self.P = int(nparts if nparts is not None else program.num_partitions)
@@ -168,6 +173,10 @@ class Executor:
         if fuse:
             self._plan_fusions()
         self.steps = self._compile()
+        self.comm_stream = None
+        if self.overlap:
+            self.steps = self._hoist_collectives(self.steps)
+            self.comm_stream = torch.cuda.Stream(device=self.device)
         if comm is not None:
             comm.ensure_workspace(self._workspace_bytes(), self.device)
 
@@ -274,10 +283,45 @@ class Executor:
         steps = []
         for k, ins in enumerate(instrs):
             fn = self._make_step(ins)
-            frees = tuple(o for o in set(self._operands_of(ins))
-                          if last_use.get(o) == k and o not in keep)
-            steps.append(_Step(ins, fn, frees))
+            ops = tuple(self._operands_of(ins))
+            frees = tuple(o for o in set(ops) if last_use.get(o) == k and o not in keep)
+            steps.append(_Step(ins, fn, frees, ops, ins.opcode in COLLECTIVES))
         return steps
+
+    def _hoist_collectives(self, steps: list) -> list:
+        """Issue order with every collective moved up to right after its last
+        operand producer (per-stream order is issue order, so this is what
+        lets weight all-gathers run under earlier GEMMs)."""
+        pending = [s for s in steps if s.coll]
+        order, issued = [], set()
+
+        def flush():
+            progress = True
+            while progress:
+                progress = False
+                for s in list(pending):
+                    if all(o in issued for o in s.ops):
+                        order.append(s)
+                        issued.add(s.ins.id)
+                        pending.remove(s)
+                        progress = True
+
+        flush()
+        for s in steps:
+            if s.coll:
+                continue
+            order.append(s)
+            issued.add(s.ins.id)
+            flush()
+        order += pending
+        last_use = {}
+        for k, s in enumerate(order):
+            for o in s.ops:
+                last_use[o] = k
+        keep = set(self.graph.outputs)
+        for k, s in enumerate(order):
+            s.frees = tuple(o for o in set(s.ops) if last_use.get(o) == k and o not in keep)
+        return order
 
     def _operands_of(self, ins: Instruction):
         f = self._fused.get(ins.id)
@@ -614,13 +658,76 @@ class Executor:
             raise EvalError(f"expected {len(self.params)} inputs, got {len(inputs)}")
         env = {"__inputs__": list(inputs)}
         keep = keep or set()
+        if self.comm_stream is None:
+            for step in self.steps:
+                env[step.ins.id] = step.fn(env, s)
+                for vid in step.frees:
+                    if vid not in keep:
+                        env.pop(vid, None)
+        else:
+            self._run_two_streams(env, keep)
+        self.last_env = env if keep else None
+        return [env[o] for o in self.graph.outputs]
+
+    def _run_two_streams(self, env: dict, keep: set) -> None:
+        """Compute on the current stream, collectives on ``comm_stream``;
+        cross-stream values are ordered with events, and tensors touched by
+        the comm stream are recorded on it so the caching allocator never
+        recycles them early."""
+        torch = _torch()
+        compute = torch.cuda.current_stream(self.device)
+        comm = self.comm_stream
+        comm.wait_stream(compute)                 # inputs / fork for graph capture
+        cs, ks = compute.cuda_stream, comm.cuda_stream
+        on_comm: dict[str, bool] = {}
+        events: dict[str, object] = {}
         for step in self.steps:
-            env[step.ins.id] = step.fn(env, s)
+            mine = step.coll
+            stream = comm if mine else compute
+            for o in step.ops:
+                if on_comm.get(o, False) != mine:
+                    ev = events.get(o)
+                    if ev is None:
+                        # producer was the other stream; record a marker now
+                        # (the producer already issued everything it needs)
+                        ev = torch.cuda.Event()
+                        ev.record(compute if mine else comm)
+                        events[o] = ev
+                    stream.wait_event(ev)
+            out = step.fn(env, ks if mine else cs)
+            env[step.ins.id] = out
+            on_comm[step.ins.id] = mine
+            if mine:
+                for o in step.ops:
+                    t = env.get(o)
+                    if t is not None and hasattr(t, "record_stream"):
+                        t.record_stream(comm)
+                out.record_stream(comm)
+                ev = torch.cuda.Event()
+                ev.record(comm)
+                events[step.ins.id] = ev
             for vid in step.frees:
                 if vid not in keep:
                     env.pop(vid, None)
-        self.last_env = env if keep else None
-        return [env[o] for o in self.graph.outputs]
+        compute.wait_stream(comm)                 # join
+
+    def capture(self, inputs):
+        """Capture one execution into a CUDA graph (after an eager warm-up
+        run that materialises constants, communicators and kernel attributes).
+        Returns ``(graph, outputs)``; ``graph.replay()`` re-runs the step on the
+        same static input/output buffers."""
+        torch = _torch()
+        self.run(inputs)
+        torch.cuda.synchronize(self.device)
+        g = torch.cuda.CUDAGraph()
+        cap = torch.cuda.Stream(device=self.device)
+        cap.wait_stream(torch.cuda.current_stream(self.device))
+        n0 = self.lib.spmd_launch_count()
+        with torch.cuda.graph(g, stream=cap):
+            outs = self.run(inputs)
+        self.launches_per_replay = self.lib.spmd_launch_count() - n0
+        torch.cuda.synchronize(self.device)
+        return g, outs
 
     def check_errors(self, stream=None) -> None:
         torch = _torch()
