@@ -1,0 +1,4 @@
+cd $GRAFT_REPO_ROOT
+T="timeout 600 torchrun --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1"
+$T --master-port 29521 scripts/multi_gpu_check.py > gpurun_out/multi4.log 2>&1; echo multi=$?
+$T --master-port 29522 bench.py --gpus 4 --steps 5 --warmup 3 > gpurun_out/bench_n4.log 2>&1; echo b4=$?
