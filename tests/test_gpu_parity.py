@@ -78,6 +78,36 @@ def test_verify_equivalence_named(name, plan, fuse):
         assert rep.collective_counts == case["verify"]["counts"]
 
 
+@pytest.mark.parametrize("kind,name", CASES)
+def test_fast_plan_two_streams_on_b200(kind, name):
+    """Fast plan + fusions + comm-stream overlap (loopback collectives on a
+    second stream, CUDA-graph captured) against the reference's outputs."""
+    import torch
+    from paper_2105_04663_b200 import partition, propagate
+    from paper_2105_04663_b200.executor import Executor, download_stacked, upload_stacked
+    from paper_2105_04663_b200.sharding import assemble_data, shard_data
+    case = _case(kind, name)
+    g = G.graph(case)
+    ann, _ = propagate(g)
+    n = case["num_devices"]
+    prog = partition(ann, n, plan="fast")
+    dev = torch.device("cuda", 0)
+    stacked = []
+    for p_src, x, p in zip(ann.parameters, G.inputs(case), prog.graph.parameters):
+        sh = shard_data(x, p_src.sharding, devices=range(n))
+        stacked.append(upload_stacked([sh[d] for d in range(n)], p.shape, dev))
+    ex = Executor(prog, nparts=n, device=dev, fuse=True, overlap=True)
+    graph, outs = ex.capture(stacked)
+    graph.replay()
+    torch.cuda.synchronize()
+    for i, oid in enumerate(g.outputs):
+        shape = g.instr(oid).shape
+        per = download_stacked(outs[i], prog.graph.instr(prog.graph.outputs[i]).shape)
+        full = assemble_data({d: per[d] for d in range(n)}, prog.output_shardings[i], shape,
+                             rtol=1e-5)
+        _close(full, G.expected(case)[i], shape.dtype.is_float, tol=1e-4)
+
+
 def test_single_device_matches_reference_oracle():
     from paper_2105_04663_b200 import evaluate_single
     for c in G.cases("named"):
