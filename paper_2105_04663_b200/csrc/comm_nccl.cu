@@ -66,7 +66,10 @@ static int subcomm(spmd_comm* c, const int32_t* groups, int ngroups, int gsize, 
     set_error("subgroups do not partition the ranks");
     return SPMD_ERR_SUBGROUP;
   }
-  std::vector<int32_t> key(groups, groups + ngroups * gsize);
+  // Key = (group size, flattened groups): ((0,2),(1,3)) and ((0,2,1,3),)
+  // flatten identically but are different partitions.
+  std::vector<int32_t> key(1, gsize);
+  key.insert(key.end(), groups, groups + ngroups * gsize);
   int color = -1, k = -1;
   std::vector<int> seen(c->nranks, 0);
   for (int i = 0; i < ngroups * gsize; ++i) {
