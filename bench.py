@@ -351,6 +351,48 @@ def main():
     achieved = dot_flops(top) / (kms * 1e-3) / 1e12
     gemm_share = None
 
+    # ---- reshard GB/s (config C5: [n0, D] f32 dim-0 -> dim-1 / -> replicated) ----
+    reshard = None
+    if world > 1:
+        from paper_2105_04663_b200.workloads import uneven
+        reshard = {}
+        D1 = 65536 * 8
+        for n0, kind in ((1000, "a2a"), (1001, "a2a"), (1001, "repl")):
+            gg, _ = uneven(n0=n0, n1=D1, kind=kind, parts=world, dtype=DType.F32,
+                           with_inputs=False)
+            ga, _ = propagate(gg)
+            rp = partition(ga, world, plan="fast")
+            rex = Executor(rp, nparts=1, device=dev, comm=comm, partition_base=rank,
+                           overlap=False)
+            rin = [torch.randn((1,) + rp.graph.parameters[0].shape.dims, device=dev)]
+            coll = next(s for s in rex.steps if s.coll)
+            keep = set(coll.ops)
+            rex.run(rin, keep=keep)
+            renv = {"__inputs__": rin}
+            renv.update({k: v for k, v in rex.last_env.items() if k in keep})
+            for _ in range(3):
+                coll.fn(renv, stream.cuda_stream)
+            torch.cuda.synchronize()
+            barrier()
+            r0, r1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            r0.record(stream)
+            for _ in range(10):
+                coll.fn(renv, stream.cuda_stream)
+            r1.record(stream)
+            torch.cuda.synchronize()
+            rms = torch.tensor([r0.elapsed_time(r1) / 10], device=dev, dtype=torch.float64)
+            dist.all_reduce(rms, op=dist.ReduceOp.MAX)
+            rms = float(rms.item())
+            src = rp.graph.instr(coll.ins.operands[0]).shape
+            if coll.ins.opcode == Op.ALL_GATHER:
+                bus = coll.ins.shape.nbytes * (world - 1) / world
+            else:
+                bus = src.nbytes * (world - 1) / world
+            reshard[f"{kind}_{n0}x{D1}_f32"] = {
+                "collective": coll.ins.opcode.value, "ms": rms,
+                "bus_gbs_per_gpu": bus / (rms * 1e-3) / 1e9,
+                "frac_of_nvlink_770": bus / (rms * 1e-3) / 1e9 / 770.0}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         v, tcpu, cores, sample = _cpu_baseline(mesh)
@@ -378,6 +420,7 @@ def main():
                          "frac": achieved / burst, "peak_source": peak_src + " burst",
                          "traffic": None, "ms_per_launch": kms,
                          "flops_per_launch": dot_flops(top)},
+            "reshard": reshard,
             "e2e": e2e, "gpu_launches": int(launches), "clocks": clocks,
             "cpu_baseline": cpu,
         }

@@ -150,6 +150,23 @@ int spmd_convolution(spmd_tensor lhs, spmd_tensor rhs, spmd_tensor out,
 /* Row softmax over the last dim: out = exp(x - max) / sum(exp(x - max)). */
 int spmd_softmax_lastdim(spmd_tensor in, spmd_tensor out, int64_t nparts, void* stream);
 
+/* ---- GShard MoE routing + dispatch/combine permutations (config C3) ---------
+ * The reference consumes a given one-hot dispatch tensor through a dense Dot
+ * (tests/test_acceptance.py:326-349); these kernels produce it (route), and
+ * replace the one-hot Dots by exact gathers (dispatch/combine). */
+/* logits [B,S,E] f32/bf16 -> expert, slot s32 [B,S] and gate f32 [B,S] */
+int spmd_moe_route(spmd_tensor logits, int capacity, spmd_tensor expert, spmd_tensor slot,
+                   spmd_tensor gate, int64_t nparts, void* stream);
+/* x [B,S,M] bf16 -> expert buffers [B,E,C,M] (== Dot(dispatch_onehot, x)) */
+int spmd_moe_dispatch(spmd_tensor x, spmd_tensor expert, spmd_tensor slot, spmd_tensor out,
+                      int64_t nparts, void* stream);
+/* y [B,E,C,M] bf16 -> out [B,S,M] (== Dot(combine_weights, y)) */
+int spmd_moe_combine(spmd_tensor y, spmd_tensor expert, spmd_tensor slot, spmd_tensor gate,
+                     spmd_tensor out, int64_t nparts, void* stream);
+/* dense dispatch / combine masks [B,S,E,C] from a routing */
+int spmd_moe_masks(spmd_tensor expert, spmd_tensor slot, spmd_tensor gate,
+                   spmd_tensor dispatch, spmd_tensor combine, int64_t nparts, void* stream);
+
 /* ---- loopback collectives: all partitions resident on this GPU ---------------
  * (simulator.py:333-390 semantics; groups is a flat [ngroups*gsize] table in
  * group order; reductions fold serially in group order, so integer and float

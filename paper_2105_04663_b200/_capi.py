@@ -83,6 +83,10 @@ _SIGNATURES = {
     "spmd_convolution": ([_T, _T, _T, ctypes.POINTER(SpmdConvDims), _I64, _P], _I),
     "spmd_softmax_lastdim": ([_T, _T, _I64, _P], _I),
     "spmd_gemm_bf16": ([_P, _P, _P, _I64, _I64, _I64, _I, _P], _I),
+    "spmd_moe_route": ([_T, _I, _T, _T, _T, _I64, _P], _I),
+    "spmd_moe_dispatch": ([_T, _T, _T, _T, _I64, _P], _I),
+    "spmd_moe_combine": ([_T, _T, _T, _T, _T, _I64, _P], _I),
+    "spmd_moe_masks": ([_T, _T, _T, _T, _T, _I64, _P], _I),
     "spmd_local_all_gather": ([_T, _T, _I, _PI32, _I, _I, _I64, _P], _I),
     "spmd_local_all_reduce": ([_T, _T, _I, _PI32, _I, _I, _I64, _P], _I),
     "spmd_local_reduce_scatter": ([_T, _T, _I, _I, _PI32, _I, _I, _I64, _P], _I),

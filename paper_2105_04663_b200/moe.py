@@ -15,11 +15,12 @@ from __future__ import annotations
 import numpy as np
 
 
-def route_top1(logits: np.ndarray, capacity: int):
-    """logits [B, S, E] -> (dispatch, combine) one-hot masks [B, S, E, C].
-
-    combine carries the softmax gate probability of the chosen expert."""
+def route_assign(logits: np.ndarray):
+    """logits [B, S, E] -> (expert [B,S] int32, slot [B,S] int32, gate [B,S]
+    float32): first-max argmax, exclusive per-(row, expert) prefix count,
+    softmax probability of the chosen expert."""
     B, S, E = logits.shape
+    logits = np.asarray(logits, np.float32)
     z = logits - logits.max(-1, keepdims=True)
     p = np.exp(z)
     p /= p.sum(-1, keepdims=True)
@@ -27,6 +28,19 @@ def route_top1(logits: np.ndarray, capacity: int):
     onehot = np.eye(E, dtype=np.int64)[expert]                 # [B, S, E]
     pos = np.cumsum(onehot, axis=1) - onehot                   # exclusive scan over S
     slot = (pos * onehot).sum(-1)                              # [B, S]
+    gate = np.take_along_axis(p, expert[..., None], -1)[..., 0].astype(np.float32)
+    return expert.astype(np.int32), slot.astype(np.int32), gate
+
+
+def route_top1(logits: np.ndarray, capacity: int):
+    """logits [B, S, E] -> (dispatch, combine) one-hot masks [B, S, E, C].
+
+    combine carries the softmax gate probability of the chosen expert."""
+    B, S, E = logits.shape
+    expert, slot, _ = route_assign(logits)
+    z = logits - logits.max(-1, keepdims=True)
+    p = np.exp(z)
+    p /= p.sum(-1, keepdims=True)
     keep = slot < capacity
     dispatch = np.zeros((B, S, E, capacity), np.float32)
     bi, si = np.nonzero(keep)
