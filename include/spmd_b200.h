@@ -142,6 +142,7 @@ typedef struct {
   int32_t lhs_spatial[SPMD_MAX_RANK], rhs_spatial[SPMD_MAX_RANK], out_spatial[SPMD_MAX_RANK];
   int32_t size[SPMD_MAX_RANK], stride[SPMD_MAX_RANK], pad_low[SPMD_MAX_RANK],
           pad_high[SPMD_MAX_RANK], base_dilation[SPMD_MAX_RANK], window_dilation[SPMD_MAX_RANK];
+  int32_t epilogue;      /* 0 none, 1 relu (fused; executor-level fusion) */
 } spmd_conv_dims;
 int spmd_convolution(spmd_tensor lhs, spmd_tensor rhs, spmd_tensor out,
                      const spmd_conv_dims* cd, int64_t nparts, void* stream);

@@ -45,7 +45,7 @@ class SpmdConvDims(ctypes.Structure):
                 ("n_spatial", ctypes.c_int32)] + \
         [(n, ctypes.c_int32 * MAX_RANK) for n in (
             "lhs_spatial", "rhs_spatial", "out_spatial", "size", "stride", "pad_low",
-            "pad_high", "base_dilation", "window_dilation")]
+            "pad_high", "base_dilation", "window_dilation")] + [("epilogue", ctypes.c_int32)]
 
 
 _T = SpmdTensor

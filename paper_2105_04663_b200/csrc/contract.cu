@@ -150,6 +150,7 @@ struct ConvArgs {
   int64_t o_st_b, o_st_c, o_st_sp[SPMD_MAX_RANK];
   int64_t stride[SPMD_MAX_RANK], pad_lo[SPMD_MAX_RANK], bd[SPMD_MAX_RANK], wd[SPMD_MAX_RANK];
   int64_t lhs_part, rhs_part, out_part, nout;
+  int relu;
 };
 
 template <typename T>
@@ -192,6 +193,7 @@ __global__ void conv_direct_kernel(const T* __restrict__ lhs, const T* __restric
     }
     int64_t ooff = p * a.out_part + b * a.o_st_b + o * a.o_st_c;
     for (int i = 0; i < a.nsp; ++i) ooff += osp[i] * a.o_st_sp[i];
+    if (a.relu && acc < (A)0) acc = 0;
     out[ooff] = from_acc<T, A>(acc);
   }
 }
@@ -329,6 +331,7 @@ extern "C" int spmd_convolution(spmd_tensor lhs, spmd_tensor rhs, spmd_tensor ou
   a.rhs_part = numel(rhs);
   a.out_part = numel(out);
   a.nout = numel(out);
+  a.relu = cd->epilogue == 1;
   int64_t total = a.nout * nparts;
   switch (lhs.dtype) {
     case SPMD_F32:

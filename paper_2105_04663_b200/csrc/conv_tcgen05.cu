@@ -1,12 +1,258 @@
-// Placeholder for the NHWC bf16 implicit-GEMM convolution on tcgen05; until it
-// lands every convolution takes the direct kernel in contract.cu.
-#include "common.cuh"
+// Implicit-GEMM convolution on tcgen05 for NHWC bf16 (config C4), replacing
+// the reference's per-output-position tensordot (simulator.py:121-154).
+//
+// GEMM view: M = output pixels (tiles of 128 consecutive wo in one (n, ho)
+// row), N = Cout, K = (kh, kw, cin) in blocks of 64 channels.  For K-block
+// (kh, kw, c0) the A tile is the input box {64 ch x 128 px} at
+// (c0, wo0 + kw - pad_w, ho + kh - pad_h, n): TMA's out-of-bounds zero fill
+// IS the convolution padding (and the masked halo rows of a spatially
+// partitioned input are already explicit), so no im2col buffer and no
+// boundary code.  B = HWIO weights, MN-major (Cout contiguous).  Same
+// warp-specialised pipeline as the 1-CTA GEMM: TMA producer, single-thread
+// MMA issuer, double-buffered TMEM accumulators, 4 epilogue warps (fused ReLU).
+// Supported: 2 spatial dims, stride 1, no dilation, Cin % 64 == 0,
+// Cout % 64 == 0; anything else returns SPMD_ERR_UNSUPPORTED (direct kernel).
+#include "tcgen05.cuh"
+
+#include <string.h>
 
 namespace spmd {
 
-int conv_tcgen05(const spmd_tensor&, const spmd_tensor&, const spmd_tensor&,
-                 const spmd_conv_dims&, int64_t, cudaStream_t) {
-  return SPMD_ERR_UNSUPPORTED;
+constexpr int CBM = 128, CBK = 64;
+
+struct ConvShape {
+  int N, Ho, Wo, Cin, Cout, KH, KW, pad_h, pad_w;
+  int nwb, nt, cin_blocks, kblocks;
+  int64_t tiles;
+  int relu;
+};
+
+template <int BN, int STAGES>
+struct ConvSmem {
+  static constexpr int A_BYTES = CBM * CBK * 2;
+  static constexpr int B_BYTES = BN * CBK * 2;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int BAR_OFF = STAGES * STAGE_BYTES;
+  static constexpr int TOTAL = BAR_OFF + 256 + 1024;
+};
+
+__device__ __forceinline__ void conv_tile(const ConvShape& g, int64_t t, int& pn, int& ho, int& wb,
+                                          int& ct) {
+  ct = (int)(t % g.nt);
+  t /= g.nt;
+  wb = (int)(t % g.nwb);
+  t /= g.nwb;
+  ho = (int)(t % g.Ho);
+  pn = (int)(t / g.Ho);
+}
+
+template <int BN, int STAGES>
+__global__ void __launch_bounds__(256, 1)
+    conv_bf16_tcgen05(const __grid_constant__ CUtensorMap map_x,
+                      const __grid_constant__ CUtensorMap map_w, bf16* __restrict__ out,
+                      ConvShape g) {
+  typedef ConvSmem<BN, STAGES> L;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint64_t* full = (uint64_t*)(smem + L::BAR_OFF);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 4);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                     smem_u32(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0 && lane == 0) {
+    int s = 0;
+    uint32_t ph = 0;
+    for (int64_t t = blockIdx.x; t < g.tiles; t += gridDim.x) {
+      int pn, ho, wb, ct;
+      conv_tile(g, t, pn, ho, wb, ct);
+      const int n = pn % g.N, p = pn / g.N;
+      for (int kb = 0; kb < g.kblocks; ++kb) {
+        const int tap = kb / g.cin_blocks, cb = kb - tap * g.cin_blocks;
+        const int kh = tap / g.KW, kw = tap - kh * g.KW;
+        mbar_wait(&empty[s], ph ^ 1);
+        uint8_t* sa = smem + s * L::STAGE_BYTES;
+        uint8_t* sb = sa + L::A_BYTES;
+        mbar_expect_tx(&full[s], L::STAGE_BYTES);
+        tma_load_5d(sa, &map_x, &full[s], cb * CBK, wb * CBM + kw - g.pad_w, ho + kh - g.pad_h, n,
+                    p);
+#pragma unroll
+        for (int c = 0; c < BN / 64; ++c)
+          tma_load_5d(sb + c * (CBK * 128), &map_w, &full[s], ct * BN + c * 64, cb * CBK, kw, kh,
+                      p);
+        if (++s == STAGES) {
+          s = 0;
+          ph ^= 1;
+        }
+      }
+    }
+  } else if (warp == 1 && lane == 0) {
+    const uint32_t idesc = make_idesc(CBM, BN, 0, 1);
+    int s = 0;
+    uint32_t ph = 0;
+    int acc = 0;
+    uint32_t acc_ph = 0;
+    for (int64_t t = blockIdx.x; t < g.tiles; t += gridDim.x) {
+      mbar_wait(&tempty[acc], acc_ph ^ 1);
+      tc_fence_after();
+      const uint32_t d_tmem = tmem + acc * BN;
+      for (int kb = 0; kb < g.kblocks; ++kb) {
+        mbar_wait(&full[s], ph);
+        tc_fence_after();
+        const uint32_t sa = smem_u32(smem + s * L::STAGE_BYTES);
+        const uint32_t sb = sa + L::A_BYTES;
+#pragma unroll
+        for (int k = 0; k < CBK / 16; ++k)
+          tc_mma(d_tmem, make_desc(sa + k * 32, 16, 1024), make_desc(sb + k * 2048, CBK * 128, 1024),
+                 idesc, (kb | k) != 0);
+        tc_commit(&empty[s]);
+        if (++s == STAGES) {
+          s = 0;
+          ph ^= 1;
+        }
+      }
+      tc_commit(&tfull[acc]);
+      if (++acc == 2) {
+        acc = 0;
+        acc_ph ^= 1;
+      }
+    }
+  } else if (warp >= 4) {
+    const int ew = warp - 4;
+    int acc = 0;
+    uint32_t acc_ph = 0;
+    for (int64_t t = blockIdx.x; t < g.tiles; t += gridDim.x) {
+      int pn, ho, wb, ct;
+      conv_tile(g, t, pn, ho, wb, ct);
+      mbar_wait(&tfull[acc], acc_ph);
+      tc_fence_after();
+      const int wo = wb * CBM + ew * 32 + lane;
+      bf16* orow = out + (((int64_t)pn * g.Ho + ho) * g.Wo + wo) * g.Cout;
+#pragma unroll 1
+      for (int c0 = 0; c0 < BN; c0 += 32) {
+        uint32_t r[32];
+        tmem_ld32(tmem + ((uint32_t)(ew * 32) << 16) + acc * BN + c0, r);
+        const int col = ct * BN + c0;
+        if (wo < g.Wo && col < g.Cout) {
+          __align__(16) bf16 v[32];
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            float f = __uint_as_float(r[j]);
+            if (g.relu) f = f > 0.f ? f : 0.f;
+            v[j] = __float2bfloat16_rn(f);
+          }
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            *reinterpret_cast<uint4*>(orow + col + 8 * j) = reinterpret_cast<uint4*>(v)[j];
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
+      if (++acc == 2) {
+        acc = 0;
+        acc_ph ^= 1;
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+  }
+}
+
+template <int BN, int STAGES>
+static int launch_conv(const CUtensorMap& mx, const CUtensorMap& mw, bf16* out, ConvShape g,
+                       cudaStream_t s) {
+  typedef ConvSmem<BN, STAGES> L;
+  static bool configured = false;
+  if (!configured) {
+    SPMD_CUDA_TRY(cudaFuncSetAttribute(conv_bf16_tcgen05<BN, STAGES>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, L::TOTAL));
+    configured = true;
+  }
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  int64_t grid = g.tiles < sms ? g.tiles : sms;
+  conv_bf16_tcgen05<BN, STAGES><<<(unsigned)grid, 256, L::TOTAL, s>>>(mx, mw, out, g);
+  return launched(s);
+}
+
+int conv_tcgen05(const spmd_tensor& lhs, const spmd_tensor& rhs, const spmd_tensor& out,
+                 const spmd_conv_dims& cd, int64_t nparts, cudaStream_t s) {
+  if (lhs.dtype != SPMD_BF16 || cd.n_spatial != 2 || lhs.rank != 4) return SPMD_ERR_UNSUPPORTED;
+  // NHWC / HWIO / NHWC only.
+  if (!(cd.lhs_batch == 0 && cd.lhs_spatial[0] == 1 && cd.lhs_spatial[1] == 2 &&
+        cd.lhs_feature == 3 && cd.rhs_spatial[0] == 0 && cd.rhs_spatial[1] == 1 &&
+        cd.rhs_in_feature == 2 && cd.rhs_out_feature == 3 && cd.out_batch == 0 &&
+        cd.out_spatial[0] == 1 && cd.out_spatial[1] == 2 && cd.out_feature == 3))
+    return SPMD_ERR_UNSUPPORTED;
+  for (int i = 0; i < 2; ++i)
+    if (cd.stride[i] != 1 || cd.base_dilation[i] != 1 || cd.window_dilation[i] != 1)
+      return SPMD_ERR_UNSUPPORTED;
+  ConvShape g;
+  memset(&g, 0, sizeof(g));
+  g.N = (int)lhs.dims[0];
+  const int H = (int)lhs.dims[1], W = (int)lhs.dims[2];
+  g.Cin = (int)lhs.dims[3];
+  g.KH = (int)rhs.dims[0];
+  g.KW = (int)rhs.dims[1];
+  g.Cout = (int)rhs.dims[3];
+  g.Ho = (int)out.dims[1];
+  g.Wo = (int)out.dims[2];
+  g.pad_h = cd.pad_low[0];
+  g.pad_w = cd.pad_low[1];
+  if (g.Cin % 64 || g.Cout % 64 || g.Wo < 64) return SPMD_ERR_UNSUPPORTED;
+  const int BN = g.Cout % 256 == 0 ? 256 : 128;
+  if (g.Cout % BN) return SPMD_ERR_UNSUPPORTED;
+  OperandView vx, vw;
+  vx.size[0] = g.Cin, vx.stride[0] = 1;
+  vx.size[1] = W, vx.stride[1] = g.Cin;
+  vx.size[2] = H, vx.stride[2] = (int64_t)W * g.Cin;
+  vx.size[3] = g.N, vx.stride[3] = (int64_t)H * W * g.Cin;
+  vx.size[4] = nparts, vx.stride[4] = numel(lhs);
+  vw.size[0] = g.Cout, vw.stride[0] = 1;
+  vw.size[1] = g.Cin, vw.stride[1] = g.Cout;
+  vw.size[2] = g.KW, vw.stride[2] = (int64_t)g.Cin * g.Cout;
+  vw.size[3] = g.KH, vw.stride[3] = (int64_t)g.KW * g.Cin * g.Cout;
+  vw.size[4] = nparts, vw.stride[4] = numel(rhs);
+  if (nparts == 1) vx.stride[4] = vw.stride[4] = 8;
+  CUtensorMap mx, mw;
+  if (!encode(&mx, lhs.data, vx, CBK, CBM) || !encode(&mw, rhs.data, vw, 64, CBK))
+    return SPMD_ERR_UNSUPPORTED;
+  g.nwb = (g.Wo + CBM - 1) / CBM;
+  g.nt = g.Cout / BN;
+  g.cin_blocks = g.Cin / CBK;
+  g.kblocks = g.KH * g.KW * g.cin_blocks;
+  g.tiles = (int64_t)nparts * g.N * g.Ho * g.nwb * g.nt;
+  g.relu = cd.epilogue == 1;
+  if (BN == 256) return launch_conv<256, 4>(mx, mw, (bf16*)out.data, g, s);
+  return launch_conv<128, 6>(mx, mw, (bf16*)out.data, g, s);
 }
 
 }  // namespace spmd

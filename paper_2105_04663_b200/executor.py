@@ -264,11 +264,12 @@ class Executor:
                 for vid in (ins.id, mxb.id, sub.id, e.id, red.id, denb.id):
                     self._fused_skip.add(vid)
                 self._fused[div.id] = ("softmax", x)
-            # dot -> relu epilogue
-            if ins.opcode == Op.DOT and only_user(ins.id, Op.RELU) and ins.shape.dtype == DType.BF16:
+            # dot / convolution -> relu epilogue
+            if ins.opcode in (Op.DOT, Op.CONVOLUTION) and only_user(ins.id, Op.RELU) \
+                    and ins.shape.dtype == DType.BF16:
                 relu = by[users[ins.id][0]]
                 self._fused_skip.add(ins.id)
-                self._fused[relu.id] = ("dot_relu", ins)
+                self._fused[relu.id] = ("dot_relu" if ins.opcode == Op.DOT else "conv_relu", ins)
 
     # ------------------------------------------------------------------
     # compilation: one closure per instruction
@@ -349,6 +350,8 @@ class Executor:
             return run
         if f is not None and f[0] == "dot_relu":
             return self._dot_step(f[1], shp, epilogue=1)
+        if f is not None and f[0] == "conv_relu":
+            return self._conv_step(f[1], epilogue=1)
 
         if op == Op.PARAMETER:
             idx = [p.id for p in self.params].index(ins.id)
@@ -557,7 +560,7 @@ class Executor:
             return out
         return run
 
-    def _conv_step(self, ins):
+    def _conv_step(self, ins, epilogue=0):
         lib, P = self.lib, self.P
         a, b = ins.operands
         ash, bsh, shp = self._shape(a), self._shape(b), ins.shape
@@ -574,6 +577,7 @@ class Executor:
             c.size[i], c.stride[i] = w.size, w.stride
             c.pad_low[i], c.pad_high[i] = w.padding_low, w.padding_high
             c.base_dilation[i], c.window_dilation[i] = w.base_dilation, w.window_dilation
+        c.epilogue = epilogue
         ref = ctypes.byref(c)
 
         def run(env, s):

@@ -1,0 +1,105 @@
+"""tcgen05 implicit-GEMM convolution (NHWC bf16) vs a plain PyTorch fp32
+reference, and the spatially partitioned C4 conv stack end to end.
+Tolerance 8e-3 normwise per conv (bf16 inputs, fp32 accumulation, one bf16
+rounding); 2e-2 for the 2-layer partitioned stack."""
+
+import ctypes
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _conv(x, w, pads, relu=False, nparts=1):
+    import torch
+    from paper_2105_04663_b200 import _capi as C
+    from paper_2105_04663_b200.executor import desc
+    from paper_2105_04663_b200.ir import DType, Shape
+    P, N, H, W, Ci = x.shape
+    KH, KW, _, Co = w.shape[1:]
+    (pl_h, ph_h), (pl_w, ph_w) = pads
+    Ho, Wo = H + pl_h + ph_h - KH + 1, W + pl_w + ph_w - KW + 1
+    out = torch.empty((P, N, Ho, Wo, Co), dtype=torch.bfloat16, device="cuda")
+    cd = C.SpmdConvDims()
+    cd.lhs_batch, cd.lhs_feature, cd.rhs_in_feature, cd.rhs_out_feature = 0, 3, 2, 3
+    cd.out_batch, cd.out_feature, cd.n_spatial = 0, 3, 2
+    for i, (ls, rs, os_, k, p) in enumerate([(1, 0, 1, KH, (pl_h, ph_h)), (2, 1, 2, KW, (pl_w, ph_w))]):
+        cd.lhs_spatial[i], cd.rhs_spatial[i], cd.out_spatial[i] = ls, rs, os_
+        cd.size[i], cd.stride[i] = k, 1
+        cd.pad_low[i], cd.pad_high[i] = p
+        cd.base_dilation[i] = cd.window_dilation[i] = 1
+    cd.epilogue = int(relu)
+    C.check(C.lib().spmd_convolution(desc(x, Shape((N, H, W, Ci), DType.BF16)),
+                                     desc(w, Shape((KH, KW, Ci, Co), DType.BF16)),
+                                     desc(out, Shape((N, Ho, Wo, Co), DType.BF16)),
+                                     ctypes.byref(cd), P, torch.cuda.current_stream().cuda_stream),
+            "conv")
+    torch.cuda.synchronize()
+    return out
+
+
+def _ref(x, w, pads, relu=False):
+    import torch
+    import torch.nn.functional as F
+    (pl_h, ph_h), (pl_w, ph_w) = pads
+    xi = F.pad(x.float().permute(0, 3, 1, 2), (pl_w, ph_w, pl_h, ph_h))
+    y = F.conv2d(xi, w.float().permute(3, 2, 0, 1)).permute(0, 2, 3, 1)
+    return torch.relu(y) if relu else y
+
+
+def _err(a, b):
+    return (a.float() - b).abs().max().item() / max(1.0, b.abs().max().item())
+
+
+@pytest.mark.parametrize("N,H,W,Ci,Co,pads,relu", [
+    (2, 16, 128, 64, 128, ((1, 1), (1, 1)), False),
+    (1, 9, 200, 128, 128, ((0, 0), (1, 1)), True),      # partitioned layout: H halo explicit
+    (2, 8, 64, 64, 256, ((1, 1), (1, 1)), False),
+    (1, 4, 300, 192, 64, ((2, 0), (0, 2)), True),
+])
+def test_conv_tcgen05(N, H, W, Ci, Co, pads, relu):
+    import torch
+    torch.manual_seed(N * H + Co)
+    x = torch.randn(1, N, H, W, Ci, device="cuda").bfloat16()
+    w = (torch.randn(1, 3, 3, Ci, Co, device="cuda") / (3 * Ci ** 0.5)).bfloat16()
+    out = _conv(x, w, pads, relu)
+    assert _err(out[0], _ref(x[0], w[0], pads, relu)) < 8e-3
+
+
+def test_conv_partition_stacked():
+    import torch
+    torch.manual_seed(3)
+    x = torch.randn(4, 1, 10, 128, 64, device="cuda").bfloat16()
+    w = (torch.randn(4, 3, 3, 64, 128, device="cuda") / 24).bfloat16()
+    out = _conv(x, w, ((0, 0), (1, 1)), nparts=4)
+    for p in range(4):
+        assert _err(out[p], _ref(x[p], w[p], ((0, 0), (1, 1)))) < 8e-3
+
+
+@pytest.mark.parametrize("mesh,mapping", [((4,), (-1, 0, -1, -1)), ((2, 4), (-1, 0, 1, -1))])
+def test_partitioned_conv_stack_bf16(mesh, mapping):
+    """C4 at small dims through propagate -> partition (halo exchange via
+    collective-permute) -> B200 (fast plan, conv+relu fused) vs the oracle."""
+    from oracle import evaluator as O
+    from paper_2105_04663_b200 import partition, propagate
+    from paper_2105_04663_b200.executor import evaluate_spmd
+    from paper_2105_04663_b200.ir import DType
+    from paper_2105_04663_b200.sharding import assemble_data, shard_data
+    from paper_2105_04663_b200.workloads import conv_stack
+    g, ins = conv_stack(mesh, mapping, N=2, H=32, W=256, C=64, layers=2, dtype=DType.BF16)
+    ann, _ = propagate(g)
+    n = int(np.prod(mesh))
+    prog = partition(ann, n, plan="fast")
+    devices = list(range(n))
+    per = {d: [] for d in devices}
+    for p, x in zip(ann.parameters, ins):
+        sh = shard_data(x, p.sharding, devices=devices)
+        for d in devices:
+            per[d].append(sh[d])
+    res = evaluate_spmd(prog, per, fuse=True)
+    out = assemble_data({d: res[d][0] for d in devices}, prog.output_shardings[0],
+                        g.instr(g.outputs[0]).shape, rtol=5e-2)
+    want = O.evaluate_single(g, ins)[0]
+    _, rel = O.rel_error(out, want)
+    assert rel < 2e-2, rel
