@@ -178,8 +178,69 @@ def _rand_like_shard(shape, device, scale, seed):
     return (t * scale).to(torch.bfloat16)
 
 
+C3 = dict(E=8, B=64, S=512, C=160, M=4096, H=16384)
+C4 = dict(N=8, H=1024, W=1024, C=128, layers=4)
+
+
+def _workload(config, world, scale=1.0):
+    """(mesh, graph, dims, flops/step, fan-in per parameter, description)."""
+    from paper_2105_04663_b200.ir import DType
+    from paper_2105_04663_b200.workloads import (conv_stack, moe_layer, transformer_flops,
+                                                 transformer_layer)
+    if config == "c2":
+        mesh = MESHES[world]
+        dims = dict(PAPER)
+        if scale != 1.0:
+            dims["B"] = max(mesh[0], int(dims["B"] * scale))
+        g, _ = transformer_layer(mesh, dtype=DType.BF16, with_inputs=False, **dims)
+        fan = {"wq": dims["M"], "wk": dims["M"], "wv": dims["M"], "wo": dims["N"] * dims["D"],
+               "wi": dims["M"], "wt": dims["H"]}
+        return mesh, g, dims, transformer_flops(**dims), fan, \
+            "C2 transformer layer (attention+FFN), paper dims"
+    if config == "c3":
+        d = dict(C3)
+        g, _ = moe_layer(world, dtype=DType.BF16, with_inputs=False, **d)
+        flops = 4.0 * d["E"] * d["B"] * d["C"] * d["M"] * d["H"]
+        return (world,), g, d, flops, {"wi": d["M"], "wo": d["H"]}, \
+            "C3 GShard MoE FFN (top-1, capacity C=160), expert GEMM FLOPs"
+    if config == "c4":
+        d = dict(C4)
+        g, _ = conv_stack((world,), (-1, 0, -1, -1), dtype=DType.BF16, with_inputs=False, **d)
+        flops = d["layers"] * 2.0 * d["N"] * d["H"] * d["W"] * d["C"] * d["C"] * 9
+        return (world,), g, d, flops, {f"w{i}": 9 * d["C"] for i in range(d["layers"])}, \
+            "C4 spatially partitioned 3x3 conv stack (NHWC, H-sharded, halo via collective-permute)"
+    raise SystemExit(f"unknown config {config}")
+
+
+def _moe_masks(inputs, names, dims, dev, seed):
+    """Replace the dispatch/combine parameters with real top-1 routings of
+    random gating logits (on-device router, then dense masks)."""
+    import torch
+    from paper_2105_04663_b200 import _capi as C
+    from paper_2105_04663_b200.executor import desc
+    from paper_2105_04663_b200.ir import DType, Shape
+    di, ci = names.index("dispatch"), names.index("combine")
+    Bl, S, E, Cap = inputs[di].shape[1:]
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(seed)
+    logits = torch.randn((1, Bl, S, E), generator=gen, device=dev)
+    ex = torch.empty((1, Bl, S), dtype=torch.int32, device=dev)
+    sl = torch.empty_like(ex)
+    gt = torch.empty((1, Bl, S), dtype=torch.float32, device=dev)
+    st = torch.cuda.current_stream(dev).cuda_stream
+    lib = C.lib()
+    C.check(lib.spmd_moe_route(desc(logits, Shape((Bl, S, E), DType.F32)), Cap,
+                               desc(ex, Shape((Bl, S), DType.S32)), desc(sl, Shape((Bl, S), DType.S32)),
+                               desc(gt, Shape((Bl, S), DType.F32)), 1, st), "route")
+    msh = Shape((Bl, S, E, Cap), DType.BF16)
+    C.check(lib.spmd_moe_masks(desc(ex, Shape((Bl, S), DType.S32)), desc(sl, Shape((Bl, S), DType.S32)),
+                               desc(gt, Shape((Bl, S), DType.F32)), desc(inputs[di], msh),
+                               desc(inputs[ci], msh), 1, st), "masks")
+
+
 def main():
     ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="c2", choices=["c2", "c3", "c4"])
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
@@ -210,27 +271,24 @@ def main():
     dev = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
-    mesh = MESHES[world]
-    dims = dict(PAPER)
-    if args.scale != 1.0:
-        dims["B"] = max(mesh[0], int(dims["B"] * args.scale))
-    g, _ = transformer_layer(mesh, dtype=DType.BF16, with_inputs=False, **dims)
+    mesh, g, dims, flops, fan, wdesc = _workload(args.config, world, args.scale)
     ann, _ = propagate(g)
     prog = partition(ann, world, plan="fast")
     comm = NcclComm.from_torch_distributed() if world > 1 else None
     ex = Executor(prog, nparts=1, device=dev, comm=comm, partition_base=rank, fuse=True,
                   overlap=(world > 1 and not args.no_overlap))
-    flops = transformer_flops(**dims)
 
-    # Synthetic local shards, generated on the device (weights ~ N(0, 1/fan_in)).
-    fan = {"x": 1, "wq": dims["M"], "wk": dims["M"], "wv": dims["M"],
-           "wo": dims["N"] * dims["D"], "wi": dims["M"], "wt": dims["H"]}
+    # Synthetic local shards, generated on the device (weights ~ N(0, 1/fan_in);
+    # MoE dispatch/combine masks from the on-device router).
     src_params = {p.attrs["index"]: p.id for p in ann.parameters}
     inputs = []
     for p in prog.graph.parameters:
         name = src_params[p.attrs["index"]]
-        inputs.append(_rand_like_shard(p.shape, dev, 1.0 / np.sqrt(fan[name]),
+        inputs.append(_rand_like_shard(p.shape, dev, 1.0 / np.sqrt(fan.get(name, 1)),
                                        seed=1000 * rank + p.attrs["index"]))
+    if args.config == "c3":
+        names = [src_params[p.attrs["index"]] for p in prog.graph.parameters]
+        _moe_masks(inputs, names, dims, dev, seed=rank)
     stream = torch.cuda.current_stream(dev)
 
     def barrier():
@@ -318,17 +376,22 @@ def main():
 
     # ---- roofline of the dominant kernel: the largest tcgen05 GEMM ----
     burst, sustained, hbm, peak_src = _peaks()
-    dots = [i for i in prog.graph.instructions if i.opcode == Op.DOT]
+    dots = [i for i in prog.graph.instructions if i.opcode in (Op.DOT, Op.CONVOLUTION)]
     from paper_2105_04663_b200.ir import dot_dim_lists
 
     def dot_flops(ins):
         a = prog.graph.instr(ins.operands[0]).shape
         bsh = prog.graph.instr(ins.operands[1]).shape
+        if ins.opcode == Op.CONVOLUTION:
+            cd = ins.attrs["conv_dims"]
+            k = a.dims[cd.lhs_feature] * int(np.prod([bsh.dims[d] for d in cd.rhs_spatial]))
+            return 2.0 * ins.shape.num_elements * k
         lb, rb, lc, rc, lf, rf = dot_dim_lists(ins.attrs, a.rank, bsh.rank)
         k = int(np.prod([a.dims[d] for d in lc]))
         return 2.0 * ins.shape.num_elements * k
 
     top = max(dots, key=dot_flops)
+    kname = "conv_bf16_tcgen05" if top.opcode == Op.CONVOLUTION else "gemm_bf16_tcgen05"
     top_step = next(s for s in ex.steps if s.ins.id == top.id or
                     (ex._fused.get(s.ins.id) or (None, None))[1] is top)
     print(f"[bench] step {ms:.2f} ms  ({value:.1f} TFLOP/s aggregate)", file=sys.stderr)
@@ -353,7 +416,7 @@ def main():
 
     # ---- reshard GB/s (config C5: [n0, D] f32 dim-0 -> dim-1 / -> replicated) ----
     reshard = None
-    if world > 1:
+    if world > 1 and args.config == "c2":
         from paper_2105_04663_b200.workloads import uneven
         reshard = {}
         D1 = 65536 * 8
@@ -394,7 +457,7 @@ def main():
                 "frac_of_nvlink_770": bus / (rms * 1e-3) / 1e9 / 770.0}
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and args.config == "c2":
         v, tcpu, cores, sample = _cpu_baseline(mesh)
         cpu = {"value": v, "unit": "TFLOP/s", "cores": cores, "kind": "port",
                "sample": sample, "seconds_per_sample": tcpu}
@@ -402,20 +465,24 @@ def main():
     stats = collective_stats(prog)
     if rank == 0:
         per_gpu = value / world
+        cfg = {"workload": wdesc, "model_dims": dims, "mesh": list(mesh),
+               "parallelism": ("dp%dxmp%d" % mesh) if args.config == "c2" else
+               ("expert%d" % world if args.config == "c3" else "spatial%d" % world),
+               "plan": "fast", "l2": "inputs larger than L2 (weights+activations)",
+               "collectives_per_step": stats["counts"]}
+        if args.config == "c2":
+            cfg.update(global_batch=dims["B"], seq_len=dims["S"])
         line = {
-            "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world,
+            "metric": METRIC if args.config == "c2" else
+            f"{args.config} throughput (TFLOP/s) at 1/2/4/8 B200",
+            "value": value, "unit": "TFLOP/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-            "dtype": "bf16", "data": "synthetic",
-            "config": {"workload": "C2 transformer layer (attention+FFN), paper dims",
-                       "model_dims": dims, "global_batch": dims["B"], "seq_len": dims["S"],
-                       "mesh": list(mesh), "parallelism": "dp%dxmp%d" % mesh,
-                       "plan": "fast", "l2": "inputs larger than L2 (weights+activations)",
-                       "collectives_per_step": stats["counts"]},
+            "dtype": "bf16", "data": "synthetic", "config": cfg,
             "tflops_per_gpu": per_gpu,
             "mfu": {"vs_spec_2250": per_gpu / SPEC_BF16_TFLOPS,
                     "vs_measured_sustained": per_gpu / sustained},
-            "roofline": {"bound": "tensor", "kernel": "gemm_bf16_tcgen05 (%s)" % top.id,
+            "roofline": {"bound": "tensor", "kernel": "%s (%s)" % (kname, top.id),
                          "achieved": achieved, "peak": burst, "unit": "TFLOP/s",
                          "frac": achieved / burst, "peak_source": peak_src + " burst",
                          "traffic": None, "ms_per_launch": kms,
