@@ -148,6 +148,12 @@ int spmd_convolution(spmd_tensor lhs, spmd_tensor rhs, spmd_tensor out,
                      const spmd_conv_dims* cd, int64_t nparts, void* stream);
 
 /* ---- fused kernels selected by the executor (same semantics as the op chain) */
+/* Uneven-shard / halo range mask (partitioner select_range chain,
+ * reference partitioner.py:205-228): out = (low <= iota_axis + offset[p] < high)
+ * ? in : fill[p]; offset s32 and fill are per-partition scalars. */
+int spmd_mask_range(spmd_tensor in, spmd_tensor offset, spmd_tensor fill, spmd_tensor out,
+                    int axis, int64_t low, int64_t high, int has_low, int64_t nparts,
+                    void* stream);
 /* Row softmax over the last dim: out = exp(x - max) / sum(exp(x - max)). */
 int spmd_softmax_lastdim(spmd_tensor in, spmd_tensor out, int64_t nparts, void* stream);
 

@@ -55,6 +55,24 @@ __global__ void strided_copy_kernel(const T* __restrict__ src, T* __restrict__ d
   }
 }
 
+// dst[dbase + p*dpart + i] = src[sbase + p*spart] for i < n, 16 bytes per store.
+template <typename T>
+__global__ void splat_kernel(const T* __restrict__ src, T* __restrict__ dst, CopyArgs a,
+                             int64_t nparts) {
+  constexpr int V = 16 / sizeof(T);
+  const int64_t per = a.n / V, total = per * nparts;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t p = i / per;
+    const T v = src[a.sbase + p * a.spart];
+    T f[V];
+#pragma unroll
+    for (int j = 0; j < V; ++j) f[j] = v;
+    *reinterpret_cast<uint4*>(dst + a.dbase + p * a.dpart + (i - p * per) * V) =
+        *reinterpret_cast<uint4*>(f);
+  }
+}
+
 template <typename T>
 __global__ void fill_kernel(T* __restrict__ out, const T* __restrict__ value, int64_t n,
                             int64_t nparts) {
@@ -99,8 +117,19 @@ int launch_copy(const void* src, void* dst, int dtype, CopyArgs a, int64_t npart
   // 16-byte vector path: innermost dim unit-stride on both sides, all offsets
   // and strides multiples of the vector width, pointers aligned.
   const int V = 16 / es;
+  // Scalar broadcast (every source stride 0, contiguous destination): splat.
+  if (a.rank == 1 && a.sst[0] == 0 && a.dst[0] == 1 && a.ndyn == 0 && a.n % V == 0 &&
+      (reinterpret_cast<uintptr_t>(dst) & 15) == 0 && a.dbase % V == 0 && a.dpart % V == 0) {
+    const int64_t work = a.n / V * nparts;
+    SPMD_DISPATCH_BYTES(dtype, T,
+                        splat_kernel<T><<<grid_for(work, 256, 2), 256, 0, s>>>(
+                            (const T*)src, (T*)dst, a, nparts));
+    return launched(s);
+  }
+  bool dyn_aligned = true;
+  for (int k = 0; k < a.ndyn; ++k) dyn_aligned = dyn_aligned && a.dyn_mul[k] % V == 0;
   bool vec = a.rank >= 1 && a.sst[a.rank - 1] == 1 && a.dst[a.rank - 1] == 1 &&
-             a.shape[a.rank - 1] % V == 0 && a.ndyn == 0 &&
+             a.shape[a.rank - 1] % V == 0 && dyn_aligned &&
              (reinterpret_cast<uintptr_t>(src) & 15) == 0 &&
              (reinterpret_cast<uintptr_t>(dst) & 15) == 0 && a.sbase % V == 0 &&
              a.dbase % V == 0 && a.spart % V == 0 && a.dpart % V == 0;

@@ -22,11 +22,10 @@ inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 
 // ---------------------------------------------------------------------------
 // sources
 // ---------------------------------------------------------------------------
-template <typename T>
-__global__ void iota_kernel(T* out, int64_t total, int64_t inner, int64_t len) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    int64_t v = (i / inner) % len;
+template <typename T, typename I>
+__global__ void iota_kernel(T* out, I total, I inner, I len) {
+  for (I i = blockIdx.x * (I)blockDim.x + threadIdx.x; i < total; i += (I)gridDim.x * blockDim.x) {
+    I v = (i / inner) % len;
     out[i] = st<T>((typename Compute<T>::type)v);
   }
 }
@@ -216,9 +215,15 @@ extern "C" int spmd_iota(spmd_tensor out, int axis, int64_t nparts, void* stream
   int64_t inner = 1;
   for (int i = axis + 1; i < out.rank; ++i) inner *= out.dims[i];
   cudaStream_t s = as_stream(stream);
-  SPMD_DISPATCH(out.dtype, T,
-                iota_kernel<T><<<grid_for(total, 256, 4), 256, 0, s>>>((T*)out.data, total, inner,
-                                                                      out.dims[axis]));
+  const bool small = total < ((int64_t)1 << 31);
+  SPMD_DISPATCH(out.dtype, T, {
+    if (small)
+      iota_kernel<T, uint32_t><<<grid_for(total, 256, 4), 256, 0, s>>>(
+          (T*)out.data, (uint32_t)total, (uint32_t)inner, (uint32_t)out.dims[axis]);
+    else
+      iota_kernel<T, uint64_t><<<grid_for(total, 256, 4), 256, 0, s>>>(
+          (T*)out.data, (uint64_t)total, (uint64_t)inner, (uint64_t)out.dims[axis]);
+  });
   return launched(s);
 }
 

@@ -264,12 +264,87 @@ class Executor:
                 for vid in (ins.id, mxb.id, sub.id, e.id, red.id, denb.id):
                     self._fused_skip.add(vid)
                 self._fused[div.id] = ("softmax", x)
+            # partitioner select_range chain -> one range-mask kernel
+            if ins.opcode == Op.SELECT and ins.id not in self._fused_skip:
+                m = self._match_range_mask(ins, users, outs)
+                if m is not None:
+                    result, skip, spec = m
+                    self._fused_skip.update(skip)
+                    self._fused[result] = spec
+                    continue
             # dot / convolution -> relu epilogue
             if ins.opcode in (Op.DOT, Op.CONVOLUTION) and only_user(ins.id, Op.RELU) \
                     and ins.shape.dtype == DType.BF16:
                 relu = by[users[ins.id][0]]
                 self._fused_skip.add(ins.id)
                 self._fused[relu.id] = ("dot_relu" if ins.opcode == Op.DOT else "conv_relu", ins)
+
+    def _match_range_mask(self, sel: Instruction, users, outs):
+        """Recognise select(iota+off < high, val, bcast(fill)) [then
+        select(iota+off >= low, ., same fill)] as emitted by the partitioner's
+        select_range (reference partitioner.py:212-228)."""
+        by = self.by_id
+
+        def get(i):
+            return by.get(i)
+
+        def scalar_bcast(i):
+            b = get(i)
+            if b is None or b.opcode != Op.BROADCAST or tuple(b.attrs["broadcast_dims"]) != ():
+                return None
+            return b
+
+        def const_int(i):
+            c = get(i)
+            if c is None or c.opcode != Op.CONSTANT:
+                return None
+            lit = np.asarray(c.attrs["literal"])
+            return int(lit) if lit.size == 1 else None
+
+        def parse_cmp(pred_id, direction):
+            pred = get(pred_id)
+            if pred is None or pred.opcode != Op.COMPARE or pred.attrs["direction"] != direction:
+                return None
+            gidx, bc = get(pred.operands[0]), scalar_bcast(pred.operands[1])
+            if gidx is None or bc is None or gidx.opcode != Op.ADD:
+                return None
+            bound = const_int(bc.operands[0])
+            if bound is None:
+                return None
+            return pred, gidx, bc, bound
+
+        if sel.id in outs:
+            return None
+        lt = parse_cmp(sel.operands[0], CompareDirection.LT)
+        if lt is None:
+            return None
+        pred_lt, gidx, bc_hi, high = lt
+        iota, boff = get(gidx.operands[0]), scalar_bcast(gidx.operands[1])
+        if iota is None or iota.opcode != Op.IOTA or boff is None:
+            return None
+        if iota.shape.dims != sel.shape.dims or boff.shape.dtype != DType.S32:
+            return None
+        fill = scalar_bcast(sel.operands[2])
+        if fill is None:
+            return None
+        val = sel.operands[1]
+        chain = [iota.id, boff.id, gidx.id, bc_hi.id, pred_lt.id, fill.id]
+        result, low, has_low = sel, 0, False
+        su = users.get(sel.id, [])
+        if len(su) == 1 and get(su[0]).opcode == Op.SELECT:
+            outer = get(su[0])
+            ge = parse_cmp(outer.operands[0], CompareDirection.GE)
+            if ge is not None and ge[1].id == gidx.id and outer.operands[1] == sel.id \
+                    and outer.operands[2] == fill.id:
+                chain += [sel.id, ge[0].id, ge[2].id]
+                result, low, has_low = outer, ge[3], True
+        allowed = set(chain) | {result.id}
+        for vid in chain:
+            if vid in outs or any(u not in allowed for u in users.get(vid, [])):
+                return None
+        spec = ("mask", val, boff.operands[0], fill.operands[0], iota.attrs["iota_dimension"],
+                low, high, has_low)
+        return result.id, chain, spec
 
     # ------------------------------------------------------------------
     # compilation: one closure per instruction
@@ -330,6 +405,8 @@ class Executor:
             return ins.operands
         if f[0] == "softmax":
             return (f[1],)
+        if f[0] == "mask":
+            return (f[1], f[2], f[3])
         return f[1].operands
 
     def _make_step(self, ins: Instruction):
@@ -352,6 +429,17 @@ class Executor:
             return self._dot_step(f[1], shp, epilogue=1)
         if f is not None and f[0] == "conv_relu":
             return self._conv_step(f[1], epilogue=1)
+        if f is not None and f[0] == "mask":
+            _, val, off, fill, axis, low, high, has_low = f
+            vsh, osh, fsh = self._shape(val), self._shape(off), self._shape(fill)
+
+            def run(env, s):
+                out = self._alloc(shp)
+                C.check(lib.spmd_mask_range(desc(env[val], vsh), desc(env[off], osh),
+                                            desc(env[fill], fsh), desc(out, shp), axis, low,
+                                            high, int(has_low), P, s), "mask_range")
+                return out
+            return run
 
         if op == Op.PARAMETER:
             idx = [p.id for p in self.params].index(ins.id)
