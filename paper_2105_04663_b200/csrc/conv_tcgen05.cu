@@ -25,6 +25,7 @@ struct ConvShape {
   int nwb, nt, cin_blocks, kblocks;
   int64_t tiles;
   int relu;
+  int tma_store;
 };
 
 template <int BN, int STAGES>
@@ -33,7 +34,8 @@ struct ConvSmem {
   static constexpr int B_BYTES = BN * CBK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int BAR_OFF = STAGES * STAGE_BYTES;
-  static constexpr int TOTAL = BAR_OFF + 256 + 1024;
+  static constexpr int EPI_OFF = BAR_OFF + 1024;
+  static constexpr int TOTAL = EPI_OFF + 8 * EPI_STAGE_BYTES + 1024;
 };
 
 __device__ __forceinline__ void conv_tile(const ConvShape& g, int64_t t, int& pn, int& ho, int& wb,
@@ -49,7 +51,8 @@ __device__ __forceinline__ void conv_tile(const ConvShape& g, int64_t t, int& pn
 template <int BN, int STAGES>
 __global__ void __launch_bounds__(256, 1)
     conv_bf16_tcgen05(const __grid_constant__ CUtensorMap map_x,
-                      const __grid_constant__ CUtensorMap map_w, bf16* __restrict__ out,
+                      const __grid_constant__ CUtensorMap map_w,
+                      const __grid_constant__ CUtensorMap map_o, bf16* __restrict__ out,
                       ConvShape g) {
   typedef ConvSmem<BN, STAGES> L;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -141,6 +144,8 @@ __global__ void __launch_bounds__(256, 1)
     }
   } else if (warp >= 4) {
     const int ew = warp - 4;
+    uint8_t* epi = smem + L::EPI_OFF + ew * 2 * EPI_STAGE_BYTES;
+    int chunk = 0;
     int acc = 0;
     uint32_t acc_ph = 0;
     for (int64_t t = blockIdx.x; t < g.tiles; t += gridDim.x) {
@@ -155,7 +160,10 @@ __global__ void __launch_bounds__(256, 1)
         uint32_t r[32];
         tmem_ld32(tmem + ((uint32_t)(ew * 32) << 16) + acc * BN + c0, r);
         const int col = ct * BN + c0;
-        if (wo < g.Wo && col < g.Cout) {
+        if (g.tma_store) {
+          epi_store_chunk(&map_o, epi + (chunk++ & 1) * EPI_STAGE_BYTES, r, g.relu, col,
+                          wb * CBM + ew * 32, pn * g.Ho + ho, lane);
+        } else if (wo < g.Wo && col < g.Cout) {
           __align__(16) bf16 v[32];
 #pragma unroll
           for (int j = 0; j < 32; ++j) {
@@ -176,6 +184,7 @@ __global__ void __launch_bounds__(256, 1)
         acc_ph ^= 1;
       }
     }
+    if (lane == 0) bulk_wait_all();
   }
   tc_fence_before();
   __syncthreads();
@@ -186,7 +195,8 @@ __global__ void __launch_bounds__(256, 1)
 }
 
 template <int BN, int STAGES>
-static int launch_conv(const CUtensorMap& mx, const CUtensorMap& mw, bf16* out, ConvShape g,
+static int launch_conv(const CUtensorMap& mx, const CUtensorMap& mw, const CUtensorMap& mo,
+                       bf16* out, ConvShape g,
                        cudaStream_t s) {
   typedef ConvSmem<BN, STAGES> L;
   static bool configured = false;
@@ -199,7 +209,7 @@ static int launch_conv(const CUtensorMap& mx, const CUtensorMap& mw, bf16* out, 
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   int64_t grid = g.tiles < sms ? g.tiles : sms;
-  conv_bf16_tcgen05<BN, STAGES><<<(unsigned)grid, 256, L::TOTAL, s>>>(mx, mw, out, g);
+  conv_bf16_tcgen05<BN, STAGES><<<(unsigned)grid, 256, L::TOTAL, s>>>(mx, mw, mo, out, g);
   return launched(s);
 }
 
@@ -251,8 +261,12 @@ int conv_tcgen05(const spmd_tensor& lhs, const spmd_tensor& rhs, const spmd_tens
   g.kblocks = g.KH * g.KW * g.cin_blocks;
   g.tiles = (int64_t)nparts * g.N * g.Ho * g.nwb * g.nt;
   g.relu = cd.epilogue == 1;
-  if (BN == 256) return launch_conv<256, 4>(mx, mw, (bf16*)out.data, g, s);
-  return launch_conv<128, 6>(mx, mw, (bf16*)out.data, g, s);
+  CUtensorMap mo;
+  g.tma_store = encode_store_map(&mo, out.data, g.Cout, g.Wo, g.Cout, nparts * g.N * g.Ho,
+                                 (int64_t)g.Wo * g.Cout);
+  if (!g.tma_store) memset(&mo, 0, sizeof(mo));
+  if (BN == 256) return launch_conv<256, 4>(mx, mw, mo, (bf16*)out.data, g, s);
+  return launch_conv<128, 6>(mx, mw, mo, (bf16*)out.data, g, s);
 }
 
 }  // namespace spmd

@@ -38,6 +38,7 @@ struct GemmShape {
   int64_t out_batch_stride;   // elements between consecutive flat batches
   int a_mn, b_mn;
   int relu;
+  int tma_store;        // epilogue through the bulk-tensor store path
 };
 
 template <int BN, int STAGES>
@@ -46,7 +47,8 @@ struct Smem {
   static constexpr int B_BYTES = BN * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int BAR_OFF = STAGES * STAGE_BYTES;
-  static constexpr int TOTAL = BAR_OFF + 256 + 1024;   // + barriers + align slack
+  static constexpr int EPI_OFF = BAR_OFF + 1024;        // 4 warps x 2 x 2 KB staging
+  static constexpr int TOTAL = EPI_OFF + 8 * EPI_STAGE_BYTES + 1024;   // + align slack
 };
 
 __device__ __forceinline__ void tile_coords(const GemmShape& g, int64_t t, int& b, int& m, int& n) {
@@ -66,7 +68,8 @@ __device__ __forceinline__ void tile_coords(const GemmShape& g, int64_t t, int& 
 template <int BN, int STAGES>
 __global__ void __launch_bounds__(256, 1)
     gemm_bf16_tcgen05(const __grid_constant__ CUtensorMap map_a,
-                      const __grid_constant__ CUtensorMap map_b, bf16* __restrict__ out,
+                      const __grid_constant__ CUtensorMap map_b,
+                      const __grid_constant__ CUtensorMap map_c, bf16* __restrict__ out,
                       GemmShape g) {
   typedef Smem<BN, STAGES> L;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -178,6 +181,8 @@ __global__ void __launch_bounds__(256, 1)
   } else if (warp >= EPI_WARP0) {
     // ---------------- epilogue ----------------
     const int ew = warp - EPI_WARP0;          // == warp % 4 -> TMEM lanes 32*ew..
+    uint8_t* epi = smem + L::EPI_OFF + ew * 2 * EPI_STAGE_BYTES;
+    int chunk = 0;
     int acc = 0;
     uint32_t acc_ph = 0;
     for (int64_t t = blockIdx.x; t < g.tiles; t += gridDim.x) {
@@ -192,7 +197,11 @@ __global__ void __launch_bounds__(256, 1)
         uint32_t r[32];
         tmem_ld32(tmem + ((uint32_t)(ew * 32) << 16) + acc * BN + c0, r);
         const int col = n * BN + c0;
-        if (row < g.M && col < g.N) {
+        if (g.tma_store) {
+          if (col < g.N)
+            epi_store_chunk(&map_c, epi + (chunk++ & 1) * EPI_STAGE_BYTES, r, g.relu, col,
+                            m * BM + ew * 32, b, lane);
+        } else if (row < g.M && col < g.N) {
           __align__(16) bf16 v[32];
 #pragma unroll
           for (int j = 0; j < 32; ++j) {
@@ -217,6 +226,7 @@ __global__ void __launch_bounds__(256, 1)
         acc_ph ^= 1;
       }
     }
+    if (lane == 0) bulk_wait_all();
   }
   tc_fence_before();
   __syncthreads();
@@ -297,13 +307,15 @@ struct Smem2 {
   static constexpr int B_BYTES = HALF * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int BAR_OFF = STAGES * STAGE_BYTES;
-  static constexpr int TOTAL = BAR_OFF + 256 + 1024;
+  static constexpr int EPI_OFF = BAR_OFF + 1024;
+  static constexpr int TOTAL = EPI_OFF + 8 * EPI_STAGE_BYTES + 1024;
 };
 
 template <int STAGES>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
     gemm_bf16_tcgen05_2sm(const __grid_constant__ CUtensorMap map_a,
-                          const __grid_constant__ CUtensorMap map_b, bf16* __restrict__ out,
+                          const __grid_constant__ CUtensorMap map_b,
+                          const __grid_constant__ CUtensorMap map_c, bf16* __restrict__ out,
                           GemmShape g) {
   typedef Smem2<STAGES> L;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -416,6 +428,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
   } else if (warp >= EPI_WARP0) {
     // ---------------- epilogue (both CTAs, own TMEM half) ----------------
     const int ew = warp - EPI_WARP0;
+    uint8_t* epi = smem + L::EPI_OFF + ew * 2 * EPI_STAGE_BYTES;
+    int chunk = 0;
     int acc = 0;
     uint32_t acc_ph = 0;
     for (int64_t t = cluster; t < g.tiles; t += nclusters) {
@@ -430,7 +444,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
         uint32_t r[32];
         tmem_ld32(tmem + ((uint32_t)(ew * 32) << 16) + acc * BN2 + c0, r);
         const int col = n * BN2 + c0;
-        if (row < g.M && col < g.N) {
+        if (g.tma_store) {
+          if (col < g.N)
+            epi_store_chunk(&map_c, epi + (chunk++ & 1) * EPI_STAGE_BYTES, r, g.relu, col,
+                            m * BM2 + rank * HALF + ew * 32, b, lane);
+        } else if (row < g.M && col < g.N) {
           __align__(16) bf16 v[32];
 #pragma unroll
           for (int j = 0; j < 32; ++j) {
@@ -455,6 +473,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
         acc_ph ^= 1;
       }
     }
+    if (lane == 0) bulk_wait_all();
   }
   tc_fence_before();
   cluster_sync();
@@ -493,7 +512,8 @@ static bool merge_dims(const DimRef* d, int n, DimRef* out) {
 }
 
 template <int BN, int STAGES>
-static int launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, bf16* out, GemmShape g,
+static int launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc,
+                       bf16* out, GemmShape g,
                        cudaStream_t s) {
   typedef Smem<BN, STAGES> L;
   static bool configured = false;
@@ -510,12 +530,13 @@ static int launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, bf16* out, 
     if (sms <= 0) sms = 148;
   }
   int64_t grid = g.tiles < sms ? g.tiles : sms;
-  gemm_bf16_tcgen05<BN, STAGES><<<(unsigned)grid, 256, L::TOTAL, s>>>(ma, mb, out, g);
+  gemm_bf16_tcgen05<BN, STAGES><<<(unsigned)grid, 256, L::TOTAL, s>>>(ma, mb, mc, out, g);
   return launched(s);
 }
 
 template <int STAGES>
-static int launch_gemm_2sm(const CUtensorMap& ma, const CUtensorMap& mb, bf16* out, GemmShape g,
+static int launch_gemm_2sm(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc,
+                           bf16* out, GemmShape g,
                            cudaStream_t s) {
   typedef Smem2<STAGES> L;
   static bool configured = false;
@@ -532,7 +553,8 @@ static int launch_gemm_2sm(const CUtensorMap& ma, const CUtensorMap& mb, bf16* o
     if (sms <= 0) sms = 148;
   }
   int64_t clusters = g.tiles < sms / 2 ? g.tiles : sms / 2;
-  gemm_bf16_tcgen05_2sm<STAGES><<<(unsigned)(2 * clusters), 256, L::TOTAL, s>>>(ma, mb, out, g);
+  gemm_bf16_tcgen05_2sm<STAGES><<<(unsigned)(2 * clusters), 256, L::TOTAL, s>>>(ma, mb, mc, out,
+                                                                                    g);
   return launched(s);
 }
 
@@ -633,7 +655,14 @@ int dot_tcgen05(const spmd_tensor& lhs, const spmd_tensor& rhs, const spmd_tenso
     vb.size[0] = N.size, vb.stride[0] = 1, vb.size[1] = K2.size, vb.stride[1] = K2.st;
   }
   g.out_batch_stride = (int64_t)g.M * g.N;
-  CUtensorMap ma, mb;
+  CUtensorMap ma, mb, mc;
+  // Bulk-tensor store epilogue whenever the output rows are 16-byte aligned.
+  {
+    const int64_t nbat = (int64_t)g.nb[0] * g.nb[1] * g.nb[2];
+    g.tma_store = (g.N % 8 == 0) &&
+                  encode_store_map(&mc, out.data, g.N, g.M, g.N, nbat, g.out_batch_stride);
+    if (!g.tma_store) memset(&mc, 0, sizeof(mc));
+  }
   if (gemm_mode() == 2 && M.size >= 256 && N.size >= 256) {
     // 2-CTA path: per-CTA boxes are 128 rows of A and 128 rows of B.
     bool ok2 = a_mn ? encode(&ma, lhs.data, va, 64, BK) : encode(&ma, lhs.data, va, BK, HALF);
@@ -642,7 +671,7 @@ int dot_tcgen05(const spmd_tensor& lhs, const spmd_tensor& rhs, const spmd_tenso
     g.mt = (g.M + BM2 - 1) / BM2;
     g.nt = (g.N + BN2 - 1) / BN2;
     g.tiles = (int64_t)g.mt * g.nt * g.nb[0] * g.nb[1] * g.nb[2];
-    return launch_gemm_2sm<6>(ma, mb, (bf16*)out.data, g, s);
+    return launch_gemm_2sm<6>(ma, mb, mc, (bf16*)out.data, g, s);
   }
   const int BNsel = N.size >= 256 ? 256 : 128;
   bool ok = a_mn ? encode(&ma, lhs.data, va, 64, BK) : encode(&ma, lhs.data, va, BK, BM);
@@ -652,8 +681,8 @@ int dot_tcgen05(const spmd_tensor& lhs, const spmd_tensor& rhs, const spmd_tenso
   g.nt = (g.N + BNsel - 1) / BNsel;
   g.tiles = (int64_t)g.mt * g.nt * g.nb[0] * g.nb[1] * g.nb[2];
   g.out_batch_stride = (int64_t)g.M * g.N;
-  if (BNsel == 256) return launch_gemm<256, 4>(ma, mb, (bf16*)out.data, g, s);
-  return launch_gemm<128, 6>(ma, mb, (bf16*)out.data, g, s);
+  if (BNsel == 256) return launch_gemm<256, 4>(ma, mb, mc, (bf16*)out.data, g, s);
+  return launch_gemm<128, 6>(ma, mb, mc, (bf16*)out.data, g, s);
 }
 
 }  // namespace spmd

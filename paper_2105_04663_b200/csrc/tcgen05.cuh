@@ -159,4 +159,73 @@ inline bool encode(CUtensorMap* map, void* base, const OperandView& v, int box_i
   return r == CUDA_SUCCESS;
 }
 
+// ---------------------------------------------------------------------------
+// TMA-store epilogue: each epilogue warp stages its 32 rows x 32 columns of
+// bf16 in a 2 KB shared buffer (64-byte rows, 16-byte chunks XOR-swizzled
+// exactly like CU_TENSOR_MAP_SWIZZLE_64B so st.shared is conflict-free) and
+// one lane issues a 3-D bulk tensor store (cols, rows, batch); the TMA unit
+// clips out-of-range rows/columns.  Two buffers per warp, bulk-group
+// double buffering.
+// ---------------------------------------------------------------------------
+constexpr int EPI_STAGE_BYTES = 32 * 64;   // 32 rows x 32 bf16
+
+// 3-D output map: dims (cols, rows, batch), element strides (1, ld, batch_stride).
+inline bool encode_store_map(CUtensorMap* map, void* base, int64_t cols, int64_t rows,
+                             int64_t ld, int64_t batch, int64_t batch_stride) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn || (reinterpret_cast<uintptr_t>(base) & 15) != 0) return false;
+  cuuint64_t dims[3] = {(cuuint64_t)cols, (cuuint64_t)rows, (cuuint64_t)(batch > 0 ? batch : 1)};
+  cuuint64_t strides[2] = {(cuuint64_t)(ld * 2), (cuuint64_t)((batch > 1 ? batch_stride : ld) * 2)};
+  if (strides[0] % 16 || strides[1] % 16) return false;
+  cuuint32_t box[3] = {32, 32, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, base, dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
+                  CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+__device__ __forceinline__ void bulk_wait_read_le1() {
+  asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() {
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
+// Stage + store one 32x32 chunk.  r: this lane's 32 fp32 accumulators of row
+// (row0 + lane), columns col..col+31.  `stage` is 512-byte aligned.
+__device__ __forceinline__ void epi_store_chunk(const CUtensorMap* map, uint8_t* stage,
+                                                const uint32_t (&r)[32], bool relu, int col,
+                                                int row0, int batch, int lane) {
+  // Buffer reuse: the store issued from this buffer two chunks ago must have
+  // finished reading shared memory.
+  if (lane == 0) bulk_wait_read_le1();
+  __syncwarp();
+  uint4 q[4];
+  __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(q);
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    float a = __uint_as_float(r[2 * j]), b = __uint_as_float(r[2 * j + 1]);
+    if (relu) {
+      a = a > 0.f ? a : 0.f;
+      b = b > 0.f ? b : 0.f;
+    }
+    h[j] = __floats2bfloat162_rn(a, b);
+  }
+  uint8_t* row = stage + lane * 64;
+  const int sw = (lane >> 1) & 3;
+#pragma unroll
+  for (int c = 0; c < 4; ++c) *reinterpret_cast<uint4*>(row + ((c ^ sw) << 4)) = q[c];
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  __syncwarp();
+  if (lane == 0) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
+            reinterpret_cast<uint64_t>(map)),
+        "r"(smem_u32(stage)), "r"(col), "r"(row0), "r"(batch)
+        : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+  }
+}
+
 }  // namespace spmd
