@@ -659,7 +659,12 @@ int dot_tcgen05(const spmd_tensor& lhs, const spmd_tensor& rhs, const spmd_tenso
   // Bulk-tensor store epilogue whenever the output rows are 16-byte aligned.
   {
     const int64_t nbat = (int64_t)g.nb[0] * g.nb[1] * g.nb[2];
-    g.tma_store = (g.N % 8 == 0) &&
+    static int direct = -1;
+    if (direct < 0) {
+      const char* e = getenv("SPMD_GEMM_EPI");
+      direct = (e && strcmp(e, "direct") == 0) ? 1 : 0;
+    }
+    g.tma_store = !direct && (g.N % 8 == 0) &&
                   encode_store_map(&mc, out.data, g.N, g.M, g.N, nbat, g.out_batch_stride);
     if (!g.tma_store) memset(&mc, 0, sizeof(mc));
   }
