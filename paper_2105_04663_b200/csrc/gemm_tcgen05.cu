@@ -39,6 +39,9 @@ struct GemmShape {
   int a_mn, b_mn;
   int relu;
   int tma_store;        // epilogue through the bulk-tensor store path
+  int group;            // rasterisation group size (tiles of the grouped dim)
+  int raster_n;         // 0: group M-tiles and sweep N; 1: group N-tiles and sweep M
+  int hint;             // 0 none, 1: A evict_last / B evict_first, 2: the reverse
 };
 
 template <int BN, int STAGES>
@@ -55,14 +58,18 @@ __device__ __forceinline__ void tile_coords(const GemmShape& g, int64_t t, int& 
   const int64_t per = (int64_t)g.mt * g.nt;
   b = (int)(t / per);
   int r = (int)(t - (int64_t)b * per);
-  // Grouped rasterisation: 8 M-tiles sweep the N-tiles together (L2 reuse).
-  const int G = 8;
-  int group = r / (G * g.nt);
+  // Grouped rasterisation: G tiles of one dim sweep the other dim together,
+  // so one operand's group stays L2-resident while the other streams.
+  const int G = g.group;
+  const int ga = g.raster_n ? g.nt : g.mt;   // grouped dim extent
+  const int gb = g.raster_n ? g.mt : g.nt;   // swept dim extent
+  int group = r / (G * gb);
   int first = group * G;
-  int gs = g.mt - first < G ? g.mt - first : G;
-  int rr = r - group * G * g.nt;
-  m = first + rr % gs;
-  n = rr / gs;
+  int gs = ga - first < G ? ga - first : G;
+  int rr = r - group * G * gb;
+  int x = first + rr % gs, y = rr / gs;
+  m = g.raster_n ? y : x;
+  n = g.raster_n ? x : y;
 }
 
 template <int BN, int STAGES>
@@ -272,6 +279,26 @@ __device__ __forceinline__ void tma_load_5d_2sm(void* dst, const CUtensorMap* ma
       : "memory");
 }
 
+__device__ __forceinline__ void tma_load_5d_2sm_hint(void* dst, const CUtensorMap* map,
+                                                     uint64_t* bar, int c0, int c1, int c2,
+                                                     int c3, int c4, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.5d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      ".L2::cache_hint [%0], [%1, {%3, %4, %5, %6, %7}], [%2], %8;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar) & PEER_MASK), "r"(c0), "r"(c1),
+      "r"(c2), "r"(c3), "r"(c4), "l"(policy)
+      : "memory");
+}
+
+__device__ __forceinline__ void load_2sm(void* dst, const CUtensorMap* map, uint64_t* bar, int c0,
+                                         int c1, int c2, int c3, int c4, int use_hint,
+                                         uint64_t policy) {
+  if (use_hint)
+    tma_load_5d_2sm_hint(dst, map, bar, c0, c1, c2, c3, c4, policy);
+  else
+    tma_load_5d_2sm(dst, map, bar, c0, c1, c2, c3, c4);
+}
+
 __device__ __forceinline__ void tc_commit_2sm_mc(uint64_t* bar) {
   asm volatile(
       "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
@@ -358,6 +385,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
     // ---------------- TMA producer (both CTAs) ----------------
     int s = 0;
     uint32_t ph = 0;
+    uint64_t pol_last, pol_first;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_last));
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_first));
+    const int hint = g.hint != 0;
+    const uint64_t pa = g.hint == 1 ? pol_last : pol_first;
+    const uint64_t pb = g.hint == 1 ? pol_first : pol_last;
     for (int64_t t = cluster; t < g.tiles; t += nclusters) {
       int b, m, n;
       tile_coords(g, t, b, m, n);
@@ -370,18 +403,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
         if (leader) mbar_expect_tx(&full[s], 2 * L::STAGE_BYTES);
         const int k0 = kb * BK;
         if (!g.a_mn) {
-          tma_load_5d_2sm(sa, &map_a, &full[s], k0, mrow, b0, b1, b2);
+          load_2sm(sa, &map_a, &full[s], k0, mrow, b0, b1, b2, hint, pa);
         } else {
 #pragma unroll
           for (int c = 0; c < HALF / 64; ++c)
-            tma_load_5d_2sm(sa + c * (BK * 128), &map_a, &full[s], mrow + c * 64, k0, b0, b1, b2);
+            load_2sm(sa + c * (BK * 128), &map_a, &full[s], mrow + c * 64, k0, b0, b1, b2, hint,
+                     pa);
         }
         if (!g.b_mn) {
-          tma_load_5d_2sm(sb, &map_b, &full[s], k0, nrow, b0, b1, b2);
+          load_2sm(sb, &map_b, &full[s], k0, nrow, b0, b1, b2, hint, pb);
         } else {
 #pragma unroll
           for (int c = 0; c < HALF / 64; ++c)
-            tma_load_5d_2sm(sb + c * (BK * 128), &map_b, &full[s], nrow + c * 64, k0, b0, b1, b2);
+            load_2sm(sb + c * (BK * 128), &map_b, &full[s], nrow + c * 64, k0, b0, b1, b2, hint,
+                     pb);
         }
         if (++s == STAGES) {
           s = 0;
@@ -629,6 +664,21 @@ int dot_tcgen05(const spmd_tensor& lhs, const spmd_tensor& rhs, const spmd_tenso
   g.a_mn = a_mn;
   g.b_mn = b_mn;
   g.relu = dd.epilogue == 1;
+  {
+    static int group = -1, raster = -1, hint = -1;
+    if (group < 0) {
+      const char* e = getenv("SPMD_GEMM_GROUP");
+      group = e ? atoi(e) : 8;
+      if (group < 1) group = 8;
+      e = getenv("SPMD_GEMM_RASTER");
+      raster = (e && strcmp(e, "n") == 0) ? 1 : 0;
+      e = getenv("SPMD_GEMM_HINT");
+      hint = e ? atoi(e) : 0;
+    }
+    g.group = group;
+    g.raster_n = raster;
+    g.hint = hint;
+  }
   // tensor-map batch dims: innermost first
   OperandView va, vb;
   for (int i = 0; i < 3; ++i) {
