@@ -78,6 +78,9 @@ const char* spmd_last_error(void);
 int spmd_check_device_errors(void* stream);
 /* Number of kernels this library has launched (for launch accounting). */
 int64_t spmd_launch_count(void);
+/* Cap the SMs used by the persistent tensor-core kernels (0 = all), leaving
+ * room for collective kernels that overlap them. */
+int spmd_set_sm_limit(int sms);
 
 /* ---- sources (simulator.py:161-172) ---------------------------------------- */
 int spmd_iota(spmd_tensor out, int axis, int64_t nparts, void* stream);

@@ -61,6 +61,7 @@ _SIGNATURES = {
     "spmd_last_error": ([], ctypes.c_char_p),
     "spmd_check_device_errors": ([_P], _I),
     "spmd_launch_count": ([], _I64),
+    "spmd_set_sm_limit": ([_I], _I),
     "spmd_iota": ([_T, _I, _I64, _P], _I),
     "spmd_partition_id": ([_T, _I64, ctypes.c_int32, _P], _I),
     "spmd_constant": ([_T, _T, _I64, _P], _I),

@@ -32,9 +32,29 @@ int* device_error_word() {
   return words[dev];
 }
 
+static std::atomic<int> g_sm_limit{0};
+
+int sm_budget() {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  const int lim = g_sm_limit.load();
+  int n = (lim > 0 && lim < sms) ? lim : sms;
+  return n < 2 ? 2 : (n & ~1);   // even: CTA pairs
+}
+
 }  // namespace spmd
 
 using namespace spmd;
+
+extern "C" int spmd_set_sm_limit(int sms) {
+  g_sm_limit.store(sms > 0 ? sms : 0);
+  return SPMD_OK;
+}
 
 extern "C" const char* spmd_version(void) { return "spmd_b200 0.1.0 (sm_100a)"; }
 

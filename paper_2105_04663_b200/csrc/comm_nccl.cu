@@ -156,7 +156,15 @@ extern "C" int spmd_comm_init(spmd_comm** comm, int nranks, int rank, const void
   c->rank = rank;
   ncclUniqueId id;
   memcpy(&id, unique_id, sizeof(id));
-  ncclResult_t r = ncclCommInitRank(&c->world, nranks, id, rank);
+  // Optional CTA cap so NCCL kernels fit beside persistent GEMMs
+  // (SPMD_NCCL_MAX_CTAS; sub-communicators inherit the config).
+  ncclConfig_t cfg = NCCL_CONFIG_INITIALIZER;
+  const char* mc = getenv("SPMD_NCCL_MAX_CTAS");
+  if (mc && atoi(mc) > 0) {
+    cfg.maxCTAs = atoi(mc);
+    cfg.minCTAs = cfg.maxCTAs < 4 ? cfg.maxCTAs : 4;
+  }
+  ncclResult_t r = ncclCommInitRankConfig(&c->world, nranks, id, rank, &cfg);
   if (r != ncclSuccess) {
     set_error(std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
     delete c;

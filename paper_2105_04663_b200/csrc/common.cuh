@@ -19,6 +19,9 @@ extern std::atomic<int64_t> g_launches;
 // Device error word (cudaMalloc'd int on the current device): bit 0 =
 // integer division by zero.  Kernels that can fault receive it as a pointer.
 int* device_error_word();
+// SMs the persistent tensor-core kernels may occupy (spmd_set_sm_limit):
+// leaves room for NCCL kernels to co-reside when collectives overlap GEMMs.
+int sm_budget();
 
 #define SPMD_CHECK_ARG(cond, msg)                  \
   do {                                             \

@@ -205,9 +205,7 @@ static int launch_conv(const CUtensorMap& mx, const CUtensorMap& mw, const CUten
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, L::TOTAL));
     configured = true;
   }
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int sms = sm_budget();
   int64_t grid = g.tiles < sms ? g.tiles : sms;
   conv_bf16_tcgen05<BN, STAGES><<<(unsigned)grid, 256, L::TOTAL, s>>>(mx, mw, mo, out, g);
   return launched(s);

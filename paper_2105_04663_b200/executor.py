@@ -177,6 +177,13 @@ class Executor:
         if self.overlap:
             self.steps = self._hoist_collectives(self.steps)
             self.comm_stream = torch.cuda.Stream(device=self.device)
+            # Leave SMs for the collective kernels that run under the GEMMs
+            # (SPMD_COMM_SMS, default 0 = let the GEMM take every SM).
+            import os
+            reserve = int(os.environ.get("SPMD_COMM_SMS", "0"))
+            if reserve > 0:
+                sms = torch.cuda.get_device_properties(self.device).multi_processor_count
+                self.lib.spmd_set_sm_limit(max(2, sms - reserve))
         if comm is not None:
             comm.ensure_workspace(self._workspace_bytes(), self.device)
 
