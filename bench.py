@@ -178,6 +178,30 @@ def _rand_like_shard(shape, device, scale, seed):
     return (t * scale).to(torch.bfloat16)
 
 
+def _traffic_for(top, prog):
+    """dram read+write bytes per launch of the top GEMM from the committed ncu
+    --set full capture (profiles/*_top_kernel_traffic.json) when the shape
+    matches; else None."""
+    import glob
+    try:
+        from paper_2105_04663_b200.ir import Op, dot_dim_lists
+        if top.opcode != Op.DOT:
+            return None
+        a = prog.graph.instr(top.operands[0]).shape
+        b = prog.graph.instr(top.operands[1]).shape
+        lb, rb, lc, rc, lf, rf = dot_dim_lists(top.attrs, a.rank, b.rank)
+        prod = lambda s, ds: int(__import__("math").prod(s.dims[d] for d in ds))
+        mnk = [prod(a, lb + lf), prod(b, rf), prod(a, lc)]
+        for fn in sorted(glob.glob(os.path.join(ROOT, "profiles", "*_top_kernel_traffic.json"))):
+            with open(fn) as f:
+                t = json.load(f)
+            if list(t["shape_mnk"]) == mnk:
+                return t["dram_bytes_read"] + t["dram_bytes_write"]
+    except Exception:
+        return None
+    return None
+
+
 C3 = dict(E=8, B=64, S=512, C=160, M=4096, H=16384)
 C4 = dict(N=8, H=1024, W=1024, C=128, layers=4)
 
@@ -485,7 +509,7 @@ def main():
             "roofline": {"bound": "tensor", "kernel": "%s (%s)" % (kname, top.id),
                          "achieved": achieved, "peak": burst, "unit": "TFLOP/s",
                          "frac": achieved / burst, "peak_source": peak_src + " burst",
-                         "traffic": None, "ms_per_launch": kms,
+                         "traffic": _traffic_for(top, prog), "ms_per_launch": kms,
                          "flops_per_launch": dot_flops(top)},
             "reshard": reshard,
             "e2e": e2e, "gpu_launches": int(launches), "clocks": clocks,

@@ -157,6 +157,12 @@ int spmd_convolution(spmd_tensor lhs, spmd_tensor rhs, spmd_tensor out,
 int spmd_mask_range(spmd_tensor in, spmd_tensor offset, spmd_tensor fill, spmd_tensor out,
                     int axis, int64_t low, int64_t high, int has_low, int64_t nparts,
                     void* stream);
+/* Halo window (reference formatting.py:109-182): out = dynamic_slice(
+ * mask(concat(pieces[0..n), axis)), start[p] on axis) in one pass; the mask
+ * (optional) is the range mask above on buffer positions. */
+int spmd_halo_window(const spmd_tensor* pieces, int npieces, int axis, spmd_tensor start,
+                     int has_mask, spmd_tensor offset, spmd_tensor fill, int64_t low,
+                     int64_t high, int has_low, spmd_tensor out, int64_t nparts, void* stream);
 /* Row softmax over the last dim: out = exp(x - max) / sum(exp(x - max)). */
 int spmd_softmax_lastdim(spmd_tensor in, spmd_tensor out, int64_t nparts, void* stream);
 

@@ -10,6 +10,8 @@
 // [P, outer, n_axis, inner] with 16-byte vectors along `inner`.
 #include "common.cuh"
 
+#include <string.h>
+
 namespace spmd {
 
 template <typename T, int V>
@@ -44,9 +46,116 @@ __global__ void mask_range_kernel(const T* __restrict__ in, T* __restrict__ out,
   }
 }
 
+// Halo window (exchange_and_slice, reference formatting.py:109-182): the
+// per-device window = DS(mask(concat(left_halo, shard, right_halo)), start)
+// read straight from the three pieces in one pass.
+struct HaloArgs {
+  const void* piece[3];
+  int64_t len[3];          // piece extents along the axis
+  int npieces;
+  int64_t outer, inner, buf_len, window;
+  const int32_t* start;    // per-partition dynamic-slice start (clamped)
+  int has_mask, has_low;
+  const int32_t* offset;   // per-partition global offset of buffer position 0
+  const void* fill;
+  int64_t low, high;
+};
+
+template <typename T, int V>
+__global__ void halo_window_kernel(T* __restrict__ out, HaloArgs a, int64_t nparts) {
+  const int64_t per_row = a.inner / V;
+  const int64_t per_part = a.outer * a.window * per_row;
+  const int64_t total = per_part * nparts;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t p = idx / per_part;
+    int64_t r = idx - p * per_part;
+    const int64_t v = r % per_row;
+    r /= per_row;
+    const int64_t i = r % a.window;
+    const int64_t o = r / a.window;
+    int64_t s0 = a.start[p];
+    s0 = s0 < 0 ? 0 : (s0 > a.buf_len - a.window ? a.buf_len - a.window : s0);
+    const int64_t j = s0 + i;
+    bool keep = true;
+    if (a.has_mask) {
+      const int64_t g = j + a.offset[p];
+      keep = g < a.high && (!a.has_low || g >= a.low);
+    }
+    T* dst = out + idx * V;
+    if (!keep) {
+      const T f = reinterpret_cast<const T*>(a.fill)[p];
+#pragma unroll
+      for (int q = 0; q < V; ++q) dst[q] = f;
+      continue;
+    }
+    int k = 0;
+    int64_t jj = j;
+    while (k < a.npieces - 1 && jj >= a.len[k]) {
+      jj -= a.len[k];
+      ++k;
+    }
+    const T* src = reinterpret_cast<const T*>(a.piece[k]) +
+                   ((p * a.outer + o) * a.len[k] + jj) * a.inner + v * V;
+    if (V == 1) {
+      dst[0] = src[0];
+    } else {
+      *reinterpret_cast<uint4*>(dst) = *reinterpret_cast<const uint4*>(src);
+    }
+  }
+}
+
 }  // namespace spmd
 
 using namespace spmd;
+
+extern "C" int spmd_halo_window(const spmd_tensor* pieces, int npieces, int axis,
+                                spmd_tensor start, int has_mask, spmd_tensor offset,
+                                spmd_tensor fill, int64_t low, int64_t high, int has_low,
+                                spmd_tensor out, int64_t nparts, void* stream) {
+  SPMD_CHECK_ARG(npieces >= 1 && npieces <= 3 && axis >= 0 && axis < out.rank,
+                 "halo_window arguments");
+  SPMD_CHECK_ARG(start.dtype == SPMD_S32 && start.rank == 0, "halo_window start");
+  HaloArgs a;
+  memset(&a, 0, sizeof(a));
+  a.npieces = npieces;
+  a.outer = a.inner = 1;
+  for (int d = 0; d < axis; ++d) a.outer *= out.dims[d];
+  for (int d = axis + 1; d < out.rank; ++d) a.inner *= out.dims[d];
+  a.window = out.dims[axis];
+  for (int k = 0; k < npieces; ++k) {
+    SPMD_CHECK_ARG(pieces[k].dtype == out.dtype && pieces[k].rank == out.rank,
+                   "halo_window piece mismatch");
+    a.piece[k] = pieces[k].data;
+    a.len[k] = pieces[k].dims[axis];
+    a.buf_len += a.len[k];
+  }
+  SPMD_CHECK_ARG(a.window <= a.buf_len, "halo_window larger than buffer");
+  a.start = (const int32_t*)start.data;
+  a.has_mask = has_mask;
+  if (has_mask) {
+    SPMD_CHECK_ARG(offset.dtype == SPMD_S32 && fill.dtype == out.dtype, "halo_window mask");
+    a.offset = (const int32_t*)offset.data;
+    a.fill = fill.data;
+    a.low = low;
+    a.high = high;
+    a.has_low = has_low;
+  }
+  const int64_t n = a.outer * a.window * a.inner * nparts;
+  if (n == 0) return SPMD_OK;
+  cudaStream_t s = as_stream(stream);
+  const int V = 16 / elem_size(out.dtype);
+  bool vec = a.inner % V == 0 && (reinterpret_cast<uintptr_t>(out.data) & 15) == 0;
+  for (int k = 0; k < npieces; ++k) vec = vec && (reinterpret_cast<uintptr_t>(a.piece[k]) & 15) == 0;
+  SPMD_DISPATCH_BYTES(out.dtype, T, {
+    if (vec)
+      halo_window_kernel<T, 16 / sizeof(T)><<<grid_for(n / V, 256), 256, 0, s>>>((T*)out.data, a,
+                                                                                nparts);
+    else
+      halo_window_kernel<T, 1><<<grid_for(n, 256, 2), 256, 0, s>>>((T*)out.data, a, nparts);
+  });
+  return launched(s);
+}
 
 // out = (low <= iota_axis + offset[p] < high) ? in : fill[p]; has_low=0 drops
 // the lower bound (low = INT64_MIN).

@@ -285,6 +285,49 @@ class Executor:
                 relu = by[users[ins.id][0]]
                 self._fused_skip.add(ins.id)
                 self._fused[relu.id] = ("dot_relu" if ins.opcode == Op.DOT else "conv_relu", ins)
+        self._plan_halo_windows(users, outs)
+
+    def _plan_halo_windows(self, users, outs):
+        """dynamic-slice(mask(concat(left, shard, right))) -> one halo-window
+        pass (the window assembly of exchange_and_slice, reference
+        formatting.py:109-182)."""
+        by = self.by_id
+        for ds in self.graph.instructions:
+            if ds.opcode != Op.DYNAMIC_SLICE or ds.id in self._fused_skip:
+                continue
+            src = ds.operands[0]
+            mask = self._fused.get(src)
+            if mask is not None and mask[0] != "mask":
+                continue
+            cat_id = mask[1] if mask is not None else src
+            cat = by.get(cat_id)
+            if cat is None or cat.opcode != Op.CONCAT or len(cat.operands) > 3:
+                continue
+            axis = cat.attrs["dim"]
+            if mask is not None and mask[4] != axis:
+                continue
+            if cat_id in outs or users.get(cat_id, []) != [src if mask is not None else ds.id]:
+                continue
+            if mask is not None and (src in outs or users.get(src, []) != [ds.id]):
+                continue
+            starts = ds.operands[1:]
+            ok = True
+            for d in range(ds.shape.rank):
+                if d == axis:
+                    continue
+                c = by.get(starts[d])
+                lit = np.asarray(c.attrs["literal"]) if c is not None and \
+                    c.opcode == Op.CONSTANT else None
+                if lit is None or lit.size != 1 or int(lit) != 0 or \
+                        ds.attrs["sizes"][d] != cat.shape.dims[d]:
+                    ok = False
+                    break
+            if not ok:
+                continue
+            self._fused_skip.add(cat_id)
+            if mask is not None:
+                self._fused_skip.add(src)
+            self._fused[ds.id] = ("halo", tuple(cat.operands), axis, starts[axis], mask)
 
     def _match_range_mask(self, sel: Instruction, users, outs):
         """Recognise select(iota+off < high, val, bcast(fill)) [then
@@ -414,6 +457,9 @@ class Executor:
             return (f[1],)
         if f[0] == "mask":
             return (f[1], f[2], f[3])
+        if f[0] == "halo":
+            mask = f[4]
+            return tuple(f[1]) + (f[3],) + ((mask[2], mask[3]) if mask is not None else ())
         return f[1].operands
 
     def _make_step(self, ins: Instruction):
@@ -436,6 +482,29 @@ class Executor:
             return self._dot_step(f[1], shp, epilogue=1)
         if f is not None and f[0] == "conv_relu":
             return self._conv_step(f[1], epilogue=1)
+        if f is not None and f[0] == "halo":
+            _, pieces, axis, start, mask = f
+            psh = [self._shape(x) for x in pieces]
+            ssh = self._shape(start)
+            if mask is not None:
+                _, _, off, fill, _, low, high, has_low = mask
+                osh, fsh = self._shape(off), self._shape(fill)
+
+            def run(env, s):
+                out = self._alloc(shp)
+                arr = (C.SpmdTensor * len(pieces))(*[desc(env[x], sh)
+                                                     for x, sh in zip(pieces, psh)])
+                if mask is None:
+                    dummy = desc(env[start], ssh)
+                    rc = lib.spmd_halo_window(arr, len(pieces), axis, desc(env[start], ssh), 0,
+                                              dummy, dummy, 0, 0, 0, desc(out, shp), P, s)
+                else:
+                    rc = lib.spmd_halo_window(arr, len(pieces), axis, desc(env[start], ssh), 1,
+                                              desc(env[off], osh), desc(env[fill], fsh), low,
+                                              high, int(has_low), desc(out, shp), P, s)
+                C.check(rc, "halo_window")
+                return out
+            return run
         if f is not None and f[0] == "mask":
             _, val, off, fill, axis, low, high, has_low = f
             vsh, osh, fsh = self._shape(val), self._shape(off), self._shape(fill)
