@@ -306,7 +306,9 @@ class Executor:
             axis = cat.attrs["dim"]
             if mask is not None and mask[4] != axis:
                 continue
-            if cat_id in outs or users.get(cat_id, []) != [src if mask is not None else ds.id]:
+            consumer = src if mask is not None else ds.id
+            if cat_id in outs or any(u != consumer and u not in self._fused_skip
+                                     for u in users.get(cat_id, [])):
                 continue
             if mask is not None and (src in outs or users.get(src, []) != [ds.id]):
                 continue
