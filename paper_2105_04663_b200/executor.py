@@ -881,6 +881,41 @@ class Executor:
                     env.pop(vid, None)
         compute.wait_stream(comm)                 # join
 
+    def timeline(self, inputs) -> list[dict]:
+        """Eager run with CUDA events around every step on the stream it is
+        issued to; returns [{id, op, stream, start_ms, end_ms}] relative to
+        the first event (diagnostics: compute-stream gaps = exposed comm)."""
+        torch = _torch()
+        marks = []
+        orig = [s.fn for s in self.steps]
+        compute = torch.cuda.current_stream(self.device)
+
+        def wrap(step, fn):
+            def run(env, s):
+                st = self.comm_stream if (step.coll and self.comm_stream is not None) else compute
+                e0 = torch.cuda.Event(enable_timing=True)
+                e1 = torch.cuda.Event(enable_timing=True)
+                e0.record(st)
+                out = fn(env, s)
+                e1.record(st)
+                marks.append((step.ins.id, step.ins.opcode.value,
+                              "comm" if st is not compute else "compute", e0, e1))
+                return out
+            return run
+
+        for s, f in zip(self.steps, orig):
+            s.fn = wrap(s, f)
+        try:
+            t0 = torch.cuda.Event(enable_timing=True)
+            t0.record(compute)
+            self.run(inputs)
+            torch.cuda.synchronize(self.device)
+        finally:
+            for s, f in zip(self.steps, orig):
+                s.fn = f
+        return [{"id": i, "op": o, "stream": st, "start_ms": t0.elapsed_time(a),
+                 "end_ms": t0.elapsed_time(b)} for i, o, st, a, b in marks]
+
     def capture(self, inputs):
         """Capture one execution into a CUDA graph (after an eager warm-up
         run that materialises constants, communicators and kernel attributes).
