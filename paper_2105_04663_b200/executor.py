@@ -176,7 +176,9 @@ class Executor:
         self.comm_stream = None
         if self.overlap:
             self.steps = self._hoist_collectives(self.steps)
-            self.comm_stream = torch.cuda.Stream(device=self.device)
+            import os
+            prio = int(os.environ.get("SPMD_COMM_PRIORITY", "0"))
+            self.comm_stream = torch.cuda.Stream(device=self.device, priority=prio)
             # Leave SMs for the collective kernels that run under the GEMMs
             # (SPMD_COMM_SMS, default 0 = let the GEMM take every SM).
             import os
