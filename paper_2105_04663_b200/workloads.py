@@ -116,12 +116,15 @@ def moe_layer(n, E=8, B=8, S=8, C=4, M=8, H=16, dtype=DType.F32, seed=0, with_in
     comb = b.parameter(Shape((B, S, E, C), dtype), sharding=ms(4, [0, -1, -1, -1]), id="combine")
     wi = b.parameter(Shape((E, M, H), dtype), sharding=ms(3, [0, -1, -1]), id="wi")
     wo = b.parameter(Shape((E, H, M), dtype), sharding=ms(3, [0, -1, -1]), id="wo")
-    dsp = _dot(b, disp, x, (0,), (0,), (1,), (1,), id="dispatched")
+    # GShard annotations on the einsum outputs: dispatch result batch-sharded,
+    # expert FFN expert-sharded (the reshard between them is the all-to-all).
+    dsp = _dot(b, disp, x, (0,), (0,), (1,), (1,), sharding=ms(4, [0, -1, -1, -1]),
+               id="dispatched")
     ebcm = b.add(Op.TRANSPOSE, [dsp], {"permutation": (1, 0, 2, 3)}, id="ebcm_b")
     ebcm_e = b.add(Op.RELU, [ebcm], sharding=ms(4, [0, -1, -1, -1]), id="ebcm_e")
-    h = _dot(b, ebcm_e, wi, (0,), (0,), (3,), (1,), id="h")
+    h = _dot(b, ebcm_e, wi, (0,), (0,), (3,), (1,), sharding=ms(4, [0, -1, -1, -1]), id="h")
     a = b.add(Op.RELU, [h], id="a")
-    y = _dot(b, a, wo, (0,), (0,), (3,), (1,), id="y")
+    y = _dot(b, a, wo, (0,), (0,), (3,), (1,), sharding=ms(4, [0, -1, -1, -1]), id="y")
     yb = b.add(Op.TRANSPOSE, [y], {"permutation": (1, 0, 2, 3)}, id="ebcm_bsh")
     yb2 = b.add(Op.RELU, [yb], sharding=ms(4, [0, -1, -1, -1]), id="ybe")
     out = _dot(b, comb, yb2, (0,), (0,), (2, 3), (1, 2), id="out")

@@ -345,12 +345,15 @@ def moe_layer(n, E, B, S, C, M, H, rng):
     comb = b.parameter(R.Shape((B, S, E, C)), sharding=ms(4, [0, -1, -1, -1]), id="combine")
     wi = b.parameter(R.Shape((E, M, H)), sharding=ms(3, [0, -1, -1]), id="wi")
     wo = b.parameter(R.Shape((E, H, M)), sharding=ms(3, [0, -1, -1]), id="wo")
-    dsp = _dot(b, disp, x, (0,), (0,), (1,), (1,), id="dispatched")          # [B,E,C,M]
+    dsp = _dot(b, disp, x, (0,), (0,), (1,), (1,), sharding=ms(4, [0, -1, -1, -1]),
+               id="dispatched")                                            # [B,E,C,M]
     ebcm = b.add(R.Op.TRANSPOSE, [dsp], {"permutation": (1, 0, 2, 3)}, id="ebcm_b")
     ebcm_e = b.add(R.Op.RELU, [ebcm], sharding=ms(4, [0, -1, -1, -1]), id="ebcm_e")
-    h = _dot(b, ebcm_e, wi, (0,), (0,), (3,), (1,), id="h")                # [E,B,C,H]
+    h = _dot(b, ebcm_e, wi, (0,), (0,), (3,), (1,), sharding=ms(4, [0, -1, -1, -1]),
+             id="h")                                                       # [E,B,C,H]
     a = b.add(R.Op.RELU, [h], id="a")
-    y = _dot(b, a, wo, (0,), (0,), (3,), (1,), id="y")                     # [E,B,C,M]
+    y = _dot(b, a, wo, (0,), (0,), (3,), (1,), sharding=ms(4, [0, -1, -1, -1]),
+             id="y")                                                       # [E,B,C,M]
     yb = b.add(R.Op.TRANSPOSE, [y], {"permutation": (1, 0, 2, 3)}, id="ebcm_bsh")
     yb2 = b.add(R.Op.RELU, [yb], sharding=ms(4, [0, -1, -1, -1]), id="ybe")
     out = _dot(b, comb, yb2, (0,), (0,), (2, 3), (1, 2), id="out")         # [B,S,M]
