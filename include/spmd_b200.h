@@ -163,6 +163,11 @@ int spmd_mask_range(spmd_tensor in, spmd_tensor offset, spmd_tensor fill, spmd_t
 int spmd_halo_window(const spmd_tensor* pieces, int npieces, int axis, spmd_tensor start,
                      int has_mask, spmd_tensor offset, spmd_tensor fill, int64_t low,
                      int64_t high, int has_low, spmd_tensor out, int64_t nparts, void* stream);
+/* Fused attention (executor fusion of Dot(q,k) -> softmax -> Dot(p,v)):
+ * q [B,S,N,D], k/v [B,T,N,D] bf16 -> out [B,N,S,D] = softmax(scale q.k^T) v,
+ * D in {64,128,256}; tcgen05 with S/O accumulators in TMEM. */
+int spmd_attention(spmd_tensor q, spmd_tensor k, spmd_tensor v, spmd_tensor out, float scale,
+                   int64_t nparts, void* stream);
 /* Row softmax over the last dim: out = exp(x - max) / sum(exp(x - max)). */
 int spmd_softmax_lastdim(spmd_tensor in, spmd_tensor out, int64_t nparts, void* stream);
 

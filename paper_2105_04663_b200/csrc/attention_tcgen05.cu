@@ -1,0 +1,360 @@
+// Fused attention on tcgen05: replaces the op chain
+//   logits = Dot(q, k)  [B,N,S,T]  ->  softmax over T  ->  ctx = Dot(probs, v)
+// of the partitioned Transformer layer (the executor recognises the chain),
+// never materialising the [B,N,S,T] logits/probabilities in HBM.
+//
+// One CTA per (128 query rows, head, batch); online softmax over 64-key tiles:
+//   warp 0     TMA producer: Q once (D/64 boxes), K_j/V_j into a 2-slot ring
+//   warp 1     MMA issuer:   S_j = Q K_j^T -> TMEM (double-buffered S),
+//                            O += P_j V_j  -> TMEM (O: D fp32 columns)
+//   warp 2     TMEM allocator
+//   warps 4-7  softmax/correction: row max/sum in fp32 (one row per thread),
+//              P_j (bf16) written to shared memory in the UMMA SW128 K-major
+//              layout, O rescaled in TMEM when the running max moves, final
+//              O / l -> bf16 staged in shared memory -> TMA bulk store.
+// Layouts: q [B,S,N,D], k/v [B,T,N,D] (the QKV projection outputs), out
+// [B,N,S,D] (the ctx Dot's output) -- all read/written with 4-D tensor maps,
+// the partition stack folded into B.  Numerics: exp2 on log2e-scaled fp32,
+// fp32 accumulation, P rounded to bf16 for the PV MMA.
+#include "tcgen05.cuh"
+
+#include <string.h>
+
+namespace spmd {
+
+template <int D>
+struct AttnSmem {
+  static constexpr int Q_BYTES = 128 * D * 2;
+  static constexpr int KV_TILE = 64 * D * 2;            // one K or V tile
+  static constexpr int SLOT = 2 * KV_TILE;              // K + V
+  static constexpr int P_BYTES = 128 * 64 * 2;
+  static constexpr int Q_OFF = 0;
+  static constexpr int KV_OFF = Q_BYTES;
+  static constexpr int P_OFF = KV_OFF + 2 * SLOT;
+  static constexpr int BAR_OFF = P_OFF + P_BYTES;
+  static constexpr int TOTAL = BAR_OFF + 256 + 1024;
+};
+
+struct AttnShape {
+  int S, T, N, Bp;     // Bp = partitions * batch
+  float scale_log2e;   // softmax scale * log2(e)
+};
+
+__device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, uint64_t* bar,
+                                            int c0, int c1, int c2, int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+      : "memory");
+}
+
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
+      "%11, %12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, "
+      "%29, %30, %31, %32};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),
+      "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]),
+      "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]),
+      "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]),
+      "r"(r[29]), "r"(r[30]), "r"(r[31]));
+}
+
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+template <int D>
+__global__ void __launch_bounds__(256, 1)
+    attention_tcgen05(const __grid_constant__ CUtensorMap map_q,
+                      const __grid_constant__ CUtensorMap map_k,
+                      const __grid_constant__ CUtensorMap map_v,
+                      const __grid_constant__ CUtensorMap map_o, AttnShape g) {
+  typedef AttnSmem<D> L;
+  constexpr int DC = D / 64;                  // 64-wide D chunks
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint64_t* bars = (uint64_t*)(smem + L::BAR_OFF);
+  uint64_t* q_full = bars + 0;
+  uint64_t* kv_full = bars + 1;     // [2]
+  uint64_t* kv_empty = bars + 3;    // [2]
+  uint64_t* s_full = bars + 5;      // [2]
+  uint64_t* s_free = bars + 7;      // [2]
+  uint64_t* p_full = bars + 9;
+  uint64_t* pv_done = bars + 10;
+  uint32_t* tmem_slot = (uint32_t*)(bars + 11);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int st = blockIdx.x % ((g.S + 127) / 128);
+  const int rest = blockIdx.x / ((g.S + 127) / 128);
+  const int n = rest % g.N, b = rest / g.N;
+  const int nT = (g.T + 63) / 64;
+
+  if (threadIdx.x == 0) {
+    mbar_init(q_full, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&kv_full[i], 1);
+      mbar_init(&kv_empty[i], 1);
+      mbar_init(&s_full[i], 1);
+      mbar_init(&s_free[i], 4);
+    }
+    mbar_init(p_full, 4);
+    mbar_init(pv_done, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                     smem_u32(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t O_COL = 0, S_COL = 256;   // S buffers at 256 and 320
+
+  uint8_t* sq = smem + L::Q_OFF;
+  uint8_t* skv = smem + L::KV_OFF;
+  uint8_t* sp = smem + L::P_OFF;
+
+  if (warp == 0 && lane == 0) {
+    // ---------------- producer ----------------
+    mbar_expect_tx(q_full, L::Q_BYTES);
+#pragma unroll
+    for (int c = 0; c < DC; ++c) tma_load_4d(sq + c * 16384, &map_q, q_full, c * 64, st * 128, n, b);
+    for (int j = 0; j < nT; ++j) {
+      const int slot = j & 1;
+      mbar_wait(&kv_empty[slot], ((j >> 1) & 1) ^ 1);
+      uint8_t* kk = skv + slot * L::SLOT;
+      uint8_t* vv = kk + L::KV_TILE;
+      mbar_expect_tx(&kv_full[slot], L::SLOT);
+#pragma unroll
+      for (int c = 0; c < DC; ++c) {
+        tma_load_4d(kk + c * 8192, &map_k, &kv_full[slot], c * 64, j * 64, n, b);
+        tma_load_4d(vv + c * 8192, &map_v, &kv_full[slot], c * 64, j * 64, n, b);
+      }
+    }
+  } else if (warp == 1 && lane == 0) {
+    // ---------------- MMA issuer ----------------
+    const uint32_t idesc_s = make_idesc(128, 64, 0, 0);
+    const uint32_t idesc_o = make_idesc(128, D, 0, 1);
+    mbar_wait(q_full, 0);
+    auto issue_s = [&](int j) {
+      const int slot = j & 1;
+      mbar_wait(&kv_full[slot], (j >> 1) & 1);
+      if (j >= 2) mbar_wait(&s_free[slot], ((j >> 1) - 1) & 1);
+      tc_fence_after();
+      const uint32_t qa = smem_u32(sq), ka = smem_u32(skv + slot * L::SLOT);
+#pragma unroll
+      for (int c = 0; c < DC; ++c)
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          tc_mma(tmem + S_COL + slot * 64, make_desc(qa + c * 16384 + k * 32, 16, 1024),
+                 make_desc(ka + c * 8192 + k * 32, 16, 1024), idesc_s, (c | k) != 0);
+      tc_commit(&s_full[slot]);
+    };
+    auto issue_pv = [&](int j) {
+      const int slot = j & 1;
+      mbar_wait(p_full, j & 1);
+      tc_fence_after();
+      const uint32_t pa = smem_u32(sp), va = smem_u32(skv + slot * L::SLOT + L::KV_TILE);
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        tc_mma(tmem + O_COL, make_desc(pa + k * 32, 16, 1024),
+               make_desc(va + k * 2048, 8192, 1024), idesc_o, (j | k) != 0);
+      tc_commit(pv_done);
+      tc_commit(&kv_empty[slot]);
+    };
+    issue_s(0);
+    for (int j = 1; j < nT; ++j) {
+      issue_s(j);
+      issue_pv(j - 1);
+    }
+    issue_pv(nT - 1);
+  } else if (warp >= 4) {
+    // ---------------- softmax / correction / epilogue ----------------
+    const int ew = warp - 4;
+    const int row = ew * 32 + lane;
+    const uint32_t lane_base = (uint32_t)(ew * 32) << 16;
+    const int srow = st * 128 + row;
+    (void)srow;
+    float m = -INFINITY, l = 0.f;
+    for (int j = 0; j < nT; ++j) {
+      const int slot = j & 1;
+      mbar_wait(&s_full[slot], (j >> 1) & 1);
+      tc_fence_after();
+      uint32_t r0[32], r1[32];
+      tmem_ld32(tmem + lane_base + S_COL + slot * 64, r0);
+      tmem_ld32(tmem + lane_base + S_COL + slot * 64 + 32, r1);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&s_free[slot]);
+      float s[64];
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        s[i] = __uint_as_float(r0[i]) * g.scale_log2e;
+        s[32 + i] = __uint_as_float(r1[i]) * g.scale_log2e;
+      }
+      const int valid = g.T - j * 64;          // mask keys beyond T
+      float mx = m;
+#pragma unroll
+      for (int i = 0; i < 64; ++i) {
+        if (i >= valid) s[i] = -INFINITY;
+        mx = fmaxf(mx, s[i]);
+      }
+      const float mb = mx == -INFINITY ? 0.f : mx;
+      const float alpha = ex2(m - mb);         // m == -inf on the first tile -> 0
+      float rs = 0.f;
+#pragma unroll
+      for (int i = 0; i < 64; ++i) {
+        s[i] = ex2(s[i] - mb);
+        rs += s[i];
+      }
+      l = l * alpha + rs;
+      m = mx;
+      // PV_{j-1} must be done: O is stable and the P buffer is free.
+      if (j > 0) {
+        mbar_wait(pv_done, (j - 1) & 1);
+        tc_fence_after();
+        if (__any_sync(0xffffffffu, alpha != 1.f)) {
+#pragma unroll 1
+          for (int c = 0; c < D; c += 32) {
+            uint32_t o[32];
+            tmem_ld32(tmem + lane_base + O_COL + c, o);
+#pragma unroll
+            for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
+            tmem_st32(tmem + lane_base + O_COL + c, o);
+          }
+          asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        }
+      }
+      // P_j (bf16) -> smem, SW128 K-major rows of 64 keys.
+      uint8_t* prow = sp + row * 128;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        uint4 v;
+        __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&v);
+#pragma unroll
+        for (int t = 0; t < 4; ++t) h[t] = __floats2bfloat162_rn(s[q * 8 + 2 * t], s[q * 8 + 2 * t + 1]);
+        *reinterpret_cast<uint4*>(prow + ((q ^ (row & 7)) << 4)) = v;
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(p_full);
+    }
+    // Final: O / l -> bf16 -> smem (Q area, SW128 chunks) -> TMA store.
+    mbar_wait(pv_done, (nT - 1) & 1);
+    tc_fence_after();
+    const float inv = l > 0.f ? 1.f / l : 0.f;
+#pragma unroll 1
+    for (int c = 0; c < D; c += 32) {
+      uint32_t o[32];
+      tmem_ld32(tmem + lane_base + O_COL + c, o);
+      uint8_t* orow = sq + (c / 64) * 16384 + row * 128;
+      const int qbase = (c % 64) / 8;          // 16-B chunk index within the 128-B row
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        uint4 v;
+        __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&v);
+#pragma unroll
+        for (int t = 0; t < 4; ++t)
+          h[t] = __floats2bfloat162_rn(__uint_as_float(o[q * 8 + 2 * t]) * inv,
+                                       __uint_as_float(o[q * 8 + 2 * t + 1]) * inv);
+        *reinterpret_cast<uint4*>(orow + (((qbase + q) ^ (row & 7)) << 4)) = v;
+      }
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("bar.sync 1, 128;" ::: "memory");
+    if (threadIdx.x == 128) {
+#pragma unroll
+      for (int c = 0; c < DC; ++c)
+        asm volatile(
+            "cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%2, %3, %4, %5}], [%1];" ::
+                "l"(reinterpret_cast<uint64_t>(&map_o)),
+            "r"(smem_u32(sq + c * 16384)), "r"(c * 64), "r"(st * 128), "r"(n), "r"(b)
+            : "memory");
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      bulk_wait_all();
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+  }
+}
+
+// 4-D bf16 map with SW128: dims (D, rows, heads, batch) with element strides.
+static bool encode4(CUtensorMap* map, void* base, int64_t d, int64_t rows, int64_t heads,
+                    int64_t batch, int64_t st_row, int64_t st_head, int64_t st_batch,
+                    int box_rows) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn || (reinterpret_cast<uintptr_t>(base) & 15)) return false;
+  cuuint64_t dims[4] = {(cuuint64_t)d, (cuuint64_t)rows, (cuuint64_t)heads, (cuuint64_t)batch};
+  cuuint64_t strides[3] = {(cuuint64_t)st_row * 2, (cuuint64_t)st_head * 2,
+                           (cuuint64_t)st_batch * 2};
+  for (int i = 0; i < 3; ++i)
+    if (strides[i] % 16) return false;
+  cuuint32_t box[4] = {64, (cuuint32_t)box_rows, 1, 1};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  return fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, base, dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
+         CUDA_SUCCESS;
+}
+
+template <int D>
+static int launch_attention(const CUtensorMap& mq, const CUtensorMap& mk, const CUtensorMap& mv,
+                            const CUtensorMap& mo, AttnShape g, cudaStream_t s) {
+  typedef AttnSmem<D> L;
+  static bool configured = false;
+  if (!configured) {
+    SPMD_CUDA_TRY(cudaFuncSetAttribute(attention_tcgen05<D>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, L::TOTAL));
+    configured = true;
+  }
+  const int64_t grid = (int64_t)((g.S + 127) / 128) * g.N * g.Bp;
+  attention_tcgen05<D><<<(unsigned)grid, 256, L::TOTAL, s>>>(mq, mk, mv, mo, g);
+  return launched(s);
+}
+
+}  // namespace spmd
+
+using namespace spmd;
+
+// q [B,S,N,D], k/v [B,T,N,D] -> out [B,N,S,D] = softmax(scale * q.k^T) . v
+extern "C" int spmd_attention(spmd_tensor q, spmd_tensor k, spmd_tensor v, spmd_tensor out,
+                              float scale, int64_t nparts, void* stream) {
+  SPMD_CHECK_ARG(q.dtype == SPMD_BF16 && k.dtype == SPMD_BF16 && v.dtype == SPMD_BF16 &&
+                     out.dtype == SPMD_BF16 && q.rank == 4 && k.rank == 4 && v.rank == 4 &&
+                     out.rank == 4,
+                 "attention expects bf16 q[B,S,N,D], k/v[B,T,N,D], out[B,N,S,D]");
+  const int64_t B = q.dims[0], S = q.dims[1], N = q.dims[2], D = q.dims[3], T = k.dims[1];
+  SPMD_CHECK_ARG(k.dims[0] == B && k.dims[2] == N && k.dims[3] == D && v.dims[0] == B &&
+                     v.dims[1] == T && v.dims[2] == N && v.dims[3] == D && out.dims[0] == B &&
+                     out.dims[1] == N && out.dims[2] == S && out.dims[3] == D,
+                 "attention shape mismatch");
+  if (!(D == 64 || D == 128 || D == 256)) return SPMD_ERR_UNSUPPORTED;
+  const int64_t Bp = B * nparts;
+  CUtensorMap mq, mk, mv, mo;
+  bool ok = encode4(&mq, q.data, D, S, N, Bp, N * D, D, S * N * D, 128) &&
+            encode4(&mk, k.data, D, T, N, Bp, N * D, D, T * N * D, 64) &&
+            encode4(&mv, v.data, D, T, N, Bp, N * D, D, T * N * D, 64) &&
+            encode4(&mo, out.data, D, S, N, Bp, D, S * D, N * S * D, 128);
+  if (!ok) return SPMD_ERR_UNSUPPORTED;
+  AttnShape g;
+  g.S = (int)S;
+  g.T = (int)T;
+  g.N = (int)N;
+  g.Bp = (int)Bp;
+  g.scale_log2e = scale * 1.4426950408889634f;
+  cudaStream_t s = as_stream(stream);
+  if (D == 64) return launch_attention<64>(mq, mk, mv, mo, g, s);
+  if (D == 128) return launch_attention<128>(mq, mk, mv, mo, g, s);
+  return launch_attention<256>(mq, mk, mv, mo, g, s);
+}

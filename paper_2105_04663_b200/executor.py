@@ -288,6 +288,46 @@ class Executor:
                 self._fused_skip.add(ins.id)
                 self._fused[relu.id] = ("dot_relu" if ins.opcode == Op.DOT else "conv_relu", ins)
         self._plan_halo_windows(users, outs)
+        self._plan_attention(users, outs)
+
+    def _plan_attention(self, users, outs):
+        """Dot(q,k) -> fused softmax -> Dot(probs, v) with the Transformer
+        layouts q/k/v [B,S|T,N,D], logits [B,N,S,T], ctx [B,N,S,D] -> one
+        flash-attention kernel (tcgen05; no logits in HBM)."""
+        import os
+        if os.environ.get("SPMD_FUSED_ATTENTION", "1") == "0":
+            return
+        by = self.by_id
+        for div_id, spec in list(self._fused.items()):
+            if spec[0] != "softmax" or div_id in outs:
+                continue
+            logits = by[spec[1]]
+            if logits.opcode != Op.DOT or logits.shape.dtype != DType.BF16:
+                continue
+            a = logits.attrs
+            if (tuple(a["lhs_batch"]), tuple(a["rhs_batch"]), tuple(a["lhs_contracting"]),
+                    tuple(a["rhs_contracting"])) != ((0, 2), (0, 2), (3,), (3,)):
+                continue
+            u = users.get(div_id, [])
+            if len(u) != 1 or by[u[0]].opcode != Op.DOT:
+                continue
+            ctx = by[u[0]]
+            c = ctx.attrs
+            if ctx.operands[0] != div_id or (tuple(c["lhs_batch"]), tuple(c["rhs_batch"]),
+                                             tuple(c["lhs_contracting"]),
+                                             tuple(c["rhs_contracting"])) != \
+                    ((0, 1), (0, 2), (3,), (1,)):
+                continue
+            if any(x != spec[1] and x not in self._fused_skip
+                   for x in users.get(logits.id, [])) or logits.id in outs:
+                continue
+            q, k = logits.operands
+            v = ctx.operands[1]
+            qs, ks, vs = self._shape(q), self._shape(k), self._shape(v)
+            if qs.rank != 4 or ks.dims != vs.dims or qs.dims[3] not in (64, 128, 256):
+                continue
+            self._fused_skip.update({logits.id, div_id})
+            self._fused[ctx.id] = ("attention", q, k, v)
 
     def _plan_halo_windows(self, users, outs):
         """dynamic-slice(mask(concat(left, shard, right))) -> one halo-window
@@ -461,6 +501,8 @@ class Executor:
             return (f[1],)
         if f[0] == "mask":
             return (f[1], f[2], f[3])
+        if f[0] == "attention":
+            return f[1:]
         if f[0] == "halo":
             mask = f[4]
             return tuple(f[1]) + (f[3],) + ((mask[2], mask[3]) if mask is not None else ())
@@ -486,6 +528,16 @@ class Executor:
             return self._dot_step(f[1], shp, epilogue=1)
         if f is not None and f[0] == "conv_relu":
             return self._conv_step(f[1], epilogue=1)
+        if f is not None and f[0] == "attention":
+            _, q, k, v = f
+            qs, ks, vs = self._shape(q), self._shape(k), self._shape(v)
+
+            def run(env, s):
+                out = self._alloc(shp)
+                C.check(lib.spmd_attention(desc(env[q], qs), desc(env[k], ks), desc(env[v], vs),
+                                           desc(out, shp), 1.0, P, s), "attention")
+                return out
+            return run
         if f is not None and f[0] == "halo":
             _, pieces, axis, start, mask = f
             psh = [self._shape(x) for x in pieces]
