@@ -88,8 +88,28 @@ def softmax():
                       "gbs": 2 * x.numel() * 2 / ms / 1e6, "max_err": err}), flush=True)
 
 
+def attention():
+    lib = C.lib()
+    B, S, N, D = 16, 1024, 128, 256
+    q = torch.randn((1, B, S, N, D), device="cuda", dtype=torch.bfloat16)
+    k = torch.randn_like(q)
+    v = torch.randn_like(q)
+    o = torch.empty((1, B, N, S, D), device="cuda", dtype=torch.bfloat16)
+    st = torch.cuda.current_stream().cuda_stream
+    qd = desc(q, Shape((B, S, N, D), DType.BF16))
+    kd = desc(k, Shape((B, S, N, D), DType.BF16))
+    vd = desc(v, Shape((B, S, N, D), DType.BF16))
+    od = desc(o, Shape((B, N, S, D), DType.BF16))
+    ms = timeit(lambda: C.check(lib.spmd_attention(qd, kd, vd, od, 0.0625, 1, st), "attn"))
+    flops = 4.0 * B * N * S * S * D
+    print(json.dumps({"kernel": "attention_tcgen05", "case": "C2 attention B16 S1024 N128 D256",
+                      "ms": ms, "tflops": flops / ms / 1e9}), flush=True)
+
+
 if __name__ == "__main__":
     what = sys.argv[1] if len(sys.argv) > 1 else "all"
+    if what in ("attention", "all"):
+        attention()
     if what in ("softmax", "all"):
         softmax()
     if what in ("gemm", "all"):
