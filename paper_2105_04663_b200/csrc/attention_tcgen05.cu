@@ -27,11 +27,11 @@ struct AttnSmem {
   static constexpr int Q_BYTES = 128 * D * 2;
   static constexpr int KV_TILE = 64 * D * 2;            // one K or V tile
   static constexpr int SLOT = 2 * KV_TILE;              // K + V
-  static constexpr int P_BYTES = 128 * 64 * 2;
+  static constexpr int P_BYTES = 128 * 64 * 2;          // one P buffer (2 used)
   static constexpr int Q_OFF = 0;
   static constexpr int KV_OFF = Q_BYTES;
   static constexpr int P_OFF = KV_OFF + 2 * SLOT;
-  static constexpr int BAR_OFF = P_OFF + P_BYTES;
+  static constexpr int BAR_OFF = P_OFF + 2 * P_BYTES;
   static constexpr int TOTAL = BAR_OFF + 256 + 1024;
 };
 
@@ -83,9 +83,9 @@ __global__ void __launch_bounds__(256, 1)
   uint64_t* kv_empty = bars + 3;    // [2]
   uint64_t* s_full = bars + 5;      // [2]
   uint64_t* s_free = bars + 7;      // [2]
-  uint64_t* p_full = bars + 9;
-  uint64_t* pv_done = bars + 10;
-  uint32_t* tmem_slot = (uint32_t*)(bars + 11);
+  uint64_t* p_full = bars + 9;      // [2] per P buffer
+  uint64_t* pv_done = bars + 11;    // [2] per P buffer
+  uint32_t* tmem_slot = (uint32_t*)(bars + 13);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int st = blockIdx.x % ((g.S + 127) / 128);
@@ -100,9 +100,9 @@ __global__ void __launch_bounds__(256, 1)
       mbar_init(&kv_empty[i], 1);
       mbar_init(&s_full[i], 1);
       mbar_init(&s_free[i], 4);
+      mbar_init(&p_full[i], 4);
+      mbar_init(&pv_done[i], 1);
     }
-    mbar_init(p_full, 4);
-    mbar_init(pv_done, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 2) {
@@ -157,15 +157,16 @@ __global__ void __launch_bounds__(256, 1)
       tc_commit(&s_full[slot]);
     };
     auto issue_pv = [&](int j) {
-      const int slot = j & 1;
-      mbar_wait(p_full, j & 1);
+      const int slot = j & 1;           // K/V slot == P buffer index
+      mbar_wait(&p_full[slot], (j >> 1) & 1);
       tc_fence_after();
-      const uint32_t pa = smem_u32(sp), va = smem_u32(skv + slot * L::SLOT + L::KV_TILE);
+      const uint32_t pa = smem_u32(sp + slot * L::P_BYTES);
+      const uint32_t va = smem_u32(skv + slot * L::SLOT + L::KV_TILE);
 #pragma unroll
       for (int k = 0; k < 4; ++k)
         tc_mma(tmem + O_COL, make_desc(pa + k * 32, 16, 1024),
                make_desc(va + k * 2048, 8192, 1024), idesc_o, (j | k) != 0);
-      tc_commit(pv_done);
+      tc_commit(&pv_done[slot]);
       tc_commit(&kv_empty[slot]);
     };
     issue_s(0);
@@ -199,14 +200,25 @@ __global__ void __launch_bounds__(256, 1)
         s[32 + i] = __uint_as_float(r1[i]) * g.scale_log2e;
       }
       const int valid = g.T - j * 64;          // mask keys beyond T
-      float mx = m;
+      float mx = -INFINITY;
 #pragma unroll
       for (int i = 0; i < 64; ++i) {
         if (i >= valid) s[i] = -INFINITY;
         mx = fmaxf(mx, s[i]);
       }
-      const float mb = mx == -INFINITY ? 0.f : mx;
-      const float alpha = ex2(m - mb);         // m == -inf on the first tile -> 0
+      // Conditional rescaling (log2 domain): keep the reference max m unless
+      // this tile exceeds it by more than 2^8; exp2(s - m) then stays <= 256
+      // and the final O / l is unchanged mathematically.
+      float alpha = 1.f;
+      bool resc = false;
+      if (m == -INFINITY) {
+        m = mx;                                  // first finite max: nothing in O yet
+      } else if (mx > m + 8.f) {
+        alpha = ex2(m - mx);
+        m = mx;
+        resc = true;
+      }
+      const float mb = m == -INFINITY ? 0.f : m;
       float rs = 0.f;
 #pragma unroll
       for (int i = 0; i < 64; ++i) {
@@ -214,25 +226,25 @@ __global__ void __launch_bounds__(256, 1)
         rs += s[i];
       }
       l = l * alpha + rs;
-      m = mx;
-      // PV_{j-1} must be done: O is stable and the P buffer is free.
-      if (j > 0) {
-        mbar_wait(pv_done, (j - 1) & 1);
+      const int pb = j & 1;
+      // P buffer pb was last read by PV_{j-2}.
+      if (j >= 2) mbar_wait(&pv_done[pb], ((j >> 1) - 1) & 1);
+      // O rescale needs every earlier PV (PV_{j-1}) complete.
+      if (j > 0 && __any_sync(0xffffffffu, resc)) {
+        mbar_wait(&pv_done[pb ^ 1], ((j - 1) >> 1) & 1);
         tc_fence_after();
-        if (__any_sync(0xffffffffu, alpha != 1.f)) {
 #pragma unroll 1
-          for (int c = 0; c < D; c += 32) {
-            uint32_t o[32];
-            tmem_ld32(tmem + lane_base + O_COL + c, o);
+        for (int c = 0; c < D; c += 32) {
+          uint32_t o[32];
+          tmem_ld32(tmem + lane_base + O_COL + c, o);
 #pragma unroll
-            for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
-            tmem_st32(tmem + lane_base + O_COL + c, o);
-          }
-          asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+          for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
+          tmem_st32(tmem + lane_base + O_COL + c, o);
         }
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
       }
       // P_j (bf16) -> smem, SW128 K-major rows of 64 keys.
-      uint8_t* prow = sp + row * 128;
+      uint8_t* prow = sp + pb * L::P_BYTES + row * 128;
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
         uint4 v;
@@ -244,10 +256,10 @@ __global__ void __launch_bounds__(256, 1)
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(p_full);
+      if (lane == 0) mbar_arrive(&p_full[pb]);
     }
     // Final: O / l -> bf16 -> smem (Q area, SW128 chunks) -> TMA store.
-    mbar_wait(pv_done, (nT - 1) & 1);
+    mbar_wait(&pv_done[(nT - 1) & 1], ((nT - 1) >> 1) & 1);
     tc_fence_after();
     const float inv = l > 0.f ? 1.f / l : 0.f;
 #pragma unroll 1
