@@ -301,6 +301,300 @@ __global__ void __launch_bounds__(256, 1)
   }
 }
 
+// ---------------------------------------------------------------------------
+// CTA-pair variant (cta_group::2, UMMA M=256): the pair owns 256 query rows
+// (128 per CTA) and splits every K tile by keys (32 per CTA) and every V tile
+// by head-dim columns (D/2 per CTA), so each K/V byte crosses L2->SMEM once
+// per 256 query rows -- the single-CTA kernel is L2-bandwidth bound at D=256.
+// Leader CTA issues the MMAs; S and O land in each CTA's own TMEM half;
+// softmax/P/correction/store run in both CTAs on their own rows.
+// ---------------------------------------------------------------------------
+constexpr uint32_t A_PEER_MASK = 0xFEFFFFFFu;
+
+__device__ __forceinline__ uint32_t a_cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void a_cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::
+                   : "memory");
+}
+__device__ __forceinline__ void tma_load_4d_2sm(void* dst, const CUtensorMap* map, uint64_t* bar,
+                                                int c0, int c1, int c2, int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar) & A_PEER_MASK), "r"(c0), "r"(c1),
+      "r"(c2), "r"(c3)
+      : "memory");
+}
+__device__ __forceinline__ void a_commit_mc(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], %1;" ::"r"(smem_u32(bar)),
+      "h"((uint16_t)3)
+      : "memory");
+}
+__device__ __forceinline__ void a_mma_2sm(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc,
+                                          uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void arrive_leader(uint64_t* bar) {
+  asm volatile(
+      "{\n.reg .b32 ra;\nmapa.shared::cluster.u32 ra, %0, 0;\n"
+      "mbarrier.arrive.shared::cluster.b64 _, [ra];\n}" ::"r"(smem_u32(bar))
+      : "memory");
+}
+
+template <int D>
+struct Attn2Smem {
+  static constexpr int Q_BYTES = 128 * D * 2;           // own 128 rows
+  static constexpr int K_HALF = 32 * D * 2;             // 32 keys x D
+  static constexpr int V_HALF = 64 * (D / 2) * 2;       // 64 keys x D/2
+  static constexpr int SLOT = K_HALF + V_HALF;
+  static constexpr int STAGES = 3;
+  static constexpr int P_BYTES = 128 * 64 * 2;
+  static constexpr int KV_OFF = Q_BYTES;
+  static constexpr int P_OFF = KV_OFF + STAGES * SLOT;
+  static constexpr int BAR_OFF = P_OFF + 2 * P_BYTES;
+  static constexpr int TOTAL = BAR_OFF + 512 + 1024;
+};
+
+template <int D>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
+    attention_tcgen05_2sm(const __grid_constant__ CUtensorMap map_q,
+                          const __grid_constant__ CUtensorMap map_k,
+                          const __grid_constant__ CUtensorMap map_v,
+                          const __grid_constant__ CUtensorMap map_o, AttnShape g) {
+  typedef Attn2Smem<D> L;
+  constexpr int DC = D / 64, NS = L::STAGES;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint64_t* bars = (uint64_t*)(smem + L::BAR_OFF);
+  uint64_t* q_full = bars + 0;
+  uint64_t* kv_full = bars + 1;            // [NS] leader
+  uint64_t* kv_empty = kv_full + NS;       // [NS] both (multicast)
+  uint64_t* s_full = kv_empty + NS;        // [2] both (multicast)
+  uint64_t* s_free = s_full + 2;           // [2] leader, 8 arrivals
+  uint64_t* p_full = s_free + 2;           // [2] leader, 8 arrivals
+  uint64_t* pv_done = p_full + 2;          // [2] both (multicast)
+  uint32_t* tmem_slot = (uint32_t*)(pv_done + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = a_cluster_rank();
+  const bool leader = rank == 0;
+  const int nSt = (g.S + 255) / 256;
+  const int cl = blockIdx.x >> 1;
+  const int st = cl % nSt;
+  const int rest = cl / nSt;
+  const int n = rest % g.N, b = rest / g.N;
+  const int nT = (g.T + 63) / 64;
+  const int row0 = st * 256 + rank * 128;
+
+  if (threadIdx.x == 0) {
+    mbar_init(q_full, 1);
+    for (int i = 0; i < NS; ++i) {
+      mbar_init(&kv_full[i], 1);
+      mbar_init(&kv_empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&s_full[i], 1);
+      mbar_init(&s_free[i], 8);
+      mbar_init(&p_full[i], 8);
+      mbar_init(&pv_done[i], 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                     smem_u32(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  tc_fence_before();
+  a_cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t O_COL = 0, S_COL = 256;
+  uint8_t* sq = smem;
+  uint8_t* skv = smem + L::KV_OFF;
+  uint8_t* sp = smem + L::P_OFF;
+
+  if (warp == 0 && lane == 0) {
+    if (leader) mbar_expect_tx(q_full, 2 * L::Q_BYTES);
+#pragma unroll
+    for (int c = 0; c < DC; ++c)
+      tma_load_4d_2sm(sq + c * 16384, &map_q, q_full, c * 64, row0, n, b);
+    for (int j = 0; j < nT; ++j) {
+      const int slot = j % NS;
+      mbar_wait(&kv_empty[slot], ((j / NS) & 1) ^ 1);
+      uint8_t* kk = skv + slot * L::SLOT;
+      uint8_t* vv = kk + L::K_HALF;
+      if (leader) mbar_expect_tx(&kv_full[slot], 2 * L::SLOT);
+#pragma unroll
+      for (int c = 0; c < DC; ++c)
+        tma_load_4d_2sm(kk + c * 4096, &map_k, &kv_full[slot], c * 64, j * 64 + rank * 32, n, b);
+#pragma unroll
+      for (int c = 0; c < DC / 2; ++c)
+        tma_load_4d_2sm(vv + c * 8192, &map_v, &kv_full[slot], rank * (D / 2) + c * 64, j * 64, n,
+                        b);
+    }
+  } else if (warp == 1 && lane == 0 && leader) {
+    const uint32_t idesc_s = make_idesc(256, 64, 0, 0);
+    const uint32_t idesc_o = make_idesc(256, D, 0, 1);
+    mbar_wait(q_full, 0);
+    auto issue_s = [&](int j) {
+      const int slot = j % NS, sb = j & 1;
+      mbar_wait(&kv_full[slot], (j / NS) & 1);
+      if (j >= 2) mbar_wait(&s_free[sb], ((j >> 1) - 1) & 1);
+      tc_fence_after();
+      const uint32_t qa = smem_u32(sq), ka = smem_u32(skv + slot * L::SLOT);
+#pragma unroll
+      for (int c = 0; c < DC; ++c)
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          a_mma_2sm(tmem + S_COL + sb * 64, make_desc(qa + c * 16384 + k * 32, 16, 1024),
+                    make_desc(ka + c * 4096 + k * 32, 16, 1024), idesc_s, (c | k) != 0);
+      a_commit_mc(&s_full[sb]);
+    };
+    auto issue_pv = [&](int j) {
+      const int slot = j % NS, pb = j & 1;
+      mbar_wait(&p_full[pb], (j >> 1) & 1);
+      tc_fence_after();
+      const uint32_t pa = smem_u32(sp + pb * L::P_BYTES);
+      const uint32_t va = smem_u32(skv + slot * L::SLOT + L::K_HALF);
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        a_mma_2sm(tmem + O_COL, make_desc(pa + k * 32, 16, 1024),
+                  make_desc(va + k * 2048, 8192, 1024), idesc_o, (j | k) != 0);
+      a_commit_mc(&pv_done[pb]);
+      a_commit_mc(&kv_empty[slot]);
+    };
+    issue_s(0);
+    for (int j = 1; j < nT; ++j) {
+      issue_s(j);
+      issue_pv(j - 1);
+    }
+    issue_pv(nT - 1);
+  } else if (warp >= 4) {
+    const int ew = warp - 4;
+    const int row = ew * 32 + lane;
+    const uint32_t lane_base = (uint32_t)(ew * 32) << 16;
+    float m = -INFINITY, l = 0.f;
+    for (int j = 0; j < nT; ++j) {
+      const int sb = j & 1;
+      mbar_wait(&s_full[sb], (j >> 1) & 1);
+      tc_fence_after();
+      uint32_t r0[32], r1[32];
+      tmem_ld32(tmem + lane_base + S_COL + sb * 64, r0);
+      tmem_ld32(tmem + lane_base + S_COL + sb * 64 + 32, r1);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) arrive_leader(&s_free[sb]);
+      float s[64];
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        s[i] = __uint_as_float(r0[i]) * g.scale_log2e;
+        s[32 + i] = __uint_as_float(r1[i]) * g.scale_log2e;
+      }
+      const int valid = g.T - j * 64;
+      float mx = -INFINITY;
+#pragma unroll
+      for (int i = 0; i < 64; ++i) {
+        if (i >= valid) s[i] = -INFINITY;
+        mx = fmaxf(mx, s[i]);
+      }
+      float alpha = 1.f;
+      bool resc = false;
+      if (m == -INFINITY) {
+        m = mx;
+      } else if (mx > m + 8.f) {
+        alpha = ex2(m - mx);
+        m = mx;
+        resc = true;
+      }
+      const float mb = m == -INFINITY ? 0.f : m;
+      float rs = 0.f;
+#pragma unroll
+      for (int i = 0; i < 64; ++i) {
+        s[i] = ex2(s[i] - mb);
+        rs += s[i];
+      }
+      l = l * alpha + rs;
+      const int pb = j & 1;
+      if (j >= 2) mbar_wait(&pv_done[pb], ((j >> 1) - 1) & 1);
+      if (j > 0 && __any_sync(0xffffffffu, resc)) {
+        mbar_wait(&pv_done[pb ^ 1], ((j - 1) >> 1) & 1);
+        tc_fence_after();
+#pragma unroll 1
+        for (int c = 0; c < D; c += 32) {
+          uint32_t o[32];
+          tmem_ld32(tmem + lane_base + O_COL + c, o);
+#pragma unroll
+          for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
+          tmem_st32(tmem + lane_base + O_COL + c, o);
+        }
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      }
+      uint8_t* prow = sp + pb * L::P_BYTES + row * 128;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        uint4 v;
+        __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&v);
+#pragma unroll
+        for (int t = 0; t < 4; ++t) h[t] = __floats2bfloat162_rn(s[q * 8 + 2 * t], s[q * 8 + 2 * t + 1]);
+        *reinterpret_cast<uint4*>(prow + ((q ^ (row & 7)) << 4)) = v;
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) arrive_leader(&p_full[pb]);
+    }
+    mbar_wait(&pv_done[(nT - 1) & 1], ((nT - 1) >> 1) & 1);
+    tc_fence_after();
+    const float inv = l > 0.f ? 1.f / l : 0.f;
+#pragma unroll 1
+    for (int c = 0; c < D; c += 32) {
+      uint32_t o[32];
+      tmem_ld32(tmem + lane_base + O_COL + c, o);
+      uint8_t* orow = sq + (c / 64) * 16384 + row * 128;
+      const int qbase = (c % 64) / 8;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        uint4 v;
+        __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&v);
+#pragma unroll
+        for (int t = 0; t < 4; ++t)
+          h[t] = __floats2bfloat162_rn(__uint_as_float(o[q * 8 + 2 * t]) * inv,
+                                       __uint_as_float(o[q * 8 + 2 * t + 1]) * inv);
+        *reinterpret_cast<uint4*>(orow + (((qbase + q) ^ (row & 7)) << 4)) = v;
+      }
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("bar.sync 1, 128;" ::: "memory");
+    if (threadIdx.x == 128) {
+#pragma unroll
+      for (int c = 0; c < DC; ++c)
+        asm volatile(
+            "cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%2, %3, %4, %5}], [%1];" ::
+                "l"(reinterpret_cast<uint64_t>(&map_o)),
+            "r"(smem_u32(sq + c * 16384)), "r"(c * 64), "r"(row0), "r"(n), "r"(b)
+            : "memory");
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      bulk_wait_all();
+    }
+  }
+  tc_fence_before();
+  a_cluster_sync();
+  if (warp == 2) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+  }
+}
+
 // 4-D bf16 map with SW128: dims (D, rows, heads, batch) with element strides.
 static bool encode4(CUtensorMap* map, void* base, int64_t d, int64_t rows, int64_t heads,
                     int64_t batch, int64_t st_row, int64_t st_head, int64_t st_batch,
@@ -335,6 +629,22 @@ static int launch_attention(const CUtensorMap& mq, const CUtensorMap& mk, const 
   return launched(s);
 }
 
+template <int D>
+static int launch_attention_2sm(const CUtensorMap& mq, const CUtensorMap& mk,
+                                const CUtensorMap& mv, const CUtensorMap& mo, AttnShape g,
+                                cudaStream_t s) {
+  typedef Attn2Smem<D> L;
+  static bool configured = false;
+  if (!configured) {
+    SPMD_CUDA_TRY(cudaFuncSetAttribute(attention_tcgen05_2sm<D>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, L::TOTAL));
+    configured = true;
+  }
+  const int64_t grid = 2 * (int64_t)((g.S + 255) / 256) * g.N * g.Bp;
+  attention_tcgen05_2sm<D><<<(unsigned)grid, 256, L::TOTAL, s>>>(mq, mk, mv, mo, g);
+  return launched(s);
+}
+
 }  // namespace spmd
 
 using namespace spmd;
@@ -366,6 +676,18 @@ extern "C" int spmd_attention(spmd_tensor q, spmd_tensor k, spmd_tensor v, spmd_
   g.Bp = (int)Bp;
   g.scale_log2e = scale * 1.4426950408889634f;
   cudaStream_t s = as_stream(stream);
+  static int mode = -1;
+  if (mode < 0) {
+    const char* e = getenv("SPMD_ATTN_MODE");
+    mode = (e && strcmp(e, "1sm") == 0) ? 1 : 2;
+  }
+  if (mode == 2 && D >= 128) {
+    CUtensorMap mk2;   // K split by keys: 32-row boxes
+    if (encode4(&mk2, k.data, D, T, N, Bp, N * D, D, T * N * D, 32)) {
+      if (D == 128) return launch_attention_2sm<128>(mq, mk2, mv, mo, g, s);
+      return launch_attention_2sm<256>(mq, mk2, mv, mo, g, s);
+    }
+  }
   if (D == 64) return launch_attention<64>(mq, mk, mv, mo, g, s);
   if (D == 128) return launch_attention<128>(mq, mk, mv, mo, g, s);
   return launch_attention<256>(mq, mk, mv, mo, g, s);
