@@ -88,6 +88,76 @@ def softmax():
                       "gbs": 2 * x.numel() * 2 / ms / 1e6, "max_err": err}), flush=True)
 
 
+def datamove():
+    """HBM-bound kernels at C4/C5 sizes: GB/s = (bytes read + written) / time."""
+    lib = C.lib()
+    st = torch.cuda.current_stream().cuda_stream
+    bf = DType.BF16
+    # C4 halo window: 8-way H-sharded [8,128,1024,128] shard + 1-row halos ->
+    # masked window [8,130,1024,128] in one pass.
+    N, c, W, Ch = 8, 128, 1024, 128
+    val = torch.randn((1, N, c, W, Ch), device="cuda", dtype=torch.bfloat16)
+    lh = torch.randn((1, N, 1, W, Ch), device="cuda", dtype=torch.bfloat16)
+    rh = torch.randn_like(lh)
+    out = torch.empty((1, N, c + 2, W, Ch), device="cuda", dtype=torch.bfloat16)
+    start = torch.zeros((1,), dtype=torch.int32, device="cuda")
+    off = torch.full((1,), 3 * 128 - 1, dtype=torch.int32, device="cuda")
+    fill = torch.zeros((1,), dtype=torch.bfloat16, device="cuda")
+    pieces = (C.SpmdTensor * 3)(desc(lh, Shape((N, 1, W, Ch), bf)),
+                                desc(val, Shape((N, c, W, Ch), bf)),
+                                desc(rh, Shape((N, 1, W, Ch), bf)))
+    sh_s = Shape((), DType.S32)
+    ms = timeit(lambda: C.check(lib.spmd_halo_window(
+        pieces, 3, 1, desc(start, sh_s), 1, desc(off, sh_s), desc(fill, Shape((), bf)), 0, 1024,
+        1, desc(out, Shape((N, c + 2, W, Ch), bf)), 1, st), "halo"))
+    by = (val.numel() + 2 * lh.numel() + out.numel()) * 2
+    print(json.dumps({"kernel": "halo_window_kernel", "case": "C4 [8,128+2,1024,128] bf16",
+                      "ms": ms, "gbs": by / ms / 1e6}), flush=True)
+    # C5 uneven mask: [1001 -> 126 rows/shard, 524288] f32 range mask on the last shard.
+    rows, D1 = 126, 524288
+    x = torch.randn((1, rows, D1), device="cuda")
+    y = torch.empty_like(x)
+    off = torch.full((1,), 7 * 126, dtype=torch.int32, device="cuda")
+    fill = torch.full((1,), float("-inf"), device="cuda")
+    f32 = DType.F32
+    ms = timeit(lambda: C.check(lib.spmd_mask_range(
+        desc(x, Shape((rows, D1), f32)), desc(off, sh_s), desc(fill, Shape((), f32)),
+        desc(y, Shape((rows, D1), f32)), 0, 0, 1001, 0, 1, st), "mask"))
+    print(json.dumps({"kernel": "mask_range_kernel", "case": "C5 [126,524288] f32",
+                      "ms": ms, "gbs": 2 * x.numel() * 4 / ms / 1e6}), flush=True)
+    # C5 padded layout: pad [1001,524288] -> [1008,524288] f32 (localize).
+    x = torch.randn((1, 1001, D1), device="cuda")
+    y = torch.empty((1, 1008, D1), device="cuda")
+    z = torch.zeros((1,), device="cuda")
+    lo, hi, it = C.i64_array([0, 0]), C.i64_array([7, 0]), C.i64_array([0, 0])
+    ms = timeit(lambda: C.check(lib.spmd_pad(desc(x, Shape((1001, D1), f32)), desc(z, Shape((), f32)),
+                                             desc(y, Shape((1008, D1), f32)), lo, hi, it, 1, st),
+                                "pad"))
+    print(json.dumps({"kernel": "fill+strided_copy (pad)", "case": "C5 [1001->1008,524288] f32",
+                      "ms": ms, "gbs": (x.numel() + y.numel()) * 4 / ms / 1e6}), flush=True)
+    # dynamic-slice of the local shard out of the padded full value.
+    s0 = torch.full((1,), 126 * 3, dtype=torch.int32, device="cuda")
+    s1 = torch.zeros((1,), dtype=torch.int32, device="cuda")
+    y2 = torch.empty((1, 126, D1), device="cuda")
+    starts = (C.SpmdTensor * 2)(desc(s0, sh_s), desc(s1, sh_s))
+    ms = timeit(lambda: C.check(lib.spmd_dynamic_slice(desc(y, Shape((1008, D1), f32)), starts,
+                                                       desc(y2, Shape((126, D1), f32)), 1, st),
+                                "ds"))
+    print(json.dumps({"kernel": "strided_copy_kernel (dynamic-slice)",
+                      "case": "C5 [1008,524288] -> [126,524288] f32", "ms": ms,
+                      "gbs": 2 * y2.numel() * 4 / ms / 1e6}), flush=True)
+    # C2 transpose ctx [16,128,1024,256] -> [16,1024,128,256] bf16.
+    a = torch.randn((1, 16, 128, 1024, 256), device="cuda", dtype=torch.bfloat16)
+    b = torch.empty((1, 16, 1024, 128, 256), device="cuda", dtype=torch.bfloat16)
+    perm = C.i32_array([0, 2, 1, 3])
+    ms = timeit(lambda: C.check(lib.spmd_transpose(desc(a, Shape((16, 128, 1024, 256), bf)),
+                                                   desc(b, Shape((16, 1024, 128, 256), bf)), perm,
+                                                   1, st), "tr"))
+    print(json.dumps({"kernel": "strided_copy_kernel (transpose)",
+                      "case": "C2 ctx [16,128,1024,256] bf16", "ms": ms,
+                      "gbs": 2 * a.numel() * 2 / ms / 1e6}), flush=True)
+
+
 def attention():
     lib = C.lib()
     B, S, N, D = 16, 1024, 128, 256
@@ -108,6 +178,8 @@ def attention():
 
 if __name__ == "__main__":
     what = sys.argv[1] if len(sys.argv) > 1 else "all"
+    if what in ("datamove", "all"):
+        datamove()
     if what in ("attention", "all"):
         attention()
     if what in ("softmax", "all"):
