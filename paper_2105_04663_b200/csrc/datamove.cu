@@ -22,6 +22,21 @@ __global__ void strided_copy_kernel(const T* __restrict__ src, T* __restrict__ d
                                     int64_t nparts) {
   const I per = (I)(a.n / V);
   const I total = per * (I)nparts;
+  // Per-partition dynamic base offsets (clamped starts), computed once per
+  // block instead of re-reading the start scalars for every element.
+  __shared__ int64_t dyn_off[SPMD_MAX_PARTS];
+  if (a.ndyn) {
+    for (int p = threadIdx.x; p < nparts && p < SPMD_MAX_PARTS; p += blockDim.x) {
+      int64_t off = 0;
+      for (int k = 0; k < a.ndyn; ++k) {
+        int64_t s0 = a.dyn_start[k][p];
+        s0 = s0 < 0 ? 0 : (s0 > a.dyn_max[k] ? a.dyn_max[k] : s0);
+        off += s0 * a.dyn_mul[k];
+      }
+      dyn_off[p] = off;
+    }
+    __syncthreads();
+  }
   for (I idx = blockIdx.x * (I)blockDim.x + threadIdx.x; idx < total;
        idx += (I)gridDim.x * blockDim.x) {
     I p = idx / per;
@@ -39,12 +54,7 @@ __global__ void strided_copy_kernel(const T* __restrict__ src, T* __restrict__ d
       }
     }
     if (a.ndyn) {
-      int64_t off = 0;
-      for (int k = 0; k < a.ndyn; ++k) {
-        int64_t s0 = a.dyn_start[k][p];
-        s0 = s0 < 0 ? 0 : (s0 > a.dyn_max[k] ? a.dyn_max[k] : s0);
-        off += s0 * a.dyn_mul[k];
-      }
+      const int64_t off = dyn_off[p];
       if (a.dyn_on_dst) d0 += off; else so += off;
     }
     if (V == 1) {
@@ -73,13 +83,72 @@ __global__ void splat_kernel(const T* __restrict__ src, T* __restrict__ dst, Cop
   }
 }
 
-template <typename T>
+template <typename T, int V>
 __global__ void fill_kernel(T* __restrict__ out, const T* __restrict__ value, int64_t n,
                             int64_t nparts) {
-  const int64_t total = n * nparts;
+  const int64_t per = n / V, total = per * nparts;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
-       i += (int64_t)gridDim.x * blockDim.x)
-    out[i] = value[i / n];
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const T v = value[i / per];
+    if (V == 1) {
+      out[i] = v;
+    } else {
+      T f[V];
+#pragma unroll
+      for (int j = 0; j < V; ++j) f[j] = v;
+      *reinterpret_cast<uint4*>(out + i * V) = *reinterpret_cast<uint4*>(f);
+    }
+  }
+}
+
+// Edge padding without interior padding, in ONE pass: every output element
+// (or 16-byte group of the last dim) either reads its source element or takes
+// the partition's pad value.  Reads the input once and writes the output once
+// (the fill+copy formulation writes the interior twice).
+struct PadArgs {
+  int rank;
+  int64_t od[SPMD_MAX_RANK];   // output dims (last in units of V)
+  int64_t id[SPMD_MAX_RANK];   // input dims (last in units of V)
+  int64_t low[SPMD_MAX_RANK];  // low padding (last in units of V)
+  int64_t ist[SPMD_MAX_RANK];  // input strides in elements
+  int64_t spart, dpart, per;   // per-partition elements in/out; V-groups out
+};
+
+template <typename T, typename I, int V>
+__global__ void pad_gather_kernel(const T* __restrict__ src, const T* __restrict__ value,
+                                  T* __restrict__ dst, PadArgs a, int64_t nparts) {
+  const I per = (I)a.per;
+  const I total = per * (I)nparts;
+  for (I idx = blockIdx.x * (I)blockDim.x + threadIdx.x; idx < total;
+       idx += (I)gridDim.x * blockDim.x) {
+    const I p = idx / per;
+    I r = idx - p * per;
+    int64_t so = 0;
+    bool inside = true;
+#pragma unroll
+    for (int k = SPMD_MAX_RANK - 1; k >= 0; --k) {
+      if (k < a.rank) {
+        const I dk = (I)a.od[k];
+        const int64_t c = (int64_t)(r % dk) - a.low[k];
+        r /= dk;
+        inside = inside && c >= 0 && c < a.id[k];
+        so += c * a.ist[k];
+      }
+    }
+    T* out = dst + (int64_t)p * a.dpart + (int64_t)(idx - p * per) * V;
+    if (V == 1) {
+      *out = inside ? src[(int64_t)p * a.spart + so] : value[p];
+    } else if (inside) {
+      *reinterpret_cast<uint4*>(out) =
+          *reinterpret_cast<const uint4*>(src + (int64_t)p * a.spart + so * V);
+    } else {
+      const T v = value[p];
+      T f[V];
+#pragma unroll
+      for (int j = 0; j < V; ++j) f[j] = v;
+      *reinterpret_cast<uint4*>(out) = *reinterpret_cast<uint4*>(f);
+    }
+  }
 }
 
 // Merge dims contiguous in both views; drop unit dims.
@@ -112,6 +181,7 @@ int launch_copy(const void* src, void* dst, int dtype, CopyArgs a, int64_t npart
   a.n = 1;
   for (int k = 0; k < a.rank; ++k) a.n *= a.shape[k];
   if (a.n == 0 || nparts == 0) return SPMD_OK;
+  SPMD_CHECK_ARG(a.ndyn == 0 || nparts <= SPMD_MAX_PARTS, "too many partitions for dynamic offsets");
   canonicalize(a);
   const int es = elem_size(dtype);
   // 16-byte vector path: innermost dim unit-stride on both sides, all offsets
@@ -161,9 +231,16 @@ int launch_copy(const void* src, void* dst, int dtype, CopyArgs a, int64_t npart
 int launch_fill(void* out, const void* value, int dtype, int64_t n, int64_t nparts,
                 cudaStream_t s) {
   if (n == 0 || nparts == 0) return SPMD_OK;
-  SPMD_DISPATCH_BYTES(dtype, T,
-                      fill_kernel<T><<<grid_for(n * nparts, 256, 4), 256, 0, s>>>(
-                          (T*)out, (const T*)value, n, nparts));
+  const int V = 16 / elem_size(dtype);
+  const bool vec = n % V == 0 && (reinterpret_cast<uintptr_t>(out) & 15) == 0;
+  SPMD_DISPATCH_BYTES(dtype, T, {
+    if (vec)
+      fill_kernel<T, 16 / sizeof(T)><<<grid_for(n / V * nparts, 256), 256, 0, s>>>(
+          (T*)out, (const T*)value, n, nparts);
+    else
+      fill_kernel<T, 1><<<grid_for(n * nparts, 256, 4), 256, 0, s>>>(
+          (T*)out, (const T*)value, n, nparts);
+  });
   return launched(s);
 }
 
@@ -237,12 +314,80 @@ extern "C" int spmd_reverse(spmd_tensor in, spmd_tensor out, const int32_t* dims
   return launch_copy(in.data, out.data, out.dtype, a, nparts, as_stream(stream));
 }
 
+static int pad_edges(const spmd_tensor& in, const spmd_tensor& value, const spmd_tensor& out,
+                     const int64_t* low, const int64_t* high, int64_t nparts, cudaStream_t s) {
+  PadArgs a;
+  memset(&a, 0, sizeof(a));
+  // Merge runs of dims that carry no padding into their left neighbour's
+  // stride walk: only dims with padding (and the last dim) need coordinates.
+  int r = 0;
+  for (int k = 0; k < in.rank; ++k) {
+    SPMD_CHECK_ARG(low[k] >= 0 && high[k] >= 0, "negative padding");
+    SPMD_CHECK_ARG(out.dims[k] == in.dims[k] + low[k] + high[k], "pad output shape mismatch");
+    if (r > 0 && low[k] == 0 && high[k] == 0 && a.low[r - 1] == 0 && a.od[r - 1] == a.id[r - 1]) {
+      a.od[r - 1] *= out.dims[k];
+      a.id[r - 1] *= in.dims[k];
+      continue;
+    }
+    a.od[r] = out.dims[k];
+    a.id[r] = in.dims[k];
+    a.low[r] = low[k];
+    ++r;
+  }
+  a.rank = r;
+  int64_t acc = 1;
+  for (int k = r - 1; k >= 0; --k) {
+    a.ist[k] = acc;
+    acc *= a.id[k];
+  }
+  a.spart = numel(in);
+  a.dpart = numel(out);
+  const int V = 16 / elem_size(out.dtype);
+  const bool vec = a.id[r - 1] % V == 0 && a.low[r - 1] % V == 0 && a.od[r - 1] % V == 0 &&
+                   (reinterpret_cast<uintptr_t>(in.data) & 15) == 0 &&
+                   (reinterpret_cast<uintptr_t>(out.data) & 15) == 0;
+  if (vec) {
+    a.id[r - 1] /= V;
+    a.od[r - 1] /= V;
+    a.low[r - 1] /= V;
+    for (int k = 0; k < r - 1; ++k) a.ist[k] /= V;
+  }
+  a.per = a.dpart / (vec ? V : 1);
+  const int64_t work = a.per * nparts;
+  const bool small = work < (int64_t)1 << 31;
+  SPMD_DISPATCH_BYTES(out.dtype, T, {
+    const T* src = (const T*)in.data;
+    const T* val = (const T*)value.data;
+    T* dst = (T*)out.data;
+    if (vec) {
+      if (small)
+        pad_gather_kernel<T, uint32_t, 16 / sizeof(T)><<<grid_for(work, 256), 256, 0, s>>>(
+            src, val, dst, a, nparts);
+      else
+        pad_gather_kernel<T, uint64_t, 16 / sizeof(T)><<<grid_for(work, 256), 256, 0, s>>>(
+            src, val, dst, a, nparts);
+    } else {
+      if (small)
+        pad_gather_kernel<T, uint32_t, 1><<<grid_for(work, 256, 2), 256, 0, s>>>(
+            src, val, dst, a, nparts);
+      else
+        pad_gather_kernel<T, uint64_t, 1><<<grid_for(work, 256, 2), 256, 0, s>>>(
+            src, val, dst, a, nparts);
+    }
+  });
+  return launched(s);
+}
+
 extern "C" int spmd_pad(spmd_tensor in, spmd_tensor value, spmd_tensor out, const int64_t* low,
                         const int64_t* high, const int64_t* interior, int64_t nparts,
                         void* stream) {
   SPMD_CHECK_ARG(in.dtype == out.dtype && value.dtype == in.dtype && value.rank == 0,
                  "pad dtype mismatch");
   cudaStream_t s = as_stream(stream);
+  bool edge_only = in.rank == out.rank && in.rank > 0;
+  for (int k = 0; k < in.rank; ++k) edge_only = edge_only && interior[k] == 0;
+  if (edge_only && numel(in) > 0 && numel(out) > 0) return pad_edges(in, value, out, low, high,
+                                                                     nparts, s);
   int rc = launch_fill(out.data, value.data, out.dtype, numel(out), nparts, s);
   if (rc) return rc;
   CopyArgs a = base_args(in);
@@ -289,6 +434,7 @@ extern "C" int spmd_dynamic_slice(spmd_tensor in, const spmd_tensor* starts, spm
     SPMD_CHECK_ARG(starts[k].dtype == SPMD_S32 || starts[k].dtype == SPMD_U32,
                    "dynamic-slice index must be s32/u32");
     SPMD_CHECK_ARG(out.dims[k] <= in.dims[k], "dynamic-slice size exceeds operand");
+    if (out.dims[k] == in.dims[k]) continue;  // start clamps to 0: static
     a.dyn_start[a.ndyn] = (const int32_t*)starts[k].data;
     a.dyn_max[a.ndyn] = in.dims[k] - out.dims[k];
     a.dyn_mul[a.ndyn] = a.sst[k];
@@ -314,6 +460,7 @@ extern "C" int spmd_dynamic_update_slice(spmd_tensor in, spmd_tensor upd, const 
   a.dyn_on_dst = 1;
   for (int k = 0; k < in.rank; ++k) {
     SPMD_CHECK_ARG(upd.dims[k] <= in.dims[k], "update larger than operand");
+    if (upd.dims[k] == in.dims[k]) continue;  // start clamps to 0: static
     a.dyn_start[a.ndyn] = (const int32_t*)starts[k].data;
     a.dyn_max[a.ndyn] = in.dims[k] - upd.dims[k];
     a.dyn_mul[a.ndyn] = a.dst[k];

@@ -105,6 +105,60 @@ __global__ void halo_window_kernel(T* __restrict__ out, HaloArgs a, int64_t npar
   }
 }
 
+// Row-uniform variant for long rows (inner >= one block's worth of vectors):
+// each block owns a chunk of one output row (partition p, outer o, window row
+// i), so the clamp / mask / piece lookup runs once per block and every thread
+// keeps U independent 16-byte loads in flight.
+template <typename T, int U>
+__global__ void __launch_bounds__(256) halo_rows_kernel(T* __restrict__ out, HaloArgs a,
+                                                        int64_t nparts, int64_t chunks) {
+  constexpr int V = 16 / sizeof(T);
+  const int64_t per_row = a.inner / V;
+  const int64_t rows = nparts * a.outer * a.window;
+  for (int64_t b = blockIdx.x; b < rows * chunks; b += gridDim.x) {
+    const int64_t row = b / chunks;
+    const int64_t v0 = (b - row * chunks) * (256 * U) + threadIdx.x;
+    const int64_t p = row / (a.outer * a.window);
+    const int64_t rr = row - p * a.outer * a.window;
+    const int64_t o = rr / a.window, i = rr - o * a.window;
+    int64_t s0 = a.start[p];
+    s0 = s0 < 0 ? 0 : (s0 > a.buf_len - a.window ? a.buf_len - a.window : s0);
+    const int64_t j = s0 + i;
+    bool keep = true;
+    if (a.has_mask) {
+      const int64_t g = j + a.offset[p];
+      keep = g < a.high && (!a.has_low || g >= a.low);
+    }
+    uint4* dst = reinterpret_cast<uint4*>(out) + row * per_row;
+    if (!keep) {
+      const T f = reinterpret_cast<const T*>(a.fill)[p];
+      T fv[V];
+#pragma unroll
+      for (int q = 0; q < V; ++q) fv[q] = f;
+      const uint4 w = *reinterpret_cast<uint4*>(fv);
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (v0 + u * 256 < per_row) dst[v0 + u * 256] = w;
+      continue;
+    }
+    int k = 0;
+    int64_t jj = j;
+    while (k < a.npieces - 1 && jj >= a.len[k]) {
+      jj -= a.len[k];
+      ++k;
+    }
+    const uint4* src = reinterpret_cast<const uint4*>(
+        reinterpret_cast<const T*>(a.piece[k]) + ((p * a.outer + o) * a.len[k] + jj) * a.inner);
+    uint4 reg[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (v0 + u * 256 < per_row) reg[u] = __ldcs(src + v0 + u * 256);
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (v0 + u * 256 < per_row) __stcs(dst + v0 + u * 256, reg[u]);
+  }
+}
+
 }  // namespace spmd
 
 using namespace spmd;
@@ -147,6 +201,15 @@ extern "C" int spmd_halo_window(const spmd_tensor* pieces, int npieces, int axis
   const int V = 16 / elem_size(out.dtype);
   bool vec = a.inner % V == 0 && (reinterpret_cast<uintptr_t>(out.data) & 15) == 0;
   for (int k = 0; k < npieces; ++k) vec = vec && (reinterpret_cast<uintptr_t>(a.piece[k]) & 15) == 0;
+  if (vec && a.inner / V >= 1024) {
+    const int64_t chunks = (a.inner / V + 1023) / 1024;
+    const int64_t blocks = a.outer * a.window * nparts * chunks;
+    const int64_t grid = blocks < 148LL * 8 ? blocks : 148LL * 8;  // 8 x 256 threads per SM
+    SPMD_DISPATCH_BYTES(out.dtype, T,
+                        halo_rows_kernel<T, 4><<<grid, 256, 0, s>>>((T*)out.data, a, nparts,
+                                                                   chunks));
+    return launched(s);
+  }
   SPMD_DISPATCH_BYTES(out.dtype, T, {
     if (vec)
       halo_window_kernel<T, 16 / sizeof(T)><<<grid_for(n / V, 256), 256, 0, s>>>((T*)out.data, a,

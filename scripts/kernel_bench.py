@@ -111,7 +111,7 @@ def datamove():
         pieces, 3, 1, desc(start, sh_s), 1, desc(off, sh_s), desc(fill, Shape((), bf)), 0, 1024,
         1, desc(out, Shape((N, c + 2, W, Ch), bf)), 1, st), "halo"))
     by = (val.numel() + 2 * lh.numel() + out.numel()) * 2
-    print(json.dumps({"kernel": "halo_window_kernel", "case": "C4 [8,128+2,1024,128] bf16",
+    print(json.dumps({"kernel": "halo_rows_kernel", "case": "C4 [8,128+2,1024,128] bf16",
                       "ms": ms, "gbs": by / ms / 1e6}), flush=True)
     # C5 uneven mask: [1001 -> 126 rows/shard, 524288] f32 range mask on the last shard.
     rows, D1 = 126, 524288
@@ -133,7 +133,7 @@ def datamove():
     ms = timeit(lambda: C.check(lib.spmd_pad(desc(x, Shape((1001, D1), f32)), desc(z, Shape((), f32)),
                                              desc(y, Shape((1008, D1), f32)), lo, hi, it, 1, st),
                                 "pad"))
-    print(json.dumps({"kernel": "fill+strided_copy (pad)", "case": "C5 [1001->1008,524288] f32",
+    print(json.dumps({"kernel": "pad_gather_kernel (pad)", "case": "C5 [1001->1008,524288] f32",
                       "ms": ms, "gbs": (x.numel() + y.numel()) * 4 / ms / 1e6}), flush=True)
     # dynamic-slice of the local shard out of the padded full value.
     s0 = torch.full((1,), 126 * 3, dtype=torch.int32, device="cuda")
