@@ -227,6 +227,22 @@ int spmd_all_to_all(spmd_comm* comm, spmd_tensor in, spmd_tensor out, int split_
 int spmd_collective_permute(spmd_comm* comm, spmd_tensor in, spmd_tensor out,
                             const int32_t* pairs, int npairs, void* stream);
 
+/* ---- Peer-memory fused collectives (CUDA IPC over NVLink/NVSwitch) -----------
+ * Collective: every rank allocates a `bytes` heap and maps every other rank's.
+ * Growing re-exchanges (all ranks must call with the same size). */
+int spmd_comm_enable_peer(spmd_comm* comm, int64_t bytes, void* stream);
+int64_t spmd_comm_peer_bytes(spmd_comm* comm);
+/* out = reduce-scatter(sum, dim)(dot(lhs, rhs)) in one tcgen05 GEMM whose
+ * epilogue stores each output tile straight into the owning rank's heap
+ * (replaces the Dot + ReduceScatter pair emitted by reference
+ * partitioner.py:751-759 and executed by simulator.py:258-275, 360-371).
+ * bf16; `dim` must be the last output dim and come from the rhs free dim;
+ * needs a heap of >= 4 * gsize * numel(out) bytes.  SPMD_ERR_UNSUPPORTED
+ * when the GEMM layout does not qualify (use spmd_dot + spmd_reduce_scatter). */
+int spmd_dot_reduce_scatter(spmd_comm* comm, spmd_tensor lhs, spmd_tensor rhs, spmd_tensor out,
+                            const spmd_dot_dims* dims, int dim, const int32_t* groups,
+                            int ngroups, int gsize, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

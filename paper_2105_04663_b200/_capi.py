@@ -107,6 +107,10 @@ _SIGNATURES = {
     "spmd_reduce_scatter": ([_P, _T, _T, _I, _I, _PI32, _I, _I, _P], _I),
     "spmd_all_to_all": ([_P, _T, _T, _I, _I, _PI32, _I, _I, _P], _I),
     "spmd_collective_permute": ([_P, _T, _T, _PI32, _I, _P], _I),
+    "spmd_comm_enable_peer": ([_P, _I64, _P], _I),
+    "spmd_comm_peer_bytes": ([_P], _I64),
+    "spmd_dot_reduce_scatter": ([_P, _T, _T, _T, ctypes.POINTER(SpmdDotDims), _I, _PI32, _I, _I,
+                                 _P], _I),
 }
 
 _lib = None

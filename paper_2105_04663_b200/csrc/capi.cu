@@ -90,6 +90,10 @@ extern "C" int spmd_check_device_errors(void* stream) {
       set_error("integer division by zero");
       return SPMD_ERR_DIV_ZERO;
     }
+    if (host & 2) {
+      set_error("peer barrier timed out (a rank did not reach the fused collective)");
+      return SPMD_ERR_NCCL;
+    }
   }
   return SPMD_OK;
 }

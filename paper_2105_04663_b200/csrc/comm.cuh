@@ -1,0 +1,41 @@
+// The communicator handle behind `spmd_comm*` (shared by the NCCL
+// collectives and the peer-memory fused kernels).
+#pragma once
+
+#include "common.cuh"
+
+#include <nccl.h>
+
+#include <map>
+#include <vector>
+
+struct spmd_comm {
+  ncclComm_t world;
+  int nranks, rank;
+  std::map<std::vector<int32_t>, ncclComm_t> splits;
+  char* ws = nullptr;
+  int64_t ws_bytes = 0;
+  // Peer-memory heap (CUDA IPC, one per rank, same size everywhere):
+  // [control page | data].  peer[q] = rank q's heap mapped into this
+  // process (peer[rank] = heap).  See peer.cu.
+  char* heap = nullptr;
+  int64_t heap_bytes = 0;   // data bytes (excluding the control page)
+  char* peer[SPMD_MAX_PARTS] = {nullptr};
+};
+
+namespace spmd {
+
+#define NCCL_TRY(expr)                                                              \
+  do {                                                                              \
+    ncclResult_t _r = (expr);                                                       \
+    if (_r != ncclSuccess) {                                                        \
+      set_error(std::string(#expr) + ": " + ncclGetErrorString(_r));                \
+      return SPMD_ERR_NCCL;                                                         \
+    }                                                                               \
+  } while (0)
+
+// Subgroup table -> (my group index, my position); validates that the groups
+// partition the ranks (reference simulator.py:322-330).
+int group_position(const spmd_comm* c, const int32_t* groups, int ngroups, int gsize, int* group,
+                   int* pos);
+}  // namespace spmd

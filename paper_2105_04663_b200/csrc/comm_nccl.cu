@@ -12,32 +12,11 @@
 //   devices that are not a target receive zeros (reference :345-350).
 // Reductions run in NCCL's order, so float results match the reference
 // within tolerance (integers exactly).
-#include "common.cuh"
+#include "comm.cuh"
 
-#include <nccl.h>
-
-#include <map>
 #include <string.h>
-#include <vector>
-
-struct spmd_comm {
-  ncclComm_t world;
-  int nranks, rank;
-  std::map<std::vector<int32_t>, ncclComm_t> splits;
-  char* ws = nullptr;
-  int64_t ws_bytes = 0;
-};
 
 namespace spmd {
-
-#define NCCL_TRY(expr)                                                              \
-  do {                                                                              \
-    ncclResult_t _r = (expr);                                                       \
-    if (_r != ncclSuccess) {                                                        \
-      set_error(std::string(#expr) + ": " + ncclGetErrorString(_r));                \
-      return SPMD_ERR_NCCL;                                                         \
-    }                                                                               \
-  } while (0)
 
 static bool nccl_type(int dtype, ncclDataType_t* t) {
   switch (dtype) {
@@ -57,6 +36,27 @@ static ncclRedOp_t nccl_op(int kind) {
     case SPMD_MIN: return ncclMin;
     default: return ncclProd;
   }
+}
+
+int group_position(const spmd_comm* c, const int32_t* groups, int ngroups, int gsize, int* group,
+                   int* pos) {
+  if (ngroups * gsize != c->nranks) {
+    set_error("subgroups do not partition the ranks");
+    return SPMD_ERR_SUBGROUP;
+  }
+  std::vector<int> seen(c->nranks, 0);
+  *group = *pos = -1;
+  for (int i = 0; i < ngroups * gsize; ++i) {
+    if (groups[i] < 0 || groups[i] >= c->nranks || seen[groups[i]]++) {
+      set_error("subgroups do not partition the ranks");
+      return SPMD_ERR_SUBGROUP;
+    }
+    if (groups[i] == c->rank) {
+      *group = i / gsize;
+      *pos = i % gsize;
+    }
+  }
+  return SPMD_OK;
 }
 
 // Sub-communicator for a subgroup partition; *pos = my position in my group.

@@ -23,6 +23,20 @@ int* device_error_word();
 // leaves room for NCCL kernels to co-reside when collectives overlap GEMMs.
 int sm_budget();
 
+// Reduce-scatter epilogue target of the tcgen05 GEMM (peer.cu): column chunk
+// j of the output goes to dst[j] (group position j's peer heap).
+struct GemmScatter {
+  int gsize, pos;
+  void* dst[8];
+  const uint32_t* epoch;
+};
+// Implemented in gemm_tcgen05.cu: returns SPMD_ERR_UNSUPPORTED when the
+// layout cannot be expressed with TMA descriptors (or, with `sc`, when the
+// scattered dim is not the whole GEMM N).
+int dot_tcgen05(const spmd_tensor& lhs, const spmd_tensor& rhs, const spmd_tensor& out,
+                const spmd_dot_dims& dd, int64_t nparts, cudaStream_t s,
+                const GemmScatter* sc = nullptr);
+
 #define SPMD_CHECK_ARG(cond, msg)                  \
   do {                                             \
     if (!(cond)) {                                 \

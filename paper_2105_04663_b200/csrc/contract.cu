@@ -133,10 +133,6 @@ static void strides_of(const spmd_tensor& t, int64_t* st) {
   }
 }
 
-// Implemented in gemm_tcgen05.cu: returns SPMD_ERR_UNSUPPORTED when the
-// layout cannot be expressed with TMA descriptors.
-int dot_tcgen05(const spmd_tensor& lhs, const spmd_tensor& rhs, const spmd_tensor& out,
-                const spmd_dot_dims& dd, int64_t nparts, cudaStream_t s);
 
 // ---------------------------------------------------------------------------
 // direct convolution (parity path; B200 implicit GEMM is in conv_tcgen05.cu)

@@ -42,6 +42,13 @@ struct GemmShape {
   int group;            // rasterisation group size (tiles of the grouped dim)
   int raster_n;         // 0: group M-tiles and sweep N; 1: group N-tiles and sweep M
   int hint;             // 0 none, 1: A evict_last / B evict_first, 2: the reverse
+  // Reduce-scatter epilogue (peer.cu): output column chunk j (sc_chunk wide)
+  // goes to group position j's peer heap, slot sc_pos, buffer parity
+  // (epoch + 1) & 1 -- P2P stores over NVLink, tile by tile.
+  int scatter, sc_g, sc_pos;
+  int64_t sc_chunk, sc_slot;
+  bf16* sc_dst[8];
+  const uint32_t* sc_epoch;
 };
 
 template <int BN, int STAGES>
@@ -464,6 +471,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
     // ---------------- epilogue (both CTAs, own TMEM half) ----------------
     const int ew = warp - EPI_WARP0;
     uint8_t* epi = smem + L::EPI_OFF + ew * 2 * EPI_STAGE_BYTES;
+    const int64_t par_off =
+        g.scatter ? (int64_t)((*(volatile const uint32_t*)g.sc_epoch + 1) & 1) * g.sc_g * g.sc_slot
+                  : 0;
     int chunk = 0;
     int acc = 0;
     uint32_t acc_ph = 0;
@@ -483,6 +493,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
           if (col < g.N)
             epi_store_chunk(&map_c, epi + (chunk++ & 1) * EPI_STAGE_BYTES, r, g.relu, col,
                             m * BM2 + rank * HALF + ew * 32, b, lane);
+        } else if (g.scatter) {
+          if (row < g.M && col < g.N) {
+            __align__(16) bf16 v[32];
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              float f = __uint_as_float(r[j]);
+              if (g.relu) f = f > 0.f ? f : 0.f;
+              v[j] = __float2bfloat16_rn(f);
+            }
+            const int j = (int)(col / g.sc_chunk);
+            const int64_t lc = col - j * g.sc_chunk;
+            bf16* d = g.sc_dst[j] + par_off + g.sc_pos * g.sc_slot + (int64_t)row * g.sc_chunk + lc;
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+              reinterpret_cast<uint4*>(d)[q] = reinterpret_cast<uint4*>(v)[q];
+          }
         } else if (row < g.M && col < g.N) {
           __align__(16) bf16 v[32];
 #pragma unroll
@@ -509,6 +535,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
       }
     }
     if (lane == 0) bulk_wait_all();
+    // Peer stores globally visible before the completion signal (peer.cu).
+    if (g.scatter) __threadfence_system();
   }
   tc_fence_before();
   cluster_sync();
@@ -591,7 +619,7 @@ static int gemm_mode() {
 }
 
 int dot_tcgen05(const spmd_tensor& lhs, const spmd_tensor& rhs, const spmd_tensor& out,
-                const spmd_dot_dims& dd, int64_t nparts, cudaStream_t s) {
+                const spmd_dot_dims& dd, int64_t nparts, cudaStream_t s, const GemmScatter* sc) {
   if (lhs.dtype != SPMD_BF16) return SPMD_ERR_UNSUPPORTED;
   int64_t ls[SPMD_MAX_RANK], rs[SPMD_MAX_RANK];
   {
@@ -706,7 +734,23 @@ int dot_tcgen05(const spmd_tensor& lhs, const spmd_tensor& rhs, const spmd_tenso
                   encode_store_map(&mc, out.data, g.N, g.M, g.N, nbat, g.out_batch_stride);
     if (!g.tma_store) memset(&mc, 0, sizeof(mc));
   }
-  if (gemm_mode() == 2 && M.size >= 256 && N.size >= 256) {
+  if (sc) {
+    // Reduce-scatter epilogue: 2-CTA kernel, no batch dims, the scattered
+    // dim is the last output dim == the whole GEMM N.
+    if (M.size < 256 || N.size < 256 || nb != 0 || N.size != out.dims[out.rank - 1] ||
+        sc->gsize < 1 || sc->gsize > 8 || N.size % sc->gsize != 0 ||
+        (N.size / sc->gsize) % 32 != 0)
+      return SPMD_ERR_UNSUPPORTED;
+    g.tma_store = 0;
+    g.scatter = 1;
+    g.sc_g = sc->gsize;
+    g.sc_pos = sc->pos;
+    g.sc_chunk = N.size / sc->gsize;
+    g.sc_slot = M.size * g.sc_chunk;
+    for (int j = 0; j < sc->gsize; ++j) g.sc_dst[j] = (bf16*)sc->dst[j];
+    g.sc_epoch = sc->epoch;
+  }
+  if ((gemm_mode() == 2 || sc) && M.size >= 256 && N.size >= 256) {
     // 2-CTA path: per-CTA boxes are 128 rows of A and 128 rows of B.
     bool ok2 = a_mn ? encode(&ma, lhs.data, va, 64, BK) : encode(&ma, lhs.data, va, BK, HALF);
     ok2 = ok2 && (b_mn ? encode(&mb, rhs.data, vb, 64, BK) : encode(&mb, rhs.data, vb, BK, HALF));

@@ -1,0 +1,221 @@
+// Peer-memory fused Dot -> reduce-scatter over NVLink / NVSwitch.
+//
+// The partitioner emits Dot followed by ReduceScatter whenever the dot's
+// contracting dim is sharded and an output dim takes the reduced sharding
+// (reference partitioner.py:751-759; C2's out-projection and FFN-out).  The
+// unfused path writes the full partial product to HBM and then runs an NCCL
+// reduce-scatter that cannot start before the last GEMM tile.  Here the GEMM
+// epilogue itself stores every output tile into the heap of the rank that
+// owns its column chunk (P2P stores through the CUDA-IPC mapping), so the
+// transfer overlaps the math tile by tile; a one-block barrier and an
+// HBM-bound slot reduction finish the collective.
+//
+// Heap (per rank, same size everywhere, opened by every other rank):
+//   control page: u32 epoch at [0]; u32 flag[q] at [64 + q] = last epoch that
+//                 rank q has completed (written remotely by q)
+//   data:         2 parity buffers x [gsize slots][rows][chunk] bf16
+// Epochs live in device memory, so the sequence is CUDA-graph replay safe:
+// the GEMM reads parity (epoch + 1) & 1, the barrier kernel increments the
+// epoch, publishes it to every rank and waits for every rank's flag.  Waiting
+// on ALL ranks (not only the group) keeps the parity buffers safe when
+// consecutive fused ops use different subgroups: rank q can only write
+// parity p again after this rank has passed the barrier of the op in between,
+// which follows this rank's reduction of parity p in stream order.
+#include "comm.cuh"
+
+#include <string.h>
+
+namespace spmd {
+
+constexpr int64_t CTRL_BYTES = 4096;
+constexpr int FLAG0 = 64;
+constexpr int ERR_PEER_TIMEOUT = 2;   // device error word bit
+
+struct PeerFlags {
+  uint32_t* remote[SPMD_MAX_PARTS];   // &flag[rank] in rank q's control page
+};
+
+__device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// One block: bump the epoch, publish it to every rank, wait for every rank.
+__global__ void peer_barrier_kernel(uint32_t* ctrl, PeerFlags pf, int nranks, int rank,
+                                    long long timeout_cycles, int* err) {
+  __shared__ uint32_t e;
+  if (threadIdx.x == 0) {
+    e = ctrl[0] + 1;
+    ctrl[0] = e;
+    __threadfence_system();
+  }
+  __syncthreads();
+  const uint32_t ep = e;
+  for (int q = threadIdx.x; q < nranks; q += blockDim.x)
+    if (q != rank) st_release_sys(pf.remote[q], ep);
+  for (int q = threadIdx.x; q < nranks; q += blockDim.x) {
+    if (q == rank) continue;
+    const long long t0 = clock64();
+    while ((int32_t)(ld_acquire_sys(&ctrl[FLAG0 + q]) - ep) < 0) {
+      if (clock64() - t0 > timeout_cycles) {
+        atomicOr(err, ERR_PEER_TIMEOUT);
+        break;
+      }
+      __nanosleep(64);
+    }
+  }
+}
+
+// out[i] = sum_j slot_j[i] (fp32 accumulation in group-position order).
+__global__ void peer_slot_reduce_kernel(const bf16* __restrict__ data, bf16* __restrict__ out,
+                                        const uint32_t* ctrl, int G, int64_t slot, int64_t nvec) {
+  const int64_t par = (int64_t)(*(volatile const uint32_t*)ctrl & 1);
+  const bf16* base = data + par * G * slot;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nvec;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (int j = 0; j < G; ++j) {
+      uint4 w = __ldcs(reinterpret_cast<const uint4*>(base + j * slot) + i);
+      const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&w);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        float2 f = __bfloat1622float2(h[q]);
+        acc[2 * q] += f.x;
+        acc[2 * q + 1] += f.y;
+      }
+    }
+    uint4 o;
+    __nv_bfloat162* oh = reinterpret_cast<__nv_bfloat162*>(&o);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) oh[q] = __floats2bfloat162_rn(acc[2 * q], acc[2 * q + 1]);
+    reinterpret_cast<uint4*>(out)[i] = o;
+  }
+}
+
+static void close_peers(spmd_comm* c) {
+  for (int q = 0; q < c->nranks; ++q)
+    if (q != c->rank && c->peer[q]) cudaIpcCloseMemHandle(c->peer[q]);
+  if (c->heap) cudaFree(c->heap);
+  memset(c->peer, 0, sizeof(c->peer));
+  c->heap = nullptr;
+  c->heap_bytes = 0;
+}
+
+static long long timeout_cycles() {
+  static long long t = -1;
+  if (t < 0) {
+    const char* e = getenv("SPMD_PEER_TIMEOUT_S");
+    const double sec = e ? atof(e) : 20.0;
+    t = (long long)(sec * 2.0e9);   // clock64 at <= 2 GHz
+  }
+  return t;
+}
+
+}  // namespace spmd
+
+using namespace spmd;
+
+extern "C" int spmd_comm_enable_peer(spmd_comm* c, int64_t bytes, void* stream) {
+  SPMD_CHECK_ARG(c && bytes >= 0, "enable_peer arguments");
+  SPMD_CHECK_ARG(c->nranks <= SPMD_MAX_PARTS, "too many ranks for the peer heap");
+  if (c->heap && c->heap_bytes >= bytes) return SPMD_OK;
+  cudaStream_t s = as_stream(stream);
+  // Collective: every rank reallocates and re-exchanges together.
+  SPMD_CUDA_TRY(cudaDeviceSynchronize());
+  close_peers(c);
+  bytes = (bytes + 4095) & ~(int64_t)4095;
+  SPMD_CUDA_TRY(cudaMalloc(&c->heap, CTRL_BYTES + bytes));
+  SPMD_CUDA_TRY(cudaMemset(c->heap, 0, CTRL_BYTES));
+  cudaIpcMemHandle_t h;
+  SPMD_CUDA_TRY(cudaIpcGetMemHandle(&h, c->heap));
+  const size_t hb = sizeof(cudaIpcMemHandle_t);
+  char* dev = nullptr;
+  SPMD_CUDA_TRY(cudaMalloc(&dev, hb * c->nranks));
+  SPMD_CUDA_TRY(cudaMemcpy(dev + hb * c->rank, &h, hb, cudaMemcpyHostToDevice));
+  ncclResult_t r = ncclAllGather(dev + hb * c->rank, dev, hb, ncclUint8, c->world, s);
+  if (r != ncclSuccess) {
+    cudaFree(dev);
+    set_error(std::string("peer handle exchange: ") + ncclGetErrorString(r));
+    return SPMD_ERR_NCCL;
+  }
+  std::vector<cudaIpcMemHandle_t> all(c->nranks);
+  SPMD_CUDA_TRY(cudaStreamSynchronize(s));
+  SPMD_CUDA_TRY(cudaMemcpy(all.data(), dev, hb * c->nranks, cudaMemcpyDeviceToHost));
+  for (int q = 0; q < c->nranks; ++q) {
+    if (q == c->rank) {
+      c->peer[q] = c->heap;
+      continue;
+    }
+    void* p = nullptr;
+    SPMD_CUDA_TRY(cudaIpcOpenMemHandle(&p, all[q], cudaIpcMemLazyEnablePeerAccess));
+    c->peer[q] = (char*)p;
+  }
+  c->heap_bytes = bytes;
+  // Everyone has mapped everyone before the first remote store.
+  r = ncclAllReduce(dev, dev, 1, ncclUint8, ncclSum, c->world, s);
+  cudaError_t e = cudaStreamSynchronize(s);
+  cudaFree(dev);
+  if (r != ncclSuccess) {
+    set_error(std::string("peer barrier: ") + ncclGetErrorString(r));
+    return SPMD_ERR_NCCL;
+  }
+  SPMD_CUDA_TRY(e);
+  return SPMD_OK;
+}
+
+extern "C" int64_t spmd_comm_peer_bytes(spmd_comm* c) { return c ? c->heap_bytes : 0; }
+
+extern "C" int spmd_dot_reduce_scatter(spmd_comm* c, spmd_tensor lhs, spmd_tensor rhs,
+                                       spmd_tensor out, const spmd_dot_dims* dd, int dim,
+                                       const int32_t* groups, int ngroups, int gsize,
+                                       void* stream) {
+  SPMD_CHECK_ARG(c && dd, "dot_reduce_scatter arguments");
+  SPMD_CHECK_ARG(lhs.dtype == SPMD_BF16 && rhs.dtype == SPMD_BF16 && out.dtype == SPMD_BF16,
+                 "dot_reduce_scatter is bf16");
+  SPMD_CHECK_ARG(out.rank >= 1 && dim == out.rank - 1, "dot_reduce_scatter scatters the last dim");
+  if (!c->heap) {
+    set_error("peer heap not enabled (spmd_comm_enable_peer)");
+    return SPMD_ERR_INVALID;
+  }
+  int grp, pos;
+  int rc = group_position(c, groups, ngroups, gsize, &grp, &pos);
+  if (rc) return rc;
+  SPMD_CHECK_ARG(gsize <= 8, "dot_reduce_scatter group size <= 8");
+  const int64_t slot = numel(out);
+  if (2 * gsize * slot * 2 > c->heap_bytes) {
+    set_error("peer heap too small for this reduce-scatter");
+    return SPMD_ERR_INVALID;
+  }
+  SPMD_CHECK_ARG(slot % 8 == 0, "dot_reduce_scatter shard must be a multiple of 8 elements");
+  cudaStream_t s = as_stream(stream);
+  spmd_tensor full = out;
+  full.dims[dim] *= gsize;
+  full.data = nullptr;
+  GemmScatter sc;
+  memset(&sc, 0, sizeof(sc));
+  sc.gsize = gsize;
+  sc.pos = pos;
+  for (int j = 0; j < gsize; ++j) sc.dst[j] = c->peer[groups[grp * gsize + j]] + CTRL_BYTES;
+  sc.epoch = (const uint32_t*)c->heap;
+  rc = dot_tcgen05(lhs, rhs, full, *dd, 1, s, &sc);
+  if (rc) return rc;
+  PeerFlags pf;
+  memset(&pf, 0, sizeof(pf));
+  for (int q = 0; q < c->nranks; ++q)
+    pf.remote[q] = (uint32_t*)c->peer[q] + FLAG0 + c->rank;
+  int* err = device_error_word();
+  if (!err) return SPMD_ERR_CUDA;
+  peer_barrier_kernel<<<1, 64, 0, s>>>((uint32_t*)c->heap, pf, c->nranks, c->rank,
+                                       timeout_cycles(), err);
+  if ((rc = launched(s))) return rc;
+  const int64_t nvec = slot / 8;
+  peer_slot_reduce_kernel<<<grid_for(nvec, 256), 256, 0, s>>>(
+      (const bf16*)(c->heap + CTRL_BYTES), (bf16*)out.data, (const uint32_t*)c->heap, gsize, slot,
+      nvec);
+  return launched(s);
+}

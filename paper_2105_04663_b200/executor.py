@@ -131,6 +131,16 @@ class NcclComm:
                                                     self._ws.numel()),
                     "spmd_comm_set_workspace")
 
+    def ensure_peer(self, nbytes: int, device) -> None:
+        """Collective: allocate / grow the CUDA-IPC peer heap used by the
+        fused dot -> reduce-scatter kernels (every rank, same size)."""
+        torch = _torch()
+        lib = C.lib()
+        if lib.spmd_comm_peer_bytes(self.handle) >= nbytes:
+            return
+        s = torch.cuda.current_stream(device).cuda_stream
+        C.check(lib.spmd_comm_enable_peer(self.handle, int(nbytes), s), "spmd_comm_enable_peer")
+
     def close(self):
         if self.handle:
             C.lib().spmd_comm_destroy(self.handle)
@@ -188,6 +198,9 @@ class Executor:
                 self.lib.spmd_set_sm_limit(max(2, sms - reserve))
         if comm is not None:
             comm.ensure_workspace(self._workspace_bytes(), self.device)
+            peer = self._peer_bytes()
+            if peer:
+                comm.ensure_peer(peer, self.device)
 
     # ------------------------------------------------------------------
     def _shape(self, vid: str) -> Shape:
@@ -197,6 +210,17 @@ class Executor:
         torch = _torch()
         return torch.empty((self.P,) + shape.dims, dtype=torch_dtype(shape.dtype),
                            device=self.device)
+
+    def _peer_bytes(self) -> int:
+        """Peer heap for the fused dot -> reduce-scatter ops: two parity
+        buffers of gsize slots of the output shard."""
+        need = 0
+        for spec in self._fused.values():
+            if spec[0] == "dot_rs":
+                rs = spec[2]
+                need = max(need, 2 * rs.shape.num_elements * len(rs.attrs["subgroups"][0]) *
+                           rs.shape.dtype.itemsize)
+        return need
 
     def _workspace_bytes(self) -> int:
         need = 0
@@ -289,6 +313,42 @@ class Executor:
                 self._fused[relu.id] = ("dot_relu" if ins.opcode == Op.DOT else "conv_relu", ins)
         self._plan_halo_windows(users, outs)
         self._plan_attention(users, outs)
+        self._plan_dot_reduce_scatter(users, outs)
+
+    def _plan_dot_reduce_scatter(self, users, outs):
+        """Dot whose only user is a sum reduce-scatter of its last dim (the
+        rhs free dim) -> one GEMM with a peer-store epilogue (peer.cu).  Only
+        with a multi-process communicator; SPMD_PEER_FUSION=0 disables."""
+        import os
+        if self.comm is None or os.environ.get("SPMD_PEER_FUSION", "1") == "0":
+            return
+        by = self.by_id
+        for rs in self.graph.instructions:
+            if rs.opcode != Op.REDUCE_SCATTER or rs.attrs["kind"] != ReduceKind.SUM:
+                continue
+            d = by.get(rs.operands[0])
+            if d is None or d.opcode != Op.DOT or d.id in outs or d.id in self._fused_skip \
+                    or users.get(d.id, []) != [rs.id] or d.shape.dtype != DType.BF16:
+                continue
+            if rs.attrs["dim"] != d.shape.rank - 1:
+                continue
+            groups = rs.attrs["subgroups"]
+            gs = len(groups[0])
+            if any(len(g) != gs for g in groups) or gs > 8:
+                continue
+            a = d.attrs
+            ls, rsh = self._shape(d.operands[0]), self._shape(d.operands[1])
+            if a["lhs_batch"] or a["rhs_batch"]:
+                continue
+            rfree = [k for k in range(rsh.rank) if k not in a["rhs_contracting"]]
+            if [rsh.dims[k] for k in rfree if rsh.dims[k] != 1] != [d.shape.dims[-1]]:
+                continue
+            n = d.shape.dims[-1]
+            m = d.shape.num_elements // n
+            if m < 256 or n < 256 or n % gs or (n // gs) % 32:
+                continue
+            self._fused_skip.add(d.id)
+            self._fused[rs.id] = ("dot_rs", d, rs)
 
     def _plan_attention(self, users, outs):
         """Dot(q,k) -> fused softmax -> Dot(probs, v) with the Transformer
@@ -455,7 +515,9 @@ class Executor:
             fn = self._make_step(ins)
             ops = tuple(self._operands_of(ins))
             frees = tuple(o for o in set(ops) if last_use.get(o) == k and o not in keep)
-            steps.append(_Step(ins, fn, frees, ops, ins.opcode in COLLECTIVES))
+            fused = self._fused.get(ins.id)
+            coll = ins.opcode in COLLECTIVES and not (fused and fused[0] == "dot_rs")
+            steps.append(_Step(ins, fn, frees, ops, coll))
         return steps
 
     def _hoist_collectives(self, steps: list) -> list:
@@ -506,7 +568,7 @@ class Executor:
         if f[0] == "halo":
             mask = f[4]
             return tuple(f[1]) + (f[3],) + ((mask[2], mask[3]) if mask is not None else ())
-        return f[1].operands
+        return f[1].operands   # dot_relu / conv_relu / dot_rs: the producer's operands
 
     def _make_step(self, ins: Instruction):
         lib = self.lib
@@ -528,6 +590,8 @@ class Executor:
             return self._dot_step(f[1], shp, epilogue=1)
         if f is not None and f[0] == "conv_relu":
             return self._conv_step(f[1], epilogue=1)
+        if f is not None and f[0] == "dot_rs":
+            return self._dot_rs_step(f[1], f[2])
         if f is not None and f[0] == "attention":
             _, q, k, v = f
             qs, ks, vs = self._shape(q), self._shape(k), self._shape(v)
@@ -777,6 +841,35 @@ class Executor:
             out = self._alloc(shp)
             C.check(lib.spmd_dot(desc(env[a], ash), desc(env[b], bsh), desc(out, shp), ref, P, s),
                     "dot")
+            return out
+        return run
+
+    def _dot_dims(self, ins, epilogue=0):
+        dd = C.SpmdDotDims()
+        at = ins.attrs
+        dd.n_batch = len(at["lhs_batch"])
+        dd.n_contract = len(at["lhs_contracting"])
+        for i, (x, y) in enumerate(zip(at["lhs_batch"], at["rhs_batch"])):
+            dd.lhs_batch[i], dd.rhs_batch[i] = x, y
+        for i, (x, y) in enumerate(zip(at["lhs_contracting"], at["rhs_contracting"])):
+            dd.lhs_contracting[i], dd.rhs_contracting[i] = x, y
+        dd.epilogue = epilogue
+        return dd
+
+    def _dot_rs_step(self, dot, rs):
+        lib, comm = self.lib, self.comm
+        a, b = dot.operands
+        ash, bsh, shp = self._shape(a), self._shape(b), rs.shape
+        dd = self._dot_dims(dot)
+        ref = ctypes.byref(dd)
+        groups, ng, gs = _groups_arg(rs.attrs["subgroups"])
+        dim = rs.attrs["dim"]
+
+        def run(env, s):
+            out = self._alloc(shp)
+            C.check(lib.spmd_dot_reduce_scatter(comm.handle, desc(env[a], ash), desc(env[b], bsh),
+                                                desc(out, shp), ref, dim, groups, ng, gs, s),
+                    "dot_reduce_scatter")
             return out
         return run
 

@@ -1,0 +1,177 @@
+"""Fused dot -> reduce-scatter over peer memory vs spmd_dot + NCCL
+reduce-scatter, one process per GPU.
+
+    torchrun --nproc-per-node N --master-addr 127.0.0.1 scripts/peer_fusion_check.py [--perf]
+
+1. Direct ABI: random bf16 GEMMs, several epochs in a row (parity buffers),
+   alternating subgroup partitions (consecutive fused ops over different
+   groups), compared with the unfused dot + NCCL reduce-scatter (fp32-accumulated
+   sums of bf16 partials: normwise 1e-2).
+2. Transformer layer (fast plan, fusions) with and without the peer fusion.
+3. --perf: C2 paper-dims step time (CUDA graph replay, max over ranks) with and
+   without the peer fusion.
+Prints one JSON line per section on rank 0; exit 1 on any failure.
+"""
+
+import ctypes
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+import torch.distributed as dist  # noqa: E402
+
+from paper_2105_04663_b200 import _capi as C  # noqa: E402
+from paper_2105_04663_b200 import partition, propagate  # noqa: E402
+from paper_2105_04663_b200.executor import Executor, NcclComm, _groups_arg, desc  # noqa: E402
+from paper_2105_04663_b200.ir import DType, Shape  # noqa: E402
+from paper_2105_04663_b200.sharding import shard_data  # noqa: E402
+from paper_2105_04663_b200.workloads import transformer_flops, transformer_layer  # noqa: E402
+
+
+def rel(a, b):
+    a, b = a.float(), b.float()
+    return ((a - b).abs().max() / b.abs().max().clamp(min=1.0)).item()
+
+
+def direct_abi(comm, rank, world, dev):
+    lib = C.lib()
+    s = torch.cuda.current_stream().cuda_stream
+    partitions = [[list(range(world))]]
+    if world >= 4:
+        partitions.append([[0, 1], [2, 3]] if world == 4 else
+                          [list(range(i, i + world // 2)) for i in (0, world // 2)])
+        partitions.append([[r for r in range(world) if r % 2 == k] for k in (0, 1)])
+    errs = []
+    M, K, N = 512, 768, 1024
+    comm.ensure_peer(2 * M * N * 2 * 2, dev)
+    dd = C.SpmdDotDims()
+    dd.n_contract = 1
+    dd.lhs_contracting[0], dd.rhs_contracting[0] = 1, 0
+    for it in range(6):
+        groups = partitions[it % len(partitions)]
+        gs = len(groups[0])
+        garr, ng, gsz = _groups_arg(groups)
+        g = torch.Generator(device=dev).manual_seed(1000 * it + rank)
+        a = torch.randn((1, M, K), device=dev, generator=g).bfloat16()
+        b = (torch.randn((1, K, N), device=dev, generator=g) * 0.05).bfloat16()
+        ash, bsh = Shape((M, K), DType.BF16), Shape((K, N), DType.BF16)
+        osh = Shape((M, N // gs), DType.BF16)
+        fused = torch.empty((1, M, N // gs), device=dev, dtype=torch.bfloat16)
+        C.check(lib.spmd_dot_reduce_scatter(comm.handle, desc(a, ash), desc(b, bsh),
+                                            desc(fused, osh), ctypes.byref(dd), 1, garr, ng, gsz,
+                                            s), "dot_reduce_scatter")
+        full = torch.empty((1, M, N), device=dev, dtype=torch.bfloat16)
+        C.check(lib.spmd_dot(desc(a, ash), desc(b, bsh), desc(full, Shape((M, N), DType.BF16)),
+                             ctypes.byref(dd), 1, s), "dot")
+        ref = torch.empty_like(fused)
+        comm.ensure_workspace(4 * M * N, dev)
+        C.check(lib.spmd_reduce_scatter(comm.handle, desc(full, Shape((M, N), DType.BF16)),
+                                        desc(ref, osh), 1, 0, garr, ng, gsz, s), "rs")
+        torch.cuda.synchronize()
+        C.check(lib.spmd_check_device_errors(s), "device")
+        errs.append(rel(fused, ref))
+    return errs
+
+
+def layer(comm, rank, world, dev, mesh, dims, fused_rs):
+    os.environ["SPMD_PEER_FUSION"] = "1" if fused_rs else "0"
+    big = dims["M"] >= 4096
+    g, ins = transformer_layer(mesh, dtype=DType.BF16, with_inputs=not big, **dims)
+    ann, _ = propagate(g)
+    prog = partition(ann, world, plan="fast")
+    stacked = []
+    gen = torch.Generator(device=dev).manual_seed(rank)
+    for k, p in enumerate(prog.graph.parameters):
+        if big:   # synthetic shard of the paper-dims layer, made on the device
+            t = torch.randn((1,) + p.shape.dims, device=dev, generator=gen) * 0.02
+        else:
+            piece = shard_data(ins[k], ann.parameters[k].sharding, devices=range(world))[rank]
+            t = torch.from_numpy(np.ascontiguousarray(piece, dtype=np.float32)).to(dev)
+        stacked.append(t.to(torch.bfloat16).reshape((1,) + p.shape.dims))
+    ex = Executor(prog, nparts=1, device=dev, comm=comm, partition_base=rank, fuse=True)
+    n_rs = sum(1 for v in ex._fused.values() if v[0] == "dot_rs")
+    return ex, stacked, n_rs
+
+
+def main():
+    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist.init_process_group("nccl", device_id=dev)
+    comm = NcclComm.from_torch_distributed()
+    failed = []
+
+    errs = direct_abi(comm, rank, world, dev)
+    allerrs = [None] * world
+    dist.all_gather_object(allerrs, errs)
+    worst = max(max(e) for e in allerrs)
+    if rank == 0:
+        print(json.dumps({"section": "direct_abi", "world": world, "max_rel": worst}), flush=True)
+    if not worst < 1e-2:
+        failed.append("direct_abi")
+
+    mesh = (1, world) if world <= 2 else (2, world // 2)
+    small = dict(B=4, S=256, M=1024, N=8, D=64, H=4096)
+    ex1, x1, n1 = layer(comm, rank, world, dev, mesh, small, True)
+    ex0, x0, n0 = layer(comm, rank, world, dev, mesh, small, False)
+    a = ex1.run(x1)[0]
+    b = ex0.run(x0)[0]
+    torch.cuda.synchronize()
+    e = rel(a, b)
+    es = [None] * world
+    dist.all_gather_object(es, e)
+    if rank == 0:
+        print(json.dumps({"section": "layer_small", "mesh": mesh, "fused_dot_rs": n1,
+                          "unfused_dot_rs": n0, "max_rel": max(es)}), flush=True)
+    if not (max(es) < 2e-2 and n1 > 0 and n0 == 0):
+        failed.append("layer_small")
+    del ex1, ex0, x1, x0
+
+    if "--perf" in sys.argv:
+        dims = dict(B=16, S=1024, M=8192, N=128, D=256, H=65536)
+        flops = transformer_flops(**dims)
+        for fused in (True, False):
+            ex, xs, n = layer(comm, rank, world, dev, mesh, dims, fused)
+            graph, outs = ex.capture(xs)
+            for _ in range(3):
+                graph.replay()
+            torch.cuda.synchronize()
+            dist.barrier()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for _ in range(10):
+                graph.replay()
+            e1.record()
+            torch.cuda.synchronize()
+            ms = torch.tensor([e0.elapsed_time(e1) / 10], device=dev)
+            dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+            C.check(C.lib().spmd_check_device_errors(torch.cuda.current_stream().cuda_stream),
+                    "device")
+            if rank == 0:
+                print(json.dumps({"section": "c2_perf", "mesh": mesh, "peer_fusion": fused,
+                                  "fused_dot_rs": n, "ms_per_step": ms.item(),
+                                  "tflops_per_gpu": flops / world / ms.item() / 1e9}), flush=True)
+            del graph, outs, ex, xs
+            torch.cuda.empty_cache()
+
+    flags = [None] * world
+    dist.all_gather_object(flags, failed)
+    rc = 0
+    if rank == 0:
+        allf = sorted({f for fl in flags for f in fl})
+        print(json.dumps({"world": world, "failed": allf}), flush=True)
+        rc = 1 if allf else 0
+    comm.close()
+    dist.barrier()
+    dist.destroy_process_group()
+    return rc
+
+
+if __name__ == "__main__":
+    sys.exit(main())
