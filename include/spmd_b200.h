@@ -242,6 +242,17 @@ int64_t spmd_comm_peer_bytes(spmd_comm* comm);
 int spmd_dot_reduce_scatter(spmd_comm* comm, spmd_tensor lhs, spmd_tensor rhs, spmd_tensor out,
                             const spmd_dot_dims* dims, int dim, const int32_t* groups,
                             int ngroups, int gsize, void* stream);
+/* All-gather through the peer heap (reference simulator.py:353-359 piece
+ * order): stage `in` at heap data offset `heap_offset` (256-aligned, caller
+ * assigned, disjoint from the reduce-scatter region and from other live
+ * all-gathers), barrier, pull every member's piece with copy-engine copies,
+ * barrier.  `channel` (0..3): one per issuing stream -- all ranks must issue
+ * the calls of a channel in the same order.  `engine`: 0 = copy engines (no
+ * SMs: for gathers hidden under GEMMs), 1 = SM pull kernel (16-byte NVLink
+ * loads: for gathers on the critical path). */
+int spmd_peer_all_gather(spmd_comm* comm, spmd_tensor in, spmd_tensor out, int dim,
+                         const int32_t* groups, int ngroups, int gsize, int64_t heap_offset,
+                         int channel, int engine, void* stream);
 
 #ifdef __cplusplus
 }

@@ -49,6 +49,13 @@ struct GemmShape {
   int64_t sc_chunk, sc_slot;
   bf16* sc_dst[8];
   const uint32_t* sc_epoch;
+  int sc_tma;           // scatter through per-destination bulk-tensor store maps
+};
+
+// Per-destination store maps of the reduce-scatter epilogue: rank j's heap as
+// (chunk cols, rows, 2 parities x gsize slots).
+struct ScatterMaps {
+  CUtensorMap m[8];
 };
 
 template <int BN, int STAGES>
@@ -350,7 +357,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
     gemm_bf16_tcgen05_2sm(const __grid_constant__ CUtensorMap map_a,
                           const __grid_constant__ CUtensorMap map_b,
                           const __grid_constant__ CUtensorMap map_c, bf16* __restrict__ out,
-                          GemmShape g) {
+                          GemmShape g, const __grid_constant__ ScatterMaps smaps) {
   typedef Smem2<STAGES> L;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
@@ -471,9 +478,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
     // ---------------- epilogue (both CTAs, own TMEM half) ----------------
     const int ew = warp - EPI_WARP0;
     uint8_t* epi = smem + L::EPI_OFF + ew * 2 * EPI_STAGE_BYTES;
-    const int64_t par_off =
-        g.scatter ? (int64_t)((*(volatile const uint32_t*)g.sc_epoch + 1) & 1) * g.sc_g * g.sc_slot
-                  : 0;
+    const int par = g.scatter ? (int)((*(volatile const uint32_t*)g.sc_epoch + 1) & 1) : 0;
+    const int64_t par_off = (int64_t)par * g.sc_g * g.sc_slot;
     int chunk = 0;
     int acc = 0;
     uint32_t acc_ph = 0;
@@ -493,6 +499,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
           if (col < g.N)
             epi_store_chunk(&map_c, epi + (chunk++ & 1) * EPI_STAGE_BYTES, r, g.relu, col,
                             m * BM2 + rank * HALF + ew * 32, b, lane);
+        } else if (g.scatter && g.sc_tma) {
+          if (col < g.N) {
+            const int j = (int)(col / g.sc_chunk);
+            epi_store_chunk(&smaps.m[j], epi + (chunk++ & 1) * EPI_STAGE_BYTES, r, g.relu,
+                            (int)(col - j * g.sc_chunk), m * BM2 + rank * HALF + ew * 32,
+                            par * g.sc_g + g.sc_pos, lane);
+          }
         } else if (g.scatter) {
           if (row < g.M && col < g.N) {
             __align__(16) bf16 v[32];
@@ -593,7 +606,7 @@ static int launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, const CUten
 
 template <int STAGES>
 static int launch_gemm_2sm(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc,
-                           bf16* out, GemmShape g,
+                           bf16* out, GemmShape g, const ScatterMaps& smaps,
                            cudaStream_t s) {
   typedef Smem2<STAGES> L;
   static bool configured = false;
@@ -605,7 +618,7 @@ static int launch_gemm_2sm(const CUtensorMap& ma, const CUtensorMap& mb, const C
   const int sms = sm_budget();
   int64_t clusters = g.tiles < sms / 2 ? g.tiles : sms / 2;
   gemm_bf16_tcgen05_2sm<STAGES><<<(unsigned)(2 * clusters), 256, L::TOTAL, s>>>(ma, mb, mc, out,
-                                                                                    g);
+                                                                                    g, smaps);
   return launched(s);
 }
 
@@ -722,6 +735,8 @@ int dot_tcgen05(const spmd_tensor& lhs, const spmd_tensor& rhs, const spmd_tenso
   }
   g.out_batch_stride = (int64_t)g.M * g.N;
   CUtensorMap ma, mb, mc;
+  ScatterMaps smaps;
+  memset(&smaps, 0, sizeof(smaps));
   // Bulk-tensor store epilogue whenever the output rows are 16-byte aligned.
   {
     const int64_t nbat = (int64_t)g.nb[0] * g.nb[1] * g.nb[2];
@@ -749,6 +764,15 @@ int dot_tcgen05(const spmd_tensor& lhs, const spmd_tensor& rhs, const spmd_tenso
     g.sc_slot = M.size * g.sc_chunk;
     for (int j = 0; j < sc->gsize; ++j) g.sc_dst[j] = (bf16*)sc->dst[j];
     g.sc_epoch = sc->epoch;
+    static int direct = -1;
+    if (direct < 0) {
+      const char* e = getenv("SPMD_SCATTER_EPI");
+      direct = (e && strcmp(e, "direct") == 0) ? 1 : 0;
+    }
+    g.sc_tma = !direct;
+    for (int j = 0; g.sc_tma && j < sc->gsize; ++j)
+      g.sc_tma = encode_store_map(&smaps.m[j], sc->dst[j], g.sc_chunk, M.size, g.sc_chunk,
+                                  2 * sc->gsize, g.sc_slot);
   }
   if ((gemm_mode() == 2 || sc) && M.size >= 256 && N.size >= 256) {
     // 2-CTA path: per-CTA boxes are 128 rows of A and 128 rows of B.
@@ -758,7 +782,7 @@ int dot_tcgen05(const spmd_tensor& lhs, const spmd_tensor& rhs, const spmd_tenso
     g.mt = (g.M + BM2 - 1) / BM2;
     g.nt = (g.N + BN2 - 1) / BN2;
     g.tiles = (int64_t)g.mt * g.nt * g.nb[0] * g.nb[1] * g.nb[2];
-    return launch_gemm_2sm<6>(ma, mb, mc, (bf16*)out.data, g, s);
+    return launch_gemm_2sm<6>(ma, mb, mc, (bf16*)out.data, g, smaps, s);
   }
   const int BNsel = N.size >= 256 ? 256 : 128;
   bool ok = a_mn ? encode(&ma, lhs.data, va, 64, BK) : encode(&ma, lhs.data, va, BK, BM);

@@ -11,9 +11,13 @@
 // HBM-bound slot reduction finish the collective.
 //
 // Heap (per rank, same size everywhere, opened by every other rank):
-//   control page: u32 epoch at [0]; u32 flag[q] at [64 + q] = last epoch that
+//   control page: per barrier channel c (one per issuing stream, so ranks
+//                 agree on the order of barriers within a channel): u32 epoch
+//                 at [256c]; u32 flag[q] at [256c + 64 + q] = last epoch that
 //                 rank q has completed (written remotely by q)
-//   data:         2 parity buffers x [gsize slots][rows][chunk] bf16
+//   data:         [0, R): 2 parity buffers x [gsize slots][rows][chunk] bf16
+//                 of the fused dot -> reduce-scatter (channel 0);
+//                 caller-assigned offsets: all-gather staging slots.
 // Epochs live in device memory, so the sequence is CUDA-graph replay safe:
 // the GEMM reads parity (epoch + 1) & 1, the barrier kernel increments the
 // epoch, publishes it to every rank and waits for every rank's flag.  Waiting
@@ -28,6 +32,8 @@
 namespace spmd {
 
 constexpr int64_t CTRL_BYTES = 4096;
+constexpr int CHANNEL_WORDS = 256;    // per barrier channel: epoch, pad, flags[64 + q]
+constexpr int NUM_CHANNELS = 4;
 constexpr int FLAG0 = 64;
 constexpr int ERR_PEER_TIMEOUT = 2;   // device error word bit
 
@@ -97,6 +103,55 @@ __global__ void peer_slot_reduce_kernel(const bf16* __restrict__ data, bf16* __r
   }
 }
 
+static long long timeout_cycles();
+
+// Barrier on channel `ch` (stream-ordered, one block).
+static int peer_barrier(spmd_comm* c, int ch, cudaStream_t s) {
+  PeerFlags pf;
+  memset(&pf, 0, sizeof(pf));
+  for (int q = 0; q < c->nranks; ++q)
+    pf.remote[q] = (uint32_t*)c->peer[q] + ch * CHANNEL_WORDS + FLAG0 + c->rank;
+  int* err = device_error_word();
+  if (!err) return SPMD_ERR_CUDA;
+  peer_barrier_kernel<<<1, 64, 0, s>>>((uint32_t*)c->heap + ch * CHANNEL_WORDS, pf, c->nranks,
+                                       c->rank, timeout_cycles(), err);
+  return launched(s);
+}
+
+// SM pull engine of the all-gather: dst[r][j][v] = src_j[r][v] in 16-byte
+// vectors, 4 independent NVLink loads in flight per thread.
+struct PullArgs {
+  const uint4* src[8];
+  int G;
+  int64_t outer, w16;   // rows of my piece, 16-byte vectors per row
+};
+
+__global__ void __launch_bounds__(512) peer_pull_kernel(PullArgs a, uint4* __restrict__ dst) {
+  const int64_t per = a.outer * a.w16;
+  const int64_t total = per * a.G;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t base = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; base < total;
+       base += 4 * stride) {
+    uint4 v[4];
+    int64_t d[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int64_t idx = base + u * stride;
+      d[u] = -1;
+      if (idx < total) {
+        const int j = (int)(idx / per);
+        const int64_t rv = idx - j * per;
+        const int64_t r = rv / a.w16, c = rv - r * a.w16;
+        v[u] = __ldcs(a.src[j] + rv);
+        d[u] = (r * a.G + j) * a.w16 + c;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (d[u] >= 0) __stcs(dst + d[u], v[u]);
+  }
+}
+
 static void close_peers(spmd_comm* c) {
   for (int q = 0; q < c->nranks; ++q)
     if (q != c->rank && c->peer[q]) cudaIpcCloseMemHandle(c->peer[q]);
@@ -122,7 +177,8 @@ using namespace spmd;
 
 extern "C" int spmd_comm_enable_peer(spmd_comm* c, int64_t bytes, void* stream) {
   SPMD_CHECK_ARG(c && bytes >= 0, "enable_peer arguments");
-  SPMD_CHECK_ARG(c->nranks <= SPMD_MAX_PARTS, "too many ranks for the peer heap");
+  SPMD_CHECK_ARG(c->nranks <= SPMD_MAX_PARTS && c->nranks <= CHANNEL_WORDS - FLAG0,
+                 "too many ranks for the peer heap");
   if (c->heap && c->heap_bytes >= bytes) return SPMD_OK;
   cudaStream_t s = as_stream(stream);
   // Collective: every rank reallocates and re-exchanges together.
@@ -204,18 +260,75 @@ extern "C" int spmd_dot_reduce_scatter(spmd_comm* c, spmd_tensor lhs, spmd_tenso
   sc.epoch = (const uint32_t*)c->heap;
   rc = dot_tcgen05(lhs, rhs, full, *dd, 1, s, &sc);
   if (rc) return rc;
-  PeerFlags pf;
-  memset(&pf, 0, sizeof(pf));
-  for (int q = 0; q < c->nranks; ++q)
-    pf.remote[q] = (uint32_t*)c->peer[q] + FLAG0 + c->rank;
-  int* err = device_error_word();
-  if (!err) return SPMD_ERR_CUDA;
-  peer_barrier_kernel<<<1, 64, 0, s>>>((uint32_t*)c->heap, pf, c->nranks, c->rank,
-                                       timeout_cycles(), err);
-  if ((rc = launched(s))) return rc;
+  if ((rc = peer_barrier(c, 0, s))) return rc;
   const int64_t nvec = slot / 8;
   peer_slot_reduce_kernel<<<grid_for(nvec, 256), 256, 0, s>>>(
       (const bf16*)(c->heap + CTRL_BYTES), (bf16*)out.data, (const uint32_t*)c->heap, gsize, slot,
       nvec);
   return launched(s);
+}
+
+// All-gather through the peer heap: stage my shard at `heap_offset`, barrier,
+// pull every group member's staged shard with copy-engine 2-D copies (no SMs
+// taken from concurrently running GEMMs), barrier (so the staging slot may be
+// rewritten by the next call).  Piece order = group order (reference
+// simulator.py:353-359).
+extern "C" int spmd_peer_all_gather(spmd_comm* c, spmd_tensor in, spmd_tensor out, int dim,
+                                    const int32_t* groups, int ngroups, int gsize,
+                                    int64_t heap_offset, int channel, int engine, void* stream) {
+  SPMD_CHECK_ARG(c && in.dtype == out.dtype && dim >= 0 && dim < in.rank &&
+                     out.dims[dim] == in.dims[dim] * gsize,
+                 "peer all-gather shape mismatch");
+  SPMD_CHECK_ARG(channel >= 0 && channel < NUM_CHANNELS, "peer barrier channel");
+  if (!c->heap) {
+    set_error("peer heap not enabled (spmd_comm_enable_peer)");
+    return SPMD_ERR_INVALID;
+  }
+  int grp, pos;
+  int rc = group_position(c, groups, ngroups, gsize, &grp, &pos);
+  if (rc) return rc;
+  const int64_t es = elem_size(in.dtype);
+  const int64_t bytes = numel(in) * es;
+  SPMD_CHECK_ARG(heap_offset >= 0 && heap_offset % 256 == 0 && heap_offset + bytes <= c->heap_bytes,
+                 "peer all-gather staging slot outside the heap");
+  if (bytes == 0) return SPMD_OK;
+  cudaStream_t s = as_stream(stream);
+  SPMD_CUDA_TRY(cudaMemcpyAsync(c->heap + CTRL_BYTES + heap_offset, in.data, bytes,
+                                cudaMemcpyDeviceToDevice, s));
+  if ((rc = peer_barrier(c, channel, s))) return rc;
+  int64_t outer = 1;
+  for (int i = 0; i < dim; ++i) outer *= in.dims[i];
+  const int64_t w = bytes / outer;   // one contiguous run of my piece
+  const bool sm = engine == 1 && gsize <= 8 && w % 16 == 0 &&
+                  (reinterpret_cast<uintptr_t>(in.data) & 15) == 0 &&
+                  (reinterpret_cast<uintptr_t>(out.data) & 15) == 0;
+  if (sm) {
+    PullArgs pa;
+    memset(&pa, 0, sizeof(pa));
+    pa.G = gsize;
+    pa.outer = outer;
+    pa.w16 = w / 16;
+    for (int j = 0; j < gsize; ++j) {
+      const int q = groups[grp * gsize + j];
+      pa.src[j] = (const uint4*)(q == c->rank ? (const char*)in.data
+                                              : c->peer[q] + CTRL_BYTES + heap_offset);
+    }
+    const int64_t work = (bytes / 16) * gsize;
+    int64_t grid = (work + 4 * 512 - 1) / (4 * 512);
+    if (grid > 148 * 4) grid = 148 * 4;
+    peer_pull_kernel<<<(unsigned)grid, 512, 0, s>>>(pa, (uint4*)out.data);
+    if ((rc = launched(s))) return rc;
+    return peer_barrier(c, channel, s);
+  }
+  for (int j = 0; j < gsize; ++j) {
+    const int q = groups[grp * gsize + j];
+    const char* src = q == c->rank ? (const char*)in.data : c->peer[q] + CTRL_BYTES + heap_offset;
+    char* dst = (char*)out.data + j * w;
+    if (outer == 1)
+      SPMD_CUDA_TRY(cudaMemcpyAsync(dst, src, w, cudaMemcpyDeviceToDevice, s));
+    else
+      SPMD_CUDA_TRY(cudaMemcpy2DAsync(dst, gsize * w, src, w, w, outer, cudaMemcpyDeviceToDevice,
+                                      s));
+  }
+  return peer_barrier(c, channel, s);
 }

@@ -201,6 +201,9 @@ class Executor:
             peer = self._peer_bytes()
             if peer:
                 comm.ensure_peer(peer, self.device)
+        else:
+            self._peer_ag = {}
+        self._peer_engine = self._plan_peer_engines()
 
     # ------------------------------------------------------------------
     def _shape(self, vid: str) -> Shape:
@@ -212,15 +215,55 @@ class Executor:
                            device=self.device)
 
     def _peer_bytes(self) -> int:
-        """Peer heap for the fused dot -> reduce-scatter ops: two parity
-        buffers of gsize slots of the output shard."""
+        """Peer heap: [0, R) two parity buffers of gsize slots of the largest
+        fused dot -> reduce-scatter shard, then one staging slot per
+        peer all-gather (offsets recorded in ``self._peer_ag``)."""
+        import os
         need = 0
         for spec in self._fused.values():
             if spec[0] == "dot_rs":
                 rs = spec[2]
                 need = max(need, 2 * rs.shape.num_elements * len(rs.attrs["subgroups"][0]) *
                            rs.shape.dtype.itemsize)
-        return need
+        off = (need + 4095) // 4096 * 4096
+        self._peer_ag = {}
+        if os.environ.get("SPMD_PEER_AG", "1") != "0":
+            for ins in self.graph.instructions:
+                if ins.opcode == Op.ALL_GATHER and ins.id not in self._fused_skip:
+                    self._peer_ag[ins.id] = off
+                    nb = self._shape(ins.operands[0]).num_elements * ins.shape.dtype.itemsize
+                    off += (nb + 4095) // 4096 * 4096
+        return off
+
+    def _plan_peer_engines(self) -> dict:
+        """Copy engines (0) for peer all-gathers that a GEMM hides on the
+        compute stream; the SM pull kernel (1) for the ones on the critical
+        path (no dot / convolution issued between the gather and its first
+        consumer).  SPMD_PEER_AG_ENGINE=ce|sm forces one."""
+        import os
+        force = os.environ.get("SPMD_PEER_AG_ENGINE", "auto")
+        heavy_ops = (Op.DOT, Op.CONVOLUTION)
+        heavy_fused = ("dot_relu", "conv_relu", "attention", "dot_rs")
+        eng = {}
+        order = self.steps
+        for i, st in enumerate(order):
+            if st.ins.id not in self._peer_ag:
+                continue
+            if force in ("ce", "sm"):
+                eng[st.ins.id] = 0 if force == "ce" else 1
+                continue
+            hidden = False
+            if self.comm_stream is not None:
+                for nxt in order[i + 1:]:
+                    if st.ins.id in nxt.ops:
+                        break
+                    f = self._fused.get(nxt.ins.id)
+                    if not nxt.coll and (nxt.ins.opcode in heavy_ops or
+                                         (f is not None and f[0] in heavy_fused)):
+                        hidden = True
+                        break
+            eng[st.ins.id] = 0 if hidden else 1
+        return eng
 
     def _workspace_bytes(self) -> int:
         need = 0
@@ -932,7 +975,14 @@ class Executor:
         def run(env, s):
             out = self._alloc(shp)
             x, y = desc(env[a], ash), desc(out, shp)
-            if op == Op.ALL_GATHER:
+            if op == Op.ALL_GATHER and ins.id in self._peer_ag:
+                # one barrier channel per issuing stream
+                ch = 1 if (self.comm_stream is not None and s == self.comm_stream.cuda_stream) \
+                    else 0
+                rc = lib.spmd_peer_all_gather(comm.handle, x, y, at["dim"], groups, ng, gs,
+                                              self._peer_ag[ins.id], ch,
+                                              self._peer_engine.get(ins.id, 1), s)
+            elif op == Op.ALL_GATHER:
                 rc = lib.spmd_local_all_gather(x, y, at["dim"], groups, ng, gs, P, s) \
                     if comm is None else \
                     lib.spmd_all_gather(comm.handle, x, y, at["dim"], groups, ng, gs, s)

@@ -78,8 +78,11 @@ def direct_abi(comm, rank, world, dev):
     return errs
 
 
-def layer(comm, rank, world, dev, mesh, dims, fused_rs):
+def layer(comm, rank, world, dev, mesh, dims, fused_rs, env=None):
     os.environ["SPMD_PEER_FUSION"] = "1" if fused_rs else "0"
+    for k in ("SPMD_PEER_AG", "SPMD_PEER_AG_ENGINE"):
+        os.environ.pop(k, None)
+    os.environ.update(env or {})
     big = dims["M"] >= 4096
     g, ins = transformer_layer(mesh, dtype=DType.BF16, with_inputs=not big, **dims)
     ann, _ = propagate(g)
@@ -136,8 +139,12 @@ def main():
     if "--perf" in sys.argv:
         dims = dict(B=16, S=1024, M=8192, N=128, D=256, H=65536)
         flops = transformer_flops(**dims)
-        for fused in (True, False):
-            ex, xs, n = layer(comm, rank, world, dev, mesh, dims, fused)
+        variants = [("peer (auto engines)", True, {}),
+                    ("peer, copy engines only", True, {"SPMD_PEER_AG_ENGINE": "ce"}),
+                    ("peer, SM pulls only", True, {"SPMD_PEER_AG_ENGINE": "sm"}),
+                    ("nccl only", False, {"SPMD_PEER_AG": "0"})]
+        for name, fused, env in variants:
+            ex, xs, n = layer(comm, rank, world, dev, mesh, dims, fused, env)
             graph, outs = ex.capture(xs)
             for _ in range(3):
                 graph.replay()
@@ -154,7 +161,7 @@ def main():
             C.check(C.lib().spmd_check_device_errors(torch.cuda.current_stream().cuda_stream),
                     "device")
             if rank == 0:
-                print(json.dumps({"section": "c2_perf", "mesh": mesh, "peer_fusion": fused,
+                print(json.dumps({"section": "c2_perf", "mesh": mesh, "variant": name,
                                   "fused_dot_rs": n, "ms_per_step": ms.item(),
                                   "tflops_per_gpu": flops / world / ms.item() / 1e9}), flush=True)
             del graph, outs, ex, xs
