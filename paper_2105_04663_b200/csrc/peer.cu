@@ -293,12 +293,12 @@ extern "C" int spmd_peer_all_gather(spmd_comm* c, spmd_tensor in, spmd_tensor ou
                  "peer all-gather staging slot outside the heap");
   if (bytes == 0) return SPMD_OK;
   cudaStream_t s = as_stream(stream);
-  SPMD_CUDA_TRY(cudaMemcpyAsync(c->heap + CTRL_BYTES + heap_offset, in.data, bytes,
-                                cudaMemcpyDeviceToDevice, s));
-  if ((rc = peer_barrier(c, channel, s))) return rc;
   int64_t outer = 1;
   for (int i = 0; i < dim; ++i) outer *= in.dims[i];
   const int64_t w = bytes / outer;   // one contiguous run of my piece
+  SPMD_CUDA_TRY(cudaMemcpyAsync(c->heap + CTRL_BYTES + heap_offset, in.data, bytes,
+                                cudaMemcpyDeviceToDevice, s));
+  if ((rc = peer_barrier(c, channel, s))) return rc;
   const bool sm = engine == 1 && gsize <= 8 && w % 16 == 0 &&
                   (reinterpret_cast<uintptr_t>(in.data) & 15) == 0 &&
                   (reinterpret_cast<uintptr_t>(out.data) & 15) == 0;

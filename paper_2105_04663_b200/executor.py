@@ -237,9 +237,12 @@ class Executor:
 
     def _plan_peer_engines(self) -> dict:
         """Copy engines (0) for peer all-gathers that a GEMM hides on the
-        compute stream; the SM pull kernel (1) for the ones on the critical
+        compute stream (no SMs taken from it); for the ones on the critical
         path (no dot / convolution issued between the gather and its first
-        consumer).  SPMD_PEER_AG_ENGINE=ce|sm forces one."""
+        consumer) the SM pull kernel (1) for pairs and NCCL (-1) for larger
+        groups, where its NVLink-multicast all-gather out-runs point-to-point
+        pulls (profiles/r1_peer_ag_bench_n4.jsonl).  SPMD_PEER_AG_ENGINE=ce|sm
+        forces one."""
         import os
         force = os.environ.get("SPMD_PEER_AG_ENGINE", "auto")
         heavy_ops = (Op.DOT, Op.CONVOLUTION)
@@ -262,7 +265,8 @@ class Executor:
                                          (f is not None and f[0] in heavy_fused)):
                         hidden = True
                         break
-            eng[st.ins.id] = 0 if hidden else 1
+            gs = len(st.ins.attrs["subgroups"][0])
+            eng[st.ins.id] = 0 if hidden else (1 if gs <= 2 else -1)
         return eng
 
     def _workspace_bytes(self) -> int:
@@ -975,7 +979,7 @@ class Executor:
         def run(env, s):
             out = self._alloc(shp)
             x, y = desc(env[a], ash), desc(out, shp)
-            if op == Op.ALL_GATHER and ins.id in self._peer_ag:
+            if op == Op.ALL_GATHER and self._peer_engine.get(ins.id, -1) >= 0:
                 # one barrier channel per issuing stream
                 ch = 1 if (self.comm_stream is not None and s == self.comm_stream.cuda_stream) \
                     else 0

@@ -1,0 +1,99 @@
+"""Peer-memory collectives (peer.cu) on one GPU: a world-of-one NCCL
+communicator still allocates / maps the CUDA-IPC heap and runs the real
+kernels -- the scatter epilogue of the tcgen05 GEMM (both parity buffers),
+the epoch barrier and the slot reduction; the all-gather staging + copy-engine
+and SM-pull engines.  Multi-GPU parity of the same paths against NCCL is
+scripts/peer_fusion_check.py and scripts/multi_gpu_check.py
+(profiles/r1_peer_fusion_n{2,4}.log)."""
+
+import ctypes
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def comm():
+    import torch
+    from paper_2105_04663_b200.executor import NcclComm
+    c = NcclComm(0, 1)
+    c.ensure_peer(64 << 20, torch.device("cuda", 0))
+    yield c
+    c.close()
+
+
+def _dd():
+    from paper_2105_04663_b200 import _capi as C
+    dd = C.SpmdDotDims()
+    dd.n_contract = 1
+    dd.lhs_contracting[0], dd.rhs_contracting[0] = 1, 0
+    return dd
+
+
+@pytest.mark.parametrize("M,K,N", [(256, 128, 256), (384, 640, 1024)])
+def test_dot_reduce_scatter_world_of_one(comm, M, K, N):
+    import torch
+    from paper_2105_04663_b200 import _capi as C
+    from paper_2105_04663_b200.executor import _groups_arg, desc
+    from paper_2105_04663_b200.ir import DType, Shape
+    lib, s = C.lib(), torch.cuda.current_stream().cuda_stream
+    garr, ng, gs = _groups_arg([[0]])
+    dd = _dd()
+    ash, bsh, osh = (Shape((M, K), DType.BF16), Shape((K, N), DType.BF16),
+                     Shape((M, N), DType.BF16))
+    for it in range(3):   # consecutive epochs alternate the parity buffers
+        torch.manual_seed(it)
+        a = torch.randn((1, M, K), device="cuda").bfloat16()
+        b = (torch.randn((1, K, N), device="cuda") * 0.05).bfloat16()
+        fused = torch.empty((1, M, N), device="cuda", dtype=torch.bfloat16)
+        plain = torch.empty_like(fused)
+        C.check(lib.spmd_dot_reduce_scatter(comm.handle, desc(a, ash), desc(b, bsh),
+                                            desc(fused, osh), ctypes.byref(dd), 1, garr, ng, gs,
+                                            s), "dot_reduce_scatter")
+        C.check(lib.spmd_dot(desc(a, ash), desc(b, bsh), desc(plain, osh), ctypes.byref(dd), 1,
+                             s), "dot")
+        torch.cuda.synchronize()
+        C.check(lib.spmd_check_device_errors(s), "device")
+        assert torch.equal(fused, plain)
+        ref = (a[0].float() @ b[0].float())
+        err = (fused[0].float() - ref).abs().max().item() / max(1.0, ref.abs().max().item())
+        assert err < 1e-2, err
+
+
+def test_dot_reduce_scatter_rejects_bad_layouts(comm):
+    import torch
+    from paper_2105_04663_b200 import _capi as C
+    from paper_2105_04663_b200.executor import EvalError, _groups_arg, desc
+    from paper_2105_04663_b200.ir import DType, Shape
+    lib, s = C.lib(), torch.cuda.current_stream().cuda_stream
+    garr, ng, gs = _groups_arg([[0]])
+    a = torch.zeros((1, 256, 64), device="cuda", dtype=torch.bfloat16)
+    b = torch.zeros((1, 64, 256), device="cuda", dtype=torch.bfloat16)
+    o = torch.zeros((1, 256, 256), device="cuda", dtype=torch.bfloat16)
+    sh = Shape((256, 256), DType.BF16)
+    with pytest.raises(EvalError):   # not the last output dim
+        C.check(lib.spmd_dot_reduce_scatter(comm.handle, desc(a, Shape((256, 64), DType.BF16)),
+                                            desc(b, Shape((64, 256), DType.BF16)), desc(o, sh),
+                                            ctypes.byref(_dd()), 0, garr, ng, gs, s), "rs")
+
+
+@pytest.mark.parametrize("engine", [0, 1])
+@pytest.mark.parametrize("dim", [0, 1])
+def test_peer_all_gather_world_of_one(comm, engine, dim):
+    import torch
+    from paper_2105_04663_b200 import _capi as C
+    from paper_2105_04663_b200.executor import _groups_arg, desc
+    from paper_2105_04663_b200.ir import DType, Shape
+    lib, s = C.lib(), torch.cuda.current_stream().cuda_stream
+    garr, ng, gs = _groups_arg([[0]])
+    x = torch.randn((1, 48, 80), device="cuda")
+    y = torch.empty_like(x)
+    sh = Shape((48, 80), DType.F32)
+    for ch in (0, 1):
+        y.zero_()
+        C.check(lib.spmd_peer_all_gather(comm.handle, desc(x, sh), desc(y, sh), dim, garr, ng, gs,
+                                         8 << 20, ch, engine, s), "peer_all_gather")
+        torch.cuda.synchronize()
+        assert torch.equal(x, y)
+    C.check(lib.spmd_check_device_errors(s), "device")
