@@ -50,6 +50,7 @@ struct GemmShape {
   bf16* sc_dst[8];
   const uint32_t* sc_epoch;
   int sc_tma;           // scatter through per-destination bulk-tensor store maps
+  int store_hint;       // 1: output stores with an L2 evict_first policy
 };
 
 // Per-destination store maps of the reduce-scatter epilogue: rank j's heap as
@@ -478,6 +479,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
     // ---------------- epilogue (both CTAs, own TMEM half) ----------------
     const int ew = warp - EPI_WARP0;
     uint8_t* epi = smem + L::EPI_OFF + ew * 2 * EPI_STAGE_BYTES;
+    uint64_t store_pol = 0;
+    if (g.store_hint) asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(store_pol));
     const int par = g.scatter ? (int)((*(volatile const uint32_t*)g.sc_epoch + 1) & 1) : 0;
     const int64_t par_off = (int64_t)par * g.sc_g * g.sc_slot;
     int chunk = 0;
@@ -498,7 +501,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
         if (g.tma_store) {
           if (col < g.N)
             epi_store_chunk(&map_c, epi + (chunk++ & 1) * EPI_STAGE_BYTES, r, g.relu, col,
-                            m * BM2 + rank * HALF + ew * 32, b, lane);
+                            m * BM2 + rank * HALF + ew * 32, b, lane, store_pol);
         } else if (g.scatter && g.sc_tma) {
           if (col < g.N) {
             const int j = (int)(col / g.sc_chunk);
@@ -707,6 +710,12 @@ int dot_tcgen05(const spmd_tensor& lhs, const spmd_tensor& rhs, const spmd_tenso
     g.group = group;
     g.raster_n = raster;
     g.hint = hint;
+    static int store_hint = -1;
+    if (store_hint < 0) {
+      const char* e = getenv("SPMD_GEMM_STORE_HINT");
+      store_hint = e ? atoi(e) : 0;
+    }
+    g.store_hint = store_hint;
   }
   // tensor-map batch dims: innermost first
   OperandView va, vb;

@@ -196,7 +196,8 @@ __device__ __forceinline__ void bulk_wait_all() {
 // (row0 + lane), columns col..col+31.  `stage` is 512-byte aligned.
 __device__ __forceinline__ void epi_store_chunk(const CUtensorMap* map, uint8_t* stage,
                                                 const uint32_t (&r)[32], bool relu, int col,
-                                                int row0, int batch, int lane) {
+                                                int row0, int batch, int lane,
+                                                uint64_t store_policy = 0) {
   // Buffer reuse: the store issued from this buffer two chunks ago must have
   // finished reading shared memory.
   if (lane == 0) bulk_wait_read_le1();
@@ -219,11 +220,20 @@ __device__ __forceinline__ void epi_store_chunk(const CUtensorMap* map, uint8_t*
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   __syncwarp();
   if (lane == 0) {
-    asm volatile(
-        "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
-            reinterpret_cast<uint64_t>(map)),
-        "r"(smem_u32(stage)), "r"(col), "r"(row0), "r"(batch)
-        : "memory");
+    if (store_policy) {
+      // streamed output: evict first so it does not displace reused operands
+      asm volatile(
+          "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group.L2::cache_hint"
+          " [%0, {%2, %3, %4}], [%1], %5;" ::"l"(reinterpret_cast<uint64_t>(map)),
+          "r"(smem_u32(stage)), "r"(col), "r"(row0), "r"(batch), "l"(store_policy)
+          : "memory");
+    } else {
+      asm volatile(
+          "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
+              reinterpret_cast<uint64_t>(map)),
+          "r"(smem_u32(stage)), "r"(col), "r"(row0), "r"(batch)
+          : "memory");
+    }
     asm volatile("cp.async.bulk.commit_group;" ::: "memory");
   }
 }

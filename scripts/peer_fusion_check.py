@@ -121,20 +121,27 @@ def main():
 
     mesh = (1, world) if world <= 2 else (2, world // 2)
     small = dict(B=4, S=256, M=1024, N=8, D=64, H=4096)
-    ex1, x1, n1 = layer(comm, rank, world, dev, mesh, small, True)
-    ex0, x0, n0 = layer(comm, rank, world, dev, mesh, small, False)
-    a = ex1.run(x1)[0]
-    b = ex0.run(x0)[0]
-    torch.cuda.synchronize()
-    e = rel(a, b)
-    es = [None] * world
-    dist.all_gather_object(es, e)
-    if rank == 0:
-        print(json.dumps({"section": "layer_small", "mesh": mesh, "fused_dot_rs": n1,
-                          "unfused_dot_rs": n0, "max_rel": max(es)}), flush=True)
-    if not (max(es) < 2e-2 and n1 > 0 and n0 == 0):
-        failed.append("layer_small")
-    del ex1, ex0, x1, x0
+    meshes = [mesh] + ([(1, world)] if world > 2 else [])
+    for lm in meshes:
+        for eng in ("auto", "ce", "sm"):
+            ex1, x1, n1 = layer(comm, rank, world, dev, lm, small, True,
+                                {"SPMD_PEER_AG_ENGINE": eng})
+            ex0, x0, n0 = layer(comm, rank, world, dev, lm, small, False, {"SPMD_PEER_AG": "0"})
+            a = ex1.run(x1)[0]
+            b = ex0.run(x0)[0]
+            torch.cuda.synchronize()
+            e = rel(a, b)
+            es = [None] * world
+            dist.all_gather_object(es, e)
+            if rank == 0:
+                print(json.dumps({"section": "layer_small", "mesh": lm, "engine": eng,
+                                  "fused_dot_rs": n1, "unfused_dot_rs": n0,
+                                  "peer_all_gathers": sum(1 for v in ex1._peer_engine.values()
+                                                          if v >= 0),
+                                  "max_rel": max(es)}), flush=True)
+            if not (max(es) < 2e-2 and n1 > 0 and n0 == 0):
+                failed.append(f"layer_small{lm}:{eng}")
+            del ex1, ex0, x1, x0
 
     if "--perf" in sys.argv:
         dims = dict(B=16, S=1024, M=8192, N=128, D=256, H=65536)
