@@ -1,0 +1,124 @@
+"""Executor planning on CPU (no kernels launched): fusion-group matching,
+the peer-heap layout and the all-gather engine policy.  The executor is built
+with a stand-in communicator; nothing here touches a GPU."""
+
+import os
+
+import pytest
+
+from paper_2105_04663_b200 import partition, propagate
+from paper_2105_04663_b200.executor import Executor
+from paper_2105_04663_b200.ir import DType, Op
+from paper_2105_04663_b200.workloads import transformer_layer
+
+
+class FakeComm:
+    handle = None
+    peer = 0
+
+    def ensure_workspace(self, nbytes, device):
+        pass
+
+    def ensure_peer(self, nbytes, device):
+        self.peer = nbytes
+
+
+def _layer(mesh, **env):
+    old = {k: os.environ.get(k) for k in env}
+    os.environ.update(env)
+    try:
+        world = mesh[0] * mesh[1]
+        g, _ = transformer_layer(mesh, B=4, S=256, M=1024, N=8, D=64, H=4096, dtype=DType.BF16,
+                                 with_inputs=False)
+        ann, _ = propagate(g)
+        prog = partition(ann, world, plan="fast")
+        comm = FakeComm()
+        ex = Executor(prog, nparts=1, device="cpu", comm=comm, partition_base=0, fuse=True,
+                      overlap=False)
+        return ex, comm
+    finally:
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+
+
+@pytest.mark.parametrize("mesh", [(1, 2), (2, 2), (1, 4), (2, 4)])
+def test_dot_reduce_scatter_fusion_matches_the_two_output_projections(mesh):
+    ex, comm = _layer(mesh)
+    rs = {k: v for k, v in ex._fused.items() if v[0] == "dot_rs"}
+    assert len(rs) == 2   # attention out-projection and FFN-out (2-D finalized)
+    for rid, (_, dot, r) in rs.items():
+        assert r.opcode == Op.REDUCE_SCATTER and dot.opcode == Op.DOT
+        assert r.attrs["dim"] == dot.shape.rank - 1 and r.operands[0] == dot.id
+        assert dot.id in ex._fused_skip
+        step = next(s for s in ex.steps if s.ins.id == rid)
+        assert not step.coll   # runs on the compute stream
+        assert step.ops == dot.operands
+    # other fusions still planned
+    kinds = {v[0] for v in ex._fused.values()}
+    assert {"softmax", "attention", "dot_relu"} <= kinds
+
+
+def test_peer_fusion_can_be_disabled():
+    ex, _ = _layer((2, 2), SPMD_PEER_FUSION="0", SPMD_PEER_AG="0")
+    assert not any(v[0] == "dot_rs" for v in ex._fused.values())
+    assert ex._peer_ag == {} and ex._peer_engine == {}
+    assert sum(1 for s in ex.steps if s.coll and s.ins.opcode == Op.REDUCE_SCATTER) == 2
+
+
+def test_no_peer_fusion_without_a_communicator():
+    g, _ = transformer_layer((2, 2), B=4, S=256, M=1024, N=8, D=64, H=4096, dtype=DType.BF16,
+                             with_inputs=False)
+    ann, _ = propagate(g)
+    prog = partition(ann, 4, plan="fast")
+    ex = Executor(prog, nparts=4, device="cpu", fuse=True, overlap=False)
+    assert not any(v[0] == "dot_rs" for v in ex._fused.values())
+    assert ex._peer_ag == {}
+
+
+@pytest.mark.parametrize("mesh", [(2, 2), (2, 4)])
+def test_peer_heap_layout_is_disjoint_and_aligned(mesh):
+    ex, comm = _layer(mesh)
+    rs_bytes = max(2 * r.shape.num_elements * len(r.attrs["subgroups"][0]) * 2
+                   for _, _, r in (v for v in ex._fused.values() if v[0] == "dot_rs"))
+    spans = []
+    for aid, off in ex._peer_ag.items():
+        ins = ex.by_id[aid]
+        nb = ex._shape(ins.operands[0]).num_elements * ins.shape.dtype.itemsize
+        assert off % 4096 == 0 and off >= rs_bytes
+        spans.append((off, off + nb))
+    spans.sort()
+    for (a0, a1), (b0, b1) in zip(spans, spans[1:]):
+        assert a1 <= b0
+    assert comm.peer >= spans[-1][1]
+    all_gathers = [i.id for i in ex.graph.instructions if i.opcode == Op.ALL_GATHER]
+    assert sorted(ex._peer_ag) == sorted(all_gathers)
+
+
+def test_engine_policy_under_overlap():
+    """Hoisted order: gathers with a GEMM between them and their consumer ride
+    the copy engines; exposed pair gathers use the SM pull; exposed 4-way
+    gathers stay on NCCL."""
+    for mesh in [(2, 2), (2, 4)]:
+        ex, _ = _layer(mesh)
+        ex.steps = ex._hoist_collectives(ex.steps)
+        ex.comm_stream = object()           # as if overlapping
+        eng = ex._plan_peer_engines()
+        order = [s.ins.id for s in ex.steps]
+        for aid, e in eng.items():
+            ins = ex.by_id[aid]
+            gs = len(ins.attrs["subgroups"][0])
+            i = order.index(aid)
+            first_use = next(k for k in range(i + 1, len(order))
+                             if aid in ex.steps[k].ops)
+            between = ex.steps[i + 1:first_use]
+            hidden = any(not s.coll and (s.ins.opcode == Op.DOT or
+                                         (ex._fused.get(s.ins.id) or ("",))[0] in
+                                         ("dot_relu", "attention", "dot_rs"))
+                         for s in between)
+            assert e == (0 if hidden else (1 if gs <= 2 else -1)), (mesh, aid)
+        # the weight gathers of the later projections are hidden, the first
+        # activation gather is not
+        assert 0 in eng.values() and any(v != 0 for v in eng.values())
