@@ -153,7 +153,8 @@ class _Step:
     fn: object              # callable(env, stream) -> tensor
     frees: tuple = ()
     ops: tuple = ()         # value ids read
-    coll: bool = False      # runs on the comm stream when overlapping
+    coll: bool = False      # runs on a comm stream when overlapping
+    lane: int = 0           # 0 compute stream, k >= 1: comm stream k - 1
 
 
 class Executor:
@@ -184,11 +185,13 @@ class Executor:
             self._plan_fusions()
         self.steps = self._compile()
         self.comm_stream = None
+        self.comm_streams = []
         if self.overlap:
             self.steps = self._hoist_collectives(self.steps)
             import os
             prio = int(os.environ.get("SPMD_COMM_PRIORITY", "0"))
             self.comm_stream = torch.cuda.Stream(device=self.device, priority=prio)
+            self.comm_streams = [self.comm_stream]
             # Leave SMs for the collective kernels that run under the GEMMs
             # (SPMD_COMM_SMS, default 0 = let the GEMM take every SM).
             import os
@@ -204,6 +207,34 @@ class Executor:
         else:
             self._peer_ag = {}
         self._peer_engine = self._plan_peer_engines()
+        self._assign_lanes()
+        self._lane_of = {st.cuda_stream: k + 1 for k, st in enumerate(self.comm_streams)}
+
+    def _assign_lanes(self) -> None:
+        """Collectives on comm lanes.  NCCL calls keep one lane (their order
+        per communicator must match across ranks); peer all-gathers alternate
+        between two lanes -- each lane is its own barrier channel, so two
+        independent gathers (x over Y and wq over X at the start of the C2
+        step) can overlap.  Default one lane: at C2 N=4 two lanes measured
+        16.54 vs 16.05 ms/step -- concurrent gathers share the per-GPU
+        NVLink/HBM bandwidth and slow the GEMM under them
+        (profiles/r1_comm_lanes_n4.log).  SPMD_COMM_LANES=2 enables it."""
+        import os
+        if not self.comm_streams:
+            return
+        lanes = int(os.environ.get("SPMD_COMM_LANES", "1"))
+        nxt = 0
+        for st in self.steps:
+            if not st.coll:
+                continue
+            st.lane = 1
+            if lanes > 1 and self._peer_engine.get(st.ins.id, -1) >= 0:
+                st.lane = 1 + nxt
+                nxt = (nxt + 1) % 2
+        if any(st.lane == 2 for st in self.steps):
+            torch = _torch()
+            self.comm_streams.append(torch.cuda.Stream(device=self.device,
+                                                       priority=self.comm_stream.priority))
 
     # ------------------------------------------------------------------
     def _shape(self, vid: str) -> Shape:
@@ -981,8 +1012,7 @@ class Executor:
             x, y = desc(env[a], ash), desc(out, shp)
             if op == Op.ALL_GATHER and self._peer_engine.get(ins.id, -1) >= 0:
                 # one barrier channel per issuing stream
-                ch = 1 if (self.comm_stream is not None and s == self.comm_stream.cuda_stream) \
-                    else 0
+                ch = self._lane_of.get(s, 0)
                 rc = lib.spmd_peer_all_gather(comm.handle, x, y, at["dim"], groups, ng, gs,
                                               self._peer_ag[ins.id], ch,
                                               self._peer_engine.get(ins.id, 1), s)
@@ -1041,46 +1071,49 @@ class Executor:
         return [env[o] for o in self.graph.outputs]
 
     def _run_two_streams(self, env: dict, keep: set) -> None:
-        """Compute on the current stream, collectives on ``comm_stream``;
-        cross-stream values are ordered with events, and tensors touched by
-        the comm stream are recorded on it so the caching allocator never
+        """Compute on the current stream, collectives on the comm lanes;
+        cross-stream values are ordered with events, and tensors touched by a
+        comm stream are recorded on it so the caching allocator never
         recycles them early."""
         torch = _torch()
         compute = torch.cuda.current_stream(self.device)
-        comm = self.comm_stream
-        comm.wait_stream(compute)                 # inputs / fork for graph capture
-        cs, ks = compute.cuda_stream, comm.cuda_stream
-        on_comm: dict[str, bool] = {}
+        streams = [compute] + self.comm_streams
+        for st in self.comm_streams:
+            st.wait_stream(compute)               # inputs / fork for graph capture
+        lane_of: dict[str, int] = {}
         events: dict[str, object] = {}
         for step in self.steps:
-            mine = step.coll
-            stream = comm if mine else compute
+            lane = step.lane if step.coll else 0
+            stream = streams[lane]
             for o in step.ops:
-                if on_comm.get(o, False) != mine:
-                    ev = events.get(o)
-                    if ev is None:
-                        # producer was the other stream; record a marker now
-                        # (the producer already issued everything it needs)
-                        ev = torch.cuda.Event()
-                        ev.record(compute if mine else comm)
-                        events[o] = ev
-                    stream.wait_event(ev)
-            out = step.fn(env, ks if mine else cs)
+                src = lane_of.get(o, 0)
+                if src == lane:
+                    continue
+                ev = events.get(o)
+                if ev is None:
+                    # produced on the compute stream: a marker recorded now
+                    # covers it (the producer was issued earlier)
+                    ev = torch.cuda.Event()
+                    ev.record(streams[src])
+                    events[o] = ev
+                stream.wait_event(ev)
+            out = step.fn(env, stream.cuda_stream)
             env[step.ins.id] = out
-            on_comm[step.ins.id] = mine
-            if mine:
+            lane_of[step.ins.id] = lane
+            if lane:
                 for o in step.ops:
                     t = env.get(o)
                     if t is not None and hasattr(t, "record_stream"):
-                        t.record_stream(comm)
-                out.record_stream(comm)
+                        t.record_stream(stream)
+                out.record_stream(stream)
                 ev = torch.cuda.Event()
-                ev.record(comm)
+                ev.record(stream)
                 events[step.ins.id] = ev
             for vid in step.frees:
                 if vid not in keep:
                     env.pop(vid, None)
-        compute.wait_stream(comm)                 # join
+        for st in self.comm_streams:
+            compute.wait_stream(st)               # join
 
     def timeline(self, inputs) -> list[dict]:
         """Eager run with CUDA events around every step on the stream it is
@@ -1093,14 +1126,14 @@ class Executor:
 
         def wrap(step, fn):
             def run(env, s):
-                st = self.comm_stream if (step.coll and self.comm_stream is not None) else compute
+                st = self.comm_streams[step.lane - 1] if (step.coll and step.lane) else compute
                 e0 = torch.cuda.Event(enable_timing=True)
                 e1 = torch.cuda.Event(enable_timing=True)
                 e0.record(st)
                 out = fn(env, s)
                 e1.record(st)
                 marks.append((step.ins.id, step.ins.opcode.value,
-                              "comm" if st is not compute else "compute", e0, e1))
+                              f"comm{step.lane}" if st is not compute else "compute", e0, e1))
                 return out
             return run
 
