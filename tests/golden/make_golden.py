@@ -16,7 +16,8 @@ Writes ``tests/golden/{random,named}.json.gz`` and ``*.npz``:
 * ``named``: hand-built graphs covering the BASELINE configs C1-C5 at small
   dims, the acceptance fixtures (priority Fig-4, 2-D FFW, conv halo grid,
   data formatting, MoE all-to-all), halo specs, and the reference's own
-  known-answer op/collective tests.
+  known-answer op/collective tests, and shifting-buffer pipelines (gpipe and
+  circular schedules, reference pipeline.py) with their bubble accounting.
 
 Everything is converted to this package's JSON graph format
 (``paper_2105_04663_b200.ir.graph_to_json``) so that tests never need the
@@ -475,6 +476,63 @@ def collective_known_answers(arrays):
     return cases
 
 
+# ---------------------------------------------------------------------------
+# pipelines (reference pipeline.py): configs recorded so the test rebuilds
+# the same graph with this package's builder
+# ---------------------------------------------------------------------------
+
+PIPELINES = [
+    # name, L, M, schedule, R, state_dims, body, devices
+    ("pipe_gpipe_L4_M8_add", 4, 8, "gpipe", 1, (6,), "add", 4),
+    ("pipe_gpipe_L2_M3_dot", 2, 3, "gpipe", 1, (4, 8), "dot", 2),
+    ("pipe_circ_L4_M8_R2_add", 4, 8, "circular", 2, (6,), "add", 4),
+    ("pipe_circ_L2_M4_R2_dot", 2, 4, "circular", 2, (4, 8), "dot", 2),
+    ("pipe_gpipe_L8_M8_add", 8, 8, "gpipe", 1, (16,), "add", 8),
+]
+
+
+def pipeline_body(ops, kind):
+    """Stage bodies shared by the generator (reference Op) and the tests
+    (this package's Op): x + w, or x + x.w (batched over the stage dim)."""
+    def add(b, x, ws):
+        return b.add(ops.ADD, [x, ws[0]])
+
+    def dot(b, x, ws):
+        y = b.add(ops.DOT, [x, ws[0]], {"lhs_batch": (0,), "rhs_batch": (0,),
+                                         "lhs_contracting": (2,), "rhs_contracting": (1,)})
+        return b.add(ops.ADD, [x, y])
+    return add if kind == "add" else dot
+
+
+def pipeline_weight_dims(state_dims, kind):
+    return (state_dims[-1], state_dims[-1]) if kind == "dot" else tuple(state_dims)
+
+
+def pipeline_cases(arrays):
+    from minispmd import pipeline as RP
+    out = []
+    for name, L, Mb, sched, Rr, sdims, kind, nd in PIPELINES:
+        rng = np.random.default_rng(L * 100 + Mb * 10 + Rr)
+        mesh = R.DeviceMesh.default(nd)
+        cfg = RP.PipelineConfig(L, Mb, sched, Rr)
+        wdims = pipeline_weight_dims(sdims, kind)
+        lead = (L,) if sched == "gpipe" else (L, Rr)
+        st_sh = R.mesh_split(1 + len(sdims), mesh, [0] + [-1] * len(sdims))
+        w_sh = R.mesh_split(len(lead) + len(wdims), mesh, [0] + [-1] * (len(lead) + len(wdims) - 1))
+        g = RP.build_pipeline(cfg, mesh, sdims, pipeline_body(R.Op, kind), [R.Shape(wdims)],
+                              input_sharding=R.Sharding.replicated(), state_sharding=st_sh,
+                              weight_shardings=[w_sh])
+        scale = 0.25 if kind == "dot" else 1.0
+        ins = [rng.standard_normal(sdims).astype(np.float32) for _ in range(Mb)]
+        ins.append((rng.standard_normal(lead + wdims) * scale).astype(np.float32))
+        case = run_case(name, g, ins, nd, arrays)
+        case["pipeline"] = {"L": L, "M": Mb, "schedule": sched, "R": Rr,
+                            "state_dims": list(sdims), "body": kind,
+                            "bubble": RP.bubble_stats(cfg).to_json()}
+        out.append(case)
+    return out
+
+
 def main():
     arrays = {}
     rand = []
@@ -484,6 +542,7 @@ def main():
         g, inputs = random_graph(rng, nd)
         rand.append(run_case(f"rand{seed}", g, inputs, nd, arrays))
     named = [run_case(name, g, ins, n, arrays) for name, g, ins, n in named_cases()]
+    named += pipeline_cases(arrays)
     extra = {"halo_specs": halo_specs(), "collectives": collective_known_answers(arrays)}
     for fname, obj in (("random.json.gz", rand), ("named.json.gz", named),
                        ("extra.json.gz", extra)):
