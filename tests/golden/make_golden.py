@@ -18,6 +18,9 @@ Writes ``tests/golden/{random,named}.json.gz`` and ``*.npz``:
   data formatting, MoE all-to-all), halo specs, and the reference's own
   known-answer op/collective tests, and shifting-buffer pipelines (gpipe and
   circular schedules, reference pipeline.py) with their bubble accounting.
+* ``textir``: the reference's ``print_graph`` text of every golden graph,
+  its propagated form and its SPMD program, and the ``ParseError``
+  line/column/message for a set of malformed inputs.
 
 Everything is converted to this package's JSON graph format
 (``paper_2105_04663_b200.ir.graph_to_json``) so that tests never need the
@@ -90,7 +93,11 @@ def gjson(g):
 # one case: propagate + partition + evaluate with the reference
 # ---------------------------------------------------------------------------
 
+REF_GRAPHS = {}   # name -> (reference graph, num_devices), for the text-IR fixtures
+
+
 def run_case(name, graph, inputs, num_devices, arrays, evaluate=True):
+    REF_GRAPHS[name] = (graph, num_devices)
     annotated, rep = R.propagate(graph)
     case = {"name": name, "num_devices": num_devices, "graph": gjson(graph),
             "propagation": {"iterations": rep.iterations,
@@ -533,6 +540,60 @@ def pipeline_cases(arrays):
     return out
 
 
+# ---------------------------------------------------------------------------
+# text IR (reference textir.py): printouts of every golden graph / program and
+# ParseError positions for malformed inputs
+# ---------------------------------------------------------------------------
+
+BAD_TEXTS = [
+    "graph @g {\n  %x = f32[8 parameter(0)\n  return %x\n}",
+    "%x = f32[8] parameter(0), sharding={devices=[2]0,0}",
+    "%y = f32[8] relu(%x)",
+    "graph @g {\n  %x = f32[8] parameter(0)\n  %y = f32[9] relu(%x)\n  return %y\n}",
+    "graph @g {\n  %x = q32[8] parameter(0)\n  return %x\n}",
+    "graph @g {\n  %x = f32[8] frobnicate(%x)\n  return %x\n}",
+    "graph @g {\n  %x = f32[8] parameter()\n  return %x\n}",
+    "graph @g {\n  %c = f32[2] constant()\n  return %c\n}",
+    "graph @g {\n  %c = f32[2] constant(), literal=[1.0,2.0,3.0]\n  return %c\n}",
+    "%x = f32[8] parameter(0), sharding={devices=[2,2]0,1,2,3}",
+    "%x = f32[8] parameter(0) $",
+    "graph @g {\n  %x = f32[8] parameter(0), sharding={devices=[2]0,1\n",
+    "graph @g {\n  %a = f32[4] parameter(0)\n  %b = f32[4] compare(%a, %a), direction=XX\n"
+    "  return %b\n}",
+    "graph @g {\n  %a = f32[4] parameter(0)\n  %z = f32[] constant(), literal=0.0\n"
+    "  %r = f32[] reduce(%a, %z), kind=avg, dims=[0]\n  return %r\n}",
+    "graph @g {\n  %x = f32[8] parameter(0)\n  %y = f32[8] negate(%x)\n}",
+    "",
+    "graph @g (mesh=[2,2]) {\n  %x = f32[4,4] parameter(0), sharding={devices=[2,2]0,1,2,3}\n"
+    "  return %x\n} trailing",
+    "graph @g {\n  %x = f32[4] parameter(1.5)\n  return %x\n}",
+]
+
+
+def textir_fixtures():
+    from minispmd import textir as RT
+    out = {"graphs": {}, "errors": []}
+    for name, (g, n) in REF_GRAPHS.items():
+        entry = {"graph": RT.print_graph(g)}
+        ann, _ = R.propagate(g)
+        entry["annotated"] = RT.print_graph(ann)
+        try:
+            entry["program"] = RT.print_graph(R.partition(ann, n).graph)
+        except Exception:   # noqa: BLE001 -- unsupported configurations have no program
+            pass
+        out["graphs"][name] = entry
+    for text in BAD_TEXTS:
+        try:
+            RT.parse_graph(text)
+            out["errors"].append({"text": text, "error": None})
+        except RT.ParseError as e:
+            out["errors"].append({"text": text, "error": "ParseError", "line": e.line,
+                                  "column": e.column, "message": str(e)})
+        except Exception as e:   # noqa: BLE001 -- record what the reference raises
+            out["errors"].append({"text": text, "error": type(e).__name__, "message": str(e)})
+    return out
+
+
 def main():
     arrays = {}
     rand = []
@@ -544,8 +605,9 @@ def main():
     named = [run_case(name, g, ins, n, arrays) for name, g, ins, n in named_cases()]
     named += pipeline_cases(arrays)
     extra = {"halo_specs": halo_specs(), "collectives": collective_known_answers(arrays)}
+    textir = textir_fixtures()
     for fname, obj in (("random.json.gz", rand), ("named.json.gz", named),
-                       ("extra.json.gz", extra)):
+                       ("extra.json.gz", extra), ("textir.json.gz", textir)):
         with gzip.open(os.path.join(HERE, fname), "wt") as f:
             json.dump(obj, f, sort_keys=True)
     buf = io.BytesIO()

@@ -53,3 +53,9 @@ def expected(case):
 def spmd_outputs(case):
     a = arrays()
     return {int(d): [a[k] for k in keys] for d, keys in case["spmd"].items()}
+
+
+def textir():
+    """Reference print_graph texts and ParseError positions (make_golden.py)."""
+    with gzip.open(os.path.join(HERE, "textir.json.gz"), "rt") as f:
+        return json.load(f)
