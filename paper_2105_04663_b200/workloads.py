@@ -97,6 +97,116 @@ def transformer_layer(mesh_dims=(2, 4), B=16, S=1024, M=8192, N=128, D=256, H=65
     return g, [_bf16(i) for i in ins] if dtype == DType.BF16 else ins
 
 
+def transformer_train_step(mesh_dims=(2, 4), B=16, S=1024, M=8192, N=128, D=256, H=65536,
+                           dtype=None, api=None):
+    """C2 training step: the forward layer plus its backward pass, as plain
+    dataflow (the paper's real workload).  ``api`` is the
+    package whose IR builds the graph -- this one, or the reference
+    ``minispmd`` for the golden fixtures (same names, same graph).
+
+    Inputs: x, the seven weights and the upstream gradient g = dL/d(out).
+    Outputs: out, dx and the seven weight gradients.  Only x, g and the
+    weights are annotated (2-D finalized) plus the weight
+    gradients, pinned to their weights' shardings: the gradient of every
+    weight is reduced over the data axis X, which the partitioner emits as a
+    reduce-scatter into the weight's shard -- GSPMD weight-update sharding.
+    """
+    import sys
+    api = api or sys.modules[__package__]
+    Op, Shape, RK, CD = api.Op, api.Shape, api.ReduceKind, api.CompareDirection
+    dtype = dtype or api.DType.F32
+    mesh = api.DeviceMesh.default(*mesh_dims)
+    ms = lambda r, m: api.mesh_split(r, mesh, m)
+    b = api.GraphBuilder("transformer_train", mesh)
+
+    def dot(x, w, lb, rb, lc, rc, id, sharding=None):
+        return b.add(Op.DOT, [x, w], {"lhs_batch": lb, "rhs_batch": rb,
+                                      "lhs_contracting": lc, "rhs_contracting": rc},
+                     sharding=sharding, id=id)
+
+    def tr(x, id):
+        return b.add(Op.TRANSPOSE, [x], {"permutation": (0, 2, 1, 3)}, id=id)
+
+    act_sh, qkv_sh, wo_sh, wi_sh, wt_sh = (ms(3, [0, -1, 1]), ms(3, [0, 1, -1]),
+                                           ms(3, [1, -1, 0]), ms(2, [0, 1]), ms(2, [1, 0]))
+    x = b.parameter(Shape((B, S, M), dtype), sharding=act_sh, id="x")
+    wq = b.parameter(Shape((M, N, D), dtype), sharding=qkv_sh, id="wq")
+    wk = b.parameter(Shape((M, N, D), dtype), sharding=qkv_sh, id="wk")
+    wv = b.parameter(Shape((M, N, D), dtype), sharding=qkv_sh, id="wv")
+    wo = b.parameter(Shape((N, D, M), dtype), sharding=wo_sh, id="wo")
+    wi = b.parameter(Shape((M, H), dtype), sharding=wi_sh, id="wi")
+    wt = b.parameter(Shape((H, M), dtype), sharding=wt_sh, id="wt")
+    g = b.parameter(Shape((B, S, M), dtype), sharding=act_sh, id="g")
+    # ---- forward (as transformer_layer) ----
+    q = dot(x, wq, (), (), (2,), (0,), "q")
+    k = dot(x, wk, (), (), (2,), (0,), "k")
+    v = dot(x, wv, (), (), (2,), (0,), "v")
+    logits = dot(q, k, (0, 2), (0, 2), (3,), (3,), "logits")
+    ninf = b.constant(np.float32(-np.inf), Shape((), dtype), id="ninf")
+    zero = b.constant(np.float32(0), Shape((), dtype), id="zero")
+    full = (B, N, S, S)
+    mx = b.add(Op.REDUCE, [logits, ninf], {"kind": RK.MAX, "dims": (3,)}, id="mx")
+    mxb = b.add(Op.BROADCAST, [mx], {"out_dims": full, "broadcast_dims": (0, 1, 2)}, id="mxb")
+    e = b.add(Op.EXP, [b.add(Op.SUBTRACT, [logits, mxb], id="shifted")], id="e")
+    den = b.add(Op.REDUCE, [e, zero], {"kind": RK.SUM, "dims": (3,)}, id="den")
+    denb = b.add(Op.BROADCAST, [den], {"out_dims": full, "broadcast_dims": (0, 1, 2)},
+                 id="denb")
+    probs = b.add(Op.DIVIDE, [e, denb], id="probs")
+    ctx = dot(probs, v, (0, 1), (0, 2), (3,), (1,), "ctx")
+    ctx_t = tr(ctx, "ctx_t")
+    attn = dot(ctx_t, wo, (), (), (2, 3), (0, 1), "attn_out")
+    res1 = b.add(Op.ADD, [attn, x], id="res1")
+    h = dot(res1, wi, (), (), (2,), (0,), "h")
+    act = b.add(Op.RELU, [h], id="act")
+    ffn = dot(act, wt, (), (), (2,), (0,), "ffn_out")
+    out = b.add(Op.ADD, [ffn, res1], id="out")
+    # ---- backward ----
+    d_wt = dot(act, g, (), (), (0, 1), (0, 1), "d_wt", sharding=wt_sh)
+    dact = dot(g, wt, (), (), (2,), (1,), "dact")
+    zb = b.add(Op.BROADCAST, [zero], {"out_dims": (B, S, H), "broadcast_dims": ()}, id="zero_bsh")
+    live = b.add(Op.COMPARE, [h, zb], {"direction": CD.GT}, id="relu_mask")
+    dh = b.add(Op.SELECT, [live, dact, zb], id="dh")
+    d_wi = dot(res1, dh, (), (), (0, 1), (0, 1), "d_wi", sharding=wi_sh)
+    dres1 = b.add(Op.ADD, [g, dot(dh, wi, (), (), (2,), (1,), "dres1_ffn")], id="dres1")
+    d_wo = dot(ctx_t, dres1, (), (), (0, 1), (0, 1), "d_wo", sharding=wo_sh)
+    dctx = tr(dot(dres1, wo, (), (), (2,), (2,), "dctx_t"), "dctx")
+    dprobs = dot(dctx, v, (0, 1), (0, 2), (3,), (3,), "dprobs")
+    dv = tr(dot(probs, dctx, (0, 1), (0, 1), (2,), (2,), "dv_t"), "dv")
+    # softmax: dlogits = p * (dp - sum_t(dp * p))
+    pdp = b.add(Op.MULTIPLY, [dprobs, probs], id="pdp")
+    spdp = b.add(Op.REDUCE, [pdp, zero], {"kind": RK.SUM, "dims": (3,)}, id="spdp")
+    spdpb = b.add(Op.BROADCAST, [spdp], {"out_dims": full, "broadcast_dims": (0, 1, 2)},
+                  id="spdpb")
+    dlogits = b.add(Op.MULTIPLY, [probs, b.add(Op.SUBTRACT, [dprobs, spdpb], id="dcentered")],
+                    id="dlogits")
+    dq = tr(dot(dlogits, k, (0, 1), (0, 2), (3,), (1,), "dq_t"), "dq")
+    dk = tr(dot(dlogits, q, (0, 1), (0, 2), (2,), (1,), "dk_t"), "dk")
+    d_wq = dot(x, dq, (), (), (0, 1), (0, 1), "d_wq", sharding=qkv_sh)
+    d_wk = dot(x, dk, (), (), (0, 1), (0, 1), "d_wk", sharding=qkv_sh)
+    d_wv = dot(x, dv, (), (), (0, 1), (0, 1), "d_wv", sharding=qkv_sh)
+    dxq = dot(dq, wq, (), (), (2, 3), (1, 2), "dx_q")
+    dxk = dot(dk, wk, (), (), (2, 3), (1, 2), "dx_k")
+    dxv = dot(dv, wv, (), (), (2, 3), (1, 2), "dx_v")
+    dx = b.add(Op.ADD, [b.add(Op.ADD, [b.add(Op.ADD, [dres1, dxq], id="dx1"), dxk], id="dx2"),
+                        dxv], id="dx")
+    return b.build([out, dx, d_wq, d_wk, d_wv, d_wo, d_wi, d_wt])
+
+
+def train_step_inputs(B, S, M, N, D, H, seed=0):
+    """Host inputs of ``transformer_train_step`` (x, weights ~ N(0, 1/fan_in), g)."""
+    rng = np.random.default_rng(seed)
+    f = lambda *d: rng.standard_normal(d).astype(np.float32)
+    return [f(B, S, M), f(M, N, D) / np.sqrt(M), f(M, N, D) / np.sqrt(M), f(M, N, D) / np.sqrt(M),
+            f(N, D, M) / np.sqrt(N * D), f(M, H) / np.sqrt(M), f(H, M) / np.sqrt(H),
+            f(B, S, M) / np.sqrt(B * S)]
+
+
+def transformer_train_flops(B, S, M, N, D, H) -> float:
+    """Forward + backward GEMM FLOPs: every forward contraction has two
+    backward ones of the same size (data and weight/operand gradients)."""
+    return 3.0 * transformer_flops(B, S, M, N, D, H)
+
+
 def transformer_flops(B, S, M, N, D, H) -> float:
     """Algorithmic forward FLOPs of one layer (softmax/elementwise excluded),
     SURVEY 8(d): 2T(3MND + NDM + 2MH) + 4 B N S^2 D."""

@@ -18,6 +18,8 @@ Writes ``tests/golden/{random,named}.json.gz`` and ``*.npz``:
   data formatting, MoE all-to-all), halo specs, and the reference's own
   known-answer op/collective tests, and shifting-buffer pipelines (gpipe and
   circular schedules, reference pipeline.py) with their bubble accounting.
+* C2 training steps (forward + backward layer, weight gradients
+  reduce-scattered into the weights' shardings) on 1x2 / 2x2 / 2x4 meshes.
 * ``textir``: the reference's ``print_graph`` text of every golden graph,
   its propagated form and its SPMD program, and the ``ParseError``
   line/column/message for a set of malformed inputs.
@@ -594,6 +596,28 @@ def textir_fixtures():
     return out
 
 
+# ---------------------------------------------------------------------------
+# C2 training step (forward + backward), built by this package's workload
+# function with the REFERENCE IR (api=minispmd): same graph, reference run
+# ---------------------------------------------------------------------------
+
+TRAIN_MESHES = [(1, 2), (2, 2), (2, 4)]
+TRAIN_DIMS = dict(B=4, S=8, M=16, N=8, D=4, H=32)
+
+
+def train_cases(arrays):
+    from paper_2105_04663_b200.workloads import train_step_inputs, transformer_train_step
+    out = []
+    for mesh in TRAIN_MESHES:
+        g = transformer_train_step(mesh, api=R, **TRAIN_DIMS)
+        ins = train_step_inputs(**TRAIN_DIMS, seed=sum(mesh))
+        name = "c2_train_%dx%d" % mesh
+        case = run_case(name, g, ins, mesh[0] * mesh[1], arrays)
+        case["train"] = {"mesh": list(mesh), "dims": TRAIN_DIMS, "seed": sum(mesh)}
+        out.append(case)
+    return out
+
+
 def main():
     arrays = {}
     rand = []
@@ -604,6 +628,7 @@ def main():
         rand.append(run_case(f"rand{seed}", g, inputs, nd, arrays))
     named = [run_case(name, g, ins, n, arrays) for name, g, ins, n in named_cases()]
     named += pipeline_cases(arrays)
+    named += train_cases(arrays)
     extra = {"halo_specs": halo_specs(), "collectives": collective_known_answers(arrays)}
     textir = textir_fixtures()
     for fname, obj in (("random.json.gz", rand), ("named.json.gz", named),
