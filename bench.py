@@ -221,6 +221,18 @@ def _workload(config, world, scale=1.0):
                "wi": dims["M"], "wt": dims["H"]}
         return mesh, g, dims, transformer_flops(**dims), fan, \
             "C2 transformer layer (attention+FFN), paper dims"
+    if config == "c2train":
+        from paper_2105_04663_b200.workloads import transformer_train_flops, transformer_train_step
+        mesh = MESHES[world]
+        dims = dict(PAPER)
+        if scale != 1.0:
+            dims["B"] = max(mesh[0], int(dims["B"] * scale))
+        g = transformer_train_step(mesh, dtype=DType.BF16, **dims)
+        fan = {"wq": dims["M"], "wk": dims["M"], "wv": dims["M"], "wo": dims["N"] * dims["D"],
+               "wi": dims["M"], "wt": dims["H"], "g": dims["B"] * dims["S"]}
+        return mesh, g, dims, transformer_train_flops(**dims), fan, \
+            "C2 training step (forward + backward layer, weight gradients reduce-scattered), " \
+            "paper dims"
     if config == "c3":
         d = dict(C3)
         g, _ = moe_layer(world, dtype=DType.BF16, with_inputs=False, **d)
@@ -264,7 +276,7 @@ def _moe_masks(inputs, names, dims, dev, seed):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--config", default="c2", choices=["c2", "c3", "c4"])
+    ap.add_argument("--config", default="c2", choices=["c2", "c2train", "c3", "c4"])
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
@@ -529,11 +541,11 @@ def main():
     if rank == 0:
         per_gpu = value / world
         cfg = {"workload": wdesc, "model_dims": dims, "mesh": list(mesh),
-               "parallelism": ("dp%dxmp%d" % mesh) if args.config == "c2" else
+               "parallelism": ("dp%dxmp%d" % mesh) if args.config in ("c2", "c2train") else
                ("expert%d" % world if args.config == "c3" else "spatial%d" % world),
                "plan": "fast", "l2": "inputs larger than L2 (weights+activations)",
                "collectives_per_step": stats["counts"]}
-        if args.config == "c2":
+        if args.config in ("c2", "c2train"):
             cfg.update(global_batch=dims["B"], seq_len=dims["S"])
         line = {
             "metric": METRIC if args.config == "c2" else
