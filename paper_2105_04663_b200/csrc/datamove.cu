@@ -17,7 +17,9 @@
 namespace spmd {
 
 
-template <typename T, typename I, int V>
+// SPLAT: the innermost dim broadcasts one source element (source stride 0);
+// each 16-byte output group repeats it.
+template <typename T, typename I, int V, bool SPLAT = false>
 __global__ void strided_copy_kernel(const T* __restrict__ src, T* __restrict__ dst, CopyArgs a,
                                     int64_t nparts) {
   const I per = (I)(a.n / V);
@@ -59,6 +61,12 @@ __global__ void strided_copy_kernel(const T* __restrict__ src, T* __restrict__ d
     }
     if (V == 1) {
       dst[d0] = src[so];
+    } else if (SPLAT) {
+      const T v = src[so];
+      T f[V];
+#pragma unroll
+      for (int j = 0; j < V; ++j) f[j] = v;
+      *reinterpret_cast<uint4*>(dst + d0) = *reinterpret_cast<uint4*>(f);
     } else {
       *reinterpret_cast<uint4*>(dst + d0) = *reinterpret_cast<const uint4*>(src + so);
     }
@@ -204,6 +212,25 @@ int launch_copy(const void* src, void* dst, int dtype, CopyArgs a, int64_t npart
              (reinterpret_cast<uintptr_t>(dst) & 15) == 0 && a.sbase % V == 0 &&
              a.dbase % V == 0 && a.spart % V == 0 && a.dpart % V == 0;
   for (int k = 0; vec && k < a.rank - 1; ++k) vec = a.sst[k] % V == 0 && a.dst[k] % V == 0;
+  // Innermost dim broadcasts (source stride 0): splat 16-byte groups.
+  bool splat = !vec && a.rank >= 1 && a.sst[a.rank - 1] == 0 && a.dst[a.rank - 1] == 1 &&
+               a.shape[a.rank - 1] % V == 0 && a.ndyn == 0 &&
+               (reinterpret_cast<uintptr_t>(dst) & 15) == 0 && a.dbase % V == 0 &&
+               a.dpart % V == 0;
+  for (int k = 0; splat && k < a.rank - 1; ++k) splat = a.dst[k] % V == 0;
+  if (splat) {
+    const int64_t w = a.n / V * nparts;
+    const bool sm = a.n * nparts < (int64_t)1 << 31;
+    SPMD_DISPATCH_BYTES(dtype, T, {
+      if (sm)
+        strided_copy_kernel<T, uint32_t, 16 / sizeof(T), true><<<grid_for(w, 256), 256, 0, s>>>(
+            (const T*)src, (T*)dst, a, nparts);
+      else
+        strided_copy_kernel<T, uint64_t, 16 / sizeof(T), true><<<grid_for(w, 256), 256, 0, s>>>(
+            (const T*)src, (T*)dst, a, nparts);
+    });
+    return launched(s);
+  }
   // The kernel walks groups of V consecutive last-dim elements (element-unit
   // index math is unchanged; each group is contiguous on both sides).
   const int64_t work = (vec ? a.n / V : a.n) * nparts;

@@ -98,6 +98,33 @@ __global__ void reduce_thread_kernel(const T* __restrict__ in, const T* __restri
   }
 }
 
+// Float reduction of a contiguous trailing run (the reduced dims are the
+// innermost ones): one warp per output, 16-byte loads, fp32 accumulation.
+template <typename T>
+__global__ void __launch_bounds__(256) reduce_rows_vec_kernel(const T* __restrict__ in,
+                                                             const T* __restrict__ init,
+                                                             T* __restrict__ out, int64_t rows,
+                                                             int64_t L, int64_t rows_per_part,
+                                                             int kind) {
+  constexpr int V = 16 / sizeof(T);
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t row = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); row < rows;
+       row += warps) {
+    const uint4* x = reinterpret_cast<const uint4*>(in + row * L);
+    float acc = identity<float>(kind);
+    for (int64_t c = lane; c < L / V; c += 32) {
+      const uint4 w = __ldcs(x + c);
+      const T* e = reinterpret_cast<const T*>(&w);
+#pragma unroll
+      for (int j = 0; j < V; ++j) acc = combine<float>(kind, acc, ld<T>(e[j]));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc = combine<float>(kind, acc, __shfl_xor_sync(~0u, acc, o));
+    if (lane == 0) out[row] = st<T>(combine<float>(kind, acc, ld<T>(init[row / rows_per_part])));
+  }
+}
+
 // Row softmax over a contiguous last dim of length L: one warp per row, the
 // row held in registers when L <= 32*32, else three streaming passes.
 template <typename T, int PER_LANE>
@@ -259,6 +286,24 @@ extern "C" int spmd_reduce(spmd_tensor in, spmd_tensor init, spmd_tensor out, co
   if (a.nout * nparts == 0) return SPMD_OK;
   cudaStream_t s = as_stream(stream);
   const bool inner_reduced = in.rank > 0 && red[in.rank - 1];
+  // reduced dims == a contiguous trailing run -> rows of length nred
+  bool trailing = inner_reduced;
+  for (int k = 0; k < in.rank; ++k) trailing = trailing && (red[k] == (k >= in.rank - ndims));
+  if (trailing && (in.dtype == SPMD_BF16 || in.dtype == SPMD_F32)) {
+    const int V = 16 / elem_size(in.dtype);
+    if (a.nred % V == 0 && (reinterpret_cast<uintptr_t>(in.data) & 15) == 0) {
+      const int64_t rows = a.nout * nparts;
+      if (in.dtype == SPMD_BF16)
+        reduce_rows_vec_kernel<bf16><<<grid_for(rows * 32, 256), 256, 0, s>>>(
+            (const bf16*)in.data, (const bf16*)init.data, (bf16*)out.data, rows, a.nred, a.nout,
+            kind);
+      else
+        reduce_rows_vec_kernel<float><<<grid_for(rows * 32, 256), 256, 0, s>>>(
+            (const float*)in.data, (const float*)init.data, (float*)out.data, rows, a.nred,
+            a.nout, kind);
+      return launched(s);
+    }
+  }
   SPMD_DISPATCH(in.dtype, T, {
     if (inner_reduced || a.nout * nparts < 148 * 64) {
       int64_t warps = a.nout * nparts;
