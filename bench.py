@@ -272,6 +272,7 @@ def _moe_masks(inputs, names, dims, dev, seed):
     C.check(lib.spmd_moe_masks(desc(ex, Shape((Bl, S), DType.S32)), desc(sl, Shape((Bl, S), DType.S32)),
                                desc(gt, Shape((Bl, S), DType.F32)), desc(inputs[di], msh),
                                desc(inputs[ci], msh), 1, st), "masks")
+    return ex, sl, gt
 
 
 def main():
@@ -311,8 +312,6 @@ def main():
     ann, _ = propagate(g)
     prog = partition(ann, world, plan="fast")
     comm = NcclComm.from_torch_distributed() if world > 1 else None
-    ex = Executor(prog, nparts=1, device=dev, comm=comm, partition_base=rank, fuse=True,
-                  overlap=(world > 1 and not args.no_overlap))
 
     # Synthetic local shards, generated on the device (weights ~ N(0, 1/fan_in);
     # MoE dispatch/combine masks from the on-device router).
@@ -322,9 +321,18 @@ def main():
         name = src_params[p.attrs["index"]]
         inputs.append(_rand_like_shard(p.shape, dev, 1.0 / np.sqrt(fan.get(name, 1)),
                                        seed=1000 * rank + p.attrs["index"]))
+    routing = None
     if args.config == "c3":
+        # On-device top-1 router -> one-hot masks (the reference graph's
+        # inputs) and the routing itself: the dispatch / combine einsums then
+        # run as the gather kernels (bit-identical to the dense Dots).
+        from paper_2105_04663_b200.executor import Routing
         names = [src_params[p.attrs["index"]] for p in prog.graph.parameters]
-        _moe_masks(inputs, names, dims, dev, seed=rank)
+        r = Routing(*_moe_masks(inputs, names, dims, dev, seed=rank))
+        idx = {name: p.attrs["index"] for p, name in zip(prog.graph.parameters, names)}
+        routing = {idx["dispatch"]: r, idx["combine"]: r}
+    ex = Executor(prog, nparts=1, device=dev, comm=comm, partition_base=rank, fuse=True,
+                  overlap=(world > 1 and not args.no_overlap), routing=routing)
     stream = torch.cuda.current_stream(dev)
 
     def barrier():
@@ -545,6 +553,10 @@ def main():
                ("expert%d" % world if args.config == "c3" else "spatial%d" % world),
                "plan": "fast", "l2": "inputs larger than L2 (weights+activations)",
                "collectives_per_step": stats["counts"]}
+        if routing:
+            cfg["dispatch_combine"] = "moe.cu gather kernels over the on-device routing " \
+                "(bit-identical to the dense one-hot Dots)"
+
         if args.config in ("c2", "c2train"):
             cfg.update(global_batch=dims["B"], seq_len=dims["S"])
         line = {

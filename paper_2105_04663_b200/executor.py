@@ -148,6 +148,16 @@ class NcclComm:
 
 
 @dataclasses.dataclass
+class Routing:
+    """A one-hot GShard routing on the device, per local partition:
+    ``expert``/``slot`` s32 ``[P, B, S]`` (slot >= capacity = dropped) and
+    ``gate`` f32 ``[P, B, S]`` -- what ``spmd_moe_route`` produces."""
+    expert: object
+    slot: object
+    gate: object
+
+
+@dataclasses.dataclass
 class _Step:
     ins: Instruction
     fn: object              # callable(env, stream) -> tensor
@@ -162,7 +172,8 @@ class Executor:
 
     def __init__(self, program, nparts: Optional[int] = None, device=None,
                  comm: Optional[NcclComm] = None, partition_base: int = 0,
-                 fuse: bool = False, overlap: Optional[bool] = None):
+                 fuse: bool = False, overlap: Optional[bool] = None,
+                 routing: Optional[Mapping[int, "Routing"]] = None):
         torch = _torch()
         self.lib = C.lib()
         # Collectives on a dedicated stream, hoisted to issue as soon as
@@ -181,6 +192,9 @@ class Executor:
         self._consts: dict[str, object] = {}
         self._fused_skip: set[str] = set()
         self._fused: dict[str, object] = {}
+        self.routing = dict(routing or {})
+        if self.routing:
+            self._plan_moe_routing()
         if fuse:
             self._plan_fusions()
         self.steps = self._compile()
@@ -385,13 +399,35 @@ class Executor:
                     continue
             # dot / convolution -> relu epilogue
             if ins.opcode in (Op.DOT, Op.CONVOLUTION) and only_user(ins.id, Op.RELU) \
-                    and ins.shape.dtype == DType.BF16:
+                    and ins.shape.dtype == DType.BF16 and ins.id not in self._fused:
                 relu = by[users[ins.id][0]]
                 self._fused_skip.add(ins.id)
                 self._fused[relu.id] = ("dot_relu" if ins.opcode == Op.DOT else "conv_relu", ins)
         self._plan_halo_windows(users, outs)
         self._plan_attention(users, outs)
         self._plan_dot_reduce_scatter(users, outs)
+
+    def _plan_moe_routing(self):
+        """GShard dispatch / combine einsums over a declared one-hot routing
+        (``routing[param_index] = Routing(expert, slot, gate)``) run as the
+        gather kernels of moe.cu.  For a one-hot mask each output element has
+        a single nonzero term, so the result is bit-identical to the dense
+        Dot (reference tests/test_acceptance.py:326-349 consumes the same
+        masks through a Dot)."""
+        pidx = {p.id: p.attrs["index"] for p in self.params}
+        for ins in self.graph.instructions:
+            if ins.opcode != Op.DOT or ins.shape.dtype != DType.BF16:
+                continue
+            mask, other = ins.operands
+            if pidx.get(mask) not in self.routing:
+                continue
+            a = ins.attrs
+            dims = (tuple(a["lhs_batch"]), tuple(a["rhs_batch"]), tuple(a["lhs_contracting"]),
+                    tuple(a["rhs_contracting"]))
+            if dims == ((0,), (0,), (1,), (1,)) and self._shape(other).rank == 3:
+                self._fused[ins.id] = ("moe_dispatch", other, pidx[mask])
+            elif dims == ((0,), (0,), (2, 3), (1, 2)) and self._shape(other).rank == 4:
+                self._fused[ins.id] = ("moe_combine", other, pidx[mask])
 
     def _plan_dot_reduce_scatter(self, users, outs):
         """Dot whose only user is a sum reduce-scatter of its last dim (the
@@ -646,6 +682,8 @@ class Executor:
         if f[0] == "halo":
             mask = f[4]
             return tuple(f[1]) + (f[3],) + ((mask[2], mask[3]) if mask is not None else ())
+        if f[0] in ("moe_dispatch", "moe_combine"):
+            return (f[1],)
         return f[1].operands   # dot_relu / conv_relu / dot_rs: the producer's operands
 
     def _make_step(self, ins: Instruction):
@@ -670,6 +708,25 @@ class Executor:
             return self._conv_step(f[1], epilogue=1)
         if f is not None and f[0] == "dot_rs":
             return self._dot_rs_step(f[1], f[2])
+        if f is not None and f[0] in ("moe_dispatch", "moe_combine"):
+            _, x, ridx = f
+            xsh = self._shape(x)
+            r = self.routing[ridx]
+            ish = Shape(tuple(r.expert.shape[1:]), DType.S32)
+            gsh = Shape(tuple(r.gate.shape[1:]), DType.F32)
+
+            def run(env, s):
+                out = self._alloc(shp)
+                if f[0] == "moe_dispatch":
+                    rc = lib.spmd_moe_dispatch(desc(env[x], xsh), desc(r.expert, ish),
+                                               desc(r.slot, ish), desc(out, shp), P, s)
+                else:
+                    rc = lib.spmd_moe_combine(desc(env[x], xsh), desc(r.expert, ish),
+                                              desc(r.slot, ish), desc(r.gate, gsh),
+                                              desc(out, shp), P, s)
+                C.check(rc, f[0])
+                return out
+            return run
         if f is not None and f[0] == "attention":
             _, q, k, v = f
             qs, ks, vs = self._shape(q), self._shape(k), self._shape(v)

@@ -103,3 +103,52 @@ def test_dispatch_combine_equal_dense_dots():
                                ctypes.byref(dd2), 1, st), "dot")
     torch.cuda.synchronize()
     assert torch.equal(out, ref2)
+
+
+@pytest.mark.parametrize("n", [1, 2, 4])
+def test_executor_routing_equals_dense_masks(n):
+    """The partitioned C3 layer (loopback mesh of n) with a declared routing:
+    dispatch/combine Dots run as the gather kernels and the output is
+    bit-identical to the same program consuming the dense one-hot masks."""
+    import torch
+    from paper_2105_04663_b200 import _capi as C_
+    from paper_2105_04663_b200 import partition, propagate
+    from paper_2105_04663_b200.executor import Executor, Routing, upload_stacked
+    from paper_2105_04663_b200.ir import DType
+    from paper_2105_04663_b200.sharding import shard_data
+    from paper_2105_04663_b200.workloads import moe_layer
+    E, B, S, C, M, H = 8, 8, 64, 16, 128, 256
+    g, ins = moe_layer(n, E=E, B=B, S=S, C=C, M=M, H=H, dtype=DType.BF16)
+    ann, _ = propagate(g)
+    prog = partition(ann, n, plan="fast")
+    dev = torch.device("cuda", 0)
+    st = torch.cuda.current_stream().cuda_stream
+    Bl = B // n
+    rng = np.random.default_rng(n)
+    logits = torch.from_numpy(rng.standard_normal((n, Bl, S, E)).astype(np.float32)).cuda()
+    ex = torch.empty((n, Bl, S), dtype=torch.int32, device="cuda")
+    sl, gt = torch.empty_like(ex), torch.empty((n, Bl, S), dtype=torch.float32, device="cuda")
+    C_.check(C_.lib().spmd_moe_route(_t(logits, DType.F32), C, _t(ex, DType.S32),
+                                     _t(sl, DType.S32), _t(gt, DType.F32), n, st), "route")
+    disp = torch.empty((n, Bl, S, E, C), dtype=torch.bfloat16, device="cuda")
+    comb = torch.empty_like(disp)
+    C_.check(C_.lib().spmd_moe_masks(_t(ex, DType.S32), _t(sl, DType.S32), _t(gt, DType.F32),
+                                     _t(disp, DType.BF16), _t(comb, DType.BF16), n, st), "masks")
+    names = [p.id for p in ann.parameters]
+    stacked = []
+    for p_src, x, p in zip(ann.parameters, ins, prog.graph.parameters):
+        stacked.append(upload_stacked([shard_data(x, p_src.sharding, devices=range(n))[d]
+                                       for d in range(n)], p.shape, dev))
+    stacked[names.index("dispatch")] = disp
+    stacked[names.index("combine")] = comb
+    idx = {p.id: p.attrs["index"] for p in ann.parameters}
+    r = Routing(ex, sl, gt)
+    routed = Executor(prog, nparts=n, device=dev, fuse=True,
+                      routing={idx["dispatch"]: r, idx["combine"]: r})
+    kinds = sorted(v[0] for v in routed._fused.values() if v[0].startswith("moe_"))
+    assert kinds == ["moe_combine", "moe_dispatch"]
+    dense = Executor(prog, nparts=n, device=dev, fuse=True)
+    a = routed.run(stacked)[0]
+    b = dense.run(stacked)[0]
+    torch.cuda.synchronize()
+    assert torch.equal(a, b)
