@@ -479,8 +479,8 @@ def main():
                     (ex._fused.get(s.ins.id) or (None, None))[1] is top)
     print(f"[bench] step {ms:.2f} ms  ({value:.1f} TFLOP/s aggregate)", file=sys.stderr)
     env = {"__inputs__": inputs}
-    # materialise the operands of the top GEMM once
-    keep = set(top.operands)
+    # materialise the operands of the top GEMM's step once
+    keep = set(top_step.ops)
     ex.run(inputs, keep=keep)
     env.update({k: v for k, v in ex.last_env.items() if k in keep})
     for _ in range(3):

@@ -206,6 +206,20 @@ int spmd_local_all_to_all(spmd_tensor in, spmd_tensor out, int split_dim, int co
 int spmd_local_collective_permute(spmd_tensor in, spmd_tensor out, const int32_t* pairs,
                                   int npairs, int64_t nparts, void* stream);
 
+/* Convolution whose input is a halo window along H (dim 1):
+ * window = DS(mask(concat(pieces)), start), the window assembly of
+ * exchange_and_slice (reference formatting.py:109-182) feeding
+ * handle_convolution (:494-540).  The conv's TMA loads read each window row
+ * straight from its piece -- no window buffer in HBM.  Masked rows
+ * (global row + offset outside [low, high)) read as zeros: the mask's fill
+ * must be 0.  `window` gives the window shape only (data unused).
+ * SPMD_ERR_UNSUPPORTED when the conv does not qualify (spmd_halo_window +
+ * spmd_convolution then). */
+int spmd_halo_convolution(const spmd_tensor* pieces, int npieces, int axis, spmd_tensor start,
+                          int has_mask, spmd_tensor offset, int64_t low, int64_t high,
+                          int has_low, spmd_tensor window, spmd_tensor rhs, spmd_tensor out,
+                          const spmd_conv_dims* dims, int64_t nparts, void* stream);
+
 /* ---- NCCL collectives: one process per GPU over NVLink/NVSwitch -------------- */
 typedef struct spmd_comm spmd_comm;
 int spmd_comm_id_bytes(void);

@@ -87,6 +87,8 @@ _SIGNATURES = {
     "spmd_mask_range": ([_T, _T, _T, _T, _I, _I64, _I64, _I, _I64, _P], _I),
     "spmd_halo_window": ([ctypes.POINTER(_T), _I, _I, _T, _I, _T, _T, _I64, _I64, _I, _T, _I64,
                           _P], _I),
+    "spmd_halo_convolution": ([ctypes.POINTER(_T), _I, _I, _T, _I, _T, _I64, _I64, _I, _T, _T,
+                               _T, ctypes.POINTER(SpmdConvDims), _I64, _P], _I),
     "spmd_gemm_bf16": ([_P, _P, _P, _I64, _I64, _I64, _I, _P], _I),
     "spmd_moe_route": ([_T, _I, _T, _T, _T, _I64, _P], _I),
     "spmd_moe_dispatch": ([_T, _T, _T, _T, _I64, _P], _I),

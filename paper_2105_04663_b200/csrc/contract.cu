@@ -195,8 +195,9 @@ __global__ void conv_direct_kernel(const T* __restrict__ lhs, const T* __restric
 }
 
 // Implemented in conv_tcgen05.cu (NHWC bf16 implicit GEMM).
+struct ConvWindow;
 int conv_tcgen05(const spmd_tensor& lhs, const spmd_tensor& rhs, const spmd_tensor& out,
-                 const spmd_conv_dims& cd, int64_t nparts, cudaStream_t s);
+                 const spmd_conv_dims& cd, int64_t nparts, cudaStream_t s, const ConvWindow* win);
 
 }  // namespace spmd
 
@@ -290,7 +291,7 @@ extern "C" int spmd_convolution(spmd_tensor lhs, spmd_tensor rhs, spmd_tensor ou
   cudaStream_t s = as_stream(stream);
   if (numel(out) * nparts == 0) return SPMD_OK;
   if (lhs.dtype == SPMD_BF16) {
-    int rc = conv_tcgen05(lhs, rhs, out, *cd, nparts, s);
+    int rc = conv_tcgen05(lhs, rhs, out, *cd, nparts, s, nullptr);
     if (rc != SPMD_ERR_UNSUPPORTED) return rc;
   }
   int64_t ls[SPMD_MAX_RANK], rs[SPMD_MAX_RANK], os[SPMD_MAX_RANK];

@@ -26,7 +26,34 @@ struct ConvShape {
   int64_t tiles;
   int relu;
   int tma_store;
+  // Halo-window input (spmd_halo_convolution): the conv input rows are the
+  // window DS(mask(concat(pieces)), start) along H, read straight from the
+  // pieces (map_x, map_x1, map_x2); masked rows load out of bounds = zeros.
+  int win, npieces, has_mask, has_low;
+  int len[3];                  // piece extents along H
+  int buf_len, win_rows, nparts;
+  const int32_t* start;        // per-partition window start (clamped)
+  const int32_t* offset;       // per-partition global row of buffer row 0
+  int64_t low, high;
 };
+
+// Window row h (start s0, global offset off) -> (piece, row in piece);
+// row -1 = masked / outside the window.
+__device__ __forceinline__ int window_row(const ConvShape& g, int s0, int off, int h,
+                                          int& piece) {
+  piece = 0;
+  if (h < 0 || h >= g.win_rows) return -1;
+  int r = s0 + h;
+  if (g.has_mask) {
+    const int64_t gl = (int64_t)r + off;
+    if (!(gl < g.high && (!g.has_low || gl >= g.low))) return -1;
+  }
+  while (piece < g.npieces - 1 && r >= g.len[piece]) {
+    r -= g.len[piece];
+    ++piece;
+  }
+  return r;
+}
 
 template <int BN, int STAGES>
 struct ConvSmem {
@@ -53,7 +80,8 @@ __global__ void __launch_bounds__(256, 1)
     conv_bf16_tcgen05(const __grid_constant__ CUtensorMap map_x,
                       const __grid_constant__ CUtensorMap map_w,
                       const __grid_constant__ CUtensorMap map_o, bf16* __restrict__ out,
-                      ConvShape g) {
+                      ConvShape g, const __grid_constant__ CUtensorMap map_x1,
+                      const __grid_constant__ CUtensorMap map_x2) {
   typedef ConvSmem<BN, STAGES> L;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
@@ -63,6 +91,15 @@ __global__ void __launch_bounds__(256, 1)
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // halo-window input: per-partition clamped start / offset, read once
+  __shared__ int win_s0[SPMD_MAX_PARTS], win_off[SPMD_MAX_PARTS];
+  if (g.win) {
+    for (int p = threadIdx.x; p < g.nparts && p < SPMD_MAX_PARTS; p += blockDim.x) {
+      int s0 = g.start[p];
+      win_s0[p] = s0 < 0 ? 0 : (s0 > g.buf_len - g.win_rows ? g.buf_len - g.win_rows : s0);
+      win_off[p] = g.has_mask ? g.offset[p] : 0;
+    }
+  }
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -92,6 +129,7 @@ __global__ void __launch_bounds__(256, 1)
       int pn, ho, wb, ct;
       conv_tile(g, t, pn, ho, wb, ct);
       const int n = pn % g.N, p = pn / g.N;
+      int row_kh = -1, row_r = 0, row_piece = 0;   // window row of the current kh
       for (int kb = 0; kb < g.kblocks; ++kb) {
         const int tap = kb / g.cin_blocks, cb = kb - tap * g.cin_blocks;
         const int kh = tap / g.KW, kw = tap - kh * g.KW;
@@ -99,8 +137,17 @@ __global__ void __launch_bounds__(256, 1)
         uint8_t* sa = smem + s * L::STAGE_BYTES;
         uint8_t* sb = sa + L::A_BYTES;
         mbar_expect_tx(&full[s], L::STAGE_BYTES);
-        tma_load_5d(sa, &map_x, &full[s], cb * CBK, wb * CBM + kw - g.pad_w, ho + kh - g.pad_h, n,
-                    p);
+        if (!g.win) {
+          tma_load_5d(sa, &map_x, &full[s], cb * CBK, wb * CBM + kw - g.pad_w, ho + kh - g.pad_h,
+                      n, p);
+        } else {
+          if (kh != row_kh) {
+            row_kh = kh;
+            row_r = window_row(g, win_s0[p], win_off[p], ho + kh - g.pad_h, row_piece);
+          }
+          const CUtensorMap* mp = row_piece == 0 ? &map_x : (row_piece == 1 ? &map_x1 : &map_x2);
+          tma_load_5d(sa, mp, &full[s], cb * CBK, wb * CBM + kw - g.pad_w, row_r, n, p);
+        }
 #pragma unroll
         for (int c = 0; c < BN / 64; ++c)
           tma_load_5d(sb + c * (CBK * 128), &map_w, &full[s], ct * BN + c * 64, cb * CBK, kw, kh,
@@ -196,7 +243,7 @@ __global__ void __launch_bounds__(256, 1)
 
 template <int BN, int STAGES>
 static int launch_conv(const CUtensorMap& mx, const CUtensorMap& mw, const CUtensorMap& mo,
-                       bf16* out, ConvShape g,
+                       bf16* out, ConvShape g, const CUtensorMap& mx1, const CUtensorMap& mx2,
                        cudaStream_t s) {
   typedef ConvSmem<BN, STAGES> L;
   static bool configured = false;
@@ -207,12 +254,22 @@ static int launch_conv(const CUtensorMap& mx, const CUtensorMap& mw, const CUten
   }
   const int sms = sm_budget();
   int64_t grid = g.tiles < sms ? g.tiles : sms;
-  conv_bf16_tcgen05<BN, STAGES><<<(unsigned)grid, 256, L::TOTAL, s>>>(mx, mw, mo, out, g);
+  conv_bf16_tcgen05<BN, STAGES><<<(unsigned)grid, 256, L::TOTAL, s>>>(mx, mw, mo, out, g, mx1,
+                                                                       mx2);
   return launched(s);
 }
 
+struct ConvWindow {
+  const spmd_tensor* pieces;
+  int npieces, has_mask, has_low;
+  const int32_t* start;
+  const int32_t* offset;
+  int64_t low, high;
+};
+
 int conv_tcgen05(const spmd_tensor& lhs, const spmd_tensor& rhs, const spmd_tensor& out,
-                 const spmd_conv_dims& cd, int64_t nparts, cudaStream_t s) {
+                 const spmd_conv_dims& cd, int64_t nparts, cudaStream_t s,
+                 const ConvWindow* win = nullptr) {
   if (lhs.dtype != SPMD_BF16 || cd.n_spatial != 2 || lhs.rank != 4) return SPMD_ERR_UNSUPPORTED;
   // NHWC / HWIO / NHWC only.
   if (!(cd.lhs_batch == 0 && cd.lhs_spatial[0] == 1 && cd.lhs_spatial[1] == 2 &&
@@ -250,9 +307,41 @@ int conv_tcgen05(const spmd_tensor& lhs, const spmd_tensor& rhs, const spmd_tens
   vw.size[3] = g.KH, vw.stride[3] = (int64_t)g.KW * g.Cin * g.Cout;
   vw.size[4] = nparts, vw.stride[4] = numel(rhs);
   if (nparts == 1) vx.stride[4] = vw.stride[4] = 8;
-  CUtensorMap mx, mw;
-  if (!encode(&mx, lhs.data, vx, CBK, CBM) || !encode(&mw, rhs.data, vw, 64, CBK))
-    return SPMD_ERR_UNSUPPORTED;
+  CUtensorMap mx, mw, mx1, mx2;
+  memset(&mx1, 0, sizeof(mx1));
+  memset(&mx2, 0, sizeof(mx2));
+  if (!encode(&mw, rhs.data, vw, 64, CBK)) return SPMD_ERR_UNSUPPORTED;
+  if (!win) {
+    if (!encode(&mx, lhs.data, vx, CBK, CBM)) return SPMD_ERR_UNSUPPORTED;
+  } else {
+    // one map per piece: [nparts][N][len_k][W][Cin]
+    g.win = 1;
+    g.npieces = win->npieces;
+    g.has_mask = win->has_mask;
+    g.has_low = win->has_low;
+    g.start = win->start;
+    g.offset = win->offset;
+    g.low = win->low;
+    g.high = win->high;
+    g.win_rows = H;
+    g.nparts = (int)nparts;
+    if (nparts > SPMD_MAX_PARTS) return SPMD_ERR_UNSUPPORTED;
+    CUtensorMap* maps[3] = {&mx, &mx1, &mx2};
+    for (int k = 0; k < win->npieces; ++k) {
+      const spmd_tensor& pc = win->pieces[k];
+      if (pc.dtype != SPMD_BF16 || pc.rank != 4 || pc.dims[0] != g.N || pc.dims[2] != W ||
+          pc.dims[3] != g.Cin)
+        return SPMD_ERR_UNSUPPORTED;
+      OperandView vp = vx;
+      vp.size[2] = pc.dims[1];
+      vp.stride[3] = pc.dims[1] * W * g.Cin;
+      vp.stride[4] = nparts == 1 ? 8 : numel(pc);
+      if (!encode(maps[k], pc.data, vp, CBK, CBM)) return SPMD_ERR_UNSUPPORTED;
+      g.len[k] = (int)pc.dims[1];
+      g.buf_len += g.len[k];
+    }
+    if (g.buf_len < H) return SPMD_ERR_UNSUPPORTED;
+  }
   g.nwb = (g.Wo + CBM - 1) / CBM;
   g.nt = g.Cout / BN;
   g.cin_blocks = g.Cin / CBK;
@@ -263,8 +352,38 @@ int conv_tcgen05(const spmd_tensor& lhs, const spmd_tensor& rhs, const spmd_tens
   g.tma_store = encode_store_map(&mo, out.data, g.Cout, g.Wo, g.Cout, nparts * g.N * g.Ho,
                                  (int64_t)g.Wo * g.Cout);
   if (!g.tma_store) memset(&mo, 0, sizeof(mo));
-  if (BN == 256) return launch_conv<256, 4>(mx, mw, mo, (bf16*)out.data, g, s);
-  return launch_conv<128, 6>(mx, mw, mo, (bf16*)out.data, g, s);
+  if (BN == 256) return launch_conv<256, 4>(mx, mw, mo, (bf16*)out.data, g, mx1, mx2, s);
+  return launch_conv<128, 6>(mx, mw, mo, (bf16*)out.data, g, mx1, mx2, s);
 }
 
 }  // namespace spmd
+
+using namespace spmd;
+
+// Convolution whose input is a halo window along H: window =
+// DS(mask(concat(pieces)), start) (reference formatting.py:109-182 feeding
+// handle_convolution :494-540), read by the conv's TMA loads straight from
+// the pieces -- no window buffer in HBM.  `window` carries the window shape
+// (its data is not read).  Masked rows read as zeros, so the caller's mask
+// fill must be 0.  SPMD_ERR_UNSUPPORTED when the conv does not qualify.
+extern "C" int spmd_halo_convolution(const spmd_tensor* pieces, int npieces, int axis,
+                                     spmd_tensor start, int has_mask, spmd_tensor offset,
+                                     int64_t low, int64_t high, int has_low, spmd_tensor window,
+                                     spmd_tensor rhs, spmd_tensor out, const spmd_conv_dims* cd,
+                                     int64_t nparts, void* stream) {
+  SPMD_CHECK_ARG(npieces >= 1 && npieces <= 3 && cd, "halo_convolution arguments");
+  SPMD_CHECK_ARG(start.dtype == SPMD_S32 && (!has_mask || offset.dtype == SPMD_S32),
+                 "halo_convolution start/offset must be s32");
+  if (axis != 1 || window.rank != 4 || cd->lhs_spatial[0] != 1) return SPMD_ERR_UNSUPPORTED;
+  ConvWindow w;
+  w.pieces = pieces;
+  w.npieces = npieces;
+  w.has_mask = has_mask;
+  w.has_low = has_low;
+  w.start = (const int32_t*)start.data;
+  w.offset = has_mask ? (const int32_t*)offset.data : nullptr;
+  w.low = low;
+  w.high = high;
+  if (numel(out) * nparts == 0) return SPMD_OK;
+  return conv_tcgen05(window, rhs, out, *cd, nparts, as_stream(stream), &w);
+}

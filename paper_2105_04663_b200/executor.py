@@ -404,8 +404,60 @@ class Executor:
                 self._fused_skip.add(ins.id)
                 self._fused[relu.id] = ("dot_relu" if ins.opcode == Op.DOT else "conv_relu", ins)
         self._plan_halo_windows(users, outs)
+        self._plan_halo_convs(users, outs)
         self._plan_attention(users, outs)
         self._plan_dot_reduce_scatter(users, outs)
+
+    def _conv_tc_eligible(self, conv) -> bool:
+        """The NHWC/HWIO bf16 shapes conv_tcgen05 takes (conv_tcgen05.cu)."""
+        cd, win = conv.attrs["conv_dims"], conv.attrs["window"]
+        ls, rs = self._shape(conv.operands[0]), self._shape(conv.operands[1])
+        if ls.dtype != DType.BF16 or ls.rank != 4 or len(win) != 2:
+            return False
+        layout = (cd.lhs_batch, tuple(cd.lhs_spatial), cd.lhs_feature, tuple(cd.rhs_spatial),
+                  cd.rhs_in_feature, cd.rhs_out_feature, cd.out_batch, tuple(cd.out_spatial),
+                  cd.out_feature)
+        if layout != (0, (1, 2), 3, (0, 1), 2, 3, 0, (1, 2), 3):
+            return False
+        if any(w.stride != 1 or w.base_dilation != 1 or w.window_dilation != 1 for w in win):
+            return False
+        # Cout tiles of 128 or 256 channels (conv_tcgen05.cu BN)
+        return ls.dims[3] % 64 == 0 and rs.dims[3] % 128 == 0 and conv.shape.dims[2] >= 64
+
+    def _plan_halo_convs(self, users, outs):
+        """Halo window along H whose only user is a tcgen05-eligible conv ->
+        the conv reads the window rows straight from the halo pieces (no
+        window buffer; unpack bytes 0 when fused into the conv
+        loader).  Needs a zero mask fill (masked rows load as TMA zeros).
+        SPMD_HALO_CONV=0 disables it."""
+        import os
+        if os.environ.get("SPMD_HALO_CONV", "1") == "0":
+            return
+        by = self.by_id
+        for ds_id, spec in list(self._fused.items()):
+            if spec[0] != "halo" or ds_id in outs:
+                continue
+            _, pieces, axis, start, mask = spec
+            u = users.get(ds_id, [])
+            if len(u) != 1 or by[u[0]].opcode != Op.CONVOLUTION:
+                continue
+            conv = by[u[0]]
+            if conv.operands[0] != ds_id or axis != 1 or not self._conv_tc_eligible(conv):
+                continue
+            if mask is not None:
+                fill = by.get(mask[3])
+                lit = np.asarray(fill.attrs["literal"]) if fill is not None and \
+                    fill.opcode == Op.CONSTANT else None
+                if lit is None or lit.size != 1 or float(lit) != 0.0:
+                    continue
+            relu = [k for k, v in self._fused.items() if v[0] == "conv_relu" and v[1] is conv]
+            del self._fused[ds_id]
+            self._fused_skip.add(ds_id)
+            entry = ("halo_conv", conv, 1 if relu else 0, spec, ds_id)
+            if relu:
+                self._fused[relu[0]] = entry
+            else:
+                self._fused[conv.id] = entry
 
     def _plan_moe_routing(self):
         """GShard dispatch / combine einsums over a declared one-hot routing
@@ -684,6 +736,10 @@ class Executor:
             return tuple(f[1]) + (f[3],) + ((mask[2], mask[3]) if mask is not None else ())
         if f[0] in ("moe_dispatch", "moe_combine"):
             return (f[1],)
+        if f[0] == "halo_conv":
+            _, conv, _, (_, pieces, _, start, mask), _ = f
+            return tuple(pieces) + (start,) + ((mask[2],) if mask is not None else ()) + \
+                (conv.operands[1],)
         return f[1].operands   # dot_relu / conv_relu / dot_rs: the producer's operands
 
     def _make_step(self, ins: Instruction):
@@ -706,6 +762,8 @@ class Executor:
             return self._dot_step(f[1], shp, epilogue=1)
         if f is not None and f[0] == "conv_relu":
             return self._conv_step(f[1], epilogue=1)
+        if f is not None and f[0] == "halo_conv":
+            return self._halo_conv_step(*f[1:])
         if f is not None and f[0] == "dot_rs":
             return self._dot_rs_step(f[1], f[2])
         if f is not None and f[0] in ("moe_dispatch", "moe_combine"):
@@ -1005,6 +1063,55 @@ class Executor:
             C.check(lib.spmd_dot_reduce_scatter(comm.handle, desc(env[a], ash), desc(env[b], bsh),
                                                 desc(out, shp), ref, dim, groups, ng, gs, s),
                     "dot_reduce_scatter")
+            return out
+        return run
+
+    def _conv_dims(self, ins, epilogue=0):
+        cd = ins.attrs["conv_dims"]
+        c = C.SpmdConvDims()
+        c.lhs_batch, c.lhs_feature = cd.lhs_batch, cd.lhs_feature
+        c.rhs_in_feature, c.rhs_out_feature = cd.rhs_in_feature, cd.rhs_out_feature
+        c.out_batch, c.out_feature = cd.out_batch, cd.out_feature
+        c.n_spatial = len(cd.lhs_spatial)
+        for i, w in enumerate(ins.attrs["window"]):
+            c.lhs_spatial[i], c.rhs_spatial[i] = cd.lhs_spatial[i], cd.rhs_spatial[i]
+            c.out_spatial[i] = cd.out_spatial[i]
+            c.size[i], c.stride[i] = w.size, w.stride
+            c.pad_low[i], c.pad_high[i] = w.padding_low, w.padding_high
+            c.base_dilation[i], c.window_dilation[i] = w.base_dilation, w.window_dilation
+        c.epilogue = epilogue
+        return c
+
+    def _halo_conv_step(self, conv, epilogue, halo, window_id):
+        lib, P = self.lib, self.P
+        _, pieces, axis, start, mask = halo
+        psh = [self._shape(x) for x in pieces]
+        ssh = self._shape(start)
+        wsh, rsh, osh = self._shape(window_id), self._shape(conv.operands[1]), conv.shape
+        rhs = conv.operands[1]
+        c = self._conv_dims(conv, epilogue)
+        ref = ctypes.byref(c)
+        if mask is not None:
+            _, _, off, _, _, low, high, has_low = mask
+            offsh = self._shape(off)
+
+        def run(env, s):
+            out = self._alloc(osh)
+            arr = (C.SpmdTensor * len(pieces))(*[desc(env[x], sh) for x, sh in zip(pieces, psh)])
+            st = desc(env[start], ssh)
+            win = C.SpmdTensor()
+            win.dtype, win.rank = C.DTYPE_CODE[wsh.dtype], wsh.rank
+            for i, d in enumerate(wsh.dims):
+                win.dims[i] = d
+            if mask is None:
+                rc = lib.spmd_halo_convolution(arr, len(pieces), axis, st, 0, st, 0, 0, 0, win,
+                                               desc(env[rhs], rsh), desc(out, osh), ref, P, s)
+            else:
+                rc = lib.spmd_halo_convolution(arr, len(pieces), axis, st, 1,
+                                               desc(env[off], offsh), low, high, int(has_low),
+                                               win, desc(env[rhs], rsh), desc(out, osh), ref, P,
+                                               s)
+            C.check(rc, "halo_convolution")
             return out
         return run
 
