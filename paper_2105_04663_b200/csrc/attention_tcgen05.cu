@@ -309,47 +309,6 @@ __global__ void __launch_bounds__(256, 1)
 // Leader CTA issues the MMAs; S and O land in each CTA's own TMEM half;
 // softmax/P/correction/store run in both CTAs on their own rows.
 // ---------------------------------------------------------------------------
-constexpr uint32_t A_PEER_MASK = 0xFEFFFFFFu;
-
-__device__ __forceinline__ uint32_t a_cluster_rank() {
-  uint32_t r;
-  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
-  return r;
-}
-__device__ __forceinline__ void a_cluster_sync() {
-  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::
-                   : "memory");
-}
-__device__ __forceinline__ void tma_load_4d_2sm(void* dst, const CUtensorMap* map, uint64_t* bar,
-                                                int c0, int c1, int c2, int c3) {
-  asm volatile(
-      "cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
-      " [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar) & A_PEER_MASK), "r"(c0), "r"(c1),
-      "r"(c2), "r"(c3)
-      : "memory");
-}
-__device__ __forceinline__ void a_commit_mc(uint64_t* bar) {
-  asm volatile(
-      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
-      " [%0], %1;" ::"r"(smem_u32(bar)),
-      "h"((uint16_t)3)
-      : "memory");
-}
-__device__ __forceinline__ void a_mma_2sm(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc,
-                                          uint32_t idesc, uint32_t accumulate) {
-  asm volatile(
-      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d_tmem),
-      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate));
-}
-__device__ __forceinline__ void arrive_leader(uint64_t* bar) {
-  asm volatile(
-      "{\n.reg .b32 ra;\nmapa.shared::cluster.u32 ra, %0, 0;\n"
-      "mbarrier.arrive.shared::cluster.b64 _, [ra];\n}" ::"r"(smem_u32(bar))
-      : "memory");
-}
-
 template <int D>
 struct Attn2Smem {
   static constexpr int Q_BYTES = 128 * D * 2;           // own 128 rows
@@ -385,7 +344,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
   uint32_t* tmem_slot = (uint32_t*)(pv_done + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t rank = a_cluster_rank();
+  const uint32_t rank = cluster_rank();
   const bool leader = rank == 0;
   const int nSt = (g.S + 255) / 256;
   const int cl = blockIdx.x >> 1;
@@ -415,7 +374,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
   }
   tc_fence_before();
-  a_cluster_sync();
+  cluster_sync();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   const uint32_t O_COL = 0, S_COL = 256;
@@ -456,9 +415,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
       for (int c = 0; c < DC; ++c)
 #pragma unroll
         for (int k = 0; k < 4; ++k)
-          a_mma_2sm(tmem + S_COL + sb * 64, make_desc(qa + c * 16384 + k * 32, 16, 1024),
+          tc_mma_2sm(tmem + S_COL + sb * 64, make_desc(qa + c * 16384 + k * 32, 16, 1024),
                     make_desc(ka + c * 4096 + k * 32, 16, 1024), idesc_s, (c | k) != 0);
-      a_commit_mc(&s_full[sb]);
+      tc_commit_2sm_mc(&s_full[sb]);
     };
     auto issue_pv = [&](int j) {
       const int slot = j % NS, pb = j & 1;
@@ -468,10 +427,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
       const uint32_t va = smem_u32(skv + slot * L::SLOT + L::K_HALF);
 #pragma unroll
       for (int k = 0; k < 4; ++k)
-        a_mma_2sm(tmem + O_COL, make_desc(pa + k * 32, 16, 1024),
+        tc_mma_2sm(tmem + O_COL, make_desc(pa + k * 32, 16, 1024),
                   make_desc(va + k * 2048, 8192, 1024), idesc_o, (j | k) != 0);
-      a_commit_mc(&pv_done[pb]);
-      a_commit_mc(&kv_empty[slot]);
+      tc_commit_2sm_mc(&pv_done[pb]);
+      tc_commit_2sm_mc(&kv_empty[slot]);
     };
     issue_s(0);
     for (int j = 1; j < nT; ++j) {
@@ -493,7 +452,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
       tmem_ld32(tmem + lane_base + S_COL + sb * 64 + 32, r1);
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) arrive_leader(&s_free[sb]);
+      if (lane == 0) mbar_arrive_leader(&s_free[sb]);
       float s[64];
 #pragma unroll
       for (int i = 0; i < 32; ++i) {
@@ -551,7 +510,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) arrive_leader(&p_full[pb]);
+      if (lane == 0) mbar_arrive_leader(&p_full[pb]);
     }
     mbar_wait(&pv_done[(nT - 1) & 1], ((nT - 1) >> 1) & 1);
     tc_fence_after();
@@ -588,7 +547,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
     }
   }
   tc_fence_before();
-  a_cluster_sync();
+  cluster_sync();
   if (warp == 2) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem));

@@ -241,6 +241,226 @@ __global__ void __launch_bounds__(256, 1)
   }
 }
 
+// ---------------------------------------------------------------------------
+// CTA-pair variant for Cout = 128 (cta_group::2, UMMA 256 x 128): the pair
+// owns 256 consecutive output pixels of one (n, ho) row; each CTA stages its
+// 128 pixels of the input box and 64 of the 128 output channels of the
+// weights, so per-SM operand smem traffic per MMA drops by a third versus
+// the 1-CTA 128 x 128 tile (which is smem-bandwidth bound at Cout = 128).
+// ---------------------------------------------------------------------------
+constexpr int CHALF = 64;   // Cout per CTA
+
+// WRES: this CTA's half of the weights (kblocks x 8 KB) stays resident in
+// smem for the whole kernel (loaded once); only input boxes stream.
+template <int STAGES, int WRES>
+struct Conv2Smem {
+  static constexpr int A_BYTES = CBM * CBK * 2;       // 128 px x 64 ch
+  static constexpr int B_BYTES = CHALF * CBK * 2;     // 64 cout x 64 ch
+  static constexpr int STAGE_BYTES = A_BYTES + (WRES ? 0 : B_BYTES);
+  static constexpr int W_OFF = STAGES * STAGE_BYTES;  // resident weights (WRES kblocks)
+  static constexpr int BAR_OFF = W_OFF + WRES * B_BYTES;
+  static constexpr int EPI_OFF = BAR_OFF + 1024;
+  static constexpr int TOTAL = EPI_OFF + 8 * EPI_STAGE_BYTES + 1024;
+};
+
+template <int STAGES, int WRES>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
+    conv_bf16_tcgen05_2sm(const __grid_constant__ CUtensorMap map_x,
+                          const __grid_constant__ CUtensorMap map_w,
+                          const __grid_constant__ CUtensorMap map_o, ConvShape g,
+                          const __grid_constant__ CUtensorMap map_x1,
+                          const __grid_constant__ CUtensorMap map_x2) {
+  typedef Conv2Smem<STAGES, WRES> L;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint64_t* full = (uint64_t*)(smem + L::BAR_OFF);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint64_t* wfull = tempty + 2;
+  uint32_t* tmem_slot = (uint32_t*)(wfull + 1);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_rank();
+  const bool leader = rank == 0;
+  const int64_t cluster = blockIdx.x >> 1, nclusters = gridDim.x >> 1;
+  __shared__ int win_s0[SPMD_MAX_PARTS], win_off[SPMD_MAX_PARTS];
+  if (g.win) {
+    for (int p = threadIdx.x; p < g.nparts && p < SPMD_MAX_PARTS; p += blockDim.x) {
+      int s0 = g.start[p];
+      win_s0[p] = s0 < 0 ? 0 : (s0 > g.buf_len - g.win_rows ? g.buf_len - g.win_rows : s0);
+      win_off[p] = g.has_mask ? g.offset[p] : 0;
+    }
+  }
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 8);   // 4 epilogue warps x 2 CTAs
+    }
+    mbar_init(wfull, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(
+                     smem_u32(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0 && lane == 0) {
+    int s = 0;
+    uint32_t ph = 0;
+    if (WRES) {
+      // whole weight half once (single output-channel tile, one partition
+      // of weights: both guaranteed by the host)
+      if (leader) mbar_expect_tx(wfull, 2 * WRES * L::B_BYTES);
+      for (int kb = 0; kb < WRES; ++kb) {
+        const int tap = kb / g.cin_blocks, cb = kb - tap * g.cin_blocks;
+        const int kh = tap / g.KW, kw = tap - kh * g.KW;
+        tma_load_5d_2sm(smem + L::W_OFF + kb * L::B_BYTES, &map_w, wfull, rank * CHALF, cb * CBK,
+                        kw, kh, 0);
+      }
+    }
+    for (int64_t t = cluster; t < g.tiles; t += nclusters) {
+      int pn, ho, wb, ct;
+      conv_tile(g, t, pn, ho, wb, ct);
+      const int n = pn % g.N, p = pn / g.N;
+      const int w0 = wb * 2 * CBM + rank * CBM;
+      int row_kh = -1, row_r = 0, row_piece = 0;
+      for (int kb = 0; kb < g.kblocks; ++kb) {
+        const int tap = kb / g.cin_blocks, cb = kb - tap * g.cin_blocks;
+        const int kh = tap / g.KW, kw = tap - kh * g.KW;
+        mbar_wait(&empty[s], ph ^ 1);
+        uint8_t* sa = smem + s * L::STAGE_BYTES;
+        uint8_t* sb = sa + L::A_BYTES;
+        if (leader) mbar_expect_tx(&full[s], 2 * L::STAGE_BYTES);
+        (void)sb;
+        if (!g.win) {
+          tma_load_5d_2sm(sa, &map_x, &full[s], cb * CBK, w0 + kw - g.pad_w, ho + kh - g.pad_h,
+                          n, p);
+        } else {
+          if (kh != row_kh) {
+            row_kh = kh;
+            row_r = window_row(g, win_s0[p], win_off[p], ho + kh - g.pad_h, row_piece);
+          }
+          const CUtensorMap* mp = row_piece == 0 ? &map_x : (row_piece == 1 ? &map_x1 : &map_x2);
+          tma_load_5d_2sm(sa, mp, &full[s], cb * CBK, w0 + kw - g.pad_w, row_r, n, p);
+        }
+        if (!WRES)
+          tma_load_5d_2sm(sb, &map_w, &full[s], ct * 2 * CHALF + rank * CHALF, cb * CBK, kw, kh,
+                          p);
+        if (++s == STAGES) {
+          s = 0;
+          ph ^= 1;
+        }
+      }
+    }
+  } else if (warp == 1 && lane == 0 && leader) {
+    const uint32_t idesc = make_idesc(2 * CBM, 2 * CHALF, 0, 1);
+    int s = 0;
+    uint32_t ph = 0;
+    int acc = 0;
+    uint32_t acc_ph = 0;
+    if (WRES) {
+      mbar_wait(wfull, 0);
+      tc_fence_after();
+    }
+    for (int64_t t = cluster; t < g.tiles; t += nclusters) {
+      mbar_wait(&tempty[acc], acc_ph ^ 1);
+      tc_fence_after();
+      const uint32_t d_tmem = tmem + acc * 2 * CHALF;
+      for (int kb = 0; kb < g.kblocks; ++kb) {
+        mbar_wait(&full[s], ph);
+        tc_fence_after();
+        const uint32_t sa = smem_u32(smem + s * L::STAGE_BYTES);
+        const uint32_t sb = WRES ? smem_u32(smem + L::W_OFF + kb * L::B_BYTES) : sa + L::A_BYTES;
+#pragma unroll
+        for (int k = 0; k < CBK / 16; ++k)
+          tc_mma_2sm(d_tmem, make_desc(sa + k * 32, 16, 1024),
+                     make_desc(sb + k * 2048, CBK * 128, 1024), idesc, (kb | k) != 0);
+        tc_commit_2sm_mc(&empty[s]);
+        if (++s == STAGES) {
+          s = 0;
+          ph ^= 1;
+        }
+      }
+      tc_commit_2sm_mc(&tfull[acc]);
+      if (++acc == 2) {
+        acc = 0;
+        acc_ph ^= 1;
+      }
+    }
+  } else if (warp >= 4) {
+    const int ew = warp - 4;
+    uint8_t* epi = smem + L::EPI_OFF + ew * 2 * EPI_STAGE_BYTES;
+    int chunk = 0;
+    int acc = 0;
+    uint32_t acc_ph = 0;
+    for (int64_t t = cluster; t < g.tiles; t += nclusters) {
+      int pn, ho, wb, ct;
+      conv_tile(g, t, pn, ho, wb, ct);
+      mbar_wait(&tfull[acc], acc_ph);
+      tc_fence_after();
+#pragma unroll 1
+      for (int c0 = 0; c0 < 2 * CHALF; c0 += 32) {
+        uint32_t r[32];
+        tmem_ld32(tmem + ((uint32_t)(ew * 32) << 16) + acc * 2 * CHALF + c0, r);
+        epi_store_chunk(&map_o, epi + (chunk++ & 1) * EPI_STAGE_BYTES, r, g.relu,
+                        ct * 2 * CHALF + c0, wb * 2 * CBM + rank * CBM + ew * 32,
+                        pn * g.Ho + ho, lane);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_leader(&tempty[acc]);
+      if (++acc == 2) {
+        acc = 0;
+        acc_ph ^= 1;
+      }
+    }
+    if (lane == 0) bulk_wait_all();
+  }
+  tc_fence_before();
+  cluster_sync();
+  if (warp == 2) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 256;" ::"r"(tmem));
+  }
+}
+
+template <int STAGES, int WRES>
+static int launch_conv_2sm(const CUtensorMap& mx, const CUtensorMap& mw, const CUtensorMap& mo,
+                           ConvShape g, const CUtensorMap& mx1, const CUtensorMap& mx2,
+                           cudaStream_t s) {
+  typedef Conv2Smem<STAGES, WRES> L;
+  static_assert(L::TOTAL <= 232448, "conv 2-CTA smem");
+  static bool configured = false;
+  if (!configured) {
+    SPMD_CUDA_TRY(cudaFuncSetAttribute(conv_bf16_tcgen05_2sm<STAGES, WRES>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, L::TOTAL));
+    configured = true;
+  }
+  const int sms = sm_budget();
+  const int64_t clusters = g.tiles < sms / 2 ? g.tiles : sms / 2;
+  conv_bf16_tcgen05_2sm<STAGES, WRES><<<(unsigned)(2 * clusters), 256, L::TOTAL, s>>>(
+      mx, mw, mo, g, mx1, mx2);
+  return launched(s);
+}
+
+static int conv_mode() {
+  static int mode = -1;
+  if (mode < 0) {
+    const char* e = getenv("SPMD_CONV_MODE");
+    mode = (e && strcmp(e, "1sm") == 0) ? 1 : 2;
+  }
+  return mode;
+}
+
 template <int BN, int STAGES>
 static int launch_conv(const CUtensorMap& mx, const CUtensorMap& mw, const CUtensorMap& mo,
                        bf16* out, ConvShape g, const CUtensorMap& mx1, const CUtensorMap& mx2,
@@ -352,6 +572,23 @@ int conv_tcgen05(const spmd_tensor& lhs, const spmd_tensor& rhs, const spmd_tens
   g.tma_store = encode_store_map(&mo, out.data, g.Cout, g.Wo, g.Cout, nparts * g.N * g.Ho,
                                  (int64_t)g.Wo * g.Cout);
   if (!g.tma_store) memset(&mo, 0, sizeof(mo));
+  if (BN == 128 && g.tma_store && conv_mode() == 2 && g.Wo >= 2 * CBM) {
+    // CTA pairs: tiles of 256 pixels, weights boxed 64 output channels per CTA
+    CUtensorMap mw2;
+    if (encode(&mw2, rhs.data, vw, CHALF, CBK)) {
+      g.nwb = (g.Wo + 2 * CBM - 1) / (2 * CBM);
+      g.tiles = (int64_t)nparts * g.N * g.Ho * g.nwb * g.nt;
+      // 3x3 x 128 input channels: weights resident in smem (one weight set)
+      static int wres = -1;
+      if (wres < 0) {
+        const char* e = getenv("SPMD_CONV_WRES");
+        wres = e ? atoi(e) : 1;
+      }
+      if (wres && g.kblocks == 18 && g.nt == 1 && nparts == 1)
+        return launch_conv_2sm<4, 18>(mx, mw2, mo, g, mx1, mx2, s);
+      return launch_conv_2sm<7, 0>(mx, mw2, mo, g, mx1, mx2, s);
+    }
+  }
   if (BN == 256) return launch_conv<256, 4>(mx, mw, mo, (bf16*)out.data, g, mx1, mx2, s);
   return launch_conv<128, 6>(mx, mw, mo, (bf16*)out.data, g, mx1, mx2, s);
 }

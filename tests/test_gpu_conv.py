@@ -57,6 +57,9 @@ def _err(a, b):
     (1, 9, 200, 128, 128, ((0, 0), (1, 1)), True),      # partitioned layout: H halo explicit
     (2, 8, 64, 64, 256, ((1, 1), (1, 1)), False),
     (1, 4, 300, 192, 64, ((2, 0), (0, 2)), True),
+    (2, 6, 512, 128, 128, ((1, 1), (1, 1)), True),      # CTA pairs, resident weights
+    (1, 5, 384, 128, 128, ((0, 0), (1, 1)), False),     # pairs, partial last 256-px tile
+    (1, 4, 512, 64, 128, ((1, 1), (1, 1)), False),      # pairs, streamed weights (Cin 64)
 ])
 def test_conv_tcgen05(N, H, W, Ci, Co, pads, relu):
     import torch
