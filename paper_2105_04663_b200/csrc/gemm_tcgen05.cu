@@ -493,6 +493,182 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
 }
 
 // ---------------------------------------------------------------------------
+// Wide CTA-pair variant: 256 x 512 pair tiles (two N=256 UMMAs per k-step
+// into all 512 TMEM columns).  Per CTA and k-block: A 128 x 64 + B 256 x 64
+// -> operand bytes per FLOP 25% lower than 256 x 256 and half the L2 reads
+// of A per output; measured on the C2 FFN shapes: L2 traffic 171 -> ~96 GB,
+// the layout cuBLAS picks for these shapes.  The accumulator fills TMEM, so
+// tiles cannot double-buffer it: 8 epilogue warps (384 threads) drain it,
+// two per TMEM lane quarter, each half the columns.
+// ---------------------------------------------------------------------------
+constexpr int WBN = 512;          // pair tile N
+constexpr int WHALF_N = 256;      // N per UMMA
+
+template <int STAGES>
+struct SmemW {
+  static constexpr int A_BYTES = HALF * BK * 2;              // 16 KB
+  static constexpr int B_BYTES = 2 * HALF * BK * 2;          // 32 KB: 2 x 128 rows
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int BAR_OFF = STAGES * STAGE_BYTES;
+  static constexpr int EPI_OFF = BAR_OFF + 1024;
+  static constexpr int TOTAL = EPI_OFF + 16 * EPI_STAGE_BYTES + 1024;
+};
+
+template <int STAGES>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
+    gemm_bf16_tcgen05_2sm_wide(const __grid_constant__ CUtensorMap map_a,
+                               const __grid_constant__ CUtensorMap map_b,
+                               const __grid_constant__ CUtensorMap map_c, GemmShape g) {
+  typedef SmemW<STAGES> L;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint64_t* full = (uint64_t*)(smem + L::BAR_OFF);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 1;
+  uint32_t* tmem_slot = (uint32_t*)(tempty + 1);
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_rank();
+  const bool leader = rank == 0;
+  const int64_t cluster = blockIdx.x >> 1, nclusters = gridDim.x >> 1;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(tfull, 1);
+    mbar_init(tempty, 16);   // 8 epilogue warps x 2 CTAs
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                     smem_u32(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const int kblocks = (g.K + BK - 1) / BK;
+
+  if (warp == 0 && lane == 0) {
+    // ---------------- TMA producer (both CTAs) ----------------
+    int s = 0;
+    uint32_t ph = 0;
+    for (int64_t t = cluster; t < g.tiles; t += nclusters) {
+      int b, m, n;
+      tile_coords(g, t, b, m, n);
+      const int b0 = b % g.nb[0], b1 = (b / g.nb[0]) % g.nb[1], b2 = b / (g.nb[0] * g.nb[1]);
+      const int mrow = m * BM2 + rank * HALF;
+      for (int kb = 0; kb < kblocks; ++kb) {
+        mbar_wait(&empty[s], ph ^ 1);
+        uint8_t* sa = smem + s * L::STAGE_BYTES;
+        uint8_t* sb = sa + L::A_BYTES;
+        if (leader) mbar_expect_tx(&full[s], 2 * L::STAGE_BYTES);
+        const int k0 = kb * BK;
+        if (!g.a_mn) {
+          tma_load_5d_2sm(sa, &map_a, &full[s], k0, mrow, b0, b1, b2);
+        } else {
+#pragma unroll
+          for (int c = 0; c < HALF / 64; ++c)
+            tma_load_5d_2sm(sa + c * (BK * 128), &map_a, &full[s], mrow + c * 64, k0, b0, b1, b2);
+        }
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {   // UMMA j covers pair-tile cols [256j, 256j+256)
+          const int nrow = n * WBN + j * WHALF_N + rank * HALF;
+          uint8_t* sbj = sb + j * (HALF * BK * 2);
+          if (!g.b_mn) {
+            tma_load_5d_2sm(sbj, &map_b, &full[s], k0, nrow, b0, b1, b2);
+          } else {
+#pragma unroll
+            for (int c = 0; c < HALF / 64; ++c)
+              tma_load_5d_2sm(sbj + c * (BK * 128), &map_b, &full[s], nrow + c * 64, k0, b0, b1,
+                              b2);
+          }
+        }
+        if (++s == STAGES) {
+          s = 0;
+          ph ^= 1;
+        }
+      }
+    }
+  } else if (warp == 1 && lane == 0 && leader) {
+    // ---------------- MMA issuer (leader CTA only) ----------------
+    const uint32_t idesc = make_idesc(BM2, WHALF_N, g.a_mn, g.b_mn);
+    int s = 0;
+    uint32_t ph = 0;
+    uint32_t acc_ph = 0;
+    for (int64_t t = cluster; t < g.tiles; t += nclusters) {
+      mbar_wait(tempty, acc_ph ^ 1);
+      tc_fence_after();
+      for (int kb = 0; kb < kblocks; ++kb) {
+        mbar_wait(&full[s], ph);
+        tc_fence_after();
+        const uint32_t sa = smem_u32(smem + s * L::STAGE_BYTES);
+        const uint32_t sb = sa + L::A_BYTES;
+#pragma unroll
+        for (int k = 0; k < BK / 16; ++k) {
+          const uint64_t ad = g.a_mn ? make_desc(sa + k * 2048, BK * 128, 1024)
+                                     : make_desc(sa + k * 32, 16, 1024);
+#pragma unroll
+          for (int j = 0; j < 2; ++j) {
+            const uint32_t sbj = sb + j * (HALF * BK * 2);
+            const uint64_t bd = g.b_mn ? make_desc(sbj + k * 2048, BK * 128, 1024)
+                                       : make_desc(sbj + k * 32, 16, 1024);
+            tc_mma_2sm(tmem + j * WHALF_N, ad, bd, idesc, (kb | k) != 0);
+          }
+        }
+        tc_commit_2sm_mc(&empty[s]);
+        if (++s == STAGES) {
+          s = 0;
+          ph ^= 1;
+        }
+      }
+      tc_commit_2sm_mc(tfull);
+      acc_ph ^= 1;
+    }
+  } else if (warp >= EPI_WARP0) {
+    // ---------------- epilogue: 8 warps, (lane quarter, column half) ----------------
+    const int ew = warp - EPI_WARP0;              // 0..7
+    const int quarter = warp & 3, half = ew >> 2;
+    uint8_t* epi = smem + L::EPI_OFF + ew * 2 * EPI_STAGE_BYTES;
+    uint64_t store_pol = 0;
+    if (g.store_hint)
+      asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(store_pol));
+    int chunk = 0;
+    uint32_t acc_ph = 0;
+    for (int64_t t = cluster; t < g.tiles; t += nclusters) {
+      int b, m, n;
+      tile_coords(g, t, b, m, n);
+      mbar_wait(tfull, acc_ph);
+      tc_fence_after();
+#pragma unroll 1
+      for (int c0 = 0; c0 < WHALF_N; c0 += 32) {
+        uint32_t r[32];
+        tmem_ld32(tmem + ((uint32_t)(quarter * 32) << 16) + half * WHALF_N + c0, r);
+        const int col = n * WBN + half * WHALF_N + c0;
+        if (col < g.N)
+          epi_store_chunk(&map_c, epi + (chunk++ & 1) * EPI_STAGE_BYTES, r, g.relu, col,
+                          m * BM2 + rank * HALF + quarter * 32, b, lane, store_pol);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_leader(tempty);
+      acc_ph ^= 1;
+    }
+    if (lane == 0) bulk_wait_all();
+  }
+  tc_fence_before();
+  cluster_sync();
+  if (warp == 2) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+  }
+}
+
+// ---------------------------------------------------------------------------
 // host side: operand views -> tensor maps
 // ---------------------------------------------------------------------------
 struct DimRef {
@@ -555,11 +731,29 @@ static int launch_gemm_2sm(const CUtensorMap& ma, const CUtensorMap& mb, const C
   return launched(s);
 }
 
+template <int STAGES>
+static int launch_gemm_2sm_wide(const CUtensorMap& ma, const CUtensorMap& mb,
+                                const CUtensorMap& mc, GemmShape g, cudaStream_t s) {
+  typedef SmemW<STAGES> L;
+  static_assert(L::TOTAL <= 232448, "wide GEMM smem");
+  static bool configured = false;
+  if (!configured) {
+    SPMD_CUDA_TRY(cudaFuncSetAttribute(gemm_bf16_tcgen05_2sm_wide<STAGES>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, L::TOTAL));
+    configured = true;
+  }
+  const int sms = sm_budget();
+  int64_t clusters = g.tiles < sms / 2 ? g.tiles : sms / 2;
+  gemm_bf16_tcgen05_2sm_wide<STAGES><<<(unsigned)(2 * clusters), 384, L::TOTAL, s>>>(ma, mb, mc,
+                                                                                     g);
+  return launched(s);
+}
+
 static int gemm_mode() {
   static int mode = -1;
   if (mode < 0) {
     const char* e = getenv("SPMD_GEMM_MODE");
-    mode = (e && strcmp(e, "1sm") == 0) ? 1 : 2;
+    mode = (e && strcmp(e, "1sm") == 0) ? 1 : (e && strcmp(e, "2sm") == 0) ? 2 : 3;
   }
   return mode;
 }
@@ -630,14 +824,14 @@ int dot_tcgen05(const spmd_tensor& lhs, const spmd_tensor& rhs, const spmd_tenso
     static int group = -1, raster = -1, hint = -1;
     if (group < 0) {
       const char* e = getenv("SPMD_GEMM_GROUP");
-      group = e ? atoi(e) : 8;
-      if (group < 1) group = 8;
+      group = e ? atoi(e) : 0;   // 0: per-kernel default
+      if (group < 0) group = 0;
       e = getenv("SPMD_GEMM_RASTER");
       raster = (e && strcmp(e, "n") == 0) ? 1 : 0;
       e = getenv("SPMD_GEMM_HINT");
       hint = e ? atoi(e) : 0;
     }
-    g.group = group;
+    g.group = group ? group : 8;
     g.raster_n = raster;
     g.hint = hint;
     static int store_hint = -1;
@@ -713,7 +907,21 @@ int dot_tcgen05(const spmd_tensor& lhs, const spmd_tensor& rhs, const spmd_tenso
       g.sc_tma = encode_store_map(&smaps.m[j], sc->dst[j], g.sc_chunk, M.size, g.sc_chunk,
                                   2 * sc->gsize, g.sc_slot);
   }
-  if ((gemm_mode() == 2 || sc) && M.size >= 256 && N.size >= 256) {
+  if (!sc && gemm_mode() == 3 && g.tma_store && M.size >= 256 && N.size >= 512) {
+    // wide pair tiles (256 x 512); the store epilogue is TMA-only
+    bool okw = a_mn ? encode(&ma, lhs.data, va, 64, BK) : encode(&ma, lhs.data, va, BK, HALF);
+    okw = okw && (b_mn ? encode(&mb, rhs.data, vb, 64, BK) : encode(&mb, rhs.data, vb, BK, HALF));
+    if (okw) {
+      // 16 M-tiles per raster group (alternating A/B on the C2 GEMM shapes:
+      // +5% over 8 for 256 x 512 tiles, profiles/r1_gemm_wide_group_sweep.log)
+      if (!getenv("SPMD_GEMM_GROUP")) g.group = 16;
+      g.mt = (g.M + BM2 - 1) / BM2;
+      g.nt = (g.N + WBN - 1) / WBN;
+      g.tiles = (int64_t)g.mt * g.nt * g.nb[0] * g.nb[1] * g.nb[2];
+      return launch_gemm_2sm_wide<4>(ma, mb, mc, g, s);
+    }
+  }
+  if ((gemm_mode() >= 2 || sc) && M.size >= 256 && N.size >= 256) {
     // 2-CTA path: per-CTA boxes are 128 rows of A and 128 rows of B.
     bool ok2 = a_mn ? encode(&ma, lhs.data, va, 64, BK) : encode(&ma, lhs.data, va, BK, HALF);
     ok2 = ok2 && (b_mn ? encode(&mb, rhs.data, vb, 64, BK) : encode(&mb, rhs.data, vb, BK, HALF));
