@@ -263,7 +263,8 @@ int spmd_dot_reduce_scatter(spmd_comm* comm, spmd_tensor lhs, spmd_tensor rhs, s
  * barrier.  `channel` (0..3): one per issuing stream -- all ranks must issue
  * the calls of a channel in the same order.  `engine`: 0 = copy engines (no
  * SMs: for gathers hidden under GEMMs), 1 = SM pull kernel (16-byte NVLink
- * loads: for gathers on the critical path). */
+ * loads, whole GPU: for gathers on the critical path), 3 = SM pull with 32
+ * CTAs (background, co-resident beside a persistent GEMM). */
 int spmd_peer_all_gather(spmd_comm* comm, spmd_tensor in, spmd_tensor out, int dim,
                          const int32_t* groups, int ngroups, int gsize, int64_t heap_offset,
                          int channel, int engine, void* stream);

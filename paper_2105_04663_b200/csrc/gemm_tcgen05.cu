@@ -518,7 +518,8 @@ template <int STAGES>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
     gemm_bf16_tcgen05_2sm_wide(const __grid_constant__ CUtensorMap map_a,
                                const __grid_constant__ CUtensorMap map_b,
-                               const __grid_constant__ CUtensorMap map_c, GemmShape g) {
+                               const __grid_constant__ CUtensorMap map_c, GemmShape g,
+                               const __grid_constant__ ScatterMaps smaps) {
   typedef SmemW<STAGES> L;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
@@ -637,6 +638,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
     uint64_t store_pol = 0;
     if (g.store_hint)
       asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(store_pol));
+    // reduce-scatter epilogue (peer.cu): parity buffer of this epoch
+    const int par = g.scatter ? (int)((*(volatile const uint32_t*)g.sc_epoch + 1) & 1) : 0;
     int chunk = 0;
     uint32_t acc_ph = 0;
     for (int64_t t = cluster; t < g.tiles; t += nclusters) {
@@ -644,14 +647,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
       tile_coords(g, t, b, m, n);
       mbar_wait(tfull, acc_ph);
       tc_fence_after();
+      const int row0 = m * BM2 + rank * HALF + quarter * 32;
 #pragma unroll 1
       for (int c0 = 0; c0 < WHALF_N; c0 += 32) {
         uint32_t r[32];
         tmem_ld32(tmem + ((uint32_t)(quarter * 32) << 16) + half * WHALF_N + c0, r);
         const int col = n * WBN + half * WHALF_N + c0;
-        if (col < g.N)
-          epi_store_chunk(&map_c, epi + (chunk++ & 1) * EPI_STAGE_BYTES, r, g.relu, col,
-                          m * BM2 + rank * HALF + quarter * 32, b, lane, store_pol);
+        if (col >= g.N) continue;
+        if (g.scatter) {
+          const int j = (int)(col / g.sc_chunk);
+          epi_store_chunk(&smaps.m[j], epi + (chunk++ & 1) * EPI_STAGE_BYTES, r, g.relu,
+                          (int)(col - j * g.sc_chunk), row0, par * g.sc_g + g.sc_pos, lane);
+        } else {
+          epi_store_chunk(&map_c, epi + (chunk++ & 1) * EPI_STAGE_BYTES, r, g.relu, col, row0,
+                          b, lane, store_pol);
+        }
       }
       tc_fence_before();
       __syncwarp();
@@ -659,6 +669,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
       acc_ph ^= 1;
     }
     if (lane == 0) bulk_wait_all();
+    // peer stores globally visible before the completion signal (peer.cu)
+    if (g.scatter) __threadfence_system();
   }
   tc_fence_before();
   cluster_sync();
@@ -733,7 +745,8 @@ static int launch_gemm_2sm(const CUtensorMap& ma, const CUtensorMap& mb, const C
 
 template <int STAGES>
 static int launch_gemm_2sm_wide(const CUtensorMap& ma, const CUtensorMap& mb,
-                                const CUtensorMap& mc, GemmShape g, cudaStream_t s) {
+                                const CUtensorMap& mc, GemmShape g, const ScatterMaps& smaps,
+                                cudaStream_t s) {
   typedef SmemW<STAGES> L;
   static_assert(L::TOTAL <= 232448, "wide GEMM smem");
   static bool configured = false;
@@ -745,7 +758,7 @@ static int launch_gemm_2sm_wide(const CUtensorMap& ma, const CUtensorMap& mb,
   const int sms = sm_budget();
   int64_t clusters = g.tiles < sms / 2 ? g.tiles : sms / 2;
   gemm_bf16_tcgen05_2sm_wide<STAGES><<<(unsigned)(2 * clusters), 384, L::TOTAL, s>>>(ma, mb, mc,
-                                                                                     g);
+                                                                                     g, smaps);
   return launched(s);
 }
 
@@ -907,7 +920,7 @@ int dot_tcgen05(const spmd_tensor& lhs, const spmd_tensor& rhs, const spmd_tenso
       g.sc_tma = encode_store_map(&smaps.m[j], sc->dst[j], g.sc_chunk, M.size, g.sc_chunk,
                                   2 * sc->gsize, g.sc_slot);
   }
-  if (!sc && gemm_mode() == 3 && g.tma_store && M.size >= 256 && N.size >= 512) {
+  if (gemm_mode() == 3 && (sc ? g.sc_tma : g.tma_store) && M.size >= 256 && N.size >= 512) {
     // wide pair tiles (256 x 512); the store epilogue is TMA-only
     bool okw = a_mn ? encode(&ma, lhs.data, va, 64, BK) : encode(&ma, lhs.data, va, BK, HALF);
     okw = okw && (b_mn ? encode(&mb, rhs.data, vb, 64, BK) : encode(&mb, rhs.data, vb, BK, HALF));
@@ -918,7 +931,7 @@ int dot_tcgen05(const spmd_tensor& lhs, const spmd_tensor& rhs, const spmd_tenso
       g.mt = (g.M + BM2 - 1) / BM2;
       g.nt = (g.N + WBN - 1) / WBN;
       g.tiles = (int64_t)g.mt * g.nt * g.nb[0] * g.nb[1] * g.nb[2];
-      return launch_gemm_2sm_wide<4>(ma, mb, mc, g, s);
+      return launch_gemm_2sm_wide<4>(ma, mb, mc, g, smaps, s);
     }
   }
   if ((gemm_mode() >= 2 || sc) && M.size >= 256 && N.size >= 256) {

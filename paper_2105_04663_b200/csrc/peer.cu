@@ -299,7 +299,9 @@ extern "C" int spmd_peer_all_gather(spmd_comm* c, spmd_tensor in, spmd_tensor ou
   SPMD_CUDA_TRY(cudaMemcpyAsync(c->heap + CTRL_BYTES + heap_offset, in.data, bytes,
                                 cudaMemcpyDeviceToDevice, s));
   if ((rc = peer_barrier(c, channel, s))) return rc;
-  const bool sm = engine == 1 && gsize <= 8 && w % 16 == 0 &&
+  // engine 1: SM pull over the whole GPU (critical path); 3: background SM
+  // pull, 32 CTAs that co-reside beside a persistent GEMM (like NCCL's)
+  const bool sm = (engine == 1 || engine == 3) && gsize <= 8 && w % 16 == 0 &&
                   (reinterpret_cast<uintptr_t>(in.data) & 15) == 0 &&
                   (reinterpret_cast<uintptr_t>(out.data) & 15) == 0;
   if (sm) {
@@ -315,7 +317,8 @@ extern "C" int spmd_peer_all_gather(spmd_comm* c, spmd_tensor in, spmd_tensor ou
     }
     const int64_t work = (bytes / 16) * gsize;
     int64_t grid = (work + 4 * 512 - 1) / (4 * 512);
-    if (grid > 148 * 4) grid = 148 * 4;
+    const int64_t cap = engine == 3 ? 32 : 148 * 4;
+    if (grid > cap) grid = cap;
     peer_pull_kernel<<<(unsigned)grid, 512, 0, s>>>(pa, (uint4*)out.data);
     if ((rc = launched(s))) return rc;
     return peer_barrier(c, channel, s);

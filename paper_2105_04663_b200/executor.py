@@ -225,32 +225,35 @@ class Executor:
         self._lane_of = {st.cuda_stream: k + 1 for k, st in enumerate(self.comm_streams)}
 
     def _assign_lanes(self) -> None:
-        """Collectives on comm lanes.  NCCL calls keep one lane (their order
-        per communicator must match across ranks); peer all-gathers alternate
-        between two lanes -- each lane is its own barrier channel, so two
-        independent gathers (x over Y and wq over X at the start of the C2
-        step) can overlap.  Default one lane: at C2 N=4 two lanes measured
-        16.54 vs 16.05 ms/step -- concurrent gathers share the per-GPU
-        NVLink/HBM bandwidth and slow the GEMM under them
-        (profiles/r1_comm_lanes_n4.log).  SPMD_COMM_LANES=2 enables it."""
+        """Collectives on comm lanes.  NCCL calls keep lane 1 (their order per
+        communicator must match across ranks).  Peer all-gathers on the
+        critical path (SM-pull engine: no GEMM hides them) take lane 2, its
+        own barrier channel, so they never queue behind weight prefetches on
+        the copy engines -- at C2 N=4 the res1 gather otherwise waited 1.6 ms
+        behind the w_out prefetch (profiles/r1_timeline_c2_n4_wide.log).
+        SPMD_COMM_LANES=1: one lane; =2: alternate all peer gathers (measured
+        slower); default "critical".
+        """
         import os
         if not self.comm_streams:
             return
-        lanes = int(os.environ.get("SPMD_COMM_LANES", "1"))
+        mode = os.environ.get("SPMD_COMM_LANES", "critical")
         nxt = 0
         for st in self.steps:
             if not st.coll:
                 continue
             st.lane = 1
-            if lanes > 1 and self._peer_engine.get(st.ins.id, -1) >= 0:
+            eng = self._peer_engine.get(st.ins.id, -1)
+            if mode == "2" and eng >= 0:
                 st.lane = 1 + nxt
                 nxt = (nxt + 1) % 2
+            elif mode == "critical" and eng == 1:
+                st.lane = 2
         if any(st.lane == 2 for st in self.steps):
             torch = _torch()
             self.comm_streams.append(torch.cuda.Stream(device=self.device,
                                                        priority=self.comm_stream.priority))
 
-    # ------------------------------------------------------------------
     def _shape(self, vid: str) -> Shape:
         return self.by_id[vid].shape
 
@@ -290,6 +293,9 @@ class Executor:
         forces one."""
         import os
         force = os.environ.get("SPMD_PEER_AG_ENGINE", "auto")
+        # hidden gathers: copy engines (0), background SM pull (3) or NCCL (-1)
+        hidden_engine = {"ce": 0, "sm": 3, "nccl": -1}[
+            os.environ.get("SPMD_PEER_HIDDEN_ENGINE", "ce")]
         heavy_ops = (Op.DOT, Op.CONVOLUTION)
         heavy_fused = ("dot_relu", "conv_relu", "attention", "dot_rs")
         eng = {}
@@ -311,7 +317,7 @@ class Executor:
                         hidden = True
                         break
             gs = len(st.ins.attrs["subgroups"][0])
-            eng[st.ins.id] = 0 if hidden else (1 if gs <= 2 else -1)
+            eng[st.ins.id] = hidden_engine if hidden else (1 if gs <= 2 else -1)
         return eng
 
     def _workspace_bytes(self) -> int:
