@@ -159,8 +159,12 @@ def run_reference(args):
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": "C2 transformer layer (bounded CPU sample)",
-                       "mesh": list(mesh), "parallelism": "dp%dxmp%d" % mesh},
+            "config": {"workload": "C2 transformer layer (attention+FFN), paper dims",
+                       "model_dims": dict(PAPER), "mesh": list(mesh),
+                       "parallelism": "dp%dxmp%d" % mesh, "global_batch": PAPER["B"],
+                       "seq_len": PAPER["S"],
+                       "cpu_sample": "each step times a bounded sample of the workload, "
+                                     "see cpu_baseline.sample"},
             "cpu_baseline": {"value": v, "unit": "TFLOP/s", "cores": cores, "kind": "port",
                              "sample": sample},
             "e2e": {"value": v, "unit": "TFLOP/s", "h2d_bytes_per_step": 0,
