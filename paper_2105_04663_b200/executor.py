@@ -225,14 +225,15 @@ class Executor:
         self._lane_of = {st.cuda_stream: k + 1 for k, st in enumerate(self.comm_streams)}
 
     def _assign_lanes(self) -> None:
-        """Collectives on comm lanes.  NCCL calls keep lane 1 (their order per
-        communicator must match across ranks).  Peer all-gathers on the
-        critical path (SM-pull engine: no GEMM hides them) take lane 2, its
-        own barrier channel, so they never queue behind weight prefetches on
-        the copy engines -- at C2 N=4 the res1 gather otherwise waited 1.6 ms
-        behind the w_out prefetch (profiles/r1_timeline_c2_n4_wide.log).
-        SPMD_COMM_LANES=1: one lane; =2: alternate all peer gathers (measured
-        slower); default "critical".
+        """Collectives on comm lanes.  Lane 1 carries only the background
+        prefetch gathers (peer copy-engine / background SM-pull engines: a
+        GEMM hides them); everything on the critical path -- exposed peer
+        gathers and every NCCL call (one stream, so NCCL's per-communicator
+        order is the same on all ranks) -- takes lane 2 with its own barrier
+        channel, so it never queues behind a prefetch.  At C2 N=4 the res1
+        gather otherwise waited 1.6 ms behind the w_out prefetch
+        (profiles/r1_timeline_c2_n4_wide.log).  SPMD_COMM_LANES=1: one lane;
+        =2: alternate all peer gathers (measured slower); default "critical".
         """
         import os
         if not self.comm_streams:
@@ -247,7 +248,7 @@ class Executor:
             if mode == "2" and eng >= 0:
                 st.lane = 1 + nxt
                 nxt = (nxt + 1) % 2
-            elif mode == "critical" and eng == 1:
+            elif mode == "critical" and eng not in (0, 3):
                 st.lane = 2
         if any(st.lane == 2 for st in self.steps):
             torch = _torch()
