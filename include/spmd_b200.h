@@ -168,6 +168,11 @@ int spmd_halo_window(const spmd_tensor* pieces, int npieces, int axis, spmd_tens
  * D in {64,128,256}; tcgen05 with S/O accumulators in TMEM. */
 int spmd_attention(spmd_tensor q, spmd_tensor k, spmd_tensor v, spmd_tensor out, float scale,
                    int64_t nparts, void* stream);
+/* Same, output layout selectable: out_bsnd = 1 writes out[B,S,N,D] (the
+ * transposed context the out-projection consumes, App. A ctx_t) straight from
+ * the epilogue's TMA store. */
+int spmd_attention_layout(spmd_tensor q, spmd_tensor k, spmd_tensor v, spmd_tensor out,
+                          float scale, int out_bsnd, int64_t nparts, void* stream);
 /* Row softmax over the last dim: out = exp(x - max) / sum(exp(x - max)). */
 int spmd_softmax_lastdim(spmd_tensor in, spmd_tensor out, int64_t nparts, void* stream);
 

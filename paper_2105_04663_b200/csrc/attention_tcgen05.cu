@@ -609,16 +609,18 @@ static int launch_attention_2sm(const CUtensorMap& mq, const CUtensorMap& mk,
 using namespace spmd;
 
 // q [B,S,N,D], k/v [B,T,N,D] -> out [B,N,S,D] = softmax(scale * q.k^T) . v
-extern "C" int spmd_attention(spmd_tensor q, spmd_tensor k, spmd_tensor v, spmd_tensor out,
-                              float scale, int64_t nparts, void* stream) {
+extern "C" int spmd_attention_layout(spmd_tensor q, spmd_tensor k, spmd_tensor v,
+                                     spmd_tensor out, float scale, int out_bsnd, int64_t nparts,
+                                     void* stream) {
   SPMD_CHECK_ARG(q.dtype == SPMD_BF16 && k.dtype == SPMD_BF16 && v.dtype == SPMD_BF16 &&
                      out.dtype == SPMD_BF16 && q.rank == 4 && k.rank == 4 && v.rank == 4 &&
                      out.rank == 4,
-                 "attention expects bf16 q[B,S,N,D], k/v[B,T,N,D], out[B,N,S,D]");
+                 "attention expects bf16 q[B,S,N,D], k/v[B,T,N,D], out[B,N,S,D] or [B,S,N,D]");
   const int64_t B = q.dims[0], S = q.dims[1], N = q.dims[2], D = q.dims[3], T = k.dims[1];
+  const int64_t od1 = out_bsnd ? S : N, od2 = out_bsnd ? N : S;
   SPMD_CHECK_ARG(k.dims[0] == B && k.dims[2] == N && k.dims[3] == D && v.dims[0] == B &&
                      v.dims[1] == T && v.dims[2] == N && v.dims[3] == D && out.dims[0] == B &&
-                     out.dims[1] == N && out.dims[2] == S && out.dims[3] == D,
+                     out.dims[1] == od1 && out.dims[2] == od2 && out.dims[3] == D,
                  "attention shape mismatch");
   if (!(D == 64 || D == 128 || D == 256)) return SPMD_ERR_UNSUPPORTED;
   const int64_t Bp = B * nparts;
@@ -626,7 +628,8 @@ extern "C" int spmd_attention(spmd_tensor q, spmd_tensor k, spmd_tensor v, spmd_
   bool ok = encode4(&mq, q.data, D, S, N, Bp, N * D, D, S * N * D, 128) &&
             encode4(&mk, k.data, D, T, N, Bp, N * D, D, T * N * D, 64) &&
             encode4(&mv, v.data, D, T, N, Bp, N * D, D, T * N * D, 64) &&
-            encode4(&mo, out.data, D, S, N, Bp, D, S * D, N * S * D, 128);
+            (out_bsnd ? encode4(&mo, out.data, D, S, N, Bp, N * D, D, S * N * D, 128)
+                      : encode4(&mo, out.data, D, S, N, Bp, D, S * D, N * S * D, 128));
   if (!ok) return SPMD_ERR_UNSUPPORTED;
   AttnShape g;
   g.S = (int)S;
@@ -650,4 +653,10 @@ extern "C" int spmd_attention(spmd_tensor q, spmd_tensor k, spmd_tensor v, spmd_
   if (D == 64) return launch_attention<64>(mq, mk, mv, mo, g, s);
   if (D == 128) return launch_attention<128>(mq, mk, mv, mo, g, s);
   return launch_attention<256>(mq, mk, mv, mo, g, s);
+}
+
+// out[B,N,S,D] (the logits->softmax->ctx Dot chain's output layout).
+extern "C" int spmd_attention(spmd_tensor q, spmd_tensor k, spmd_tensor v, spmd_tensor out,
+                              float scale, int64_t nparts, void* stream) {
+  return spmd_attention_layout(q, k, v, out, scale, 0, nparts, stream);
 }

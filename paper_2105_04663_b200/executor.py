@@ -560,7 +560,16 @@ class Executor:
             if qs.rank != 4 or ks.dims != vs.dims or qs.dims[3] not in (64, 128, 256):
                 continue
             self._fused_skip.update({logits.id, div_id})
-            self._fused[ctx.id] = ("attention", q, k, v)
+            # ctx -> transpose(0,2,1,3) (App. A ctx_t): the kernel stores
+            # [B,S,N,D] directly
+            cu = users.get(ctx.id, [])
+            tr = by[cu[0]] if len(cu) == 1 else None
+            if tr is not None and ctx.id not in outs and tr.opcode == Op.TRANSPOSE and \
+                    tuple(tr.attrs["permutation"]) == (0, 2, 1, 3):
+                self._fused_skip.add(ctx.id)
+                self._fused[tr.id] = ("attention", q, k, v, 1)
+            else:
+                self._fused[ctx.id] = ("attention", q, k, v, 0)
 
     def _plan_halo_windows(self, users, outs):
         """dynamic-slice(mask(concat(left, shard, right))) -> one halo-window
@@ -737,7 +746,7 @@ class Executor:
         if f[0] == "mask":
             return (f[1], f[2], f[3])
         if f[0] == "attention":
-            return f[1:]
+            return f[1:4]
         if f[0] == "halo":
             mask = f[4]
             return tuple(f[1]) + (f[3],) + ((mask[2], mask[3]) if mask is not None else ())
@@ -793,13 +802,14 @@ class Executor:
                 return out
             return run
         if f is not None and f[0] == "attention":
-            _, q, k, v = f
+            _, q, k, v, bsnd = f
             qs, ks, vs = self._shape(q), self._shape(k), self._shape(v)
 
             def run(env, s):
                 out = self._alloc(shp)
-                C.check(lib.spmd_attention(desc(env[q], qs), desc(env[k], ks), desc(env[v], vs),
-                                           desc(out, shp), 1.0, P, s), "attention")
+                C.check(lib.spmd_attention_layout(desc(env[q], qs), desc(env[k], ks),
+                                                  desc(env[v], vs), desc(out, shp), 1.0, bsnd, P,
+                                                  s), "attention")
                 return out
             return run
         if f is not None and f[0] == "halo":

@@ -85,3 +85,24 @@ def test_executor_uses_fused_attention():
     b = plain.run(stacked)[0].float()
     err = (a - b).abs().max().item() / max(1.0, b.abs().max().item())
     assert err < 2e-2, err
+
+
+@pytest.mark.parametrize("D", [64, 256])
+def test_attention_writes_bsnd_layout(D):
+    """out_bsnd=1: the kernel stores the transposed context [B,S,N,D]
+    directly; equal to the [B,N,S,D] output permuted."""
+    import torch
+    from paper_2105_04663_b200 import _capi as C
+    from paper_2105_04663_b200.executor import desc
+    from paper_2105_04663_b200.ir import DType, Shape
+    B, S, N = 2, 256, 4
+    torch.manual_seed(D)
+    q, k, v = (torch.randn(1, B, S, N, D, device="cuda").bfloat16() for _ in range(3))
+    a = _attn(q, k, v, scale=D ** -0.5)
+    out = torch.empty((1, B, S, N, D), dtype=torch.bfloat16, device="cuda")
+    sh = Shape((B, S, N, D), DType.BF16)
+    C.check(C.lib().spmd_attention_layout(desc(q, sh), desc(k, sh), desc(v, sh), desc(out, sh),
+                                          D ** -0.5, 1, 1,
+                                          torch.cuda.current_stream().cuda_stream), "attention")
+    torch.cuda.synchronize()
+    assert torch.equal(out, a.permute(0, 1, 3, 2, 4))
