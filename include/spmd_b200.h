@@ -261,6 +261,15 @@ int64_t spmd_comm_peer_bytes(spmd_comm* comm);
 int spmd_dot_reduce_scatter(spmd_comm* comm, spmd_tensor lhs, spmd_tensor rhs, spmd_tensor out,
                             const spmd_dot_dims* dims, int dim, const int32_t* groups,
                             int ngroups, int gsize, void* stream);
+/* out = all-to-all(split 1, concat 0)(dot(lhs, rhs)) for a dot with one
+ * batch dim (output dim 0): the expert FFN-out einsum + GShard combine
+ * all-to-all (C3).  The GEMM epilogue stores each output row chunk into the
+ * owning member's heap (slot pos * batch + b), then a barrier and one copy.
+ * bf16; needs a heap of >= 4 * numel(out) bytes; SPMD_ERR_UNSUPPORTED when
+ * the layout does not qualify (spmd_dot + spmd_all_to_all then). */
+int spmd_dot_all_to_all(spmd_comm* comm, spmd_tensor lhs, spmd_tensor rhs, spmd_tensor out,
+                        const spmd_dot_dims* dims, int split_dim, int concat_dim,
+                        const int32_t* groups, int ngroups, int gsize, void* stream);
 /* All-gather through the peer heap (reference simulator.py:353-359 piece
  * order): stage `in` at heap data offset `heap_offset` (256-aligned, caller
  * assigned, disjoint from the reduce-scatter region and from other live

@@ -114,6 +114,8 @@ _SIGNATURES = {
     "spmd_comm_peer_bytes": ([_P], _I64),
     "spmd_dot_reduce_scatter": ([_P, _T, _T, _T, ctypes.POINTER(SpmdDotDims), _I, _PI32, _I, _I,
                                  _P], _I),
+    "spmd_dot_all_to_all": ([_P, _T, _T, _T, ctypes.POINTER(SpmdDotDims), _I, _I, _PI32, _I, _I,
+                             _P], _I),
     "spmd_peer_all_gather": ([_P, _T, _T, _I, _PI32, _I, _I, _I64, _I, _I, _P], _I),
 }
 

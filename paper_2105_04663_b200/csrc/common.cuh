@@ -29,6 +29,11 @@ struct GemmScatter {
   int gsize, pos;
   void* dst[8];
   const uint32_t* epoch;
+  // rows != 0: all-to-all mode -- output ROW chunks of `rchunk` rows go to
+  // group member row / rchunk, slot slot_base + batch of nslots (no reduce)
+  int rows;
+  int64_t rchunk;
+  int slot_base, nslots;
 };
 // Implemented in gemm_tcgen05.cu: returns SPMD_ERR_UNSUPPORTED when the
 // layout cannot be expressed with TMA descriptors (or, with `sc`, when the

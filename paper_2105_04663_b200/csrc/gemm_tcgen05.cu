@@ -51,6 +51,9 @@ struct GemmShape {
   const uint32_t* sc_epoch;
   int sc_tma;           // scatter through per-destination bulk-tensor store maps
   int store_hint;       // 1: output stores with an L2 evict_first policy
+  int sc_rows;          // all-to-all (row-chunk) scatter, wide kernel only
+  int64_t sc_rchunk;
+  int sc_slot_base, sc_nslots;
 };
 
 // Per-destination store maps of the reduce-scatter epilogue: rank j's heap as
@@ -654,7 +657,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
         tmem_ld32(tmem + ((uint32_t)(quarter * 32) << 16) + half * WHALF_N + c0, r);
         const int col = n * WBN + half * WHALF_N + c0;
         if (col >= g.N) continue;
-        if (g.scatter) {
+        if (g.scatter && g.sc_rows) {
+          if (row0 >= g.M) continue;
+          const int j = (int)(row0 / g.sc_rchunk);
+          epi_store_chunk(&smaps.m[j], epi + (chunk++ & 1) * EPI_STAGE_BYTES, r, g.relu, col,
+                          (int)(row0 - j * g.sc_rchunk),
+                          par * g.sc_nslots + g.sc_slot_base + b, lane);
+        } else if (g.scatter) {
           const int j = (int)(col / g.sc_chunk);
           epi_store_chunk(&smaps.m[j], epi + (chunk++ & 1) * EPI_STAGE_BYTES, r, g.relu,
                           (int)(col - j * g.sc_chunk), row0, par * g.sc_g + g.sc_pos, lane);
@@ -895,7 +904,29 @@ int dot_tcgen05(const spmd_tensor& lhs, const spmd_tensor& rhs, const spmd_tenso
                   encode_store_map(&mc, out.data, g.N, g.M, g.N, nbat, g.out_batch_stride);
     if (!g.tma_store) memset(&mc, 0, sizeof(mc));
   }
-  if (sc) {
+  if (sc && sc->rows) {
+    // All-to-all epilogue (wide kernel): one batch dim (the concat dim), the
+    // split dim = the leading GEMM row dim, whole row chunks per member.
+    const int64_t nbat = (int64_t)g.nb[0] * g.nb[1] * g.nb[2];
+    if (M.size < 256 || N.size < 512 || gemm_mode() != 3 ||
+        sc->gsize < 1 || sc->gsize > 8 || sc->rchunk % 32 != 0 ||
+        sc->rchunk * sc->gsize != M.size || nbat * sc->gsize != sc->nslots)
+      return SPMD_ERR_UNSUPPORTED;
+    g.tma_store = 0;
+    g.scatter = 1;
+    g.sc_rows = 1;
+    g.sc_g = sc->gsize;
+    g.sc_pos = sc->pos;
+    g.sc_rchunk = sc->rchunk;
+    g.sc_slot_base = sc->slot_base;
+    g.sc_nslots = sc->nslots;
+    g.sc_epoch = sc->epoch;
+    g.sc_tma = 1;
+    for (int j = 0; g.sc_tma && j < sc->gsize; ++j)
+      g.sc_tma = encode_store_map(&smaps.m[j], sc->dst[j], N.size, sc->rchunk, N.size,
+                                  2 * sc->nslots, sc->rchunk * N.size);
+    if (!g.sc_tma) return SPMD_ERR_UNSUPPORTED;
+  } else if (sc) {
     // Reduce-scatter epilogue: 2-CTA kernel, no batch dims, the scattered
     // dim is the last output dim == the whole GEMM N.
     if (M.size < 256 || N.size < 256 || nb != 0 || N.size != out.dims[out.rank - 1] ||

@@ -152,6 +152,16 @@ __global__ void __launch_bounds__(512) peer_pull_kernel(PullArgs a, uint4* __res
   }
 }
 
+// out[i] = parity buffer (epoch & 1) of the all-to-all landing zone.
+__global__ void peer_parity_copy_kernel(const uint4* __restrict__ data, uint4* __restrict__ out,
+                                        const uint32_t* ctrl, int64_t n16) {
+  const int64_t par = (int64_t)(*(volatile const uint32_t*)ctrl & 1);
+  const uint4* src = data + par * n16;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n16;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = __ldcs(src + i);
+}
+
 static void close_peers(spmd_comm* c) {
   for (int q = 0; q < c->nranks; ++q)
     if (q != c->rank && c->peer[q]) cudaIpcCloseMemHandle(c->peer[q]);
@@ -334,4 +344,66 @@ extern "C" int spmd_peer_all_gather(spmd_comm* c, spmd_tensor in, spmd_tensor ou
                                       s));
   }
   return peer_barrier(c, channel, s);
+}
+
+// out = all-to-all(split_dim = 1, concat_dim = 0)(dot(lhs, rhs)) for a dot
+// with one batch dim (the output's dim 0) -- the expert FFN-out einsum
+// followed by the GShard combine all-to-all (C3; reference partitioner.py
+// _try_all_to_all :283-318, simulator.py:372-390).  The wide GEMM's epilogue
+// stores every 32-row output chunk into the heap of the member that owns its
+// row block (rows = the flattened free dims, split on the leading one), in
+// slot pos * batch + b of the concat dim, overlapping the exchange with the
+// math; a barrier and one copy out of this epoch's parity buffer finish it.
+extern "C" int spmd_dot_all_to_all(spmd_comm* c, spmd_tensor lhs, spmd_tensor rhs,
+                                   spmd_tensor out, const spmd_dot_dims* dd, int split_dim,
+                                   int concat_dim, const int32_t* groups, int ngroups, int gsize,
+                                   void* stream) {
+  SPMD_CHECK_ARG(c && dd, "dot_all_to_all arguments");
+  SPMD_CHECK_ARG(lhs.dtype == SPMD_BF16 && rhs.dtype == SPMD_BF16 && out.dtype == SPMD_BF16,
+                 "dot_all_to_all is bf16");
+  if (split_dim != 1 || concat_dim != 0 || out.rank < 3 || dd->n_batch != 1 ||
+      dd->lhs_batch[0] != 0 || dd->rhs_batch[0] != 0)
+    return SPMD_ERR_UNSUPPORTED;
+  if (!c->heap) {
+    set_error("peer heap not enabled (spmd_comm_enable_peer)");
+    return SPMD_ERR_INVALID;
+  }
+  int grp, pos;
+  int rc = group_position(c, groups, ngroups, gsize, &grp, &pos);
+  if (rc) return rc;
+  SPMD_CHECK_ARG(gsize <= 8 && out.dims[0] % gsize == 0, "dot_all_to_all group");
+  // dot output [batch, d1 * gsize, d2...] (pre-exchange); out = [batch * gsize, d1, d2...]
+  spmd_tensor full = out;
+  full.dims[0] = out.dims[0] / gsize;
+  full.dims[1] = out.dims[1] * gsize;
+  full.data = nullptr;
+  const int64_t n = numel(out);
+  if (2 * n * 2 > c->heap_bytes) {
+    set_error("peer heap too small for this all-to-all");
+    return SPMD_ERR_INVALID;
+  }
+  SPMD_CHECK_ARG(n % 8 == 0, "dot_all_to_all size");
+  int64_t inner = 1;   // one output row = the last dim (GEMM N)
+  int64_t rows_per_batch = 1;
+  for (int d = 1; d < out.rank - 1; ++d) rows_per_batch *= full.dims[d];
+  inner = out.dims[out.rank - 1];
+  (void)inner;
+  GemmScatter sc;
+  memset(&sc, 0, sizeof(sc));
+  sc.gsize = gsize;
+  sc.pos = pos;
+  for (int j = 0; j < gsize; ++j) sc.dst[j] = c->peer[groups[grp * gsize + j]] + CTRL_BYTES;
+  sc.epoch = (const uint32_t*)c->heap;
+  sc.rows = 1;
+  sc.rchunk = rows_per_batch / gsize;
+  sc.slot_base = pos * (int)full.dims[0];
+  sc.nslots = (int)out.dims[0];
+  cudaStream_t s = as_stream(stream);
+  rc = dot_tcgen05(lhs, rhs, full, *dd, 1, s, &sc);
+  if (rc) return rc;
+  if ((rc = peer_barrier(c, 0, s))) return rc;
+  const int64_t n16 = n / 8;
+  peer_parity_copy_kernel<<<grid_for(n16, 256), 256, 0, s>>>(
+      (const uint4*)(c->heap + CTRL_BYTES), (uint4*)out.data, (const uint32_t*)c->heap, n16);
+  return launched(s);
 }

@@ -274,6 +274,8 @@ class Executor:
                 rs = spec[2]
                 need = max(need, 2 * rs.shape.num_elements * len(rs.attrs["subgroups"][0]) *
                            rs.shape.dtype.itemsize)
+            elif spec[0] == "dot_a2a":
+                need = max(need, 2 * spec[2].shape.num_elements * spec[2].shape.dtype.itemsize)
         off = (need + 4095) // 4096 * 4096
         self._peer_ag = {}
         if os.environ.get("SPMD_PEER_AG", "1") != "0":
@@ -298,7 +300,7 @@ class Executor:
         hidden_engine = {"ce": 0, "sm": 3, "nccl": -1}[
             os.environ.get("SPMD_PEER_HIDDEN_ENGINE", "ce")]
         heavy_ops = (Op.DOT, Op.CONVOLUTION)
-        heavy_fused = ("dot_relu", "conv_relu", "attention", "dot_rs")
+        heavy_fused = ("dot_relu", "conv_relu", "attention", "dot_rs", "dot_a2a")
         eng = {}
         order = self.steps
         for i, st in enumerate(order):
@@ -522,6 +524,35 @@ class Executor:
                 continue
             self._fused_skip.add(d.id)
             self._fused[rs.id] = ("dot_rs", d, rs)
+        # Dot (one batch dim) -> all-to-all(split 1, concat 0): the expert
+        # FFN-out einsum + GShard combine exchange (C3) -> wide GEMM with a
+        # row-scatter epilogue (peer.cu spmd_dot_all_to_all).
+        for a2a in self.graph.instructions:
+            if a2a.opcode != Op.ALL_TO_ALL or a2a.attrs["split_dim"] != 1 or \
+                    a2a.attrs["concat_dim"] != 0:
+                continue
+            d = by.get(a2a.operands[0])
+            if d is None or d.opcode != Op.DOT or d.id in outs or d.id in self._fused_skip \
+                    or d.id in self._fused or users.get(d.id, []) != [a2a.id] \
+                    or d.shape.dtype != DType.BF16 or d.shape.rank < 3:
+                continue
+            at = d.attrs
+            if tuple(at["lhs_batch"]) != (0,) or tuple(at["rhs_batch"]) != (0,):
+                continue
+            groups = a2a.attrs["subgroups"]
+            gs = len(groups[0])
+            if any(len(g) != gs for g in groups) or gs > 8:
+                continue
+            rsh = self._shape(d.operands[1])
+            rfree = [k for k in range(rsh.rank) if k not in at["rhs_contracting"] and k != 0]
+            if [rsh.dims[k] for k in rfree if rsh.dims[k] != 1] != [d.shape.dims[-1]]:
+                continue
+            rows = int(np.prod(d.shape.dims[1:-1]))
+            if d.shape.dims[-1] < 512 or rows < 256 or d.shape.dims[1] % gs or \
+                    (rows // gs) % 32:
+                continue
+            self._fused_skip.add(d.id)
+            self._fused[a2a.id] = ("dot_a2a", d, a2a)
 
     def _plan_attention(self, users, outs):
         """Dot(q,k) -> fused softmax -> Dot(probs, v) with the Transformer
@@ -698,7 +729,7 @@ class Executor:
             ops = tuple(self._operands_of(ins))
             frees = tuple(o for o in set(ops) if last_use.get(o) == k and o not in keep)
             fused = self._fused.get(ins.id)
-            coll = ins.opcode in COLLECTIVES and not (fused and fused[0] == "dot_rs")
+            coll = ins.opcode in COLLECTIVES and not (fused and fused[0] in ("dot_rs", "dot_a2a"))
             steps.append(_Step(ins, fn, frees, ops, coll))
         return steps
 
@@ -782,6 +813,8 @@ class Executor:
             return self._halo_conv_step(*f[1:])
         if f is not None and f[0] == "dot_rs":
             return self._dot_rs_step(f[1], f[2])
+        if f is not None and f[0] == "dot_a2a":
+            return self._dot_a2a_step(f[1], f[2])
         if f is not None and f[0] in ("moe_dispatch", "moe_combine"):
             _, x, ridx = f
             xsh = self._shape(x)
@@ -1065,6 +1098,22 @@ class Executor:
             dd.lhs_contracting[i], dd.rhs_contracting[i] = x, y
         dd.epilogue = epilogue
         return dd
+
+    def _dot_a2a_step(self, dot, a2a):
+        lib, comm = self.lib, self.comm
+        a, b = dot.operands
+        ash, bsh, shp = self._shape(a), self._shape(b), a2a.shape
+        dd = self._dot_dims(dot)
+        ref = ctypes.byref(dd)
+        groups, ng, gs = _groups_arg(a2a.attrs["subgroups"])
+
+        def run(env, s):
+            out = self._alloc(shp)
+            C.check(lib.spmd_dot_all_to_all(comm.handle, desc(env[a], ash), desc(env[b], bsh),
+                                            desc(out, shp), ref, 1, 0, groups, ng, gs, s),
+                    "dot_all_to_all")
+            return out
+        return run
 
     def _dot_rs_step(self, dot, rs):
         lib, comm = self.lib, self.comm

@@ -1,0 +1,13 @@
+cd $GRAFT_REPO_ROOT
+timeout 600 python -m pytest tests/test_gpu_peer.py -q -x > gpurun_out/a2a_tests.log 2>&1; echo tests=$?; tail -1 gpurun_out/a2a_tests.log
+for n in 2 4; do
+timeout 900 torchrun --nnodes=1 --nproc-per-node $n --master-addr 127.0.0.1 --master-port 2972$n scripts/peer_fusion_check.py > gpurun_out/a2a_check$n.log 2>&1; echo check$n=$?; grep "moe\|failed" gpurun_out/a2a_check$n.log | tail -2
+done
+T4="timeout 900 torchrun --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1"
+for F in 1 0 1 0; do
+SPMD_PEER_FUSION=$F $T4 --master-port 29730 bench.py --gpus 4 --config c3 --no-e2e > gpurun_out/a2a_c3_$F.log 2>&1
+grep "^{" gpurun_out/a2a_c3_$F.log | python -c "
+import sys,json
+for l in sys.stdin:
+    d=json.loads(l); print('fusion=$F', d['ms_per_step'], round(d['tflops_per_gpu'],1), d['clocks']['sm_mhz'])"
+done

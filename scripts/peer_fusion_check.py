@@ -143,6 +143,34 @@ def main():
                 failed.append(f"layer_small{lm}:{eng}")
             del ex1, ex0, x1, x0
 
+    # MoE layer: expert FFN-out einsum + combine all-to-all fused over peer
+    # memory (and the dense dispatch einsum + all-to-all) vs NCCL
+    from paper_2105_04663_b200.workloads import moe_layer
+    outs = {}
+    for fused in (True, False):
+        os.environ["SPMD_PEER_FUSION"] = "1" if fused else "0"
+        g, ins = moe_layer(world, E=8, B=8, S=64, C=64, M=512, H=1024, dtype=DType.BF16)
+        ann, _ = propagate(g)
+        prog = partition(ann, world, plan="fast")
+        xs = []
+        for k, p in enumerate(prog.graph.parameters):
+            piece = shard_data(ins[k], ann.parameters[k].sharding, devices=range(world))[rank]
+            t = torch.from_numpy(np.ascontiguousarray(piece, dtype=np.float32)).to(dev)
+            xs.append(t.to(torch.bfloat16).reshape((1,) + p.shape.dims))
+        ex = Executor(prog, nparts=1, device=dev, comm=comm, partition_base=rank, fuse=True)
+        n_a2a = sum(1 for v in ex._fused.values() if v[0] == "dot_a2a")
+        outs[fused] = (ex.run(xs)[0], n_a2a)
+    torch.cuda.synchronize()
+    same = bool(torch.equal(outs[True][0], outs[False][0]))
+    flags = [None] * world
+    dist.all_gather_object(flags, same)
+    if rank == 0:
+        print(json.dumps({"section": "moe_dot_a2a", "fused_dot_a2a": outs[True][1],
+                          "unfused": outs[False][1], "ranks_equal": flags}), flush=True)
+    if not (all(flags) and outs[True][1] > 0 and outs[False][1] == 0):
+        failed.append("moe_dot_a2a")
+    os.environ.pop("SPMD_PEER_FUSION", None)
+
     if "--perf" in sys.argv:
         dims = dict(B=16, S=1024, M=8192, N=128, D=256, H=65536)
         flops = transformer_flops(**dims)

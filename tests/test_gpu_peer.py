@@ -97,3 +97,35 @@ def test_peer_all_gather_world_of_one(comm, engine, dim):
         torch.cuda.synchronize()
         assert torch.equal(x, y)
     C.check(lib.spmd_check_device_errors(s), "device")
+
+
+def test_dot_all_to_all_world_of_one(comm):
+    """Expert-FFN einsum [E,B,C,H] x [E,H,M] with the row-scatter epilogue:
+    with one member the all-to-all is the identity, so the result equals the
+    plain tcgen05 dot bit for bit (both parity buffers exercised)."""
+    import torch
+    from paper_2105_04663_b200 import _capi as C
+    from paper_2105_04663_b200.executor import _groups_arg, desc
+    from paper_2105_04663_b200.ir import DType, Shape
+    lib, s = C.lib(), torch.cuda.current_stream().cuda_stream
+    garr, ng, gs = _groups_arg([[0]])
+    E, B, Cc, H, M = 2, 8, 64, 256, 512
+    dd = C.SpmdDotDims()
+    dd.n_batch, dd.n_contract = 1, 1
+    dd.lhs_batch[0] = dd.rhs_batch[0] = 0
+    dd.lhs_contracting[0], dd.rhs_contracting[0] = 3, 1
+    ash, bsh = Shape((E, B, Cc, H), DType.BF16), Shape((E, H, M), DType.BF16)
+    osh = Shape((E, B, Cc, M), DType.BF16)
+    for it in range(3):
+        torch.manual_seed(10 + it)
+        a = torch.randn((1, E, B, Cc, H), device="cuda").bfloat16()
+        b = (torch.randn((1, E, H, M), device="cuda") * 0.05).bfloat16()
+        fused = torch.empty((1, E, B, Cc, M), device="cuda", dtype=torch.bfloat16)
+        plain = torch.empty_like(fused)
+        C.check(lib.spmd_dot_all_to_all(comm.handle, desc(a, ash), desc(b, bsh), desc(fused, osh),
+                                        ctypes.byref(dd), 1, 0, garr, ng, gs, s), "dot_a2a")
+        C.check(lib.spmd_dot(desc(a, ash), desc(b, bsh), desc(plain, osh), ctypes.byref(dd), 1,
+                             s), "dot")
+        torch.cuda.synchronize()
+        C.check(lib.spmd_check_device_errors(s), "device")
+        assert torch.equal(fused, plain)
