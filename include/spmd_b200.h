@@ -270,6 +270,13 @@ int spmd_dot_reduce_scatter(spmd_comm* comm, spmd_tensor lhs, spmd_tensor rhs, s
 int spmd_dot_all_to_all(spmd_comm* comm, spmd_tensor lhs, spmd_tensor rhs, spmd_tensor out,
                         const spmd_dot_dims* dims, int split_dim, int concat_dim,
                         const int32_t* groups, int ngroups, int gsize, void* stream);
+/* x [B,S,M] bf16 routed by expert/slot s32 [B,S] (spmd_moe_route) -> out
+ * [B*G, E/G, C, M] = all-to-all(split 1, concat 0)(dispatch(x)): every row is
+ * pushed straight into the owning member's heap (empty capacity slots as
+ * zeros), barrier, one copy.  Needs a comm workspace of >= B*E*C*4 bytes. */
+int spmd_moe_dispatch_all_to_all(spmd_comm* comm, spmd_tensor x, spmd_tensor expert,
+                                 spmd_tensor slot, spmd_tensor out, const int32_t* groups,
+                                 int ngroups, int gsize, void* stream);
 /* All-gather through the peer heap (reference simulator.py:353-359 piece
  * order): stage `in` at heap data offset `heap_offset` (256-aligned, caller
  * assigned, disjoint from the reduce-scatter region and from other live

@@ -407,3 +407,113 @@ extern "C" int spmd_dot_all_to_all(spmd_comm* c, spmd_tensor lhs, spmd_tensor rh
       (const uint4*)(c->heap + CTRL_BYTES), (uint4*)out.data, (const uint32_t*)c->heap, n16);
   return launched(s);
 }
+
+// ---------------------------------------------------------------------------
+// Fused GShard dispatch + all-to-all (C3): x [B_loc, S, M] routed by
+// (expert, slot) -> every member j receives rows [pos*B_loc + b, e_loc, c, :]
+// for its experts e = j*E_loc + e_loc, written straight into its heap
+// (16-byte NVLink stores, empty slots as zeros, so no receiver-side clear).
+// ---------------------------------------------------------------------------
+__global__ void moe_inverse_kernel(const int32_t* __restrict__ expert,
+                                   const int32_t* __restrict__ slot, int32_t* __restrict__ inv,
+                                   int64_t tokens, int S, int E, int C) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < tokens;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int sl = slot[t];
+    if (sl < C) inv[((t / S) * E + expert[t]) * (int64_t)C + sl] = (int32_t)(t % S);
+  }
+}
+
+struct DispatchPush {
+  uint4* dst[8];      // member j's landing zone (data start of its heap)
+  int G, pos, Bl, S, E, El, C;
+  int64_t m16;        // 16-byte vectors per row
+  int64_t slot_rows;  // rows of one parity buffer: B * E_loc * C
+};
+
+__global__ void __launch_bounds__(256) moe_dispatch_push_kernel(const uint4* __restrict__ x,
+                                                                const int32_t* __restrict__ inv,
+                                                                DispatchPush a,
+                                                                const uint32_t* ctrl) {
+  const int64_t par = (int64_t)((*(volatile const uint32_t*)ctrl + 1) & 1);
+  const int lane = threadIdx.x & 31;
+  const int64_t rows = (int64_t)a.G * a.Bl * a.El * a.C;   // (j, b, e_loc, c)
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t w = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); w < rows;
+       w += warps) {
+    int64_t r = w;
+    const int c = (int)(r % a.C);
+    r /= a.C;
+    const int el = (int)(r % a.El);
+    r /= a.El;
+    const int b = (int)(r % a.Bl);
+    const int j = (int)(r / a.Bl);
+    const int s = inv[((int64_t)b * a.E + j * a.El + el) * a.C + c];
+    const int64_t drow = par * a.slot_rows +
+                         (((int64_t)(a.pos * a.Bl + b) * a.El + el) * a.C + c);
+    uint4* dst = a.dst[j] + drow * a.m16;
+    if (s < 0) {
+      for (int64_t i = lane; i < a.m16; i += 32) dst[i] = make_uint4(0, 0, 0, 0);
+    } else {
+      const uint4* src = x + ((int64_t)b * a.S + s) * a.m16;
+      for (int64_t i = lane; i < a.m16; i += 32) dst[i] = __ldcs(src + i);
+    }
+  }
+  __threadfence_system();   // peer stores visible before the barrier signal
+}
+
+// x [B_loc, S, M] bf16, expert/slot s32 [B_loc, S] (spmd_moe_route) ->
+// out [B_loc * G, E / G, C, M] = all-to-all(split 1, concat 0)(dispatch(x)).
+extern "C" int spmd_moe_dispatch_all_to_all(spmd_comm* c, spmd_tensor x, spmd_tensor expert,
+                                            spmd_tensor slot, spmd_tensor out,
+                                            const int32_t* groups, int ngroups, int gsize,
+                                            void* stream) {
+  SPMD_CHECK_ARG(c && x.dtype == SPMD_BF16 && out.dtype == SPMD_BF16 && x.rank == 3 &&
+                     out.rank == 4 && expert.dtype == SPMD_S32 && slot.dtype == SPMD_S32,
+                 "moe dispatch all-to-all expects bf16 x [B,S,M] -> [B*G, E/G, C, M]");
+  if (!c->heap) {
+    set_error("peer heap not enabled (spmd_comm_enable_peer)");
+    return SPMD_ERR_INVALID;
+  }
+  int grp, pos;
+  int rc = group_position(c, groups, ngroups, gsize, &grp, &pos);
+  if (rc) return rc;
+  const int Bl = (int)x.dims[0], S = (int)x.dims[1], M = (int)x.dims[2];
+  const int El = (int)out.dims[1], C = (int)out.dims[2], E = El * gsize;
+  SPMD_CHECK_ARG(gsize <= 8 && out.dims[0] == (int64_t)Bl * gsize && out.dims[3] == M &&
+                     M % 8 == 0,
+                 "moe dispatch all-to-all shape");
+  const int64_t n = numel(out);
+  if (2 * n * 2 > c->heap_bytes) {
+    set_error("peer heap too small for this all-to-all");
+    return SPMD_ERR_INVALID;
+  }
+  const int64_t inv_bytes = (int64_t)Bl * E * C * 4;
+  if (c->ws_bytes < inv_bytes) {
+    set_error("collective workspace too small for the dispatch index");
+    return SPMD_ERR_INVALID;
+  }
+  cudaStream_t s = as_stream(stream);
+  int32_t* inv = (int32_t*)c->ws;
+  SPMD_CUDA_TRY(cudaMemsetAsync(inv, 0xff, inv_bytes, s));   // -1: empty slot
+  const int64_t tokens = (int64_t)Bl * S;
+  moe_inverse_kernel<<<grid_for(tokens, 256), 256, 0, s>>>(
+      (const int32_t*)expert.data, (const int32_t*)slot.data, inv, tokens, S, E, C);
+  if ((rc = launched(s))) return rc;
+  DispatchPush a;
+  memset(&a, 0, sizeof(a));
+  for (int j = 0; j < gsize; ++j)
+    a.dst[j] = (uint4*)(c->peer[groups[grp * gsize + j]] + CTRL_BYTES);
+  a.G = gsize, a.pos = pos, a.Bl = Bl, a.S = S, a.E = E, a.El = El, a.C = C;
+  a.m16 = M / 8;
+  a.slot_rows = (int64_t)Bl * gsize * El * C;
+  const int64_t rows = (int64_t)gsize * Bl * El * C;
+  moe_dispatch_push_kernel<<<grid_for(rows * 32, 256), 256, 0, s>>>(
+      (const uint4*)x.data, inv, a, (const uint32_t*)c->heap);
+  if ((rc = launched(s))) return rc;
+  if ((rc = peer_barrier(c, 0, s))) return rc;
+  const int64_t n16 = n / 8;
+  peer_parity_copy_kernel<<<grid_for(n16, 256), 256, 0, s>>>(
+      (const uint4*)(c->heap + CTRL_BYTES), (uint4*)out.data, (const uint32_t*)c->heap, n16);
+  return launched(s);
+}

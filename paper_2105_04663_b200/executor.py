@@ -276,6 +276,8 @@ class Executor:
                            rs.shape.dtype.itemsize)
             elif spec[0] == "dot_a2a":
                 need = max(need, 2 * spec[2].shape.num_elements * spec[2].shape.dtype.itemsize)
+            elif spec[0] == "moe_dispatch_a2a":
+                need = max(need, 2 * spec[3].shape.num_elements * spec[3].shape.dtype.itemsize)
         off = (need + 4095) // 4096 * 4096
         self._peer_ag = {}
         if os.environ.get("SPMD_PEER_AG", "1") != "0":
@@ -325,6 +327,10 @@ class Executor:
 
     def _workspace_bytes(self) -> int:
         need = 0
+        for spec in self._fused.values():   # dispatch index [B, E, C] s32
+            if spec[0] == "moe_dispatch_a2a":
+                sh = spec[3].shape
+                need = max(need, sh.dims[0] * sh.dims[1] * sh.dims[2] * 4)
         for ins in self.graph.instructions:
             if ins.opcode in COLLECTIVES and ins.opcode != Op.COLLECTIVE_PERMUTE:
                 src = self._shape(ins.operands[0])
@@ -524,6 +530,21 @@ class Executor:
                 continue
             self._fused_skip.add(d.id)
             self._fused[rs.id] = ("dot_rs", d, rs)
+        # routed dispatch -> all-to-all(split 1, concat 0): push rows into the
+        # owners' heaps (peer.cu spmd_moe_dispatch_all_to_all)
+        for a2a in self.graph.instructions:
+            if a2a.opcode != Op.ALL_TO_ALL or a2a.attrs["split_dim"] != 1 or \
+                    a2a.attrs["concat_dim"] != 0:
+                continue
+            spec = self._fused.get(a2a.operands[0])
+            if spec is None or spec[0] != "moe_dispatch" or a2a.operands[0] in outs or \
+                    users.get(a2a.operands[0], []) != [a2a.id]:
+                continue
+            groups = a2a.attrs["subgroups"]
+            if any(len(g) != len(groups[0]) for g in groups) or len(groups[0]) > 8:
+                continue
+            self._fused_skip.add(a2a.operands[0])
+            self._fused[a2a.id] = ("moe_dispatch_a2a", spec[1], spec[2], a2a)
         # Dot (one batch dim) -> all-to-all(split 1, concat 0): the expert
         # FFN-out einsum + GShard combine exchange (C3) -> wide GEMM with a
         # row-scatter epilogue (peer.cu spmd_dot_all_to_all).
@@ -729,7 +750,8 @@ class Executor:
             ops = tuple(self._operands_of(ins))
             frees = tuple(o for o in set(ops) if last_use.get(o) == k and o not in keep)
             fused = self._fused.get(ins.id)
-            coll = ins.opcode in COLLECTIVES and not (fused and fused[0] in ("dot_rs", "dot_a2a"))
+            coll = ins.opcode in COLLECTIVES and not (
+                fused and fused[0] in ("dot_rs", "dot_a2a", "moe_dispatch_a2a"))
             steps.append(_Step(ins, fn, frees, ops, coll))
         return steps
 
@@ -781,7 +803,7 @@ class Executor:
         if f[0] == "halo":
             mask = f[4]
             return tuple(f[1]) + (f[3],) + ((mask[2], mask[3]) if mask is not None else ())
-        if f[0] in ("moe_dispatch", "moe_combine"):
+        if f[0] in ("moe_dispatch", "moe_combine", "moe_dispatch_a2a"):
             return (f[1],)
         if f[0] == "halo_conv":
             _, conv, _, (_, pieces, _, start, mask), _ = f
@@ -815,6 +837,21 @@ class Executor:
             return self._dot_rs_step(f[1], f[2])
         if f is not None and f[0] == "dot_a2a":
             return self._dot_a2a_step(f[1], f[2])
+        if f is not None and f[0] == "moe_dispatch_a2a":
+            _, x, ridx, a2a = f
+            xsh, r = self._shape(x), self.routing[ridx]
+            ish = Shape(tuple(r.expert.shape[1:]), DType.S32)
+            groups, ng, gs = _groups_arg(a2a.attrs["subgroups"])
+            comm = self.comm
+
+            def run(env, s):
+                out = self._alloc(shp)
+                C.check(lib.spmd_moe_dispatch_all_to_all(comm.handle, desc(env[x], xsh),
+                                                         desc(r.expert, ish), desc(r.slot, ish),
+                                                         desc(out, shp), groups, ng, gs, s),
+                        "moe_dispatch_all_to_all")
+                return out
+            return run
         if f is not None and f[0] in ("moe_dispatch", "moe_combine"):
             _, x, ridx = f
             xsh = self._shape(x)

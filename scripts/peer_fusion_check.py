@@ -171,6 +171,56 @@ def main():
         failed.append("moe_dot_a2a")
     os.environ.pop("SPMD_PEER_FUSION", None)
 
+    # routed MoE: dispatch pushed straight into the experts' owners' heaps
+    # (spmd_moe_dispatch_all_to_all) + fused FFN-out/combine exchange, vs the
+    # same routing with NCCL all-to-alls
+    from paper_2105_04663_b200.executor import Routing
+    E, Bg, S_, Cc, M_, H_ = 8, 8, 64, 32, 512, 1024
+    Bl = Bg // world
+    st = torch.cuda.current_stream().cuda_stream
+    gen = torch.Generator(device=dev).manual_seed(100 + rank)
+    logits = torch.randn((1, Bl, S_, E), device=dev, generator=gen)
+    ex_t = torch.empty((1, Bl, S_), dtype=torch.int32, device=dev)
+    sl_t, gt_t = torch.empty_like(ex_t), torch.empty((1, Bl, S_), dtype=torch.float32, device=dev)
+    lib = C.lib()
+    f32, s32, bf = DType.F32, DType.S32, DType.BF16
+    C.check(lib.spmd_moe_route(desc(logits, Shape((Bl, S_, E), f32)), Cc,
+                               desc(ex_t, Shape((Bl, S_), s32)), desc(sl_t, Shape((Bl, S_), s32)),
+                               desc(gt_t, Shape((Bl, S_), f32)), 1, st), "route")
+    outs = {}
+    for fused in (True, False):
+        os.environ["SPMD_PEER_FUSION"] = "1" if fused else "0"
+        g, ins = moe_layer(world, E=E, B=Bg, S=S_, C=Cc, M=M_, H=H_, dtype=DType.BF16)
+        ann, _ = propagate(g)
+        prog = partition(ann, world, plan="fast")
+        xs = []
+        for k, p in enumerate(prog.graph.parameters):
+            piece = shard_data(ins[k], ann.parameters[k].sharding, devices=range(world))[rank]
+            t = torch.from_numpy(np.ascontiguousarray(piece, dtype=np.float32)).to(dev)
+            xs.append(t.to(torch.bfloat16).reshape((1,) + p.shape.dims))
+        names = [p.id for p in ann.parameters]
+        msh = Shape((Bl, S_, E, Cc), bf)
+        C.check(lib.spmd_moe_masks(desc(ex_t, Shape((Bl, S_), s32)), desc(sl_t, Shape((Bl, S_), s32)),
+                                   desc(gt_t, Shape((Bl, S_), f32)),
+                                   desc(xs[names.index("dispatch")], msh),
+                                   desc(xs[names.index("combine")], msh), 1, st), "masks")
+        idx = {p.id: p.attrs["index"] for p in ann.parameters}
+        r = Routing(ex_t, sl_t, gt_t)
+        ex = Executor(prog, nparts=1, device=dev, comm=comm, partition_base=rank, fuse=True,
+                      routing={idx["dispatch"]: r, idx["combine"]: r})
+        kinds = sorted(v[0] for v in ex._fused.values())
+        outs[fused] = (ex.run(xs)[0], kinds)
+    torch.cuda.synchronize()
+    same = bool(torch.equal(outs[True][0], outs[False][0]))
+    flags = [None] * world
+    dist.all_gather_object(flags, same)
+    if rank == 0:
+        print(json.dumps({"section": "moe_routed", "fused": outs[True][1],
+                          "unfused": outs[False][1], "ranks_equal": flags}), flush=True)
+    if not (all(flags) and "moe_dispatch_a2a" in outs[True][1]):
+        failed.append("moe_routed")
+    os.environ.pop("SPMD_PEER_FUSION", None)
+
     if "--perf" in sys.argv:
         dims = dict(B=16, S=1024, M=8192, N=128, D=256, H=65536)
         flops = transformer_flops(**dims)
