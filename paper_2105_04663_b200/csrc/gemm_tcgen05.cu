@@ -561,6 +561,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
     // ---------------- TMA producer (both CTAs) ----------------
     int s = 0;
     uint32_t ph = 0;
+    uint64_t pol_last, pol_first;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_last));
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_first));
+    const int hint = g.hint != 0;
+    const uint64_t pa = g.hint == 1 ? pol_last : pol_first;
+    const uint64_t pb = g.hint == 1 ? pol_first : pol_last;
     for (int64_t t = cluster; t < g.tiles; t += nclusters) {
       int b, m, n;
       tile_coords(g, t, b, m, n);
@@ -573,23 +579,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
         if (leader) mbar_expect_tx(&full[s], 2 * L::STAGE_BYTES);
         const int k0 = kb * BK;
         if (!g.a_mn) {
-          tma_load_5d_2sm(sa, &map_a, &full[s], k0, mrow, b0, b1, b2);
+          load_2sm(sa, &map_a, &full[s], k0, mrow, b0, b1, b2, hint, pa);
         } else {
 #pragma unroll
           for (int c = 0; c < HALF / 64; ++c)
-            tma_load_5d_2sm(sa + c * (BK * 128), &map_a, &full[s], mrow + c * 64, k0, b0, b1, b2);
+            load_2sm(sa + c * (BK * 128), &map_a, &full[s], mrow + c * 64, k0, b0, b1, b2, hint,
+                     pa);
         }
 #pragma unroll
         for (int j = 0; j < 2; ++j) {   // UMMA j covers pair-tile cols [256j, 256j+256)
           const int nrow = n * WBN + j * WHALF_N + rank * HALF;
           uint8_t* sbj = sb + j * (HALF * BK * 2);
           if (!g.b_mn) {
-            tma_load_5d_2sm(sbj, &map_b, &full[s], k0, nrow, b0, b1, b2);
+            load_2sm(sbj, &map_b, &full[s], k0, nrow, b0, b1, b2, hint, pb);
           } else {
 #pragma unroll
             for (int c = 0; c < HALF / 64; ++c)
-              tma_load_5d_2sm(sbj + c * (BK * 128), &map_b, &full[s], nrow + c * 64, k0, b0, b1,
-                              b2);
+              load_2sm(sbj + c * (BK * 128), &map_b, &full[s], nrow + c * 64, k0, b0, b1, b2,
+                       hint, pb);
           }
         }
         if (++s == STAGES) {
