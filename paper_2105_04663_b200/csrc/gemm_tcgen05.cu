@@ -915,23 +915,25 @@ int dot_tcgen05(const spmd_tensor& lhs, const spmd_tensor& rhs, const spmd_tenso
     // All-to-all epilogue (wide kernel): one batch dim (the concat dim), the
     // split dim = the leading GEMM row dim, whole row chunks per member.
     const int64_t nbat = (int64_t)g.nb[0] * g.nb[1] * g.nb[2];
+    // rchunk 0: reduce-scatter on the leading row dim -> M / gsize rows each
+    const int64_t rchunk = sc->rchunk ? sc->rchunk : M.size / (sc->gsize ? sc->gsize : 1);
     if (M.size < 256 || N.size < 512 || gemm_mode() != 3 ||
-        sc->gsize < 1 || sc->gsize > 8 || sc->rchunk % 32 != 0 ||
-        sc->rchunk * sc->gsize != M.size || nbat * sc->gsize != sc->nslots)
+        sc->gsize < 1 || sc->gsize > 8 || rchunk % 32 != 0 ||
+        rchunk * sc->gsize != M.size || nbat * sc->gsize != sc->nslots)
       return SPMD_ERR_UNSUPPORTED;
     g.tma_store = 0;
     g.scatter = 1;
     g.sc_rows = 1;
     g.sc_g = sc->gsize;
     g.sc_pos = sc->pos;
-    g.sc_rchunk = sc->rchunk;
+    g.sc_rchunk = rchunk;
     g.sc_slot_base = sc->slot_base;
     g.sc_nslots = sc->nslots;
     g.sc_epoch = sc->epoch;
     g.sc_tma = 1;
     for (int j = 0; g.sc_tma && j < sc->gsize; ++j)
-      g.sc_tma = encode_store_map(&smaps.m[j], sc->dst[j], N.size, sc->rchunk, N.size,
-                                  2 * sc->nslots, sc->rchunk * N.size);
+      g.sc_tma = encode_store_map(&smaps.m[j], sc->dst[j], N.size, rchunk, N.size,
+                                  2 * sc->nslots, rchunk * N.size);
     if (!g.sc_tma) return SPMD_ERR_UNSUPPORTED;
   } else if (sc) {
     // Reduce-scatter epilogue: 2-CTA kernel, no batch dims, the scattered

@@ -243,7 +243,8 @@ extern "C" int spmd_dot_reduce_scatter(spmd_comm* c, spmd_tensor lhs, spmd_tenso
   SPMD_CHECK_ARG(c && dd, "dot_reduce_scatter arguments");
   SPMD_CHECK_ARG(lhs.dtype == SPMD_BF16 && rhs.dtype == SPMD_BF16 && out.dtype == SPMD_BF16,
                  "dot_reduce_scatter is bf16");
-  SPMD_CHECK_ARG(out.rank >= 1 && dim == out.rank - 1, "dot_reduce_scatter scatters the last dim");
+  SPMD_CHECK_ARG(out.rank >= 1 && (dim == out.rank - 1 || (dim == 0 && out.rank >= 2)),
+                 "dot_reduce_scatter scatters the last dim or the leading (row) dim");
   if (!c->heap) {
     set_error("peer heap not enabled (spmd_comm_enable_peer)");
     return SPMD_ERR_INVALID;
@@ -268,6 +269,14 @@ extern "C" int spmd_dot_reduce_scatter(spmd_comm* c, spmd_tensor lhs, spmd_tenso
   sc.pos = pos;
   for (int j = 0; j < gsize; ++j) sc.dst[j] = c->peer[groups[grp * gsize + j]] + CTRL_BYTES;
   sc.epoch = (const uint32_t*)c->heap;
+  if (dim == 0 && out.rank >= 2 && dim != out.rank - 1) {
+    // split on the leading output dim = GEMM rows (no batch dims): member j
+    // gets rows [j * R/G, (j+1) * R/G) into slot `pos` (wide kernel)
+    sc.rows = 1;
+    sc.rchunk = 0;   // M / gsize
+    sc.slot_base = pos;
+    sc.nslots = gsize;
+  }
   rc = dot_tcgen05(lhs, rhs, full, *dd, 1, s, &sc);
   if (rc) return rc;
   if ((rc = peer_barrier(c, 0, s))) return rc;

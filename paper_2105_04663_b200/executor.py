@@ -511,8 +511,6 @@ class Executor:
             if d is None or d.opcode != Op.DOT or d.id in outs or d.id in self._fused_skip \
                     or users.get(d.id, []) != [rs.id] or d.shape.dtype != DType.BF16:
                 continue
-            if rs.attrs["dim"] != d.shape.rank - 1:
-                continue
             groups = rs.attrs["subgroups"]
             gs = len(groups[0])
             if any(len(g) != gs for g in groups) or gs > 8:
@@ -521,12 +519,22 @@ class Executor:
             ls, rsh = self._shape(d.operands[0]), self._shape(d.operands[1])
             if a["lhs_batch"] or a["rhs_batch"]:
                 continue
+            lfree = [k for k in range(ls.rank) if k not in a["lhs_contracting"]]
             rfree = [k for k in range(rsh.rank) if k not in a["rhs_contracting"]]
-            if [rsh.dims[k] for k in rfree if rsh.dims[k] != 1] != [d.shape.dims[-1]]:
-                continue
-            n = d.shape.dims[-1]
-            m = d.shape.num_elements // n
-            if m < 256 or n < 256 or n % gs or (n // gs) % 32:
+            m = int(np.prod([ls.dims[k] for k in lfree]))
+            n = int(np.prod([rsh.dims[k] for k in rfree]))
+            if rs.attrs["dim"] == d.shape.rank - 1:
+                # column split: the last output dim is the whole GEMM N
+                if [rsh.dims[k] for k in rfree if rsh.dims[k] != 1] != [d.shape.dims[-1]]:
+                    continue
+                if m < 256 or n < 256 or n % gs or (n // gs) % 32:
+                    continue
+            elif rs.attrs["dim"] == 0 and lfree and d.shape.rank >= 2:
+                # row split (wide GEMM): the leading output dim leads the rows
+                if m < 256 or n < 512 or m % gs or (m // gs) % 32 or \
+                        d.shape.dims[0] % gs:
+                    continue
+            else:
                 continue
             self._fused_skip.add(d.id)
             self._fused[rs.id] = ("dot_rs", d, rs)

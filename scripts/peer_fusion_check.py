@@ -78,6 +78,40 @@ def direct_abi(comm, rank, world, dev):
     return errs
 
 
+def direct_abi_rows(comm, rank, world, dev):
+    """Row-split reduce-scatter (weight-gradient shape dW[M,N,D] = x^T.dy
+    split on M) vs dot + NCCL reduce-scatter on dim 0."""
+    lib = C.lib()
+    s = torch.cuda.current_stream().cuda_stream
+    T, M, N, D = 512, 256 * world, 8, 128
+    garr, ng, gsz = _groups_arg([list(range(world))])
+    dd = C.SpmdDotDims()
+    dd.n_contract = 1
+    dd.lhs_contracting[0], dd.rhs_contracting[0] = 0, 0
+    errs = []
+    for it in range(3):
+        g = torch.Generator(device=dev).manual_seed(77 * it + rank)
+        a = torch.randn((1, T, M), device=dev, generator=g).bfloat16()
+        b = (torch.randn((1, T, N, D), device=dev, generator=g) * 0.05).bfloat16()
+        ash, bsh = Shape((T, M), DType.BF16), Shape((T, N, D), DType.BF16)
+        osh = Shape((M // world, N, D), DType.BF16)
+        fused = torch.empty((1, M // world, N, D), device=dev, dtype=torch.bfloat16)
+        C.check(lib.spmd_dot_reduce_scatter(comm.handle, desc(a, ash), desc(b, bsh),
+                                            desc(fused, osh), ctypes.byref(dd), 0, garr, ng, gsz,
+                                            s), "dot_rs_rows")
+        full = torch.empty((1, M, N, D), device=dev, dtype=torch.bfloat16)
+        C.check(lib.spmd_dot(desc(a, ash), desc(b, bsh), desc(full, Shape((M, N, D), DType.BF16)),
+                             ctypes.byref(dd), 1, s), "dot")
+        ref = torch.empty_like(fused)
+        comm.ensure_workspace(4 * M * N * D, dev)
+        C.check(lib.spmd_reduce_scatter(comm.handle, desc(full, Shape((M, N, D), DType.BF16)),
+                                        desc(ref, osh), 0, 0, garr, ng, gsz, s), "rs")
+        torch.cuda.synchronize()
+        C.check(lib.spmd_check_device_errors(s), "device")
+        errs.append(rel(fused, ref))
+    return errs
+
+
 def layer(comm, rank, world, dev, mesh, dims, fused_rs, env=None):
     os.environ["SPMD_PEER_FUSION"] = "1" if fused_rs else "0"
     for k in ("SPMD_PEER_AG", "SPMD_PEER_AG_ENGINE"):
@@ -110,7 +144,7 @@ def main():
     comm = NcclComm.from_torch_distributed()
     failed = []
 
-    errs = direct_abi(comm, rank, world, dev)
+    errs = direct_abi(comm, rank, world, dev) + direct_abi_rows(comm, rank, world, dev)
     allerrs = [None] * world
     dist.all_gather_object(allerrs, errs)
     worst = max(max(e) for e in allerrs)
@@ -142,6 +176,36 @@ def main():
             if not (max(es) < 2e-2 and n1 > 0 and n0 == 0):
                 failed.append(f"layer_small{lm}:{eng}")
             del ex1, ex0, x1, x0
+
+    # training step (forward + backward): all weight-gradient reduce-scatters
+    # fused (row and column splits) vs NCCL
+    from paper_2105_04663_b200.workloads import train_step_inputs, transformer_train_step
+    tdims = dict(B=4, S=256, M=1024, N=8, D=64, H=2048)
+    res = {}
+    for fusedflag in (True, False):
+        os.environ["SPMD_PEER_FUSION"] = "1" if fusedflag else "0"
+        tg = transformer_train_step(mesh, dtype=DType.BF16, **tdims)
+        tann, _ = propagate(tg)
+        tprog = partition(tann, world, plan="fast")
+        tins = train_step_inputs(**tdims, seed=5)
+        txs = []
+        for k, p in enumerate(tprog.graph.parameters):
+            piece = shard_data(tins[k], tann.parameters[k].sharding, devices=range(world))[rank]
+            t = torch.from_numpy(np.ascontiguousarray(piece, dtype=np.float32)).to(dev)
+            txs.append(t.to(torch.bfloat16).reshape((1,) + p.shape.dims))
+        tex = Executor(tprog, nparts=1, device=dev, comm=comm, partition_base=rank, fuse=True)
+        n_fused = sum(1 for v in tex._fused.values() if v[0] == "dot_rs")
+        res[fusedflag] = ([o.float() for o in tex.run(txs)], n_fused)
+    torch.cuda.synchronize()
+    terr = max(rel(a, b) for a, b in zip(res[True][0], res[False][0]))
+    tall = [None] * world
+    dist.all_gather_object(tall, terr)
+    if rank == 0:
+        print(json.dumps({"section": "train_step", "mesh": mesh, "fused_dot_rs": res[True][1],
+                          "unfused": res[False][1], "max_rel": max(tall)}), flush=True)
+    if not (max(tall) < 2e-2 and res[True][1] >= 6 and res[False][1] == 0):
+        failed.append("train_step")
+    os.environ.pop("SPMD_PEER_FUSION", None)
 
     # MoE layer: expert FFN-out einsum + combine all-to-all fused over peer
     # memory (and the dense dispatch einsum + all-to-all) vs NCCL

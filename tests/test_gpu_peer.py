@@ -129,3 +129,35 @@ def test_dot_all_to_all_world_of_one(comm):
         torch.cuda.synchronize()
         C.check(lib.spmd_check_device_errors(s), "device")
         assert torch.equal(fused, plain)
+
+
+def test_dot_reduce_scatter_rows_world_of_one(comm):
+    """Reduce-scatter on the leading (row) output dim -- the weight-gradient
+    case dW[M,N,D] = x^T.dy split on M -- through the row-scatter epilogue:
+    with one member it equals the plain dot bit for bit."""
+    import torch
+    from paper_2105_04663_b200 import _capi as C
+    from paper_2105_04663_b200.executor import _groups_arg, desc
+    from paper_2105_04663_b200.ir import DType, Shape
+    lib, s = C.lib(), torch.cuda.current_stream().cuda_stream
+    garr, ng, gs = _groups_arg([[0]])
+    T, M, N, D = 256, 256, 8, 64   # x [T, M], dy [T, N, D] -> dW [M, N, D]
+    dd = C.SpmdDotDims()
+    dd.n_contract = 1
+    dd.lhs_contracting[0], dd.rhs_contracting[0] = 0, 0
+    ash, bsh = Shape((T, M), DType.BF16), Shape((T, N, D), DType.BF16)
+    osh = Shape((M, N, D), DType.BF16)
+    for it in range(2):
+        torch.manual_seed(20 + it)
+        a = torch.randn((1, T, M), device="cuda").bfloat16()
+        b = (torch.randn((1, T, N, D), device="cuda") * 0.05).bfloat16()
+        fused = torch.empty((1, M, N, D), device="cuda", dtype=torch.bfloat16)
+        plain = torch.empty_like(fused)
+        C.check(lib.spmd_dot_reduce_scatter(comm.handle, desc(a, ash), desc(b, bsh),
+                                            desc(fused, osh), ctypes.byref(dd), 0, garr, ng, gs,
+                                            s), "dot_rs_rows")
+        C.check(lib.spmd_dot(desc(a, ash), desc(b, bsh), desc(plain, osh), ctypes.byref(dd), 1,
+                             s), "dot")
+        torch.cuda.synchronize()
+        C.check(lib.spmd_check_device_errors(s), "device")
+        assert torch.equal(fused, plain)
