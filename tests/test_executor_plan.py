@@ -122,3 +122,58 @@ def test_engine_policy_under_overlap():
         # the weight gathers of the later projections are hidden, the first
         # activation gather is not
         assert 0 in eng.values() and any(v != 0 for v in eng.values())
+
+
+@pytest.mark.parametrize("mesh", [(2, 2), (2, 4)])
+def test_training_step_gradient_reduce_scatters_all_fuse(mesh):
+    """Every weight-gradient reduce-scatter of the training step becomes a
+    fused GEMM epilogue: column splits (last dim) and row splits (dim 0,
+    dW[M, ...] split on M, wide kernel)."""
+    from paper_2105_04663_b200.workloads import transformer_train_step
+    g = transformer_train_step(mesh, dtype=DType.BF16, B=16, S=1024, M=8192, N=128, D=256,
+                               H=65536)
+    prog = partition(propagate(g)[0], mesh[0] * mesh[1], plan="fast")
+    comm = FakeComm()
+    ex = Executor(prog, nparts=1, device="cpu", comm=comm, partition_base=0, fuse=True,
+                  overlap=False)
+    rs = [i for i in prog.graph.instructions if i.opcode == Op.REDUCE_SCATTER]
+    fused = {k: v for k, v in ex._fused.items() if v[0] == "dot_rs"}
+    assert len(rs) == 12 and len(fused) == 12
+    dims = {v[2].attrs["dim"] for v in fused.values()}
+    assert 0 in dims and any(d > 0 for d in dims)
+    assert comm.peer > 0
+
+
+class _Arr:
+    def __init__(self, *shape):
+        self.shape = shape
+
+
+@pytest.mark.parametrize("routed", [False, True])
+def test_moe_all_to_alls_fuse(routed):
+    """C3 over 4: the expert FFN-out einsum + combine all-to-all fuse into the
+    GEMM's row-scatter epilogue; the dispatch exchange fuses with the dense
+    dispatch einsum, or -- under a declared routing -- with the dispatch
+    gather (rows pushed into the owners' heaps)."""
+    from paper_2105_04663_b200.executor import Routing
+    from paper_2105_04663_b200.workloads import moe_layer
+    g, _ = moe_layer(4, E=8, B=64, S=512, C=160, M=4096, H=16384, dtype=DType.BF16,
+                     with_inputs=False)
+    ann, _ = propagate(g)
+    prog = partition(ann, 4, plan="fast")
+    routing = None
+    if routed:
+        r = Routing(_Arr(1, 16, 512), _Arr(1, 16, 512), _Arr(1, 16, 512))
+        idx = {p.id: p.attrs["index"] for p in ann.parameters}
+        routing = {idx["dispatch"]: r, idx["combine"]: r}
+    ex = Executor(prog, nparts=1, device="cpu", comm=FakeComm(), partition_base=0, fuse=True,
+                  overlap=False, routing=routing)
+    kinds = sorted(v[0] for k, v in ex._fused.items() if k not in ex._fused_skip)
+    a2a = [i.id for i in prog.graph.instructions if i.opcode == Op.ALL_TO_ALL]
+    assert len(a2a) == 2
+    if routed:
+        assert ex._fused[a2a[0]][0] == "moe_dispatch_a2a" and ex._fused[a2a[1]][0] == "dot_a2a"
+        assert "moe_combine" in kinds
+    else:
+        assert [ex._fused[x][0] for x in a2a] == ["dot_a2a", "dot_a2a"]
+    assert not any(s.coll for s in ex.steps if s.ins.id in a2a)
