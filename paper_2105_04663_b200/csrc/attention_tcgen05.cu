@@ -448,8 +448,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
       mbar_wait(&s_full[sb], (j >> 1) & 1);
       tc_fence_after();
       uint32_t r0[32], r1[32];
-      tmem_ld32(tmem + lane_base + S_COL + sb * 64, r0);
-      tmem_ld32(tmem + lane_base + S_COL + sb * 64 + 32, r1);
+      tmem_ld32_nowait(tmem + lane_base + S_COL + sb * 64, r0);
+      tmem_ld32_nowait(tmem + lane_base + S_COL + sb * 64 + 32, r1);
+      tmem_wait_ld();
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_leader(&s_free[sb]);

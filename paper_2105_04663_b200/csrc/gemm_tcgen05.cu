@@ -658,18 +658,28 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
       mbar_wait(tfull, acc_ph);
       tc_fence_after();
       const int row0 = m * BM2 + rank * HALF + quarter * 32;
+      const uint32_t tbase = tmem + ((uint32_t)(quarter * 32) << 16) + half * WHALF_N;
+      // software-pipelined drain: chunk c+1's TMEM load is in flight while
+      // chunk c is converted and stored
+      uint32_t ra[32], rb[32];
+      tmem_ld32_nowait(tbase, ra);
+      tmem_wait_ld();
 #pragma unroll 1
       for (int c0 = 0; c0 < WHALF_N; c0 += 32) {
         uint32_t r[32];
-        tmem_ld32(tmem + ((uint32_t)(quarter * 32) << 16) + half * WHALF_N + c0, r);
+#pragma unroll
+        for (int i = 0; i < 32; ++i) r[i] = ra[i];
+        if (c0 + 32 < WHALF_N) tmem_ld32_nowait(tbase + c0 + 32, rb);
         const int col = n * WBN + half * WHALF_N + c0;
-        if (col >= g.N) continue;
-        if (g.scatter && g.sc_rows) {
-          if (row0 >= g.M) continue;
-          const int j = (int)(row0 / g.sc_rchunk);
-          epi_store_chunk(&smaps.m[j], epi + (chunk++ & 1) * EPI_STAGE_BYTES, r, g.relu, col,
-                          (int)(row0 - j * g.sc_rchunk),
-                          par * g.sc_nslots + g.sc_slot_base + b, lane);
+        if (col >= g.N) {
+          // past N: nothing to store (keep the load pipeline in step)
+        } else if (g.scatter && g.sc_rows) {
+          if (row0 < g.M) {
+            const int j = (int)(row0 / g.sc_rchunk);
+            epi_store_chunk(&smaps.m[j], epi + (chunk++ & 1) * EPI_STAGE_BYTES, r, g.relu, col,
+                            (int)(row0 - j * g.sc_rchunk),
+                            par * g.sc_nslots + g.sc_slot_base + b, lane);
+          }
         } else if (g.scatter) {
           const int j = (int)(col / g.sc_chunk);
           epi_store_chunk(&smaps.m[j], epi + (chunk++ & 1) * EPI_STAGE_BYTES, r, g.relu,
@@ -677,6 +687,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
         } else {
           epi_store_chunk(&map_c, epi + (chunk++ & 1) * EPI_STAGE_BYTES, r, g.relu, col, row0,
                           b, lane, store_pol);
+        }
+        if (c0 + 32 < WHALF_N) {
+          tmem_wait_ld();
+#pragma unroll
+          for (int i = 0; i < 32; ++i) ra[i] = rb[i];
         }
       }
       tc_fence_before();
