@@ -299,8 +299,7 @@ class Executor:
         import os
         force = os.environ.get("SPMD_PEER_AG_ENGINE", "auto")
         # hidden gathers: copy engines (0), background SM pull (3) or NCCL (-1)
-        hidden_engine = {"ce": 0, "sm": 3, "nccl": -1}[
-            os.environ.get("SPMD_PEER_HIDDEN_ENGINE", "ce")]
+        hidden_mode = os.environ.get("SPMD_PEER_HIDDEN_ENGINE", "ce")
         heavy_ops = (Op.DOT, Op.CONVOLUTION)
         heavy_fused = ("dot_relu", "conv_relu", "attention", "dot_rs", "dot_a2a")
         eng = {}
@@ -322,7 +321,16 @@ class Executor:
                         hidden = True
                         break
             gs = len(st.ins.attrs["subgroups"][0])
-            eng[st.ins.id] = hidden_engine if hidden else (1 if gs <= 2 else -1)
+            if hidden:
+                # copy engines move contiguous pieces well; a gather along an
+                # inner dim is a 2-D copy of many short rows (slow on the
+                # copy engines): "mixed" sends those to the background SM pull
+                leading = all(d == 1 for d in self._shape(st.ins.operands[0]).dims[
+                    :st.ins.attrs["dim"]])
+                eng[st.ins.id] = {"ce": 0, "sm": 3, "nccl": -1}.get(
+                    hidden_mode, 0 if leading else 3)
+            else:
+                eng[st.ins.id] = 1 if gs <= 2 else -1
         return eng
 
     def _workspace_bytes(self) -> int:
