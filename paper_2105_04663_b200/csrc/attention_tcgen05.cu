@@ -589,6 +589,284 @@ static int launch_attention(const CUtensorMap& mq, const CUtensorMap& mk, const 
   return launched(s);
 }
 
+// ---------------------------------------------------------------------------
+// 128-key tiles for the CTA pair: S = Q.K^T per tile is one N=128 UMMA chain
+// (64 keys per CTA), PV has K=128, and the per-key barrier / issue overheads
+// halve.  P is single-buffered (32 KB): the softmax keeps its 128 values in
+// registers while PV(j-1) drains, then writes P(j).  TMEM: O [0, D), S double
+// buffer at 256 and 384.  SPMD_ATTN_KT=64 selects the 64-key kernel.
+// ---------------------------------------------------------------------------
+template <int D>
+struct Attn2SmemK128 {
+  static constexpr int Q_BYTES = 128 * D * 2;           // own 128 rows
+  static constexpr int K_HALF = 64 * D * 2;             // 64 keys x D
+  static constexpr int V_HALF = 128 * (D / 2) * 2;      // 128 keys x D/2
+  static constexpr int SLOT = K_HALF + V_HALF;
+  static constexpr int STAGES = D >= 256 ? 2 : 3;
+  static constexpr int P_BYTES = 128 * 128 * 2;         // 128 rows x 128 keys
+  static constexpr int KV_OFF = Q_BYTES;
+  static constexpr int P_OFF = KV_OFF + STAGES * SLOT;
+  static constexpr int BAR_OFF = P_OFF + P_BYTES;
+  static constexpr int TOTAL = BAR_OFF + 512 + 1024;
+};
+
+template <int D>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
+    attention_tcgen05_2sm_k128(const __grid_constant__ CUtensorMap map_q,
+                               const __grid_constant__ CUtensorMap map_k,
+                               const __grid_constant__ CUtensorMap map_v,
+                               const __grid_constant__ CUtensorMap map_o, AttnShape g) {
+  typedef Attn2SmemK128<D> L;
+  constexpr int DC = D / 64, NS = L::STAGES, KT = 128;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint64_t* bars = (uint64_t*)(smem + L::BAR_OFF);
+  uint64_t* q_full = bars + 0;
+  uint64_t* kv_full = bars + 1;            // [NS] leader
+  uint64_t* kv_empty = kv_full + NS;       // [NS] both (multicast)
+  uint64_t* s_full = kv_empty + NS;        // [2] both (multicast)
+  uint64_t* s_free = s_full + 2;           // [2] leader, 8 arrivals
+  uint64_t* p_full = s_free + 2;           // [1] leader, 8 arrivals
+  uint64_t* pv_done = p_full + 1;          // [1] both (multicast)
+  uint32_t* tmem_slot = (uint32_t*)(pv_done + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_rank();
+  const bool leader = rank == 0;
+  const int nSt = (g.S + 255) / 256;
+  const int cl = blockIdx.x >> 1;
+  const int st = cl % nSt;
+  const int rest = cl / nSt;
+  const int n = rest % g.N, b = rest / g.N;
+  const int nT = (g.T + KT - 1) / KT;
+  const int row0 = st * 256 + rank * 128;
+
+  if (threadIdx.x == 0) {
+    mbar_init(q_full, 1);
+    for (int i = 0; i < NS; ++i) {
+      mbar_init(&kv_full[i], 1);
+      mbar_init(&kv_empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&s_full[i], 1);
+      mbar_init(&s_free[i], 8);
+    }
+    mbar_init(p_full, 8);
+    mbar_init(pv_done, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                     smem_u32(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t O_COL = 0, S_COL = 256;
+  uint8_t* sq = smem;
+  uint8_t* skv = smem + L::KV_OFF;
+  uint8_t* sp = smem + L::P_OFF;
+
+  if (warp == 0 && lane == 0) {
+    if (leader) mbar_expect_tx(q_full, 2 * L::Q_BYTES);
+#pragma unroll
+    for (int c = 0; c < DC; ++c)
+      tma_load_4d_2sm(sq + c * 16384, &map_q, q_full, c * 64, row0, n, b);
+    for (int j = 0; j < nT; ++j) {
+      const int slot = j % NS;
+      mbar_wait(&kv_empty[slot], ((j / NS) & 1) ^ 1);
+      uint8_t* kk = skv + slot * L::SLOT;
+      uint8_t* vv = kk + L::K_HALF;
+      if (leader) mbar_expect_tx(&kv_full[slot], 2 * L::SLOT);
+      // K: this CTA's 64 keys, D in 64-wide chunks of 64 rows x 128 B
+#pragma unroll
+      for (int c = 0; c < DC; ++c)
+        tma_load_4d_2sm(kk + c * 8192, &map_k, &kv_full[slot], c * 64, j * KT + rank * 64, n, b);
+      // V: all 128 keys, this CTA's D/2 columns, chunks of 128 rows x 128 B
+#pragma unroll
+      for (int c = 0; c < DC / 2; ++c)
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+          tma_load_4d_2sm(vv + c * 16384 + h * 8192, &map_v, &kv_full[slot],
+                          rank * (D / 2) + c * 64, j * KT + h * 64, n, b);
+    }
+  } else if (warp == 1 && lane == 0 && leader) {
+    const uint32_t idesc_s = make_idesc(256, KT, 0, 0);
+    const uint32_t idesc_o = make_idesc(256, D, 0, 1);
+    mbar_wait(q_full, 0);
+    auto issue_s = [&](int j) {
+      const int slot = j % NS, sb = j & 1;
+      mbar_wait(&kv_full[slot], (j / NS) & 1);
+      if (j >= 2) mbar_wait(&s_free[sb], ((j >> 1) - 1) & 1);
+      tc_fence_after();
+      const uint32_t qa = smem_u32(sq), ka = smem_u32(skv + slot * L::SLOT);
+#pragma unroll
+      for (int c = 0; c < DC; ++c)
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          tc_mma_2sm(tmem + S_COL + sb * KT, make_desc(qa + c * 16384 + k * 32, 16, 1024),
+                     make_desc(ka + c * 8192 + k * 32, 16, 1024), idesc_s, (c | k) != 0);
+      tc_commit_2sm_mc(&s_full[sb]);
+    };
+    auto issue_pv = [&](int j) {
+      const int slot = j % NS;
+      mbar_wait(p_full, j & 1);
+      tc_fence_after();
+      const uint32_t pa = smem_u32(sp);
+      const uint32_t va = smem_u32(skv + slot * L::SLOT + L::K_HALF);
+#pragma unroll
+      for (int k = 0; k < KT / 16; ++k)
+        tc_mma_2sm(tmem + O_COL, make_desc(pa + (k >> 2) * 16384 + (k & 3) * 32, 16, 1024),
+                   make_desc(va + k * 2048, 16384, 1024), idesc_o, (j | k) != 0);
+      tc_commit_2sm_mc(pv_done);
+      tc_commit_2sm_mc(&kv_empty[slot]);
+    };
+    issue_s(0);
+    for (int j = 1; j < nT; ++j) {
+      issue_s(j);
+      issue_pv(j - 1);
+    }
+    issue_pv(nT - 1);
+  } else if (warp >= 4) {
+    const int ew = warp - 4;
+    const int row = ew * 32 + lane;
+    const uint32_t lane_base = (uint32_t)(ew * 32) << 16;
+    float m = -INFINITY, l = 0.f;
+    for (int j = 0; j < nT; ++j) {
+      const int sb = j & 1;
+      mbar_wait(&s_full[sb], (j >> 1) & 1);
+      tc_fence_after();
+      float s[KT];
+      {
+        uint32_t r[4][32];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) tmem_ld32_nowait(tmem + lane_base + S_COL + sb * KT + q * 32, r[q]);
+        tmem_wait_ld();
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+#pragma unroll
+          for (int i = 0; i < 32; ++i) s[q * 32 + i] = __uint_as_float(r[q][i]) * g.scale_log2e;
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_leader(&s_free[sb]);
+      const int valid = g.T - j * KT;
+      float mx = -INFINITY;
+#pragma unroll
+      for (int i = 0; i < KT; ++i) {
+        if (i >= valid) s[i] = -INFINITY;
+        mx = fmaxf(mx, s[i]);
+      }
+      float alpha = 1.f;
+      bool resc = false;
+      if (m == -INFINITY) {
+        m = mx;
+      } else if (mx > m + 8.f) {
+        alpha = ex2(m - mx);
+        m = mx;
+        resc = true;
+      }
+      const float mb = m == -INFINITY ? 0.f : m;
+      float rs = 0.f;
+#pragma unroll
+      for (int i = 0; i < KT; ++i) {
+        s[i] = ex2(s[i] - mb);
+        rs += s[i];
+      }
+      l = l * alpha + rs;
+      // P is single-buffered and O may need rescaling: PV(j-1) must be done
+      if (j >= 1) mbar_wait(pv_done, (j - 1) & 1);
+      if (j > 0 && __any_sync(0xffffffffu, resc)) {
+        tc_fence_after();
+#pragma unroll 1
+        for (int c = 0; c < D; c += 32) {
+          uint32_t o[32];
+          tmem_ld32(tmem + lane_base + O_COL + c, o);
+#pragma unroll
+          for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
+          tmem_st32(tmem + lane_base + O_COL + c, o);
+        }
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      }
+#pragma unroll
+      for (int a = 0; a < 2; ++a) {          // two 64-key SW128 atoms
+        uint8_t* prow = sp + a * 16384 + row * 128;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          uint4 v;
+          __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&v);
+#pragma unroll
+          for (int t = 0; t < 4; ++t)
+            h[t] = __floats2bfloat162_rn(s[a * 64 + q * 8 + 2 * t], s[a * 64 + q * 8 + 2 * t + 1]);
+          *reinterpret_cast<uint4*>(prow + ((q ^ (row & 7)) << 4)) = v;
+        }
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_leader(p_full);
+    }
+    mbar_wait(pv_done, (nT - 1) & 1);
+    tc_fence_after();
+    const float inv = l > 0.f ? 1.f / l : 0.f;
+#pragma unroll 1
+    for (int c = 0; c < D; c += 32) {
+      uint32_t o[32];
+      tmem_ld32(tmem + lane_base + O_COL + c, o);
+      uint8_t* orow = sq + (c / 64) * 16384 + row * 128;
+      const int qbase = (c % 64) / 8;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        uint4 v;
+        __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&v);
+#pragma unroll
+        for (int t = 0; t < 4; ++t)
+          h[t] = __floats2bfloat162_rn(__uint_as_float(o[q * 8 + 2 * t]) * inv,
+                                       __uint_as_float(o[q * 8 + 2 * t + 1]) * inv);
+        *reinterpret_cast<uint4*>(orow + (((qbase + q) ^ (row & 7)) << 4)) = v;
+      }
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("bar.sync 1, 128;" ::: "memory");
+    if (threadIdx.x == 128) {
+#pragma unroll
+      for (int c = 0; c < DC; ++c)
+        asm volatile(
+            "cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%2, %3, %4, %5}], [%1];" ::
+                "l"(reinterpret_cast<uint64_t>(&map_o)),
+            "r"(smem_u32(sq + c * 16384)), "r"(c * 64), "r"(row0), "r"(n), "r"(b)
+            : "memory");
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      bulk_wait_all();
+    }
+  }
+  tc_fence_before();
+  cluster_sync();
+  if (warp == 2) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+  }
+}
+
+template <int D>
+static int launch_attention_2sm_k128(const CUtensorMap& mq, const CUtensorMap& mk,
+                                     const CUtensorMap& mv, const CUtensorMap& mo, AttnShape g,
+                                     cudaStream_t s) {
+  typedef Attn2SmemK128<D> L;
+  static_assert(L::TOTAL <= 232448, "attention k128 smem");
+  static bool configured = false;
+  if (!configured) {
+    SPMD_CUDA_TRY(cudaFuncSetAttribute(attention_tcgen05_2sm_k128<D>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, L::TOTAL));
+    configured = true;
+  }
+  const int64_t grid = 2 * (int64_t)((g.S + 255) / 256) * g.N * g.Bp;
+  attention_tcgen05_2sm_k128<D><<<(unsigned)grid, 256, L::TOTAL, s>>>(mq, mk, mv, mo, g);
+  return launched(s);
+}
+
 template <int D>
 static int launch_attention_2sm(const CUtensorMap& mq, const CUtensorMap& mk,
                                 const CUtensorMap& mv, const CUtensorMap& mo, AttnShape g,
@@ -643,6 +921,19 @@ extern "C" int spmd_attention_layout(spmd_tensor q, spmd_tensor k, spmd_tensor v
   if (mode < 0) {
     const char* e = getenv("SPMD_ATTN_MODE");
     mode = (e && strcmp(e, "1sm") == 0) ? 1 : 2;
+  }
+  // key tile: 128 for D=128 (549 vs 469 TF/s at T=1024), 64 for D=256 (equal at
+  // T=1024, 993 vs 955 TF/s at T=4096: 3 K/V stages fit) -- profiles/r1_attention_kt.jsonl
+  static int kt_env = -2;
+  if (kt_env == -2) {
+    const char* e = getenv("SPMD_ATTN_KT");
+    kt_env = e ? atoi(e) : -1;
+  }
+  const int kt = kt_env > 0 ? kt_env : (D == 128 ? 128 : 64);
+  if (mode == 2 && D >= 128 && kt == 128) {
+    // 128-key tiles: K boxes of 64 rows (mk), V boxes of 64 rows (mv)
+    if (D == 128) return launch_attention_2sm_k128<128>(mq, mk, mv, mo, g, s);
+    return launch_attention_2sm_k128<256>(mq, mk, mv, mo, g, s);
   }
   if (mode == 2 && D >= 128) {
     CUtensorMap mk2;   // K split by keys: 32-row boxes
