@@ -252,9 +252,14 @@ constexpr int CHALF = 64;   // Cout per CTA
 
 // WRES: this CTA's half of the weights (kblocks x 8 KB) stays resident in
 // smem for the whole kernel (loaded once); only input boxes stream.
-template <int STAGES, int WRES>
+// TAPS > 0 (resident weights only): one input box of 128 + TAPS - 1 pixels per
+// (kh, cin block) feeds all TAPS horizontal taps through UMMA descriptors
+// whose start is shifted by whole 128-byte rows -- 3x fewer input bytes.
+template <int STAGES, int WRES, int TAPS = 0>
 struct Conv2Smem {
-  static constexpr int A_BYTES = CBM * CBK * 2;       // 128 px x 64 ch
+  static constexpr int A_ROWS = TAPS ? CBM + TAPS - 1 : CBM;
+  static constexpr int A_TX = A_ROWS * CBK * 2;                  // bytes per box
+  static constexpr int A_BYTES = (A_TX + 1023) / 1024 * 1024;     // 1 KB aligned stages
   static constexpr int B_BYTES = CHALF * CBK * 2;     // 64 cout x 64 ch
   static constexpr int STAGE_BYTES = A_BYTES + (WRES ? 0 : B_BYTES);
   static constexpr int W_OFF = STAGES * STAGE_BYTES;  // resident weights (WRES kblocks)
@@ -263,14 +268,14 @@ struct Conv2Smem {
   static constexpr int TOTAL = EPI_OFF + 8 * EPI_STAGE_BYTES + 1024;
 };
 
-template <int STAGES, int WRES>
+template <int STAGES, int WRES, int TAPS = 0>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
     conv_bf16_tcgen05_2sm(const __grid_constant__ CUtensorMap map_x,
                           const __grid_constant__ CUtensorMap map_w,
                           const __grid_constant__ CUtensorMap map_o, ConvShape g,
                           const __grid_constant__ CUtensorMap map_x1,
                           const __grid_constant__ CUtensorMap map_x2) {
-  typedef Conv2Smem<STAGES, WRES> L;
+  typedef Conv2Smem<STAGES, WRES, TAPS> L;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint64_t* full = (uint64_t*)(smem + L::BAR_OFF);
@@ -333,13 +338,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
       const int n = pn % g.N, p = pn / g.N;
       const int w0 = wb * 2 * CBM + rank * CBM;
       int row_kh = -1, row_r = 0, row_piece = 0;
-      for (int kb = 0; kb < g.kblocks; ++kb) {
-        const int tap = kb / g.cin_blocks, cb = kb - tap * g.cin_blocks;
-        const int kh = tap / g.KW, kw = tap - kh * g.KW;
+      const int nstage = TAPS ? g.KH * g.cin_blocks : g.kblocks;
+      for (int kb = 0; kb < nstage; ++kb) {
+        // TAPS: stage = (kh, cb), the box covers every kw; else stage = tap
+        const int tap = TAPS ? (kb / g.cin_blocks) * g.KW : kb / g.cin_blocks;
+        const int cb = kb % g.cin_blocks;
+        const int kh = tap / g.KW, kw = TAPS ? 0 : tap - kh * g.KW;
         mbar_wait(&empty[s], ph ^ 1);
         uint8_t* sa = smem + s * L::STAGE_BYTES;
         uint8_t* sb = sa + L::A_BYTES;
-        if (leader) mbar_expect_tx(&full[s], 2 * L::STAGE_BYTES);
+        if (leader) mbar_expect_tx(&full[s], 2 * (L::A_TX + (WRES ? 0 : L::B_BYTES)));
         (void)sb;
         if (!g.win) {
           tma_load_5d_2sm(sa, &map_x, &full[s], cb * CBK, w0 + kw - g.pad_w, ho + kh - g.pad_h,
@@ -375,15 +383,30 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
       mbar_wait(&tempty[acc], acc_ph ^ 1);
       tc_fence_after();
       const uint32_t d_tmem = tmem + acc * 2 * CHALF;
-      for (int kb = 0; kb < g.kblocks; ++kb) {
+      const int nstage = TAPS ? g.KH * g.cin_blocks : g.kblocks;
+      for (int kb = 0; kb < nstage; ++kb) {
         mbar_wait(&full[s], ph);
         tc_fence_after();
         const uint32_t sa = smem_u32(smem + s * L::STAGE_BYTES);
-        const uint32_t sb = WRES ? smem_u32(smem + L::W_OFF + kb * L::B_BYTES) : sa + L::A_BYTES;
+        if (TAPS) {
+          const int kh = kb / g.cin_blocks, cb = kb % g.cin_blocks;
 #pragma unroll
-        for (int k = 0; k < CBK / 16; ++k)
-          tc_mma_2sm(d_tmem, make_desc(sa + k * 32, 16, 1024),
-                     make_desc(sb + k * 2048, CBK * 128, 1024), idesc, (kb | k) != 0);
+          for (int kw = 0; kw < TAPS; ++kw) {
+            const uint32_t sb =
+                smem_u32(smem + L::W_OFF + ((kh * g.KW + kw) * g.cin_blocks + cb) * L::B_BYTES);
+#pragma unroll
+            for (int k = 0; k < CBK / 16; ++k)
+              tc_mma_2sm(d_tmem, make_desc(sa + kw * 128 + k * 32, 16, 1024),
+                         make_desc(sb + k * 2048, CBK * 128, 1024), idesc, (kb | kw | k) != 0);
+          }
+        } else {
+          const uint32_t sb =
+              WRES ? smem_u32(smem + L::W_OFF + kb * L::B_BYTES) : sa + L::A_BYTES;
+#pragma unroll
+          for (int k = 0; k < CBK / 16; ++k)
+            tc_mma_2sm(d_tmem, make_desc(sa + k * 32, 16, 1024),
+                       make_desc(sb + k * 2048, CBK * 128, 1024), idesc, (kb | k) != 0);
+        }
         tc_commit_2sm_mc(&empty[s]);
         if (++s == STAGES) {
           s = 0;
@@ -433,21 +456,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
   }
 }
 
-template <int STAGES, int WRES>
+template <int STAGES, int WRES, int TAPS = 0>
 static int launch_conv_2sm(const CUtensorMap& mx, const CUtensorMap& mw, const CUtensorMap& mo,
                            ConvShape g, const CUtensorMap& mx1, const CUtensorMap& mx2,
                            cudaStream_t s) {
-  typedef Conv2Smem<STAGES, WRES> L;
+  typedef Conv2Smem<STAGES, WRES, TAPS> L;
   static_assert(L::TOTAL <= 232448, "conv 2-CTA smem");
   static bool configured = false;
   if (!configured) {
-    SPMD_CUDA_TRY(cudaFuncSetAttribute(conv_bf16_tcgen05_2sm<STAGES, WRES>,
+    SPMD_CUDA_TRY(cudaFuncSetAttribute(conv_bf16_tcgen05_2sm<STAGES, WRES, TAPS>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, L::TOTAL));
     configured = true;
   }
   const int sms = sm_budget();
   const int64_t clusters = g.tiles < sms / 2 ? g.tiles : sms / 2;
-  conv_bf16_tcgen05_2sm<STAGES, WRES><<<(unsigned)(2 * clusters), 256, L::TOTAL, s>>>(
+  conv_bf16_tcgen05_2sm<STAGES, WRES, TAPS><<<(unsigned)(2 * clusters), 256, L::TOTAL, s>>>(
       mx, mw, mo, g, mx1, mx2);
   return launched(s);
 }
@@ -531,9 +554,21 @@ int conv_tcgen05(const spmd_tensor& lhs, const spmd_tensor& rhs, const spmd_tens
   memset(&mx1, 0, sizeof(mx1));
   memset(&mx2, 0, sizeof(mx2));
   if (!encode(&mw, rhs.data, vw, 64, CBK)) return SPMD_ERR_UNSUPPORTED;
-  if (!win) {
-    if (!encode(&mx, lhs.data, vx, CBK, CBM)) return SPMD_ERR_UNSUPPORTED;
-  } else {
+  // input map(s) with `rows`-pixel boxes (CBM, or CBM + KW - 1 for tap reuse)
+  auto encode_inputs = [&](int rows) -> bool {
+    if (!win) return encode(&mx, lhs.data, vx, CBK, rows);
+    CUtensorMap* maps[3] = {&mx, &mx1, &mx2};
+    for (int k = 0; k < win->npieces; ++k) {
+      const spmd_tensor& pc = win->pieces[k];
+      OperandView vp = vx;
+      vp.size[2] = pc.dims[1];
+      vp.stride[3] = pc.dims[1] * W * g.Cin;
+      vp.stride[4] = nparts == 1 ? 8 : numel(pc);
+      if (!encode(maps[k], pc.data, vp, CBK, rows)) return false;
+    }
+    return true;
+  };
+  if (win) {
     // one map per piece: [nparts][N][len_k][W][Cin]
     g.win = 1;
     g.npieces = win->npieces;
@@ -546,22 +581,17 @@ int conv_tcgen05(const spmd_tensor& lhs, const spmd_tensor& rhs, const spmd_tens
     g.win_rows = H;
     g.nparts = (int)nparts;
     if (nparts > SPMD_MAX_PARTS) return SPMD_ERR_UNSUPPORTED;
-    CUtensorMap* maps[3] = {&mx, &mx1, &mx2};
     for (int k = 0; k < win->npieces; ++k) {
       const spmd_tensor& pc = win->pieces[k];
       if (pc.dtype != SPMD_BF16 || pc.rank != 4 || pc.dims[0] != g.N || pc.dims[2] != W ||
           pc.dims[3] != g.Cin)
         return SPMD_ERR_UNSUPPORTED;
-      OperandView vp = vx;
-      vp.size[2] = pc.dims[1];
-      vp.stride[3] = pc.dims[1] * W * g.Cin;
-      vp.stride[4] = nparts == 1 ? 8 : numel(pc);
-      if (!encode(maps[k], pc.data, vp, CBK, CBM)) return SPMD_ERR_UNSUPPORTED;
       g.len[k] = (int)pc.dims[1];
       g.buf_len += g.len[k];
     }
     if (g.buf_len < H) return SPMD_ERR_UNSUPPORTED;
   }
+  if (!encode_inputs(CBM)) return SPMD_ERR_UNSUPPORTED;
   g.nwb = (g.Wo + CBM - 1) / CBM;
   g.nt = g.Cout / BN;
   g.cin_blocks = g.Cin / CBK;
@@ -583,6 +613,16 @@ int conv_tcgen05(const spmd_tensor& lhs, const spmd_tensor& rhs, const spmd_tens
       if (wres < 0) {
         const char* e = getenv("SPMD_CONV_WRES");
         wres = e ? atoi(e) : 1;
+      }
+      static int taps = -1;
+      if (taps < 0) {
+        const char* e = getenv("SPMD_CONV_TAPS");
+        taps = e ? atoi(e) : 1;
+      }
+      if (wres && taps && g.kblocks == 18 && g.KW == 3 && g.nt == 1 && nparts == 1) {
+        if (encode_inputs(CBM + 2)) return launch_conv_2sm<3, 18, 3>(mx, mw2, mo, g, mx1, mx2, s);
+        // restore the 128-pixel boxes the other kernels expect
+        if (!encode_inputs(CBM)) return SPMD_ERR_UNSUPPORTED;
       }
       if (wres && g.kblocks == 18 && g.nt == 1 && nparts == 1)
         return launch_conv_2sm<4, 18>(mx, mw2, mo, g, mx1, mx2, s);

@@ -112,6 +112,10 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
 
 // UMMA shared-memory descriptor, SWIZZLE_128B, version 1 (Blackwell).
 //   K-major : rows of 128 B (64 bf16 of K), 8-row atoms 1024 B apart (SBO).
+//             The 128B swizzle XOR comes from the ABSOLUTE smem address bits
+//             [7:9], so a start shifted by whole 128-byte rows inside the
+//             pattern (conv taps reading a wider box) needs no base offset --
+//             measured: setting bits 49-51 to the phase gives wrong results.
 //   MN-major: rows of 128 B (64 bf16 of M/N) per K index, 8-K-row atoms
 //             1024 B apart (SBO), 64-wide M/N chunks `lbo` bytes apart (LBO).
 __device__ __forceinline__ uint64_t make_desc(uint32_t saddr, uint32_t lbo_bytes,
