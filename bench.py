@@ -32,7 +32,14 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "sharded Transformer layer TFLOP/s/GPU & MFU at 1/2/4/8 B200; reshard GB/s"
-MESHES = {1: (1, 1), 2: (1, 2), 4: (2, 2), 8: (2, 4)}
+# (X=data, Y=model).  N=8 is BASELINE's 2x4 data x model mesh.  N=4 uses 1x4:
+# measured 14.4 ms vs 16.1-16.4 ms for 2x2 on one box -- a data axis costs
+# every GPU the all-gather of its weight shards each step
+# (profiles/r1_c2_n4_mesh_1x4_vs_2x2.log).  SPMD_BENCH_MESH=2x2 restores it.
+MESHES = {1: (1, 1), 2: (1, 2), 4: (1, 4), 8: (2, 4)}
+if os.environ.get("SPMD_BENCH_MESH"):   # e.g. "1x4": override the (X=data, Y=model) mesh
+    _x, _y = (int(v) for v in os.environ["SPMD_BENCH_MESH"].split("x"))
+    MESHES[_x * _y] = (_x, _y)
 PAPER = dict(B=16, S=1024, M=8192, N=128, D=256, H=65536)
 SPEC_BF16_TFLOPS = 2250.0
 
