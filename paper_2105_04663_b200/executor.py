@@ -165,6 +165,7 @@ class _Step:
     ops: tuple = ()         # value ids read
     coll: bool = False      # runs on a comm stream when overlapping
     lane: int = 0           # 0 compute stream, k >= 1: comm stream k - 1
+    after: tuple = ()       # extra value ids to wait for (just-in-time prefetch)
 
 
 class Executor:
@@ -221,8 +222,56 @@ class Executor:
         else:
             self._peer_ag = {}
         self._peer_engine = self._plan_peer_engines()
+        if self.comm_streams:
+            self.steps = self._jit_prefetch(self.steps)
         self._assign_lanes()
         self._lane_of = {st.cuda_stream: k + 1 for k, st in enumerate(self.comm_streams)}
+
+    def _jit_prefetch(self, steps: list) -> list:
+        """Background prefetch gathers (peer engines 0/3) move from "as early
+        as the operands exist" to just before the heavy compute step
+        SPMD_PREFETCH_DEPTH GEMMs ahead of their first consumer, and start only
+        when that GEMM can start.  They no longer pile up at the start of the
+        step, where they compete for NVLink with the critical gathers (at C2
+        2x2 the first critical gather took 0.50 instead of ~0.17 ms,
+        profiles/r1_timeline_c2_n4_wide.log).  SPMD_PREFETCH=asap keeps the
+        hoisted order."""
+        import os
+        if os.environ.get("SPMD_PREFETCH", "jit") == "asap":
+            return steps
+        # GEMMs ahead: 2 measured best at C2 2x2 (15.28 ms vs 15.76 for 1 and
+        # 15.56-16.81 for as-soon-as-possible, profiles/r1_c2_n4_ab_wide_lanes_engines.log)
+        depth = max(1, int(os.environ.get("SPMD_PREFETCH_DEPTH", "2")))
+        heavy_ops = (Op.DOT, Op.CONVOLUTION)
+        heavy_fused = ("dot_relu", "conv_relu", "attention", "dot_rs", "dot_a2a", "halo_conv")
+
+        def heavy(st):
+            f = self._fused.get(st.ins.id)
+            return not st.coll and (st.ins.opcode in heavy_ops or
+                                    (f is not None and f[0] in heavy_fused))
+        order = list(steps)
+        for g in [st for st in order if st.coll and self._peer_engine.get(st.ins.id, -1) in (0, 3)]:
+            i = order.index(g)
+            first = next((k for k in range(i + 1, len(order)) if g.ins.id in order[k].ops), None)
+            if first is None:
+                continue
+            hs = [k for k in range(first - 1, i, -1) if heavy(order[k])][:depth]
+            h = hs[-1] if hs else None
+            if h is None or h <= i + 1:
+                continue
+            # start when the GEMM it rides under can start: wait for that
+            # GEMM's operands too
+            g.after = tuple(o for o in order[h].ops if o not in g.ops)
+            order.pop(i)
+            order.insert(h - 1, g)     # h shifted down by one after the pop
+        last_use = {}
+        for k, st in enumerate(order):
+            for o in st.ops:
+                last_use[o] = k
+        keep = set(self.graph.outputs)
+        for k, st in enumerate(order):
+            st.frees = tuple(o for o in set(st.ops) if last_use.get(o) == k and o not in keep)
+        return order
 
     def _assign_lanes(self) -> None:
         """Collectives on comm lanes.  Lane 1 carries only the background
@@ -1368,7 +1417,9 @@ class Executor:
         for step in self.steps:
             lane = step.lane if step.coll else 0
             stream = streams[lane]
-            for o in step.ops:
+            for o in tuple(step.ops) + tuple(step.after):
+                if o not in lane_of and o not in env:
+                    continue
                 src = lane_of.get(o, 0)
                 if src == lane:
                     continue
