@@ -175,6 +175,16 @@ int spmd_attention_layout(spmd_tensor q, spmd_tensor k, spmd_tensor v, spmd_tens
                           float scale, int out_bsnd, int64_t nparts, void* stream);
 /* Row softmax over the last dim: out = exp(x - max) / sum(exp(x - max)). */
 int spmd_softmax_lastdim(spmd_tensor in, spmd_tensor out, int64_t nparts, void* stream);
+/* Softmax backward over the last dim (bf16, rows <= 1024):
+ * out = p * (dp - sum_last(dp * p)) -- the reference training graph's
+ * multiply/reduce/broadcast/subtract/multiply chain (minispmd evaluator.py
+ * elementwise + reduce ops) in one pass, fp32 row sum. */
+int spmd_softmax_backward_lastdim(spmd_tensor p, spmd_tensor dp, spmd_tensor out,
+                                  int64_t nparts, void* stream);
+/* ReLU backward: out = h > 0 ? g : 0 (compare GT + select over broadcast
+ * zeros in the reference graph), bf16 or f32. */
+int spmd_relu_backward(spmd_tensor h, spmd_tensor g, spmd_tensor out, int64_t nparts,
+                       void* stream);
 
 /* ---- GShard MoE routing + dispatch/combine permutations (config C3) ---------
  * The reference consumes a given one-hot dispatch tensor through a dense Dot

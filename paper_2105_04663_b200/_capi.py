@@ -83,6 +83,8 @@ _SIGNATURES = {
     "spmd_dot": ([_T, _T, _T, ctypes.POINTER(SpmdDotDims), _I64, _P], _I),
     "spmd_convolution": ([_T, _T, _T, ctypes.POINTER(SpmdConvDims), _I64, _P], _I),
     "spmd_softmax_lastdim": ([_T, _T, _I64, _P], _I),
+    "spmd_softmax_backward_lastdim": ([_T, _T, _T, _I64, _P], _I),
+    "spmd_relu_backward": ([_T, _T, _T, _I64, _P], _I),
     "spmd_attention": ([_T, _T, _T, _T, ctypes.c_float, _I64, _P], _I),
     "spmd_attention_layout": ([_T, _T, _T, _T, ctypes.c_float, _I, _I64, _P], _I),
     "spmd_mask_range": ([_T, _T, _T, _T, _I, _I64, _I64, _I, _I64, _P], _I),

@@ -315,3 +315,56 @@ extern "C" int spmd_convert(spmd_tensor in, spmd_tensor out, int64_t nparts, voi
   }
   return launched(s);
 }
+
+// ReLU backward: out = h > 0 ? g : 0 -- the compare / broadcast-zero / select
+// chain of the training graph in one pass (16-byte vectors for bf16/f32).
+template <typename T, int V>
+__global__ void relu_bwd_kernel(const T* __restrict__ h, const T* __restrict__ g,
+                                T* __restrict__ out, int64_t n) {
+  const int64_t nv = n / V;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nv;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    if constexpr (V == 1) {
+      out[i] = ld<T>(h[i]) > 0.f ? g[i] : st<T>(0.f);
+    } else {
+      const uint4 hv = __ldcs(reinterpret_cast<const uint4*>(h) + i);
+      const uint4 gv = __ldcs(reinterpret_cast<const uint4*>(g) + i);
+      uint4 ov;
+      const T* hh = reinterpret_cast<const T*>(&hv);
+      const T* gg = reinterpret_cast<const T*>(&gv);
+      T* oo = reinterpret_cast<T*>(&ov);
+#pragma unroll
+      for (int j = 0; j < V; ++j) oo[j] = ld<T>(hh[j]) > 0.f ? gg[j] : st<T>(0.f);
+      __stcs(reinterpret_cast<uint4*>(out) + i, ov);
+    }
+  }
+}
+
+extern "C" int spmd_relu_backward(spmd_tensor h, spmd_tensor g, spmd_tensor out, int64_t nparts,
+                                  void* stream) {
+  SPMD_CHECK_ARG(h.dtype == g.dtype && h.dtype == out.dtype &&
+                     (h.dtype == SPMD_BF16 || h.dtype == SPMD_F32) && numel(h) == numel(g) &&
+                     numel(h) == numel(out),
+                 "relu backward expects bf16/f32 h, g, out of one shape");
+  const int64_t n = numel(h) * nparts;
+  if (n == 0) return SPMD_OK;
+  const int V = 16 / elem_size(h.dtype);
+  cudaStream_t s = as_stream(stream);
+  if (n % V || (reinterpret_cast<uintptr_t>(h.data) & 15) ||
+      (reinterpret_cast<uintptr_t>(g.data) & 15) || (reinterpret_cast<uintptr_t>(out.data) & 15)) {
+    if (h.dtype == SPMD_BF16)
+      relu_bwd_kernel<bf16, 1><<<grid_for(n, 256), 256, 0, s>>>(
+          (const bf16*)h.data, (const bf16*)g.data, (bf16*)out.data, n);
+    else
+      relu_bwd_kernel<float, 1><<<grid_for(n, 256), 256, 0, s>>>(
+          (const float*)h.data, (const float*)g.data, (float*)out.data, n);
+    return launched(s);
+  }
+  if (h.dtype == SPMD_BF16)
+    relu_bwd_kernel<bf16, 8><<<grid_for(n / 8, 256), 256, 0, s>>>(
+        (const bf16*)h.data, (const bf16*)g.data, (bf16*)out.data, n);
+  else
+    relu_bwd_kernel<float, 4><<<grid_for(n / 4, 256), 256, 0, s>>>(
+        (const float*)h.data, (const float*)g.data, (float*)out.data, n);
+  return launched(s);
+}

@@ -317,6 +317,112 @@ extern "C" int spmd_reduce(spmd_tensor in, spmd_tensor init, spmd_tensor out, co
   return launched(s);
 }
 
+// Softmax backward over rows: out = p * (dp - sum_row(dp * p)), bf16 rows in
+// registers (one warp per row, 16-byte loads), fp32 row sum -- the
+// multiply / reduce / broadcast / subtract / multiply chain of the training
+// graph in one pass (reads p and dp once, writes out once).
+template <int CH>
+__global__ void __launch_bounds__(256, 4)
+    softmax_bwd_rows_bf16(const bf16* __restrict__ p, const bf16* __restrict__ dp,
+                          bf16* __restrict__ out, int64_t rows, int L) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t row = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); row < rows;
+       row += warps) {
+    const uint4* pp = reinterpret_cast<const uint4*>(p + row * L);
+    const uint4* gg = reinterpret_cast<const uint4*>(dp + row * L);
+    uint4* y = reinterpret_cast<uint4*>(out + row * L);
+    const int nch = L >> 3;
+    uint4 rp[CH], rg[CH];
+#pragma unroll
+    for (int i = 0; i < CH; ++i) {
+      const int c = lane + 32 * i;
+      rp[i] = c < nch ? __ldcs(pp + c) : make_uint4(0, 0, 0, 0);
+      rg[i] = c < nch ? __ldcs(gg + c) : make_uint4(0, 0, 0, 0);
+    }
+    float sum = 0.f;
+#pragma unroll
+    for (int i = 0; i < CH; ++i) {
+      const __nv_bfloat162* a = reinterpret_cast<const __nv_bfloat162*>(&rp[i]);
+      const __nv_bfloat162* b = reinterpret_cast<const __nv_bfloat162*>(&rg[i]);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float2 fa = __bfloat1622float2(a[j]), fb = __bfloat1622float2(b[j]);
+        sum = fmaf(fa.x, fb.x, fmaf(fa.y, fb.y, sum));
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+#pragma unroll
+    for (int i = 0; i < CH; ++i) {
+      const int c = lane + 32 * i;
+      if (c >= nch) continue;
+      const __nv_bfloat162* a = reinterpret_cast<const __nv_bfloat162*>(&rp[i]);
+      const __nv_bfloat162* b = reinterpret_cast<const __nv_bfloat162*>(&rg[i]);
+      uint4 o;
+      __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&o);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float2 fa = __bfloat1622float2(a[j]), fb = __bfloat1622float2(b[j]);
+        h[j] = __floats2bfloat162_rn(fa.x * (fb.x - sum), fa.y * (fb.y - sum));
+      }
+      __stcs(y + c, o);
+    }
+  }
+}
+
+// Any row length / alignment / float dtype: warp per row, two passes.
+template <typename T>
+__global__ void softmax_bwd_rows_kernel(const T* __restrict__ p, const T* __restrict__ dp,
+                                        T* __restrict__ out, int64_t rows, int64_t L) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t row = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); row < rows;
+       row += warps) {
+    const T* a = p + row * L;
+    const T* b = dp + row * L;
+    float sum = 0.f;
+    for (int64_t i = lane; i < L; i += 32) sum = fmaf(ld<T>(a[i]), ld<T>(b[i]), sum);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    for (int64_t i = lane; i < L; i += 32) out[row * L + i] = st<T>(ld<T>(a[i]) * (ld<T>(b[i]) - sum));
+  }
+}
+
+extern "C" int spmd_softmax_backward_lastdim(spmd_tensor p, spmd_tensor dp, spmd_tensor out,
+                                             int64_t nparts, void* stream) {
+  SPMD_CHECK_ARG(p.dtype == dp.dtype && p.dtype == out.dtype &&
+                     (p.dtype == SPMD_BF16 || p.dtype == SPMD_F32) && p.rank >= 1 &&
+                     numel(p) == numel(dp) && numel(p) == numel(out),
+                 "softmax backward expects bf16/f32 p, dp, out of one shape");
+  const int64_t L = p.dims[p.rank - 1];
+  const int64_t rows = L ? numel(p) / L * nparts : 0;
+  if (rows == 0) return SPMD_OK;
+  cudaStream_t s = as_stream(stream);
+  if (p.dtype == SPMD_F32 || L % 8 || L > 1024 || (reinterpret_cast<uintptr_t>(p.data) & 15) ||
+      (reinterpret_cast<uintptr_t>(dp.data) & 15) || (reinterpret_cast<uintptr_t>(out.data) & 15)) {
+    const unsigned grid = grid_for(rows * 32, 256);
+    if (p.dtype == SPMD_F32)
+      softmax_bwd_rows_kernel<float><<<grid, 256, 0, s>>>((const float*)p.data,
+                                                          (const float*)dp.data,
+                                                          (float*)out.data, rows, L);
+    else
+      softmax_bwd_rows_kernel<bf16><<<grid, 256, 0, s>>>((const bf16*)p.data, (const bf16*)dp.data,
+                                                         (bf16*)out.data, rows, L);
+    return launched(s);
+  }
+  const unsigned grid = grid_for(rows * 32, 256);
+  const bf16 *a = (const bf16*)p.data, *b = (const bf16*)dp.data;
+  bf16* o = (bf16*)out.data;
+  if (L <= 256)
+    softmax_bwd_rows_bf16<1><<<grid, 256, 0, s>>>(a, b, o, rows, (int)L);
+  else if (L <= 512)
+    softmax_bwd_rows_bf16<2><<<grid, 256, 0, s>>>(a, b, o, rows, (int)L);
+  else
+    softmax_bwd_rows_bf16<4><<<grid, 256, 0, s>>>(a, b, o, rows, (int)L);
+  return launched(s);
+}
+
 extern "C" int spmd_softmax_lastdim(spmd_tensor in, spmd_tensor out, int64_t nparts,
                                     void* stream) {
   SPMD_CHECK_ARG(in.dtype == out.dtype && (in.dtype == SPMD_F32 || in.dtype == SPMD_BF16) &&

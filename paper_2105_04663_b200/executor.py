@@ -475,10 +475,85 @@ class Executor:
                 relu = by[users[ins.id][0]]
                 self._fused_skip.add(ins.id)
                 self._fused[relu.id] = ("dot_relu" if ins.opcode == Op.DOT else "conv_relu", ins)
+        self._plan_backward(users, outs, only_user, const_value)
         self._plan_halo_windows(users, outs)
         self._plan_halo_convs(users, outs)
         self._plan_attention(users, outs)
         self._plan_dot_reduce_scatter(users, outs)
+
+    def _plan_backward(self, users, outs, only_user, const_value):
+        """Training-step backward chains (workloads.transformer_train_step):
+
+        * softmax backward ``p * (dp - bcast(sum_t(dp * p)))`` -> one row
+          kernel (spmd_softmax_backward_lastdim), bf16/f32, full rows local;
+        * ReLU backward ``select(h > bcast(0), g, bcast(0))`` -> one
+          elementwise kernel (spmd_relu_backward).  When ``h`` is a bf16 DOT
+          whose other user is its forward RELU, the DOT takes the ReLU
+          epilogue and the mask reads ``relu(h) > 0`` (the same predicate,
+          NaN included) so ``h`` is never written.
+        SPMD_BWD_FUSION=0 disables both."""
+        import os
+        if os.environ.get("SPMD_BWD_FUSION", "1") == "0":
+            return
+        by = self.by_id
+
+        def zero_bcast(vid):
+            z = by.get(vid)
+            return z is not None and z.opcode == Op.BROADCAST and \
+                tuple(z.attrs["broadcast_dims"]) == () and const_value(z.operands[0]) == 0.0
+
+        taken = lambda vid: vid in self._fused or vid in self._fused_skip
+        for ins in self.graph.instructions:
+            if ins.opcode == Op.REDUCE and ins.attrs["kind"] == ReduceKind.SUM \
+                    and ins.shape.dtype in (DType.BF16, DType.F32) and not taken(ins.id):
+                pdp = by[ins.operands[0]]
+                rank = pdp.shape.rank
+                if pdp.opcode != Op.MULTIPLY or tuple(ins.attrs["dims"]) != (rank - 1,) \
+                        or const_value(ins.operands[1]) != 0.0 or not only_user(pdp.id, Op.REDUCE) \
+                        or not only_user(ins.id, Op.BROADCAST) or taken(pdp.id):
+                    continue
+                spb = by[users[ins.id][0]]
+                if tuple(spb.attrs["broadcast_dims"]) != tuple(range(rank - 1)) \
+                        or not only_user(spb.id, Op.SUBTRACT):
+                    continue
+                sub = by[users[spb.id][0]]
+                dp = sub.operands[0]
+                if sub.operands[1] != spb.id or dp not in pdp.operands \
+                        or not only_user(sub.id, Op.MULTIPLY):
+                    continue
+                p = pdp.operands[1] if pdp.operands[0] == dp else pdp.operands[0]
+                mul = by[users[sub.id][0]]
+                if sorted(mul.operands) != sorted((p, sub.id)) or p == dp or taken(mul.id) \
+                        or self._shape(p) != self._shape(dp):
+                    continue
+                self._fused_skip.update((pdp.id, ins.id, spb.id, sub.id))
+                self._fused[mul.id] = ("softmax_bwd", p, dp)
+            elif ins.opcode == Op.SELECT and not taken(ins.id):
+                pred, g, z = ins.operands
+                cmp = by[pred]
+                if cmp.opcode != Op.COMPARE or cmp.attrs["direction"].name != "GT" \
+                        or not only_user(pred, Op.SELECT) or not zero_bcast(z) \
+                        or not zero_bcast(cmp.operands[1]) or taken(pred):
+                    continue
+                h = by[cmp.operands[0]]
+                if h.shape.dtype not in (DType.BF16, DType.F32) or self._shape(g) != h.shape:
+                    continue
+                skip = {pred}
+                for zid in {z, cmp.operands[1]}:
+                    if zid not in outs and all(u in (pred, ins.id) for u in users[zid]):
+                        skip.add(zid)
+                src = h.id
+                hu = [by[u] for u in users.get(h.id, [])]
+                if h.opcode == Op.DOT and h.shape.dtype == DType.BF16 and h.id not in outs \
+                        and not taken(h.id) and len(hu) == 2 \
+                        and {u.opcode for u in hu} == {Op.RELU, Op.COMPARE}:
+                    relu = next(u for u in hu if u.opcode == Op.RELU)
+                    if not taken(relu.id):
+                        self._fused_skip.add(h.id)
+                        self._fused[relu.id] = ("dot_relu", h)
+                        src = relu.id
+                self._fused_skip.update(skip)
+                self._fused[ins.id] = ("relu_bwd", src, g)
 
     def _conv_tc_eligible(self, conv) -> bool:
         """The NHWC/HWIO bf16 shapes conv_tcgen05 takes (conv_tcgen05.cu)."""
@@ -861,6 +936,8 @@ class Executor:
             return ins.operands
         if f[0] == "softmax":
             return (f[1],)
+        if f[0] in ("softmax_bwd", "relu_bwd"):
+            return (f[1], f[2])
         if f[0] == "mask":
             return (f[1], f[2], f[3])
         if f[0] == "attention":
@@ -890,6 +967,17 @@ class Executor:
                 out = self._alloc(shp)
                 C.check(lib.spmd_softmax_lastdim(desc(env[x], xs), desc(out, shp), P, s),
                         "spmd_softmax_lastdim")
+                return out
+            return run
+        if f is not None and f[0] in ("softmax_bwd", "relu_bwd"):
+            _, a, b = f
+            ash, bsh = self._shape(a), self._shape(b)
+            fn = lib.spmd_softmax_backward_lastdim if f[0] == "softmax_bwd" \
+                else lib.spmd_relu_backward
+
+            def run(env, s):
+                out = self._alloc(shp)
+                C.check(fn(desc(env[a], ash), desc(env[b], bsh), desc(out, shp), P, s), f[0])
                 return out
             return run
         if f is not None and f[0] == "dot_relu":

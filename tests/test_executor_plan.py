@@ -177,3 +177,40 @@ def test_moe_all_to_alls_fuse(routed):
     else:
         assert [ex._fused[x][0] for x in a2a] == ["dot_a2a", "dot_a2a"]
     assert not any(s.coll for s in ex.steps if s.ins.id in a2a)
+
+
+@pytest.mark.parametrize("mesh", [(1, 1), (2, 2), (2, 4)])
+def test_training_step_backward_chains_fuse(mesh):
+    """Softmax backward (multiply/reduce/broadcast/subtract/multiply) and ReLU
+    backward (compare/select over broadcast zeros) each become one kernel;
+    the FFN-in GEMM takes the ReLU epilogue and the mask reads relu(h)."""
+    from paper_2105_04663_b200.workloads import transformer_train_step
+    g = transformer_train_step(mesh, dtype=DType.BF16, B=16, S=1024, M=8192, N=128, D=256,
+                               H=65536)
+    prog = partition(propagate(g)[0], mesh[0] * mesh[1], plan="fast")
+    ex = Executor(prog, nparts=1, device="cpu", comm=FakeComm(), partition_base=0, fuse=True,
+                  overlap=False)
+    by = ex.by_id
+    sb = [v for v in ex._fused.values() if v[0] == "softmax_bwd"]
+    rb = [v for v in ex._fused.values() if v[0] == "relu_bwd"]
+    assert len(sb) == 1 and len(rb) == 1
+    assert by[sb[0][1]].opcode == Op.DIVIDE          # probs
+    relu = by[rb[0][1]]
+    assert relu.opcode == Op.RELU and ex._fused[relu.id][0] == "dot_relu"
+    skipped = {by[i].opcode for i in ex._fused_skip}
+    assert {Op.COMPARE, Op.SUBTRACT, Op.REDUCE, Op.BROADCAST, Op.MULTIPLY} <= skipped
+    assert not any(s.ins.opcode in (Op.COMPARE, Op.SUBTRACT) for s in ex.steps)
+
+
+def test_backward_fusion_can_be_disabled():
+    ex, _ = _layer((2, 2))
+    from paper_2105_04663_b200.workloads import transformer_train_step
+    os.environ["SPMD_BWD_FUSION"] = "0"
+    try:
+        g = transformer_train_step((2, 2), dtype=DType.BF16, B=4, S=256, M=256, N=4, D=64, H=512)
+        prog = partition(propagate(g)[0], 4, plan="fast")
+        ex = Executor(prog, nparts=1, device="cpu", comm=FakeComm(), partition_base=0, fuse=True,
+                      overlap=False)
+    finally:
+        os.environ.pop("SPMD_BWD_FUSION")
+    assert not any(v[0] in ("softmax_bwd", "relu_bwd") for v in ex._fused.values())
