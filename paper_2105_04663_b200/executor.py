@@ -207,13 +207,6 @@ class Executor:
             prio = int(os.environ.get("SPMD_COMM_PRIORITY", "0"))
             self.comm_stream = torch.cuda.Stream(device=self.device, priority=prio)
             self.comm_streams = [self.comm_stream]
-            # Leave SMs for the collective kernels that run under the GEMMs
-            # (SPMD_COMM_SMS, default 0 = let the GEMM take every SM).
-            import os
-            reserve = int(os.environ.get("SPMD_COMM_SMS", "0"))
-            if reserve > 0:
-                sms = torch.cuda.get_device_properties(self.device).multi_processor_count
-                self.lib.spmd_set_sm_limit(max(2, sms - reserve))
         if comm is not None:
             comm.ensure_workspace(self._workspace_bytes(), self.device)
             peer = self._peer_bytes()
@@ -224,8 +217,29 @@ class Executor:
         self._peer_engine = self._plan_peer_engines()
         if self.comm_streams:
             self.steps = self._jit_prefetch(self.steps)
+        self._sm_limit = self._plan_sm_limit()
         self._assign_lanes()
         self._lane_of = {st.cuda_stream: k + 1 for k, st in enumerate(self.comm_streams)}
+
+    def _plan_sm_limit(self) -> int:
+        """GEMM/conv SM budget while this executor runs (0 = every SM).
+
+        The persistent tcgen05 GEMM holds every SM (one CTA with the whole
+        register file each), so a kernel queued on a comm lane -- the peer
+        barrier that brackets every copy-engine gather, or an NCCL kernel --
+        cannot start until the GEMM ends: a 256 MB pair gather under GEMMs
+        took 5.7 ms instead of 0.9 ms (profiles/r1_gather_under_gemm.jsonl).
+        With overlapped collectives the GEMM leaves SPMD_COMM_SMS SMs
+        (default 2) to them; costs the GEMM <= 1.4%."""
+        import os
+        if not self.comm_streams or self.comm is None or \
+                not any(st.coll for st in self.steps):
+            return 0
+        reserve = int(os.environ.get("SPMD_COMM_SMS", "2"))
+        if reserve <= 0:
+            return 0
+        sms = _torch().cuda.get_device_properties(self.device).multi_processor_count
+        return max(2, sms - reserve)
 
     def _jit_prefetch(self, steps: list) -> list:
         """Background prefetch gathers (peer engines 0/3) move from "as early
@@ -1479,6 +1493,7 @@ class Executor:
             raise EvalError(f"expected {len(self.params)} inputs, got {len(inputs)}")
         env = {"__inputs__": list(inputs)}
         keep = keep or set()
+        self.lib.spmd_set_sm_limit(self._sm_limit)   # process-wide; captured into graphs
         if self.comm_stream is None:
             for step in self.steps:
                 env[step.ins.id] = step.fn(env, s)
