@@ -175,10 +175,11 @@ int spmd_attention_layout(spmd_tensor q, spmd_tensor k, spmd_tensor v, spmd_tens
                           float scale, int out_bsnd, int64_t nparts, void* stream);
 /* Row softmax over the last dim: out = exp(x - max) / sum(exp(x - max)). */
 int spmd_softmax_lastdim(spmd_tensor in, spmd_tensor out, int64_t nparts, void* stream);
-/* Softmax backward over the last dim (bf16, rows <= 1024):
- * out = p * (dp - sum_last(dp * p)) -- the reference training graph's
- * multiply/reduce/broadcast/subtract/multiply chain (minispmd evaluator.py
- * elementwise + reduce ops) in one pass, fp32 row sum. */
+/* Softmax backward over the last dim (bf16 or f32; 16-byte vector path for
+ * bf16 rows of L % 8 == 0, L <= 1024): out = p * (dp - sum_last(dp * p)) --
+ * the training graph's multiply/reduce/broadcast/subtract/multiply chain
+ * (reference simulator.py:173-198 elementwise, :242-257 reduce) in one pass,
+ * fp32 row sum. */
 int spmd_softmax_backward_lastdim(spmd_tensor p, spmd_tensor dp, spmd_tensor out,
                                   int64_t nparts, void* stream);
 /* ReLU backward: out = h > 0 ? g : 0 (compare GT + select over broadcast
@@ -295,10 +296,23 @@ int spmd_moe_dispatch_all_to_all(spmd_comm* comm, spmd_tensor x, spmd_tensor exp
  * the calls of a channel in the same order.  `engine`: 0 = copy engines (no
  * SMs: for gathers hidden under GEMMs), 1 = SM pull kernel (16-byte NVLink
  * loads, whole GPU: for gathers on the critical path), 3 = SM pull with 32
- * CTAs (background, co-resident beside a persistent GEMM). */
+ * CTAs (background, co-resident beside a persistent GEMM), 4 = pre-staged:
+ * every member already staged its piece with spmd_peer_stage and passed a
+ * spmd_peer_barrier since, and none overwrites it before a later barrier --
+ * only the copy-engine pulls are issued (no kernel, so the gather never waits
+ * for SMs a persistent GEMM holds). */
 int spmd_peer_all_gather(spmd_comm* comm, spmd_tensor in, spmd_tensor out, int dim,
                          const int32_t* groups, int ngroups, int gsize, int64_t heap_offset,
                          int channel, int engine, void* stream);
+/* Stage `in` at heap data offset `heap_offset` (copy engine) for engine-4
+ * gathers: the executor stages every parameter (weight) gather of a step at
+ * the step start, then one barrier; another barrier at the step end keeps
+ * the slots stable until every member has pulled. */
+int spmd_peer_stage(spmd_comm* comm, spmd_tensor in, int64_t heap_offset, void* stream);
+/* Device-side barrier of all ranks on `channel` (epoch flags in the peer
+ * heap control page; graph-replay safe; times out into the device error
+ * word). */
+int spmd_peer_barrier(spmd_comm* comm, int channel, void* stream);
 
 #ifdef __cplusplus
 }

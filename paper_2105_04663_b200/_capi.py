@@ -120,6 +120,8 @@ _SIGNATURES = {
                              _P], _I),
     "spmd_moe_dispatch_all_to_all": ([_P, _T, _T, _T, _T, _PI32, _I, _I, _P], _I),
     "spmd_peer_all_gather": ([_P, _T, _T, _I, _PI32, _I, _I, _I64, _I, _I, _P], _I),
+    "spmd_peer_stage": ([_P, _T, _I64, _P], _I),
+    "spmd_peer_barrier": ([_P, _I, _P], _I),
 }
 
 _lib = None

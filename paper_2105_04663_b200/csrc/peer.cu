@@ -315,9 +315,12 @@ extern "C" int spmd_peer_all_gather(spmd_comm* c, spmd_tensor in, spmd_tensor ou
   int64_t outer = 1;
   for (int i = 0; i < dim; ++i) outer *= in.dims[i];
   const int64_t w = bytes / outer;   // one contiguous run of my piece
-  SPMD_CUDA_TRY(cudaMemcpyAsync(c->heap + CTRL_BYTES + heap_offset, in.data, bytes,
-                                cudaMemcpyDeviceToDevice, s));
-  if ((rc = peer_barrier(c, channel, s))) return rc;
+  const bool staged = engine == 4;   // pieces staged + barrier passed by the caller
+  if (!staged) {
+    SPMD_CUDA_TRY(cudaMemcpyAsync(c->heap + CTRL_BYTES + heap_offset, in.data, bytes,
+                                  cudaMemcpyDeviceToDevice, s));
+    if ((rc = peer_barrier(c, channel, s))) return rc;
+  }
   // engine 1: SM pull over the whole GPU (critical path); 3: background SM
   // pull, 32 CTAs that co-reside beside a persistent GEMM (like NCCL's)
   const bool sm = (engine == 1 || engine == 3) && gsize <= 8 && w % 16 == 0 &&
@@ -352,7 +355,31 @@ extern "C" int spmd_peer_all_gather(spmd_comm* c, spmd_tensor in, spmd_tensor ou
       SPMD_CUDA_TRY(cudaMemcpy2DAsync(dst, gsize * w, src, w, w, outer, cudaMemcpyDeviceToDevice,
                                       s));
   }
-  return peer_barrier(c, channel, s);
+  return staged ? SPMD_OK : peer_barrier(c, channel, s);
+}
+
+extern "C" int spmd_peer_stage(spmd_comm* c, spmd_tensor in, int64_t heap_offset, void* stream) {
+  SPMD_CHECK_ARG(c, "peer stage arguments");
+  if (!c->heap) {
+    set_error("peer heap not enabled (spmd_comm_enable_peer)");
+    return SPMD_ERR_INVALID;
+  }
+  const int64_t bytes = numel(in) * elem_size(in.dtype);
+  SPMD_CHECK_ARG(heap_offset >= 0 && heap_offset % 256 == 0 && heap_offset + bytes <= c->heap_bytes,
+                 "peer stage slot outside the heap");
+  if (bytes == 0) return SPMD_OK;
+  SPMD_CUDA_TRY(cudaMemcpyAsync(c->heap + CTRL_BYTES + heap_offset, in.data, bytes,
+                                cudaMemcpyDeviceToDevice, as_stream(stream)));
+  return SPMD_OK;
+}
+
+extern "C" int spmd_peer_barrier(spmd_comm* c, int channel, void* stream) {
+  SPMD_CHECK_ARG(c && channel >= 0 && channel < NUM_CHANNELS, "peer barrier channel");
+  if (!c->heap) {
+    set_error("peer heap not enabled (spmd_comm_enable_peer)");
+    return SPMD_ERR_INVALID;
+  }
+  return peer_barrier(c, channel, as_stream(stream));
 }
 
 // out = all-to-all(split_dim = 1, concat_dim = 0)(dot(lhs, rhs)) for a dot

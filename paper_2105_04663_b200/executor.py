@@ -215,11 +215,38 @@ class Executor:
         else:
             self._peer_ag = {}
         self._peer_engine = self._plan_peer_engines()
+        self._staged_exposed: list = []
+        self._staged = self._plan_staged_gathers()
         if self.comm_streams:
             self.steps = self._jit_prefetch(self.steps)
         self._sm_limit = self._plan_sm_limit()
         self._assign_lanes()
         self._lane_of = {st.cuda_stream: k + 1 for k, st in enumerate(self.comm_streams)}
+
+    def _plan_staged_gathers(self) -> dict:
+        """Peer all-gathers of parameters (the weight gathers, GSPMD's
+        2-D-finalized weight AG over X) -> pre-staged copy-engine pulls
+        (engine 4): every weight shard is staged into the peer heap at the
+        step start, one barrier follows, and each gather is then only
+        copy-engine reads of the members' slots -- no barrier kernel that
+        would wait for the SMs a persistent GEMM holds.  A barrier at the
+        step end keeps the slots until every member has pulled.
+        Returns {all-gather id: parameter index}.  SPMD_PEER_STAGE=0
+        disables it."""
+        import os
+        if not self.comm_streams or os.environ.get("SPMD_PEER_STAGE", "1") == "0":
+            return {}
+        pids = [p.id for p in self.params]
+        staged = {}
+        self._staged_exposed = []     # on the critical path: spread over both lanes
+        for aid in self._peer_ag:
+            src = self.by_id[self.by_id[aid].operands[0]]
+            if src.opcode == Op.PARAMETER and self._peer_engine.get(aid, -1) >= 0:
+                staged[aid] = pids.index(src.id)
+                if self._peer_engine[aid] not in (0, 3):
+                    self._staged_exposed.append(aid)
+                self._peer_engine[aid] = 4
+        return staged
 
     def _plan_sm_limit(self) -> int:
         """GEMM/conv SM budget while this executor runs (0 = every SM).
@@ -229,13 +256,15 @@ class Executor:
         barrier that brackets every copy-engine gather, or an NCCL kernel --
         cannot start until the GEMM ends: a 256 MB pair gather under GEMMs
         took 5.7 ms instead of 0.9 ms (profiles/r1_gather_under_gemm.jsonl).
-        With overlapped collectives the GEMM leaves SPMD_COMM_SMS SMs
-        (default 2) to them; costs the GEMM <= 1.4%."""
+        With overlapped collectives the GEMM leaves SPMD_COMM_SMS SMs to
+        them (default 2; 0 when the weight gathers are pre-staged and need
+        no kernel, since a reserved pair costs a GEMM whose tile count is a
+        multiple of 74 pairs up to one extra tile round)."""
         import os
         if not self.comm_streams or self.comm is None or \
                 not any(st.coll for st in self.steps):
             return 0
-        reserve = int(os.environ.get("SPMD_COMM_SMS", "2"))
+        reserve = int(os.environ.get("SPMD_COMM_SMS", "0" if self._staged else "2"))
         if reserve <= 0:
             return 0
         sms = _torch().cuda.get_device_properties(self.device).multi_processor_count
@@ -290,7 +319,10 @@ class Executor:
     def _assign_lanes(self) -> None:
         """Collectives on comm lanes.  Lane 1 carries only the background
         prefetch gathers (peer copy-engine / background SM-pull engines: a
-        GEMM hides them); everything on the critical path -- exposed peer
+        GEMM hides them) and the pre-staged weight gathers (copy-engine reads
+        only, in program order after the staging barrier, so the first one
+        overlaps the activation gather on lane 2); everything on the critical
+        path -- exposed peer
         gathers and every NCCL call (one stream, so NCCL's per-communicator
         order is the same on all ranks) -- takes lane 2 with its own barrier
         channel, so it never queues behind a prefetch.  At C2 N=4 the res1
@@ -311,7 +343,11 @@ class Executor:
             if mode == "2" and eng >= 0:
                 st.lane = 1 + nxt
                 nxt = (nxt + 1) % 2
-            elif mode == "critical" and eng not in (0, 3):
+            elif mode == "critical" and eng == 4 and st.ins.id in self._staged_exposed:
+                # exposed staged gathers (no barrier, so any lane): alternate,
+                # so e.g. the x and w_q gathers before the first GEMM overlap
+                st.lane = 2 - self._staged_exposed.index(st.ins.id) % 2
+            elif mode == "critical" and eng not in (0, 3, 4):
                 st.lane = 2
         if any(st.lane == 2 for st in self.steps):
             torch = _torch()
@@ -1515,11 +1551,28 @@ class Executor:
         streams = [compute] + self.comm_streams
         for st in self.comm_streams:
             st.wait_stream(compute)               # inputs / fork for graph capture
+        if self._staged:
+            # weight shards -> peer heap slots, then one barrier (lane 1)
+            st = self.comm_streams[0]
+            for aid, k in self._staged.items():
+                t = env["__inputs__"][k]
+                C.check(self.lib.spmd_peer_stage(self.comm.handle,
+                                                 desc(t, self._shape(self.by_id[aid].operands[0])),
+                                                 self._peer_ag[aid], st.cuda_stream), "peer_stage")
+                t.record_stream(st)
+            C.check(self.lib.spmd_peer_barrier(self.comm.handle, self._lane_of[st.cuda_stream],
+                                               st.cuda_stream), "peer_barrier")
+            staged_ev = torch.cuda.Event()
+            staged_ev.record(st)
+            staged_wait = {1}                     # lanes ordered after the staging
         lane_of: dict[str, int] = {}
         events: dict[str, object] = {}
         for step in self.steps:
             lane = step.lane if step.coll else 0
             stream = streams[lane]
+            if self._staged and step.ins.id in self._staged and lane not in staged_wait:
+                stream.wait_event(staged_ev)
+                staged_wait.add(lane)
             for o in tuple(step.ops) + tuple(step.after):
                 if o not in lane_of and o not in env:
                     continue
@@ -1551,6 +1604,11 @@ class Executor:
                     env.pop(vid, None)
         for st in self.comm_streams:
             compute.wait_stream(st)               # join
+        if self._staged:
+            # every member has pulled the staged slots before any restages
+            st = self.comm_streams[0]
+            C.check(self.lib.spmd_peer_barrier(self.comm.handle, self._lane_of[st.cuda_stream],
+                                               compute.cuda_stream), "peer_barrier")
 
     def timeline(self, inputs) -> list[dict]:
         """Eager run with CUDA events around every step on the stream it is
