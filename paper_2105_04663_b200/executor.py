@@ -216,6 +216,7 @@ class Executor:
             self._peer_ag = {}
         self._peer_engine = self._plan_peer_engines()
         self._staged_exposed: list = []
+        self._act_staged: set = set()
         self._staged = self._plan_staged_gathers()
         if self.comm_streams:
             self.steps = self._jit_prefetch(self.steps)
@@ -238,10 +239,22 @@ class Executor:
             return {}
         pids = [p.id for p in self.params]
         staged = {}
-        self._staged_exposed = []     # on the critical path: spread over both lanes
+        wide = os.environ.get("SPMD_PEER_STAGE_WIDE", "1") == "1"
+        # activation staging measured slower (profiles/r1_c2_n4_ab_stage_act.log)
+        act = os.environ.get("SPMD_PEER_STAGE_ACT", "0") == "1"
         for aid in self._peer_ag:
             src = self.by_id[self.by_id[aid].operands[0]]
-            if src.opcode == Op.PARAMETER and self._peer_engine.get(aid, -1) >= 0:
+            if src.opcode != Op.PARAMETER:
+                if act:
+                    # activation gathers: staged on the compute stream right
+                    # after the producer (copy + barrier while no GEMM runs),
+                    # then copy-engine pulls on the critical lane
+                    self._act_staged.add(aid)
+                    self._peer_engine[aid] = 4
+                continue
+            if wide and self._peer_engine.get(aid, -1) < 0:
+                self._peer_engine[aid] = 1        # exposed NCCL gather -> staged pulls too
+            if self._peer_engine.get(aid, -1) >= 0:
                 staged[aid] = pids.index(src.id)
                 if self._peer_engine[aid] not in (0, 3):
                     self._staged_exposed.append(aid)
@@ -343,6 +356,8 @@ class Executor:
             if mode == "2" and eng >= 0:
                 st.lane = 1 + nxt
                 nxt = (nxt + 1) % 2
+            elif mode == "critical" and st.ins.id in self._act_staged:
+                st.lane = 2
             elif mode == "critical" and eng == 4 and st.ins.id in self._staged_exposed:
                 # exposed staged gathers (no barrier, so any lane): alternate,
                 # so e.g. the x and w_q gathers before the first GEMM overlap
@@ -1483,6 +1498,22 @@ class Executor:
             if op == Op.ALL_GATHER and self._peer_engine.get(ins.id, -1) >= 0:
                 # one barrier channel per issuing stream
                 ch = self._lane_of.get(s, 0)
+                if ins.id in self._act_staged:
+                    # stage + barrier on the compute stream (issued in program
+                    # order right after the producer), pulls on this lane
+                    torch = _torch()
+                    cs = torch.cuda.current_stream(self.device)
+                    lane = torch.cuda.ExternalStream(s, device=self.device)
+                    ready = torch.cuda.Event()     # x may come from another lane
+                    ready.record(lane)
+                    cs.wait_event(ready)
+                    C.check(lib.spmd_peer_stage(comm.handle, x, self._peer_ag[ins.id],
+                                                cs.cuda_stream), "peer_stage")
+                    C.check(lib.spmd_peer_barrier(comm.handle, 0, cs.cuda_stream),
+                            "peer_barrier")
+                    ev = torch.cuda.Event()
+                    ev.record(cs)
+                    lane.wait_event(ev)
                 rc = lib.spmd_peer_all_gather(comm.handle, x, y, at["dim"], groups, ng, gs,
                                               self._peer_ag[ins.id], ch,
                                               self._peer_engine.get(ins.id, 1), s)
@@ -1604,7 +1635,7 @@ class Executor:
                     env.pop(vid, None)
         for st in self.comm_streams:
             compute.wait_stream(st)               # join
-        if self._staged:
+        if self._staged or self._act_staged:
             # every member has pulled the staged slots before any restages
             st = self.comm_streams[0]
             C.check(self.lib.spmd_peer_barrier(self.comm.handle, self._lane_of[st.cuda_stream],
