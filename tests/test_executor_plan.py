@@ -214,3 +214,37 @@ def test_backward_fusion_can_be_disabled():
     finally:
         os.environ.pop("SPMD_BWD_FUSION")
     assert not any(v[0] in ("softmax_bwd", "relu_bwd") for v in ex._fused.values())
+
+
+@pytest.mark.parametrize("mesh", [(2, 2), (1, 4), (2, 4)])
+def test_parameter_gathers_are_prestaged(mesh):
+    """Overlapped runs stage every parameter all-gather (weights, and the x
+    input) into the peer heap at the step start: engine 4 (copy-engine pulls
+    only).  Activation gathers keep their engine unless SPMD_PEER_STAGE_ACT."""
+    ex, _ = _layer(mesh)
+    ex.steps = ex._hoist_collectives(ex.steps)
+    ex.comm_stream = object()
+    ex.comm_streams = [ex.comm_stream]
+    ex._peer_engine = ex._plan_peer_engines()
+    ex._staged_exposed, ex._act_staged = [], set()
+    staged = ex._plan_staged_gathers()
+    pids = [p.id for p in ex.params]
+    for aid in ex._peer_ag:
+        src = ex.by_id[ex.by_id[aid].operands[0]]
+        if src.opcode == Op.PARAMETER:
+            assert staged[aid] == pids.index(src.id) and ex._peer_engine[aid] == 4
+        else:
+            assert aid not in staged and ex._peer_engine[aid] != 4
+    if mesh[0] > 1:          # weights gathered over the data axis
+        assert len(staged) >= 6
+    assert not ex._act_staged
+
+
+def test_prestaging_can_be_disabled():
+    os.environ["SPMD_PEER_STAGE"] = "0"
+    try:
+        ex, _ = _layer((2, 2))
+        ex.comm_streams = [object()]
+        assert ex._plan_staged_gathers() == {}
+    finally:
+        os.environ.pop("SPMD_PEER_STAGE")

@@ -78,7 +78,7 @@ def test_dot_reduce_scatter_rejects_bad_layouts(comm):
                                             ctypes.byref(_dd()), 0, garr, ng, gs, s), "rs")
 
 
-@pytest.mark.parametrize("engine", [0, 1])
+@pytest.mark.parametrize("engine", [0, 1, 3, 4])
 @pytest.mark.parametrize("dim", [0, 1])
 def test_peer_all_gather_world_of_one(comm, engine, dim):
     import torch
@@ -92,6 +92,9 @@ def test_peer_all_gather_world_of_one(comm, engine, dim):
     sh = Shape((48, 80), DType.F32)
     for ch in (0, 1):
         y.zero_()
+        if engine == 4:     # pre-staged: stage + barrier first (executor step start)
+            C.check(lib.spmd_peer_stage(comm.handle, desc(x, sh), 8 << 20, s), "stage")
+            C.check(lib.spmd_peer_barrier(comm.handle, ch, s), "barrier")
         C.check(lib.spmd_peer_all_gather(comm.handle, desc(x, sh), desc(y, sh), dim, garr, ng, gs,
                                          8 << 20, ch, engine, s), "peer_all_gather")
         torch.cuda.synchronize()
