@@ -261,6 +261,16 @@ class Executor:
                 self._peer_engine[aid] = 4
         return staged
 
+    def _stage_phases(self) -> list:
+        """Staging order: exposed gathers' shards, then the rest
+        (SPMD_STAGE_PHASES=1: one phase)."""
+        import os
+        if os.environ.get("SPMD_STAGE_PHASES", "2") == "1":
+            return [list(self._staged)]
+        first = [a for a in self._staged if a in self._staged_exposed]
+        rest = [a for a in self._staged if a not in self._staged_exposed]
+        return [p for p in (first, rest) if p]
+
     def _plan_sm_limit(self) -> int:
         """GEMM/conv SM budget while this executor runs (0 = every SM).
 
@@ -359,9 +369,11 @@ class Executor:
             elif mode == "critical" and st.ins.id in self._act_staged:
                 st.lane = 2
             elif mode == "critical" and eng == 4 and st.ins.id in self._staged_exposed:
-                # exposed staged gathers (no barrier, so any lane): alternate,
-                # so e.g. the x and w_q gathers before the first GEMM overlap
-                st.lane = 2 - self._staged_exposed.index(st.ins.id) % 2
+                # exposed staged gathers: lane 2, which waits only for the
+                # first staging phase (SPMD_STAGE_PHASES=1: alternate lanes,
+                # so e.g. the x and w_q pulls overlap)
+                st.lane = 2 if os.environ.get("SPMD_STAGE_PHASES", "2") != "1" else \
+                    2 - self._staged_exposed.index(st.ins.id) % 2
             elif mode == "critical" and eng not in (0, 3, 4):
                 st.lane = 2
         if any(st.lane == 2 for st in self.steps):
@@ -1582,28 +1594,35 @@ class Executor:
         streams = [compute] + self.comm_streams
         for st in self.comm_streams:
             st.wait_stream(compute)               # inputs / fork for graph capture
+        staged_ev: dict = {}
         if self._staged:
-            # weight shards -> peer heap slots, then one barrier (lane 1)
+            # parameter shards -> peer heap slots, each phase closed by one
+            # barrier on lane 1: the exposed gathers' shards first (their
+            # pulls start after a small copy), then the rest
             st = self.comm_streams[0]
-            for aid, k in self._staged.items():
-                t = env["__inputs__"][k]
-                C.check(self.lib.spmd_peer_stage(self.comm.handle,
-                                                 desc(t, self._shape(self.by_id[aid].operands[0])),
-                                                 self._peer_ag[aid], st.cuda_stream), "peer_stage")
-                t.record_stream(st)
-            C.check(self.lib.spmd_peer_barrier(self.comm.handle, self._lane_of[st.cuda_stream],
-                                               st.cuda_stream), "peer_barrier")
-            staged_ev = torch.cuda.Event()
-            staged_ev.record(st)
-            staged_wait = {1}                     # lanes ordered after the staging
+            for phase in self._stage_phases():
+                for aid in phase:
+                    t = env["__inputs__"][self._staged[aid]]
+                    C.check(self.lib.spmd_peer_stage(
+                        self.comm.handle, desc(t, self._shape(self.by_id[aid].operands[0])),
+                        self._peer_ag[aid], st.cuda_stream), "peer_stage")
+                    t.record_stream(st)
+                C.check(self.lib.spmd_peer_barrier(self.comm.handle,
+                                                   self._lane_of[st.cuda_stream],
+                                                   st.cuda_stream), "peer_barrier")
+                ev = torch.cuda.Event()
+                ev.record(st)
+                staged_ev.update({aid: ev for aid in phase})
+        staged_waited: set = set()                # (lane, event id) pairs issued
         lane_of: dict[str, int] = {}
         events: dict[str, object] = {}
         for step in self.steps:
             lane = step.lane if step.coll else 0
             stream = streams[lane]
-            if self._staged and step.ins.id in self._staged and lane not in staged_wait:
-                stream.wait_event(staged_ev)
-                staged_wait.add(lane)
+            ev = staged_ev.get(step.ins.id)
+            if ev is not None and lane != 1 and (lane, id(ev)) not in staged_waited:
+                stream.wait_event(ev)             # lane 1 is ordered after it already
+                staged_waited.add((lane, id(ev)))
             for o in tuple(step.ops) + tuple(step.after):
                 if o not in lane_of and o not in env:
                     continue
