@@ -21,6 +21,10 @@ struct spmd_comm {
   char* heap = nullptr;
   int64_t heap_bytes = 0;   // data bytes (excluding the control page)
   char* peer[SPMD_MAX_PARTS] = {nullptr};
+  // Fork streams/events for per-member parallel copy-engine pulls of
+  // pre-staged gathers, one set per barrier channel (created lazily).
+  cudaStream_t fork[4][SPMD_MAX_PARTS] = {};
+  cudaEvent_t fork_ev[4][SPMD_MAX_PARTS + 1] = {};
 };
 
 namespace spmd {

@@ -176,6 +176,12 @@ extern "C" int spmd_comm_init(spmd_comm** comm, int nranks, int rank, const void
 
 extern "C" int spmd_comm_destroy(spmd_comm* c) {
   if (!c) return SPMD_OK;
+  for (auto& row : c->fork)
+    for (auto& st : row)
+      if (st) cudaStreamDestroy(st);
+  for (auto& row : c->fork_ev)
+    for (auto& ev : row)
+      if (ev) cudaEventDestroy(ev);
   for (auto& kv : c->splits) ncclCommDestroy(kv.second);
   ncclCommDestroy(c->world);
   delete c;

@@ -171,6 +171,11 @@ static void close_peers(spmd_comm* c) {
   c->heap_bytes = 0;
 }
 
+static bool getenv_flag(const char* name) {
+  const char* e = getenv(name);
+  return e && *e && strcmp(e, "0") != 0;
+}
+
 static long long timeout_cycles() {
   static long long t = -1;
   if (t < 0) {
@@ -345,15 +350,37 @@ extern "C" int spmd_peer_all_gather(spmd_comm* c, spmd_tensor in, spmd_tensor ou
     if ((rc = launched(s))) return rc;
     return peer_barrier(c, channel, s);
   }
+  // Staged gathers of more than two members pull every member's piece on its
+  // own forked stream (event fork/join, graph-capturable), so the copy
+  // engines read the peers concurrently instead of one after another.
+  const bool fork = staged && gsize > 2 && !getenv_flag("SPMD_PEER_SERIAL_PULLS");
+  cudaEvent_t* fev = c->fork_ev[channel];
+  if (fork) {
+    for (int j = 0; j <= gsize; ++j)
+      if (!fev[j]) SPMD_CUDA_TRY(cudaEventCreateWithFlags(&fev[j], cudaEventDisableTiming));
+    for (int j = 0; j < gsize; ++j)
+      if (!c->fork[channel][j])
+        SPMD_CUDA_TRY(cudaStreamCreateWithFlags(&c->fork[channel][j], cudaStreamNonBlocking));
+    SPMD_CUDA_TRY(cudaEventRecord(fev[gsize], s));
+  }
   for (int j = 0; j < gsize; ++j) {
     const int q = groups[grp * gsize + j];
     const char* src = q == c->rank ? (const char*)in.data : c->peer[q] + CTRL_BYTES + heap_offset;
     char* dst = (char*)out.data + j * w;
+    cudaStream_t sj = s;
+    if (fork) {
+      sj = c->fork[channel][j];
+      SPMD_CUDA_TRY(cudaStreamWaitEvent(sj, fev[gsize], 0));
+    }
     if (outer == 1)
-      SPMD_CUDA_TRY(cudaMemcpyAsync(dst, src, w, cudaMemcpyDeviceToDevice, s));
+      SPMD_CUDA_TRY(cudaMemcpyAsync(dst, src, w, cudaMemcpyDeviceToDevice, sj));
     else
       SPMD_CUDA_TRY(cudaMemcpy2DAsync(dst, gsize * w, src, w, w, outer, cudaMemcpyDeviceToDevice,
-                                      s));
+                                      sj));
+    if (fork) {
+      SPMD_CUDA_TRY(cudaEventRecord(fev[j], sj));
+      SPMD_CUDA_TRY(cudaStreamWaitEvent(s, fev[j], 0));
+    }
   }
   return staged ? SPMD_OK : peer_barrier(c, channel, s);
 }
