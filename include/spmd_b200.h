@@ -309,6 +309,15 @@ int spmd_peer_all_gather(spmd_comm* comm, spmd_tensor in, spmd_tensor out, int d
  * the step start, then one barrier; another barrier at the step end keeps
  * the slots stable until every member has pulled. */
 int spmd_peer_stage(spmd_comm* comm, spmd_tensor in, int64_t heap_offset, void* stream);
+/* Collective-permute through the peer heap (reference simulator.py:372-390;
+ * non-targets zero-filled): the sender's copy engine writes `in` into the
+ * target's heap slot at `heap_offset` (uniform layout, caller assigned),
+ * barrier on `channel`, the receiver copies its slot to `out`.  Callers keep
+ * the slot live until a later barrier (the executor closes each step with
+ * one). */
+int spmd_peer_collective_permute(spmd_comm* comm, spmd_tensor in, spmd_tensor out,
+                                 const int32_t* pairs, int npairs, int64_t heap_offset,
+                                 int channel, void* stream);
 /* Device-side barrier of all ranks on `channel` (epoch flags in the peer
  * heap control page; graph-replay safe; times out into the device error
  * word). */

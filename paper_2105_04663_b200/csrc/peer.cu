@@ -580,3 +580,46 @@ extern "C" int spmd_moe_dispatch_all_to_all(spmd_comm* c, spmd_tensor x, spmd_te
       (const uint4*)(c->heap + CTRL_BYTES), (uint4*)out.data, (const uint32_t*)c->heap, n16);
   return launched(s);
 }
+
+// Collective-permute through the peer heap (reference simulator.py:372-390:
+// each target receives its source's buffer, non-targets are zero-filled):
+// the sender's copy engine writes `in` straight into the target's heap slot
+// at `heap_offset`, one barrier, then the receiver copies the slot out.
+// Latency ~ two copy-engine launches + one barrier instead of NCCL's
+// send/recv protocol (the halo exchange of a conv layer is ~2 MB).
+extern "C" int spmd_peer_collective_permute(spmd_comm* c, spmd_tensor in, spmd_tensor out,
+                                            const int32_t* pairs, int npairs,
+                                            int64_t heap_offset, int channel, void* stream) {
+  SPMD_CHECK_ARG(c && in.dtype == out.dtype && numel(in) == numel(out), "permute mismatch");
+  SPMD_CHECK_ARG(channel >= 0 && channel < NUM_CHANNELS, "peer barrier channel");
+  if (!c->heap) {
+    set_error("peer heap not enabled (spmd_comm_enable_peer)");
+    return SPMD_ERR_INVALID;
+  }
+  int send_to = -1, recv_from = -1;
+  std::vector<int> src_seen(c->nranks, 0), dst_seen(c->nranks, 0);
+  for (int i = 0; i < npairs; ++i) {
+    const int a = pairs[2 * i], b = pairs[2 * i + 1];
+    if (a < 0 || b < 0 || a >= c->nranks || b >= c->nranks || src_seen[a]++ || dst_seen[b]++) {
+      set_error("collective-permute pairs must have distinct sources and distinct targets");
+      return SPMD_ERR_SUBGROUP;
+    }
+    if (a == c->rank) send_to = b;
+    if (b == c->rank) recv_from = a;
+  }
+  const int64_t bytes = numel(in) * elem_size(in.dtype);
+  SPMD_CHECK_ARG(heap_offset >= 0 && heap_offset % 256 == 0 && heap_offset + bytes <= c->heap_bytes,
+                 "peer permute slot outside the heap");
+  cudaStream_t s = as_stream(stream);
+  if (send_to >= 0)
+    SPMD_CUDA_TRY(cudaMemcpyAsync(c->peer[send_to] + CTRL_BYTES + heap_offset, in.data, bytes,
+                                  cudaMemcpyDeviceToDevice, s));
+  int rc = peer_barrier(c, channel, s);
+  if (rc) return rc;
+  if (recv_from < 0)
+    SPMD_CUDA_TRY(cudaMemsetAsync(out.data, 0, bytes, s));
+  else if (bytes)
+    SPMD_CUDA_TRY(cudaMemcpyAsync(out.data, c->heap + CTRL_BYTES + heap_offset, bytes,
+                                  cudaMemcpyDeviceToDevice, s));
+  return SPMD_OK;
+}

@@ -214,6 +214,7 @@ class Executor:
                 comm.ensure_peer(peer, self.device)
         else:
             self._peer_ag = {}
+            self._peer_cp = {}
         self._peer_engine = self._plan_peer_engines()
         self._staged_exposed: list = []
         self._act_staged: set = set()
@@ -411,6 +412,15 @@ class Executor:
                 if ins.opcode == Op.ALL_GATHER and ins.id not in self._fused_skip:
                     self._peer_ag[ins.id] = off
                     nb = self._shape(ins.operands[0]).num_elements * ins.shape.dtype.itemsize
+                    off += (nb + 4095) // 4096 * 4096
+        # collective-permutes (halo exchanges, pipeline shifts): one landing
+        # slot each, written by the source rank's copy engine
+        self._peer_cp = {}
+        if os.environ.get("SPMD_PEER_CP", "1") != "0":
+            for ins in self.graph.instructions:
+                if ins.opcode == Op.COLLECTIVE_PERMUTE and ins.id not in self._fused_skip:
+                    self._peer_cp[ins.id] = off
+                    nb = ins.shape.num_elements * ins.shape.dtype.itemsize
                     off += (nb + 4095) // 4096 * 4096
         return off
 
@@ -1493,6 +1503,10 @@ class Executor:
                     C.check(lib.spmd_local_collective_permute(desc(env[a], ash), desc(out, shp),
                                                               pairs, npairs, P, s),
                             "collective-permute")
+                elif ins.id in self._peer_cp:
+                    C.check(lib.spmd_peer_collective_permute(
+                        comm.handle, desc(env[a], ash), desc(out, shp), pairs, npairs,
+                        self._peer_cp[ins.id], self._lane_of.get(s, 0), s), "collective-permute")
                 else:
                     C.check(lib.spmd_collective_permute(comm.handle, desc(env[a], ash),
                                                         desc(out, shp), pairs, npairs, s),
@@ -1579,6 +1593,9 @@ class Executor:
                 for vid in step.frees:
                     if vid not in keep:
                         env.pop(vid, None)
+            if self._peer_cp:
+                # landing slots are read before any rank writes them again
+                C.check(self.lib.spmd_peer_barrier(self.comm.handle, 0, s), "peer_barrier")
         else:
             self._run_two_streams(env, keep)
         self.last_env = env if keep else None
@@ -1654,8 +1671,9 @@ class Executor:
                     env.pop(vid, None)
         for st in self.comm_streams:
             compute.wait_stream(st)               # join
-        if self._staged or self._act_staged:
-            # every member has pulled the staged slots before any restages
+        if self._staged or self._act_staged or self._peer_cp:
+            # every member has read the staged / landing slots before any
+            # rank writes them again
             st = self.comm_streams[0]
             C.check(self.lib.spmd_peer_barrier(self.comm.handle, self._lane_of[st.cuda_stream],
                                                compute.cuda_stream), "peer_barrier")

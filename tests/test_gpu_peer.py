@@ -164,3 +164,24 @@ def test_dot_reduce_scatter_rows_world_of_one(comm):
         torch.cuda.synchronize()
         C.check(lib.spmd_check_device_errors(s), "device")
         assert torch.equal(fused, plain)
+
+
+@pytest.mark.parametrize("pairs", [[(0, 0)], []])
+def test_peer_collective_permute_world_of_one(comm, pairs):
+    """Self pair: out == in through the heap slot; no pair: zero-filled."""
+    import torch
+    from paper_2105_04663_b200 import _capi as C
+    from paper_2105_04663_b200.executor import desc
+    from paper_2105_04663_b200.ir import DType, Shape
+    lib, s = C.lib(), torch.cuda.current_stream().cuda_stream
+    x = torch.randn((1, 3, 1000), device="cuda")
+    y = torch.full_like(x, 7.0)
+    sh = Shape((3, 1000), DType.F32)
+    flat = [v for p in pairs for v in p]
+    arr = (ctypes.c_int32 * max(1, len(flat)))(*flat)
+    for ch in (0, 2):
+        C.check(lib.spmd_peer_collective_permute(comm.handle, desc(x, sh), desc(y, sh), arr,
+                                                 len(pairs), 4 << 20, ch, s), "peer_cp")
+        torch.cuda.synchronize()
+        assert torch.equal(y, x if pairs else torch.zeros_like(x))
+    C.check(lib.spmd_check_device_errors(s), "device")
