@@ -318,6 +318,12 @@ int spmd_peer_stage(spmd_comm* comm, spmd_tensor in, int64_t heap_offset, void* 
 int spmd_peer_collective_permute(spmd_comm* comm, spmd_tensor in, spmd_tensor out,
                                  const int32_t* pairs, int npairs, int64_t heap_offset,
                                  int channel, void* stream);
+/* Same, the sent buffer being the slice [start, start + out.dims[axis]) of
+ * `src` along `axis`, every other dim whole (a halo slab): one 2-D
+ * copy-engine write from the producer's output, no slice kernel. */
+int spmd_peer_slice_collective_permute(spmd_comm* comm, spmd_tensor src, int axis, int64_t start,
+                                       spmd_tensor out, const int32_t* pairs, int npairs,
+                                       int64_t heap_offset, int channel, void* stream);
 /* Device-side barrier of all ranks on `channel` (epoch flags in the peer
  * heap control page; graph-replay safe; times out into the device error
  * word). */

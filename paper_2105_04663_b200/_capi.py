@@ -123,6 +123,7 @@ _SIGNATURES = {
     "spmd_peer_stage": ([_P, _T, _I64, _P], _I),
     "spmd_peer_barrier": ([_P, _I, _P], _I),
     "spmd_peer_collective_permute": ([_P, _T, _T, _PI32, _I, _I64, _I, _P], _I),
+    "spmd_peer_slice_collective_permute": ([_P, _T, _I, _I64, _T, _PI32, _I, _I64, _I, _P], _I),
 }
 
 _lib = None

@@ -587,10 +587,45 @@ extern "C" int spmd_moe_dispatch_all_to_all(spmd_comm* c, spmd_tensor x, spmd_te
 // at `heap_offset`, one barrier, then the receiver copies the slot out.
 // Latency ~ two copy-engine launches + one barrier instead of NCCL's
 // send/recv protocol (the halo exchange of a conv layer is ~2 MB).
+static int peer_permute(spmd_comm* c, const char* src, int64_t rows, int64_t width,
+                        int64_t pitch, spmd_tensor out, const int32_t* pairs, int npairs,
+                        int64_t heap_offset, int channel, cudaStream_t s);
+
 extern "C" int spmd_peer_collective_permute(spmd_comm* c, spmd_tensor in, spmd_tensor out,
                                             const int32_t* pairs, int npairs,
                                             int64_t heap_offset, int channel, void* stream) {
   SPMD_CHECK_ARG(c && in.dtype == out.dtype && numel(in) == numel(out), "permute mismatch");
+  const int64_t bytes = numel(in) * elem_size(in.dtype);
+  return peer_permute(c, (const char*)in.data, 1, bytes, bytes, out, pairs, npairs, heap_offset,
+                      channel, as_stream(stream));
+}
+
+// Same, the sent buffer being the slice [start, start + out.dims[axis]) of
+// `src` along `axis` with every other dim whole (the halo slab of a
+// spatially partitioned conv): one 2-D copy-engine write of the slab rows
+// straight from the producer's output, no slice kernel.
+extern "C" int spmd_peer_slice_collective_permute(spmd_comm* c, spmd_tensor src, int axis,
+                                                  int64_t start, spmd_tensor out,
+                                                  const int32_t* pairs, int npairs,
+                                                  int64_t heap_offset, int channel,
+                                                  void* stream) {
+  SPMD_CHECK_ARG(c && src.dtype == out.dtype && src.rank == out.rank && axis >= 0 &&
+                     axis < src.rank && start >= 0 && start + out.dims[axis] <= src.dims[axis],
+                 "slice permute mismatch");
+  int64_t outer = 1, inner = elem_size(src.dtype);
+  for (int d = 0; d < src.rank; ++d) {
+    if (d != axis) SPMD_CHECK_ARG(src.dims[d] == out.dims[d], "slice permute: only `axis` is sliced");
+    if (d < axis) outer *= src.dims[d];
+    if (d > axis) inner *= src.dims[d];
+  }
+  return peer_permute(c, (const char*)src.data + start * inner, outer, out.dims[axis] * inner,
+                      src.dims[axis] * inner, out, pairs, npairs, heap_offset, channel,
+                      as_stream(stream));
+}
+
+static int peer_permute(spmd_comm* c, const char* src, int64_t rows, int64_t width,
+                        int64_t pitch, spmd_tensor out, const int32_t* pairs, int npairs,
+                        int64_t heap_offset, int channel, cudaStream_t s) {
   SPMD_CHECK_ARG(channel >= 0 && channel < NUM_CHANNELS, "peer barrier channel");
   if (!c->heap) {
     set_error("peer heap not enabled (spmd_comm_enable_peer)");
@@ -607,13 +642,18 @@ extern "C" int spmd_peer_collective_permute(spmd_comm* c, spmd_tensor in, spmd_t
     if (a == c->rank) send_to = b;
     if (b == c->rank) recv_from = a;
   }
-  const int64_t bytes = numel(in) * elem_size(in.dtype);
+  const int64_t bytes = rows * width;
+  SPMD_CHECK_ARG(bytes == numel(out) * elem_size(out.dtype), "permute mismatch");
   SPMD_CHECK_ARG(heap_offset >= 0 && heap_offset % 256 == 0 && heap_offset + bytes <= c->heap_bytes,
                  "peer permute slot outside the heap");
-  cudaStream_t s = as_stream(stream);
-  if (send_to >= 0)
-    SPMD_CUDA_TRY(cudaMemcpyAsync(c->peer[send_to] + CTRL_BYTES + heap_offset, in.data, bytes,
-                                  cudaMemcpyDeviceToDevice, s));
+  if (send_to >= 0 && bytes) {
+    char* dst = c->peer[send_to] + CTRL_BYTES + heap_offset;
+    if (rows == 1)
+      SPMD_CUDA_TRY(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, s));
+    else
+      SPMD_CUDA_TRY(cudaMemcpy2DAsync(dst, width, src, pitch, width, rows,
+                                      cudaMemcpyDeviceToDevice, s));
+  }
   int rc = peer_barrier(c, channel, s);
   if (rc) return rc;
   if (recv_from < 0)

@@ -567,6 +567,7 @@ class Executor:
         self._plan_halo_convs(users, outs)
         self._plan_attention(users, outs)
         self._plan_dot_reduce_scatter(users, outs)
+        self._plan_slice_permutes(users, outs)
 
     def _plan_backward(self, users, outs, only_user, const_value):
         """Training-step backward chains (workloads.transformer_train_step):
@@ -641,6 +642,32 @@ class Executor:
                         src = relu.id
                 self._fused_skip.update(skip)
                 self._fused[ins.id] = ("relu_bwd", src, g)
+
+    def _plan_slice_permutes(self, users, outs):
+        """Slice (one dim, stride 1) -> CollectivePermute, the slice's only
+        user: the halo slab of a spatially partitioned conv
+        (formatting.py:54-182 exchange_and_slice).  With a multi-process
+        communicator the peer permute writes the slab rows straight from the
+        sliced tensor (spmd_peer_slice_collective_permute)."""
+        import os
+        if self.comm is None or self.P != 1 or os.environ.get("SPMD_PEER_CP", "1") == "0":
+            return
+        by = self.by_id
+        for cp in self.graph.instructions:
+            if cp.opcode != Op.COLLECTIVE_PERMUTE or cp.id in self._fused:
+                continue
+            sl = by[cp.operands[0]]
+            if sl.opcode != Op.SLICE or sl.id in outs or users.get(sl.id) != [cp.id] \
+                    or sl.id in self._fused or sl.id in self._fused_skip:
+                continue
+            src = self._shape(sl.operands[0])
+            a = sl.attrs
+            cut = [d for d in range(src.rank)
+                   if (a["starts"][d], a["limits"][d]) != (0, src.dims[d])]
+            if len(cut) != 1 or any(x != 1 for x in a["strides"]):
+                continue
+            self._fused_skip.add(sl.id)
+            self._fused[cp.id] = ("slice_cp", sl, cp, cut[0])
 
     def _conv_tc_eligible(self, conv) -> bool:
         """The NHWC/HWIO bf16 shapes conv_tcgen05 takes (conv_tcgen05.cu)."""
@@ -1025,6 +1052,8 @@ class Executor:
             return (f[1],)
         if f[0] in ("softmax_bwd", "relu_bwd"):
             return (f[1], f[2])
+        if f[0] == "slice_cp":
+            return (f[1].operands[0],)
         if f[0] == "mask":
             return (f[1], f[2], f[3])
         if f[0] == "attention":
@@ -1054,6 +1083,22 @@ class Executor:
                 out = self._alloc(shp)
                 C.check(lib.spmd_softmax_lastdim(desc(env[x], xs), desc(out, shp), P, s),
                         "spmd_softmax_lastdim")
+                return out
+            return run
+        if f is not None and f[0] == "slice_cp":
+            _, sl, cp, axis = f
+            x, xsh = sl.operands[0], self._shape(sl.operands[0])
+            start = sl.attrs["starts"][axis]
+            pairs = (ctypes.c_int32 * max(1, 2 * len(cp.attrs["pairs"])))(
+                *[v for pr in cp.attrs["pairs"] for v in pr])
+            npairs = len(cp.attrs["pairs"])
+            comm = self.comm
+
+            def run(env, s):
+                out = self._alloc(shp)
+                C.check(lib.spmd_peer_slice_collective_permute(
+                    comm.handle, desc(env[x], xsh), axis, start, desc(out, shp), pairs, npairs,
+                    self._peer_cp[cp.id], self._lane_of.get(s, 0), s), "collective-permute")
                 return out
             return run
         if f is not None and f[0] in ("softmax_bwd", "relu_bwd"):

@@ -248,3 +248,20 @@ def test_prestaging_can_be_disabled():
         assert ex._plan_staged_gathers() == {}
     finally:
         os.environ.pop("SPMD_PEER_STAGE")
+
+
+def test_halo_slab_slices_fuse_into_the_peer_permute():
+    """C4 over 4: every halo slab (slice of one dim -> collective-permute)
+    becomes one peer permute reading the slab rows from the conv output."""
+    from paper_2105_04663_b200.workloads import conv_stack
+    g, _ = conv_stack((4,), N=8, H=64, W=64, C=128, layers=2, with_inputs=False)
+    prog = partition(propagate(g)[0], 4, plan="fast")
+    ex = Executor(prog, nparts=1, device="cpu", comm=FakeComm(), partition_base=0, fuse=True,
+                  overlap=False)
+    cps = [i for i in prog.graph.instructions if i.opcode == Op.COLLECTIVE_PERMUTE]
+    assert len(cps) == 4
+    for cp in cps:
+        kind, sl, cp2, axis = ex._fused[cp.id]
+        assert kind == "slice_cp" and cp2 is cp and axis == 1 and sl.id in ex._fused_skip
+        assert cp.id in ex._peer_cp
+    assert not any(s.ins.opcode == Op.SLICE for s in ex.steps)
