@@ -81,6 +81,20 @@ int64_t spmd_launch_count(void);
 /* Cap the SMs used by the persistent tensor-core kernels (0 = all), leaving
  * room for collective kernels that overlap them. */
 int spmd_set_sm_limit(int sms);
+/* Runtime tuning options, read at every launch (each starts from its SPMD_*
+ * environment variable): "gemm_mode" (1: 1-CTA, 2: 256x256 CTA pairs,
+ * 3: 256x512 wide pairs), "gemm_group", "gemm_raster_n", "gemm_hint",
+ * "gemm_store_hint", "gemm_epi_direct", "scatter_epi_direct", "attn_mode",
+ * "attn_kt", "conv_mode", "conv_wres", "conv_taps", "nccl_max_ctas",
+ * "peer_timeout_ms", "peer_serial_pulls".  Unknown names -> SPMD_ERR_INVALID.
+ * Not part of the reference interface (tuning and variant selection). */
+int spmd_set_option(const char* name, int64_t value);
+int spmd_get_option(const char* name, int64_t* value);
+/* C[M,N] = A[M,K] . B[K,N] (+ReLU if relu), row-major bf16, A K-major and B
+ * MN-major: the tcgen05 GEMM alone, for micro-benchmarks (the Dot of
+ * simulator.py:258-275 without the dimension-number plumbing). */
+int spmd_gemm_bf16(const void* a, const void* b, void* c, int64_t M, int64_t N, int64_t K,
+                   int relu, void* stream);
 
 /* ---- sources (simulator.py:161-172) ---------------------------------------- */
 int spmd_iota(spmd_tensor out, int axis, int64_t nparts, void* stream);
@@ -262,12 +276,23 @@ int spmd_collective_permute(spmd_comm* comm, spmd_tensor in, spmd_tensor out,
  * Growing re-exchanges (all ranks must call with the same size). */
 int spmd_comm_enable_peer(spmd_comm* comm, int64_t bytes, void* stream);
 int64_t spmd_comm_peer_bytes(spmd_comm* comm);
+/* Reserve the fused-op landing zone [0, 3H) of the heap (grows only; H is
+ * rounded up to 4 KiB).  H must be >= the per-parity bytes of every fused op
+ * below (gsize * numel(out) * 2 for a dot -> reduce-scatter, numel(out) * 2
+ * for the all-to-all ones).  Parity p of an op with unit (slot / row) u
+ * starts at unit p * ceil(H / u): both parities of ANY two ops are disjoint,
+ * so back-to-back fused ops of different sizes never overwrite a buffer a
+ * peer is still reducing.  All ranks reserve the same H, before enable_peer
+ * sizes the heap to >= 3H + the staging slots (offsets >= 3H). */
+int spmd_comm_reserve_fused(spmd_comm* comm, int64_t half_bytes);
+int64_t spmd_comm_fused_half(spmd_comm* comm);
 /* out = reduce-scatter(sum, dim)(dot(lhs, rhs)) in one tcgen05 GEMM whose
  * epilogue stores each output tile straight into the owning rank's heap
  * (replaces the Dot + ReduceScatter pair emitted by reference
  * partitioner.py:751-759 and executed by simulator.py:258-275, 360-371).
- * bf16; `dim` must be the last output dim and come from the rhs free dim;
- * needs a heap of >= 4 * gsize * numel(out) bytes.  SPMD_ERR_UNSUPPORTED
+ * bf16; `dim` must be the last output dim and come from the rhs free dim
+ * (or the leading row dim of a dot without batch dims); needs
+ * spmd_comm_reserve_fused(>= 2 * gsize * numel(out)).  SPMD_ERR_UNSUPPORTED
  * when the GEMM layout does not qualify (use spmd_dot + spmd_reduce_scatter). */
 int spmd_dot_reduce_scatter(spmd_comm* comm, spmd_tensor lhs, spmd_tensor rhs, spmd_tensor out,
                             const spmd_dot_dims* dims, int dim, const int32_t* groups,
@@ -276,7 +301,7 @@ int spmd_dot_reduce_scatter(spmd_comm* comm, spmd_tensor lhs, spmd_tensor rhs, s
  * batch dim (output dim 0): the expert FFN-out einsum + GShard combine
  * all-to-all (C3).  The GEMM epilogue stores each output row chunk into the
  * owning member's heap (slot pos * batch + b), then a barrier and one copy.
- * bf16; needs a heap of >= 4 * numel(out) bytes; SPMD_ERR_UNSUPPORTED when
+ * bf16; needs spmd_comm_reserve_fused(>= 2 * numel(out)); SPMD_ERR_UNSUPPORTED when
  * the layout does not qualify (spmd_dot + spmd_all_to_all then). */
 int spmd_dot_all_to_all(spmd_comm* comm, spmd_tensor lhs, spmd_tensor rhs, spmd_tensor out,
                         const spmd_dot_dims* dims, int split_dim, int concat_dim,
@@ -284,14 +309,15 @@ int spmd_dot_all_to_all(spmd_comm* comm, spmd_tensor lhs, spmd_tensor rhs, spmd_
 /* x [B,S,M] bf16 routed by expert/slot s32 [B,S] (spmd_moe_route) -> out
  * [B*G, E/G, C, M] = all-to-all(split 1, concat 0)(dispatch(x)): every row is
  * pushed straight into the owning member's heap (empty capacity slots as
- * zeros), barrier, one copy.  Needs a comm workspace of >= B*E*C*4 bytes. */
+ * zeros), barrier, one copy.  `index_scratch`: caller-owned s32 of >= B*E*C
+ * elements (the (batch, expert, slot) -> token table; stream-ordered with
+ * this call only).  Needs spmd_comm_reserve_fused(>= 2 * numel(out)). */
 int spmd_moe_dispatch_all_to_all(spmd_comm* comm, spmd_tensor x, spmd_tensor expert,
-                                 spmd_tensor slot, spmd_tensor out, const int32_t* groups,
-                                 int ngroups, int gsize, void* stream);
+                                 spmd_tensor slot, spmd_tensor out, spmd_tensor index_scratch,
+                                 const int32_t* groups, int ngroups, int gsize, void* stream);
 /* All-gather through the peer heap (reference simulator.py:353-359 piece
  * order): stage `in` at heap data offset `heap_offset` (256-aligned, caller
- * assigned, disjoint from the reduce-scatter region and from other live
- * all-gathers), barrier, pull every member's piece with copy-engine copies,
+ * assigned, >= 3 * fused_half and disjoint from other live all-gathers), barrier, pull every member's piece with copy-engine copies,
  * barrier.  `channel` (0..3): one per issuing stream -- all ranks must issue
  * the calls of a channel in the same order.  `engine`: 0 = copy engines (no
  * SMs: for gathers hidden under GEMMs), 1 = SM pull kernel (16-byte NVLink

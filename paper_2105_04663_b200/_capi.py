@@ -62,6 +62,8 @@ _SIGNATURES = {
     "spmd_check_device_errors": ([_P], _I),
     "spmd_launch_count": ([], _I64),
     "spmd_set_sm_limit": ([_I], _I),
+    "spmd_set_option": ([ctypes.c_char_p, _I64], _I),
+    "spmd_get_option": ([ctypes.c_char_p, _PI64], _I),
     "spmd_iota": ([_T, _I, _I64, _P], _I),
     "spmd_partition_id": ([_T, _I64, ctypes.c_int32, _P], _I),
     "spmd_constant": ([_T, _T, _I64, _P], _I),
@@ -114,11 +116,13 @@ _SIGNATURES = {
     "spmd_collective_permute": ([_P, _T, _T, _PI32, _I, _P], _I),
     "spmd_comm_enable_peer": ([_P, _I64, _P], _I),
     "spmd_comm_peer_bytes": ([_P], _I64),
+    "spmd_comm_reserve_fused": ([_P, _I64], _I),
+    "spmd_comm_fused_half": ([_P], _I64),
     "spmd_dot_reduce_scatter": ([_P, _T, _T, _T, ctypes.POINTER(SpmdDotDims), _I, _PI32, _I, _I,
                                  _P], _I),
     "spmd_dot_all_to_all": ([_P, _T, _T, _T, ctypes.POINTER(SpmdDotDims), _I, _I, _PI32, _I, _I,
                              _P], _I),
-    "spmd_moe_dispatch_all_to_all": ([_P, _T, _T, _T, _T, _PI32, _I, _I, _P], _I),
+    "spmd_moe_dispatch_all_to_all": ([_P, _T, _T, _T, _T, _T, _PI32, _I, _I, _P], _I),
     "spmd_peer_all_gather": ([_P, _T, _T, _I, _PI32, _I, _I, _I64, _I, _I, _P], _I),
     "spmd_peer_stage": ([_P, _T, _I64, _P], _I),
     "spmd_peer_barrier": ([_P, _I, _P], _I),
@@ -175,6 +179,34 @@ def check(status: int, fn: str = "spmd") -> None:
     if status in (ERR_INVALID, ERR_SHAPE, ERR_UNSUPPORTED):
         raise ex.EvalError(f"{fn}: {msg}")
     raise SpmdError(status, fn, msg)
+
+
+def set_option(name: str, value: int) -> None:
+    """spmd_set_option: switch a kernel variant / tuning knob at run time."""
+    check(lib().spmd_set_option(name.encode(), int(value)), "spmd_set_option")
+
+
+def get_option(name: str) -> int:
+    v = ctypes.c_int64()
+    check(lib().spmd_get_option(name.encode(), ctypes.byref(v)), "spmd_get_option")
+    return v.value
+
+
+class option:
+    """Context manager: ``with option("gemm_mode", 2): ...`` restores the
+    previous value on exit."""
+
+    def __init__(self, name: str, value: int):
+        self.name, self.value = name, value
+
+    def __enter__(self):
+        self.old = get_option(self.name)
+        set_option(self.name, self.value)
+        return self
+
+    def __exit__(self, *exc):
+        set_option(self.name, self.old)
+        return False
 
 
 def i32_array(vals: Sequence[int]):

@@ -578,12 +578,8 @@ template <int D>
 static int launch_attention(const CUtensorMap& mq, const CUtensorMap& mk, const CUtensorMap& mv,
                             const CUtensorMap& mo, AttnShape g, cudaStream_t s) {
   typedef AttnSmem<D> L;
-  static bool configured = false;
-  if (!configured) {
-    SPMD_CUDA_TRY(cudaFuncSetAttribute(attention_tcgen05<D>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, L::TOTAL));
-    configured = true;
-  }
+  static std::atomic<uint64_t> attr_done{0};
+  if (int rc = set_smem_attr((const void*)attention_tcgen05<D>, L::TOTAL, &attr_done)) return rc;
   const int64_t grid = (int64_t)((g.S + 127) / 128) * g.N * g.Bp;
   attention_tcgen05<D><<<(unsigned)grid, 256, L::TOTAL, s>>>(mq, mk, mv, mo, g);
   return launched(s);
@@ -856,12 +852,8 @@ static int launch_attention_2sm_k128(const CUtensorMap& mq, const CUtensorMap& m
                                      cudaStream_t s) {
   typedef Attn2SmemK128<D> L;
   static_assert(L::TOTAL <= 232448, "attention k128 smem");
-  static bool configured = false;
-  if (!configured) {
-    SPMD_CUDA_TRY(cudaFuncSetAttribute(attention_tcgen05_2sm_k128<D>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, L::TOTAL));
-    configured = true;
-  }
+  static std::atomic<uint64_t> attr_done{0};
+  if (int rc = set_smem_attr((const void*)attention_tcgen05_2sm_k128<D>, L::TOTAL, &attr_done)) return rc;
   const int64_t grid = 2 * (int64_t)((g.S + 255) / 256) * g.N * g.Bp;
   attention_tcgen05_2sm_k128<D><<<(unsigned)grid, 256, L::TOTAL, s>>>(mq, mk, mv, mo, g);
   return launched(s);
@@ -872,12 +864,8 @@ static int launch_attention_2sm(const CUtensorMap& mq, const CUtensorMap& mk,
                                 const CUtensorMap& mv, const CUtensorMap& mo, AttnShape g,
                                 cudaStream_t s) {
   typedef Attn2Smem<D> L;
-  static bool configured = false;
-  if (!configured) {
-    SPMD_CUDA_TRY(cudaFuncSetAttribute(attention_tcgen05_2sm<D>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, L::TOTAL));
-    configured = true;
-  }
+  static std::atomic<uint64_t> attr_done{0};
+  if (int rc = set_smem_attr((const void*)attention_tcgen05_2sm<D>, L::TOTAL, &attr_done)) return rc;
   const int64_t grid = 2 * (int64_t)((g.S + 255) / 256) * g.N * g.Bp;
   attention_tcgen05_2sm<D><<<(unsigned)grid, 256, L::TOTAL, s>>>(mq, mk, mv, mo, g);
   return launched(s);
@@ -917,18 +905,10 @@ extern "C" int spmd_attention_layout(spmd_tensor q, spmd_tensor k, spmd_tensor v
   g.Bp = (int)Bp;
   g.scale_log2e = scale * 1.4426950408889634f;
   cudaStream_t s = as_stream(stream);
-  static int mode = -1;
-  if (mode < 0) {
-    const char* e = getenv("SPMD_ATTN_MODE");
-    mode = (e && strcmp(e, "1sm") == 0) ? 1 : 2;
-  }
+  const int mode = option(OPT_ATTN_MODE) == 1 ? 1 : 2;
   // key tile: 128 for D=128 (549 vs 469 TF/s at T=1024), 64 for D=256 (equal at
   // T=1024, 993 vs 955 TF/s at T=4096: 3 K/V stages fit) -- profiles/r1_attention_kt.jsonl
-  static int kt_env = -2;
-  if (kt_env == -2) {
-    const char* e = getenv("SPMD_ATTN_KT");
-    kt_env = e ? atoi(e) : -1;
-  }
+  const int kt_env = (int)option(OPT_ATTN_KT);
   const int kt = kt_env > 0 ? kt_env : (D == 128 ? 128 : 64);
   if (mode == 2 && D >= 128 && kt == 128) {
     // 128-key tiles: K boxes of 64 rows (mk), V boxes of 64 rows (mv)

@@ -4,6 +4,8 @@
 #include "common.cuh"
 
 #include <mutex>
+#include <stdlib.h>
+#include <string.h>
 
 namespace spmd {
 
@@ -47,9 +49,103 @@ int sm_budget() {
   return n < 2 ? 2 : (n & ~1);   // even: CTA pairs
 }
 
+struct OptDef {
+  const char* name;
+  const char* env;
+  int64_t def;
+};
+static const OptDef kOpts[OPT_COUNT] = {
+    {"gemm_mode", "SPMD_GEMM_MODE", 3},
+    {"gemm_group", "SPMD_GEMM_GROUP", 0},
+    {"gemm_raster_n", "SPMD_GEMM_RASTER", 0},
+    {"gemm_hint", "SPMD_GEMM_HINT", 0},
+    {"gemm_store_hint", "SPMD_GEMM_STORE_HINT", 0},
+    {"gemm_epi_direct", "SPMD_GEMM_EPI", 0},
+    {"scatter_epi_direct", "SPMD_SCATTER_EPI", 0},
+    {"attn_mode", "SPMD_ATTN_MODE", 2},
+    {"attn_kt", "SPMD_ATTN_KT", 0},
+    {"conv_mode", "SPMD_CONV_MODE", 2},
+    {"conv_wres", "SPMD_CONV_WRES", 1},
+    {"conv_taps", "SPMD_CONV_TAPS", 1},
+    {"nccl_max_ctas", "SPMD_NCCL_MAX_CTAS", 0},
+    {"peer_timeout_ms", "SPMD_PEER_TIMEOUT_MS", 20000},
+    {"peer_serial_pulls", "SPMD_PEER_SERIAL_PULLS", 0},
+};
+static std::atomic<int64_t> g_opts[OPT_COUNT];
+static std::once_flag g_opts_once;
+
+// Environment spellings kept from the per-kernel getenv()s they replace.
+static int64_t parse_env(int id, const char* e) {
+  if (!strcmp(e, "1sm")) return 1;
+  if (!strcmp(e, "2sm")) return 2;
+  if (!strcmp(e, "wide")) return 3;
+  if (!strcmp(e, "direct")) return 1;
+  if (id == OPT_GEMM_RASTER_N) return !strcmp(e, "n") ? 1 : atoll(e);
+  if (id == OPT_GEMM_MODE || id == OPT_ATTN_MODE || id == OPT_CONV_MODE) {
+    const int64_t v = atoll(e);
+    return v > 0 ? v : kOpts[id].def;
+  }
+  return atoll(e);
+}
+
+static void init_options() {
+  std::call_once(g_opts_once, [] {
+    for (int i = 0; i < OPT_COUNT; ++i) {
+      const char* e = getenv(kOpts[i].env);
+      g_opts[i].store(e && *e ? parse_env(i, e) : kOpts[i].def);
+    }
+    // seconds spelling of the peer timeout
+    const char* t = getenv("SPMD_PEER_TIMEOUT_S");
+    if (t && *t && !getenv("SPMD_PEER_TIMEOUT_MS"))
+      g_opts[OPT_PEER_TIMEOUT_MS].store((int64_t)(atof(t) * 1000.0));
+  });
+}
+
+int64_t option(int id) {
+  init_options();
+  return (id >= 0 && id < OPT_COUNT) ? g_opts[id].load(std::memory_order_relaxed) : 0;
+}
+
+static int find_option(const char* name) {
+  for (int i = 0; name && i < OPT_COUNT; ++i)
+    if (!strcmp(kOpts[i].name, name)) return i;
+  return -1;
+}
+
+int set_smem_attr(const void* kernel, int bytes, std::atomic<uint64_t>* done_mask) {
+  int dev = 0;
+  SPMD_CUDA_TRY(cudaGetDevice(&dev));
+  const uint64_t bit = 1ull << (dev & 63);
+  if (done_mask->load() & bit) return SPMD_OK;
+  SPMD_CUDA_TRY(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  done_mask->fetch_or(bit);
+  return SPMD_OK;
+}
+
 }  // namespace spmd
 
 using namespace spmd;
+
+extern "C" int spmd_set_option(const char* name, int64_t value) {
+  init_options();
+  const int i = find_option(name);
+  if (i < 0) {
+    set_error(std::string("unknown option: ") + (name ? name : "(null)"));
+    return SPMD_ERR_INVALID;
+  }
+  g_opts[i].store(value);
+  return SPMD_OK;
+}
+
+extern "C" int spmd_get_option(const char* name, int64_t* value) {
+  const int i = find_option(name);
+  if (i < 0 || !value) {
+    set_error(std::string("unknown option: ") + (name ? name : "(null)"));
+    return SPMD_ERR_INVALID;
+  }
+  *value = option(i);
+  return SPMD_OK;
+}
 
 extern "C" int spmd_set_sm_limit(int sms) {
   g_sm_limit.store(sms > 0 ? sms : 0);

@@ -20,6 +20,12 @@ struct spmd_comm {
   // process (peer[rank] = heap).  See peer.cu.
   char* heap = nullptr;
   int64_t heap_bytes = 0;   // data bytes (excluding the control page)
+  // Fused-op landing zone: parity p of every fused dot -> reduce-scatter /
+  // all-to-all and of the MoE dispatch push starts at the first whole unit
+  // (slot or row) at or past p * fused_half, so the two parities of ANY two
+  // ops are disjoint ([0, half) vs [half, 3 * half)).  Staging / landing
+  // slots of the peer gathers and permutes live at offsets >= 3 * half.
+  int64_t fused_half = 0;
   char* peer[SPMD_MAX_PARTS] = {nullptr};
   // Fork streams/events for per-member parallel copy-engine pulls of
   // pre-staged gathers, one set per barrier channel (created lazily).

@@ -159,9 +159,9 @@ extern "C" int spmd_comm_init(spmd_comm** comm, int nranks, int rank, const void
   // Optional CTA cap so NCCL kernels fit beside persistent GEMMs
   // (SPMD_NCCL_MAX_CTAS; sub-communicators inherit the config).
   ncclConfig_t cfg = NCCL_CONFIG_INITIALIZER;
-  const char* mc = getenv("SPMD_NCCL_MAX_CTAS");
-  if (mc && atoi(mc) > 0) {
-    cfg.maxCTAs = atoi(mc);
+  const int max_ctas = (int)option(OPT_NCCL_MAX_CTAS);
+  if (max_ctas > 0) {
+    cfg.maxCTAs = max_ctas;
     cfg.minCTAs = cfg.maxCTAs < 4 ? cfg.maxCTAs : 4;
   }
   ncclResult_t r = ncclCommInitRankConfig(&c->world, nranks, id, rank, &cfg);

@@ -23,8 +23,36 @@ int* device_error_word();
 // leaves room for NCCL kernels to co-reside when collectives overlap GEMMs.
 int sm_budget();
 
+// Runtime tuning options (spmd_set_option / spmd_get_option).  Each starts
+// from its SPMD_* environment variable (read once, at first use) and is read
+// again at every launch, so a process can switch kernel variants (tests force
+// every GEMM path this way) without restarting.
+enum Option : int {
+  OPT_GEMM_MODE = 0,        // 1: 1-CTA tiles, 2: 256x256 CTA pairs, 3: 256x512 wide pairs
+  OPT_GEMM_GROUP,           // M-tiles per raster group (0: kernel default)
+  OPT_GEMM_RASTER_N,        // 1: raster along N inside a group
+  OPT_GEMM_HINT,            // L2 cache hint of the operand loads
+  OPT_GEMM_STORE_HINT,      // 1: evict-first output stores
+  OPT_GEMM_EPI_DIRECT,      // 1: st.global epilogue instead of TMA stores
+  OPT_SCATTER_EPI_DIRECT,   // 1: st.global peer stores in the reduce-scatter epilogue
+  OPT_ATTN_MODE,            // 1: 1-CTA attention, 2: CTA pairs
+  OPT_ATTN_KT,              // key tile (0: per head dim)
+  OPT_CONV_MODE,            // 1: 1-CTA conv, 2: CTA pairs
+  OPT_CONV_WRES,            // 1: weights resident in smem
+  OPT_CONV_TAPS,            // 1: one input box feeds the 3 kw taps
+  OPT_NCCL_MAX_CTAS,        // NCCL maxCTAs at communicator creation (0: NCCL default)
+  OPT_PEER_TIMEOUT_MS,      // peer barrier timeout
+  OPT_PEER_SERIAL_PULLS,    // 1: staged gathers pull members one after another
+  OPT_COUNT
+};
+int64_t option(int id);
+// cudaFuncAttributeMaxDynamicSharedMemorySize once per (kernel, device):
+// the attribute is per device, so a process driving two GPUs sets it twice.
+int set_smem_attr(const void* kernel, int bytes, std::atomic<uint64_t>* done_mask);
+
 // Reduce-scatter epilogue target of the tcgen05 GEMM (peer.cu): column chunk
-// j of the output goes to dst[j] (group position j's peer heap).
+// j of the output goes to dst[j] (group position j's peer heap), slot
+// parity * par_slots + pos.
 struct GemmScatter {
   int gsize, pos;
   void* dst[8];
@@ -34,6 +62,9 @@ struct GemmScatter {
   int rows;
   int64_t rchunk;
   int slot_base, nslots;
+  // Slots per parity buffer: parity p of the landing zone starts at slot
+  // p * par_slots (peer.cu fused_parity: a fixed byte stride for all ops).
+  int par_slots;
 };
 // Implemented in gemm_tcgen05.cu: returns SPMD_ERR_UNSUPPORTED when the
 // layout cannot be expressed with TMA descriptors (or, with `sc`, when the

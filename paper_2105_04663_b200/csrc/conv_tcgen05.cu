@@ -462,12 +462,8 @@ static int launch_conv_2sm(const CUtensorMap& mx, const CUtensorMap& mw, const C
                            cudaStream_t s) {
   typedef Conv2Smem<STAGES, WRES, TAPS> L;
   static_assert(L::TOTAL <= 232448, "conv 2-CTA smem");
-  static bool configured = false;
-  if (!configured) {
-    SPMD_CUDA_TRY(cudaFuncSetAttribute(conv_bf16_tcgen05_2sm<STAGES, WRES, TAPS>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, L::TOTAL));
-    configured = true;
-  }
+  static std::atomic<uint64_t> attr_done{0};
+  if (int rc = set_smem_attr((const void*)conv_bf16_tcgen05_2sm<STAGES, WRES, TAPS>, L::TOTAL, &attr_done)) return rc;
   const int sms = sm_budget();
   const int64_t clusters = g.tiles < sms / 2 ? g.tiles : sms / 2;
   conv_bf16_tcgen05_2sm<STAGES, WRES, TAPS><<<(unsigned)(2 * clusters), 256, L::TOTAL, s>>>(
@@ -475,26 +471,15 @@ static int launch_conv_2sm(const CUtensorMap& mx, const CUtensorMap& mw, const C
   return launched(s);
 }
 
-static int conv_mode() {
-  static int mode = -1;
-  if (mode < 0) {
-    const char* e = getenv("SPMD_CONV_MODE");
-    mode = (e && strcmp(e, "1sm") == 0) ? 1 : 2;
-  }
-  return mode;
-}
+static int conv_mode() { return option(OPT_CONV_MODE) == 1 ? 1 : 2; }
 
 template <int BN, int STAGES>
 static int launch_conv(const CUtensorMap& mx, const CUtensorMap& mw, const CUtensorMap& mo,
                        bf16* out, ConvShape g, const CUtensorMap& mx1, const CUtensorMap& mx2,
                        cudaStream_t s) {
   typedef ConvSmem<BN, STAGES> L;
-  static bool configured = false;
-  if (!configured) {
-    SPMD_CUDA_TRY(cudaFuncSetAttribute(conv_bf16_tcgen05<BN, STAGES>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, L::TOTAL));
-    configured = true;
-  }
+  static std::atomic<uint64_t> attr_done{0};
+  if (int rc = set_smem_attr((const void*)conv_bf16_tcgen05<BN, STAGES>, L::TOTAL, &attr_done)) return rc;
   const int sms = sm_budget();
   int64_t grid = g.tiles < sms ? g.tiles : sms;
   conv_bf16_tcgen05<BN, STAGES><<<(unsigned)grid, 256, L::TOTAL, s>>>(mx, mw, mo, out, g, mx1,
@@ -609,16 +594,7 @@ int conv_tcgen05(const spmd_tensor& lhs, const spmd_tensor& rhs, const spmd_tens
       g.nwb = (g.Wo + 2 * CBM - 1) / (2 * CBM);
       g.tiles = (int64_t)nparts * g.N * g.Ho * g.nwb * g.nt;
       // 3x3 x 128 input channels: weights resident in smem (one weight set)
-      static int wres = -1;
-      if (wres < 0) {
-        const char* e = getenv("SPMD_CONV_WRES");
-        wres = e ? atoi(e) : 1;
-      }
-      static int taps = -1;
-      if (taps < 0) {
-        const char* e = getenv("SPMD_CONV_TAPS");
-        taps = e ? atoi(e) : 1;
-      }
+      const int64_t wres = option(OPT_CONV_WRES), taps = option(OPT_CONV_TAPS);
       if (wres && taps && g.kblocks == 18 && g.KW == 3 && g.nt == 1 && nparts == 1) {
         if (encode_inputs(CBM + 2)) return launch_conv_2sm<3, 18, 3>(mx, mw2, mo, g, mx1, mx2, s);
         // restore the 128-pixel boxes the other kernels expect

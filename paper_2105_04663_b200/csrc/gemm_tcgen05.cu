@@ -45,7 +45,9 @@ struct GemmShape {
   // Reduce-scatter epilogue (peer.cu): output column chunk j (sc_chunk wide)
   // goes to group position j's peer heap, slot sc_pos, buffer parity
   // (epoch + 1) & 1 -- P2P stores over NVLink, tile by tile.
-  int scatter, sc_g, sc_pos;
+  // Parity p starts at slot p * sc_par (peer.cu: a fixed stride for every
+  // fused op, so consecutive ops of different sizes never overlap).
+  int scatter, sc_g, sc_pos, sc_par;
   int64_t sc_chunk, sc_slot;
   bf16* sc_dst[8];
   const uint32_t* sc_epoch;
@@ -415,7 +417,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
     uint64_t store_pol = 0;
     if (g.store_hint) asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(store_pol));
     const int par = g.scatter ? (int)((*(volatile const uint32_t*)g.sc_epoch + 1) & 1) : 0;
-    const int64_t par_off = (int64_t)par * g.sc_g * g.sc_slot;
+    const int64_t par_off = (int64_t)par * g.sc_par * g.sc_slot;
     int chunk = 0;
     int acc = 0;
     uint32_t acc_ph = 0;
@@ -440,7 +442,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
             const int j = (int)(col / g.sc_chunk);
             epi_store_chunk(&smaps.m[j], epi + (chunk++ & 1) * EPI_STAGE_BYTES, r, g.relu,
                             (int)(col - j * g.sc_chunk), m * BM2 + rank * HALF + ew * 32,
-                            par * g.sc_g + g.sc_pos, lane);
+                            par * g.sc_par + g.sc_pos, lane);
           }
         } else if (g.scatter) {
           if (row < g.M && col < g.N) {
@@ -678,12 +680,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
             const int j = (int)(row0 / g.sc_rchunk);
             epi_store_chunk(&smaps.m[j], epi + (chunk++ & 1) * EPI_STAGE_BYTES, r, g.relu, col,
                             (int)(row0 - j * g.sc_rchunk),
-                            par * g.sc_nslots + g.sc_slot_base + b, lane);
+                            par * g.sc_par + g.sc_slot_base + b, lane);
           }
         } else if (g.scatter) {
           const int j = (int)(col / g.sc_chunk);
           epi_store_chunk(&smaps.m[j], epi + (chunk++ & 1) * EPI_STAGE_BYTES, r, g.relu,
-                          (int)(col - j * g.sc_chunk), row0, par * g.sc_g + g.sc_pos, lane);
+                          (int)(col - j * g.sc_chunk), row0, par * g.sc_par + g.sc_pos, lane);
         } else {
           epi_store_chunk(&map_c, epi + (chunk++ & 1) * EPI_STAGE_BYTES, r, g.relu, col, row0,
                           b, lane, store_pol);
@@ -744,12 +746,8 @@ static int launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, const CUten
                        bf16* out, GemmShape g,
                        cudaStream_t s) {
   typedef Smem<BN, STAGES> L;
-  static bool configured = false;
-  if (!configured) {
-    SPMD_CUDA_TRY(cudaFuncSetAttribute(gemm_bf16_tcgen05<BN, STAGES>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, L::TOTAL));
-    configured = true;
-  }
+  static std::atomic<uint64_t> attr_done{0};
+  if (int rc = set_smem_attr((const void*)gemm_bf16_tcgen05<BN, STAGES>, L::TOTAL, &attr_done)) return rc;
   const int sms = sm_budget();
   int64_t grid = g.tiles < sms ? g.tiles : sms;
   gemm_bf16_tcgen05<BN, STAGES><<<(unsigned)grid, 256, L::TOTAL, s>>>(ma, mb, mc, out, g);
@@ -761,12 +759,8 @@ static int launch_gemm_2sm(const CUtensorMap& ma, const CUtensorMap& mb, const C
                            bf16* out, GemmShape g, const ScatterMaps& smaps,
                            cudaStream_t s) {
   typedef Smem2<STAGES> L;
-  static bool configured = false;
-  if (!configured) {
-    SPMD_CUDA_TRY(cudaFuncSetAttribute(gemm_bf16_tcgen05_2sm<STAGES>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, L::TOTAL));
-    configured = true;
-  }
+  static std::atomic<uint64_t> attr_done{0};
+  if (int rc = set_smem_attr((const void*)gemm_bf16_tcgen05_2sm<STAGES>, L::TOTAL, &attr_done)) return rc;
   const int sms = sm_budget();
   int64_t clusters = g.tiles < sms / 2 ? g.tiles : sms / 2;
   gemm_bf16_tcgen05_2sm<STAGES><<<(unsigned)(2 * clusters), 256, L::TOTAL, s>>>(ma, mb, mc, out,
@@ -780,12 +774,8 @@ static int launch_gemm_2sm_wide(const CUtensorMap& ma, const CUtensorMap& mb,
                                 cudaStream_t s) {
   typedef SmemW<STAGES> L;
   static_assert(L::TOTAL <= 232448, "wide GEMM smem");
-  static bool configured = false;
-  if (!configured) {
-    SPMD_CUDA_TRY(cudaFuncSetAttribute(gemm_bf16_tcgen05_2sm_wide<STAGES>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, L::TOTAL));
-    configured = true;
-  }
+  static std::atomic<uint64_t> attr_done{0};
+  if (int rc = set_smem_attr((const void*)gemm_bf16_tcgen05_2sm_wide<STAGES>, L::TOTAL, &attr_done)) return rc;
   const int sms = sm_budget();
   int64_t clusters = g.tiles < sms / 2 ? g.tiles : sms / 2;
   gemm_bf16_tcgen05_2sm_wide<STAGES><<<(unsigned)(2 * clusters), 384, L::TOTAL, s>>>(ma, mb, mc,
@@ -793,14 +783,7 @@ static int launch_gemm_2sm_wide(const CUtensorMap& ma, const CUtensorMap& mb,
   return launched(s);
 }
 
-static int gemm_mode() {
-  static int mode = -1;
-  if (mode < 0) {
-    const char* e = getenv("SPMD_GEMM_MODE");
-    mode = (e && strcmp(e, "1sm") == 0) ? 1 : (e && strcmp(e, "2sm") == 0) ? 2 : 3;
-  }
-  return mode;
-}
+static int gemm_mode() { return (int)option(OPT_GEMM_MODE); }
 
 int dot_tcgen05(const spmd_tensor& lhs, const spmd_tensor& rhs, const spmd_tensor& out,
                 const spmd_dot_dims& dd, int64_t nparts, cudaStream_t s, const GemmScatter* sc) {
@@ -864,27 +847,11 @@ int dot_tcgen05(const spmd_tensor& lhs, const spmd_tensor& rhs, const spmd_tenso
   g.a_mn = a_mn;
   g.b_mn = b_mn;
   g.relu = dd.epilogue == 1;
-  {
-    static int group = -1, raster = -1, hint = -1;
-    if (group < 0) {
-      const char* e = getenv("SPMD_GEMM_GROUP");
-      group = e ? atoi(e) : 0;   // 0: per-kernel default
-      if (group < 0) group = 0;
-      e = getenv("SPMD_GEMM_RASTER");
-      raster = (e && strcmp(e, "n") == 0) ? 1 : 0;
-      e = getenv("SPMD_GEMM_HINT");
-      hint = e ? atoi(e) : 0;
-    }
-    g.group = group ? group : 8;
-    g.raster_n = raster;
-    g.hint = hint;
-    static int store_hint = -1;
-    if (store_hint < 0) {
-      const char* e = getenv("SPMD_GEMM_STORE_HINT");
-      store_hint = e ? atoi(e) : 0;
-    }
-    g.store_hint = store_hint;
-  }
+  const int group_opt = (int)option(OPT_GEMM_GROUP);   // 0: per-kernel default
+  g.group = group_opt > 0 ? group_opt : 8;
+  g.raster_n = (int)option(OPT_GEMM_RASTER_N);
+  g.hint = (int)option(OPT_GEMM_HINT);
+  g.store_hint = (int)option(OPT_GEMM_STORE_HINT);
   // tensor-map batch dims: innermost first
   OperandView va, vb;
   for (int i = 0; i < 3; ++i) {
@@ -917,11 +884,7 @@ int dot_tcgen05(const spmd_tensor& lhs, const spmd_tensor& rhs, const spmd_tenso
   // Bulk-tensor store epilogue whenever the output rows are 16-byte aligned.
   {
     const int64_t nbat = (int64_t)g.nb[0] * g.nb[1] * g.nb[2];
-    static int direct = -1;
-    if (direct < 0) {
-      const char* e = getenv("SPMD_GEMM_EPI");
-      direct = (e && strcmp(e, "direct") == 0) ? 1 : 0;
-    }
+    const int direct = (int)option(OPT_GEMM_EPI_DIRECT);
     g.tma_store = !direct && (g.N % 8 == 0) &&
                   encode_store_map(&mc, out.data, g.N, g.M, g.N, nbat, g.out_batch_stride);
     if (!g.tma_store) memset(&mc, 0, sizeof(mc));
@@ -944,11 +907,12 @@ int dot_tcgen05(const spmd_tensor& lhs, const spmd_tensor& rhs, const spmd_tenso
     g.sc_rchunk = rchunk;
     g.sc_slot_base = sc->slot_base;
     g.sc_nslots = sc->nslots;
+    g.sc_par = sc->par_slots;
     g.sc_epoch = sc->epoch;
-    g.sc_tma = 1;
+    g.sc_tma = sc->par_slots >= sc->nslots;
     for (int j = 0; g.sc_tma && j < sc->gsize; ++j)
       g.sc_tma = encode_store_map(&smaps.m[j], sc->dst[j], N.size, rchunk, N.size,
-                                  2 * sc->nslots, rchunk * N.size);
+                                  sc->par_slots + sc->nslots, rchunk * N.size);
     if (!g.sc_tma) return SPMD_ERR_UNSUPPORTED;
   } else if (sc) {
     // Reduce-scatter epilogue: 2-CTA kernel, no batch dims, the scattered
@@ -963,17 +927,14 @@ int dot_tcgen05(const spmd_tensor& lhs, const spmd_tensor& rhs, const spmd_tenso
     g.sc_pos = sc->pos;
     g.sc_chunk = N.size / sc->gsize;
     g.sc_slot = M.size * g.sc_chunk;
+    if (sc->par_slots < sc->gsize) return SPMD_ERR_UNSUPPORTED;
+    g.sc_par = sc->par_slots;
     for (int j = 0; j < sc->gsize; ++j) g.sc_dst[j] = (bf16*)sc->dst[j];
     g.sc_epoch = sc->epoch;
-    static int direct = -1;
-    if (direct < 0) {
-      const char* e = getenv("SPMD_SCATTER_EPI");
-      direct = (e && strcmp(e, "direct") == 0) ? 1 : 0;
-    }
-    g.sc_tma = !direct;
+    g.sc_tma = !option(OPT_SCATTER_EPI_DIRECT);
     for (int j = 0; g.sc_tma && j < sc->gsize; ++j)
       g.sc_tma = encode_store_map(&smaps.m[j], sc->dst[j], g.sc_chunk, M.size, g.sc_chunk,
-                                  2 * sc->gsize, g.sc_slot);
+                                  sc->par_slots + sc->gsize, g.sc_slot);
   }
   if (gemm_mode() == 3 && (sc ? g.sc_tma : g.tma_store) && M.size >= 256 && N.size >= 512) {
     // wide pair tiles (256 x 512); the store epilogue is TMA-only
@@ -982,7 +943,7 @@ int dot_tcgen05(const spmd_tensor& lhs, const spmd_tensor& rhs, const spmd_tenso
     if (okw) {
       // 16 M-tiles per raster group (alternating A/B on the C2 GEMM shapes:
       // +5% over 8 for 256 x 512 tiles, profiles/r1_gemm_wide_group_sweep.log)
-      if (!getenv("SPMD_GEMM_GROUP")) g.group = 16;
+      if (group_opt <= 0) g.group = 16;
       g.mt = (g.M + BM2 - 1) / BM2;
       g.nt = (g.N + WBN - 1) / WBN;
       g.tiles = (int64_t)g.mt * g.nt * g.nb[0] * g.nb[1] * g.nb[2];

@@ -15,9 +15,14 @@
 //                 agree on the order of barriers within a channel): u32 epoch
 //                 at [256c]; u32 flag[q] at [256c + 64 + q] = last epoch that
 //                 rank q has completed (written remotely by q)
-//   data:         [0, R): 2 parity buffers x [gsize slots][rows][chunk] bf16
-//                 of the fused dot -> reduce-scatter (channel 0);
-//                 caller-assigned offsets: all-gather staging slots.
+//   data:         [0, 3H): the fused-op landing zone (H = fused_half,
+//                 spmd_comm_reserve_fused): parity p of an op whose unit
+//                 (slot / row) is u bytes starts at unit p * ceil(H / u), so
+//                 parity 0 of every op lies in [0, H) and parity 1 in
+//                 [H, 3H) -- consecutive fused ops of different sizes never
+//                 overlap across parities;
+//                 caller-assigned offsets >= 3H: all-gather staging slots,
+//                 collective-permute landing slots.
 // Epochs live in device memory, so the sequence is CUDA-graph replay safe:
 // the GEMM reads parity (epoch + 1) & 1, the barrier kernel increments the
 // epoch, publishes it to every rank and waits for every rank's flag.  Waiting
@@ -79,9 +84,10 @@ __global__ void peer_barrier_kernel(uint32_t* ctrl, PeerFlags pf, int nranks, in
 
 // out[i] = sum_j slot_j[i] (fp32 accumulation in group-position order).
 __global__ void peer_slot_reduce_kernel(const bf16* __restrict__ data, bf16* __restrict__ out,
-                                        const uint32_t* ctrl, int G, int64_t slot, int64_t nvec) {
+                                        const uint32_t* ctrl, int G, int64_t slot,
+                                        int64_t par_slots, int64_t nvec) {
   const int64_t par = (int64_t)(*(volatile const uint32_t*)ctrl & 1);
-  const bf16* base = data + par * G * slot;
+  const bf16* base = data + par * par_slots * slot;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nvec;
        i += (int64_t)gridDim.x * blockDim.x) {
     float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
@@ -154,9 +160,9 @@ __global__ void __launch_bounds__(512) peer_pull_kernel(PullArgs a, uint4* __res
 
 // out[i] = parity buffer (epoch & 1) of the all-to-all landing zone.
 __global__ void peer_parity_copy_kernel(const uint4* __restrict__ data, uint4* __restrict__ out,
-                                        const uint32_t* ctrl, int64_t n16) {
+                                        const uint32_t* ctrl, int64_t par16, int64_t n16) {
   const int64_t par = (int64_t)(*(volatile const uint32_t*)ctrl & 1);
-  const uint4* src = data + par * n16;
+  const uint4* src = data + par * par16;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n16;
        i += (int64_t)gridDim.x * blockDim.x)
     out[i] = __ldcs(src + i);
@@ -171,19 +177,29 @@ static void close_peers(spmd_comm* c) {
   c->heap_bytes = 0;
 }
 
-static bool getenv_flag(const char* name) {
-  const char* e = getenv(name);
-  return e && *e && strcmp(e, "0") != 0;
+// Units per parity of a fused op that lands `units` units of `unit_bytes`
+// per parity: ceil(H / unit).  Fails when the reserved region is too small.
+static int fused_parity(const spmd_comm* c, int64_t unit_bytes, int64_t units,
+                        int64_t* par_units) {
+  const int64_t h = c->fused_half;
+  if (h <= 0 || unit_bytes <= 0 || units * unit_bytes > h || 3 * h > c->heap_bytes) {
+    set_error("peer heap fused region too small for this op (spmd_comm_reserve_fused)");
+    return SPMD_ERR_INVALID;
+  }
+  *par_units = (h + unit_bytes - 1) / unit_bytes;
+  return SPMD_OK;
+}
+
+static int check_slot(const spmd_comm* c, int64_t off, int64_t bytes, const char* what) {
+  if (off < 3 * c->fused_half || off % 256 != 0 || off + bytes > c->heap_bytes) {
+    set_error(std::string(what) + ": slot outside the heap or inside the fused region");
+    return SPMD_ERR_INVALID;
+  }
+  return SPMD_OK;
 }
 
 static long long timeout_cycles() {
-  static long long t = -1;
-  if (t < 0) {
-    const char* e = getenv("SPMD_PEER_TIMEOUT_S");
-    const double sec = e ? atof(e) : 20.0;
-    t = (long long)(sec * 2.0e9);   // clock64 at <= 2 GHz
-  }
-  return t;
+  return (long long)option(OPT_PEER_TIMEOUT_MS) * 2000000LL;   // clock64 at <= 2 GHz
 }
 
 }  // namespace spmd
@@ -241,6 +257,15 @@ extern "C" int spmd_comm_enable_peer(spmd_comm* c, int64_t bytes, void* stream) 
 
 extern "C" int64_t spmd_comm_peer_bytes(spmd_comm* c) { return c ? c->heap_bytes : 0; }
 
+extern "C" int spmd_comm_reserve_fused(spmd_comm* c, int64_t half_bytes) {
+  SPMD_CHECK_ARG(c && half_bytes >= 0, "reserve_fused arguments");
+  half_bytes = (half_bytes + 4095) & ~(int64_t)4095;
+  if (half_bytes > c->fused_half) c->fused_half = half_bytes;
+  return SPMD_OK;
+}
+
+extern "C" int64_t spmd_comm_fused_half(spmd_comm* c) { return c ? c->fused_half : 0; }
+
 extern "C" int spmd_dot_reduce_scatter(spmd_comm* c, spmd_tensor lhs, spmd_tensor rhs,
                                        spmd_tensor out, const spmd_dot_dims* dd, int dim,
                                        const int32_t* groups, int ngroups, int gsize,
@@ -259,10 +284,8 @@ extern "C" int spmd_dot_reduce_scatter(spmd_comm* c, spmd_tensor lhs, spmd_tenso
   if (rc) return rc;
   SPMD_CHECK_ARG(gsize <= 8, "dot_reduce_scatter group size <= 8");
   const int64_t slot = numel(out);
-  if (2 * gsize * slot * 2 > c->heap_bytes) {
-    set_error("peer heap too small for this reduce-scatter");
-    return SPMD_ERR_INVALID;
-  }
+  int64_t par_slots = 0;
+  if ((rc = fused_parity(c, slot * 2, gsize, &par_slots))) return rc;
   SPMD_CHECK_ARG(slot % 8 == 0, "dot_reduce_scatter shard must be a multiple of 8 elements");
   cudaStream_t s = as_stream(stream);
   spmd_tensor full = out;
@@ -274,6 +297,7 @@ extern "C" int spmd_dot_reduce_scatter(spmd_comm* c, spmd_tensor lhs, spmd_tenso
   sc.pos = pos;
   for (int j = 0; j < gsize; ++j) sc.dst[j] = c->peer[groups[grp * gsize + j]] + CTRL_BYTES;
   sc.epoch = (const uint32_t*)c->heap;
+  sc.par_slots = (int)par_slots;
   if (dim == 0 && out.rank >= 2 && dim != out.rank - 1) {
     // split on the leading output dim = GEMM rows (no batch dims): member j
     // gets rows [j * R/G, (j+1) * R/G) into slot `pos` (wide kernel)
@@ -288,7 +312,7 @@ extern "C" int spmd_dot_reduce_scatter(spmd_comm* c, spmd_tensor lhs, spmd_tenso
   const int64_t nvec = slot / 8;
   peer_slot_reduce_kernel<<<grid_for(nvec, 256), 256, 0, s>>>(
       (const bf16*)(c->heap + CTRL_BYTES), (bf16*)out.data, (const uint32_t*)c->heap, gsize, slot,
-      nvec);
+      par_slots, nvec);
   return launched(s);
 }
 
@@ -313,8 +337,7 @@ extern "C" int spmd_peer_all_gather(spmd_comm* c, spmd_tensor in, spmd_tensor ou
   if (rc) return rc;
   const int64_t es = elem_size(in.dtype);
   const int64_t bytes = numel(in) * es;
-  SPMD_CHECK_ARG(heap_offset >= 0 && heap_offset % 256 == 0 && heap_offset + bytes <= c->heap_bytes,
-                 "peer all-gather staging slot outside the heap");
+  if ((rc = check_slot(c, heap_offset, bytes, "peer all-gather staging"))) return rc;
   if (bytes == 0) return SPMD_OK;
   cudaStream_t s = as_stream(stream);
   int64_t outer = 1;
@@ -353,7 +376,7 @@ extern "C" int spmd_peer_all_gather(spmd_comm* c, spmd_tensor in, spmd_tensor ou
   // Staged gathers of more than two members pull every member's piece on its
   // own forked stream (event fork/join, graph-capturable), so the copy
   // engines read the peers concurrently instead of one after another.
-  const bool fork = staged && gsize > 2 && !getenv_flag("SPMD_PEER_SERIAL_PULLS");
+  const bool fork = staged && gsize > 2 && !option(OPT_PEER_SERIAL_PULLS);
   cudaEvent_t* fev = c->fork_ev[channel];
   if (fork) {
     for (int j = 0; j <= gsize; ++j)
@@ -392,8 +415,7 @@ extern "C" int spmd_peer_stage(spmd_comm* c, spmd_tensor in, int64_t heap_offset
     return SPMD_ERR_INVALID;
   }
   const int64_t bytes = numel(in) * elem_size(in.dtype);
-  SPMD_CHECK_ARG(heap_offset >= 0 && heap_offset % 256 == 0 && heap_offset + bytes <= c->heap_bytes,
-                 "peer stage slot outside the heap");
+  if (int rc = check_slot(c, heap_offset, bytes, "peer stage")) return rc;
   if (bytes == 0) return SPMD_OK;
   SPMD_CUDA_TRY(cudaMemcpyAsync(c->heap + CTRL_BYTES + heap_offset, in.data, bytes,
                                 cudaMemcpyDeviceToDevice, as_stream(stream)));
@@ -441,16 +463,14 @@ extern "C" int spmd_dot_all_to_all(spmd_comm* c, spmd_tensor lhs, spmd_tensor rh
   full.dims[1] = out.dims[1] * gsize;
   full.data = nullptr;
   const int64_t n = numel(out);
-  if (2 * n * 2 > c->heap_bytes) {
-    set_error("peer heap too small for this all-to-all");
-    return SPMD_ERR_INVALID;
-  }
   SPMD_CHECK_ARG(n % 8 == 0, "dot_all_to_all size");
-  int64_t inner = 1;   // one output row = the last dim (GEMM N)
-  int64_t rows_per_batch = 1;
+  int64_t rows_per_batch = 1;   // GEMM rows of one batch (the flattened free dims)
   for (int d = 1; d < out.rank - 1; ++d) rows_per_batch *= full.dims[d];
-  inner = out.dims[out.rank - 1];
-  (void)inner;
+  SPMD_CHECK_ARG(rows_per_batch % gsize == 0, "dot_all_to_all split");
+  // one slot = one member's row chunk of one batch: n / out.dims[0] elements
+  const int64_t slot = n / out.dims[0];
+  int64_t par_slots = 0;
+  if ((rc = fused_parity(c, slot * 2, out.dims[0], &par_slots))) return rc;
   GemmScatter sc;
   memset(&sc, 0, sizeof(sc));
   sc.gsize = gsize;
@@ -461,13 +481,15 @@ extern "C" int spmd_dot_all_to_all(spmd_comm* c, spmd_tensor lhs, spmd_tensor rh
   sc.rchunk = rows_per_batch / gsize;
   sc.slot_base = pos * (int)full.dims[0];
   sc.nslots = (int)out.dims[0];
+  sc.par_slots = (int)par_slots;
   cudaStream_t s = as_stream(stream);
   rc = dot_tcgen05(lhs, rhs, full, *dd, 1, s, &sc);
   if (rc) return rc;
   if ((rc = peer_barrier(c, 0, s))) return rc;
   const int64_t n16 = n / 8;
   peer_parity_copy_kernel<<<grid_for(n16, 256), 256, 0, s>>>(
-      (const uint4*)(c->heap + CTRL_BYTES), (uint4*)out.data, (const uint32_t*)c->heap, n16);
+      (const uint4*)(c->heap + CTRL_BYTES), (uint4*)out.data, (const uint32_t*)c->heap,
+      par_slots * slot / 8, n16);
   return launched(s);
 }
 
@@ -491,7 +513,7 @@ struct DispatchPush {
   uint4* dst[8];      // member j's landing zone (data start of its heap)
   int G, pos, Bl, S, E, El, C;
   int64_t m16;        // 16-byte vectors per row
-  int64_t slot_rows;  // rows of one parity buffer: B * E_loc * C
+  int64_t par_rows;   // rows per parity (fused_parity: parity p starts at row p * par_rows)
 };
 
 __global__ void __launch_bounds__(256) moe_dispatch_push_kernel(const uint4* __restrict__ x,
@@ -512,7 +534,7 @@ __global__ void __launch_bounds__(256) moe_dispatch_push_kernel(const uint4* __r
     const int b = (int)(r % a.Bl);
     const int j = (int)(r / a.Bl);
     const int s = inv[((int64_t)b * a.E + j * a.El + el) * a.C + c];
-    const int64_t drow = par * a.slot_rows +
+    const int64_t drow = par * a.par_rows +
                          (((int64_t)(a.pos * a.Bl + b) * a.El + el) * a.C + c);
     uint4* dst = a.dst[j] + drow * a.m16;
     if (s < 0) {
@@ -529,8 +551,8 @@ __global__ void __launch_bounds__(256) moe_dispatch_push_kernel(const uint4* __r
 // out [B_loc * G, E / G, C, M] = all-to-all(split 1, concat 0)(dispatch(x)).
 extern "C" int spmd_moe_dispatch_all_to_all(spmd_comm* c, spmd_tensor x, spmd_tensor expert,
                                             spmd_tensor slot, spmd_tensor out,
-                                            const int32_t* groups, int ngroups, int gsize,
-                                            void* stream) {
+                                            spmd_tensor index_scratch, const int32_t* groups,
+                                            int ngroups, int gsize, void* stream) {
   SPMD_CHECK_ARG(c && x.dtype == SPMD_BF16 && out.dtype == SPMD_BF16 && x.rank == 3 &&
                      out.rank == 4 && expert.dtype == SPMD_S32 && slot.dtype == SPMD_S32,
                  "moe dispatch all-to-all expects bf16 x [B,S,M] -> [B*G, E/G, C, M]");
@@ -547,17 +569,14 @@ extern "C" int spmd_moe_dispatch_all_to_all(spmd_comm* c, spmd_tensor x, spmd_te
                      M % 8 == 0,
                  "moe dispatch all-to-all shape");
   const int64_t n = numel(out);
-  if (2 * n * 2 > c->heap_bytes) {
-    set_error("peer heap too small for this all-to-all");
-    return SPMD_ERR_INVALID;
-  }
+  int64_t par_rows = 0;
+  if ((rc = fused_parity(c, (int64_t)M * 2, n / M, &par_rows))) return rc;
   const int64_t inv_bytes = (int64_t)Bl * E * C * 4;
-  if (c->ws_bytes < inv_bytes) {
-    set_error("collective workspace too small for the dispatch index");
-    return SPMD_ERR_INVALID;
-  }
+  SPMD_CHECK_ARG(index_scratch.data && index_scratch.dtype == SPMD_S32 &&
+                     numel(index_scratch) * 4 >= inv_bytes,
+                 "moe dispatch all-to-all: index scratch must hold B*E*C s32");
   cudaStream_t s = as_stream(stream);
-  int32_t* inv = (int32_t*)c->ws;
+  int32_t* inv = (int32_t*)index_scratch.data;
   SPMD_CUDA_TRY(cudaMemsetAsync(inv, 0xff, inv_bytes, s));   // -1: empty slot
   const int64_t tokens = (int64_t)Bl * S;
   moe_inverse_kernel<<<grid_for(tokens, 256), 256, 0, s>>>(
@@ -569,7 +588,7 @@ extern "C" int spmd_moe_dispatch_all_to_all(spmd_comm* c, spmd_tensor x, spmd_te
     a.dst[j] = (uint4*)(c->peer[groups[grp * gsize + j]] + CTRL_BYTES);
   a.G = gsize, a.pos = pos, a.Bl = Bl, a.S = S, a.E = E, a.El = El, a.C = C;
   a.m16 = M / 8;
-  a.slot_rows = (int64_t)Bl * gsize * El * C;
+  a.par_rows = par_rows;
   const int64_t rows = (int64_t)gsize * Bl * El * C;
   moe_dispatch_push_kernel<<<grid_for(rows * 32, 256), 256, 0, s>>>(
       (const uint4*)x.data, inv, a, (const uint32_t*)c->heap);
@@ -577,7 +596,8 @@ extern "C" int spmd_moe_dispatch_all_to_all(spmd_comm* c, spmd_tensor x, spmd_te
   if ((rc = peer_barrier(c, 0, s))) return rc;
   const int64_t n16 = n / 8;
   peer_parity_copy_kernel<<<grid_for(n16, 256), 256, 0, s>>>(
-      (const uint4*)(c->heap + CTRL_BYTES), (uint4*)out.data, (const uint32_t*)c->heap, n16);
+      (const uint4*)(c->heap + CTRL_BYTES), (uint4*)out.data, (const uint32_t*)c->heap,
+      par_rows * (M / 8), n16);
   return launched(s);
 }
 
@@ -644,8 +664,7 @@ static int peer_permute(spmd_comm* c, const char* src, int64_t rows, int64_t wid
   }
   const int64_t bytes = rows * width;
   SPMD_CHECK_ARG(bytes == numel(out) * elem_size(out.dtype), "permute mismatch");
-  SPMD_CHECK_ARG(heap_offset >= 0 && heap_offset % 256 == 0 && heap_offset + bytes <= c->heap_bytes,
-                 "peer permute slot outside the heap");
+  if (int rc = check_slot(c, heap_offset, bytes, "peer permute landing")) return rc;
   if (send_to >= 0 && bytes) {
     char* dst = c->peer[send_to] + CTRL_BYTES + heap_offset;
     if (rows == 1)

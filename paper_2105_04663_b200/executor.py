@@ -131,6 +131,15 @@ class NcclComm:
                                                     self._ws.numel()),
                     "spmd_comm_set_workspace")
 
+    def reserve_fused(self, half_bytes: int) -> int:
+        """Grow the fused-op landing zone to >= ``half_bytes`` per parity
+        (peer.cu fused_parity); returns the communicator's H.  Every rank
+        compiles the same program, so every rank reserves the same H."""
+        lib = C.lib()
+        C.check(lib.spmd_comm_reserve_fused(self.handle, int(half_bytes)),
+                "spmd_comm_reserve_fused")
+        return int(lib.spmd_comm_fused_half(self.handle))
+
     def ensure_peer(self, nbytes: int, device) -> None:
         """Collective: allocate / grow the CUDA-IPC peer heap used by the
         fused dot -> reduce-scatter kernels (every rank, same size)."""
@@ -210,11 +219,14 @@ class Executor:
         if comm is not None:
             comm.ensure_workspace(self._workspace_bytes(), self.device)
             peer = self._peer_bytes()
+            self._peer_bytes_used = peer
             if peer:
                 comm.ensure_peer(peer, self.device)
         else:
             self._peer_ag = {}
             self._peer_cp = {}
+            self._peer_bytes_used = 0
+            self._fused_half = 0
         self._peer_engine = self._plan_peer_engines()
         self._staged_exposed: list = []
         self._act_staged: set = set()
@@ -391,21 +403,27 @@ class Executor:
                            device=self.device)
 
     def _peer_bytes(self) -> int:
-        """Peer heap: [0, R) two parity buffers of gsize slots of the largest
-        fused dot -> reduce-scatter shard, then one staging slot per
-        peer all-gather (offsets recorded in ``self._peer_ag``)."""
+        """Peer heap: [0, 3H) the fused-op landing zone (H = per-parity bytes
+        of the largest fused dot -> reduce-scatter / all-to-all / MoE
+        dispatch, reserved on the communicator so every executor sharing it
+        uses the same parity stride: peer.cu fused_parity), then one staging
+        slot per peer all-gather and one landing slot per peer permute
+        (offsets recorded in ``self._peer_ag`` / ``self._peer_cp``)."""
         import os
-        need = 0
+        half = 0
         for spec in self._fused.values():
             if spec[0] == "dot_rs":
                 rs = spec[2]
-                need = max(need, 2 * rs.shape.num_elements * len(rs.attrs["subgroups"][0]) *
+                half = max(half, rs.shape.num_elements * len(rs.attrs["subgroups"][0]) *
                            rs.shape.dtype.itemsize)
             elif spec[0] == "dot_a2a":
-                need = max(need, 2 * spec[2].shape.num_elements * spec[2].shape.dtype.itemsize)
+                half = max(half, spec[2].shape.num_elements * spec[2].shape.dtype.itemsize)
             elif spec[0] == "moe_dispatch_a2a":
-                need = max(need, 2 * spec[3].shape.num_elements * spec[3].shape.dtype.itemsize)
-        off = (need + 4095) // 4096 * 4096
+                half = max(half, spec[3].shape.num_elements * spec[3].shape.dtype.itemsize)
+        if self.comm is not None:
+            half = self.comm.reserve_fused(half)
+        self._fused_half = half
+        off = 3 * half
         self._peer_ag = {}
         if os.environ.get("SPMD_PEER_AG", "1") != "0":
             for ins in self.graph.instructions:
@@ -471,10 +489,6 @@ class Executor:
 
     def _workspace_bytes(self) -> int:
         need = 0
-        for spec in self._fused.values():   # dispatch index [B, E, C] s32
-            if spec[0] == "moe_dispatch_a2a":
-                sh = spec[3].shape
-                need = max(need, sh.dims[0] * sh.dims[1] * sh.dims[2] * 4)
         for ins in self.graph.instructions:
             if ins.opcode in COLLECTIVES and ins.opcode != Op.COLLECTIVE_PERMUTE:
                 src = self._shape(ins.operands[0])
@@ -1128,12 +1142,17 @@ class Executor:
             ish = Shape(tuple(r.expert.shape[1:]), DType.S32)
             groups, ng, gs = _groups_arg(a2a.attrs["subgroups"])
             comm = self.comm
+            # (batch, expert, slot) -> token table, private to this op
+            nidx = shp.dims[0] * shp.dims[1] * shp.dims[2]
+            idx = _torch().empty((nidx,), dtype=_torch().int32, device=self.device)
+            idx_sh = Shape((nidx,), DType.S32)
 
             def run(env, s):
                 out = self._alloc(shp)
                 C.check(lib.spmd_moe_dispatch_all_to_all(comm.handle, desc(env[x], xsh),
                                                          desc(r.expert, ish), desc(r.slot, ish),
-                                                         desc(out, shp), groups, ng, gs, s),
+                                                         desc(out, shp), desc(idx, idx_sh),
+                                                         groups, ng, gs, s),
                         "moe_dispatch_all_to_all")
                 return out
             return run
@@ -1629,6 +1648,11 @@ class Executor:
         s = stream if stream is not None else torch.cuda.current_stream(self.device).cuda_stream
         if len(inputs) != len(self.params):
             raise EvalError(f"expected {len(self.params)} inputs, got {len(inputs)}")
+        if self.comm is not None and self._peer_bytes_used and \
+                self.lib.spmd_comm_fused_half(self.comm.handle) != self._fused_half:
+            raise EvalError("the communicator's fused peer region grew after this executor "
+                            "was compiled (its staging slots would overlap it): rebuild the "
+                            "Executor")
         env = {"__inputs__": list(inputs)}
         keep = keep or set()
         self.lib.spmd_set_sm_limit(self._sm_limit)   # process-wide; captured into graphs
@@ -1643,6 +1667,11 @@ class Executor:
                 C.check(self.lib.spmd_peer_barrier(self.comm.handle, 0, s), "peer_barrier")
         else:
             self._run_two_streams(env, keep)
+        if self._peer_bytes_used and not torch.cuda.is_current_stream_capturing():
+            # a peer barrier that timed out only sets the device error word:
+            # surface it here (graph replays: the caller checks after them)
+            C.check(self.lib.spmd_check_device_errors(
+                torch.cuda.current_stream(self.device).cuda_stream), "peer barrier")
         self.last_env = env if keep else None
         return [env[o] for o in self.graph.outputs]
 
@@ -1699,7 +1728,14 @@ class Executor:
                     ev.record(streams[src])
                     events[o] = ev
                 stream.wait_event(ev)
-            out = step.fn(env, stream.cuda_stream)
+            if lane:
+                # lane outputs and temporaries come from the lane's own
+                # allocator pool: a block the compute stream freed while its
+                # readers are still queued is never handed to a lane kernel
+                with torch.cuda.stream(stream):
+                    out = step.fn(env, stream.cuda_stream)
+            else:
+                out = step.fn(env, stream.cuda_stream)
             env[step.ins.id] = out
             lane_of[step.ins.id] = lane
             if lane:
@@ -1707,7 +1743,9 @@ class Executor:
                     t = env.get(o)
                     if t is not None and hasattr(t, "record_stream"):
                         t.record_stream(stream)
-                out.record_stream(stream)
+                # consumers run on the compute stream (or other lanes): the
+                # block is recycled only after their uses complete
+                out.record_stream(compute)
                 ev = torch.cuda.Event()
                 ev.record(stream)
                 events[step.ins.id] = ev

@@ -39,6 +39,11 @@ def rel(a, b):
 
 
 def direct_abi(comm, rank, world, dev):
+    """Fused dot -> reduce-scatter vs dot + NCCL reduce-scatter.  The fused
+    ops run back to back with NO host sync and alternate sizes and subgroups
+    (the training step's pattern): a peer that passed op k's barrier writes
+    op k+1's tiles while this rank may still reduce op k, which the fixed
+    parity stride (peer.cu fused_parity) must keep apart."""
     lib = C.lib()
     s = torch.cuda.current_stream().cuda_stream
     partitions = [[list(range(world))]]
@@ -46,13 +51,16 @@ def direct_abi(comm, rank, world, dev):
         partitions.append([[0, 1], [2, 3]] if world == 4 else
                           [list(range(i, i + world // 2)) for i in (0, world // 2)])
         partitions.append([[r for r in range(world) if r % 2 == k] for k in (0, 1)])
-    errs = []
-    M, K, N = 512, 768, 1024
-    comm.ensure_peer(2 * M * N * 2 * 2, dev)
+    K, N = 768, 1024
+    sizes = [512, 2048, 256, 1024, 2048, 512, 256, 1536]
+    comm.reserve_fused(max(sizes) * N * 2)
+    comm.ensure_peer(3 * max(sizes) * N * 2 + (1 << 20), dev)
+    comm.ensure_workspace(4 * max(sizes) * N, dev)
     dd = C.SpmdDotDims()
     dd.n_contract = 1
     dd.lhs_contracting[0], dd.rhs_contracting[0] = 1, 0
-    for it in range(6):
+    runs = []
+    for it, M in enumerate(sizes):
         groups = partitions[it % len(partitions)]
         gs = len(groups[0])
         garr, ng, gsz = _groups_arg(groups)
@@ -65,11 +73,13 @@ def direct_abi(comm, rank, world, dev):
         C.check(lib.spmd_dot_reduce_scatter(comm.handle, desc(a, ash), desc(b, bsh),
                                             desc(fused, osh), ctypes.byref(dd), 1, garr, ng, gsz,
                                             s), "dot_reduce_scatter")
+        runs.append((a, b, ash, bsh, osh, fused, garr, ng, gsz, M))
+    errs = []
+    for a, b, ash, bsh, osh, fused, garr, ng, gsz, M in runs:
         full = torch.empty((1, M, N), device=dev, dtype=torch.bfloat16)
         C.check(lib.spmd_dot(desc(a, ash), desc(b, bsh), desc(full, Shape((M, N), DType.BF16)),
                              ctypes.byref(dd), 1, s), "dot")
         ref = torch.empty_like(fused)
-        comm.ensure_workspace(4 * M * N, dev)
         C.check(lib.spmd_reduce_scatter(comm.handle, desc(full, Shape((M, N), DType.BF16)),
                                         desc(ref, osh), 1, 0, garr, ng, gsz, s), "rs")
         torch.cuda.synchronize()
@@ -89,6 +99,8 @@ def direct_abi_rows(comm, rank, world, dev):
     dd.n_contract = 1
     dd.lhs_contracting[0], dd.rhs_contracting[0] = 0, 0
     errs = []
+    comm.reserve_fused(M * N * D * 2)
+    comm.ensure_peer(3 * M * N * D * 2 + (1 << 20), dev)
     for it in range(3):
         g = torch.Generator(device=dev).manual_seed(77 * it + rank)
         a = torch.randn((1, T, M), device=dev, generator=g).bfloat16()

@@ -15,9 +15,15 @@ from paper_2105_04663_b200.workloads import transformer_layer
 class FakeComm:
     handle = None
     peer = 0
+    half = 0
 
     def ensure_workspace(self, nbytes, device):
         pass
+
+    def reserve_fused(self, half_bytes):
+        # spmd_comm_reserve_fused: grows only, 4 KiB granules
+        self.half = max(self.half, (int(half_bytes) + 4095) // 4096 * 4096)
+        return self.half
 
     def ensure_peer(self, nbytes, device):
         self.peer = nbytes
@@ -142,6 +148,38 @@ def test_training_step_gradient_reduce_scatters_all_fuse(mesh):
     dims = {v[2].attrs["dim"] for v in fused.values()}
     assert 0 in dims and any(d > 0 for d in dims)
     assert comm.peer > 0
+    _check_fused_parity_layout(ex, comm)
+
+
+def _check_fused_parity_layout(ex, comm):
+    """peer.cu fused_parity: parity p of a fused op with unit u bytes (slot /
+    row) and n units per parity starts at unit p * ceil(H / u).  Parity 0 of
+    EVERY op must lie in [0, H) and parity 1 in [H, 3H), so back-to-back
+    fused ops of different sizes (the training step's 67M -> 268M -> 67M
+    element reduce-scatters) never write into the buffer a peer is still
+    reducing; staging / landing slots start at or after 3H."""
+    H = comm.half
+    assert H > 0 and ex._fused_half == H
+    sizes = set()
+    for kind, *spec in ex._fused.values():
+        if kind == "dot_rs":
+            rs = spec[1]
+            u, n = rs.shape.nbytes, len(rs.attrs["subgroups"][0])
+        elif kind == "dot_a2a":
+            a2a = spec[1]
+            u, n = a2a.shape.nbytes // a2a.shape.dims[0], a2a.shape.dims[0]
+        elif kind == "moe_dispatch_a2a":
+            sh = spec[2].shape
+            u, n = sh.dims[-1] * sh.dtype.itemsize, sh.num_elements // sh.dims[-1]
+        else:
+            continue
+        sizes.add(u * n)
+        k = -(-H // u)
+        p0, p1 = (0, n * u), (k * u, k * u + n * u)
+        assert p0[1] <= H <= p1[0] and p1[1] <= 3 * H, (kind, u, n, H)
+    assert len(sizes) > 1          # the case the fixed stride exists for
+    slots = list(ex._peer_ag.values()) + list(ex._peer_cp.values())
+    assert all(off >= 3 * H for off in slots)
 
 
 class _Arr:

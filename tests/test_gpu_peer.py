@@ -18,6 +18,7 @@ def comm():
     import torch
     from paper_2105_04663_b200.executor import NcclComm
     c = NcclComm(0, 1)
+    c.reserve_fused(2 << 20)       # fused landing zone [0, 6 MiB); slots above it
     c.ensure_peer(64 << 20, torch.device("cuda", 0))
     yield c
     c.close()
@@ -181,7 +182,54 @@ def test_peer_collective_permute_world_of_one(comm, pairs):
     arr = (ctypes.c_int32 * max(1, len(flat)))(*flat)
     for ch in (0, 2):
         C.check(lib.spmd_peer_collective_permute(comm.handle, desc(x, sh), desc(y, sh), arr,
-                                                 len(pairs), 4 << 20, ch, s), "peer_cp")
+                                                 len(pairs), 16 << 20, ch, s), "peer_cp")
         torch.cuda.synchronize()
         assert torch.equal(y, x if pairs else torch.zeros_like(x))
     C.check(lib.spmd_check_device_errors(s), "device")
+
+
+def test_peer_slots_inside_the_fused_region_are_rejected(comm):
+    """Staging / landing slots below 3 * fused_half would alias the fused
+    ops' parity buffers: refused with EvalError (peer.cu check_slot)."""
+    import torch
+    from paper_2105_04663_b200 import _capi as C
+    from paper_2105_04663_b200.executor import EvalError, desc
+    from paper_2105_04663_b200.ir import DType, Shape
+    lib, s = C.lib(), torch.cuda.current_stream().cuda_stream
+    x = torch.randn((1, 1024), device="cuda")
+    with pytest.raises(EvalError):
+        C.check(lib.spmd_peer_stage(comm.handle, desc(x, Shape((1024,), DType.F32)), 1 << 20, s),
+                "stage")
+
+
+def test_fused_ops_of_different_sizes_back_to_back(comm):
+    """Consecutive fused dot -> reduce-scatters of different sizes (the
+    training step's pattern) alternate parities at the fixed stride and stay
+    bit-equal to the plain dot."""
+    import torch
+    from paper_2105_04663_b200 import _capi as C
+    from paper_2105_04663_b200.executor import _groups_arg, desc
+    from paper_2105_04663_b200.ir import DType, Shape
+    lib, s = C.lib(), torch.cuda.current_stream().cuda_stream
+    garr, ng, gs = _groups_arg([[0]])
+    dd = _dd()
+    outs = []
+    for it, (M, K, N) in enumerate([(256, 128, 1024), (512, 256, 1536), (256, 64, 512),
+                                    (768, 128, 1024)]):
+        torch.manual_seed(40 + it)
+        a = torch.randn((1, M, K), device="cuda").bfloat16()
+        b = (torch.randn((1, K, N), device="cuda") * 0.05).bfloat16()
+        ash, bsh, osh = (Shape((M, K), DType.BF16), Shape((K, N), DType.BF16),
+                         Shape((M, N), DType.BF16))
+        fused = torch.empty((1, M, N), device="cuda", dtype=torch.bfloat16)
+        plain = torch.empty_like(fused)
+        C.check(lib.spmd_dot_reduce_scatter(comm.handle, desc(a, ash), desc(b, bsh),
+                                            desc(fused, osh), ctypes.byref(dd), 1, garr, ng, gs,
+                                            s), "dot_reduce_scatter")
+        C.check(lib.spmd_dot(desc(a, ash), desc(b, bsh), desc(plain, osh), ctypes.byref(dd), 1,
+                             s), "dot")
+        outs.append((fused, plain))
+    torch.cuda.synchronize()
+    C.check(lib.spmd_check_device_errors(s), "device")
+    for fused, plain in outs:
+        assert torch.equal(fused, plain)
