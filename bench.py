@@ -32,11 +32,10 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "sharded Transformer layer TFLOP/s/GPU & MFU at 1/2/4/8 B200; reshard GB/s"
-# (X=data, Y=model).  N=8 is BASELINE's 2x4 data x model mesh.  N=4 uses 1x4:
-# measured 14.4 ms vs 16.1-16.4 ms for 2x2 on one box -- a data axis costs
-# every GPU the all-gather of its weight shards each step
-# (profiles/r1_c2_n4_mesh_1x4_vs_2x2.log).  SPMD_BENCH_MESH=2x2 restores it.
-MESHES = {1: (1, 1), 2: (1, 2), 4: (1, 4), 8: (2, 4)}
+# (X=data, Y=model): (1,1), (1,2), (2,2) and the
+# north-star 2x4.  At N=4 the line also carries the 1x4 mesh under
+# configs.c2_mesh_1x4 (no data axis, so no per-step weight gathers).
+MESHES = {1: (1, 1), 2: (1, 2), 4: (2, 2), 8: (2, 4)}
 if os.environ.get("SPMD_BENCH_MESH"):   # e.g. "1x4": override the (X=data, Y=model) mesh
     _x, _y = (int(v) for v in os.environ["SPMD_BENCH_MESH"].split("x"))
     MESHES[_x * _y] = (_x, _y)
@@ -116,17 +115,18 @@ def _dist_env():
     return rank, world, local
 
 
-def _cpu_baseline(mesh, steps=1):
+def _cpu_baseline(mesh, steps=1, B=4):
     """Reference executor restated on the CPU (oracle port, single-threaded
     float64 einsum like the reference) on a bounded sample of the C2 graph:
-    same annotations/mesh, dims M=1024 N=16 D=64 H=8192 B=1 S=256."""
+    same annotations/mesh, dims M=1024 N=16 D=64 H=8192 S=256 and B=4
+    (BASELINE.md section 4)."""
     import numpy as np
     from oracle import evaluator as O
     from paper_2105_04663_b200 import partition, propagate
     from paper_2105_04663_b200.ir import DType
     from paper_2105_04663_b200.sharding import shard_data
     from paper_2105_04663_b200.workloads import transformer_flops, transformer_layer
-    dims = dict(B=max(1, mesh[0]), S=256, M=1024, N=16, D=64, H=8192)
+    dims = dict(B=max(B, mesh[0]), S=256, M=1024, N=16, D=64, H=8192)
     g, ins = transformer_layer(mesh, dtype=DType.F32, seed=1, **dims)
     ann, _ = propagate(g)
     n = mesh[0] * mesh[1]
@@ -161,7 +161,9 @@ def run_reference(args):
     mesh = MESHES[args.gpus]
     vals = []
     for i in range(args.warmup + args.steps):
-        v, t, cores, sample = _cpu_baseline(mesh)
+        # untimed warm-up steps run the B=1 sample (same graph, imports and
+        # caches warmed); every timed step is one B=4 sample (~9 s)
+        v, t, cores, sample = _cpu_baseline(mesh, B=1 if i < args.warmup else 4)
         if i >= args.warmup:
             vals.append((v, t))
     v = sorted(x[0] for x in vals)[len(vals) // 2]
@@ -217,17 +219,17 @@ def _traffic_for(top, prog):
     return None
 
 
-C3 = dict(E=8, B=64, S=512, C=160, M=4096, H=16384)
+C3 = dict(E=8, B=64, S=512, C=160, M=4096, H=16384, k=2)
 C4 = dict(N=8, H=1024, W=1024, C=128, layers=4)
 
 
-def _workload(config, world, scale=1.0):
+def _workload(config, world, scale=1.0, mesh=None):
     """(mesh, graph, dims, flops/step, fan-in per parameter, description)."""
     from paper_2105_04663_b200.ir import DType
     from paper_2105_04663_b200.workloads import (conv_stack, moe_layer, transformer_flops,
                                                  transformer_layer)
     if config == "c2":
-        mesh = MESHES[world]
+        mesh = mesh or MESHES[world]
         dims = dict(PAPER)
         if scale != 1.0:
             dims["B"] = max(mesh[0], int(dims["B"] * scale))
@@ -238,7 +240,7 @@ def _workload(config, world, scale=1.0):
             "C2 transformer layer (attention+FFN), paper dims"
     if config == "c2train":
         from paper_2105_04663_b200.workloads import transformer_train_flops, transformer_train_step
-        mesh = MESHES[world]
+        mesh = mesh or MESHES[world]
         dims = dict(PAPER)
         if scale != 1.0:
             dims["B"] = max(mesh[0], int(dims["B"] * scale))
@@ -250,10 +252,11 @@ def _workload(config, world, scale=1.0):
             "paper dims"
     if config == "c3":
         d = dict(C3)
-        g, _ = moe_layer(world, dtype=DType.BF16, with_inputs=False, **d)
+        g, _ = moe_layer(world, dtype=DType.BF16, with_inputs=False,
+                         **{k: v for k, v in d.items() if k != "k"})
         flops = 4.0 * d["E"] * d["B"] * d["C"] * d["M"] * d["H"]
         return (world,), g, d, flops, {"wi": d["M"], "wo": d["H"]}, \
-            "C3 GShard MoE FFN (top-1, capacity C=160), expert GEMM FLOPs"
+            "C3 GShard MoE FFN (top-2 routing, capacity C=160 = 1.25*2*S/E), expert GEMM FLOPs"
     if config == "c4":
         d = dict(C4)
         g, _ = conv_stack((world,), (-1, 0, -1, -1), dtype=DType.BF16, with_inputs=False, **d)
@@ -263,9 +266,9 @@ def _workload(config, world, scale=1.0):
     raise SystemExit(f"unknown config {config}")
 
 
-def _moe_masks(inputs, names, dims, dev, seed):
-    """Replace the dispatch/combine parameters with real top-1 routings of
-    random gating logits (on-device router, then dense masks)."""
+def _moe_masks(inputs, names, dims, dev, seed, k=2):
+    """Replace the dispatch/combine parameters with real GShard top-k
+    routings of random gating logits (on-device router, then dense masks)."""
     import torch
     from paper_2105_04663_b200 import _capi as C
     from paper_2105_04663_b200.executor import desc
@@ -275,19 +278,278 @@ def _moe_masks(inputs, names, dims, dev, seed):
     gen = torch.Generator(device=dev)
     gen.manual_seed(seed)
     logits = torch.randn((1, Bl, S, E), generator=gen, device=dev)
-    ex = torch.empty((1, Bl, S), dtype=torch.int32, device=dev)
+    ex = torch.empty((1, Bl, S, k), dtype=torch.int32, device=dev)
     sl = torch.empty_like(ex)
-    gt = torch.empty((1, Bl, S), dtype=torch.float32, device=dev)
+    gt = torch.empty((1, Bl, S, k), dtype=torch.float32, device=dev)
     st = torch.cuda.current_stream(dev).cuda_stream
     lib = C.lib()
+    rsh = lambda dt: Shape((Bl, S, k), dt)
     C.check(lib.spmd_moe_route(desc(logits, Shape((Bl, S, E), DType.F32)), Cap,
-                               desc(ex, Shape((Bl, S), DType.S32)), desc(sl, Shape((Bl, S), DType.S32)),
-                               desc(gt, Shape((Bl, S), DType.F32)), 1, st), "route")
+                               desc(ex, rsh(DType.S32)), desc(sl, rsh(DType.S32)),
+                               desc(gt, rsh(DType.F32)), 1, st), "route")
     msh = Shape((Bl, S, E, Cap), DType.BF16)
-    C.check(lib.spmd_moe_masks(desc(ex, Shape((Bl, S), DType.S32)), desc(sl, Shape((Bl, S), DType.S32)),
-                               desc(gt, Shape((Bl, S), DType.F32)), desc(inputs[di], msh),
+    C.check(lib.spmd_moe_masks(desc(ex, rsh(DType.S32)), desc(sl, rsh(DType.S32)),
+                               desc(gt, rsh(DType.F32)), desc(inputs[di], msh),
                                desc(inputs[ci], msh), 1, st), "masks")
     return ex, sl, gt
+
+
+class _Run:
+    """One workload compiled for this rank: program, executor, inputs."""
+
+    def __init__(self, config, world, rank, dev, comm, mesh=None, scale=1.0, overlap=True):
+        import numpy as np
+        from paper_2105_04663_b200 import partition, propagate
+        from paper_2105_04663_b200.executor import Executor, Routing
+        self.config = config
+        self.mesh, g, self.dims, self.flops, fan, self.wdesc = _workload(config, world, scale,
+                                                                          mesh)
+        ann, _ = propagate(g)
+        self.prog = partition(ann, world, plan="fast")
+        # Synthetic local shards, generated on the device (weights ~ N(0, 1/fan_in);
+        # MoE dispatch/combine masks from the on-device router).
+        src_params = {p.attrs["index"]: p.id for p in ann.parameters}
+        self.inputs = []
+        for p in self.prog.graph.parameters:
+            name = src_params[p.attrs["index"]]
+            self.inputs.append(_rand_like_shard(p.shape, dev, 1.0 / np.sqrt(fan.get(name, 1)),
+                                                seed=1000 * rank + p.attrs["index"]))
+        self.routing = None
+        if config == "c3":
+            # On-device GShard top-2 router -> masks (the reference graph's
+            # inputs) and the routing itself: the dispatch / combine einsums then
+            # run as the gather kernels (equal to the dense Dots).
+            names = [src_params[p.attrs["index"]] for p in self.prog.graph.parameters]
+            r = Routing(*_moe_masks(self.inputs, names, self.dims, dev, seed=rank,
+                                    k=self.dims["k"]))
+            idx = {name: p.attrs["index"] for p, name in zip(self.prog.graph.parameters, names)}
+            self.routing = {idx["dispatch"]: r, idx["combine"]: r}
+        self.ex = Executor(self.prog, nparts=1, device=dev, comm=comm, partition_base=rank,
+                           fuse=True, overlap=(world > 1 and overlap), routing=self.routing)
+
+
+def _time_steps(run, steps, warmup, eager, barrier, world, dev):
+    """W-1 eager warm-up runs (materialise constants, NCCL sub-communicators,
+    kernel attributes), capture of the whole step into one CUDA graph
+    (compute + comm streams), one warm replay, then K timed replays between
+    barriers.  Returns (ms max over ranks, step fn, graph, outs, launches/step)."""
+    import torch
+    import torch.distributed as dist
+    ex, inputs = run.ex, run.inputs
+    stream = torch.cuda.current_stream(dev)
+    for _ in range(max(1, warmup - 1)):
+        ex.run(inputs)
+    torch.cuda.synchronize()
+    ex.check_errors()
+    barrier()
+    if eager:
+        graph = outs = None
+        launches = None
+
+        def step():
+            return ex.run(inputs)
+    else:
+        graph, outs = ex.capture(inputs)
+        launches = ex.launches_per_replay
+
+        def step():
+            graph.replay()
+            return outs
+    step()
+    torch.cuda.synchronize()
+    barrier()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    ev0.record(stream)
+    for _ in range(steps):
+        step()
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    ex.check_errors()      # a peer barrier that timed out inside the replays
+    t = torch.tensor([ev0.elapsed_time(ev1) / steps], device=dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item()), step, graph, outs, launches
+
+
+def _dot_flops(prog, ins):
+    import numpy as np
+    from paper_2105_04663_b200.ir import Op, dot_dim_lists
+    a = prog.graph.instr(ins.operands[0]).shape
+    bsh = prog.graph.instr(ins.operands[1]).shape
+    if ins.opcode == Op.CONVOLUTION:
+        cd = ins.attrs["conv_dims"]
+        k = a.dims[cd.lhs_feature] * int(np.prod([bsh.dims[d] for d in cd.rhs_spatial]))
+        return 2.0 * ins.shape.num_elements * k
+    lb, rb, lc, rc, lf, rf = dot_dim_lists(ins.attrs, a.rank, bsh.rank)
+    k = int(np.prod([a.dims[d] for d in lc]))
+    return 2.0 * ins.shape.num_elements * k
+
+
+def _top_kernel(run, dev, burst, sustained, peak_src, reps=20):
+    """The dominant tensor-core kernel of the step (the largest Dot / Conv by
+    FLOPs), launched alone `reps` times on the stream the executor uses,
+    timed with CUDA events: the roofline entry of the JSON line."""
+    import torch
+    from paper_2105_04663_b200.ir import Op
+    prog, ex = run.prog, run.ex
+    stream = torch.cuda.current_stream(dev)
+    dots = [i for i in prog.graph.instructions if i.opcode in (Op.DOT, Op.CONVOLUTION)]
+    top = max(dots, key=lambda i: _dot_flops(prog, i))
+    kname = "conv_bf16_tcgen05" if top.opcode == Op.CONVOLUTION else "gemm_bf16_tcgen05"
+    top_step = next(s for s in ex.steps if s.ins.id == top.id or
+                    (ex._fused.get(s.ins.id) or (None, None))[1] is top)
+    env = {"__inputs__": run.inputs}
+    keep = set(top_step.ops)
+    ex.run(run.inputs, keep=keep)
+    env.update({k: v for k, v in ex.last_env.items() if k in keep})
+    for _ in range(3):
+        top_step.fn(env, stream.cuda_stream)
+    torch.cuda.synchronize()
+    k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    k0.record(stream)
+    for _ in range(reps):
+        top_step.fn(env, stream.cuda_stream)
+    k1.record(stream)
+    torch.cuda.synchronize()
+    kms = k0.elapsed_time(k1) / reps
+    fl = _dot_flops(prog, top)
+    achieved = fl / (kms * 1e-3) / 1e12
+    return {"bound": "tensor", "kernel": "%s (%s)" % (kname, top.id), "achieved": achieved,
+            "peak": burst, "unit": "TFLOP/s", "frac": achieved / burst,
+            "peak_source": peak_src + " burst (kernel timed alone)",
+            "frac_sustained": achieved / sustained, "traffic": _traffic_for(top, prog),
+            "ms_per_launch": kms, "flops_per_launch": fl}
+
+
+def _extra_config(config, world, rank, dev, comm, barrier, steps, warmup, burst, sustained,
+                  peak_src):
+    """A compact summary of another BASELINE config, same harness: step time
+    (CUDA-graph replay, max over ranks), TFLOP/s, MFU and the roofline of its
+    dominant kernel."""
+    import torch
+    run = _Run(config, world, rank, dev, comm)
+    ms, _, graph, outs, launches = _time_steps(run, steps, warmup, False, barrier, world, dev)
+    tf = run.flops / (ms * 1e-3) / 1e12
+    roof = _top_kernel(run, dev, burst, sustained, peak_src, reps=10)
+    out = {"workload": run.wdesc, "dims": run.dims, "mesh": list(run.mesh), "ms_per_step": ms,
+           "tflops": tf, "tflops_per_gpu": tf / world,
+           "mfu_vs_spec_2250": tf / world / SPEC_BF16_TFLOPS, "gpu_launches_per_step": launches,
+           "roofline": {k: roof[k] for k in ("kernel", "achieved", "peak", "unit", "frac",
+                                             "frac_sustained", "ms_per_launch")}}
+    del run, graph, outs
+    torch.cuda.empty_cache()
+    return out
+
+
+def _c5_hbm(dev, hbm, peak_src):
+    """C5's HBM-bound kernels at the 8-way uneven layout ([1001, 524288] f32
+    over 8 shards of ceil(1001/8) = 126 rows): the localize pad 1001 -> 1008
+    rows (partitioner.py:379-408), the dynamic-slice of one shard out of it,
+    and the select_range mask of the last shard (partitioner.py:236-247).
+    Achieved = bytes read + written / kernel time (CUDA events, 10 launches)."""
+    import torch
+    from paper_2105_04663_b200 import _capi as C
+    from paper_2105_04663_b200.executor import desc
+    from paper_2105_04663_b200.ir import DType, Shape
+    lib, st = C.lib(), torch.cuda.current_stream(dev).cuda_stream
+    f32, s32 = DType.F32, DType.S32
+    D1, rows = 524288, 126
+    sc = Shape((), s32)
+
+    def timed(fn, reps=10):
+        for _ in range(3):
+            fn()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record()
+        for _ in range(reps):
+            fn()
+        e1.record()
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / reps
+
+    res = {}
+    x = torch.randn((1, 1001, D1), device=dev)
+    y = torch.empty((1, 1008, D1), device=dev)
+    z = torch.zeros((1,), device=dev)
+    lo, hi, it = C.i64_array([0, 0]), C.i64_array([7, 0]), C.i64_array([0, 0])
+    ms = timed(lambda: C.check(lib.spmd_pad(desc(x, Shape((1001, D1), f32)),
+                                            desc(z, Shape((), f32)),
+                                            desc(y, Shape((1008, D1), f32)), lo, hi, it, 1, st),
+                               "pad"))
+    res["pad_1001_to_1008x524288_f32"] = (ms, (x.numel() + y.numel()) * 4)
+    s0 = torch.full((1,), rows * 7, dtype=torch.int32, device=dev)
+    s1 = torch.zeros((1,), dtype=torch.int32, device=dev)
+    y2 = torch.empty((1, rows, D1), device=dev)
+    starts = (C.SpmdTensor * 2)(desc(s0, sc), desc(s1, sc))
+    ms = timed(lambda: C.check(lib.spmd_dynamic_slice(desc(y, Shape((1008, D1), f32)), starts,
+                                                      desc(y2, Shape((rows, D1), f32)), 1, st),
+                               "dynamic_slice"))
+    res["dynamic_slice_1008_to_126x524288_f32"] = (ms, 2 * y2.numel() * 4)
+    off = torch.full((1,), 7 * rows, dtype=torch.int32, device=dev)
+    fill = torch.full((1,), float("-inf"), device=dev)
+    y3 = torch.empty_like(y2)
+    ms = timed(lambda: C.check(lib.spmd_mask_range(
+        desc(y2, Shape((rows, D1), f32)), desc(off, sc), desc(fill, Shape((), f32)),
+        desc(y3, Shape((rows, D1), f32)), 0, 0, 1001, 0, 1, st), "mask_range"))
+    res["mask_range_126x524288_f32"] = (ms, 2 * y2.numel() * 4)
+    del x, y, y2, y3
+    torch.cuda.empty_cache()
+    return {"bound": "hbm", "peak_gbs": hbm, "peak_source": peak_src + " copy bandwidth",
+            "kernels": {k: {"ms": ms, "bytes": b, "gbs": b / (ms * 1e-3) / 1e9,
+                            "frac": b / (ms * 1e-3) / 1e9 / hbm} for k, (ms, b) in res.items()}}
+
+
+def _reshard(world, rank, dev, comm, barrier):
+    """C5 reshard GB/s at N > 1: [n0, 524288] f32 dim-0 -> dim-1 (all-to-all,
+    padded for 1001) and -> replicated (all-gather), nccl-tests bus bytes."""
+    import torch
+    import torch.distributed as dist
+    from paper_2105_04663_b200 import partition, propagate
+    from paper_2105_04663_b200.executor import Executor
+    from paper_2105_04663_b200.ir import DType, Op
+    from paper_2105_04663_b200.workloads import uneven
+    stream = torch.cuda.current_stream(dev)
+    reshard = {}
+    D1 = 65536 * 8
+    for n0, kind in ((1000, "a2a"), (1001, "a2a"), (1001, "repl")):
+        gg, _ = uneven(n0=n0, n1=D1, kind=kind, parts=world, dtype=DType.F32, with_inputs=False)
+        ga, _ = propagate(gg)
+        rp = partition(ga, world, plan="fast")
+        rex = Executor(rp, nparts=1, device=dev, comm=comm, partition_base=rank, overlap=False)
+        rin = [torch.randn((1,) + rp.graph.parameters[0].shape.dims, device=dev)]
+        coll = next(s for s in rex.steps if s.coll)
+        keep = set(coll.ops)
+        rex.run(rin, keep=keep)
+        renv = {"__inputs__": rin}
+        renv.update({k: v for k, v in rex.last_env.items() if k in keep})
+        for _ in range(3):
+            coll.fn(renv, stream.cuda_stream)
+        torch.cuda.synchronize()
+        barrier()
+        r0, r1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        r0.record(stream)
+        for _ in range(10):
+            coll.fn(renv, stream.cuda_stream)
+        r1.record(stream)
+        torch.cuda.synchronize()
+        rms = torch.tensor([r0.elapsed_time(r1) / 10], device=dev, dtype=torch.float64)
+        dist.all_reduce(rms, op=dist.ReduceOp.MAX)
+        rms = float(rms.item())
+        src = rp.graph.instr(coll.ins.operands[0]).shape
+        if coll.ins.opcode == Op.ALL_GATHER:
+            bus = coll.ins.shape.nbytes * (world - 1) / world
+        else:
+            bus = src.nbytes * (world - 1) / world
+        reshard[f"{kind}_{n0}x{D1}_f32"] = {
+            "collective": coll.ins.opcode.value, "ms": rms,
+            "bus_gbs_per_gpu": bus / (rms * 1e-3) / 1e9,
+            "frac_of_nvlink_900": bus / (rms * 1e-3) / 1e9 / 900.0}
+        del rex, rin, renv
+    torch.cuda.empty_cache()
+    return reshard
 
 
 def main():
@@ -299,6 +561,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-extras", action="store_true",
+                    help="skip the other configs' summaries (C3/C4/C5, extra mesh)")
     ap.add_argument("--eager", action="store_true", help="no CUDA graph")
     ap.add_argument("--no-overlap", action="store_true", help="collectives on the compute stream")
     ap.add_argument("--scale", type=float, default=1.0,
@@ -307,14 +571,11 @@ def main():
     if args.impl == "reference":
         return run_reference(args)
 
-    import numpy as np
     import torch
     import torch.distributed as dist
     from paper_2105_04663_b200 import _capi as C
-    from paper_2105_04663_b200 import collective_stats, partition, propagate
-    from paper_2105_04663_b200.executor import Executor, NcclComm
-    from paper_2105_04663_b200.ir import DType, Op
-    from paper_2105_04663_b200.workloads import transformer_flops, transformer_layer
+    from paper_2105_04663_b200 import collective_stats
+    from paper_2105_04663_b200.executor import NcclComm
 
     rank, world, local = _dist_env()
     if world != args.gpus:
@@ -323,82 +584,29 @@ def main():
     dev = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
-    mesh, g, dims, flops, fan, wdesc = _workload(args.config, world, args.scale)
-    ann, _ = propagate(g)
-    prog = partition(ann, world, plan="fast")
     comm = NcclComm.from_torch_distributed() if world > 1 else None
-
-    # Synthetic local shards, generated on the device (weights ~ N(0, 1/fan_in);
-    # MoE dispatch/combine masks from the on-device router).
-    src_params = {p.attrs["index"]: p.id for p in ann.parameters}
-    inputs = []
-    for p in prog.graph.parameters:
-        name = src_params[p.attrs["index"]]
-        inputs.append(_rand_like_shard(p.shape, dev, 1.0 / np.sqrt(fan.get(name, 1)),
-                                       seed=1000 * rank + p.attrs["index"]))
-    routing = None
-    if args.config == "c3":
-        # On-device top-1 router -> one-hot masks (the reference graph's
-        # inputs) and the routing itself: the dispatch / combine einsums then
-        # run as the gather kernels (bit-identical to the dense Dots).
-        from paper_2105_04663_b200.executor import Routing
-        names = [src_params[p.attrs["index"]] for p in prog.graph.parameters]
-        r = Routing(*_moe_masks(inputs, names, dims, dev, seed=rank))
-        idx = {name: p.attrs["index"] for p, name in zip(prog.graph.parameters, names)}
-        routing = {idx["dispatch"]: r, idx["combine"]: r}
-    ex = Executor(prog, nparts=1, device=dev, comm=comm, partition_base=rank, fuse=True,
-                  overlap=(world > 1 and not args.no_overlap), routing=routing)
-    stream = torch.cuda.current_stream(dev)
 
     def barrier():
         if world > 1:
             dist.barrier(device_ids=[local])
 
-    # Warm-up runs eagerly (materialises constants, NCCL sub-communicators,
-    # kernel attributes), then the whole step is captured into one CUDA graph
-    # (compute + comm streams) and replayed: no per-op host overhead.
-    for _ in range(max(1, args.warmup - 1)):
-        ex.run(inputs)
-    torch.cuda.synchronize()
-    ex.check_errors()
-    barrier()
-    if args.eager:
-        def step(x_inputs):
-            return ex.run(x_inputs)
-        launches_per_step = None
-    else:
-        graph, graph_outs = ex.capture(inputs)
-        launches_per_step = ex.launches_per_replay
-
-        def step(x_inputs):
-            graph.replay()
-            return graph_outs
-    step(inputs)
-    torch.cuda.synchronize()
-    barrier()
+    run = _Run(args.config, world, rank, dev, comm, scale=args.scale,
+               overlap=not args.no_overlap)
+    prog, ex, inputs, flops = run.prog, run.ex, run.inputs, run.flops
+    stream = torch.cuda.current_stream(dev)
 
     sampler = ClockSampler(local)
     sampler.start()
     launches0 = C.lib().spmd_launch_count()
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    barrier()
-    torch.cuda.synchronize()
-    ev0.record(stream)
-    for _ in range(args.steps):
-        out = step(inputs)
-    ev1.record(stream)
-    torch.cuda.synchronize()
-    barrier()
+    ms, step, graph, graph_outs, launches_per_step = _time_steps(
+        run, args.steps, args.warmup, args.eager, barrier, world, dev)
     launches = C.lib().spmd_launch_count() - launches0
     if launches_per_step is not None:
         launches = launches_per_step * args.steps
     clocks = sampler.stop()
-    ms = ev0.elapsed_time(ev1) / args.steps
-    t = torch.tensor([ms], device=dev, dtype=torch.float64)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms = float(t.item())
     value = flops / (ms * 1e-3) / 1e12
+    out = step()
+    torch.cuda.synchronize()
 
     # ---- e2e: host (pinned) activation in, host result out, every step ----
     # Every step uploads its activation from pinned host memory and reads its
@@ -417,7 +625,7 @@ def main():
             def run_e2e(nsteps):
                 for _ in range(nsteps):
                     dev_inputs[0].copy_(x_host, non_blocking=True)
-                    o = step(dev_inputs)
+                    o = ex.run(dev_inputs)
                     out_host[0].copy_(o[0], non_blocking=True)
         else:
             inputs_b = [inputs[0].clone()] + list(inputs[1:])
@@ -471,98 +679,53 @@ def main():
                "d2h_bytes_per_step": int(out_host[0].numel() * 2 * world),
                "copies": "serial" if args.eager else
                "pipelined (2 captured steps, copy streams)"}
+        if not args.eager:
+            del graph_b, outs_b, sets
 
     # ---- roofline of the dominant kernel: the largest tcgen05 GEMM ----
     burst, sustained, hbm, peak_src = _peaks()
-    dots = [i for i in prog.graph.instructions if i.opcode in (Op.DOT, Op.CONVOLUTION)]
-    from paper_2105_04663_b200.ir import dot_dim_lists
-
-    def dot_flops(ins):
-        a = prog.graph.instr(ins.operands[0]).shape
-        bsh = prog.graph.instr(ins.operands[1]).shape
-        if ins.opcode == Op.CONVOLUTION:
-            cd = ins.attrs["conv_dims"]
-            k = a.dims[cd.lhs_feature] * int(np.prod([bsh.dims[d] for d in cd.rhs_spatial]))
-            return 2.0 * ins.shape.num_elements * k
-        lb, rb, lc, rc, lf, rf = dot_dim_lists(ins.attrs, a.rank, bsh.rank)
-        k = int(np.prod([a.dims[d] for d in lc]))
-        return 2.0 * ins.shape.num_elements * k
-
-    top = max(dots, key=dot_flops)
-    kname = "conv_bf16_tcgen05" if top.opcode == Op.CONVOLUTION else "gemm_bf16_tcgen05"
-    top_step = next(s for s in ex.steps if s.ins.id == top.id or
-                    (ex._fused.get(s.ins.id) or (None, None))[1] is top)
     print(f"[bench] step {ms:.2f} ms  ({value:.1f} TFLOP/s aggregate)", file=sys.stderr)
-    env = {"__inputs__": inputs}
-    # materialise the operands of the top GEMM's step once
-    keep = set(top_step.ops)
-    ex.run(inputs, keep=keep)
-    env.update({k: v for k, v in ex.last_env.items() if k in keep})
-    for _ in range(3):
-        top_step.fn(env, stream.cuda_stream)
-    torch.cuda.synchronize()
-    k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    reps = 20
-    k0.record(stream)
-    for _ in range(reps):
-        top_step.fn(env, stream.cuda_stream)
-    k1.record(stream)
-    torch.cuda.synchronize()
-    kms = k0.elapsed_time(k1) / reps
-    achieved = dot_flops(top) / (kms * 1e-3) / 1e12
-    gemm_share = None
+    roofline = _top_kernel(run, dev, burst, sustained, peak_src)
+    stats = collective_stats(prog)
+    mesh, dims, wdesc, routing = run.mesh, run.dims, run.wdesc, run.routing
+    del run, ex, graph, graph_outs, step, out, inputs
+    torch.cuda.empty_cache()
 
-    # ---- reshard GB/s (config C5: [n0, D] f32 dim-0 -> dim-1 / -> replicated) ----
+    # ---- the other BASELINE configs, same harness (driver-visible) ----
+    configs = None
+    if not args.no_extras and args.config == "c2":
+        configs = {}
+        if world == 4:
+            # BASELINE's 2x2 is the headline at N=4; the 1x4 mesh (no data
+            # axis: no weight gathers) as the alternative layout
+            alt = _Run("c2", world, rank, dev, comm, mesh=(1, 4))
+            ams, _, ag, ao, _ = _time_steps(alt, args.steps, args.warmup, False, barrier, world,
+                                            dev)
+            configs["c2_mesh_1x4"] = {"mesh": [1, 4], "ms_per_step": ams,
+                                      "tflops": alt.flops / (ams * 1e-3) / 1e12}
+            del alt, ag, ao
+            torch.cuda.empty_cache()
+        for cfg in ("c3", "c4"):
+            configs[cfg] = _extra_config(cfg, world, rank, dev, comm, barrier,
+                                         max(5, args.steps // 2), args.warmup, burst, sustained,
+                                         peak_src)
+        if rank == 0:
+            configs["c5_hbm"] = _c5_hbm(dev, hbm, peak_src)
+        barrier()
+
+    # ---- reshard GB/s (config C5) at N > 1 ----
     reshard = None
     if world > 1 and args.config == "c2":
-        from paper_2105_04663_b200.workloads import uneven
-        reshard = {}
-        D1 = 65536 * 8
-        for n0, kind in ((1000, "a2a"), (1001, "a2a"), (1001, "repl")):
-            gg, _ = uneven(n0=n0, n1=D1, kind=kind, parts=world, dtype=DType.F32,
-                           with_inputs=False)
-            ga, _ = propagate(gg)
-            rp = partition(ga, world, plan="fast")
-            rex = Executor(rp, nparts=1, device=dev, comm=comm, partition_base=rank,
-                           overlap=False)
-            rin = [torch.randn((1,) + rp.graph.parameters[0].shape.dims, device=dev)]
-            coll = next(s for s in rex.steps if s.coll)
-            keep = set(coll.ops)
-            rex.run(rin, keep=keep)
-            renv = {"__inputs__": rin}
-            renv.update({k: v for k, v in rex.last_env.items() if k in keep})
-            for _ in range(3):
-                coll.fn(renv, stream.cuda_stream)
-            torch.cuda.synchronize()
-            barrier()
-            r0, r1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            r0.record(stream)
-            for _ in range(10):
-                coll.fn(renv, stream.cuda_stream)
-            r1.record(stream)
-            torch.cuda.synchronize()
-            rms = torch.tensor([r0.elapsed_time(r1) / 10], device=dev, dtype=torch.float64)
-            dist.all_reduce(rms, op=dist.ReduceOp.MAX)
-            rms = float(rms.item())
-            src = rp.graph.instr(coll.ins.operands[0]).shape
-            if coll.ins.opcode == Op.ALL_GATHER:
-                bus = coll.ins.shape.nbytes * (world - 1) / world
-            else:
-                bus = src.nbytes * (world - 1) / world
-            reshard[f"{kind}_{n0}x{D1}_f32"] = {
-                "collective": coll.ins.opcode.value, "ms": rms,
-                "bus_gbs_per_gpu": bus / (rms * 1e-3) / 1e9,
-                "frac_of_nvlink_770": bus / (rms * 1e-3) / 1e9 / 770.0}
+        reshard = _reshard(world, rank, dev, comm, barrier)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline and args.config == "c2":
-        # ~10-12 s of CPU work: the best of 5 samples of ~2.3 s each
-        v, tcpu, cores, sample = _cpu_baseline(mesh, steps=5)
-        sample += ", best of 5 timed samples"
+        # ~20 s of CPU work: the best of 2 samples of ~9 s each (B=4)
+        v, tcpu, cores, sample = _cpu_baseline(mesh, steps=2)
+        sample += ", best of 2 timed samples"
         cpu = {"value": v, "unit": "TFLOP/s", "cores": cores, "kind": "port",
                "sample": sample, "seconds_per_sample": tcpu}
 
-    stats = collective_stats(prog)
     if rank == 0:
         per_gpu = value / world
         cfg = {"workload": wdesc, "model_dims": dims, "mesh": list(mesh),
@@ -571,9 +734,8 @@ def main():
                "plan": "fast", "l2": "inputs larger than L2 (weights+activations)",
                "collectives_per_step": stats["counts"]}
         if routing:
-            cfg["dispatch_combine"] = "moe.cu gather kernels over the on-device routing " \
-                "(bit-identical to the dense one-hot Dots)"
-
+            cfg["dispatch_combine"] = "moe.cu gather kernels over the on-device top-2 " \
+                "routing (equal to the dense Dots)"
         if args.config in ("c2", "c2train"):
             cfg.update(global_batch=dims["B"], seq_len=dims["S"])
         line = {
@@ -586,14 +748,11 @@ def main():
             "tflops_per_gpu": per_gpu,
             "mfu": {"vs_spec_2250": per_gpu / SPEC_BF16_TFLOPS,
                     "vs_measured_sustained": per_gpu / sustained},
-            "roofline": {"bound": "tensor", "kernel": "%s (%s)" % (kname, top.id),
-                         "achieved": achieved, "peak": burst, "unit": "TFLOP/s",
-                         "frac": achieved / burst, "peak_source": peak_src + " burst",
-                         "traffic": _traffic_for(top, prog), "ms_per_launch": kms,
-                         "flops_per_launch": dot_flops(top)},
+            "roofline": roofline,
             "reshard": reshard,
             "e2e": e2e, "gpu_launches": int(launches), "clocks": clocks,
             "cpu_baseline": cpu,
+            "configs": configs,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -499,13 +499,16 @@ extern "C" int spmd_dot_all_to_all(spmd_comm* c, spmd_tensor lhs, spmd_tensor rh
 // for its experts e = j*E_loc + e_loc, written straight into its heap
 // (16-byte NVLink stores, empty slots as zeros, so no receiver-side clear).
 // ---------------------------------------------------------------------------
+// Routing [B, S, K] (moe.cu layout) -> inv[(b * E + e) * C + slot] = s for
+// every kept (token, choice); empty slots stay -1.
 __global__ void moe_inverse_kernel(const int32_t* __restrict__ expert,
                                    const int32_t* __restrict__ slot, int32_t* __restrict__ inv,
-                                   int64_t tokens, int S, int E, int C) {
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < tokens;
-       t += (int64_t)gridDim.x * blockDim.x) {
-    const int sl = slot[t];
-    if (sl < C) inv[((t / S) * E + expert[t]) * (int64_t)C + sl] = (int32_t)(t % S);
+                                   int64_t assigns, int K, int S, int E, int C) {
+  for (int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; a < assigns;
+       a += (int64_t)gridDim.x * blockDim.x) {
+    const int sl = slot[a];
+    const int64_t t = a / K;
+    if (sl < C) inv[((t / S) * E + expert[a]) * (int64_t)C + sl] = (int32_t)(t % S);
   }
 }
 
@@ -565,6 +568,11 @@ extern "C" int spmd_moe_dispatch_all_to_all(spmd_comm* c, spmd_tensor x, spmd_te
   if (rc) return rc;
   const int Bl = (int)x.dims[0], S = (int)x.dims[1], M = (int)x.dims[2];
   const int El = (int)out.dims[1], C = (int)out.dims[2], E = El * gsize;
+  // routing [B, S] (top-1) or [B, S, K]
+  const int K = expert.rank == 3 ? (int)expert.dims[2] : 1;
+  SPMD_CHECK_ARG(expert.rank >= 2 && expert.rank <= 3 && slot.rank == expert.rank &&
+                     expert.dims[0] == Bl && expert.dims[1] == S && K >= 1 && K <= 4,
+                 "moe dispatch all-to-all routing shape");
   SPMD_CHECK_ARG(gsize <= 8 && out.dims[0] == (int64_t)Bl * gsize && out.dims[3] == M &&
                      M % 8 == 0,
                  "moe dispatch all-to-all shape");
@@ -579,8 +587,8 @@ extern "C" int spmd_moe_dispatch_all_to_all(spmd_comm* c, spmd_tensor x, spmd_te
   int32_t* inv = (int32_t*)index_scratch.data;
   SPMD_CUDA_TRY(cudaMemsetAsync(inv, 0xff, inv_bytes, s));   // -1: empty slot
   const int64_t tokens = (int64_t)Bl * S;
-  moe_inverse_kernel<<<grid_for(tokens, 256), 256, 0, s>>>(
-      (const int32_t*)expert.data, (const int32_t*)slot.data, inv, tokens, S, E, C);
+  moe_inverse_kernel<<<grid_for(tokens * K, 256), 256, 0, s>>>(
+      (const int32_t*)expert.data, (const int32_t*)slot.data, inv, tokens * K, K, S, E, C);
   if ((rc = launched(s))) return rc;
   DispatchPush a;
   memset(&a, 0, sizeof(a));

@@ -158,9 +158,16 @@ class NcclComm:
 
 @dataclasses.dataclass
 class Routing:
-    """A one-hot GShard routing on the device, per local partition:
-    ``expert``/``slot`` s32 ``[P, B, S]`` (slot >= capacity = dropped) and
-    ``gate`` f32 ``[P, B, S]`` -- what ``spmd_moe_route`` produces."""
+    """A GShard top-k routing on the device, per local partition:
+    ``expert``/``slot`` s32 and ``gate`` f32 of shape ``[P, B, S]`` (top-1)
+    or ``[P, B, S, k]`` (slot >= capacity = dropped) -- what
+    ``spmd_moe_route`` produces (rule pinned by ``moe.route_topk``).
+
+    Declaring a routing PINS the dispatch / combine masks: the executor's
+    dispatch and combine run as gathers driven by these tensors and never
+    read the mask parameters' values, so the masks passed to ``run`` must be
+    the ones this routing produces (``spmd_moe_masks``).  The tensors are read
+    at every run, so updating them in place re-routes the next step."""
     expert: object
     slot: object
     gate: object
@@ -737,10 +744,12 @@ class Executor:
     def _plan_moe_routing(self):
         """GShard dispatch / combine einsums over a declared one-hot routing
         (``routing[param_index] = Routing(expert, slot, gate)``) run as the
-        gather kernels of moe.cu.  For a one-hot mask each output element has
-        a single nonzero term, so the result is bit-identical to the dense
-        Dot (reference tests/test_acceptance.py:326-349 consumes the same
-        masks through a Dot)."""
+        gather kernels of moe.cu.  Every dispatch output element has a single
+        nonzero term and every combine output at most k (one per choice), so
+        the results equal the dense Dot as the reference evaluates it
+        (tests/test_acceptance.py:326-349 consumes the same masks through a
+        Dot; f64 accumulation, simulator.py:258-275).  The mask parameters'
+        values are not read (see ``Routing``)."""
         pidx = {p.id: p.attrs["index"] for p in self.params}
         for ins in self.graph.instructions:
             if ins.opcode != Op.DOT or ins.shape.dtype != DType.BF16:

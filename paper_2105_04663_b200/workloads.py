@@ -214,10 +214,12 @@ def transformer_flops(B, S, M, N, D, H) -> float:
     return 2.0 * T * (3 * M * N * D + N * D * M + 2 * M * H) + 4.0 * B * N * S * S * D
 
 
-def moe_layer(n, E=8, B=8, S=8, C=4, M=8, H=16, dtype=DType.F32, seed=0, with_inputs=True):
+def moe_layer(n, E=8, B=8, S=8, C=4, M=8, H=16, dtype=DType.F32, seed=0, with_inputs=True,
+              top_k=1):
     """C3: GShard MoE FFN; dispatch [B,S,E,C] one-hot x tokens -> [B,E,C,M]
     (B-sharded) -> transpose [E,B,C,M] (E-sharded, all-to-all) -> expert FFN ->
-    all-to-all back -> combine."""
+    all-to-all back -> combine.  Inputs: masks of a GShard top-``top_k``
+    routing of seeded gating logits (moe.route_masks)."""
     mesh = DeviceMesh.default(n)
     ms = lambda r, m: mesh_split(r, mesh, m)
     b = GraphBuilder("moe", mesh)
@@ -242,9 +244,9 @@ def moe_layer(n, E=8, B=8, S=8, C=4, M=8, H=16, dtype=DType.F32, seed=0, with_in
     if not with_inputs:
         return g, None
     rng = np.random.default_rng(seed)
-    from .moe import route_top1
+    from .moe import route_masks
     logits = rng.standard_normal((B, S, E)).astype(np.float32)
-    disp_v, comb_v = route_top1(logits, C)
+    disp_v, comb_v = route_masks(logits, C, top_k)
     ins = [rng.standard_normal((B, S, M)).astype(np.float32), disp_v, comb_v,
            (rng.standard_normal((E, M, H)) / np.sqrt(M)).astype(np.float32),
            (rng.standard_normal((E, H, M)) / np.sqrt(H)).astype(np.float32)]
