@@ -86,7 +86,8 @@ int spmd_set_sm_limit(int sms);
  * 3: 256x512 wide pairs), "gemm_group", "gemm_raster_n", "gemm_hint",
  * "gemm_store_hint", "gemm_epi_direct", "scatter_epi_direct", "attn_mode",
  * "attn_kt", "conv_mode", "conv_wres", "conv_taps", "nccl_max_ctas",
- * "peer_timeout_ms", "peer_serial_pulls".  Unknown names -> SPMD_ERR_INVALID.
+ * "peer_timeout_ms", "peer_serial_pulls", "f32_dot_tc" (large f32 Dots as 3xTF32
+ * tensor-core GEMMs, default 1).  Unknown names -> SPMD_ERR_INVALID.
  * Not part of the reference interface (tuning and variant selection). */
 int spmd_set_option(const char* name, int64_t value);
 int spmd_get_option(const char* name, int64_t* value);
@@ -142,8 +143,11 @@ int spmd_reduce(spmd_tensor in, spmd_tensor init, spmd_tensor out, const int32_t
 
 /* ---- contractions (simulator.py:258-277) ------------------------------------
  * Generalised dot: out[batch, lhs_free, rhs_free] = sum_k lhs*rhs.  BF16 runs on
- * tcgen05 tensor cores (fp32 TMEM accumulation); F32 accumulates in fp64 and
- * integers in int64 (as the reference), rounding once. */
+ * tcgen05 tensor cores (fp32 TMEM accumulation).  F32: Dots with M, N >= 256
+ * and K >= 64 run as a 3xTF32 tcgen05 GEMM (hi*hi + hi*lo + lo*hi, ~1e-6
+ * normwise vs the f64 reference; option "f32_dot_tc" = 0 disables), smaller
+ * ones accumulate in fp64; integers accumulate in int64 (as the reference),
+ * rounding once. */
 typedef struct {
   int32_t n_batch, n_contract;
   int32_t lhs_batch[SPMD_MAX_RANK], rhs_batch[SPMD_MAX_RANK];

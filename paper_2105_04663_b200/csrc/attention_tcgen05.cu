@@ -871,6 +871,415 @@ static int launch_attention_2sm(const CUtensorMap& mq, const CUtensorMap& mk,
   return launched(s);
 }
 
+// ---------------------------------------------------------------------------
+// Persistent CTA-pair attention with two softmax warps per TMEM lane quarter
+// (the default for D = 128 / 256).  Same data split as the 128-key-tile
+// kernel above (pair = 256 query rows; K tiles split by keys, V tiles by
+// head-dim halves), but:
+//  * persistent: one CTA pair per two SMs walks (q-tile, head, batch) work
+//    items; the Q buffer is released as soon as the item's last S MMA has
+//    completed, so the next item's Q load and first S MMAs overlap this
+//    item's last softmax and its epilogue (the O accumulator is only
+//    overwritten by the next item's first PV MMA, which waits for P, i.e.
+//    after the epilogue has read O out of TMEM);
+//  * 8 softmax warps (2 per SMSP): warp (quarter q, half h) owns rows
+//    32q..32q+31 and keys 64h..64h+63 of every 128-key tile, so two
+//    independent instruction streams per SMSP hide the MUFU / TMEM-load /
+//    barrier latencies the 4-warp kernel stalls on (ncu r1: 29% tensor-pipe
+//    active).  The two warps of a quarter exchange their partial row max
+//    through shared memory (named barrier per quarter pair) so both scale
+//    their half of P by the same running max; row sums stay per warp and are
+//    added in the epilogue;
+//  * row max / row sum as 8-way trees, scale folded into one FFMA per exp2;
+//  * epilogue staged through the P buffer (two 64-column SW128 atoms per
+//    round, one per warp half) and written with TMA bulk-tensor stores.
+// Warps: 0 TMA producer, 1 MMA issuer (leader CTA), 2 TMEM allocator,
+// 3 idle, 4-11 softmax / correction / epilogue.
+// ---------------------------------------------------------------------------
+template <int D>
+struct AttnPSmem {
+  static constexpr int Q_BYTES = 128 * D * 2;           // own 128 rows
+  static constexpr int K_HALF = 64 * D * 2;             // own 64 keys x D
+  static constexpr int V_HALF = 128 * (D / 2) * 2;      // 128 keys x own D/2
+  static constexpr int STAGES = D >= 256 ? 2 : 4;       // per ring (K ring, V ring)
+  static constexpr int P_BYTES = 128 * 128 * 2;         // 128 rows x 128 keys
+  static constexpr int K_OFF = Q_BYTES;
+  static constexpr int V_OFF = K_OFF + STAGES * K_HALF;
+  static constexpr int P_OFF = V_OFF + STAGES * V_HALF;
+  static constexpr int RED_OFF = P_OFF + P_BYTES;       // [2 halves][128 rows] f32
+  static constexpr int BAR_OFF = RED_OFF + 1024;
+  static constexpr int TOTAL = BAR_OFF + 256 + 1024;
+};
+
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n.reg .pred P;\nelect.sync _|P, 0xffffffff;\nselp.u32 %0, 1, 0, P;\n}" : "=r"(pred));
+  return pred != 0;
+}
+
+__device__ __forceinline__ void named_sync(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+template <int D>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
+    attention_tcgen05_2sm_pp(const __grid_constant__ CUtensorMap map_q,
+                             const __grid_constant__ CUtensorMap map_k,
+                             const __grid_constant__ CUtensorMap map_v,
+                             const __grid_constant__ CUtensorMap map_o, AttnShape g) {
+  typedef AttnPSmem<D> L;
+  constexpr int DC = D / 64, NS = L::STAGES, KT = 128, DH = D / 2;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint64_t* bars = (uint64_t*)(smem + L::BAR_OFF);
+  uint64_t* q_full = bars + 0;             // leader, 1 arrival + tx
+  uint64_t* q_empty = bars + 1;            // both (multicast commit)
+  // K and V have separate rings: a K slot frees when its S MMA completes, a
+  // V slot when its PV MMA does, so K(j+2) streams in while PV(j) still runs
+  // (one shared K+V ring of 2 slots waited for PV(j) -- ncu: the MMA warp
+  // starved on the loads 27% of the time)
+  uint64_t* k_full = bars + 2;             // [NS] leader
+  uint64_t* k_empty = k_full + NS;         // [NS] both (multicast)
+  uint64_t* v_full = k_empty + NS;         // [NS] leader
+  uint64_t* v_empty = v_full + NS;         // [NS] both (multicast)
+  uint64_t* s_full = v_empty + NS;         // [2] both (multicast)
+  uint64_t* s_free = s_full + 2;           // [2] leader, 16 arrivals
+  uint64_t* p_full = s_free + 2;           // [1] leader, 16 arrivals
+  uint64_t* pv_done = p_full + 1;          // [1] both (multicast)
+  uint32_t* tmem_slot = (uint32_t*)(pv_done + 1);
+  float* red = (float*)(smem + L::RED_OFF);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_rank();
+  const bool leader = rank == 0;
+  const int nSt = (g.S + 255) / 256;
+  const int items = nSt * g.N * g.Bp;
+  const int cl = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+  const int nT = (g.T + KT - 1) / KT;
+
+  if (threadIdx.x == 0) {
+    mbar_init(q_full, 1);
+    mbar_init(q_empty, 1);
+    for (int i = 0; i < NS; ++i) {
+      mbar_init(&k_full[i], 1);
+      mbar_init(&k_empty[i], 1);
+      mbar_init(&v_full[i], 1);
+      mbar_init(&v_empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&s_full[i], 1);
+      mbar_init(&s_free[i], 16);
+    }
+    mbar_init(p_full, 16);
+    mbar_init(pv_done, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                     smem_u32(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t O_COL = 0, S_COL = 256;
+  uint8_t* sq = smem;
+  uint8_t* sk = smem + L::K_OFF;
+  uint8_t* sv = smem + L::V_OFF;
+  uint8_t* sp = smem + L::P_OFF;
+
+  if (warp == 0 && lane == 0) {
+    // ---------------- TMA producer ----------------
+    // Flat order over this pair's tiles t: V(t-1), [Q(item) at an item's
+    // first tile], K(t) -- K runs one tile ahead of V, matching the MMA
+    // order S(t+1) before PV(t).
+    const int my_items = cl < items ? (items - cl + ncl - 1) / ncl : 0;
+    const int G = my_items * nT;
+    int item = cl, j = 0, it = 0;          // coordinates of tile t
+    int pn = 0, pb = 0, pj = 0;            // coordinates of tile t - 1
+    for (int t = 0; t <= G; ++t) {
+      if (t >= 1) {
+        const int slot = (t - 1) % NS;
+        mbar_wait(&v_empty[slot], (((t - 1) / NS) & 1) ^ 1);
+        uint8_t* vv = sv + slot * L::V_HALF;
+        if (leader) mbar_expect_tx(&v_full[slot], 2 * L::V_HALF);
+#pragma unroll
+        for (int c = 0; c < DC / 2; ++c)
+#pragma unroll
+          for (int h = 0; h < 2; ++h)
+            tma_load_4d_2sm(vv + c * 16384 + h * 8192, &map_v, &v_full[slot],
+                            (int)rank * DH + c * 64, pj * KT + h * 64, pn, pb);
+      }
+      if (t == G) break;
+      const int st = item % nSt, rest = item / nSt;
+      const int n = rest % g.N, b = rest / g.N;
+      if (j == 0) {
+        if (it > 0) mbar_wait(q_empty, (it - 1) & 1);
+        if (leader) mbar_expect_tx(q_full, 2 * L::Q_BYTES);
+#pragma unroll
+        for (int c = 0; c < DC; ++c)
+          tma_load_4d_2sm(sq + c * 16384, &map_q, q_full, c * 64, st * 256 + (int)rank * 128, n,
+                          b);
+      }
+      const int slot = t % NS;
+      mbar_wait(&k_empty[slot], ((t / NS) & 1) ^ 1);
+      uint8_t* kk = sk + slot * L::K_HALF;
+      if (leader) mbar_expect_tx(&k_full[slot], 2 * L::K_HALF);
+#pragma unroll
+      for (int c = 0; c < DC; ++c)
+        tma_load_4d_2sm(kk + c * 8192, &map_k, &k_full[slot], c * 64, j * KT + (int)rank * 64, n,
+                        b);
+      pn = n, pb = b, pj = j;
+      if (++j == nT) {
+        j = 0;
+        item += ncl;
+        ++it;
+      }
+    }
+  } else if (warp == 1 && leader) {
+    // ---------------- MMA issuer (flat sequence over this pair's tiles) ----------------
+    // The whole warp runs the loop (uniform control flow, so descriptors and
+    // counters live in uniform registers); one elected lane issues.  An S
+    // MMA here is only 64 tensor cycles, so per-MMA issue cost matters:
+    // descriptors are precomputed and advanced by constants.
+    const uint32_t idesc_s = make_idesc(256, KT, 0, 0);
+    const uint32_t idesc_o = make_idesc(256, D, 0, 1);
+    const int my_items = cl < items ? (items - cl + ncl - 1) / ncl : 0;
+    const int G = my_items * nT;
+    const uint64_t qd0 = make_desc(smem_u32(sq), 16, 1024);
+    const uint64_t kd0 = make_desc(smem_u32(sk), 16, 1024);
+    const uint64_t vd0 = make_desc(smem_u32(sv), 16384, 1024);
+    const uint64_t pd0 = make_desc(smem_u32(sp), 16, 1024);
+    constexpr uint32_t K16 = L::K_HALF >> 4, V16 = L::V_HALF >> 4;
+    // S side counters (tile gs = 0, 1, ...) and PV side counters
+    int s_j = 0, s_slot = 0, s_item = 0;
+    uint32_t s_kvph = 0;
+    int p_j = 0, p_slot = 0;
+    uint32_t p_vph = 0;
+    auto issue_s = [&](int gi) {
+      const int sb = gi & 1;
+      if (s_j == 0) mbar_wait(q_full, s_item & 1);
+      mbar_wait(&k_full[s_slot], s_kvph);
+      if (gi >= 2) mbar_wait(&s_free[sb], ((gi >> 1) - 1) & 1);
+      tc_fence_after();
+      if (elect_one()) {
+        const uint64_t kd = kd0 + (uint64_t)(s_slot * K16);
+#pragma unroll
+        for (int c = 0; c < DC; ++c)
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            tc_mma_2sm(tmem + S_COL + sb * KT, qd0 + (uint64_t)((c * 16384 + k * 32) >> 4),
+                       kd + (uint64_t)((c * 8192 + k * 32) >> 4), idesc_s, (c | k) != 0);
+        tc_commit_2sm_mc(&s_full[sb]);
+        tc_commit_2sm_mc(&k_empty[s_slot]);
+        if (s_j == nT - 1) tc_commit_2sm_mc(q_empty);   // Q smem free once these finish
+      }
+      __syncwarp();
+      if (++s_slot == NS) {
+        s_slot = 0;
+        s_kvph ^= 1;
+      }
+      if (++s_j == nT) {
+        s_j = 0;
+        ++s_item;
+      }
+    };
+    auto issue_pv = [&](int gi) {
+      mbar_wait(&v_full[p_slot], p_vph);
+      mbar_wait(p_full, gi & 1);
+      tc_fence_after();
+      if (elect_one()) {
+        const uint64_t vd = vd0 + (uint64_t)(p_slot * V16);
+#pragma unroll
+        for (int k = 0; k < KT / 16; ++k)
+          tc_mma_2sm(tmem + O_COL, pd0 + (uint64_t)(((k >> 2) * 16384 + (k & 3) * 32) >> 4),
+                     vd + (uint64_t)((k * 2048) >> 4), idesc_o, (p_j | k) != 0);
+        tc_commit_2sm_mc(pv_done);
+        tc_commit_2sm_mc(&v_empty[p_slot]);
+      }
+      __syncwarp();
+      if (++p_slot == NS) {
+        p_slot = 0;
+        p_vph ^= 1;
+      }
+      if (++p_j == nT) p_j = 0;
+    };
+    if (G > 0) {
+      issue_s(0);
+      for (int gi = 1; gi < G; ++gi) {
+        issue_s(gi);
+        issue_pv(gi - 1);
+      }
+      issue_pv(G - 1);
+    }
+  } else if (warp >= 4) {
+    // ---------------- softmax / correction / epilogue ----------------
+    const int qd = warp & 3, h = (warp - 4) >> 2;
+    const int row = qd * 32 + lane;
+    const uint32_t lane_base = (uint32_t)(qd * 32) << 16;
+    const int pair_bar = 1 + qd;          // the two warps of this lane quarter
+    float* my_red = red + h * 128 + row;
+    const float* other_red = red + (1 - h) * 128 + row;
+    const float c = g.scale_log2e;        // > 0 (host-checked)
+    int gt = 0;
+    for (int item = cl; item < items; item += ncl) {
+      const int st = item % nSt, rest = item / nSt;
+      const int n = rest % g.N, b = rest / g.N;
+      const int row0 = st * 256 + (int)rank * 128;
+      float m = -INFINITY, l = 0.f;       // running max (raw logits), this half's row sum
+      for (int j = 0; j < nT; ++j, ++gt) {
+        const int sb = gt & 1;
+        mbar_wait(&s_full[sb], (gt >> 1) & 1);
+        tc_fence_after();
+        float s[64];
+        {
+          uint32_t r[2][32];
+          tmem_ld32_nowait(tmem + lane_base + S_COL + sb * KT + h * 64, r[0]);
+          tmem_ld32_nowait(tmem + lane_base + S_COL + sb * KT + h * 64 + 32, r[1]);
+          tmem_wait_ld();
+#pragma unroll
+          for (int q = 0; q < 2; ++q)
+#pragma unroll
+            for (int i = 0; i < 32; ++i) s[q * 32 + i] = __uint_as_float(r[q][i]);
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_leader(&s_free[sb]);
+        const int valid = g.T - j * KT - h * 64;
+        if (valid < 64) {
+#pragma unroll
+          for (int i = 0; i < 64; ++i)
+            if (i >= valid) s[i] = -INFINITY;
+        }
+        float t8[8];
+#pragma unroll
+        for (int a = 0; a < 8; ++a) t8[a] = s[a];
+#pragma unroll
+        for (int i = 8; i < 64; ++i) t8[i & 7] = fmaxf(t8[i & 7], s[i]);
+        float pm = fmaxf(fmaxf(fmaxf(t8[0], t8[1]), fmaxf(t8[2], t8[3])),
+                         fmaxf(fmaxf(t8[4], t8[5]), fmaxf(t8[6], t8[7])));
+        *my_red = pm;
+        named_sync(pair_bar, 64);
+        const float mx = fmaxf(pm, *other_red);
+        named_sync(pair_bar, 64);          // red is rewritten next tile
+        float alpha = 1.f;
+        bool resc = false;
+        if (m == -INFINITY) {
+          m = mx;
+        } else if ((mx - m) * c > 8.f) {    // rescale only when the max grows by > 2^8
+          alpha = ex2((m - mx) * c);
+          m = mx;
+          resc = true;
+        }
+        const float nmc = m == -INFINITY ? 0.f : -m * c;
+#pragma unroll
+        for (int i = 0; i < 64; ++i) s[i] = ex2(fmaf(s[i], c, nmc));
+#pragma unroll
+        for (int a = 0; a < 8; ++a) t8[a] = s[a];
+#pragma unroll
+        for (int i = 8; i < 64; ++i) t8[i & 7] += s[i];
+        l = l * alpha + (((t8[0] + t8[1]) + (t8[2] + t8[3])) + ((t8[4] + t8[5]) + (t8[6] + t8[7])));
+        // P is single-buffered and O may need rescaling: PV(gt-1) must be done
+        if (gt >= 1) mbar_wait(pv_done, (gt - 1) & 1);
+        if (j > 0 && __any_sync(0xffffffffu, resc)) {
+          tc_fence_after();
+#pragma unroll 1
+          for (int cc = 0; cc < DH; cc += 32) {
+            uint32_t o[32];
+            tmem_ld32(tmem + lane_base + O_COL + h * DH + cc, o);
+#pragma unroll
+            for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
+            tmem_st32(tmem + lane_base + O_COL + h * DH + cc, o);
+          }
+          asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        }
+        uint8_t* prow = sp + h * 16384 + row * 128;   // SW128 atom h = keys 64h..64h+63
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          uint4 v;
+          __nv_bfloat162* hv = reinterpret_cast<__nv_bfloat162*>(&v);
+#pragma unroll
+          for (int t = 0; t < 4; ++t)
+            hv[t] = __floats2bfloat162_rn(s[q * 8 + 2 * t], s[q * 8 + 2 * t + 1]);
+          *reinterpret_cast<uint4*>(prow + ((q ^ (row & 7)) << 4)) = v;
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_leader(p_full);
+      }
+      // ---- epilogue: O / l -> bf16 -> P buffer (SW128 atoms) -> TMA store ----
+      mbar_wait(pv_done, (gt - 1) & 1);
+      tc_fence_after();
+      *my_red = l;
+      named_sync(pair_bar, 64);
+      const float lt = l + *other_red;
+      named_sync(pair_bar, 64);
+      const float inv = lt > 0.f ? 1.f / lt : 0.f;
+#pragma unroll 1
+      for (int rd = 0; rd < DH / 64; ++rd) {
+        // this warp's 64 columns of the round: h * DH + rd * 64 .. + 63 -> atom h
+        uint8_t* orow = sp + h * 16384 + row * 128;
+#pragma unroll
+        for (int half = 0; half < 2; ++half) {
+          uint32_t o[32];
+          tmem_ld32(tmem + lane_base + O_COL + h * DH + rd * 64 + half * 32, o);
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            uint4 v;
+            __nv_bfloat162* hv = reinterpret_cast<__nv_bfloat162*>(&v);
+#pragma unroll
+            for (int t = 0; t < 4; ++t)
+              hv[t] = __floats2bfloat162_rn(__uint_as_float(o[q * 8 + 2 * t]) * inv,
+                                            __uint_as_float(o[q * 8 + 2 * t + 1]) * inv);
+            *reinterpret_cast<uint4*>(orow + (((half * 4 + q) ^ (row & 7)) << 4)) = v;
+          }
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        named_sync(5, 256);
+        if (warp == 4 && lane == 0) {
+#pragma unroll
+          for (int a = 0; a < 2; ++a)
+            asm volatile(
+                "cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%2, %3, %4, %5}], "
+                "[%1];" ::"l"(reinterpret_cast<uint64_t>(&map_o)),
+                "r"(smem_u32(sp + a * 16384)), "r"(a * DH + rd * 64), "r"(row0), "r"(n), "r"(b)
+                : "memory");
+          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+          asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        }
+        named_sync(5, 256);                // P buffer readable again
+      }
+      tc_fence_before();
+    }
+    if (warp == 4 && lane == 0) bulk_wait_all();
+  }
+  tc_fence_before();
+  cluster_sync();
+  if (warp == 2) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+  }
+}
+
+template <int D>
+static int launch_attention_2sm_pp(const CUtensorMap& mq, const CUtensorMap& mk,
+                                   const CUtensorMap& mv, const CUtensorMap& mo, AttnShape g,
+                                   cudaStream_t s) {
+  typedef AttnPSmem<D> L;
+  static_assert(L::TOTAL <= 232448, "persistent attention smem");
+  static std::atomic<uint64_t> attr_done{0};
+  if (int rc = set_smem_attr((const void*)attention_tcgen05_2sm_pp<D>, L::TOTAL, &attr_done))
+    return rc;
+  const int64_t items = (int64_t)((g.S + 255) / 256) * g.N * g.Bp;
+  const int pairs = sm_budget() / 2;
+  const int64_t clusters = items < pairs ? items : pairs;
+  attention_tcgen05_2sm_pp<D><<<(unsigned)(2 * clusters), 384, L::TOTAL, s>>>(mq, mk, mv, mo, g);
+  return launched(s);
+}
+
 }  // namespace spmd
 
 using namespace spmd;
@@ -908,14 +1317,20 @@ extern "C" int spmd_attention_layout(spmd_tensor q, spmd_tensor k, spmd_tensor v
   const int mode = option(OPT_ATTN_MODE) == 1 ? 1 : 2;
   // key tile: 128 for D=128 (549 vs 469 TF/s at T=1024), 64 for D=256 (equal at
   // T=1024, 993 vs 955 TF/s at T=4096: 3 K/V stages fit) -- profiles/r1_attention_kt.jsonl
-  const int kt_env = (int)option(OPT_ATTN_KT);
-  const int kt = kt_env > 0 ? kt_env : (D == 128 ? 128 : 64);
+  // option attn_kt: 0 = the persistent kernel (default); 64 / 128 = the
+  // round-1 non-persistent kernels with that key tile
+  const int kt = (int)option(OPT_ATTN_KT);
+  if (mode == 2 && D >= 128 && kt == 0 && scale > 0.f) {
+    // persistent CTA pairs, 8 softmax warps, 128-key tiles (default)
+    if (D == 128) return launch_attention_2sm_pp<128>(mq, mk, mv, mo, g, s);
+    return launch_attention_2sm_pp<256>(mq, mk, mv, mo, g, s);
+  }
   if (mode == 2 && D >= 128 && kt == 128) {
     // 128-key tiles: K boxes of 64 rows (mk), V boxes of 64 rows (mv)
     if (D == 128) return launch_attention_2sm_k128<128>(mq, mk, mv, mo, g, s);
     return launch_attention_2sm_k128<256>(mq, mk, mv, mo, g, s);
   }
-  if (mode == 2 && D >= 128) {
+  if (mode == 2 && D >= 128 && kt != 128) {
     CUtensorMap mk2;   // K split by keys: 32-row boxes
     if (encode4(&mk2, k.data, D, T, N, Bp, N * D, D, T * N * D, 32)) {
       if (D == 128) return launch_attention_2sm<128>(mq, mk2, mv, mo, g, s);

@@ -70,6 +70,7 @@ static const OptDef kOpts[OPT_COUNT] = {
     {"nccl_max_ctas", "SPMD_NCCL_MAX_CTAS", 0},
     {"peer_timeout_ms", "SPMD_PEER_TIMEOUT_MS", 20000},
     {"peer_serial_pulls", "SPMD_PEER_SERIAL_PULLS", 0},
+    {"f32_dot_tc", "SPMD_F32_DOT_TC", 1},
 };
 static std::atomic<int64_t> g_opts[OPT_COUNT];
 static std::once_flag g_opts_once;

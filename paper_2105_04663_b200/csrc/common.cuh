@@ -43,6 +43,7 @@ enum Option : int {
   OPT_NCCL_MAX_CTAS,        // NCCL maxCTAs at communicator creation (0: NCCL default)
   OPT_PEER_TIMEOUT_MS,      // peer barrier timeout
   OPT_PEER_SERIAL_PULLS,    // 1: staged gathers pull members one after another
+  OPT_F32_DOT_TC,           // 1: large f32 Dots on the tensor cores (3xTF32)
   OPT_COUNT
 };
 int64_t option(int id);
@@ -72,6 +73,10 @@ struct GemmScatter {
 int dot_tcgen05(const spmd_tensor& lhs, const spmd_tensor& rhs, const spmd_tensor& out,
                 const spmd_dot_dims& dd, int64_t nparts, cudaStream_t s,
                 const GemmScatter* sc = nullptr);
+// Implemented in gemm_tf32x3.cu: large f32 Dots as a 3xTF32 tcgen05 GEMM;
+// SPMD_ERR_UNSUPPORTED for small / untileable ones (SIMT fp64 path then).
+int dot_tf32x3(const spmd_tensor& lhs, const spmd_tensor& rhs, const spmd_tensor& out,
+               const spmd_dot_dims& dd, int64_t nparts, cudaStream_t s);
 
 #define SPMD_CHECK_ARG(cond, msg)                  \
   do {                                             \

@@ -2,7 +2,8 @@
 // 121-154).
 //
 // BF16 dots with a TMA-describable layout go to the tcgen05/TMEM GEMM
-// (gemm_tcgen05.cu).  Everything else -- F32 (fp64 accumulation, one
+// (gemm_tcgen05.cu), large F32 dots to the 3xTF32 tcgen05 GEMM
+// (gemm_tf32x3.cu).  Everything else -- small F32 (fp64 accumulation, one
 // rounding, as the reference's float64 einsum), S32/U32 (int64 accumulation,
 // wrap on the final cast, exact), and odd-layout BF16 -- runs the tiled SIMT
 // kernel below, which addresses operands through arbitrary batch / free /
@@ -211,6 +212,10 @@ extern "C" int spmd_dot(spmd_tensor lhs, spmd_tensor rhs, spmd_tensor out, const
   if (numel(out) * nparts == 0) return SPMD_OK;
   if (lhs.dtype == SPMD_BF16) {
     int rc = dot_tcgen05(lhs, rhs, out, *dd, nparts, s);
+    if (rc != SPMD_ERR_UNSUPPORTED) return rc;
+  }
+  if (lhs.dtype == SPMD_F32) {
+    int rc = dot_tf32x3(lhs, rhs, out, *dd, nparts, s);
     if (rc != SPMD_ERR_UNSUPPORTED) return rc;
   }
   int64_t ls[SPMD_MAX_RANK], rs[SPMD_MAX_RANK];

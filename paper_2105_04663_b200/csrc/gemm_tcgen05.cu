@@ -785,9 +785,12 @@ static int launch_gemm_2sm_wide(const CUtensorMap& ma, const CUtensorMap& mb,
 
 static int gemm_mode() { return (int)option(OPT_GEMM_MODE); }
 
-int dot_tcgen05(const spmd_tensor& lhs, const spmd_tensor& rhs, const spmd_tensor& out,
-                const spmd_dot_dims& dd, int64_t nparts, cudaStream_t s, const GemmScatter* sc) {
-  if (lhs.dtype != SPMD_BF16) return SPMD_ERR_UNSUPPORTED;
+// Dot dimension numbers -> one (batch x M x N x K) GEMM over the operands'
+// own layouts (no transposes): M / N / K each merge into one strided dim,
+// up to 3 batch dims (the partition stack included) become tensor-map dims.
+// Shared by the bf16 kernels and the 3xTF32 f32 kernel (gemm_tf32x3.cu).
+int gemm_layout(const spmd_tensor& lhs, const spmd_tensor& rhs, const spmd_tensor& out,
+                const spmd_dot_dims& dd, int64_t nparts, GemmLayout* L) {
   int64_t ls[SPMD_MAX_RANK], rs[SPMD_MAX_RANK];
   {
     int64_t a = 1;
@@ -832,35 +835,28 @@ int dot_tcgen05(const spmd_tensor& lhs, const spmd_tensor& rhs, const spmd_tenso
     ++nb;
   }
   if (nb > 3) return SPMD_ERR_UNSUPPORTED;
-  if (M.size < 64 || N.size < 64 || K.size < 16) return SPMD_ERR_UNSUPPORTED;
   const int a_mn = M.st == 1 && K.st != 1;
   const int b_mn = N.st == 1 && K2.st != 1 ? 1 : 0;
   if (!a_mn && K.st != 1) return SPMD_ERR_UNSUPPORTED;
   const int b_k = K2.st == 1;
   if (!b_mn && !b_k) return SPMD_ERR_UNSUPPORTED;
 
-  GemmShape g;
-  memset(&g, 0, sizeof(g));
-  g.M = (int)M.size;
-  g.N = (int)N.size;
-  g.K = (int)K.size;
-  g.a_mn = a_mn;
-  g.b_mn = b_mn;
-  g.relu = dd.epilogue == 1;
-  const int group_opt = (int)option(OPT_GEMM_GROUP);   // 0: per-kernel default
-  g.group = group_opt > 0 ? group_opt : 8;
-  g.raster_n = (int)option(OPT_GEMM_RASTER_N);
-  g.hint = (int)option(OPT_GEMM_HINT);
-  g.store_hint = (int)option(OPT_GEMM_STORE_HINT);
+  L->nbatch = nb;
+  L->M = (int)M.size;
+  L->N = (int)N.size;
+  L->K = (int)K.size;
+  L->a_mn = a_mn;
+  L->b_mn = b_mn;
   // tensor-map batch dims: innermost first
-  OperandView va, vb;
+  OperandView& va = L->va;
+  OperandView& vb = L->vb;
   for (int i = 0; i < 3; ++i) {
     int src = nb - 1 - i;   // innermost batch dim first
     va.size[2 + i] = src >= 0 ? lb[src].size : 1;
     va.stride[2 + i] = src >= 0 ? lb[src].st : 1;
     vb.size[2 + i] = src >= 0 ? rb[src].size : 1;
     vb.stride[2 + i] = src >= 0 ? rb[src].st : 1;
-    g.nb[i] = (int)(src >= 0 ? lb[src].size : 1);
+    L->nb[i] = (int)(src >= 0 ? lb[src].size : 1);
   }
   // give unit dims a harmless stride (tensor maps need 16B multiples)
   for (int i = 2; i < 5; ++i) {
@@ -877,6 +873,32 @@ int dot_tcgen05(const spmd_tensor& lhs, const spmd_tensor& rhs, const spmd_tenso
   } else {
     vb.size[0] = N.size, vb.stride[0] = 1, vb.size[1] = K2.size, vb.stride[1] = K2.st;
   }
+  return SPMD_OK;
+}
+
+int dot_tcgen05(const spmd_tensor& lhs, const spmd_tensor& rhs, const spmd_tensor& out,
+                const spmd_dot_dims& dd, int64_t nparts, cudaStream_t s, const GemmScatter* sc) {
+  if (lhs.dtype != SPMD_BF16) return SPMD_ERR_UNSUPPORTED;
+  GemmLayout lay;
+  if (int rc = gemm_layout(lhs, rhs, out, dd, nparts, &lay)) return rc;
+  if (lay.M < 64 || lay.N < 64 || lay.K < 16) return SPMD_ERR_UNSUPPORTED;
+  const int a_mn = lay.a_mn, b_mn = lay.b_mn;
+  const OperandView& va = lay.va;
+  const OperandView& vb = lay.vb;
+  GemmShape g;
+  memset(&g, 0, sizeof(g));
+  g.M = lay.M;
+  g.N = lay.N;
+  g.K = lay.K;
+  g.a_mn = a_mn;
+  g.b_mn = b_mn;
+  g.relu = dd.epilogue == 1;
+  const int group_opt = (int)option(OPT_GEMM_GROUP);   // 0: per-kernel default
+  g.group = group_opt > 0 ? group_opt : 8;
+  g.raster_n = (int)option(OPT_GEMM_RASTER_N);
+  g.hint = (int)option(OPT_GEMM_HINT);
+  g.store_hint = (int)option(OPT_GEMM_STORE_HINT);
+  for (int i = 0; i < 3; ++i) g.nb[i] = lay.nb[i];
   g.out_batch_stride = (int64_t)g.M * g.N;
   CUtensorMap ma, mb, mc;
   ScatterMaps smaps;
@@ -894,10 +916,10 @@ int dot_tcgen05(const spmd_tensor& lhs, const spmd_tensor& rhs, const spmd_tenso
     // split dim = the leading GEMM row dim, whole row chunks per member.
     const int64_t nbat = (int64_t)g.nb[0] * g.nb[1] * g.nb[2];
     // rchunk 0: reduce-scatter on the leading row dim -> M / gsize rows each
-    const int64_t rchunk = sc->rchunk ? sc->rchunk : M.size / (sc->gsize ? sc->gsize : 1);
-    if (M.size < 256 || N.size < 512 || gemm_mode() != 3 ||
+    const int64_t rchunk = sc->rchunk ? sc->rchunk : (int64_t)g.M / (sc->gsize ? sc->gsize : 1);
+    if ((int64_t)g.M < 256 || (int64_t)g.N < 512 || gemm_mode() != 3 ||
         sc->gsize < 1 || sc->gsize > 8 || rchunk % 32 != 0 ||
-        rchunk * sc->gsize != M.size || nbat * sc->gsize != sc->nslots)
+        rchunk * sc->gsize != (int64_t)g.M || nbat * sc->gsize != sc->nslots)
       return SPMD_ERR_UNSUPPORTED;
     g.tma_store = 0;
     g.scatter = 1;
@@ -911,32 +933,32 @@ int dot_tcgen05(const spmd_tensor& lhs, const spmd_tensor& rhs, const spmd_tenso
     g.sc_epoch = sc->epoch;
     g.sc_tma = sc->par_slots >= sc->nslots;
     for (int j = 0; g.sc_tma && j < sc->gsize; ++j)
-      g.sc_tma = encode_store_map(&smaps.m[j], sc->dst[j], N.size, rchunk, N.size,
-                                  sc->par_slots + sc->nslots, rchunk * N.size);
+      g.sc_tma = encode_store_map(&smaps.m[j], sc->dst[j], (int64_t)g.N, rchunk, (int64_t)g.N,
+                                  sc->par_slots + sc->nslots, rchunk * (int64_t)g.N);
     if (!g.sc_tma) return SPMD_ERR_UNSUPPORTED;
   } else if (sc) {
     // Reduce-scatter epilogue: 2-CTA kernel, no batch dims, the scattered
     // dim is the last output dim == the whole GEMM N.
-    if (M.size < 256 || N.size < 256 || nb != 0 || N.size != out.dims[out.rank - 1] ||
-        sc->gsize < 1 || sc->gsize > 8 || N.size % sc->gsize != 0 ||
-        (N.size / sc->gsize) % 32 != 0)
+    if ((int64_t)g.M < 256 || (int64_t)g.N < 256 || lay.nbatch != 0 || (int64_t)g.N != out.dims[out.rank - 1] ||
+        sc->gsize < 1 || sc->gsize > 8 || (int64_t)g.N % sc->gsize != 0 ||
+        ((int64_t)g.N / sc->gsize) % 32 != 0)
       return SPMD_ERR_UNSUPPORTED;
     g.tma_store = 0;
     g.scatter = 1;
     g.sc_g = sc->gsize;
     g.sc_pos = sc->pos;
-    g.sc_chunk = N.size / sc->gsize;
-    g.sc_slot = M.size * g.sc_chunk;
+    g.sc_chunk = (int64_t)g.N / sc->gsize;
+    g.sc_slot = (int64_t)g.M * g.sc_chunk;
     if (sc->par_slots < sc->gsize) return SPMD_ERR_UNSUPPORTED;
     g.sc_par = sc->par_slots;
     for (int j = 0; j < sc->gsize; ++j) g.sc_dst[j] = (bf16*)sc->dst[j];
     g.sc_epoch = sc->epoch;
     g.sc_tma = !option(OPT_SCATTER_EPI_DIRECT);
     for (int j = 0; g.sc_tma && j < sc->gsize; ++j)
-      g.sc_tma = encode_store_map(&smaps.m[j], sc->dst[j], g.sc_chunk, M.size, g.sc_chunk,
+      g.sc_tma = encode_store_map(&smaps.m[j], sc->dst[j], g.sc_chunk, (int64_t)g.M, g.sc_chunk,
                                   sc->par_slots + sc->gsize, g.sc_slot);
   }
-  if (gemm_mode() == 3 && (sc ? g.sc_tma : g.tma_store) && M.size >= 256 && N.size >= 512) {
+  if (gemm_mode() == 3 && (sc ? g.sc_tma : g.tma_store) && (int64_t)g.M >= 256 && (int64_t)g.N >= 512) {
     // wide pair tiles (256 x 512); the store epilogue is TMA-only
     bool okw = a_mn ? encode(&ma, lhs.data, va, 64, BK) : encode(&ma, lhs.data, va, BK, HALF);
     okw = okw && (b_mn ? encode(&mb, rhs.data, vb, 64, BK) : encode(&mb, rhs.data, vb, BK, HALF));
@@ -950,7 +972,7 @@ int dot_tcgen05(const spmd_tensor& lhs, const spmd_tensor& rhs, const spmd_tenso
       return launch_gemm_2sm_wide<4>(ma, mb, mc, g, smaps, s);
     }
   }
-  if ((gemm_mode() >= 2 || sc) && M.size >= 256 && N.size >= 256) {
+  if ((gemm_mode() >= 2 || sc) && (int64_t)g.M >= 256 && (int64_t)g.N >= 256) {
     // 2-CTA path: per-CTA boxes are 128 rows of A and 128 rows of B.
     bool ok2 = a_mn ? encode(&ma, lhs.data, va, 64, BK) : encode(&ma, lhs.data, va, BK, HALF);
     ok2 = ok2 && (b_mn ? encode(&mb, rhs.data, vb, 64, BK) : encode(&mb, rhs.data, vb, BK, HALF));
@@ -960,7 +982,7 @@ int dot_tcgen05(const spmd_tensor& lhs, const spmd_tensor& rhs, const spmd_tenso
     g.tiles = (int64_t)g.mt * g.nt * g.nb[0] * g.nb[1] * g.nb[2];
     return launch_gemm_2sm<6>(ma, mb, mc, (bf16*)out.data, g, smaps, s);
   }
-  const int BNsel = N.size >= 256 ? 256 : 128;
+  const int BNsel = (int64_t)g.N >= 256 ? 256 : 128;
   bool ok = a_mn ? encode(&ma, lhs.data, va, 64, BK) : encode(&ma, lhs.data, va, BK, BM);
   ok = ok && (b_mn ? encode(&mb, rhs.data, vb, 64, BK) : encode(&mb, rhs.data, vb, BK, BNsel));
   if (!ok) return SPMD_ERR_UNSUPPORTED;

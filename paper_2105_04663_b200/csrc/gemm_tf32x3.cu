@@ -1,0 +1,349 @@
+// f32 Dot on the tensor cores: 3xTF32 split GEMM (config C1, the f32 einsum
+// BSM,MH->BSH; reference simulator.py:258-275 evaluates it as a float64
+// einsum rounded once to float32).
+//
+// Every f32 operand x is split into x_hi = tf32(x) (round to nearest) and
+// x_lo = x - x_hi (exact in f32; the tensor core reads it as tf32 again),
+// and the product is accumulated as
+//     A.B ~= A_hi.B_hi + A_hi.B_lo + A_lo.B_hi          (fp32 in TMEM)
+// dropping only A_lo.B_lo (~2^-22 relative).  The products run as
+// tcgen05.mma kind::tf32 (UMMA 256x256x8 per CTA pair); the result matches
+// the f64 reference to ~1e-6 normwise (the test bound is the reference's own
+// default tolerance, 1e-4).  Against the SIMT fp64 path (contract.cu) this is
+// the tensor-core rate: 3 tf32 MMAs per fp32 product at 1.1 PF/s dense.
+//
+// Structure = the 2-CTA bf16 GEMM (gemm_tcgen05.cu) with fp32 elements:
+// 128-byte rows hold 32 K elements, a k-block stages A_hi, A_lo, B_hi, B_lo
+// (16 KB each per CTA), the leader issues 4 K-steps x 3 products; 4
+// epilogue warps per CTA drain their 32 TMEM lanes as fp32 rows.
+// The hi / lo operands are produced by one HBM pass (split_tf32_kernel) into
+// stream-ordered scratch (cudaMallocAsync, graph-capturable).
+#include "tcgen05.cuh"
+
+#include <string.h>
+
+namespace spmd {
+
+constexpr int TBK = 32;                  // fp32 K elements per 128-byte row
+constexpr int TBM = 256, TBN = 256, THALF = 128;
+
+template <int STAGES>
+struct SmemT {
+  static constexpr int OP_BYTES = THALF * TBK * 4;          // 16 KB: one of A_hi/A_lo/B_hi/B_lo
+  static constexpr int STAGE_BYTES = 4 * OP_BYTES;
+  static constexpr int BAR_OFF = STAGES * STAGE_BYTES;
+  static constexpr int TOTAL = BAR_OFF + 256 + 1024;
+};
+
+struct TShape {
+  int M, N, K, a_mn, b_mn;
+  int nb[3];
+  int mt, nt, group;
+  int64_t tiles;
+  float* out;
+  int64_t out_batch;     // elements between batches (M * N)
+};
+
+__device__ __forceinline__ void tc_mma_2sm_tf32(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc,
+                                                uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate));
+}
+
+// Instruction descriptor: kind::tf32, tf32 x tf32 -> f32.
+__host__ __device__ constexpr uint32_t make_idesc_tf32(int M, int N, int a_mn, int b_mn) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)a_mn << 15) | ((uint32_t)b_mn << 16) |
+         ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+
+__device__ __forceinline__ void ttile_coords(const TShape& g, int64_t t, int& b, int& m, int& n) {
+  const int64_t per = (int64_t)g.mt * g.nt;
+  b = (int)(t / per);
+  const int r = (int)(t - (int64_t)b * per);
+  const int G = g.group;
+  const int group = r / (G * g.nt);
+  const int first = group * G;
+  const int gs = g.mt - first < G ? g.mt - first : G;
+  const int rr = r - group * G * g.nt;
+  m = first + rr % gs;
+  n = rr / gs;
+}
+
+__global__ void split_tf32_kernel(const float* __restrict__ x, float* __restrict__ hi,
+                                  float* __restrict__ lo, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const float v = x[i];
+    uint32_t h;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(h) : "f"(v));
+    const float hf = __uint_as_float(h);
+    hi[i] = hf;
+    lo[i] = isfinite(v) ? v - hf : 0.f;
+  }
+}
+
+template <int STAGES>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
+    gemm_f32_3xtf32_2sm(const __grid_constant__ CUtensorMap map_ah,
+                        const __grid_constant__ CUtensorMap map_al,
+                        const __grid_constant__ CUtensorMap map_bh,
+                        const __grid_constant__ CUtensorMap map_bl, TShape g) {
+  typedef SmemT<STAGES> L;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint64_t* full = (uint64_t*)(smem + L::BAR_OFF);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_rank();
+  const bool leader = rank == 0;
+  const int64_t cluster = blockIdx.x >> 1, nclusters = gridDim.x >> 1;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 8);   // 4 epilogue warps x 2 CTAs
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                     smem_u32(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const int kblocks = (g.K + TBK - 1) / TBK;
+
+  if (warp == 0 && lane == 0) {
+    // ---------------- TMA producer (both CTAs) ----------------
+    int s = 0;
+    uint32_t ph = 0;
+    for (int64_t t = cluster; t < g.tiles; t += nclusters) {
+      int b, m, n;
+      ttile_coords(g, t, b, m, n);
+      const int b0 = b % g.nb[0], b1 = (b / g.nb[0]) % g.nb[1], b2 = b / (g.nb[0] * g.nb[1]);
+      const int mrow = m * TBM + rank * THALF, nrow = n * TBN + rank * THALF;
+      for (int kb = 0; kb < kblocks; ++kb) {
+        mbar_wait(&empty[s], ph ^ 1);
+        uint8_t* st = smem + s * L::STAGE_BYTES;
+        if (leader) mbar_expect_tx(&full[s], 2 * L::STAGE_BYTES);
+        const int k0 = kb * TBK;
+        const CUtensorMap* ma[2] = {&map_ah, &map_al};
+        const CUtensorMap* mb[2] = {&map_bh, &map_bl};
+#pragma unroll
+        for (int p = 0; p < 2; ++p) {
+          uint8_t* sa = st + p * L::OP_BYTES;
+          uint8_t* sb = st + (2 + p) * L::OP_BYTES;
+          if (!g.a_mn) {
+            tma_load_5d_2sm(sa, ma[p], &full[s], k0, mrow, b0, b1, b2);
+          } else {
+#pragma unroll
+            for (int c = 0; c < THALF / 32; ++c)
+              tma_load_5d_2sm(sa + c * (TBK * 128), ma[p], &full[s], mrow + c * 32, k0, b0, b1,
+                              b2);
+          }
+          if (!g.b_mn) {
+            tma_load_5d_2sm(sb, mb[p], &full[s], k0, nrow, b0, b1, b2);
+          } else {
+#pragma unroll
+            for (int c = 0; c < THALF / 32; ++c)
+              tma_load_5d_2sm(sb + c * (TBK * 128), mb[p], &full[s], nrow + c * 32, k0, b0, b1,
+                              b2);
+          }
+        }
+        if (++s == STAGES) {
+          s = 0;
+          ph ^= 1;
+        }
+      }
+    }
+  } else if (warp == 1 && leader) {
+    // ---------------- MMA issuer (leader CTA, whole warp, one elected lane) ----------------
+    const uint32_t idesc = make_idesc_tf32(TBM, TBN, g.a_mn, g.b_mn);
+    // K-major: a K-step of 8 fp32 is 32 bytes inside the 128-byte row;
+    // MN-major: a K-step is one 8-row atom (1024 bytes), 32-wide chunks 4 KB apart.
+    const uint32_t a_lbo = g.a_mn ? TBK * 128 : 16, b_lbo = g.b_mn ? TBK * 128 : 16;
+    const uint32_t a_step = g.a_mn ? 1024 : 32, b_step = g.b_mn ? 1024 : 32;
+    int s = 0;
+    uint32_t ph = 0;
+    int acc = 0;
+    uint32_t acc_ph = 0;
+    for (int64_t t = cluster; t < g.tiles; t += nclusters) {
+      mbar_wait(&tempty[acc], acc_ph ^ 1);
+      tc_fence_after();
+      const uint32_t d_tmem = tmem + acc * TBN;
+      for (int kb = 0; kb < kblocks; ++kb) {
+        mbar_wait(&full[s], ph);
+        tc_fence_after();
+        uint32_t pred;
+        asm volatile("{\n.reg .pred P;\nelect.sync _|P, 0xffffffff;\nselp.u32 %0, 1, 0, P;\n}"
+                     : "=r"(pred));
+        if (pred) {
+          const uint32_t st = smem_u32(smem + s * L::STAGE_BYTES);
+          const uint32_t ah = st, al = st + L::OP_BYTES;
+          const uint32_t bh = st + 2 * L::OP_BYTES, bl = st + 3 * L::OP_BYTES;
+#pragma unroll
+          for (int k = 0; k < TBK / 8; ++k) {
+            const uint64_t dah = make_desc(ah + k * a_step, a_lbo, 1024);
+            const uint64_t dal = make_desc(al + k * a_step, a_lbo, 1024);
+            const uint64_t dbh = make_desc(bh + k * b_step, b_lbo, 1024);
+            const uint64_t dbl = make_desc(bl + k * b_step, b_lbo, 1024);
+            // small terms first, then the leading product
+            tc_mma_2sm_tf32(d_tmem, dal, dbh, idesc, (kb | k) != 0);
+            tc_mma_2sm_tf32(d_tmem, dah, dbl, idesc, 1);
+            tc_mma_2sm_tf32(d_tmem, dah, dbh, idesc, 1);
+          }
+          tc_commit_2sm_mc(&empty[s]);
+          if (kb == kblocks - 1) tc_commit_2sm_mc(&tfull[acc]);
+        }
+        __syncwarp();
+        if (++s == STAGES) {
+          s = 0;
+          ph ^= 1;
+        }
+      }
+      if (++acc == 2) {
+        acc = 0;
+        acc_ph ^= 1;
+      }
+    }
+  } else if (warp >= 4) {
+    // ---------------- epilogue: 4 warps per CTA, own TMEM lane quarter ----------------
+    const int ew = warp - 4;
+    int acc = 0;
+    uint32_t acc_ph = 0;
+    for (int64_t t = cluster; t < g.tiles; t += nclusters) {
+      int b, m, n;
+      ttile_coords(g, t, b, m, n);
+      mbar_wait(&tfull[acc], acc_ph);
+      tc_fence_after();
+      const int row = m * TBM + rank * THALF + ew * 32 + lane;
+      float* orow = g.out + (int64_t)b * g.out_batch + (int64_t)row * g.N;
+      const uint32_t tbase = tmem + ((uint32_t)(ew * 32) << 16) + acc * TBN;
+#pragma unroll 1
+      for (int c0 = 0; c0 < TBN; c0 += 32) {
+        uint32_t r[32];
+        tmem_ld32(tbase + c0, r);
+        const int col = n * TBN + c0;
+        if (row < g.M && col < g.N) {
+          if (col + 32 <= g.N && (g.N & 3) == 0) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+              reinterpret_cast<float4*>(orow + col)[j] =
+                  make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]),
+                              __uint_as_float(r[4 * j + 2]), __uint_as_float(r[4 * j + 3]));
+          } else {
+            for (int j = 0; j < 32 && col + j < g.N; ++j) orow[col + j] = __uint_as_float(r[j]);
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_leader(&tempty[acc]);
+      if (++acc == 2) {
+        acc = 0;
+        acc_ph ^= 1;
+      }
+    }
+  }
+  tc_fence_before();
+  cluster_sync();
+  if (warp == 2) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+  }
+}
+
+// 5-D fp32 tensor map over an OperandView (element strides), 128B swizzle.
+static bool encode_f32(CUtensorMap* map, void* base, const OperandView& v, int box_inner,
+                       int box_outer) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn || (reinterpret_cast<uintptr_t>(base) & 15) != 0) return false;
+  cuuint64_t dims[5], strides[4];
+  cuuint32_t box[5] = {(cuuint32_t)box_inner, (cuuint32_t)box_outer, 1, 1, 1};
+  cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+  for (int i = 0; i < 5; ++i) dims[i] = (cuuint64_t)v.size[i];
+  for (int i = 1; i < 5; ++i) {
+    strides[i - 1] = (cuuint64_t)(v.stride[i] * 4);
+    if (strides[i - 1] % 16 != 0 || strides[i - 1] >= ((cuuint64_t)1 << 40)) return false;
+  }
+  return fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 5, base, dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
+         CUDA_SUCCESS;
+}
+
+// f32 Dot -> 3xTF32 tcgen05 GEMM; SPMD_ERR_UNSUPPORTED when the layout or the
+// size does not qualify (the caller then runs the SIMT fp64 kernel).
+int dot_tf32x3(const spmd_tensor& lhs, const spmd_tensor& rhs, const spmd_tensor& out,
+               const spmd_dot_dims& dd, int64_t nparts, cudaStream_t s) {
+  if (lhs.dtype != SPMD_F32 || !option(OPT_F32_DOT_TC) || dd.epilogue != 0)
+    return SPMD_ERR_UNSUPPORTED;
+  GemmLayout lay;
+  if (gemm_layout(lhs, rhs, out, dd, nparts, &lay) != SPMD_OK) return SPMD_ERR_UNSUPPORTED;
+  // small Dots (the parity-sized golden cases) stay on the exact fp64 path
+  if (lay.M < 256 || lay.N < 256 || lay.K < 64) return SPMD_ERR_UNSUPPORTED;
+  const int64_t na = numel(lhs) * nparts, nb = numel(rhs) * nparts;
+  float* scratch = nullptr;
+  if (cudaMallocAsync((void**)&scratch, (size_t)(2 * (na + nb)) * 4, s) != cudaSuccess) {
+    cudaGetLastError();
+    return SPMD_ERR_UNSUPPORTED;
+  }
+  float *ah = scratch, *al = scratch + na, *bh = scratch + 2 * na, *bl = bh + nb;
+  split_tf32_kernel<<<grid_for(na, 256), 256, 0, s>>>((const float*)lhs.data, ah, al, na);
+  if (int rc = launched(s)) return rc;
+  split_tf32_kernel<<<grid_for(nb, 256), 256, 0, s>>>((const float*)rhs.data, bh, bl, nb);
+  if (int rc = launched(s)) return rc;
+  CUtensorMap mah, mal, mbh, mbl;
+  bool ok = lay.a_mn ? encode_f32(&mah, ah, lay.va, 32, TBK) && encode_f32(&mal, al, lay.va, 32, TBK)
+                     : encode_f32(&mah, ah, lay.va, TBK, THALF) &&
+                           encode_f32(&mal, al, lay.va, TBK, THALF);
+  ok = ok && (lay.b_mn ? encode_f32(&mbh, bh, lay.vb, 32, TBK) && encode_f32(&mbl, bl, lay.vb, 32, TBK)
+                       : encode_f32(&mbh, bh, lay.vb, TBK, THALF) &&
+                             encode_f32(&mbl, bl, lay.vb, TBK, THALF));
+  if (!ok) {
+    cudaFreeAsync(scratch, s);
+    return SPMD_ERR_UNSUPPORTED;
+  }
+  TShape g;
+  memset(&g, 0, sizeof(g));
+  g.M = lay.M;
+  g.N = lay.N;
+  g.K = lay.K;
+  g.a_mn = lay.a_mn;
+  g.b_mn = lay.b_mn;
+  for (int i = 0; i < 3; ++i) g.nb[i] = lay.nb[i];
+  g.mt = (g.M + TBM - 1) / TBM;
+  g.nt = (g.N + TBN - 1) / TBN;
+  g.group = 8;
+  g.tiles = (int64_t)g.mt * g.nt * g.nb[0] * g.nb[1] * g.nb[2];
+  g.out = (float*)out.data;
+  g.out_batch = (int64_t)g.M * g.N;
+  typedef SmemT<3> L;
+  static_assert(L::TOTAL <= 232448, "3xTF32 GEMM smem");
+  static std::atomic<uint64_t> attr_done{0};
+  if (int rc = set_smem_attr((const void*)gemm_f32_3xtf32_2sm<3>, L::TOTAL, &attr_done)) return rc;
+  const int sms = sm_budget();
+  const int64_t clusters = g.tiles < sms / 2 ? g.tiles : sms / 2;
+  gemm_f32_3xtf32_2sm<3><<<(unsigned)(2 * clusters), 256, L::TOTAL, s>>>(mah, mal, mbh, mbl, g);
+  int rc = launched(s);
+  cudaFreeAsync(scratch, s);
+  return rc;
+}
+
+}  // namespace spmd

@@ -164,6 +164,17 @@ struct OperandView {
   int64_t stride[5];   // elements; stride[0] must be 1
 };
 
+// GEMM view of a Dot (gemm_tcgen05.cu gemm_layout): element strides of the
+// operands as 5-D tensor-map views (inner, outer, 3 batch dims).
+struct GemmLayout {
+  int M, N, K, a_mn, b_mn;
+  int nbatch;     // batch dims of size > 1 (partition stack included)
+  int nb[3];
+  OperandView va, vb;
+};
+int gemm_layout(const spmd_tensor& lhs, const spmd_tensor& rhs, const spmd_tensor& out,
+                const spmd_dot_dims& dd, int64_t nparts, GemmLayout* L);
+
 inline bool encode(CUtensorMap* map, void* base, const OperandView& v, int box_inner,
                    int box_outer) {
   EncodeTiledFn fn = encode_fn();

@@ -106,3 +106,24 @@ def test_attention_writes_bsnd_layout(D):
                                           torch.cuda.current_stream().cuda_stream), "attention")
     torch.cuda.synchronize()
     assert torch.equal(out, a.permute(0, 1, 3, 2, 4))
+
+
+@pytest.mark.parametrize("kt", [0, 64, 128])
+@pytest.mark.parametrize("B,S,T,N,D", [(4, 1024, 1024, 16, 256), (2, 300, 200, 5, 256),
+                                       (3, 512, 640, 7, 128), (1, 1024, 1000, 40, 128)])
+def test_attention_variants_many_items(kt, B, S, T, N, D):
+    """Every kernel variant (attn_kt 0: the persistent CTA-pair kernel with 8
+    softmax warps, >= 4 work items per CTA pair on the first case; 64 / 128:
+    the round-1 kernels), with partial query / key tiles."""
+    import torch
+    from paper_2105_04663_b200 import _capi as C
+    torch.manual_seed(B * S + T + N + D + kt)
+    q = torch.randn(1, B, S, N, D, device="cuda").bfloat16()
+    k = torch.randn(1, B, T, N, D, device="cuda").bfloat16()
+    v = torch.randn(1, B, T, N, D, device="cuda").bfloat16()
+    scale = 1.0 / D ** 0.5
+    with C.option("attn_kt", kt):
+        out = _attn(q, k, v, scale=scale)[0].float()
+    ref = _ref(q[0], k[0], v[0], scale)
+    err = (out - ref).abs().max().item() / max(1.0, ref.abs().max().item())
+    assert err < 1e-2, err
