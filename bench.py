@@ -41,6 +41,7 @@ if os.environ.get("SPMD_BENCH_MESH"):   # e.g. "1x4": override the (X=data, Y=mo
     MESHES[_x * _y] = (_x, _y)
 PAPER = dict(B=16, S=1024, M=8192, N=128, D=256, H=65536)
 SPEC_BF16_TFLOPS = 2250.0
+TF32_SPEC_TFLOPS = 1100.0      # B200_PROFILING.md dense tf32
 
 
 def _peaks():
@@ -186,13 +187,14 @@ def run_reference(args):
     return 0
 
 
-def _rand_like_shard(shape, device, scale, seed):
+def _rand_like_shard(shape, device, scale, seed, nparts=1):
     import torch
+    from paper_2105_04663_b200.executor import torch_dtype
     gen = torch.Generator(device=device)
     gen.manual_seed(seed)
-    t = torch.randn((1,) + tuple(shape.dims), generator=gen, device=device,
+    t = torch.randn((nparts,) + tuple(shape.dims), generator=gen, device=device,
                     dtype=torch.float32)
-    return (t * scale).to(torch.bfloat16)
+    return (t * scale).to(torch_dtype(shape.dtype))
 
 
 def _traffic_for(top, prog):
@@ -219,6 +221,7 @@ def _traffic_for(top, prog):
     return None
 
 
+C1 = dict(B=16, S=1024, M=8192, H=8192)
 C3 = dict(E=8, B=64, S=512, C=160, M=4096, H=16384, k=2)
 C4 = dict(N=8, H=1024, W=1024, C=128, layers=4)
 
@@ -250,6 +253,13 @@ def _workload(config, world, scale=1.0, mesh=None):
         return mesh, g, dims, transformer_train_flops(**dims), fan, \
             "C2 training step (forward + backward layer, weight gradients reduce-scattered), " \
             "paper dims"
+    if config == "c1":
+        from paper_2105_04663_b200.workloads import einsum_c1
+        d = dict(C1)
+        g, _ = einsum_c1((2, 2), dtype=DType.F32, with_inputs=False, **d)
+        flops = 2.0 * d["B"] * d["S"] * d["M"] * d["H"]
+        return (2, 2), g, d, flops, {"w": d["M"]}, \
+            "C1 2-D sharded einsum BSM,MH->BSH f32 (3xTF32 tensor cores), 2x2 mesh"
     if config == "c3":
         d = dict(C3)
         g, _ = moe_layer(world, dtype=DType.BF16, with_inputs=False,
@@ -305,7 +315,11 @@ class _Run:
         self.mesh, g, self.dims, self.flops, fan, self.wdesc = _workload(config, world, scale,
                                                                           mesh)
         ann, _ = propagate(g)
-        self.prog = partition(ann, world, plan="fast")
+        # C1's 2x2 mesh is simulated on one GPU (4 partitions, loopback
+        # collectives) unless 4 ranks run it
+        parts = self.mesh[0] * self.mesh[1] if config == "c1" else world
+        self.nparts = parts // world
+        self.prog = partition(ann, parts, plan="fast")
         # Synthetic local shards, generated on the device (weights ~ N(0, 1/fan_in);
         # MoE dispatch/combine masks from the on-device router).
         src_params = {p.attrs["index"]: p.id for p in ann.parameters}
@@ -313,7 +327,8 @@ class _Run:
         for p in self.prog.graph.parameters:
             name = src_params[p.attrs["index"]]
             self.inputs.append(_rand_like_shard(p.shape, dev, 1.0 / np.sqrt(fan.get(name, 1)),
-                                                seed=1000 * rank + p.attrs["index"]))
+                                                seed=1000 * rank + p.attrs["index"],
+                                                nparts=self.nparts))
         self.routing = None
         if config == "c3":
             # On-device GShard top-2 router -> masks (the reference graph's
@@ -324,8 +339,9 @@ class _Run:
                                     k=self.dims["k"]))
             idx = {name: p.attrs["index"] for p, name in zip(self.prog.graph.parameters, names)}
             self.routing = {idx["dispatch"]: r, idx["combine"]: r}
-        self.ex = Executor(self.prog, nparts=1, device=dev, comm=comm, partition_base=rank,
-                           fuse=True, overlap=(world > 1 and overlap), routing=self.routing)
+        self.ex = Executor(self.prog, nparts=self.nparts, device=dev, comm=comm,
+                           partition_base=rank * self.nparts, fuse=True,
+                           overlap=(world > 1 and overlap), routing=self.routing)
 
 
 def _time_steps(run, steps, warmup, eager, barrier, world, dev):
@@ -392,7 +408,7 @@ def _top_kernel(run, dev, burst, sustained, peak_src, reps=20):
     FLOPs), launched alone `reps` times on the stream the executor uses,
     timed with CUDA events: the roofline entry of the JSON line."""
     import torch
-    from paper_2105_04663_b200.ir import Op
+    from paper_2105_04663_b200.ir import DType, Op
     prog, ex = run.prog, run.ex
     stream = torch.cuda.current_stream(dev)
     dots = [i for i in prog.graph.instructions if i.opcode in (Op.DOT, Op.CONVOLUTION)]
@@ -414,8 +430,17 @@ def _top_kernel(run, dev, burst, sustained, peak_src, reps=20):
     k1.record(stream)
     torch.cuda.synchronize()
     kms = k0.elapsed_time(k1) / reps
-    fl = _dot_flops(prog, top)
+    fl = _dot_flops(prog, top) * run.nparts
     achieved = fl / (kms * 1e-3) / 1e12
+    if top.shape.dtype == DType.F32:
+        # 3xTF32: three tf32 MMAs per f32 product; no measured tf32 peak in
+        # MEASURED_PEAKS.json -> B200_PROFILING.md's dense tf32 spec
+        peak = TF32_SPEC_TFLOPS / 3.0
+        return {"bound": "tensor", "kernel": "gemm_f32_3xtf32_2sm (%s)" % top.id,
+                "achieved": achieved, "peak": peak, "unit": "TFLOP/s (f32 products)",
+                "frac": achieved / peak,
+                "peak_source": "spec dense tf32 1.1 PF/s / 3 MMAs per f32 product",
+                "ms_per_launch": kms, "flops_per_launch": fl}
     return {"bound": "tensor", "kernel": "%s (%s)" % (kname, top.id), "achieved": achieved,
             "peak": burst, "unit": "TFLOP/s", "frac": achieved / burst,
             "peak_source": peak_src + " burst (kernel timed alone)",
@@ -434,10 +459,16 @@ def _extra_config(config, world, rank, dev, comm, barrier, steps, warmup, burst,
     tf = run.flops / (ms * 1e-3) / 1e12
     roof = _top_kernel(run, dev, burst, sustained, peak_src, reps=10)
     out = {"workload": run.wdesc, "dims": run.dims, "mesh": list(run.mesh), "ms_per_step": ms,
-           "tflops": tf, "tflops_per_gpu": tf / world,
-           "mfu_vs_spec_2250": tf / world / SPEC_BF16_TFLOPS, "gpu_launches_per_step": launches,
+           "tflops": tf, "tflops_per_gpu": tf / world, "gpu_launches_per_step": launches,
            "roofline": {k: roof[k] for k in ("kernel", "achieved", "peak", "unit", "frac",
-                                             "frac_sustained", "ms_per_launch")}}
+                                             "frac_sustained", "ms_per_launch", "peak_source")
+                        if k in roof}}
+    if config == "c1":
+        out["dtype"] = "f32 (3xTF32 split on tcgen05 kind::tf32)"
+        if run.nparts > 1:
+            out["mesh_simulated_on_one_gpu"] = True
+    else:
+        out["mfu_vs_spec_2250"] = tf / world / SPEC_BF16_TFLOPS
     del run, graph, outs
     torch.cuda.empty_cache()
     return out
@@ -554,7 +585,7 @@ def _reshard(world, rank, dev, comm, barrier):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--config", default="c2", choices=["c2", "c2train", "c3", "c4"])
+    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c2train", "c3", "c4"])
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
@@ -615,9 +646,9 @@ def main():
     # and step k-1's download run on copy streams under step k's compute.
     e2e = None
     if not args.no_e2e:
-        x_host = torch.empty(inputs[0].shape, dtype=torch.bfloat16, pin_memory=True)
+        x_host = torch.empty(inputs[0].shape, dtype=inputs[0].dtype, pin_memory=True)
         x_host.copy_(inputs[0].cpu())
-        out_host = [torch.empty(out[0].shape, dtype=torch.bfloat16, pin_memory=True)
+        out_host = [torch.empty(out[0].shape, dtype=out[0].dtype, pin_memory=True)
                     for _ in range(2)]
         if args.eager:
             dev_inputs = list(inputs)
@@ -675,8 +706,8 @@ def main():
         ems = float(t.item())
         e2e = {"value": flops / (ems * 1e-3) / 1e12, "unit": "TFLOP/s",
                "ms_per_step": ems,
-               "h2d_bytes_per_step": int(x_host.numel() * 2 * world),
-               "d2h_bytes_per_step": int(out_host[0].numel() * 2 * world),
+               "h2d_bytes_per_step": int(x_host.numel() * x_host.element_size() * world),
+               "d2h_bytes_per_step": int(out_host[0].numel() * out_host[0].element_size() * world),
                "copies": "serial" if args.eager else
                "pipelined (2 captured steps, copy streams)"}
         if not args.eager:
@@ -705,7 +736,7 @@ def main():
                                       "tflops": alt.flops / (ams * 1e-3) / 1e12}
             del alt, ag, ao
             torch.cuda.empty_cache()
-        for cfg in ("c3", "c4"):
+        for cfg in ("c1", "c3", "c4") if world in (1, 4) else ("c3", "c4"):
             configs[cfg] = _extra_config(cfg, world, rank, dev, comm, barrier,
                                          max(5, args.steps // 2), args.warmup, burst, sustained,
                                          peak_src)
@@ -729,7 +760,7 @@ def main():
     if rank == 0:
         per_gpu = value / world
         cfg = {"workload": wdesc, "model_dims": dims, "mesh": list(mesh),
-               "parallelism": ("dp%dxmp%d" % mesh) if args.config in ("c2", "c2train") else
+               "parallelism": ("dp%dxmp%d" % mesh) if args.config in ("c1", "c2", "c2train") else
                ("expert%d" % world if args.config == "c3" else "spatial%d" % world),
                "plan": "fast", "l2": "inputs larger than L2 (weights+activations)",
                "collectives_per_step": stats["counts"]}
@@ -744,7 +775,8 @@ def main():
             "value": value, "unit": "TFLOP/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-            "dtype": "bf16", "data": "synthetic", "config": cfg,
+            "dtype": "f32" if args.config == "c1" else "bf16", "data": "synthetic",
+            "config": cfg,
             "tflops_per_gpu": per_gpu,
             "mfu": {"vs_spec_2250": per_gpu / SPEC_BF16_TFLOPS,
                     "vs_measured_sustained": per_gpu / sustained},

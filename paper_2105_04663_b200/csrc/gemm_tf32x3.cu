@@ -12,6 +12,8 @@
 // default tolerance, 1e-4).  Against the SIMT fp64 path (contract.cu) this is
 // the tensor-core rate: 3 tf32 MMAs per fp32 product at 1.1 PF/s dense.
 //
+// Both operands are fed K-major: an MN-major operand (the C1 weight w[M,H]
+// contracting M) is transposed by the split pass.
 // Structure = the 2-CTA bf16 GEMM (gemm_tcgen05.cu) with fp32 elements:
 // 128-byte rows hold 32 K elements, a k-block stages A_hi, A_lo, B_hi, B_lo
 // (16 KB each per CTA), the leader issues 4 K-steps x 3 products; 4
@@ -36,7 +38,7 @@ struct SmemT {
 };
 
 struct TShape {
-  int M, N, K, a_mn, b_mn;
+  int M, N, K;
   int nb[3];
   int mt, nt, group;
   int64_t tiles;
@@ -85,6 +87,81 @@ __global__ void split_tf32_kernel(const float* __restrict__ x, float* __restrict
     hi[i] = hf;
     lo[i] = isfinite(v) ? v - hf : 0.f;
   }
+}
+
+// MN-major operand (MN contiguous, K strided) -> K-major dense hi / lo copies
+// [batch][MN][K] through a 32x32 shared-memory tile (coalesced both ways).
+// Measured: with the MN-major SW128 descriptors that serve the bf16 GEMM, a
+// kind::tf32 MMA returned an all-zero result for an MN-major B (K-major B
+// exact), so both operands are fed K-major.
+struct SplitView {
+  int64_t mn, k, st_k;              // MN extent (stride 1), K extent and stride
+  int64_t bsize[3], bstride[3];     // batch dims (innermost first)
+};
+
+__global__ void split_tf32_transpose_kernel(const float* __restrict__ x, SplitView v,
+                                            float* __restrict__ hi, float* __restrict__ lo) {
+  __shared__ float tile[32][33];
+  const int64_t b = blockIdx.z;
+  int64_t boff = 0, r = b;
+  for (int i = 0; i < 3; ++i) {
+    boff += (r % v.bsize[i]) * v.bstride[i];
+    r /= v.bsize[i];
+  }
+  const int64_t mn0 = (int64_t)blockIdx.x * 32, k0 = (int64_t)blockIdx.y * 32;
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int64_t k = k0 + i, mn = mn0 + threadIdx.x;
+    tile[i][threadIdx.x] = (k < v.k && mn < v.mn) ? x[boff + k * v.st_k + mn] : 0.f;
+  }
+  __syncthreads();
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int64_t mn = mn0 + i, k = k0 + threadIdx.x;
+    if (mn < v.mn && k < v.k) {
+      const float val = tile[threadIdx.x][i];
+      uint32_t h;
+      asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(h) : "f"(val));
+      const float hf = __uint_as_float(h);
+      const int64_t o = (b * v.mn + mn) * v.k + k;
+      hi[o] = hf;
+      lo[o] = isfinite(val) ? val - hf : 0.f;
+    }
+  }
+}
+
+// Split one operand into hi / lo K-major copies at `hi`, `lo` (each sized for
+// the operand's own layout when it is K-major, else dense [batch][MN][K]) and
+// rewrite `view` to describe them.
+static int split_operand(const float* src, int64_t n, OperandView* view, int mn_major, float* hi,
+                         float* lo, cudaStream_t s) {
+  if (!mn_major) {
+    split_tf32_kernel<<<grid_for(n, 256), 256, 0, s>>>(src, hi, lo, n);
+    return launched(s);
+  }
+  SplitView v;
+  v.mn = view->size[0];
+  v.k = view->size[1];
+  v.st_k = view->stride[1];
+  int64_t nb = 1;
+  for (int i = 0; i < 3; ++i) {
+    v.bsize[i] = view->size[2 + i];
+    v.bstride[i] = view->stride[2 + i];
+    nb *= v.bsize[i];
+  }
+  if (nb > 65535) return SPMD_ERR_UNSUPPORTED;
+  dim3 grid((unsigned)((v.mn + 31) / 32), (unsigned)((v.k + 31) / 32), (unsigned)nb);
+  split_tf32_transpose_kernel<<<grid, dim3(32, 8), 0, s>>>(src, v, hi, lo);
+  // K-major dense view [b2][b1][b0][MN][K]
+  OperandView kv;
+  kv.size[0] = v.k, kv.stride[0] = 1;
+  kv.size[1] = v.mn, kv.stride[1] = v.k;
+  int64_t st = v.mn * v.k;
+  for (int i = 0; i < 3; ++i) {
+    kv.size[2 + i] = v.bsize[i];
+    kv.stride[2 + i] = v.bsize[i] > 1 ? st : 8;
+    st *= v.bsize[i];
+  }
+  *view = kv;
+  return launched(s);
 }
 
 template <int STAGES>
@@ -147,24 +224,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
         const CUtensorMap* mb[2] = {&map_bh, &map_bl};
 #pragma unroll
         for (int p = 0; p < 2; ++p) {
-          uint8_t* sa = st + p * L::OP_BYTES;
-          uint8_t* sb = st + (2 + p) * L::OP_BYTES;
-          if (!g.a_mn) {
-            tma_load_5d_2sm(sa, ma[p], &full[s], k0, mrow, b0, b1, b2);
-          } else {
-#pragma unroll
-            for (int c = 0; c < THALF / 32; ++c)
-              tma_load_5d_2sm(sa + c * (TBK * 128), ma[p], &full[s], mrow + c * 32, k0, b0, b1,
-                              b2);
-          }
-          if (!g.b_mn) {
-            tma_load_5d_2sm(sb, mb[p], &full[s], k0, nrow, b0, b1, b2);
-          } else {
-#pragma unroll
-            for (int c = 0; c < THALF / 32; ++c)
-              tma_load_5d_2sm(sb + c * (TBK * 128), mb[p], &full[s], nrow + c * 32, k0, b0, b1,
-                              b2);
-          }
+          tma_load_5d_2sm(st + p * L::OP_BYTES, ma[p], &full[s], k0, mrow, b0, b1, b2);
+          tma_load_5d_2sm(st + (2 + p) * L::OP_BYTES, mb[p], &full[s], k0, nrow, b0, b1, b2);
         }
         if (++s == STAGES) {
           s = 0;
@@ -174,11 +235,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
     }
   } else if (warp == 1 && leader) {
     // ---------------- MMA issuer (leader CTA, whole warp, one elected lane) ----------------
-    const uint32_t idesc = make_idesc_tf32(TBM, TBN, g.a_mn, g.b_mn);
-    // K-major: a K-step of 8 fp32 is 32 bytes inside the 128-byte row;
-    // MN-major: a K-step is one 8-row atom (1024 bytes), 32-wide chunks 4 KB apart.
-    const uint32_t a_lbo = g.a_mn ? TBK * 128 : 16, b_lbo = g.b_mn ? TBK * 128 : 16;
-    const uint32_t a_step = g.a_mn ? 1024 : 32, b_step = g.b_mn ? 1024 : 32;
+    const uint32_t idesc = make_idesc_tf32(TBM, TBN, 0, 0);
+    // K-major: a K-step of 8 fp32 is 32 bytes inside the 128-byte row
     int s = 0;
     uint32_t ph = 0;
     int acc = 0;
@@ -199,10 +257,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
           const uint32_t bh = st + 2 * L::OP_BYTES, bl = st + 3 * L::OP_BYTES;
 #pragma unroll
           for (int k = 0; k < TBK / 8; ++k) {
-            const uint64_t dah = make_desc(ah + k * a_step, a_lbo, 1024);
-            const uint64_t dal = make_desc(al + k * a_step, a_lbo, 1024);
-            const uint64_t dbh = make_desc(bh + k * b_step, b_lbo, 1024);
-            const uint64_t dbl = make_desc(bl + k * b_step, b_lbo, 1024);
+            const uint64_t dah = make_desc(ah + k * 32, 16, 1024);
+            const uint64_t dal = make_desc(al + k * 32, 16, 1024);
+            const uint64_t dbh = make_desc(bh + k * 32, 16, 1024);
+            const uint64_t dbl = make_desc(bl + k * 32, 16, 1024);
             // small terms first, then the leading product
             tc_mma_2sm_tf32(d_tmem, dal, dbh, idesc, (kb | k) != 0);
             tc_mma_2sm_tf32(d_tmem, dah, dbl, idesc, 1);
@@ -304,18 +362,19 @@ int dot_tf32x3(const spmd_tensor& lhs, const spmd_tensor& rhs, const spmd_tensor
     cudaGetLastError();
     return SPMD_ERR_UNSUPPORTED;
   }
+  // an MN-major operand's dense transpose is never larger than its buffer
+  // (the view covers a sub-box of it), so the same scratch sizes hold
   float *ah = scratch, *al = scratch + na, *bh = scratch + 2 * na, *bl = bh + nb;
-  split_tf32_kernel<<<grid_for(na, 256), 256, 0, s>>>((const float*)lhs.data, ah, al, na);
-  if (int rc = launched(s)) return rc;
-  split_tf32_kernel<<<grid_for(nb, 256), 256, 0, s>>>((const float*)rhs.data, bh, bl, nb);
-  if (int rc = launched(s)) return rc;
+  OperandView va = lay.va, vb = lay.vb;
+  int rc = split_operand((const float*)lhs.data, na, &va, lay.a_mn, ah, al, s);
+  if (rc == SPMD_OK) rc = split_operand((const float*)rhs.data, nb, &vb, lay.b_mn, bh, bl, s);
+  if (rc != SPMD_OK) {
+    cudaFreeAsync(scratch, s);
+    return rc;
+  }
   CUtensorMap mah, mal, mbh, mbl;
-  bool ok = lay.a_mn ? encode_f32(&mah, ah, lay.va, 32, TBK) && encode_f32(&mal, al, lay.va, 32, TBK)
-                     : encode_f32(&mah, ah, lay.va, TBK, THALF) &&
-                           encode_f32(&mal, al, lay.va, TBK, THALF);
-  ok = ok && (lay.b_mn ? encode_f32(&mbh, bh, lay.vb, 32, TBK) && encode_f32(&mbl, bl, lay.vb, 32, TBK)
-                       : encode_f32(&mbh, bh, lay.vb, TBK, THALF) &&
-                             encode_f32(&mbl, bl, lay.vb, TBK, THALF));
+  bool ok = encode_f32(&mah, ah, va, TBK, THALF) && encode_f32(&mal, al, va, TBK, THALF) &&
+            encode_f32(&mbh, bh, vb, TBK, THALF) && encode_f32(&mbl, bl, vb, TBK, THALF);
   if (!ok) {
     cudaFreeAsync(scratch, s);
     return SPMD_ERR_UNSUPPORTED;
@@ -325,8 +384,6 @@ int dot_tf32x3(const spmd_tensor& lhs, const spmd_tensor& rhs, const spmd_tensor
   g.M = lay.M;
   g.N = lay.N;
   g.K = lay.K;
-  g.a_mn = lay.a_mn;
-  g.b_mn = lay.b_mn;
   for (int i = 0; i < 3; ++i) g.nb[i] = lay.nb[i];
   g.mt = (g.M + TBM - 1) / TBM;
   g.nt = (g.N + TBN - 1) / TBN;
@@ -341,7 +398,7 @@ int dot_tf32x3(const spmd_tensor& lhs, const spmd_tensor& rhs, const spmd_tensor
   const int sms = sm_budget();
   const int64_t clusters = g.tiles < sms / 2 ? g.tiles : sms / 2;
   gemm_f32_3xtf32_2sm<3><<<(unsigned)(2 * clusters), 256, L::TOTAL, s>>>(mah, mal, mbh, mbl, g);
-  int rc = launched(s);
+  rc = launched(s);
   cudaFreeAsync(scratch, s);
   return rc;
 }
