@@ -354,6 +354,26 @@ int spmd_peer_collective_permute(spmd_comm* comm, spmd_tensor in, spmd_tensor ou
 int spmd_peer_slice_collective_permute(spmd_comm* comm, spmd_tensor src, int axis, int64_t start,
                                        spmd_tensor out, const int32_t* pairs, int npairs,
                                        int64_t heap_offset, int channel, void* stream);
+/* Push-based all-to-all (reference simulator.py:382-387 semantics: piece j
+ * of `in` split along split_dim goes to group member j, concatenated along
+ * concat_dim in group order): every rank writes each member's piece straight
+ * into that member's landing zone at heap data offset `heap_offset` (>= 3 *
+ * fused_half, 256-aligned, same on every rank, sized numel(out)), already in
+ * the member's output layout -- no pack / unpack pass -- then one barrier on
+ * `channel`.  out.data == NULL: the zone (spmd_comm_heap_ptr) is the result,
+ * valid until the zone is reused after a later barrier; else it is copied
+ * to out. */
+int spmd_peer_all_to_all(spmd_comm* comm, spmd_tensor in, spmd_tensor out, int split_dim,
+                         int concat_dim, const int32_t* groups, int ngroups, int gsize,
+                         int64_t heap_offset, int channel, void* stream);
+/* Push-based all-gather along `dim` (simulator.py:353-359 piece order): every
+ * rank writes its shard into slot `pos` of every member's landing zone, one
+ * barrier; out.data == NULL as for spmd_peer_all_to_all. */
+int spmd_peer_push_all_gather(spmd_comm* comm, spmd_tensor in, spmd_tensor out, int dim,
+                              const int32_t* groups, int ngroups, int gsize,
+                              int64_t heap_offset, int channel, void* stream);
+/* Device address of this rank's heap data at `offset` (NULL if outside). */
+void* spmd_comm_heap_ptr(spmd_comm* comm, int64_t offset);
 /* Device-side barrier of all ranks on `channel` (epoch flags in the peer
  * heap control page; graph-replay safe; times out into the device error
  * word). */

@@ -126,6 +126,9 @@ _SIGNATURES = {
     "spmd_peer_all_gather": ([_P, _T, _T, _I, _PI32, _I, _I, _I64, _I, _I, _P], _I),
     "spmd_peer_stage": ([_P, _T, _I64, _P], _I),
     "spmd_peer_barrier": ([_P, _I, _P], _I),
+    "spmd_peer_all_to_all": ([_P, _T, _T, _I, _I, _PI32, _I, _I, _I64, _I, _P], _I),
+    "spmd_peer_push_all_gather": ([_P, _T, _T, _I, _PI32, _I, _I, _I64, _I, _P], _I),
+    "spmd_comm_heap_ptr": ([_P, _I64], ctypes.c_void_p),
     "spmd_peer_collective_permute": ([_P, _T, _T, _PI32, _I, _I64, _I, _P], _I),
     "spmd_peer_slice_collective_permute": ([_P, _T, _I, _I64, _T, _PI32, _I, _I64, _I, _P], _I),
 }

@@ -255,6 +255,9 @@ struct CopyArgs {
   int64_t dyn_max[SPMD_MAX_RANK];
   int64_t dyn_mul[SPMD_MAX_RANK];
   int dyn_on_dst;
+  // 1: every thread ends with __threadfence_system() -- the destination is a
+  // peer's heap (NVLink stores) and a peer barrier follows (peer.cu)
+  int fence_sys;
 };
 
 int launch_copy(const void* src, void* dst, int dtype, CopyArgs a, int64_t nparts,

@@ -71,6 +71,7 @@ __global__ void strided_copy_kernel(const T* __restrict__ src, T* __restrict__ d
       *reinterpret_cast<uint4*>(dst + d0) = *reinterpret_cast<const uint4*>(src + so);
     }
   }
+  if (a.fence_sys) __threadfence_system();
 }
 
 // dst[dbase + p*dpart + i] = src[sbase + p*spart] for i < n, 16 bytes per store.

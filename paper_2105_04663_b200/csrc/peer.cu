@@ -609,6 +609,124 @@ extern "C" int spmd_moe_dispatch_all_to_all(spmd_comm* c, spmd_tensor x, spmd_te
   return launched(s);
 }
 
+// ---------------------------------------------------------------------------
+// Push-based all-to-all / all-gather through the peer heap (C5 resharding,
+// reference simulator.py:353-359, 382-387; partitioner.py:283-318).  Every
+// rank writes each member's piece of its input straight into that member's
+// landing zone at `heap_offset` -- in the member's final output layout, so
+// the strided send side needs no pack pass -- with 16-byte NVLink stores
+// (the affine copy kernel with a trailing system fence), then one barrier.
+// The landing zone then IS the output: the executor hands out a view of it
+// (`out.data == NULL`), or it is copied to `out`.  Zones stay stable until a
+// later barrier (the executor closes each step with one).
+// ---------------------------------------------------------------------------
+static void row_major(const spmd_tensor& t, int64_t* st) {
+  int64_t acc = 1;
+  for (int k = t.rank - 1; k >= 0; --k) {
+    st[k] = acc;
+    acc *= t.dims[k];
+  }
+}
+
+// in: this rank's operand; zone_shape: one member's output shape.  piece j of
+// `in` (index j of `sdim` split G ways, or the whole input when sdim < 0)
+// lands at index pos of `cdim` (split G ways) in member j's zone.
+static int peer_push(spmd_comm* c, const spmd_tensor& in, const spmd_tensor& zone_shape,
+                     int sdim, int cdim, const int32_t* members, int gsize, int pos,
+                     int64_t heap_offset, cudaStream_t s) {
+  int64_t ist[SPMD_MAX_RANK], ost[SPMD_MAX_RANK];
+  row_major(in, ist);
+  row_major(zone_shape, ost);
+  spmd_tensor piece = in;
+  if (sdim >= 0) piece.dims[sdim] /= gsize;
+  for (int j = 0; j < gsize; ++j) {
+    CopyArgs a;
+    memset(&a, 0, sizeof(a));
+    a.rank = in.rank;
+    for (int k = 0; k < in.rank; ++k) {
+      a.shape[k] = piece.dims[k];
+      a.sst[k] = ist[k];
+      a.dst[k] = ost[k];
+    }
+    a.sbase = sdim >= 0 ? (int64_t)j * piece.dims[sdim] * ist[sdim] : 0;
+    a.dbase = (int64_t)pos * piece.dims[cdim] * ost[cdim];
+    a.fence_sys = 1;
+    char* zone = c->peer[members[j]] + CTRL_BYTES + heap_offset;
+    if (int rc = launch_copy(in.data, zone, in.dtype, a, 1, s)) return rc;
+  }
+  return SPMD_OK;
+}
+
+static int finish_zone(spmd_comm* c, const spmd_tensor& out, int64_t heap_offset, int64_t bytes,
+                       cudaStream_t s) {
+  if (out.data && bytes)
+    SPMD_CUDA_TRY(cudaMemcpyAsync(out.data, c->heap + CTRL_BYTES + heap_offset, bytes,
+                                  cudaMemcpyDeviceToDevice, s));
+  return SPMD_OK;
+}
+
+extern "C" int spmd_peer_all_to_all(spmd_comm* c, spmd_tensor in, spmd_tensor out,
+                                    int split_dim, int concat_dim, const int32_t* groups,
+                                    int ngroups, int gsize, int64_t heap_offset, int channel,
+                                    void* stream) {
+  SPMD_CHECK_ARG(c && in.dtype == out.dtype && in.rank == out.rank && split_dim >= 0 &&
+                     split_dim < in.rank && concat_dim >= 0 && concat_dim < in.rank &&
+                     in.dims[split_dim] % gsize == 0,
+                 "peer all-to-all arguments");
+  SPMD_CHECK_ARG(channel >= 0 && channel < NUM_CHANNELS, "peer barrier channel");
+  if (!c->heap) {
+    set_error("peer heap not enabled (spmd_comm_enable_peer)");
+    return SPMD_ERR_INVALID;
+  }
+  int grp, pos;
+  int rc = group_position(c, groups, ngroups, gsize, &grp, &pos);
+  if (rc) return rc;
+  for (int k = 0; k < in.rank; ++k) {
+    int64_t want = in.dims[k];
+    if (k == split_dim) want /= gsize;
+    if (k == concat_dim) want *= gsize;
+    SPMD_CHECK_ARG(out.dims[k] == want, "peer all-to-all output shape");
+  }
+  const int64_t bytes = numel(out) * elem_size(out.dtype);
+  if ((rc = check_slot(c, heap_offset, bytes, "peer all-to-all landing"))) return rc;
+  cudaStream_t s = as_stream(stream);
+  if ((rc = peer_push(c, in, out, split_dim, concat_dim, groups + grp * gsize, gsize, pos,
+                      heap_offset, s)))
+    return rc;
+  if ((rc = peer_barrier(c, channel, s))) return rc;
+  return finish_zone(c, out, heap_offset, bytes, s);
+}
+
+extern "C" int spmd_peer_push_all_gather(spmd_comm* c, spmd_tensor in, spmd_tensor out, int dim,
+                                         const int32_t* groups, int ngroups, int gsize,
+                                         int64_t heap_offset, int channel, void* stream) {
+  SPMD_CHECK_ARG(c && in.dtype == out.dtype && in.rank == out.rank && dim >= 0 &&
+                     dim < in.rank && out.dims[dim] == in.dims[dim] * gsize,
+                 "peer all-gather arguments");
+  SPMD_CHECK_ARG(channel >= 0 && channel < NUM_CHANNELS, "peer barrier channel");
+  if (!c->heap) {
+    set_error("peer heap not enabled (spmd_comm_enable_peer)");
+    return SPMD_ERR_INVALID;
+  }
+  int grp, pos;
+  int rc = group_position(c, groups, ngroups, gsize, &grp, &pos);
+  if (rc) return rc;
+  const int64_t bytes = numel(out) * elem_size(out.dtype);
+  if ((rc = check_slot(c, heap_offset, bytes, "peer all-gather landing"))) return rc;
+  cudaStream_t s = as_stream(stream);
+  if ((rc = peer_push(c, in, out, -1, dim, groups + grp * gsize, gsize, pos, heap_offset, s)))
+    return rc;
+  if ((rc = peer_barrier(c, channel, s))) return rc;
+  return finish_zone(c, out, heap_offset, bytes, s);
+}
+
+// Device address of this rank's heap data at `offset` (the landing zone the
+// push collectives leave their result in).
+extern "C" void* spmd_comm_heap_ptr(spmd_comm* c, int64_t offset) {
+  if (!c || !c->heap || offset < 0 || offset > c->heap_bytes) return nullptr;
+  return c->heap + CTRL_BYTES + offset;
+}
+
 // Collective-permute through the peer heap (reference simulator.py:372-390:
 // each target receives its source's buffer, non-targets are zero-filled):
 // the sender's copy engine writes `in` straight into the target's heap slot

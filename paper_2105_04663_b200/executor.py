@@ -131,6 +131,23 @@ class NcclComm:
                                                     self._ws.numel()),
                     "spmd_comm_set_workspace")
 
+    def heap_view(self, offset: int, dims, dtype, device):
+        """A tensor aliasing this rank's peer heap at data offset ``offset``
+        (the landing zone of a push collective); valid while the heap lives
+        and until the zone is rewritten (after a later barrier)."""
+        torch = _torch()
+        lib = C.lib()
+        ptr = lib.spmd_comm_heap_ptr(self.handle, int(offset))
+        if not ptr:
+            raise EvalError(f"peer heap offset {offset} outside the heap")
+        nbytes = int(np.prod(dims)) * dtype.itemsize
+
+        class _Zone:
+            __cuda_array_interface__ = {"shape": (nbytes,), "typestr": "|u1",
+                                        "data": (int(ptr), False), "version": 3}
+        raw = torch.as_tensor(_Zone(), device=device)
+        return raw.view(torch_dtype(dtype)).view(tuple(dims))
+
     def reserve_fused(self, half_bytes: int) -> int:
         """Grow the fused-op landing zone to >= ``half_bytes`` per parity
         (peer.cu fused_parity); returns the communicator's H.  Every rank
@@ -232,6 +249,7 @@ class Executor:
         else:
             self._peer_ag = {}
             self._peer_cp = {}
+            self._peer_a2a = {}
             self._peer_bytes_used = 0
             self._fused_half = 0
         self._peer_engine = self._plan_peer_engines()
@@ -438,6 +456,17 @@ class Executor:
                     self._peer_ag[ins.id] = off
                     nb = self._shape(ins.operands[0]).num_elements * ins.shape.dtype.itemsize
                     off += (nb + 4095) // 4096 * 4096
+        # all-to-alls (C5 resharding; MoE exchanges not fused into a GEMM):
+        # one landing zone each, holding this rank's output -- every member
+        # pushes its piece there (spmd_peer_all_to_all), and the zone is the
+        # value the consumers read
+        self._peer_a2a = {}
+        if os.environ.get("SPMD_PEER_A2A", "1") != "0":
+            for ins in self.graph.instructions:
+                if ins.opcode == Op.ALL_TO_ALL and ins.id not in self._fused_skip and \
+                        ins.id not in self._fused:
+                    self._peer_a2a[ins.id] = off
+                    off += (ins.shape.nbytes + 4095) // 4096 * 4096
         # collective-permutes (halo exchanges, pipeline shifts): one landing
         # slot each, written by the source rank's copy engine
         self._peer_cp = {}
@@ -1638,6 +1667,32 @@ class Executor:
                                         groups, ng, gs, s)
             C.check(rc, op.value)
             return out
+
+        if op == Op.ALL_TO_ALL and comm is not None and ins.id in self._peer_a2a:
+            off = self._peer_a2a[ins.id]
+            keep_copy = ins.id in self.graph.outputs   # outputs outlive the step
+            zone = {}
+
+            def run_peer(env, s):
+                x = desc(env[a], ash)
+                if keep_copy:
+                    out = self._alloc(shp)
+                    y = desc(out, shp)
+                else:
+                    # the heap may have been re-allocated (grown) since the
+                    # last run: re-derive the view from its current address
+                    ptr = lib.spmd_comm_heap_ptr(comm.handle, off)
+                    if zone.get("ptr") != ptr:
+                        zone["ptr"] = ptr
+                        zone["t"] = comm.heap_view(off, (1,) + shp.dims, shp.dtype, self.device)
+                    out = zone["t"]
+                    y = desc(out, shp)
+                    y.data = None                # the landing zone is the result
+                C.check(lib.spmd_peer_all_to_all(comm.handle, x, y, at["split_dim"],
+                                                 at["concat_dim"], groups, ng, gs, off,
+                                                 self._lane_of.get(s, 0), s), "all-to-all")
+                return out
+            return run_peer
         return run
 
     def _constant(self, ins: Instruction):
@@ -1671,7 +1726,7 @@ class Executor:
                 for vid in step.frees:
                     if vid not in keep:
                         env.pop(vid, None)
-            if self._peer_cp:
+            if self._peer_cp or self._peer_a2a:
                 # landing slots are read before any rank writes them again
                 C.check(self.lib.spmd_peer_barrier(self.comm.handle, 0, s), "peer_barrier")
         else:
@@ -1763,7 +1818,7 @@ class Executor:
                     env.pop(vid, None)
         for st in self.comm_streams:
             compute.wait_stream(st)               # join
-        if self._staged or self._act_staged or self._peer_cp:
+        if self._staged or self._act_staged or self._peer_cp or self._peer_a2a:
             # every member has read the staged / landing slots before any
             # rank writes them again
             st = self.comm_streams[0]

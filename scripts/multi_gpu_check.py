@@ -53,7 +53,7 @@ def main():
     dist.init_process_group("nccl", device_id=dev)
     comm = NcclComm.from_torch_distributed()
     results = {}
-    cases = [c for kind in ("named", "random") for c in G.cases(kind)
+    cases = [c for kind in G.KINDS for c in G.cases(kind)
              if c.get("num_devices") == world and "spmd" in c]
     for case in cases:
         prog_graph = G.program(case)

@@ -405,8 +405,8 @@ def conv_stack(mesh_dims, mapping, N, H, W, C, layers, rng):
     return g, ins
 
 
-def uneven_case(n0, n1, kind, rng):
-    mesh = R.DeviceMesh.default(8)
+def uneven_case(n0, n1, kind, rng, parts=8):
+    mesh = R.DeviceMesh.default(parts)
     b = R.GraphBuilder("uneven", mesh)
     x = b.parameter(R.Shape((n0, n1)), sharding=R.mesh_split(2, mesh, [0, -1]), id="x")
     if kind == "a2a":
@@ -618,7 +618,35 @@ def train_cases(arrays):
     return out
 
 
+def c5_world_cases(arrays):
+    """C5 at world sizes 2 and 4 (the 8-device C5 cases cannot run one
+    process per GPU on a 2/4-GPU box): uneven dims 1000/1001/999 (and a
+    1001-wide second dim) over 2 and 4 shards, each reshard kind."""
+    rng = np.random.default_rng(5005)
+    out = []
+    for parts in (2, 4):
+        for n0, n1 in ((1000, 16), (1001, 16), (999, 16), (16, 1001)):
+            for kind in ("a2a", "repl", "reduce_max", "reduce_sum"):
+                g, ins = uneven_case(n0, n1, kind, rng, parts=parts)
+                out.append(run_case(f"c5w{parts}_{kind}_{n0}x{n1}", g, ins, parts, arrays))
+    return out
+
+
+def write_c5w():
+    arrays = {}
+    cases = c5_world_cases(arrays)
+    with gzip.open(os.path.join(HERE, "c5w.json.gz"), "wt") as f:
+        json.dump(cases, f, sort_keys=True)
+    buf = io.BytesIO()
+    np.savez_compressed(buf, **arrays)
+    with open(os.path.join(HERE, "c5w_arrays.npz"), "wb") as f:
+        f.write(buf.getvalue())
+    print("c5w cases:", len(cases), "arrays:", len(arrays))
+
+
 def main():
+    if "--only" in sys.argv and sys.argv[sys.argv.index("--only") + 1] == "c5w":
+        return write_c5w()
     arrays = {}
     rand = []
     for seed in range(240):
@@ -640,6 +668,7 @@ def main():
     with open(os.path.join(HERE, "arrays.npz"), "wb") as f:
         f.write(buf.getvalue())
     print("cases:", len(rand), len(named), "arrays:", len(arrays))
+    write_c5w()
 
 
 if __name__ == "__main__":

@@ -21,11 +21,17 @@ def cases(kind: str):
 
 @functools.lru_cache(None)
 def arrays():
-    return dict(np.load(os.path.join(HERE, "arrays.npz")))
+    out = dict(np.load(os.path.join(HERE, "arrays.npz")))
+    out.update(np.load(os.path.join(HERE, "c5w_arrays.npz")))   # C5 over 2 / 4 shards
+    return out
+
+
+# case kinds holding reference-run graphs, programs and outputs
+KINDS = ("named", "random", "c5w")
 
 
 def case_by_name(name):
-    for kind in ("named", "random"):
+    for kind in KINDS:
         for c in cases(kind):
             if c["name"] == name:
                 return c

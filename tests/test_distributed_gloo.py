@@ -18,11 +18,16 @@ import numpy as np
 import pytest
 import torch.multiprocessing as mp
 
+# C5 (uneven dims over 2 / 4 shards): every reshard kind crosses the process
+# boundary, including the fast plan's padded all-to-all for 1001 / 999
+C5W_2 = ["c5w2_%s_%s" % (k, d) for k in ("a2a", "repl", "reduce_max", "reduce_sum")
+         for d in ("1000x16", "1001x16", "999x16", "16x1001")]
+C5W_4 = [n.replace("c5w2", "c5w4") for n in C5W_2]
 CASES_2 = ["priority_fig4", "acc5_reshape", "shift_8_1_0_2", "c2_1x2", "c3_moe_2",
-           "c4_conv_2"]
+           "c4_conv_2"] + C5W_2
 CASES_4 = ["c1_8x16x32x24", "ffw_final", "ffw_attempt", "acc7_moe", "c3_moe_4", "c4_conv_4",
            "acc5_pad", "acc5_reverse", "acc5_slice", "rotate_8_3_4", "c2_2x2", "rand25",
-           "rand110"]
+           "rand110"] + C5W_4
 
 
 def _free_port():

@@ -12,8 +12,7 @@ from paper_2105_04663_b200.sharding import assemble_data, shard_data
 
 import golden_io as G
 
-CASES = [("random", c["name"]) for c in G.cases("random") if "expected" in c] + \
-        [("named", c["name"]) for c in G.cases("named") if "expected" in c]
+CASES = [(k, c["name"]) for k in G.KINDS for c in G.cases(k) if "expected" in c]
 
 
 def _case(kind, name):

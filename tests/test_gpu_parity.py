@@ -17,9 +17,8 @@ import golden_io as G
 
 pytestmark = pytest.mark.gpu
 
-CASES = [("random", c["name"]) for c in G.cases("random") if "spmd" in c] + \
-        [("named", c["name"]) for c in G.cases("named") if "spmd" in c]
-NAMED = [c["name"] for c in G.cases("named") if "spmd" in c]
+CASES = [(k, c["name"]) for k in G.KINDS for c in G.cases(k) if "spmd" in c]
+NAMED = [c["name"] for k in ("named", "c5w") for c in G.cases(k) if "spmd" in c]
 
 
 def _case(kind, name):
