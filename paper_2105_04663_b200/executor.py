@@ -1668,12 +1668,16 @@ class Executor:
             C.check(rc, op.value)
             return out
 
-        if op == Op.ALL_TO_ALL and comm is not None and ins.id in self._peer_a2a:
-            off = self._peer_a2a[ins.id]
+        if op == Op.ALL_TO_ALL and comm is not None:
+            # peer landing zones are assigned after compilation (_peer_bytes):
+            # choose the engine at run time
             keep_copy = ins.id in self.graph.outputs   # outputs outlive the step
             zone = {}
 
-            def run_peer(env, s):
+            def run_a2a(env, s):
+                if ins.id not in self._peer_a2a:
+                    return run(env, s)
+                off = self._peer_a2a[ins.id]
                 x = desc(env[a], ash)
                 if keep_copy:
                     out = self._alloc(shp)
@@ -1692,7 +1696,7 @@ class Executor:
                                                  at["concat_dim"], groups, ng, gs, off,
                                                  self._lane_of.get(s, 0), s), "all-to-all")
                 return out
-            return run_peer
+            return run_a2a
         return run
 
     def _constant(self, ins: Instruction):
@@ -1888,19 +1892,28 @@ class Executor:
 # host <-> device
 # ---------------------------------------------------------------------------
 
+def bf16_bits(x: np.ndarray) -> np.ndarray:
+    """float32 -> bf16 bit patterns (uint16), round to nearest even; NaN stays
+    a quiet NaN (the device conversion __float2bfloat16_rn)."""
+    u = np.ascontiguousarray(x, dtype=np.float32).view(np.uint32).astype(np.uint64)
+    r = ((u + 0x7FFF + ((u >> 16) & 1)) >> 16).astype(np.uint16)
+    nan = np.isnan(x)
+    if nan.any():
+        r = np.where(nan, ((u >> 16) | 0x40).astype(np.uint16), r)
+    return r
+
+
 def upload_stacked(arrays: Sequence[np.ndarray], shape: Shape, device, lib=None):
     """Stack per-partition host arrays into one device tensor ``[P, *dims]``."""
     torch = _torch()
     lib = lib or C.lib()
     P = len(arrays)
     if shape.dtype == DType.BF16:
+        # round on the host (nearest-even, as the device convert) and ship
+        # 2 bytes per element
         host = np.stack([np.asarray(a, dtype=np.float32).reshape(shape.dims) for a in arrays])
-        f32 = torch.from_numpy(np.ascontiguousarray(host)).to(device)
-        out = torch.empty((P,) + shape.dims, dtype=torch.bfloat16, device=device)
-        s = torch.cuda.current_stream(device).cuda_stream
-        C.check(lib.spmd_convert(desc(f32, Shape(shape.dims, DType.F32)), desc(out, shape), P, s),
-                "convert")
-        return out
+        bits = torch.from_numpy(np.ascontiguousarray(bf16_bits(host)).view(np.int16))
+        return bits.to(device).view(torch.bfloat16)
     host = np.stack([np.asarray(a, dtype=np_dtype(shape.dtype)).reshape(shape.dims)
                      for a in arrays])
     if shape.dtype == DType.U32:
@@ -1916,11 +1929,9 @@ def download_stacked(t, shape: Shape, lib=None) -> list[np.ndarray]:
     torch = _torch()
     lib = lib or C.lib()
     if shape.dtype == DType.BF16:
-        f32 = torch.empty(t.shape, dtype=torch.float32, device=t.device)
-        s = torch.cuda.current_stream(t.device).cuda_stream
-        C.check(lib.spmd_convert(desc(t, shape), desc(f32, Shape(shape.dims, DType.F32)),
-                                 t.shape[0], s), "convert")
-        host = f32.cpu().numpy()
+        # 2 bytes per element over PCIe, widened exactly on the host
+        bits = t.contiguous().view(torch.int16).cpu().numpy().view(np.uint16)
+        host = (bits.astype(np.uint32) << 16).view(np.float32)
     else:
         host = t.cpu().numpy()
         if shape.dtype == DType.U32:
@@ -1934,23 +1945,70 @@ def download_stacked(t, shape: Shape, lib=None) -> list[np.ndarray]:
 # reference-compatible entry points
 # ---------------------------------------------------------------------------
 
+class _Compiled:
+    """One compiled program behind the reference-signature entry points:
+    the Executor, and from the second call on a CUDA graph of the whole
+    step over static input buffers (each call then costs the uploads, one
+    replay and the downloads -- no per-op host overhead, no recompilation)."""
+
+    def __init__(self, program, n, dev, fuse):
+        self.ex = Executor(program, nparts=n, device=dev, fuse=fuse)
+        self.calls = 0
+        self.graph = None
+        self.static_in = None
+        self.static_out = None
+
+
+_COMPILED: dict = {}          # (id(program), fuse, device) -> (weakref, _Compiled)
+
+
+def _compiled(program, n, dev, fuse) -> _Compiled:
+    import weakref
+    key = (id(program), bool(fuse), str(dev))
+    hit = _COMPILED.get(key)
+    if hit is not None and hit[0]() is program:
+        return hit[1]
+    entry = _Compiled(program, n, dev, fuse)
+    try:
+        ref = weakref.ref(program, lambda _r, k=key: _COMPILED.pop(k, None))
+    except TypeError:         # not weak-referenceable: cache by identity only
+        ref = (lambda p=program: p)
+    _COMPILED[key] = (ref, entry)
+    return entry
+
+
 def evaluate_spmd(program, per_device_inputs: Mapping[int, Sequence[np.ndarray]],
                   fuse: bool = False, device=None) -> dict[int, list[np.ndarray]]:
     """Lockstep-equivalent evaluation of ``program`` on a simulated mesh of
     ``program.num_partitions`` partitions stacked on one B200
-    (reference ``simulator.py:393-426``)."""
+    (reference ``simulator.py:393-426``).  The compiled executor is cached
+    per program; repeated calls replay a captured CUDA graph."""
     torch = _torch()
     dev = torch.device(device) if device is not None else torch.device("cuda", 0)
     n = program.num_partitions
-    ex = Executor(program, nparts=n, device=dev, fuse=fuse)
     params = program.graph.parameters
     for d in range(n):
         if len(per_device_inputs[d]) != len(params):
             raise EvalError(f"device {d}: expected {len(params)} inputs")
+    entry = _compiled(program, n, dev, fuse)
+    ex = entry.ex
     stacked = [upload_stacked([per_device_inputs[d][k] for d in range(n)], p.shape, dev)
                for k, p in enumerate(params)]
     with torch.cuda.device(dev):
-        outs = ex.run(stacked)
+        entry.calls += 1
+        if entry.graph is None and entry.calls >= 2 and ex.comm is None:
+            try:
+                entry.static_in = [t.clone() for t in stacked]
+                entry.graph, entry.static_out = ex.capture(entry.static_in)
+            except Exception:     # noqa: BLE001 -- capture-incompatible program: stay eager
+                entry.graph, entry.static_in = None, None
+        if entry.graph is not None:
+            for dst, src in zip(entry.static_in, stacked):
+                dst.copy_(src)
+            entry.graph.replay()
+            outs = entry.static_out
+        else:
+            outs = ex.run(stacked)
         ex.check_errors()
     host = [download_stacked(o, program.graph.instr(oid).shape)
             for o, oid in zip(outs, program.graph.outputs)]

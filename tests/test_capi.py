@@ -50,3 +50,19 @@ def test_library_loads_and_reports_version():
         pytest.skip("library not built")
     assert b"sm_100a" in C.lib().spmd_version()
     assert C.lib().spmd_status_string(4) == b"integer division by zero"
+
+
+def test_host_bf16_rounding_matches_the_oracle():
+    """upload_stacked ships bf16 bit patterns rounded on the host; they must
+    equal the oracle's round-to-nearest-even (and the device conversion)."""
+    import numpy as np
+    from oracle import evaluator as O
+    from paper_2105_04663_b200.executor import bf16_bits
+    rng = np.random.default_rng(0)
+    x = np.concatenate([rng.standard_normal(10000).astype(np.float32) * 10.0 ** rng.integers(-30, 30, 10000),
+                        np.array([0.0, -0.0, np.inf, -np.inf, 1.0 + 2 ** -8, 1.0 + 3 * 2 ** -8,
+                                  3.3895314e38], np.float32)]).astype(np.float32)
+    got = (bf16_bits(x).astype(np.uint32) << 16).view(np.float32)
+    np.testing.assert_array_equal(got, O.to_bf16(x))
+    nan = (bf16_bits(np.array([np.nan], np.float32)).astype(np.uint32) << 16).view(np.float32)
+    assert np.isnan(nan).all()

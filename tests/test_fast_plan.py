@@ -55,3 +55,62 @@ def test_fast_plan_moves_less_data():
     fast = collective_stats(partition(ann, 8, plan="fast"))
     assert fast["counts"] == {"all-gather": 8, "reduce-scatter": 2}
     assert fast["total_bytes"] < ref["total_bytes"] / 4
+
+
+def _feature_conv(mesh_dims, Co, dtype):
+    from paper_2105_04663_b200.ir import ConvDims, DType, GraphBuilder, Op, Shape, WindowDim
+    from paper_2105_04663_b200.sharding import DeviceMesh, mesh_split
+    mesh = DeviceMesh.default(*mesh_dims)
+    b = GraphBuilder("featconv", mesh)
+    N, H, W, Ci = 2, 8, 6, 4
+    cd = ConvDims(lhs_batch=0, lhs_feature=3, lhs_spatial=(1, 2), rhs_in_feature=2,
+                  rhs_out_feature=3, rhs_spatial=(0, 1), out_batch=0, out_feature=3,
+                  out_spatial=(1, 2))
+    win = (WindowDim(3, 1, 1, 1), WindowDim(3, 1, 1, 1))
+    x = b.parameter(Shape((N, H, W, Ci), dtype), sharding=mesh_split(4, mesh, [-1, 0, -1, -1]),
+                    id="x")
+    w = b.parameter(Shape((3, 3, Ci, Co), dtype), sharding=mesh_split(4, mesh, [-1, -1, -1, 1]),
+                    id="w")
+    y = b.add(Op.CONVOLUTION, [x, w], {"conv_dims": cd, "window": win},
+              sharding=mesh_split(4, mesh, [-1, 0, -1, 1]), id="y")
+    g = b.build([y])
+    rng = np.random.default_rng(Co)
+    ins = [rng.integers(-4, 5, (N, H, W, Ci)).astype(np.int32),
+           rng.integers(-4, 5, (3, 3, Ci, Co)).astype(np.int32)]
+    if dtype == DType.F32:
+        ins = [i.astype(np.float32) for i in ins]
+    return g, ins
+
+
+@pytest.mark.parametrize("Co", [8, 6, 7])
+def test_fast_plan_partitions_conv_output_features(Co):
+    """Feature-dim conv partitioning (the reference forces
+    the weights replicated, formatting.py:507): with the output tiled on its
+    feature dim, the fast plan tiles the weights' output-feature dim the same
+    way -- the only collectives left are the halo permutes -- and the result
+    equals the single-device oracle exactly (int32 conv), even (Co=8) and
+    uneven (Co=6, 7 over 2) channel counts."""
+    from paper_2105_04663_b200.ir import DType, Op
+    g, ins = _feature_conv((2, 2), Co, DType.S32)
+    ann, _ = propagate(g)
+    want = O.evaluate_single(g, ins)[0]
+    for plan in ("reference", "fast"):
+        prog = partition(ann, 4, plan=plan)
+        kinds = {i.opcode for i in prog.graph.instructions}
+        if plan == "fast":
+            colls = {i.opcode for i in prog.graph.instructions
+                     if i.opcode in (Op.ALL_GATHER, Op.ALL_REDUCE, Op.ALL_TO_ALL,
+                                     Op.REDUCE_SCATTER)}
+            assert not colls, colls
+            conv = next(i for i in prog.graph.instructions if i.opcode == Op.CONVOLUTION)
+            assert conv.shape.dims[3] == -(-Co // 2)        # half the filters per device
+        devices = list(range(4))
+        per = {d: [] for d in devices}
+        for p, x in zip(ann.parameters, ins):
+            sh = shard_data(x, p.sharding, devices=devices)
+            for d in devices:
+                per[d].append(sh[d])
+        res = O.evaluate_spmd(prog, per)
+        full = assemble_data({d: res[d][0] for d in devices}, prog.output_shardings[0],
+                             g.instr(g.outputs[0]).shape)
+        np.testing.assert_array_equal(full, want)

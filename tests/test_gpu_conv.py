@@ -137,3 +137,31 @@ def test_halo_conv_fusion_equals_window_then_conv(n, H, monkeypatch):
     b = plain.run(stacked)[0]
     torch.cuda.synchronize()
     assert torch.equal(a, b)
+
+
+@pytest.mark.parametrize("Co", [8, 7])
+def test_feature_partitioned_conv_on_b200(Co):
+    """Fast-plan feature-dim conv partitioning (weights tiled on the output
+    feature dim, halo permutes only) executed on the B200, exact (int32)."""
+    import sys
+    import os
+    sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+    from oracle import evaluator as O
+    from paper_2105_04663_b200 import partition, propagate
+    from paper_2105_04663_b200.executor import evaluate_spmd
+    from paper_2105_04663_b200.ir import DType
+    from paper_2105_04663_b200.sharding import assemble_data, shard_data
+    from test_fast_plan import _feature_conv
+    g, ins = _feature_conv((2, 2), Co, DType.S32)
+    ann, _ = propagate(g)
+    prog = partition(ann, 4, plan="fast")
+    devices = list(range(4))
+    per = {d: [] for d in devices}
+    for p, x in zip(ann.parameters, ins):
+        sh = shard_data(x, p.sharding, devices=devices)
+        for d in devices:
+            per[d].append(sh[d])
+    res = evaluate_spmd(prog, per, fuse=True)
+    full = assemble_data({d: res[d][0] for d in devices}, prog.output_shardings[0],
+                         g.instr(g.outputs[0]).shape)
+    np.testing.assert_array_equal(full, O.evaluate_single(g, ins)[0])
