@@ -580,7 +580,71 @@ def _reshard(world, rank, dev, comm, barrier):
             "frac_of_nvlink_900": bus / (rms * 1e-3) / 1e9 / 900.0}
         del rex, rin, renv
     torch.cuda.empty_cache()
+    reshard["engines"] = _reshard_engines(world, dev, comm, barrier)
     return reshard
+
+
+def _reshard_engines(world, dev, comm, barrier):
+    """The same C5 transitions ([1008, 524288] f32, the padded 1001 rows)
+    through each engine of the C ABI, bus GB/s per GPU (max over ranks):
+    NCCL (pack + ncclAllToAll / ncclAllGather), the peer pull all-gather
+    (16-byte NVLink loads) and the push collectives (16-byte NVLink stores
+    straight into the members' landing zones, no pack pass)."""
+    import torch
+    import torch.distributed as dist
+    from paper_2105_04663_b200 import _capi as C
+    from paper_2105_04663_b200.executor import _groups_arg, desc
+    from paper_2105_04663_b200.ir import DType, Shape
+    lib = C.lib()
+    s = torch.cuda.current_stream(dev).cuda_stream
+    D1, rows = 524288, -(-1008 // world)
+    G = world
+    groups, ng, gs = _groups_arg([list(range(world))])
+    x = torch.randn((1, rows, D1), device=dev)
+    ag_out = torch.empty((1, rows * G, D1), device=dev)
+    a2a_out = torch.empty((1, rows * G, D1 // G), device=dev)
+    xs = desc(x, Shape((rows, D1), DType.F32))
+    ag_sh, a2a_sh = Shape((rows * G, D1), DType.F32), Shape((rows * G, D1 // G), DType.F32)
+    comm.ensure_workspace(2 * x.numel() * 4 * G, dev)
+    off = 3 * int(lib.spmd_comm_fused_half(comm.handle)) + 4096
+    comm.ensure_peer(off + ag_out.numel() * 4 + (1 << 20), dev)
+    zone_ag = desc(ag_out, ag_sh)
+    zone_ag.data = None
+    zone_a2a = desc(a2a_out, a2a_sh)
+    zone_a2a.data = None
+    variants = {
+        "all-gather/nccl": lambda: lib.spmd_all_gather(comm.handle, xs, desc(ag_out, ag_sh), 0,
+                                                       groups, ng, gs, s),
+        "all-gather/peer-pull": lambda: lib.spmd_peer_all_gather(
+            comm.handle, xs, desc(ag_out, ag_sh), 0, groups, ng, gs, off, 0, 1, s),
+        "all-gather/peer-push": lambda: lib.spmd_peer_push_all_gather(
+            comm.handle, xs, zone_ag, 0, groups, ng, gs, off, 0, s),
+        "all-to-all/nccl": lambda: lib.spmd_all_to_all(comm.handle, xs, desc(a2a_out, a2a_sh), 1,
+                                                       0, groups, ng, gs, s),
+        "all-to-all/peer-push": lambda: lib.spmd_peer_all_to_all(
+            comm.handle, xs, zone_a2a, 1, 0, groups, ng, gs, off, 0, s),
+    }
+    out = {}
+    for name, fn in variants.items():
+        for _ in range(3):
+            C.check(fn(), name)
+        torch.cuda.synchronize()
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(10):
+            C.check(fn(), name)
+        e1.record()
+        torch.cuda.synchronize()
+        ms = torch.tensor([e0.elapsed_time(e1) / 10], device=dev, dtype=torch.float64)
+        dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+        ms = float(ms.item())
+        bus = (ag_out.numel() if name.startswith("all-gather") else x.numel()) * 4 * (G - 1) / G
+        out[name] = {"ms": ms, "bus_gbs_per_gpu": bus / (ms * 1e-3) / 1e9}
+    C.check(lib.spmd_check_device_errors(s), "reshard engines")
+    del x, ag_out, a2a_out
+    torch.cuda.empty_cache()
+    return out
 
 
 def main():

@@ -38,6 +38,10 @@ struct AttnSmem {
 struct AttnShape {
   int S, T, N, Bp;     // Bp = partitions * batch
   float scale_log2e;   // softmax scale * log2(e)
+  // output for direct stores (persistent kernel): element strides of a
+  // query row, a head and a batch (the [B,S,N,D] or [B,N,S,D] layout)
+  bf16* out;
+  int64_t o_row, o_head, o_batch;
 };
 
 __device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, uint64_t* bar,
@@ -891,8 +895,11 @@ static int launch_attention_2sm(const CUtensorMap& mq, const CUtensorMap& mk,
 //    their half of P by the same running max; row sums stay per warp and are
 //    added in the epilogue;
 //  * row max / row sum as 8-way trees, scale folded into one FFMA per exp2;
-//  * epilogue staged through the P buffer (two 64-column SW128 atoms per
-//    round, one per warp half) and written with TMA bulk-tensor stores.
+//  * separate K and V rings (a K slot frees after its S MMA, a V slot after
+//    its PV MMA), K loaded one tile ahead of V;
+//  * O drained after the NEXT item's first tile has been softmaxed (the
+//    final-PV wait overlaps it), each softmax warp staging its own rows in
+//    its own slice of the P buffer and storing them with TMA.
 // Warps: 0 TMA producer, 1 MMA issuer (leader CTA), 2 TMEM allocator,
 // 3 idle, 4-11 softmax / correction / epilogue.
 // ---------------------------------------------------------------------------
@@ -1022,6 +1029,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
         for (int c = 0; c < DC; ++c)
           tma_load_4d_2sm(sq + c * 16384, &map_q, q_full, c * 64, st * 256 + (int)rank * 128, n,
                           b);
+        // Q is read once, from HBM: pull the next item's Q into L2 now, so
+        // its load at the item boundary (after this item's last S MMA frees
+        // the Q buffer) is an L2 hit and the tensor pipe does not idle on it
+        const int nx = item + ncl;
+        if (nx < items) {
+          const int nst = nx % nSt, nrest = nx / nSt;
+#pragma unroll
+          for (int c = 0; c < DC; ++c)
+            asm volatile(
+                "cp.async.bulk.prefetch.tensor.4d.L2.global [%0, {%1, %2, %3, %4}];" ::"l"(
+                    reinterpret_cast<uint64_t>(&map_q)),
+                "r"(c * 64), "r"(nst * 256 + (int)rank * 128), "r"(nrest % g.N), "r"(nrest / g.N)
+                : "memory");
+        }
       }
       const int slot = t % NS;
       mbar_wait(&k_empty[slot], ((t / NS) & 1) ^ 1);
@@ -1123,105 +1144,35 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
     float* my_red = red + h * 128 + row;
     const float* other_red = red + (1 - h) * 128 + row;
     const float c = g.scale_log2e;        // > 0 (host-checked)
-    int gt = 0;
-    for (int item = cl; item < items; item += ncl) {
-      const int st = item % nSt, rest = item / nSt;
-      const int n = rest % g.N, b = rest / g.N;
-      const int row0 = st * 256 + (int)rank * 128;
-      float m = -INFINITY, l = 0.f;       // running max (raw logits), this half's row sum
-      for (int j = 0; j < nT; ++j, ++gt) {
-        const int sb = gt & 1;
-        mbar_wait(&s_full[sb], (gt >> 1) & 1);
-        tc_fence_after();
-        float s[64];
-        {
-          uint32_t r[2][32];
-          tmem_ld32_nowait(tmem + lane_base + S_COL + sb * KT + h * 64, r[0]);
-          tmem_ld32_nowait(tmem + lane_base + S_COL + sb * KT + h * 64 + 32, r[1]);
-          tmem_wait_ld();
-#pragma unroll
-          for (int q = 0; q < 2; ++q)
-#pragma unroll
-            for (int i = 0; i < 32; ++i) s[q * 32 + i] = __uint_as_float(r[q][i]);
-        }
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive_leader(&s_free[sb]);
-        const int valid = g.T - j * KT - h * 64;
-        if (valid < 64) {
-#pragma unroll
-          for (int i = 0; i < 64; ++i)
-            if (i >= valid) s[i] = -INFINITY;
-        }
-        float t8[8];
-#pragma unroll
-        for (int a = 0; a < 8; ++a) t8[a] = s[a];
-#pragma unroll
-        for (int i = 8; i < 64; ++i) t8[i & 7] = fmaxf(t8[i & 7], s[i]);
-        float pm = fmaxf(fmaxf(fmaxf(t8[0], t8[1]), fmaxf(t8[2], t8[3])),
-                         fmaxf(fmaxf(t8[4], t8[5]), fmaxf(t8[6], t8[7])));
-        *my_red = pm;
-        named_sync(pair_bar, 64);
-        const float mx = fmaxf(pm, *other_red);
-        named_sync(pair_bar, 64);          // red is rewritten next tile
-        float alpha = 1.f;
-        bool resc = false;
-        if (m == -INFINITY) {
-          m = mx;
-        } else if ((mx - m) * c > 8.f) {    // rescale only when the max grows by > 2^8
-          alpha = ex2((m - mx) * c);
-          m = mx;
-          resc = true;
-        }
-        const float nmc = m == -INFINITY ? 0.f : -m * c;
-#pragma unroll
-        for (int i = 0; i < 64; ++i) s[i] = ex2(fmaf(s[i], c, nmc));
-#pragma unroll
-        for (int a = 0; a < 8; ++a) t8[a] = s[a];
-#pragma unroll
-        for (int i = 8; i < 64; ++i) t8[i & 7] += s[i];
-        l = l * alpha + (((t8[0] + t8[1]) + (t8[2] + t8[3])) + ((t8[4] + t8[5]) + (t8[6] + t8[7])));
-        // P is single-buffered and O may need rescaling: PV(gt-1) must be done
-        if (gt >= 1) mbar_wait(pv_done, (gt - 1) & 1);
-        if (j > 0 && __any_sync(0xffffffffu, resc)) {
-          tc_fence_after();
-#pragma unroll 1
-          for (int cc = 0; cc < DH; cc += 32) {
-            uint32_t o[32];
-            tmem_ld32(tmem + lane_base + O_COL + h * DH + cc, o);
-#pragma unroll
-            for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
-            tmem_st32(tmem + lane_base + O_COL + h * DH + cc, o);
-          }
-          asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-        }
-        uint8_t* prow = sp + h * 16384 + row * 128;   // SW128 atom h = keys 64h..64h+63
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          uint4 v;
-          __nv_bfloat162* hv = reinterpret_cast<__nv_bfloat162*>(&v);
-#pragma unroll
-          for (int t = 0; t < 4; ++t)
-            hv[t] = __floats2bfloat162_rn(s[q * 8 + 2 * t], s[q * 8 + 2 * t + 1]);
-          *reinterpret_cast<uint4*>(prow + ((q ^ (row & 7)) << 4)) = v;
-        }
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive_leader(p_full);
-      }
-      // ---- epilogue: O / l -> bf16 -> P buffer (SW128 atoms) -> TMA store ----
-      mbar_wait(pv_done, (gt - 1) & 1);
-      tc_fence_after();
-      *my_red = l;
+    // Flat loop over this pair's tiles.  At an item boundary the next item's
+    // first tile is softmaxed BEFORE waiting for the previous item's last PV
+    // and draining its O (ncu: the softmax warps spent 27% of their time in
+    // the drain -- the final-PV wait, barriers and the smem/TMA store path).
+    // O is written straight from registers to global memory (each thread one
+    // row, its half of the head dim: 16-byte stores), so the drain needs no
+    // shared memory, no named barriers and does not hold the P buffer.
+    const int my_items = cl < items ? (items - cl + ncl - 1) / ncl : 0;
+    const int G = my_items * nT;
+    int item = cl, j = 0;
+    int cst = 0, cn = 0, cb = 0;          // current item (query tile, head, batch)
+    float m = -INFINITY, l = 0.f;         // running max (raw logits), this half's row sum
+    // Drain of a finished item's O: each warp stages its 32 rows x 64
+    // columns (one round of its half of the head dim) in the SW128 layout,
+    // in exactly the 4 KB of the P buffer it writes P into (atom h, rows
+    // 32q..32q+31) -- no other warp touches that region, so the drain needs
+    // no cross-warp barrier -- and one lane stores the box with TMA (per-row
+    // 16-byte global stores measured ~20% of the softmax warps' time: one
+    // L1 transaction per lane).
+    auto drain = [&](float lsum, int st_, int n_, int b_) {
+      *my_red = lsum;
       named_sync(pair_bar, 64);
-      const float lt = l + *other_red;
+      const float lt = lsum + *other_red;
       named_sync(pair_bar, 64);
       const float inv = lt > 0.f ? 1.f / lt : 0.f;
+      uint8_t* stage = sp + h * 16384 + qd * 4096;
+      uint8_t* srow = stage + lane * 128;
 #pragma unroll 1
       for (int rd = 0; rd < DH / 64; ++rd) {
-        // this warp's 64 columns of the round: h * DH + rd * 64 .. + 63 -> atom h
-        uint8_t* orow = sp + h * 16384 + row * 128;
 #pragma unroll
         for (int half = 0; half < 2; ++half) {
           uint32_t o[32];
@@ -1231,30 +1182,131 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
             uint4 v;
             __nv_bfloat162* hv = reinterpret_cast<__nv_bfloat162*>(&v);
 #pragma unroll
-            for (int t = 0; t < 4; ++t)
-              hv[t] = __floats2bfloat162_rn(__uint_as_float(o[q * 8 + 2 * t]) * inv,
-                                            __uint_as_float(o[q * 8 + 2 * t + 1]) * inv);
-            *reinterpret_cast<uint4*>(orow + (((half * 4 + q) ^ (row & 7)) << 4)) = v;
+            for (int u = 0; u < 4; ++u)
+              hv[u] = __floats2bfloat162_rn(__uint_as_float(o[q * 8 + 2 * u]) * inv,
+                                            __uint_as_float(o[q * 8 + 2 * u + 1]) * inv);
+            *reinterpret_cast<uint4*>(srow + (((half * 4 + q) ^ (row & 7)) << 4)) = v;
           }
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        named_sync(5, 256);
-        if (warp == 4 && lane == 0) {
-#pragma unroll
-          for (int a = 0; a < 2; ++a)
-            asm volatile(
-                "cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%2, %3, %4, %5}], "
-                "[%1];" ::"l"(reinterpret_cast<uint64_t>(&map_o)),
-                "r"(smem_u32(sp + a * 16384)), "r"(a * DH + rd * 64), "r"(row0), "r"(n), "r"(b)
-                : "memory");
+        __syncwarp();
+        if (lane == 0) {
+          asm volatile(
+              "cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%2, %3, %4, %5}], "
+              "[%1];" ::"l"(reinterpret_cast<uint64_t>(&map_o)),
+              "r"(smem_u32(stage)), "r"(h * DH + rd * 64),
+              "r"(st_ * 256 + (int)rank * 128 + qd * 32), "r"(n_), "r"(b_)
+              : "memory");
           asm volatile("cp.async.bulk.commit_group;" ::: "memory");
           asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
         }
-        named_sync(5, 256);                // P buffer readable again
+        __syncwarp();
+      }
+    };
+    for (int t = 0; t < G; ++t) {
+      float l_prev = 0.f;
+      int pst = cst, pn = cn, pb = cb;
+      if (j == 0) {
+        const int rest = item / nSt;
+        cst = item % nSt, cn = rest % g.N, cb = rest / g.N;
+        l_prev = l;
+        m = -INFINITY;
+        l = 0.f;
+      }
+      const int sb = t & 1;
+      mbar_wait(&s_full[sb], (t >> 1) & 1);
+      tc_fence_after();
+      float s[64];
+      {
+        uint32_t r[2][32];
+        tmem_ld32_nowait(tmem + lane_base + S_COL + sb * KT + h * 64, r[0]);
+        tmem_ld32_nowait(tmem + lane_base + S_COL + sb * KT + h * 64 + 32, r[1]);
+        tmem_wait_ld();
+#pragma unroll
+        for (int q = 0; q < 2; ++q)
+#pragma unroll
+          for (int i = 0; i < 32; ++i) s[q * 32 + i] = __uint_as_float(r[q][i]);
       }
       tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_leader(&s_free[sb]);
+      const int valid = g.T - j * KT - h * 64;
+      if (valid < 64) {
+#pragma unroll
+        for (int i = 0; i < 64; ++i)
+          if (i >= valid) s[i] = -INFINITY;
+      }
+      float t8[8];
+#pragma unroll
+      for (int a = 0; a < 8; ++a) t8[a] = s[a];
+#pragma unroll
+      for (int i = 8; i < 64; ++i) t8[i & 7] = fmaxf(t8[i & 7], s[i]);
+      float pm = fmaxf(fmaxf(fmaxf(t8[0], t8[1]), fmaxf(t8[2], t8[3])),
+                       fmaxf(fmaxf(t8[4], t8[5]), fmaxf(t8[6], t8[7])));
+      *my_red = pm;
+      named_sync(pair_bar, 64);
+      const float mx = fmaxf(pm, *other_red);
+      named_sync(pair_bar, 64);          // red is rewritten next tile
+      float alpha = 1.f;
+      bool resc = false;
+      if (m == -INFINITY) {
+        m = mx;
+      } else if ((mx - m) * c > 8.f) {    // rescale only when the max grows by > 2^8
+        alpha = ex2((m - mx) * c);
+        m = mx;
+        resc = true;
+      }
+      const float nmc = m == -INFINITY ? 0.f : -m * c;
+#pragma unroll
+      for (int i = 0; i < 64; ++i) s[i] = ex2(fmaf(s[i], c, nmc));
+#pragma unroll
+      for (int a = 0; a < 8; ++a) t8[a] = s[a];
+#pragma unroll
+      for (int i = 8; i < 64; ++i) t8[i & 7] += s[i];
+      l = l * alpha + (((t8[0] + t8[1]) + (t8[2] + t8[3])) + ((t8[4] + t8[5]) + (t8[6] + t8[7])));
+      // P is single-buffered and O may need rescaling / draining: PV(t-1) done
+      if (t >= 1) mbar_wait(pv_done, (t - 1) & 1);
+      if (j == 0 && t > 0) {
+        tc_fence_after();
+        drain(l_prev, pst, pn, pb);       // previous item's O, before PV(t) overwrites it
+      }
+      if (j > 0 && __any_sync(0xffffffffu, resc)) {
+        tc_fence_after();
+#pragma unroll 1
+        for (int cc = 0; cc < DH; cc += 32) {
+          uint32_t o[32];
+          tmem_ld32(tmem + lane_base + O_COL + h * DH + cc, o);
+#pragma unroll
+          for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
+          tmem_st32(tmem + lane_base + O_COL + h * DH + cc, o);
+        }
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      }
+      uint8_t* prow = sp + h * 16384 + row * 128;   // SW128 atom h = keys 64h..64h+63
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        uint4 v;
+        __nv_bfloat162* hv = reinterpret_cast<__nv_bfloat162*>(&v);
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          hv[u] = __floats2bfloat162_rn(s[q * 8 + 2 * u], s[q * 8 + 2 * u + 1]);
+        *reinterpret_cast<uint4*>(prow + ((q ^ (row & 7)) << 4)) = v;
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_leader(p_full);
+      if (++j == nT) {
+        j = 0;
+        item += ncl;
+      }
     }
-    if (warp == 4 && lane == 0) bulk_wait_all();
+    if (G > 0) {
+      mbar_wait(pv_done, (G - 1) & 1);
+      tc_fence_after();
+      drain(l, cst, cn, cb);
+    }
+    if (lane == 0) bulk_wait_all();
   }
   tc_fence_before();
   cluster_sync();
@@ -1313,6 +1365,10 @@ extern "C" int spmd_attention_layout(spmd_tensor q, spmd_tensor k, spmd_tensor v
   g.N = (int)N;
   g.Bp = (int)Bp;
   g.scale_log2e = scale * 1.4426950408889634f;
+  g.out = (bf16*)out.data;
+  g.o_row = out_bsnd ? N * D : D;
+  g.o_head = out_bsnd ? D : S * D;
+  g.o_batch = S * N * D;
   cudaStream_t s = as_stream(stream);
   const int mode = option(OPT_ATTN_MODE) == 1 ? 1 : 2;
   // key tile: 128 for D=128 (549 vs 469 TF/s at T=1024), 64 for D=256 (equal at
@@ -1321,9 +1377,14 @@ extern "C" int spmd_attention_layout(spmd_tensor q, spmd_tensor k, spmd_tensor v
   // round-1 non-persistent kernels with that key tile
   const int kt = (int)option(OPT_ATTN_KT);
   if (mode == 2 && D >= 128 && kt == 0 && scale > 0.f) {
-    // persistent CTA pairs, 8 softmax warps, 128-key tiles (default)
-    if (D == 128) return launch_attention_2sm_pp<128>(mq, mk, mv, mo, g, s);
-    return launch_attention_2sm_pp<256>(mq, mk, mv, mo, g, s);
+    // persistent CTA pairs, 8 softmax warps, 128-key tiles (default); each
+    // softmax warp stores its own 32-row output boxes
+    CUtensorMap mo32;
+    if (out_bsnd ? encode4(&mo32, out.data, D, S, N, Bp, N * D, D, S * N * D, 32)
+                 : encode4(&mo32, out.data, D, S, N, Bp, D, S * D, N * S * D, 32)) {
+      if (D == 128) return launch_attention_2sm_pp<128>(mq, mk, mv, mo32, g, s);
+      return launch_attention_2sm_pp<256>(mq, mk, mv, mo32, g, s);
+    }
   }
   if (mode == 2 && D >= 128 && kt == 128) {
     // 128-key tiles: K boxes of 64 rows (mk), V boxes of 64 rows (mv)

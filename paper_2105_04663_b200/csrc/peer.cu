@@ -628,33 +628,106 @@ static void row_major(const spmd_tensor& t, int64_t* st) {
   }
 }
 
+// One launch pushes all G pieces: chunk c of the flattened (piece, element)
+// space goes to destination c % G, so the NVLink stores to the peers and the
+// local copy of this rank's own piece run concurrently (G sequential copies
+// measured 544 GB/s per GPU at G = 2).  Index math as the affine copy kernel
+// (datamove.cu): pieces share shape and strides, differ in source offset and
+// destination pointer.
+struct PushArgs {
+  int rank;
+  int64_t shape[SPMD_MAX_RANK], sst[SPMD_MAX_RANK], dst[SPMD_MAX_RANK];
+  int64_t n;                  // elements per piece (a multiple of V when vectorised)
+  int64_t sbase[8];           // source offset of piece j
+  int64_t dbase;              // destination offset (same in every member's zone)
+  char* out[8];               // member j's landing zone
+  int G;
+};
+
+template <typename T, int V>
+__global__ void __launch_bounds__(256) peer_push_kernel(const T* __restrict__ src, PushArgs a) {
+  const int64_t per = a.n / V;                       // vectors per piece
+  const int64_t chunks = (per + 255) / 256;           // 256-vector chunks per piece
+  const int64_t total = chunks * a.G;
+  for (int64_t c = blockIdx.x; c < total; c += gridDim.x) {
+    const int j = (int)(c % a.G);
+    const int64_t v = (c / a.G) * 256 + threadIdx.x;
+    if (v >= per) continue;
+    int64_t r = v * V, so = a.sbase[j], d0 = a.dbase;
+#pragma unroll
+    for (int k = SPMD_MAX_RANK - 1; k >= 0; --k) {
+      if (k < a.rank) {
+        const int64_t ck = r % a.shape[k];
+        r /= a.shape[k];
+        so += ck * a.sst[k];
+        d0 += ck * a.dst[k];
+      }
+    }
+    T* dst = reinterpret_cast<T*>(a.out[j]);
+    if (V == 1)
+      dst[d0] = src[so];
+    else
+      *reinterpret_cast<uint4*>(dst + d0) = __ldcs(reinterpret_cast<const uint4*>(src + so));
+  }
+  __threadfence_system();   // peer stores visible before the barrier signal
+}
+
 // in: this rank's operand; zone_shape: one member's output shape.  piece j of
 // `in` (index j of `sdim` split G ways, or the whole input when sdim < 0)
 // lands at index pos of `cdim` (split G ways) in member j's zone.
 static int peer_push(spmd_comm* c, const spmd_tensor& in, const spmd_tensor& zone_shape,
                      int sdim, int cdim, const int32_t* members, int gsize, int pos,
                      int64_t heap_offset, cudaStream_t s) {
+  SPMD_CHECK_ARG(gsize >= 1 && gsize <= 8, "peer push group size <= 8");
   int64_t ist[SPMD_MAX_RANK], ost[SPMD_MAX_RANK];
   row_major(in, ist);
   row_major(zone_shape, ost);
   spmd_tensor piece = in;
   if (sdim >= 0) piece.dims[sdim] /= gsize;
-  for (int j = 0; j < gsize; ++j) {
-    CopyArgs a;
-    memset(&a, 0, sizeof(a));
-    a.rank = in.rank;
-    for (int k = 0; k < in.rank; ++k) {
-      a.shape[k] = piece.dims[k];
-      a.sst[k] = ist[k];
-      a.dst[k] = ost[k];
+  // merge dims contiguous in both views (fewer div/mods per element)
+  PushArgs a;
+  memset(&a, 0, sizeof(a));
+  int r = 0;
+  for (int k = 0; k < in.rank; ++k) {
+    if (piece.dims[k] == 1) continue;
+    if (r > 0 && a.sst[r - 1] == ist[k] * piece.dims[k] && a.dst[r - 1] == ost[k] * piece.dims[k]) {
+      a.shape[r - 1] *= piece.dims[k];
+      a.sst[r - 1] = ist[k];
+      a.dst[r - 1] = ost[k];
+      continue;
     }
-    a.sbase = sdim >= 0 ? (int64_t)j * piece.dims[sdim] * ist[sdim] : 0;
-    a.dbase = (int64_t)pos * piece.dims[cdim] * ost[cdim];
-    a.fence_sys = 1;
-    char* zone = c->peer[members[j]] + CTRL_BYTES + heap_offset;
-    if (int rc = launch_copy(in.data, zone, in.dtype, a, 1, s)) return rc;
+    a.shape[r] = piece.dims[k];
+    a.sst[r] = ist[k];
+    a.dst[r] = ost[k];
+    ++r;
   }
-  return SPMD_OK;
+  a.rank = r;
+  a.n = numel(piece);
+  if (a.n == 0) return SPMD_OK;
+  a.G = gsize;
+  a.dbase = (int64_t)pos * piece.dims[cdim] * ost[cdim];
+  for (int j = 0; j < gsize; ++j) {
+    a.sbase[j] = sdim >= 0 ? (int64_t)j * piece.dims[sdim] * ist[sdim] : 0;
+    a.out[j] = c->peer[members[j]] + CTRL_BYTES + heap_offset;
+  }
+  const int es = elem_size(in.dtype);
+  const int V = 16 / es;
+  bool vec = r >= 1 && a.sst[r - 1] == 1 && a.dst[r - 1] == 1 && a.shape[r - 1] % V == 0 &&
+             a.dbase % V == 0 && (reinterpret_cast<uintptr_t>(in.data) & 15) == 0 &&
+             (heap_offset & 15) == 0;
+  for (int k = 0; vec && k < r - 1; ++k) vec = a.sst[k] % V == 0 && a.dst[k] % V == 0;
+  for (int j = 0; vec && j < gsize; ++j) vec = a.sbase[j] % V == 0;
+  const int64_t vecs = vec ? a.n / V : a.n;
+  int64_t grid = ((vecs + 255) / 256) * gsize;
+  if (grid > 148LL * 16) grid = 148LL * 16;
+  if (grid < 1) grid = 1;
+  SPMD_DISPATCH_BYTES(in.dtype, T, {
+    if (vec)
+      peer_push_kernel<T, 16 / sizeof(T)><<<(unsigned)grid, 256, 0, s>>>((const T*)in.data, a);
+    else
+      peer_push_kernel<T, 1><<<(unsigned)grid, 256, 0, s>>>((const T*)in.data, a);
+  });
+  return launched(s);
 }
 
 static int finish_zone(spmd_comm* c, const spmd_tensor& out, int64_t heap_offset, int64_t bytes,

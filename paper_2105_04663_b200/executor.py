@@ -250,6 +250,7 @@ class Executor:
             self._peer_ag = {}
             self._peer_cp = {}
             self._peer_a2a = {}
+            self._peer_agp = {}
             self._peer_bytes_used = 0
             self._fused_half = 0
         self._peer_engine = self._plan_peer_engines()
@@ -456,6 +457,17 @@ class Executor:
                     self._peer_ag[ins.id] = off
                     nb = self._shape(ins.operands[0]).num_elements * ins.shape.dtype.itemsize
                     off += (nb + 4095) // 4096 * 4096
+        # push all-gathers (SPMD_PEER_AG_PUSH=1): gathers of computed values
+        # (not parameters, which are pre-staged) get a landing zone holding
+        # the whole output; every member pushes its shard into every zone
+        self._peer_agp = {}
+        if os.environ.get("SPMD_PEER_AG_PUSH", "0") == "1":
+            pids = {p.id for p in self.params}
+            for ins in self.graph.instructions:
+                if ins.opcode == Op.ALL_GATHER and ins.id not in self._fused_skip and \
+                        ins.operands[0] not in pids:
+                    self._peer_agp[ins.id] = off
+                    off += (ins.shape.nbytes + 4095) // 4096 * 4096
         # all-to-alls (C5 resharding; MoE exchanges not fused into a GEMM):
         # one landing zone each, holding this rank's output -- every member
         # pushes its piece there (spmd_peer_all_to_all), and the zone is the
@@ -1668,16 +1680,16 @@ class Executor:
             C.check(rc, op.value)
             return out
 
-        if op == Op.ALL_TO_ALL and comm is not None:
+        if op in (Op.ALL_TO_ALL, Op.ALL_GATHER) and comm is not None:
             # peer landing zones are assigned after compilation (_peer_bytes):
             # choose the engine at run time
             keep_copy = ins.id in self.graph.outputs   # outputs outlive the step
             zone = {}
-
             def run_a2a(env, s):
-                if ins.id not in self._peer_a2a:
+                zones = self._peer_a2a if op == Op.ALL_TO_ALL else self._peer_agp
+                if ins.id not in zones:
                     return run(env, s)
-                off = self._peer_a2a[ins.id]
+                off = zones[ins.id]
                 x = desc(env[a], ash)
                 if keep_copy:
                     out = self._alloc(shp)
@@ -1692,9 +1704,14 @@ class Executor:
                     out = zone["t"]
                     y = desc(out, shp)
                     y.data = None                # the landing zone is the result
-                C.check(lib.spmd_peer_all_to_all(comm.handle, x, y, at["split_dim"],
-                                                 at["concat_dim"], groups, ng, gs, off,
-                                                 self._lane_of.get(s, 0), s), "all-to-all")
+                if op == Op.ALL_TO_ALL:
+                    rc = lib.spmd_peer_all_to_all(comm.handle, x, y, at["split_dim"],
+                                                  at["concat_dim"], groups, ng, gs, off,
+                                                  self._lane_of.get(s, 0), s)
+                else:
+                    rc = lib.spmd_peer_push_all_gather(comm.handle, x, y, at["dim"], groups, ng,
+                                                       gs, off, self._lane_of.get(s, 0), s)
+                C.check(rc, op.value)
                 return out
             return run_a2a
         return run
@@ -1730,7 +1747,7 @@ class Executor:
                 for vid in step.frees:
                     if vid not in keep:
                         env.pop(vid, None)
-            if self._peer_cp or self._peer_a2a:
+            if self._peer_cp or self._peer_a2a or self._peer_agp:
                 # landing slots are read before any rank writes them again
                 C.check(self.lib.spmd_peer_barrier(self.comm.handle, 0, s), "peer_barrier")
         else:
@@ -1822,7 +1839,8 @@ class Executor:
                     env.pop(vid, None)
         for st in self.comm_streams:
             compute.wait_stream(st)               # join
-        if self._staged or self._act_staged or self._peer_cp or self._peer_a2a:
+        if self._staged or self._act_staged or self._peer_cp or self._peer_a2a or \
+                self._peer_agp:
             # every member has read the staged / landing slots before any
             # rank writes them again
             st = self.comm_streams[0]
