@@ -457,11 +457,14 @@ class Executor:
                     self._peer_ag[ins.id] = off
                     nb = self._shape(ins.operands[0]).num_elements * ins.shape.dtype.itemsize
                     off += (nb + 4095) // 4096 * 4096
-        # push all-gathers (SPMD_PEER_AG_PUSH=1): gathers of computed values
-        # (not parameters, which are pre-staged) get a landing zone holding
-        # the whole output; every member pushes its shard into every zone
+        # push all-gathers: gathers of computed values (parameters are
+        # pre-staged) get a landing zone holding the whole output; every
+        # member pushes its shard into every zone.  Used for the gathers on
+        # the critical path (engine 1 / NCCL), where SMs are free: 652 vs 475
+        # (pull) vs 467 (NCCL) GB/s per GPU at N=2 (profiles/r2_bench_n2.log);
+        # gathers hidden under a GEMM keep the copy engines.
         self._peer_agp = {}
-        if os.environ.get("SPMD_PEER_AG_PUSH", "0") == "1":
+        if os.environ.get("SPMD_PEER_AG_PUSH", "1") != "0":
             pids = {p.id for p in self.params}
             for ins in self.graph.instructions:
                 if ins.opcode == Op.ALL_GATHER and ins.id not in self._fused_skip and \
@@ -1687,7 +1690,8 @@ class Executor:
             zone = {}
             def run_a2a(env, s):
                 zones = self._peer_a2a if op == Op.ALL_TO_ALL else self._peer_agp
-                if ins.id not in zones:
+                if ins.id not in zones or (op == Op.ALL_GATHER and
+                                           self._peer_engine.get(ins.id, -1) not in (1, -1)):
                     return run(env, s)
                 off = zones[ins.id]
                 x = desc(env[a], ash)
