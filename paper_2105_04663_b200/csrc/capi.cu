@@ -71,6 +71,8 @@ static const OptDef kOpts[OPT_COUNT] = {
     {"peer_timeout_ms", "SPMD_PEER_TIMEOUT_MS", 20000},
     {"peer_serial_pulls", "SPMD_PEER_SERIAL_PULLS", 0},
     {"f32_dot_tc", "SPMD_F32_DOT_TC", 1},
+    {"gemm_persistent", "SPMD_GEMM_PERSISTENT", 1},
+    {"gemm_dynamic", "SPMD_GEMM_DYNAMIC", 1},
 };
 static std::atomic<int64_t> g_opts[OPT_COUNT];
 static std::once_flag g_opts_once;

@@ -44,6 +44,8 @@ enum Option : int {
   OPT_PEER_TIMEOUT_MS,      // peer barrier timeout
   OPT_PEER_SERIAL_PULLS,    // 1: staged gathers pull members one after another
   OPT_F32_DOT_TC,           // 1: large f32 Dots on the tensor cores (3xTF32)
+  OPT_GEMM_PERSISTENT,      // 1: one CTA pair per 2 SMs walks the tiles; 0: one pair per tile
+  OPT_GEMM_DYNAMIC,         // 1: persistent wide GEMM takes tiles from a global counter
   OPT_COUNT
 };
 int64_t option(int id);

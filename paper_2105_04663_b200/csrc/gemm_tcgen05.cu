@@ -21,6 +21,8 @@
 // Tile 128 x BN x 64, BN in {128, 256}; SWIZZLE_128B everywhere.
 #include "tcgen05.cuh"
 
+#include <mutex>
+
 #include <cuda.h>
 #include <string.h>
 
@@ -31,6 +33,9 @@ constexpr int BK = 64;
 constexpr int EPI_WARP0 = 4;
 
 struct GemmShape {
+  // wide kernel: non-null -> dynamic tile order (tile_ring_*): a global
+  // counter hands out tiles first come, first served
+  int* tile_counter;
   int M, N, K;
   int nb[3];            // batch extents (innermost first in tensor-map order)
   int mt, nt;           // tile counts
@@ -509,6 +514,80 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
 constexpr int WBN = 512;          // pair tile N
 constexpr int WHALF_N = 256;      // N per UMMA
 
+// ---------------------------------------------------------------------------
+// Dynamic tile order for the persistent wide kernel.  A static round-robin
+// (pair c takes tiles c, c+74, ...) lets the 74 pairs drift apart over ~110
+// tiles, so the tiles in flight spread far beyond one raster group and L2
+// reuse collapses: ncu on the C2 FFN-in GEMM measured 22-35 GB of DRAM reads
+// (cuBLAS 12.5 GB) and, under the 1 kW power cap, ~7% lower SM clocks.  A
+// non-persistent launch (the hardware hands tiles out in order) cut the
+// DRAM reads to 13.5 GB but loses the epilogue/mainloop overlap.  Here the
+// leader CTA's producer thread takes the next tile from a global counter and
+// publishes it through a small ring (tile id in both CTAs' shared memory,
+// mbarriers) to its peer producer, the MMA warp and the 16 epilogue warps:
+// tiles are consumed in global order, the kernel stays persistent.
+// ---------------------------------------------------------------------------
+constexpr int TILE_RING = 4;
+constexpr int TILE_RING_CONSUMERS = 1 + 1 + 16;   // peer producer, MMA warp, 2 x 8 epilogue warps
+
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t phase) {
+  uint32_t addr = smem_u32(bar);
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAITC_%=:\n"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAITC_%=;\n"
+      "}\n" ::"r"(addr),
+      "r"(phase)
+      : "memory");
+}
+
+// arrive on the barrier at the same smem offset in cluster CTA `cta`
+__device__ __forceinline__ void mbar_arrive_cta(uint64_t* bar, uint32_t cta) {
+  asm volatile(
+      "{\n.reg .b32 ra;\n"
+      "mapa.shared::cluster.u32 ra, %0, %1;\n"
+      "mbarrier.arrive.release.cluster.shared::cluster.b64 _, [ra];\n}" ::"r"(smem_u32(bar)),
+      "r"(cta)
+      : "memory");
+}
+
+__device__ __forceinline__ void st_cluster_u32(uint32_t* p, uint32_t cta, uint32_t v) {
+  asm volatile(
+      "{\n.reg .b32 ra;\n"
+      "mapa.shared::cluster.u32 ra, %0, %1;\n"
+      "st.shared::cluster.u32 [ra], %2;\n}" ::"r"(smem_u32(p)),
+      "r"(cta), "r"(v)
+      : "memory");
+}
+
+// Scheduler side (leader producer): fetch the next tile and publish it in
+// slot i % TILE_RING of both CTAs.  Returns the tile (>= g.tiles: done).
+__device__ __forceinline__ int64_t ring_publish(const GemmShape& g, int32_t* ids, uint64_t* rfull,
+                                                uint64_t* rempty, int i) {
+  const int slot = i % TILE_RING;
+  mbar_wait_cluster(&rempty[slot], ((i / TILE_RING) & 1) ^ 1);
+  int t = atomicAdd(g.tile_counter, 1);
+  if (t > g.tiles) t = (int)g.tiles;
+  ids[slot] = t;
+  st_cluster_u32((uint32_t*)&ids[slot], 1, (uint32_t)t);
+  mbar_arrive_cta(&rfull[slot], 0);
+  mbar_arrive_cta(&rfull[slot], 1);
+  return t;
+}
+
+// Consumer side: the tile of slot i % TILE_RING; `notify` = this thread
+// releases the slot (one arrival on the leader's ring-empty barrier).
+__device__ __forceinline__ int64_t ring_take(int32_t* ids, uint64_t* rfull, uint64_t* rempty,
+                                             int i, bool notify) {
+  const int slot = i % TILE_RING;
+  mbar_wait_cluster(&rfull[slot], (i / TILE_RING) & 1);
+  const int64_t t = *(volatile int32_t*)&ids[slot];
+  if (notify) mbar_arrive_cta(&rempty[slot], 0);
+  return t;
+}
+
 template <int STAGES>
 struct SmemW {
   static constexpr int A_BYTES = HALF * BK * 2;              // 16 KB
@@ -532,17 +611,25 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 1;
-  uint32_t* tmem_slot = (uint32_t*)(tempty + 1);
+  uint64_t* rfull = tempty + 1;            // [TILE_RING] tile-id ring (dynamic order)
+  uint64_t* rempty = rfull + TILE_RING;    // [TILE_RING] leader only
+  int32_t* ring_ids = (int32_t*)(rempty + TILE_RING);
+  uint32_t* tmem_slot = (uint32_t*)(ring_ids + TILE_RING);
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const uint32_t rank = cluster_rank();
   const bool leader = rank == 0;
   const int64_t cluster = blockIdx.x >> 1, nclusters = gridDim.x >> 1;
+  const bool dyn = g.tile_counter != nullptr;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
+    }
+    for (int r = 0; r < TILE_RING; ++r) {
+      mbar_init(&rfull[r], 1);
+      mbar_init(&rempty[r], TILE_RING_CONSUMERS);
     }
     mbar_init(tfull, 1);
     mbar_init(tempty, 16);   // 8 epilogue warps x 2 CTAs
@@ -569,7 +656,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
     const int hint = g.hint != 0;
     const uint64_t pa = g.hint == 1 ? pol_last : pol_first;
     const uint64_t pb = g.hint == 1 ? pol_first : pol_last;
-    for (int64_t t = cluster; t < g.tiles; t += nclusters) {
+    for (int64_t it = 0, t = cluster;; ++it) {
+      if (dyn)
+        t = leader ? ring_publish(g, ring_ids, rfull, rempty, (int)it)
+                   : ring_take(ring_ids, rfull, rempty, (int)it, true);
+      else if (it > 0)
+        t += nclusters;
+      if (t >= g.tiles) break;
       int b, m, n;
       tile_coords(g, t, b, m, n);
       const int b0 = b % g.nb[0], b1 = (b / g.nb[0]) % g.nb[1], b2 = b / (g.nb[0] * g.nb[1]);
@@ -613,7 +706,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
     int s = 0;
     uint32_t ph = 0;
     uint32_t acc_ph = 0;
-    for (int64_t t = cluster; t < g.tiles; t += nclusters) {
+    for (int64_t it = 0, t = cluster;; ++it) {
+      if (dyn)
+        t = ring_take(ring_ids, rfull, rempty, (int)it, true);
+      else if (it > 0)
+        t += nclusters;
+      if (t >= g.tiles) break;
       mbar_wait(tempty, acc_ph ^ 1);
       tc_fence_after();
       for (int kb = 0; kb < kblocks; ++kb) {
@@ -654,7 +752,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
     const int par = g.scatter ? (int)((*(volatile const uint32_t*)g.sc_epoch + 1) & 1) : 0;
     int chunk = 0;
     uint32_t acc_ph = 0;
-    for (int64_t t = cluster; t < g.tiles; t += nclusters) {
+    for (int64_t it = 0, t = cluster;; ++it) {
+      if (dyn) {
+        t = ring_take(ring_ids, rfull, rempty, (int)it, false);
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cta(&rempty[(int)it % TILE_RING], 0);
+      } else if (it > 0) {
+        t += nclusters;
+      }
+      if (t >= g.tiles) break;
       int b, m, n;
       tile_coords(g, t, b, m, n);
       mbar_wait(tfull, acc_ph);
@@ -762,10 +868,33 @@ static int launch_gemm_2sm(const CUtensorMap& ma, const CUtensorMap& mb, const C
   static std::atomic<uint64_t> attr_done{0};
   if (int rc = set_smem_attr((const void*)gemm_bf16_tcgen05_2sm<STAGES>, L::TOTAL, &attr_done)) return rc;
   const int sms = sm_budget();
-  int64_t clusters = g.tiles < sms / 2 ? g.tiles : sms / 2;
+  int64_t clusters = g.tiles < sms / 2 || !option(OPT_GEMM_PERSISTENT) ? g.tiles : sms / 2;
   gemm_bf16_tcgen05_2sm<STAGES><<<(unsigned)(2 * clusters), 256, L::TOTAL, s>>>(ma, mb, mc, out,
                                                                                     g, smaps);
   return launched(s);
+}
+
+// Per-launch tile counters of the dynamic schedule: a ring of 256 counters
+// per device (128 bytes apart), each zeroed on the stream right before its
+// launch (a memset node under graph capture), so launches in flight never
+// share one.
+static int* next_tile_counter(cudaStream_t s) {
+  static std::mutex mu;
+  static int* bufs[64] = {nullptr};
+  static unsigned next[64] = {0};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+  int* p;
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    if (!bufs[dev] && cudaMalloc(&bufs[dev], 256 * 128) != cudaSuccess) {
+      bufs[dev] = nullptr;
+      return nullptr;
+    }
+    p = bufs[dev] + (next[dev]++ % 256) * 32;
+  }
+  if (cudaMemsetAsync(p, 0, sizeof(int), s) != cudaSuccess) return nullptr;
+  return p;
 }
 
 template <int STAGES>
@@ -777,7 +906,15 @@ static int launch_gemm_2sm_wide(const CUtensorMap& ma, const CUtensorMap& mb,
   static std::atomic<uint64_t> attr_done{0};
   if (int rc = set_smem_attr((const void*)gemm_bf16_tcgen05_2sm_wide<STAGES>, L::TOTAL, &attr_done)) return rc;
   const int sms = sm_budget();
-  int64_t clusters = g.tiles < sms / 2 ? g.tiles : sms / 2;
+  int64_t clusters = g.tiles < sms / 2 || !option(OPT_GEMM_PERSISTENT) ? g.tiles : sms / 2;
+  g.tile_counter = nullptr;
+  if (option(OPT_GEMM_DYNAMIC) && clusters < g.tiles) {
+    g.tile_counter = next_tile_counter(s);
+    if (!g.tile_counter) {
+      set_error("tile counter allocation failed");
+      return SPMD_ERR_CUDA;
+    }
+  }
   gemm_bf16_tcgen05_2sm_wide<STAGES><<<(unsigned)(2 * clusters), 384, L::TOTAL, s>>>(ma, mb, mc,
                                                                                      g, smaps);
   return launched(s);

@@ -17,7 +17,10 @@ from paper_2105_04663_b200 import _capi as C  # noqa: E402
 args = [a for a in sys.argv[1:] if not a.startswith("--")]
 M, N, K = (int(v) for v in args[:3]) if len(args) >= 3 else (16384, 65536, 8192)
 ncu = "--ncu" in sys.argv
-settings = [(g, r) for r in (0, 1) for g in (4, 8, 16, 32)]
+# (gemm_group, gemm_raster_n, gemm_hint, gemm_store_hint)
+settings = [(g, r, 0, 0) for r in (0, 1) for g in (4, 8, 16, 32)]
+if "--hints" in sys.argv:
+    settings = [(16, 0, h, sh) for h in (0, 1, 2) for sh in (0, 1)]
 st = torch.cuda.current_stream().cuda_stream
 a = torch.randn(M, K, device="cuda", dtype=torch.bfloat16)
 b = torch.randn(K, N, device="cuda", dtype=torch.bfloat16) * 0.01
@@ -30,8 +33,9 @@ def run():
 
 best = {}
 for rnd in range(1 if ncu else 3):
-    for g, r in settings:
-        with C.option("gemm_group", g), C.option("gemm_raster_n", r):
+    for g, r, h, sh in settings:
+        with C.option("gemm_group", g), C.option("gemm_raster_n", r), C.option("gemm_hint", h), \
+                C.option("gemm_store_hint", sh):
             if ncu:
                 run()
                 torch.cuda.synchronize()
@@ -45,7 +49,8 @@ for rnd in range(1 if ncu else 3):
             e1.record()
             torch.cuda.synchronize()
             ms = e0.elapsed_time(e1) / 5
-            best[(g, r)] = min(best.get((g, r), 1e9), ms)
-for (g, r), ms in sorted(best.items()):
-    print(json.dumps({"M": M, "N": N, "K": K, "group": g, "raster_n": r, "ms": round(ms, 3),
+            best[(g, r, h, sh)] = min(best.get((g, r, h, sh), 1e9), ms)
+for (g, r, h, sh), ms in sorted(best.items()):
+    print(json.dumps({"M": M, "N": N, "K": K, "group": g, "raster_n": r, "hint": h,
+                      "store_hint": sh, "ms": round(ms, 3),
                       "tflops": round(2.0 * M * N * K / ms / 1e9, 1)}), flush=True)
