@@ -1100,9 +1100,11 @@ int dot_tcgen05(const spmd_tensor& lhs, const spmd_tensor& rhs, const spmd_tenso
     bool okw = a_mn ? encode(&ma, lhs.data, va, 64, BK) : encode(&ma, lhs.data, va, BK, HALF);
     okw = okw && (b_mn ? encode(&mb, rhs.data, vb, 64, BK) : encode(&mb, rhs.data, vb, BK, HALF));
     if (okw) {
-      // 16 M-tiles per raster group (alternating A/B on the C2 GEMM shapes:
-      // +5% over 8 for 256 x 512 tiles, profiles/r1_gemm_wide_group_sweep.log)
-      if (group_opt <= 0) g.group = 16;
+      // Raster groups of 8 M-tiles under the dynamic tile order (ncu on
+      // FFN-in, profiles/r2_gemm_dyn_raster_ncu.csv: DRAM reads 12.5 GB vs
+      // 14.6 at 16 and 19.4 at 4, SM clock 1.43 vs 1.41 / 1.41 GHz under the
+      // power cap).  The round-1 static order preferred 16.
+      if (group_opt <= 0) g.group = option(OPT_GEMM_DYNAMIC) ? 8 : 16;
       g.mt = (g.M + BM2 - 1) / BM2;
       g.nt = (g.N + WBN - 1) / WBN;
       g.tiles = (int64_t)g.mt * g.nt * g.nb[0] * g.nb[1] * g.nb[2];
