@@ -327,6 +327,174 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
   }
 }
 
+// Wide variant: 256 x 512 pair tiles (two N=256 halves per K step, the whole
+// TMEM as one accumulator, 8 epilogue warps), 2 stages of A_hi/A_lo/B_hi/B_lo
+// = 96 KB per CTA.  L2 -> SM bytes per MMA cycle fall from 42 B/clk/SM (the
+// 256 x 256 kernel: 64 KB per 1536 cycles, at the L2 cap) to 31.
+template <int STAGES>
+struct SmemTW {
+  static constexpr int A_BYTES = THALF * TBK * 4;           // 16 KB
+  static constexpr int B_BYTES = 2 * THALF * TBK * 4;       // 32 KB: two N=256 halves
+  static constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;
+  static constexpr int BAR_OFF = STAGES * STAGE_BYTES;
+  static constexpr int TOTAL = BAR_OFF + 256 + 1024;
+};
+
+template <int STAGES>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
+    gemm_f32_3xtf32_2sm_wide(const __grid_constant__ CUtensorMap map_ah,
+                             const __grid_constant__ CUtensorMap map_al,
+                             const __grid_constant__ CUtensorMap map_bh,
+                             const __grid_constant__ CUtensorMap map_bl, TShape g) {
+  typedef SmemTW<STAGES> L;
+  constexpr int WN = 512, HN = 256;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint64_t* full = (uint64_t*)(smem + L::BAR_OFF);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 1;
+  uint32_t* tmem_slot = (uint32_t*)(tempty + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_rank();
+  const bool leader = rank == 0;
+  const int64_t cluster = blockIdx.x >> 1, nclusters = gridDim.x >> 1;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(tfull, 1);
+    mbar_init(tempty, 16);   // 8 epilogue warps x 2 CTAs
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                     smem_u32(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const int kblocks = (g.K + TBK - 1) / TBK;
+
+  if (warp == 0 && lane == 0) {
+    int s = 0;
+    uint32_t ph = 0;
+    for (int64_t t = cluster; t < g.tiles; t += nclusters) {
+      int b, m, n;
+      ttile_coords(g, t, b, m, n);
+      const int b0 = b % g.nb[0], b1 = (b / g.nb[0]) % g.nb[1], b2 = b / (g.nb[0] * g.nb[1]);
+      const int mrow = m * TBM + rank * THALF;
+      for (int kb = 0; kb < kblocks; ++kb) {
+        mbar_wait(&empty[s], ph ^ 1);
+        uint8_t* st = smem + s * L::STAGE_BYTES;
+        if (leader) mbar_expect_tx(&full[s], 2 * L::STAGE_BYTES);
+        const int k0 = kb * TBK;
+        tma_load_5d_2sm(st, &map_ah, &full[s], k0, mrow, b0, b1, b2);
+        tma_load_5d_2sm(st + L::A_BYTES, &map_al, &full[s], k0, mrow, b0, b1, b2);
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          const int nrow = n * WN + j * HN + rank * THALF;
+          tma_load_5d_2sm(st + 2 * L::A_BYTES + j * (L::B_BYTES / 2), &map_bh, &full[s], k0, nrow,
+                          b0, b1, b2);
+          tma_load_5d_2sm(st + 2 * L::A_BYTES + L::B_BYTES + j * (L::B_BYTES / 2), &map_bl,
+                          &full[s], k0, nrow, b0, b1, b2);
+        }
+        if (++s == STAGES) {
+          s = 0;
+          ph ^= 1;
+        }
+      }
+    }
+  } else if (warp == 1 && leader) {
+    const uint32_t idesc = make_idesc_tf32(TBM, HN, 0, 0);
+    int s = 0;
+    uint32_t ph = 0, acc_ph = 0;
+    for (int64_t t = cluster; t < g.tiles; t += nclusters) {
+      mbar_wait(tempty, acc_ph ^ 1);
+      tc_fence_after();
+      for (int kb = 0; kb < kblocks; ++kb) {
+        mbar_wait(&full[s], ph);
+        tc_fence_after();
+        uint32_t pred;
+        asm volatile("{\n.reg .pred P;\nelect.sync _|P, 0xffffffff;\nselp.u32 %0, 1, 0, P;\n}"
+                     : "=r"(pred));
+        if (pred) {
+          const uint32_t st = smem_u32(smem + s * L::STAGE_BYTES);
+          const uint32_t ah = st, al = st + L::A_BYTES;
+          const uint32_t bh = st + 2 * L::A_BYTES, bl = bh + L::B_BYTES;
+#pragma unroll
+          for (int k = 0; k < TBK / 8; ++k) {
+            const uint64_t dah = make_desc(ah + k * 32, 16, 1024);
+            const uint64_t dal = make_desc(al + k * 32, 16, 1024);
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+              const uint64_t dbh = make_desc(bh + j * (L::B_BYTES / 2) + k * 32, 16, 1024);
+              const uint64_t dbl = make_desc(bl + j * (L::B_BYTES / 2) + k * 32, 16, 1024);
+              const uint32_t d = tmem + j * HN;
+              tc_mma_2sm_tf32(d, dal, dbh, idesc, (kb | k) != 0);
+              tc_mma_2sm_tf32(d, dah, dbl, idesc, 1);
+              tc_mma_2sm_tf32(d, dah, dbh, idesc, 1);
+            }
+          }
+          tc_commit_2sm_mc(&empty[s]);
+          if (kb == kblocks - 1) tc_commit_2sm_mc(tfull);
+        }
+        __syncwarp();
+        if (++s == STAGES) {
+          s = 0;
+          ph ^= 1;
+        }
+      }
+      acc_ph ^= 1;
+    }
+  } else if (warp >= 4) {
+    // 8 epilogue warps: (TMEM lane quarter, column half)
+    const int ew = warp - 4, quarter = warp & 3, half = ew >> 2;
+    uint32_t acc_ph = 0;
+    for (int64_t t = cluster; t < g.tiles; t += nclusters) {
+      int b, m, n;
+      ttile_coords(g, t, b, m, n);
+      mbar_wait(tfull, acc_ph);
+      tc_fence_after();
+      const int row = m * TBM + rank * THALF + quarter * 32 + lane;
+      float* orow = g.out + (int64_t)b * g.out_batch + (int64_t)row * g.N;
+      const uint32_t tbase = tmem + ((uint32_t)(quarter * 32) << 16) + half * HN;
+#pragma unroll 1
+      for (int c0 = 0; c0 < HN; c0 += 32) {
+        uint32_t r[32];
+        tmem_ld32(tbase + c0, r);
+        const int col = n * WN + half * HN + c0;
+        if (row < g.M && col < g.N) {
+          if (col + 32 <= g.N && (g.N & 3) == 0) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+              reinterpret_cast<float4*>(orow + col)[j] =
+                  make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]),
+                              __uint_as_float(r[4 * j + 2]), __uint_as_float(r[4 * j + 3]));
+          } else {
+            for (int j = 0; j < 32 && col + j < g.N; ++j) orow[col + j] = __uint_as_float(r[j]);
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_leader(tempty);
+      acc_ph ^= 1;
+    }
+  }
+  tc_fence_before();
+  cluster_sync();
+  if (warp == 2) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+  }
+}
+
 // 5-D fp32 tensor map over an OperandView (element strides), 128B swizzle.
 static bool encode_f32(CUtensorMap* map, void* base, const OperandView& v, int box_inner,
                        int box_outer) {
@@ -385,17 +553,33 @@ int dot_tf32x3(const spmd_tensor& lhs, const spmd_tensor& rhs, const spmd_tensor
   g.N = lay.N;
   g.K = lay.K;
   for (int i = 0; i < 3; ++i) g.nb[i] = lay.nb[i];
-  g.mt = (g.M + TBM - 1) / TBM;
-  g.nt = (g.N + TBN - 1) / TBN;
   g.group = 8;
-  g.tiles = (int64_t)g.mt * g.nt * g.nb[0] * g.nb[1] * g.nb[2];
   g.out = (float*)out.data;
   g.out_batch = (int64_t)g.M * g.N;
+  const int sms = sm_budget();
+  if (g.N >= 512 && option(OPT_GEMM_MODE) == 3) {
+    g.mt = (g.M + TBM - 1) / TBM;
+    g.nt = (g.N + 511) / 512;
+    g.tiles = (int64_t)g.mt * g.nt * g.nb[0] * g.nb[1] * g.nb[2];
+    typedef SmemTW<2> LW;
+    static_assert(LW::TOTAL <= 232448, "3xTF32 wide GEMM smem");
+    static std::atomic<uint64_t> attr_w{0};
+    if (int rc = set_smem_attr((const void*)gemm_f32_3xtf32_2sm_wide<2>, LW::TOTAL, &attr_w))
+      return rc;
+    const int64_t clusters = g.tiles < sms / 2 ? g.tiles : sms / 2;
+    gemm_f32_3xtf32_2sm_wide<2><<<(unsigned)(2 * clusters), 384, LW::TOTAL, s>>>(mah, mal, mbh,
+                                                                               mbl, g);
+    rc = launched(s);
+    cudaFreeAsync(scratch, s);
+    return rc;
+  }
+  g.mt = (g.M + TBM - 1) / TBM;
+  g.nt = (g.N + TBN - 1) / TBN;
+  g.tiles = (int64_t)g.mt * g.nt * g.nb[0] * g.nb[1] * g.nb[2];
   typedef SmemT<3> L;
   static_assert(L::TOTAL <= 232448, "3xTF32 GEMM smem");
   static std::atomic<uint64_t> attr_done{0};
   if (int rc = set_smem_attr((const void*)gemm_f32_3xtf32_2sm<3>, L::TOTAL, &attr_done)) return rc;
-  const int sms = sm_budget();
   const int64_t clusters = g.tiles < sms / 2 ? g.tiles : sms / 2;
   gemm_f32_3xtf32_2sm<3><<<(unsigned)(2 * clusters), 256, L::TOTAL, s>>>(mah, mal, mbh, mbl, g);
   rc = launched(s);
