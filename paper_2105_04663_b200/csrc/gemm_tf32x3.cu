@@ -514,6 +514,24 @@ static bool encode_f32(CUtensorMap* map, void* base, const OperandView& v, int b
          CUDA_SUCCESS;
 }
 
+// The hi / lo scratch comes from the device's stream-ordered pool.  Its
+// default release threshold (0) hands freed memory back to the driver at
+// every synchronisation, so each call re-mapped ~GBs (measured: 3xTF32 calls
+// in a fresh process at 60-130 instead of ~240 TF/s); keep it cached.
+static void keep_pool_memory() {
+  static std::atomic<uint64_t> done{0};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return;
+  const uint64_t bit = 1ull << dev;
+  if (done.load() & bit) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t thr = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  done.fetch_or(bit);
+}
+
 // f32 Dot -> 3xTF32 tcgen05 GEMM; SPMD_ERR_UNSUPPORTED when the layout or the
 // size does not qualify (the caller then runs the SIMT fp64 kernel).
 int dot_tf32x3(const spmd_tensor& lhs, const spmd_tensor& rhs, const spmd_tensor& out,
@@ -525,6 +543,7 @@ int dot_tf32x3(const spmd_tensor& lhs, const spmd_tensor& rhs, const spmd_tensor
   // small Dots (the parity-sized golden cases) stay on the exact fp64 path
   if (lay.M < 256 || lay.N < 256 || lay.K < 64) return SPMD_ERR_UNSUPPORTED;
   const int64_t na = numel(lhs) * nparts, nb = numel(rhs) * nparts;
+  keep_pool_memory();
   float* scratch = nullptr;
   if (cudaMallocAsync((void**)&scratch, (size_t)(2 * (na + nb)) * 4, s) != cudaSuccess) {
     cudaGetLastError();
@@ -557,7 +576,16 @@ int dot_tf32x3(const spmd_tensor& lhs, const spmd_tensor& rhs, const spmd_tensor
   g.out = (float*)out.data;
   g.out_batch = (int64_t)g.M * g.N;
   const int sms = sm_budget();
-  if (g.N >= 512 && option(OPT_GEMM_MODE) == 3) {
+  // 256 x 512 tiles move fewer L2 bytes per MMA, 256 x 256 tiles quantise
+  // better over the 74 CTA pairs: take the wide tile unless its last wave is
+  // emptier (measured at C1's 8192 x 4096 x 4096: 256 tiles = 3.5 waves, wide
+  // 241 vs 266 TF/s; 8192^3: wide 278 vs 275)
+  const int64_t nbt = (int64_t)g.nb[0] * g.nb[1] * g.nb[2];
+  const int64_t t_wide = (int64_t)((g.M + TBM - 1) / TBM) * ((g.N + 511) / 512) * nbt;
+  const int64_t t_sq = (int64_t)((g.M + TBM - 1) / TBM) * ((g.N + TBN - 1) / TBN) * nbt;
+  const int64_t pairs = sms / 2;
+  auto wave_eff = [&](int64_t t) { return (double)t / (double)(((t + pairs - 1) / pairs) * pairs); };
+  if (g.N >= 512 && option(OPT_GEMM_MODE) == 3 && wave_eff(t_wide) >= wave_eff(t_sq) - 0.02) {
     g.mt = (g.M + TBM - 1) / TBM;
     g.nt = (g.N + 511) / 512;
     g.tiles = (int64_t)g.mt * g.nt * g.nb[0] * g.nb[1] * g.nb[2];

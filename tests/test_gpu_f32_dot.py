@@ -49,11 +49,12 @@ def _err(a, b):
 
 @pytest.mark.parametrize("mode", [3, 2])
 @pytest.mark.parametrize("M,N,K", [(256, 256, 64), (1024, 768, 512), (4096, 4096, 4096),
-                                   (300, 520, 1000), (2048, 256, 8192), (2304, 3072, 2048)])
+                                   (300, 520, 1000), (2048, 256, 8192), (2304, 3072, 2048),
+                                   (4096, 8192, 1024)])
 def test_f32_dot_3xtf32_vs_float64(M, N, K, mode):
     """x[M,K] . w[K,N] (B MN-major, the C1 weight layout), partial tiles and
-    long K included; gemm_mode 3: 256 x 512 pair tiles when N >= 512 (else
-    256 x 256), 2: always 256 x 256."""
+    long K included; gemm_mode 3: 256 x 512 pair tiles when N >= 512 and the
+    waves quantise as well (else 256 x 256), 2: always 256 x 256."""
     import torch
     from paper_2105_04663_b200 import _capi as C
     g = torch.Generator(device="cuda").manual_seed(M + N + K)
