@@ -408,17 +408,25 @@ class Executor:
             elif mode == "critical" and st.ins.id in self._act_staged:
                 st.lane = 2
             elif mode == "critical" and eng == 4 and st.ins.id in self._staged_exposed:
-                # exposed staged gathers: lane 2, which waits only for the
-                # first staging phase (SPMD_STAGE_PHASES=1: alternate lanes,
-                # so e.g. the x and w_q pulls overlap)
-                st.lane = 2 if os.environ.get("SPMD_STAGE_PHASES", "2") != "1" else \
-                    2 - self._staged_exposed.index(st.ins.id) % 2
+                # exposed staged gathers wait only for the first staging phase;
+                # they alternate lanes 2 and 3, so e.g. the x and w_q pulls
+                # before the first GEMM run on two copy engines at once (one
+                # lane serialised them: 0.29 + 0.32 ms exposed at 2x2,
+                # profiles/r2_timeline_c2_2x2.log).  SPMD_STAGE_PHASES=1:
+                # alternate lanes 2 and 1 (round 1)
+                k = self._staged_exposed.index(st.ins.id) % 2
+                if os.environ.get("SPMD_STAGE_PHASES", "2") == "1":
+                    st.lane = 2 - k
+                else:
+                    st.lane = 2 + (k if os.environ.get("SPMD_EXPOSED_SPLIT", "1") != "0" else 0)
             elif mode == "critical" and eng not in (0, 3, 4):
                 st.lane = 2
-        if any(st.lane == 2 for st in self.steps):
-            torch = _torch()
-            self.comm_streams.append(torch.cuda.Stream(device=self.device,
-                                                       priority=self.comm_stream.priority))
+        torch = _torch()
+        for lane in (2, 3):
+            if any(st.lane >= lane for st in self.steps if st.coll) and \
+                    len(self.comm_streams) < lane:
+                self.comm_streams.append(torch.cuda.Stream(device=self.device,
+                                                           priority=self.comm_stream.priority))
 
     def _shape(self, vid: str) -> Shape:
         return self.by_id[vid].shape
