@@ -74,6 +74,49 @@ __global__ void strided_copy_kernel(const T* __restrict__ src, T* __restrict__ d
   if (a.fence_sys) __threadfence_system();
 }
 
+// Row-chunk variant of strided_copy_kernel for a contiguous innermost dim of
+// >= ROW_MIN_VECS vectors: rows = nparts x (outer dims); each block handles
+// 256 x ROW_U vectors of one row with ROW_U independent loads in flight.
+template <typename T>
+__global__ void __launch_bounds__(256) row_copy_kernel(const T* __restrict__ src,
+                                                       T* __restrict__ dst, CopyArgs a,
+                                                       int64_t nparts, int64_t chunks) {
+  constexpr int V = 16 / sizeof(T);
+  const int r = a.rank - 1;                    // dim r is the row (contiguous on both sides)
+  const int64_t per_row = a.shape[r] / V;
+  int64_t rows_per_part = 1;
+  for (int k = 0; k < r; ++k) rows_per_part *= a.shape[k];
+  const int64_t rows = rows_per_part * nparts;
+  for (int64_t b = blockIdx.x; b < rows * chunks; b += gridDim.x) {
+    const int64_t row = b / chunks, chunk = b - row * chunks;
+    const int64_t p = row / rows_per_part;
+    int64_t q = row - p * rows_per_part;
+    int64_t so = a.sbase + p * a.spart, d0 = a.dbase + p * a.dpart;
+    for (int k = r - 1; k >= 0; --k) {
+      const int64_t c = q % a.shape[k];
+      q /= a.shape[k];
+      so += c * a.sst[k];
+      d0 += c * a.dst[k];
+    }
+    for (int k = 0; k < a.ndyn; ++k) {
+      int64_t s0 = a.dyn_start[k][p];
+      s0 = s0 < 0 ? 0 : (s0 > a.dyn_max[k] ? a.dyn_max[k] : s0);
+      if (a.dyn_on_dst) d0 += s0 * a.dyn_mul[k]; else so += s0 * a.dyn_mul[k];
+    }
+    const uint4* s4 = reinterpret_cast<const uint4*>(src + so);
+    uint4* d4 = reinterpret_cast<uint4*>(dst + d0);
+    const int64_t v0 = chunk * (256 * ROW_U) + threadIdx.x;
+    uint4 v[ROW_U];
+#pragma unroll
+    for (int u = 0; u < ROW_U; ++u)
+      if (v0 + u * 256 < per_row) v[u] = __ldcs(s4 + v0 + u * 256);
+#pragma unroll
+    for (int u = 0; u < ROW_U; ++u)
+      if (v0 + u * 256 < per_row) __stcs(d4 + v0 + u * 256, v[u]);
+  }
+  if (a.fence_sys) __threadfence_system();
+}
+
 // dst[dbase + p*dpart + i] = src[sbase + p*spart] for i < n, 16 bytes per store.
 template <typename T>
 __global__ void splat_kernel(const T* __restrict__ src, T* __restrict__ dst, CopyArgs a,
@@ -160,6 +203,52 @@ __global__ void pad_gather_kernel(const T* __restrict__ src, const T* __restrict
   }
 }
 
+// Row-chunk variant of pad_gather_kernel: every output row (all dims but the
+// last) is decided once per block; the last dim may carry its own low / high
+// padding (vector units).
+template <typename T>
+__global__ void __launch_bounds__(256) pad_rows_kernel(const T* __restrict__ src,
+                                                       const T* __restrict__ value,
+                                                       T* __restrict__ dst, PadArgs a,
+                                                       int64_t nparts, int64_t chunks) {
+  constexpr int V = 16 / sizeof(T);
+  const int r = a.rank - 1;
+  const int64_t per_row = a.od[r];            // output vectors per row
+  int64_t rows_per_part = 1;
+  for (int k = 0; k < r; ++k) rows_per_part *= a.od[k];
+  const int64_t rows = rows_per_part * nparts;
+  for (int64_t b = blockIdx.x; b < rows * chunks; b += gridDim.x) {
+    const int64_t row = b / chunks, chunk = b - row * chunks;
+    const int64_t p = row / rows_per_part;
+    int64_t q = row - p * rows_per_part;
+    int64_t so = 0;
+    bool inside = true;
+    for (int k = r - 1; k >= 0; --k) {
+      const int64_t c = q % a.od[k] - a.low[k];
+      q /= a.od[k];
+      inside = inside && c >= 0 && c < a.id[k];
+      so += c * a.ist[k];
+    }
+    T f[V];
+    const T pv = value[p];
+#pragma unroll
+    for (int j = 0; j < V; ++j) f[j] = pv;
+    const uint4 fill = *reinterpret_cast<uint4*>(f);
+    const uint4* s4 = reinterpret_cast<const uint4*>(src + p * a.spart) + so;
+    uint4* d4 = reinterpret_cast<uint4*>(dst + p * a.dpart) + (row - p * rows_per_part) * per_row;
+    const int64_t v0 = chunk * (256 * ROW_U) + threadIdx.x;
+    uint4 v[ROW_U];
+#pragma unroll
+    for (int u = 0; u < ROW_U; ++u) {
+      const int64_t c = v0 + u * 256 - a.low[r];
+      v[u] = (inside && c >= 0 && c < a.id[r]) ? __ldcs(s4 + c) : fill;
+    }
+#pragma unroll
+    for (int u = 0; u < ROW_U; ++u)
+      if (v0 + u * 256 < per_row) __stcs(d4 + v0 + u * 256, v[u]);
+  }
+}
+
 // Merge dims contiguous in both views; drop unit dims.
 static void canonicalize(CopyArgs& a) {
   int64_t sh[SPMD_MAX_RANK], ss[SPMD_MAX_RANK], ds[SPMD_MAX_RANK];
@@ -230,6 +319,15 @@ int launch_copy(const void* src, void* dst, int dtype, CopyArgs a, int64_t npart
         strided_copy_kernel<T, uint64_t, 16 / sizeof(T), true><<<grid_for(w, 256), 256, 0, s>>>(
             (const T*)src, (T*)dst, a, nparts);
     });
+    return launched(s);
+  }
+  if (vec && a.shape[a.rank - 1] / V >= ROW_MIN_VECS) {
+    const int64_t chunks = (a.shape[a.rank - 1] / V + 256 * ROW_U - 1) / (256 * ROW_U);
+    int64_t rows = nparts;
+    for (int k = 0; k < a.rank - 1; ++k) rows *= a.shape[k];
+    SPMD_DISPATCH_BYTES(dtype, T,
+                        row_copy_kernel<T><<<row_grid(rows, chunks), 256, 0, s>>>(
+                            (const T*)src, (T*)dst, a, nparts, chunks));
     return launched(s);
   }
   // The kernel walks groups of V consecutive last-dim elements (element-unit
@@ -381,6 +479,16 @@ static int pad_edges(const spmd_tensor& in, const spmd_tensor& value, const spmd
     for (int k = 0; k < r - 1; ++k) a.ist[k] /= V;
   }
   a.per = a.dpart / (vec ? V : 1);
+  if (vec && a.od[r - 1] >= ROW_MIN_VECS) {
+    const int64_t chunks = (a.od[r - 1] + 256 * ROW_U - 1) / (256 * ROW_U);
+    int64_t rows = nparts;
+    for (int k = 0; k < r - 1; ++k) rows *= a.od[k];
+    SPMD_DISPATCH_BYTES(out.dtype, T,
+                        pad_rows_kernel<T><<<row_grid(rows, chunks), 256, 0, s>>>(
+                            (const T*)in.data, (const T*)value.data, (T*)out.data, a, nparts,
+                            chunks));
+    return launched(s);
+  }
   const int64_t work = a.per * nparts;
   const bool small = work < (int64_t)1 << 31;
   SPMD_DISPATCH_BYTES(out.dtype, T, {

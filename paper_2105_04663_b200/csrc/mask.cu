@@ -46,6 +46,44 @@ __global__ void mask_range_kernel(const T* __restrict__ in, T* __restrict__ out,
   }
 }
 
+// Row-chunk variant: rows = [P, outer, n_axis], each `inner` contiguous;
+// the predicate is decided once per block.
+template <typename T>
+__global__ void __launch_bounds__(256) mask_rows_kernel(const T* __restrict__ in,
+                                                        T* __restrict__ out,
+                                                        const int32_t* __restrict__ offset,
+                                                        const T* __restrict__ fill,
+                                                        int64_t outer, int64_t n_axis,
+                                                        int64_t inner, int64_t nparts,
+                                                        int64_t low, int64_t high,
+                                                        int64_t chunks) {
+  constexpr int V = 16 / sizeof(T);
+  const int64_t per_row = inner / V;
+  const int64_t rows_per_part = outer * n_axis;
+  const int64_t rows = rows_per_part * nparts;
+  for (int64_t b = blockIdx.x; b < rows * chunks; b += gridDim.x) {
+    const int64_t row = b / chunks, chunk = b - row * chunks;
+    const int64_t p = row / rows_per_part;
+    const int64_t gidx = (row - p * rows_per_part) % n_axis + offset[p];
+    const bool keep = gidx < high && gidx >= low;
+    T f[V];
+    const T fv = fill[p];
+#pragma unroll
+    for (int j = 0; j < V; ++j) f[j] = fv;
+    const uint4 fillv = *reinterpret_cast<uint4*>(f);
+    const uint4* s4 = reinterpret_cast<const uint4*>(in) + row * per_row;
+    uint4* d4 = reinterpret_cast<uint4*>(out) + row * per_row;
+    const int64_t v0 = chunk * (256 * ROW_U) + threadIdx.x;
+    uint4 v[ROW_U];
+#pragma unroll
+    for (int u = 0; u < ROW_U; ++u)
+      v[u] = (keep && v0 + u * 256 < per_row) ? __ldcs(s4 + v0 + u * 256) : fillv;
+#pragma unroll
+    for (int u = 0; u < ROW_U; ++u)
+      if (v0 + u * 256 < per_row) __stcs(d4 + v0 + u * 256, v[u]);
+  }
+}
+
 // Halo window (exchange_and_slice, reference formatting.py:109-182): the
 // per-device window = DS(mask(concat(left_halo, shard, right_halo)), start)
 // read straight from the three pieces in one pass.
@@ -241,6 +279,14 @@ extern "C" int spmd_mask_range(spmd_tensor in, spmd_tensor offset, spmd_tensor f
   const int V = 16 / es;
   const bool vec = inner % V == 0 && (reinterpret_cast<uintptr_t>(in.data) & 15) == 0 &&
                    (reinterpret_cast<uintptr_t>(out.data) & 15) == 0;
+  if (vec && inner / V >= ROW_MIN_VECS) {
+    const int64_t chunks = (inner / V + 256 * ROW_U - 1) / (256 * ROW_U);
+    SPMD_DISPATCH_BYTES(in.dtype, T,
+                        mask_rows_kernel<T><<<row_grid(outer * n * nparts, chunks), 256, 0, s>>>(
+                            (const T*)in.data, (T*)out.data, (const int32_t*)offset.data,
+                            (const T*)fill.data, outer, n, inner, nparts, low, high, chunks));
+    return launched(s);
+  }
   SPMD_DISPATCH_BYTES(in.dtype, T, {
     if (vec)
       mask_range_kernel<T, 16 / sizeof(T)><<<grid_for(outer * n * inner * nparts / V, 256), 256, 0,

@@ -116,7 +116,17 @@ __global__ void moe_dispatch_kernel(const uint16_t* __restrict__ x, const int32_
     const int e = expert[a];
     const uint4* src = reinterpret_cast<const uint4*>(x + t * (int64_t)M);
     uint4* dst = reinterpret_cast<uint4*>(out + ((row * E + e) * (int64_t)C + sl) * M);
-    for (int i = lane; i < M / V; i += 32) dst[i] = __ldcs(src + i);
+    // 4 independent 16-byte loads in flight per lane (one row is M/V vectors)
+    const int nv = M / V;
+    for (int i0 = lane; i0 < nv; i0 += 128) {
+      uint4 v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (i0 + 32 * u < nv) v[u] = __ldcs(src + i0 + 32 * u);
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (i0 + 32 * u < nv) dst[i0 + 32 * u] = v[u];
+    }
   }
 }
 

@@ -53,6 +53,9 @@ def _np_pad(x, v, low, high, interior):
     ((3, 4, 32), (0, 1, 16), (2, 0, 0), (0, 0, 0), "pred"),
     ((4, 9), (2, 1), (1, 0), (1, 2), "s32"),              # interior: fill+copy path
     ((16,), (0,), (0,), (0,), "s32"),                     # no-op pad
+    ((9, 12288), (0, 0), (7, 0), (0, 0), "f32"),          # row-chunk kernel (3072 vectors)
+    ((6, 8200), (1, 8), (2, 0), (0, 0), "f32"),           # row-chunk kernel, padded rows
+    ((5, 16388), (0, 4), (1, 4), (0, 0), "s32"),          # row-chunk, partial last chunk
 ])
 def test_pad_matches_numpy(dims, low, high, interior, dt):
     from paper_2105_04663_b200.ir import DType
@@ -70,13 +73,14 @@ def test_pad_matches_numpy(dims, low, high, interior, dt):
         np.testing.assert_array_equal(got[p], _np_pad(x[p], vals[p], low, high, interior))
 
 
+@pytest.mark.parametrize("W", [64, 12292])    # generic / row-chunk copy kernel
 @pytest.mark.parametrize("update", [False, True])
-def test_dynamic_slice_clamped_per_partition(update):
+def test_dynamic_slice_clamped_per_partition(update, W):
     import torch
     from paper_2105_04663_b200 import _capi as C
     from paper_2105_04663_b200.executor import desc
     from paper_2105_04663_b200.ir import DType, Shape
-    P, R, W, r = 4, 40, 64, 9
+    P, R, r = 4, 40, 9
     rng = np.random.default_rng(5)
     x = rng.standard_normal((P, R, W)).astype(np.float32)
     starts0 = np.array([-3, 5, 31, 100], dtype=np.int32)   # clamp low / mid / edge / high
@@ -142,3 +146,32 @@ def test_halo_window_matches_numpy(inner):
         keep = (g >= low) & (g < high)
         masked = np.where(keep[None, :, None], buf, fills[p])
         np.testing.assert_array_equal(got[p], masked[:, s0:s0 + window])
+
+
+@pytest.mark.parametrize("inner", [8, 16384 + 36])      # element kernel / row-chunk kernel
+def test_mask_range_matches_select_chain(inner):
+    """spmd_mask_range = select(low <= iota + offset[p] < high, x, fill[p])
+    (reference partitioner.py:205-247 select_range / mask_uneven)."""
+    import torch
+    from paper_2105_04663_b200 import _capi as C
+    from paper_2105_04663_b200.executor import desc
+    from paper_2105_04663_b200.ir import DType, Shape
+    P, outer, n = 3, 2, 13
+    rng = np.random.default_rng(inner)
+    x = rng.standard_normal((P, outer, n, inner)).astype(np.float32)
+    offs = np.array([0, 10, 27], dtype=np.int32)
+    fills = np.array([-1.0, 0.0, np.inf], dtype=np.float32)
+    low, high = 3, 30
+    out = torch.empty((P, outer, n, inner), device="cuda")
+    sh = Shape((outer, n, inner), DType.F32)
+    xt, ot, ft = _dev(x), _dev(offs), _dev(fills)      # keep the buffers alive
+    C.check(C.lib().spmd_mask_range(desc(xt, sh), desc(ot, Shape((), DType.S32)),
+                                     desc(ft, Shape((), DType.F32)), desc(out, sh), 1,
+                                     low, high, 1, P, torch.cuda.current_stream().cuda_stream),
+            "mask_range")
+    torch.cuda.synchronize()
+    got = out.cpu().numpy()
+    for p in range(P):
+        g = np.arange(n) + offs[p]
+        keep = ((g >= low) & (g < high))[None, :, None]
+        np.testing.assert_array_equal(got[p], np.where(keep, x[p], fills[p]))
