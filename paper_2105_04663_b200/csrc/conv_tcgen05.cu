@@ -369,8 +369,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
         }
       }
     }
-  } else if (warp == 1 && lane == 0 && leader) {
+  } else if (warp == 1 && leader) {
+    // The whole warp runs the loop (uniform control flow: descriptors and
+    // counters in uniform registers), one elected lane issues.  A conv MMA
+    // (UMMA 256 x 128 x 16) is only 64 tensor cycles, so the per-MMA issue
+    // cost is on the critical path (ncu: tensor pipe 62% active): the
+    // descriptors are precomputed and advanced by constant offsets.
     const uint32_t idesc = make_idesc(2 * CBM, 2 * CHALF, 0, 1);
+    const uint64_t a0 = make_desc(smem_u32(smem), 16, 1024);
+    const uint64_t w0d = make_desc(smem_u32(smem + L::W_OFF), CBK * 128, 1024);
+    constexpr uint32_t STAGE16 = L::STAGE_BYTES >> 4, B16 = L::B_BYTES >> 4, A16 = L::A_BYTES >> 4;
     int s = 0;
     uint32_t ph = 0;
     int acc = 0;
@@ -384,36 +392,44 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
       tc_fence_after();
       const uint32_t d_tmem = tmem + acc * 2 * CHALF;
       const int nstage = TAPS ? g.KH * g.cin_blocks : g.kblocks;
+      int kh = 0, cb = 0;
       for (int kb = 0; kb < nstage; ++kb) {
         mbar_wait(&full[s], ph);
         tc_fence_after();
-        const uint32_t sa = smem_u32(smem + s * L::STAGE_BYTES);
-        if (TAPS) {
-          const int kh = kb / g.cin_blocks, cb = kb % g.cin_blocks;
+        if (elect_one()) {
+          const uint64_t ad = a0 + (uint64_t)(s * STAGE16);
+          if (TAPS) {
 #pragma unroll
-          for (int kw = 0; kw < TAPS; ++kw) {
-            const uint32_t sb =
-                smem_u32(smem + L::W_OFF + ((kh * g.KW + kw) * g.cin_blocks + cb) * L::B_BYTES);
+            for (int kw = 0; kw < TAPS; ++kw) {
+              const uint64_t bd = w0d + (uint64_t)(((kh * g.KW + kw) * g.cin_blocks + cb) * B16);
+#pragma unroll
+              for (int k = 0; k < CBK / 16; ++k)
+                tc_mma_2sm(d_tmem, ad + (uint64_t)((kw * 128 + k * 32) >> 4),
+                           bd + (uint64_t)((k * 2048) >> 4), idesc, (kb | kw | k) != 0);
+            }
+          } else {
+            const uint64_t bd = WRES ? w0d + (uint64_t)(kb * B16)
+                                     : make_desc(smem_u32(smem + s * L::STAGE_BYTES) + A16 * 16,
+                                                 CBK * 128, 1024);
 #pragma unroll
             for (int k = 0; k < CBK / 16; ++k)
-              tc_mma_2sm(d_tmem, make_desc(sa + kw * 128 + k * 32, 16, 1024),
-                         make_desc(sb + k * 2048, CBK * 128, 1024), idesc, (kb | kw | k) != 0);
+              tc_mma_2sm(d_tmem, ad + (uint64_t)((k * 32) >> 4),
+                         bd + (uint64_t)((k * 2048) >> 4), idesc, (kb | k) != 0);
           }
-        } else {
-          const uint32_t sb =
-              WRES ? smem_u32(smem + L::W_OFF + kb * L::B_BYTES) : sa + L::A_BYTES;
-#pragma unroll
-          for (int k = 0; k < CBK / 16; ++k)
-            tc_mma_2sm(d_tmem, make_desc(sa + k * 32, 16, 1024),
-                       make_desc(sb + k * 2048, CBK * 128, 1024), idesc, (kb | k) != 0);
+          tc_commit_2sm_mc(&empty[s]);
         }
-        tc_commit_2sm_mc(&empty[s]);
+        __syncwarp();
+        if (++cb == g.cin_blocks) {
+          cb = 0;
+          ++kh;
+        }
         if (++s == STAGES) {
           s = 0;
           ph ^= 1;
         }
       }
-      tc_commit_2sm_mc(&tfull[acc]);
+      if (elect_one()) tc_commit_2sm_mc(&tfull[acc]);
+      __syncwarp();
       if (++acc == 2) {
         acc = 0;
         acc_ph ^= 1;
