@@ -1,4 +1,4 @@
-"""The N>1 host path on CPU with real processes (gloo, world_size 2 and 4).
+"""The N>1 host path on CPU with real processes (gloo, world_size 2, 4 and 8).
 
 Each rank does what a GPU rank does in bench.py / scripts/multi_gpu_check.py:
 partitions the same annotated graph (both planners), takes partition id =
@@ -28,6 +28,11 @@ CASES_2 = ["priority_fig4", "acc5_reshape", "shift_8_1_0_2", "c2_1x2", "c3_moe_2
 CASES_4 = ["c1_8x16x32x24", "ffw_final", "ffw_attempt", "acc7_moe", "c3_moe_4", "c4_conv_4",
            "acc5_pad", "acc5_reverse", "acc5_slice", "rotate_8_3_4", "c2_2x2", "rand25",
            "rand110"] + C5W_4
+# the 8-device configs the scaling run's N=8 executes (C2 2x4 / 4x2 / 1x8,
+# C3 8 experts, C4 8 shards and 2x4, C5 over 8, the C2 training step)
+CASES_8 = ["c2_2x4", "c2_4x2", "c2_1x8", "c3_moe_8", "c4_conv_8", "c4_conv_2x4",
+           "c5_a2a_1001x16", "c5_repl_999x16", "c5_reduce_sum_16x1001", "c2_train_2x4",
+           "pipe_gpipe_L8_M8_add", "rand13"]
 
 
 def _free_port():
@@ -105,7 +110,7 @@ def _work(rank, world, port, names, q):
         q.put(failures)
 
 
-@pytest.mark.parametrize("world,names", [(2, CASES_2), (4, CASES_4)])
+@pytest.mark.parametrize("world,names", [(2, CASES_2), (4, CASES_4), (8, CASES_8)])
 def test_multiprocess_partitioned_execution(world, names):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
