@@ -211,7 +211,9 @@ def _traffic_for(top, prog):
         lb, rb, lc, rc, lf, rf = dot_dim_lists(top.attrs, a.rank, b.rank)
         prod = lambda s, ds: int(__import__("math").prod(s.dims[d] for d in ds))
         mnk = [prod(a, lb + lf), prod(b, rf), prod(a, lc)]
-        for fn in sorted(glob.glob(os.path.join(ROOT, "profiles", "*_top_kernel_traffic.json"))):
+        # newest round first
+        for fn in sorted(glob.glob(os.path.join(ROOT, "profiles", "*_top_kernel_traffic.json")),
+                         reverse=True):
             with open(fn) as f:
                 t = json.load(f)
             if list(t["shape_mnk"]) == mnk:
