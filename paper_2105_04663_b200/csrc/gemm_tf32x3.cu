@@ -76,17 +76,33 @@ __device__ __forceinline__ void ttile_coords(const TShape& g, int64_t t, int& b,
   n = rr / gs;
 }
 
+__device__ __forceinline__ void split1(float v, float& h, float& l) {
+  uint32_t u;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(u) : "f"(v));
+  h = __uint_as_float(u);
+  l = isfinite(v) ? v - h : 0.f;
+}
+
+// K-major operand: elementwise split, 16-byte vectors (scalar tail / when
+// misaligned).
 __global__ void split_tf32_kernel(const float* __restrict__ x, float* __restrict__ hi,
                                   float* __restrict__ lo, int64_t n) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const float v = x[i];
-    uint32_t h;
-    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(h) : "f"(v));
-    const float hf = __uint_as_float(h);
-    hi[i] = hf;
-    lo[i] = isfinite(v) ? v - hf : 0.f;
+  const bool vec = ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(hi) |
+                     reinterpret_cast<uintptr_t>(lo)) & 15) == 0;
+  const int64_t nv = vec ? n / 4 : 0;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nv; i += stride) {
+    const float4 v = __ldcs(reinterpret_cast<const float4*>(x) + i);
+    float4 h, l;
+    split1(v.x, h.x, l.x);
+    split1(v.y, h.y, l.y);
+    split1(v.z, h.z, l.z);
+    split1(v.w, h.w, l.w);
+    reinterpret_cast<float4*>(hi)[i] = h;
+    reinterpret_cast<float4*>(lo)[i] = l;
   }
+  for (int64_t i = nv * 4 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride)
+    split1(x[i], hi[i], lo[i]);
 }
 
 // MN-major operand (MN contiguous, K strided) -> K-major dense hi / lo copies
@@ -99,31 +115,72 @@ struct SplitView {
   int64_t bsize[3], bstride[3];     // batch dims (innermost first)
 };
 
-__global__ void split_tf32_transpose_kernel(const float* __restrict__ x, SplitView v,
-                                            float* __restrict__ hi, float* __restrict__ lo) {
-  __shared__ float tile[32][33];
+// 64 x 64 tiles, 256 threads: 16-byte loads along MN and 16-byte stores
+// along K (the 32 x 32 / 4-byte version ran at 3.1 TB/s on C1's weight).
+__global__ void __launch_bounds__(256) split_tf32_transpose_kernel(const float* __restrict__ x,
+                                                                   SplitView v,
+                                                                   float* __restrict__ hi,
+                                                                   float* __restrict__ lo) {
+  __shared__ float tile[64][65];
   const int64_t b = blockIdx.z;
   int64_t boff = 0, r = b;
   for (int i = 0; i < 3; ++i) {
     boff += (r % v.bsize[i]) * v.bstride[i];
     r /= v.bsize[i];
   }
-  const int64_t mn0 = (int64_t)blockIdx.x * 32, k0 = (int64_t)blockIdx.y * 32;
-  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
-    const int64_t k = k0 + i, mn = mn0 + threadIdx.x;
-    tile[i][threadIdx.x] = (k < v.k && mn < v.mn) ? x[boff + k * v.st_k + mn] : 0.f;
+  const int64_t mn0 = (int64_t)blockIdx.x * 64, k0 = (int64_t)blockIdx.y * 64;
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;   // 16 x 16
+  const bool vec_in = (v.mn & 3) == 0 && (v.st_k & 3) == 0 && (boff & 3) == 0 &&
+                      (reinterpret_cast<uintptr_t>(x) & 15) == 0;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int kk = ty + 16 * i;
+    const int64_t k = k0 + kk, mn = mn0 + 4 * tx;
+    float4 f = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (k < v.k) {
+      const float* src = x + boff + k * v.st_k + mn;
+      if (vec_in && mn + 3 < v.mn) {
+        f = __ldcs(reinterpret_cast<const float4*>(src));
+      } else {
+        if (mn < v.mn) f.x = src[0];
+        if (mn + 1 < v.mn) f.y = src[1];
+        if (mn + 2 < v.mn) f.z = src[2];
+        if (mn + 3 < v.mn) f.w = src[3];
+      }
+    }
+    tile[kk][4 * tx] = f.x;
+    tile[kk][4 * tx + 1] = f.y;
+    tile[kk][4 * tx + 2] = f.z;
+    tile[kk][4 * tx + 3] = f.w;
   }
   __syncthreads();
-  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
-    const int64_t mn = mn0 + i, k = k0 + threadIdx.x;
-    if (mn < v.mn && k < v.k) {
-      const float val = tile[threadIdx.x][i];
+  const bool vec_out = (v.k & 3) == 0 && (reinterpret_cast<uintptr_t>(hi) & 15) == 0 &&
+                       (reinterpret_cast<uintptr_t>(lo) & 15) == 0;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int mm = ty + 16 * i;
+    const int64_t mn = mn0 + mm, k = k0 + 4 * tx;
+    if (mn >= v.mn) continue;
+    float val[4], h4[4], l4[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      val[j] = tile[4 * tx + j][mm];
       uint32_t h;
-      asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(h) : "f"(val));
-      const float hf = __uint_as_float(h);
-      const int64_t o = (b * v.mn + mn) * v.k + k;
-      hi[o] = hf;
-      lo[o] = isfinite(val) ? val - hf : 0.f;
+      asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(h) : "f"(val[j]));
+      h4[j] = __uint_as_float(h);
+      l4[j] = isfinite(val[j]) ? val[j] - h4[j] : 0.f;
+    }
+    const int64_t o = (b * v.mn + mn) * v.k + k;
+    if (vec_out && k + 3 < v.k) {
+      *reinterpret_cast<float4*>(hi + o) = make_float4(h4[0], h4[1], h4[2], h4[3]);
+      *reinterpret_cast<float4*>(lo + o) = make_float4(l4[0], l4[1], l4[2], l4[3]);
+    } else {
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if (k + j < v.k) {
+          hi[o + j] = h4[j];
+          lo[o + j] = l4[j];
+        }
     }
   }
 }
@@ -134,7 +191,7 @@ __global__ void split_tf32_transpose_kernel(const float* __restrict__ x, SplitVi
 static int split_operand(const float* src, int64_t n, OperandView* view, int mn_major, float* hi,
                          float* lo, cudaStream_t s) {
   if (!mn_major) {
-    split_tf32_kernel<<<grid_for(n, 256), 256, 0, s>>>(src, hi, lo, n);
+    split_tf32_kernel<<<grid_for((n + 3) / 4, 256), 256, 0, s>>>(src, hi, lo, n);
     return launched(s);
   }
   SplitView v;
@@ -148,8 +205,8 @@ static int split_operand(const float* src, int64_t n, OperandView* view, int mn_
     nb *= v.bsize[i];
   }
   if (nb > 65535) return SPMD_ERR_UNSUPPORTED;
-  dim3 grid((unsigned)((v.mn + 31) / 32), (unsigned)((v.k + 31) / 32), (unsigned)nb);
-  split_tf32_transpose_kernel<<<grid, dim3(32, 8), 0, s>>>(src, v, hi, lo);
+  dim3 grid((unsigned)((v.mn + 63) / 64), (unsigned)((v.k + 63) / 64), (unsigned)nb);
+  split_tf32_transpose_kernel<<<grid, 256, 0, s>>>(src, v, hi, lo);
   // K-major dense view [b2][b1][b0][MN][K]
   OperandView kv;
   kv.size[0] = v.k, kv.stride[0] = 1;
@@ -543,15 +600,17 @@ int dot_tf32x3(const spmd_tensor& lhs, const spmd_tensor& rhs, const spmd_tensor
   // small Dots (the parity-sized golden cases) stay on the exact fp64 path
   if (lay.M < 256 || lay.N < 256 || lay.K < 64) return SPMD_ERR_UNSUPPORTED;
   const int64_t na = numel(lhs) * nparts, nb = numel(rhs) * nparts;
+  // each of the four split copies starts 16-byte aligned (vector stores, TMA)
+  const int64_t na4 = (na + 3) & ~(int64_t)3, nb4 = (nb + 3) & ~(int64_t)3;
   keep_pool_memory();
   float* scratch = nullptr;
-  if (cudaMallocAsync((void**)&scratch, (size_t)(2 * (na + nb)) * 4, s) != cudaSuccess) {
+  if (cudaMallocAsync((void**)&scratch, (size_t)(2 * (na4 + nb4)) * 4, s) != cudaSuccess) {
     cudaGetLastError();
     return SPMD_ERR_UNSUPPORTED;
   }
   // an MN-major operand's dense transpose is never larger than its buffer
   // (the view covers a sub-box of it), so the same scratch sizes hold
-  float *ah = scratch, *al = scratch + na, *bh = scratch + 2 * na, *bl = bh + nb;
+  float *ah = scratch, *al = scratch + na4, *bh = scratch + 2 * na4, *bl = bh + nb4;
   OperandView va = lay.va, vb = lay.vb;
   int rc = split_operand((const float*)lhs.data, na, &va, lay.a_mn, ah, al, s);
   if (rc == SPMD_OK) rc = split_operand((const float*)rhs.data, nb, &vb, lay.b_mn, bh, bl, s);
