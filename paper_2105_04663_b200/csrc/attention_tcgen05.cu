@@ -118,7 +118,11 @@ __global__ void __launch_bounds__(256, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const uint32_t O_COL = 0, S_COL = 256;   // S buffers at 256 and 320
+  // TMEM columns: O [0, 256); smem-P variant: S double-buffered [256, 512);
+  // TP: S single-buffered [256, 384) and P(t) double-buffered [384, 512), so
+  // a PV UMMA reading P and the next S UMMA writing S never share columns
+  // (no reliance on UMMA execution order for that hazard)
+  const uint32_t O_COL = 0, S_COL = 256, P_COL = 384;   // S buffers at 256 and 320
 
   uint8_t* sq = smem + L::Q_OFF;
   uint8_t* skv = smem + L::KV_OFF;
@@ -381,7 +385,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
   cluster_sync();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const uint32_t O_COL = 0, S_COL = 256;
+  // TMEM columns: O [0, 256); smem-P variant: S double-buffered [256, 512);
+  // TP: S single-buffered [256, 384) and P(t) double-buffered [384, 512), so
+  // a PV UMMA reading P and the next S UMMA writing S never share columns
+  // (no reliance on UMMA execution order for that hazard)
+  const uint32_t O_COL = 0, S_COL = 256, P_COL = 384;
   uint8_t* sq = smem;
   uint8_t* skv = smem + L::KV_OFF;
   uint8_t* sp = smem + L::P_OFF;
@@ -664,7 +672,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
   cluster_sync();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const uint32_t O_COL = 0, S_COL = 256;
+  // TMEM columns: O [0, 256); smem-P variant: S double-buffered [256, 512);
+  // TP: S single-buffered [256, 384) and P(t) double-buffered [384, 512), so
+  // a PV UMMA reading P and the next S UMMA writing S never share columns
+  // (no reliance on UMMA execution order for that hazard)
+  const uint32_t O_COL = 0, S_COL = 256, P_COL = 384;
   uint8_t* sq = smem;
   uint8_t* skv = smem + L::KV_OFF;
   uint8_t* sp = smem + L::P_OFF;
@@ -922,7 +934,14 @@ __device__ __forceinline__ void named_sync(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 
-template <int D>
+// TP = true: P goes from the softmax warps into tensor memory (tcgen05.st,
+// packed bf16, double-buffered) and the PV UMMA reads A from TMEM, so the
+// P smem buffer is only the O drain's staging area.  That lets the softmax
+// warps hand P(t) of a new item to the MMA warp BEFORE draining the previous
+// item's O, and the drain releases O's columns (o_free) as soon as they are
+// in registers -- the first PV of the next item no longer waits for the O
+// stores.  TP = false: P staged in shared memory (SS UMMA).
+template <int D, bool TP>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
     attention_tcgen05_2sm_pp(const __grid_constant__ CUtensorMap map_q,
                              const __grid_constant__ CUtensorMap map_k,
@@ -947,7 +966,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
   uint64_t* s_free = s_full + 2;           // [2] leader, 16 arrivals
   uint64_t* p_full = s_free + 2;           // [1] leader, 16 arrivals
   uint64_t* pv_done = p_full + 1;          // [1] both (multicast)
-  uint32_t* tmem_slot = (uint32_t*)(pv_done + 1);
+  uint64_t* o_free = pv_done + 1;          // [1] leader, 16 arrivals (TP: O drained to registers)
+  uint32_t* tmem_slot = (uint32_t*)(o_free + 1);
   float* red = (float*)(smem + L::RED_OFF);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -973,6 +993,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
     }
     mbar_init(p_full, 16);
     mbar_init(pv_done, 1);
+    mbar_init(o_free, 16);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 2) {
@@ -984,7 +1005,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
   cluster_sync();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const uint32_t O_COL = 0, S_COL = 256;
+  // TMEM columns: O [0, 256); smem-P variant: S double-buffered [256, 512);
+  // TP: S single-buffered [256, 384) and P(t) double-buffered [384, 512), so
+  // a PV UMMA reading P and the next S UMMA writing S never share columns
+  // (no reliance on UMMA execution order for that hazard)
+  const uint32_t O_COL = 0, S_COL = 256, P_COL = 384;
   uint8_t* sq = smem;
   uint8_t* sk = smem + L::K_OFF;
   uint8_t* sv = smem + L::V_OFF;
@@ -1070,13 +1095,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
     // S side counters (tile gs = 0, 1, ...) and PV side counters
     int s_j = 0, s_slot = 0, s_item = 0;
     uint32_t s_kvph = 0;
-    int p_j = 0, p_slot = 0;
+    int p_j = 0, p_slot = 0, p_item = 0;
     uint32_t p_vph = 0;
     auto issue_s = [&](int gi) {
-      const int sb = gi & 1;
+      const int sb = TP ? 0 : gi & 1;
       if (s_j == 0) mbar_wait(q_full, s_item & 1);
       mbar_wait(&k_full[s_slot], s_kvph);
-      if (gi >= 2) mbar_wait(&s_free[sb], ((gi >> 1) - 1) & 1);
+      if (TP) {
+        if (gi >= 1) mbar_wait(&s_free[0], (gi - 1) & 1);   // softmax(gi-1) read S
+      } else if (gi >= 2) {
+        mbar_wait(&s_free[sb], ((gi >> 1) - 1) & 1);
+      }
       tc_fence_after();
       if (elect_one()) {
         const uint64_t kd = kd0 + (uint64_t)(s_slot * K16);
@@ -1103,13 +1132,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
     auto issue_pv = [&](int gi) {
       mbar_wait(&v_full[p_slot], p_vph);
       mbar_wait(p_full, gi & 1);
+      // TP: the first PV of an item overwrites O -- wait until the previous
+      // item's O is out of TMEM (in the softmax warps' registers)
+      if (TP && p_j == 0 && p_item > 0) mbar_wait(o_free, (p_item - 1) & 1);
       tc_fence_after();
       if (elect_one()) {
         const uint64_t vd = vd0 + (uint64_t)(p_slot * V16);
+        const uint32_t pa = tmem + P_COL + (uint32_t)((gi & 1) * 64);
 #pragma unroll
-        for (int k = 0; k < KT / 16; ++k)
-          tc_mma_2sm(tmem + O_COL, pd0 + (uint64_t)(((k >> 2) * 16384 + (k & 3) * 32) >> 4),
-                     vd + (uint64_t)((k * 2048) >> 4), idesc_o, (p_j | k) != 0);
+        for (int k = 0; k < KT / 16; ++k) {
+          if (TP)
+            tc_mma_2sm_ts(tmem + O_COL, pa + (uint32_t)(k * 8), vd + (uint64_t)((k * 2048) >> 4),
+                          idesc_o, (p_j | k) != 0);
+          else
+            tc_mma_2sm(tmem + O_COL, pd0 + (uint64_t)(((k >> 2) * 16384 + (k & 3) * 32) >> 4),
+                       vd + (uint64_t)((k * 2048) >> 4), idesc_o, (p_j | k) != 0);
+        }
         tc_commit_2sm_mc(pv_done);
         tc_commit_2sm_mc(&v_empty[p_slot]);
       }
@@ -1118,10 +1156,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
         p_slot = 0;
         p_vph ^= 1;
       }
-      if (++p_j == nT) p_j = 0;
+      if (++p_j == nT) {
+        p_j = 0;
+        ++p_item;
+      }
     };
     if (G > 0) {
       issue_s(0);
+      // (issuing an item's last PV before the next item's first S -- whose
+      // Q is still loading -- measured 5% slower: the new item's softmax
+      // pipeline then starts later; profiles/r2_attn_ab_pvfirst.log)
       for (int gi = 1; gi < G; ++gi) {
         issue_s(gi);
         issue_pv(gi - 1);
@@ -1196,6 +1240,57 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
         __syncwarp();
       }
     };
+    // TP drain: all of this thread's O columns (its row, its half of the head
+    // dim) into registers first, release O (o_free), then normalise and
+    // store through this warp's 4 KB staging slice, 64 columns per TMA box.
+    auto drain_tp = [&](float lsum, int st_, int n_, int b_, bool release) {
+      constexpr int NQ = DH / 32;
+      uint32_t o[NQ][32];
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) tmem_ld32_nowait(tmem + lane_base + O_COL + h * DH + q * 32, o[q]);
+      *my_red = lsum;
+      named_sync(pair_bar, 64);
+      const float lt = lsum + *other_red;
+      named_sync(pair_bar, 64);
+      const float inv = lt > 0.f ? 1.f / lt : 0.f;
+      tmem_wait_ld();
+      if (release) {
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_leader(o_free);
+      }
+      uint8_t* stage = sp + h * 16384 + qd * 4096;
+      uint8_t* srow = stage + lane * 128;
+#pragma unroll
+      for (int rd = 0; rd < DH / 64; ++rd) {
+        // the staging slice is free once the previous box's store has read it
+        if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        __syncwarp();
+#pragma unroll
+        for (int half = 0; half < 2; ++half)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            uint4 v;
+            __nv_bfloat162* hv = reinterpret_cast<__nv_bfloat162*>(&v);
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+              hv[u] = __floats2bfloat162_rn(__uint_as_float(o[rd * 2 + half][q * 8 + 2 * u]) * inv,
+                                            __uint_as_float(o[rd * 2 + half][q * 8 + 2 * u + 1]) * inv);
+            *reinterpret_cast<uint4*>(srow + (((half * 4 + q) ^ (row & 7)) << 4)) = v;
+          }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) {
+          asm volatile(
+              "cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%2, %3, %4, %5}], "
+              "[%1];" ::"l"(reinterpret_cast<uint64_t>(&map_o)),
+              "r"(smem_u32(stage)), "r"(h * DH + rd * 64),
+              "r"(st_ * 256 + (int)rank * 128 + qd * 32), "r"(n_), "r"(b_)
+              : "memory");
+          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        }
+      }
+    };
     for (int t = 0; t < G; ++t) {
       float l_prev = 0.f;
       int pst = cst, pn = cn, pb = cb;
@@ -1206,8 +1301,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
         m = -INFINITY;
         l = 0.f;
       }
-      const int sb = t & 1;
-      mbar_wait(&s_full[sb], (t >> 1) & 1);
+      const int sb = TP ? 0 : t & 1;
+      mbar_wait(&s_full[sb], TP ? (t & 1) : ((t >> 1) & 1));
       tc_fence_after();
       float s[64];
       {
@@ -1257,38 +1352,75 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
 #pragma unroll
       for (int i = 8; i < 64; ++i) t8[i & 7] += s[i];
       l = l * alpha + (((t8[0] + t8[1]) + (t8[2] + t8[3])) + ((t8[4] + t8[5]) + (t8[6] + t8[7])));
-      // P is single-buffered and O may need rescaling / draining: PV(t-1) done
-      if (t >= 1) mbar_wait(pv_done, (t - 1) & 1);
-      if (j == 0 && t > 0) {
-        tc_fence_after();
-        drain(l_prev, pst, pn, pb);       // previous item's O, before PV(t) overwrites it
-      }
-      if (j > 0 && __any_sync(0xffffffffu, resc)) {
-        tc_fence_after();
+      if (TP) {
+        // PV(t-1) landed: needed by an O rescale / drain, and waited on every
+        // tile so this warp never falls two phases behind pv_done (a parity
+        // wait cannot tell phase k from k-2: skipping the wait on tiles
+        // without a rescale let a later rescale pass early now and then)
+        if (t >= 1) mbar_wait(pv_done, (t - 1) & 1);
+        if (j > 0 && __any_sync(0xffffffffu, resc)) {
+          tc_fence_after();
 #pragma unroll 1
-        for (int cc = 0; cc < DH; cc += 32) {
-          uint32_t o[32];
-          tmem_ld32(tmem + lane_base + O_COL + h * DH + cc, o);
+          for (int cc = 0; cc < DH; cc += 32) {
+            uint32_t o[32];
+            tmem_ld32(tmem + lane_base + O_COL + h * DH + cc, o);
 #pragma unroll
-          for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
-          tmem_st32(tmem + lane_base + O_COL + h * DH + cc, o);
+            for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
+            tmem_st32(tmem + lane_base + O_COL + h * DH + cc, o);
+          }
+        }
+        // P(t) into its TMEM buffer (the one PV(t-2) read)
+        {
+          uint32_t pk[32];
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            __nv_bfloat162 b2 = __floats2bfloat162_rn(s[2 * i], s[2 * i + 1]);
+            pk[i] = *reinterpret_cast<uint32_t*>(&b2);
+          }
+          tmem_st32(tmem + lane_base + P_COL + (t & 1) * 64 + h * 32, pk);
         }
         asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_leader(p_full);
+        if (j == 0 && t > 0) {
+          tc_fence_after();
+          drain_tp(l_prev, pst, pn, pb, true);   // the previous item's O
+        }
+      } else {
+        // P is single-buffered and O may need rescaling / draining: PV(t-1) done
+        if (t >= 1) mbar_wait(pv_done, (t - 1) & 1);
+        if (j == 0 && t > 0) {
+          tc_fence_after();
+          drain(l_prev, pst, pn, pb);       // previous item's O, before PV(t) overwrites it
+        }
+        if (j > 0 && __any_sync(0xffffffffu, resc)) {
+          tc_fence_after();
+  #pragma unroll 1
+          for (int cc = 0; cc < DH; cc += 32) {
+            uint32_t o[32];
+            tmem_ld32(tmem + lane_base + O_COL + h * DH + cc, o);
+  #pragma unroll
+            for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
+            tmem_st32(tmem + lane_base + O_COL + h * DH + cc, o);
+          }
+          asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        }
+        uint8_t* prow = sp + h * 16384 + row * 128;   // SW128 atom h = keys 64h..64h+63
+  #pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          uint4 v;
+          __nv_bfloat162* hv = reinterpret_cast<__nv_bfloat162*>(&v);
+  #pragma unroll
+          for (int u = 0; u < 4; ++u)
+            hv[u] = __floats2bfloat162_rn(s[q * 8 + 2 * u], s[q * 8 + 2 * u + 1]);
+          *reinterpret_cast<uint4*>(prow + ((q ^ (row & 7)) << 4)) = v;
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_leader(p_full);
       }
-      uint8_t* prow = sp + h * 16384 + row * 128;   // SW128 atom h = keys 64h..64h+63
-#pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        uint4 v;
-        __nv_bfloat162* hv = reinterpret_cast<__nv_bfloat162*>(&v);
-#pragma unroll
-        for (int u = 0; u < 4; ++u)
-          hv[u] = __floats2bfloat162_rn(s[q * 8 + 2 * u], s[q * 8 + 2 * u + 1]);
-        *reinterpret_cast<uint4*>(prow + ((q ^ (row & 7)) << 4)) = v;
-      }
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive_leader(p_full);
       if (++j == nT) {
         j = 0;
         item += ncl;
@@ -1297,7 +1429,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
     if (G > 0) {
       mbar_wait(pv_done, (G - 1) & 1);
       tc_fence_after();
-      drain(l, cst, cn, cb);
+      if (TP)
+        drain_tp(l, cst, cn, cb, false);
+      else
+        drain(l, cst, cn, cb);
     }
     if (lane == 0) bulk_wait_all();
   }
@@ -1309,19 +1444,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
   }
 }
 
-template <int D>
+template <int D, bool TP>
 static int launch_attention_2sm_pp(const CUtensorMap& mq, const CUtensorMap& mk,
                                    const CUtensorMap& mv, const CUtensorMap& mo, AttnShape g,
                                    cudaStream_t s) {
   typedef AttnPSmem<D> L;
   static_assert(L::TOTAL <= 232448, "persistent attention smem");
   static std::atomic<uint64_t> attr_done{0};
-  if (int rc = set_smem_attr((const void*)attention_tcgen05_2sm_pp<D>, L::TOTAL, &attr_done))
+  if (int rc = set_smem_attr((const void*)attention_tcgen05_2sm_pp<D, TP>, L::TOTAL, &attr_done))
     return rc;
   const int64_t items = (int64_t)((g.S + 255) / 256) * g.N * g.Bp;
   const int pairs = sm_budget() / 2;
   const int64_t clusters = items < pairs ? items : pairs;
-  attention_tcgen05_2sm_pp<D><<<(unsigned)(2 * clusters), 384, L::TOTAL, s>>>(mq, mk, mv, mo, g);
+  attention_tcgen05_2sm_pp<D, TP><<<(unsigned)(2 * clusters), 384, L::TOTAL, s>>>(mq, mk, mv, mo,
+                                                                                 g);
   return launched(s);
 }
 
@@ -1366,17 +1502,24 @@ extern "C" int spmd_attention_layout(spmd_tensor q, spmd_tensor k, spmd_tensor v
   const int mode = option(OPT_ATTN_MODE) == 1 ? 1 : 2;
   // key tile: 128 for D=128 (549 vs 469 TF/s at T=1024), 64 for D=256 (equal at
   // T=1024, 993 vs 955 TF/s at T=4096: 3 K/V stages fit) -- profiles/r1_attention_kt.jsonl
-  // option attn_kt: 0 = the persistent kernel (default); 64 / 128 = the
-  // round-1 non-persistent kernels with that key tile
+  // option attn_kt: 0 = the persistent kernel with P in tensor memory
+  // (default; same-box A/B, median of 8 rotated rounds: C2 shape +6%,
+  // T=4096 +7%, D=128 +4%: profiles/r2_attn_ab_tp.log); 1 = the persistent
+  // kernel with P in shared memory; 64 / 128 = the round-1 non-persistent
+  // kernels with that key tile
   const int kt = (int)option(OPT_ATTN_KT);
-  if (mode == 2 && D >= 128 && kt == 0 && scale > 0.f) {
+  if (mode == 2 && D >= 128 && (kt == 0 || kt == 1) && scale > 0.f) {
     // persistent CTA pairs, 8 softmax warps, 128-key tiles (default); each
     // softmax warp stores its own 32-row output boxes
     CUtensorMap mo32;
     if (out_bsnd ? encode4(&mo32, out.data, D, S, N, Bp, N * D, D, S * N * D, 32)
                  : encode4(&mo32, out.data, D, S, N, Bp, D, S * D, N * S * D, 32)) {
-      if (D == 128) return launch_attention_2sm_pp<128>(mq, mk, mv, mo32, g, s);
-      return launch_attention_2sm_pp<256>(mq, mk, mv, mo32, g, s);
+      if (kt == 0) {
+        if (D == 128) return launch_attention_2sm_pp<128, true>(mq, mk, mv, mo32, g, s);
+        return launch_attention_2sm_pp<256, true>(mq, mk, mv, mo32, g, s);
+      }
+      if (D == 128) return launch_attention_2sm_pp<128, false>(mq, mk, mv, mo32, g, s);
+      return launch_attention_2sm_pp<256, false>(mq, mk, mv, mo32, g, s);
     }
   }
   if (mode == 2 && D >= 128 && kt == 128) {

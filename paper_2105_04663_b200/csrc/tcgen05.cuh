@@ -340,6 +340,19 @@ __device__ __forceinline__ void tc_mma_2sm(uint32_t d_tmem, uint64_t a_desc, uin
       "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate));
 }
 
+// A from tensor memory (kind::f16, K-major packed bf16 pairs: row m of A is
+// TMEM lane m of each CTA of the pair, 8 columns per 16-element K step).
+__device__ __forceinline__ void tc_mma_2sm_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc,
+                                              uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n"
+      "}\n" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate));
+}
+
 // One lane of a converged warp (the MMA issuers run the whole warp through
 // their loops so descriptors and counters stay in uniform registers).
 __device__ __forceinline__ bool elect_one() {

@@ -3,7 +3,8 @@
     python scripts/attn_shapes.py
 
 For each kernel variant (option attn_kt: 0 = persistent 8-softmax-warp
-kernel, 64 / 128 = the round-1 non-persistent kernels) times
+kernel with P in tensor memory, 1 = the same with P in shared memory,
+64 / 128 = the round-1 non-persistent kernels) times
 spmd_attention with CUDA events (10 launches after 3 warm-ups) and checks
 one head against an fp32 torch reference.  One JSON line per case.
 """
@@ -34,7 +35,7 @@ for B, S, T, N, D in cases:
                                                desc(v, Shape((B, T, N, D), DType.BF16)),
                                                desc(o, Shape((B, N, S, D), DType.BF16)), scale, 1,
                                                st), "a")
-    for kt in (0, 64, 128):
+    for kt in (0, 1, 64, 128):
         with C.option("attn_kt", kt):
             for _ in range(3):
                 f()

@@ -108,13 +108,14 @@ def test_attention_writes_bsnd_layout(D):
     assert torch.equal(out, a.permute(0, 1, 3, 2, 4))
 
 
-@pytest.mark.parametrize("kt", [0, 64, 128])
+@pytest.mark.parametrize("kt", [0, 1, 64, 128])
 @pytest.mark.parametrize("B,S,T,N,D", [(4, 1024, 1024, 16, 256), (2, 300, 200, 5, 256),
                                        (3, 512, 640, 7, 128), (1, 1024, 1000, 40, 128)])
 def test_attention_variants_many_items(kt, B, S, T, N, D):
-    """Every kernel variant (attn_kt 0: the persistent CTA-pair kernel with 8
-    softmax warps, >= 4 work items per CTA pair on the first case; 64 / 128:
-    the round-1 kernels), with partial query / key tiles."""
+    """Every kernel variant (attn_kt 0 / 1: the persistent CTA-pair kernel
+    with 8 softmax warps, P in tensor memory / in shared memory, >= 4 work
+    items per CTA pair on the first case; 64 / 128: the round-1 kernels),
+    with partial query / key tiles."""
     import torch
     from paper_2105_04663_b200 import _capi as C
     torch.manual_seed(B * S + T + N + D + kt)
