@@ -118,11 +118,11 @@ __global__ void __launch_bounds__(256, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  // TMEM columns: O [0, 256); smem-P variant: S double-buffered [256, 512);
-  // TP: S single-buffered [256, 384) and P(t) double-buffered [384, 512), so
-  // a PV UMMA reading P and the next S UMMA writing S never share columns
-  // (no reliance on UMMA execution order for that hazard)
-  const uint32_t O_COL = 0, S_COL = 256, P_COL = 384;   // S buffers at 256 and 320
+  // TMEM columns: O [0, 256); S double-buffered [256, 512).  TP: P(t)
+  // overwrites the first 64 columns of S(t)'s buffer (packed bf16) -- the
+  // next S UMMA into that buffer is issued after PV(t) by the same thread,
+  // and tcgen05.mma operations from one thread execute in issue order
+  const uint32_t O_COL = 0, S_COL = 256;   // S buffers at 256 and 320
 
   uint8_t* sq = smem + L::Q_OFF;
   uint8_t* skv = smem + L::KV_OFF;
@@ -385,11 +385,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
   cluster_sync();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  // TMEM columns: O [0, 256); smem-P variant: S double-buffered [256, 512);
-  // TP: S single-buffered [256, 384) and P(t) double-buffered [384, 512), so
-  // a PV UMMA reading P and the next S UMMA writing S never share columns
-  // (no reliance on UMMA execution order for that hazard)
-  const uint32_t O_COL = 0, S_COL = 256, P_COL = 384;
+  // TMEM columns: O [0, 256); S double-buffered [256, 512).  TP: P(t)
+  // overwrites the first 64 columns of S(t)'s buffer (packed bf16) -- the
+  // next S UMMA into that buffer is issued after PV(t) by the same thread,
+  // and tcgen05.mma operations from one thread execute in issue order
+  const uint32_t O_COL = 0, S_COL = 256;
   uint8_t* sq = smem;
   uint8_t* skv = smem + L::KV_OFF;
   uint8_t* sp = smem + L::P_OFF;
@@ -672,11 +672,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
   cluster_sync();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  // TMEM columns: O [0, 256); smem-P variant: S double-buffered [256, 512);
-  // TP: S single-buffered [256, 384) and P(t) double-buffered [384, 512), so
-  // a PV UMMA reading P and the next S UMMA writing S never share columns
-  // (no reliance on UMMA execution order for that hazard)
-  const uint32_t O_COL = 0, S_COL = 256, P_COL = 384;
+  // TMEM columns: O [0, 256); S double-buffered [256, 512).  TP: P(t)
+  // overwrites the first 64 columns of S(t)'s buffer (packed bf16) -- the
+  // next S UMMA into that buffer is issued after PV(t) by the same thread,
+  // and tcgen05.mma operations from one thread execute in issue order
+  const uint32_t O_COL = 0, S_COL = 256;
   uint8_t* sq = smem;
   uint8_t* skv = smem + L::KV_OFF;
   uint8_t* sp = smem + L::P_OFF;
@@ -934,8 +934,8 @@ __device__ __forceinline__ void named_sync(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 
-// TP = true: P goes from the softmax warps into tensor memory (tcgen05.st,
-// packed bf16, double-buffered) and the PV UMMA reads A from TMEM, so the
+// TP = true: P goes from the softmax warps into tensor memory over S
+// (tcgen05.st, packed bf16) and the PV UMMA reads A from TMEM, so the
 // P smem buffer is only the O drain's staging area.  That lets the softmax
 // warps hand P(t) of a new item to the MMA warp BEFORE draining the previous
 // item's O, and the drain releases O's columns (o_free) as soon as they are
@@ -1005,11 +1005,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
   cluster_sync();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  // TMEM columns: O [0, 256); smem-P variant: S double-buffered [256, 512);
-  // TP: S single-buffered [256, 384) and P(t) double-buffered [384, 512), so
-  // a PV UMMA reading P and the next S UMMA writing S never share columns
-  // (no reliance on UMMA execution order for that hazard)
-  const uint32_t O_COL = 0, S_COL = 256, P_COL = 384;
+  // TMEM columns: O [0, 256); S double-buffered [256, 512).  TP: P(t)
+  // overwrites the first 64 columns of S(t)'s buffer (packed bf16) -- the
+  // next S UMMA into that buffer is issued after PV(t) by the same thread,
+  // and tcgen05.mma operations from one thread execute in issue order
+  const uint32_t O_COL = 0, S_COL = 256;
   uint8_t* sq = smem;
   uint8_t* sk = smem + L::K_OFF;
   uint8_t* sv = smem + L::V_OFF;
@@ -1098,14 +1098,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
     int p_j = 0, p_slot = 0, p_item = 0;
     uint32_t p_vph = 0;
     auto issue_s = [&](int gi) {
-      const int sb = TP ? 0 : gi & 1;
+      const int sb = gi & 1;
       if (s_j == 0) mbar_wait(q_full, s_item & 1);
       mbar_wait(&k_full[s_slot], s_kvph);
-      if (TP) {
-        if (gi >= 1) mbar_wait(&s_free[0], (gi - 1) & 1);   // softmax(gi-1) read S
-      } else if (gi >= 2) {
-        mbar_wait(&s_free[sb], ((gi >> 1) - 1) & 1);
-      }
+      if (gi >= 2) mbar_wait(&s_free[sb], ((gi >> 1) - 1) & 1);
       tc_fence_after();
       if (elect_one()) {
         const uint64_t kd = kd0 + (uint64_t)(s_slot * K16);
@@ -1138,7 +1134,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
       tc_fence_after();
       if (elect_one()) {
         const uint64_t vd = vd0 + (uint64_t)(p_slot * V16);
-        const uint32_t pa = tmem + P_COL + (uint32_t)((gi & 1) * 64);
+        const uint32_t pa = tmem + S_COL + (uint32_t)((gi & 1) * KT);
 #pragma unroll
         for (int k = 0; k < KT / 16; ++k) {
           if (TP)
@@ -1301,8 +1297,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
         m = -INFINITY;
         l = 0.f;
       }
-      const int sb = TP ? 0 : t & 1;
-      mbar_wait(&s_full[sb], TP ? (t & 1) : ((t >> 1) & 1));
+      const int sb = t & 1;
+      mbar_wait(&s_full[sb], (t >> 1) & 1);
       tc_fence_after();
       float s[64];
       {
@@ -1369,7 +1365,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
             tmem_st32(tmem + lane_base + O_COL + h * DH + cc, o);
           }
         }
-        // P(t) into its TMEM buffer (the one PV(t-2) read)
+        // P(t) into TMEM over S(t): both warps of this lane quarter finished
+        // reading S(t) before the max-exchange barriers above
         {
           uint32_t pk[32];
 #pragma unroll
@@ -1377,7 +1374,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
             __nv_bfloat162 b2 = __floats2bfloat162_rn(s[2 * i], s[2 * i + 1]);
             pk[i] = *reinterpret_cast<uint32_t*>(&b2);
           }
-          tmem_st32(tmem + lane_base + P_COL + (t & 1) * 64 + h * 32, pk);
+          tmem_st32(tmem + lane_base + S_COL + sb * KT + h * 32, pk);
         }
         asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
         tc_fence_before();
