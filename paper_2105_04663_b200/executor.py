@@ -257,6 +257,8 @@ class Executor:
         self._staged_exposed: list = []
         self._act_staged: set = set()
         self._staged = self._plan_staged_gathers()
+        if comm is not None:
+            self._add_param_push_zones()
         if self.comm_streams:
             self.steps = self._jit_prefetch(self.steps)
         self._sm_limit = self._plan_sm_limit()
@@ -279,6 +281,12 @@ class Executor:
         pids = [p.id for p in self.params]
         staged = {}
         wide = os.environ.get("SPMD_PEER_STAGE_WIDE", "1") == "1"
+        # exposed parameter gathers: pushed from the parameter itself
+        # (peer_push_kernel, 661 / 677 GB/s per GPU at N=2 / 4 vs 463 / 342
+        # for staged pulls: profiles/r2_bench_n{2,4}_final.log) unless
+        # SPMD_PEER_AG_PUSH_PARAMS=0
+        push_params = os.environ.get("SPMD_PEER_AG_PUSH", "1") != "0" and \
+            os.environ.get("SPMD_PEER_AG_PUSH_PARAMS", "1") != "0"
         # activation staging measured slower (profiles/r1_c2_n4_ab_stage_act.log)
         act = os.environ.get("SPMD_PEER_STAGE_ACT", "0") == "1"
         for aid in self._peer_ag:
@@ -291,6 +299,8 @@ class Executor:
                     self._act_staged.add(aid)
                     self._peer_engine[aid] = 4
                 continue
+            if push_params and self._peer_engine.get(aid, -1) not in (0, 3):
+                continue                          # exposed: push engine (1 / -1)
             if wide and self._peer_engine.get(aid, -1) < 0:
                 self._peer_engine[aid] = 1        # exposed NCCL gather -> staged pulls too
             if self._peer_engine.get(aid, -1) >= 0:
@@ -299,6 +309,28 @@ class Executor:
                     self._staged_exposed.append(aid)
                 self._peer_engine[aid] = 4
         return staged
+
+    def _add_param_push_zones(self) -> None:
+        """Parameter all-gathers left on the critical path (engine 1 / -1:
+        not staged, _plan_staged_gathers) -- C5's replicate reshard, a
+        step's first x / weight gathers -- get a push landing zone after the
+        heap regions _peer_bytes laid out; every member pushes its shard
+        straight from the parameter (spmd_peer_push_all_gather)."""
+        import os
+        if os.environ.get("SPMD_PEER_AG_PUSH", "1") == "0" or \
+                os.environ.get("SPMD_PEER_AG_PUSH_PARAMS", "1") == "0":
+            return
+        pids = {p.id for p in self.params}
+        off = self._peer_bytes_used
+        for ins in self.graph.instructions:
+            if ins.opcode == Op.ALL_GATHER and ins.id not in self._fused_skip and \
+                    ins.id not in self._peer_agp and ins.operands[0] in pids and \
+                    self._peer_engine.get(ins.id, 0) in (1, -1):
+                self._peer_agp[ins.id] = off
+                off += (ins.shape.nbytes + 4095) // 4096 * 4096
+        if off != self._peer_bytes_used:
+            self._peer_bytes_used = off
+            self.comm.ensure_peer(off, self.device)
 
     def _stage_phases(self) -> list:
         """Staging order: exposed gathers' shards, then the rest
@@ -471,6 +503,8 @@ class Executor:
         # the critical path (engine 1 / NCCL), where SMs are free: 652 vs 475
         # (pull) vs 467 (NCCL) GB/s per GPU at N=2 (profiles/r2_bench_n2.log);
         # gathers hidden under a GEMM keep the copy engines.
+        # (parameter gathers left on the critical path get theirs later,
+        # _add_param_push_zones, once the engines are planned)
         self._peer_agp = {}
         if os.environ.get("SPMD_PEER_AG_PUSH", "1") != "0":
             pids = {p.id for p in self.params}

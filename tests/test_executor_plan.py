@@ -254,27 +254,51 @@ def test_backward_fusion_can_be_disabled():
     assert not any(v[0] in ("softmax_bwd", "relu_bwd") for v in ex._fused.values())
 
 
+@pytest.mark.parametrize("push_params", ["1", "0"])
 @pytest.mark.parametrize("mesh", [(2, 2), (1, 4), (2, 4)])
-def test_parameter_gathers_are_prestaged(mesh):
-    """Overlapped runs stage every parameter all-gather (weights, and the x
-    input) into the peer heap at the step start: engine 4 (copy-engine pulls
-    only).  Activation gathers keep their engine unless SPMD_PEER_STAGE_ACT."""
-    ex, _ = _layer(mesh)
-    ex.steps = ex._hoist_collectives(ex.steps)
-    ex.comm_stream = object()
-    ex.comm_streams = [ex.comm_stream]
-    ex._peer_engine = ex._plan_peer_engines()
-    ex._staged_exposed, ex._act_staged = [], set()
-    staged = ex._plan_staged_gathers()
+def test_parameter_gathers_are_prestaged(mesh, push_params):
+    """Overlapped runs stage the parameter all-gathers a GEMM hides (weights)
+    into the peer heap at the step start: engine 4 (copy-engine pulls only).
+    The exposed ones (the step's first gathers) are pushed straight from the
+    parameter (engine 1 / -1, push zone) -- unless SPMD_PEER_AG_PUSH_PARAMS=0,
+    which stages every one.  Activation gathers keep their engine unless
+    SPMD_PEER_STAGE_ACT."""
+    os.environ["SPMD_PEER_AG_PUSH_PARAMS"] = push_params
+    try:
+        ex, _ = _layer(mesh)
+        ex.steps = ex._hoist_collectives(ex.steps)
+        ex.comm_stream = object()
+        ex.comm_streams = [ex.comm_stream]
+        ex._peer_engine = ex._plan_peer_engines()
+        planned = dict(ex._peer_engine)
+        ex._staged_exposed, ex._act_staged = [], set()
+        staged = ex._plan_staged_gathers()
+        # (the executor was built without overlap: drop the parameter push
+        # zones planned then and re-plan them for the overlapped engines)
+        pset = {p.id for p in ex.params}
+        ex._peer_agp = {k: v for k, v in ex._peer_agp.items()
+                        if ex.by_id[k].operands[0] not in pset}
+        ex._add_param_push_zones()
+    finally:
+        os.environ.pop("SPMD_PEER_AG_PUSH_PARAMS")
     pids = [p.id for p in ex.params]
+    pushed = 0
     for aid in ex._peer_ag:
         src = ex.by_id[ex.by_id[aid].operands[0]]
         if src.opcode == Op.PARAMETER:
-            assert staged[aid] == pids.index(src.id) and ex._peer_engine[aid] == 4
+            if push_params == "1" and planned.get(aid, -1) not in (0, 3):
+                assert aid not in staged and ex._peer_engine[aid] in (1, -1)
+                assert aid in ex._peer_agp
+                pushed += 1
+            else:
+                assert staged[aid] == pids.index(src.id) and ex._peer_engine[aid] == 4
+                assert aid not in ex._peer_agp
         else:
             assert aid not in staged and ex._peer_engine[aid] != 4
+    if push_params == "1":
+        assert pushed >= 1          # the step's first gathers are exposed
     if mesh[0] > 1:          # weights gathered over the data axis
-        assert len(staged) >= 6
+        assert len(staged) + pushed >= 6
     assert not ex._act_staged
 
 
