@@ -429,6 +429,8 @@ class Executor:
             return
         mode = os.environ.get("SPMD_COMM_LANES", "critical")
         nxt = 0
+        npush = 0
+        pids = {p.id for p in self.params}
         for st in self.steps:
             if not st.coll:
                 continue
@@ -451,6 +453,18 @@ class Executor:
                     st.lane = 2 - k
                 else:
                     st.lane = 2 + (k if os.environ.get("SPMD_EXPOSED_SPLIT", "1") != "0" else 0)
+            elif mode == "critical" and eng in (1, -1) and st.ins.id in self._peer_agp and \
+                    self.by_id[st.ins.id].operands[0] in pids:
+                # exposed parameter gathers on the push engine (the step's
+                # first x and w_q gathers): lanes 2 and 3 alternate so they
+                # run at once (one lane serialised them: 0.35 + 0.32 ms before
+                # the first GEMM at 2x2, profiles/r2_timeline_c2_n4_push.log;
+                # concurrent: first GEMM 0.12 ms earlier in the eager
+                # timeline, r2_timeline_c2_n4_lanes.log; graph-replayed step
+                # within noise, 13.67 vs 13.71 ms: r2_ab_exposed_split_push.log)
+                st.lane = 2 + (npush % 2 if os.environ.get("SPMD_EXPOSED_SPLIT", "1") != "0"
+                               else 0)
+                npush += 1
             elif mode == "critical" and eng not in (0, 3, 4):
                 st.lane = 2
         torch = _torch()
