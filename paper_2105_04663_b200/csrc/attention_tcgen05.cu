@@ -1017,27 +1017,33 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
 
   if (warp == 0 && lane == 0) {
     // ---------------- TMA producer ----------------
-    // Flat order over this pair's tiles t: V(t-1), [Q(item) at an item's
-    // first tile], K(t) -- K runs one tile ahead of V, matching the MMA
-    // order S(t+1) before PV(t).
+    // Flat order over this pair's tiles t: [Q(item) at an item's first
+    // tile], K(t), then V(t-1) -- K runs one tile ahead of V, matching the
+    // MMA order S(t+1) before PV(t).  K(t) goes first: its slot frees when
+    // S(t-2) completes, V(t-1)'s only when PV(t-3) does (one UMMA group
+    // later), so waiting for the V slot first delayed every K load
+    // (same-box A/B: +0.3..1.2% median, profiles/r2_attn_ab_kfirst.log).
     const int my_items = cl < items ? (items - cl + ncl - 1) / ncl : 0;
     const int G = my_items * nT;
     int item = cl, j = 0, it = 0;          // coordinates of tile t
     int pn = 0, pb = 0, pj = 0;            // coordinates of tile t - 1
+    auto load_v = [&](int tv) {            // V(tv) at the coordinates (pn, pb, pj)
+      const int slot = tv % NS;
+      mbar_wait(&v_empty[slot], ((tv / NS) & 1) ^ 1);
+      uint8_t* vv = sv + slot * L::V_HALF;
+      if (leader) mbar_expect_tx(&v_full[slot], 2 * L::V_HALF);
+#pragma unroll
+      for (int c = 0; c < DC / 2; ++c)
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+          tma_load_4d_2sm(vv + c * 16384 + h * 8192, &map_v, &v_full[slot],
+                          (int)rank * DH + c * 64, pj * KT + h * 64, pn, pb);
+    };
     for (int t = 0; t <= G; ++t) {
-      if (t >= 1) {
-        const int slot = (t - 1) % NS;
-        mbar_wait(&v_empty[slot], (((t - 1) / NS) & 1) ^ 1);
-        uint8_t* vv = sv + slot * L::V_HALF;
-        if (leader) mbar_expect_tx(&v_full[slot], 2 * L::V_HALF);
-#pragma unroll
-        for (int c = 0; c < DC / 2; ++c)
-#pragma unroll
-          for (int h = 0; h < 2; ++h)
-            tma_load_4d_2sm(vv + c * 16384 + h * 8192, &map_v, &v_full[slot],
-                            (int)rank * DH + c * 64, pj * KT + h * 64, pn, pb);
+      if (t == G) {
+        if (t >= 1) load_v(t - 1);
+        break;
       }
-      if (t == G) break;
       const int st = item % nSt, rest = item / nSt;
       const int n = rest % g.N, b = rest / g.N;
       if (j == 0) {
@@ -1070,6 +1076,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
       for (int c = 0; c < DC; ++c)
         tma_load_4d_2sm(kk + c * 8192, &map_k, &k_full[slot], c * 64, j * KT + (int)rank * 64, n,
                         b);
+      if (t >= 1) load_v(t - 1);
       pn = n, pb = b, pj = j;
       if (++j == nT) {
         j = 0;
