@@ -952,13 +952,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint64_t* bars = (uint64_t*)(smem + L::BAR_OFF);
-  uint64_t* q_full = bars + 0;             // leader, 1 arrival + tx
-  uint64_t* q_empty = bars + 1;            // both (multicast commit)
+  // Q per 64-column chunk c (the S UMMAs' K steps): at an item boundary
+  // chunk c of the next Q loads as soon as the last S UMMA's chunk-c steps
+  // are done, and the next item's first S starts on chunk 0 while the rest
+  // streams in (one barrier for all of Q: -1.5% at the C2 shape, best of
+  // 4 same-box rounds, profiles/r2_attn_ab_qchunk.log)
+  uint64_t* q_full = bars + 0;             // [DC] leader, 1 arrival + tx
+  uint64_t* q_empty = q_full + DC;         // [DC] both (multicast commit)
   // K and V have separate rings: a K slot frees when its S MMA completes, a
   // V slot when its PV MMA does, so K(j+2) streams in while PV(j) still runs
   // (one shared K+V ring of 2 slots waited for PV(j) -- ncu: the MMA warp
   // starved on the loads 27% of the time)
-  uint64_t* k_full = bars + 2;             // [NS] leader
+  uint64_t* k_full = q_empty + DC;        // [NS] leader
   uint64_t* k_empty = k_full + NS;         // [NS] both (multicast)
   uint64_t* v_full = k_empty + NS;         // [NS] leader
   uint64_t* v_empty = v_full + NS;         // [NS] both (multicast)
@@ -979,8 +984,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
   const int nT = (g.T + KT - 1) / KT;
 
   if (threadIdx.x == 0) {
-    mbar_init(q_full, 1);
-    mbar_init(q_empty, 1);
+    for (int c = 0; c < DC; ++c) {
+      mbar_init(&q_full[c], 1);
+      mbar_init(&q_empty[c], 1);
+    }
     for (int i = 0; i < NS; ++i) {
       mbar_init(&k_full[i], 1);
       mbar_init(&k_empty[i], 1);
@@ -1047,12 +1054,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
       const int st = item % nSt, rest = item / nSt;
       const int n = rest % g.N, b = rest / g.N;
       if (j == 0) {
-        if (it > 0) mbar_wait(q_empty, (it - 1) & 1);
-        if (leader) mbar_expect_tx(q_full, 2 * L::Q_BYTES);
-#pragma unroll
-        for (int c = 0; c < DC; ++c)
-          tma_load_4d_2sm(sq + c * 16384, &map_q, q_full, c * 64, st * 256 + (int)rank * 128, n,
-                          b);
+#pragma unroll 1
+        for (int c = 0; c < DC; ++c) {
+          if (it > 0) mbar_wait(&q_empty[c], (it - 1) & 1);
+          if (leader) mbar_expect_tx(&q_full[c], 2 * (L::Q_BYTES / DC));
+          tma_load_4d_2sm(sq + c * 16384, &map_q, &q_full[c], c * 64, st * 256 + (int)rank * 128,
+                          n, b);
+        }
         // Q is read once, from HBM: pull the next item's Q into L2 now, so
         // its load at the item boundary (after this item's last S MMA frees
         // the Q buffer) is an L2 hit and the tensor pipe does not idle on it
@@ -1106,21 +1114,26 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
     uint32_t p_vph = 0;
     auto issue_s = [&](int gi) {
       const int sb = gi & 1;
-      if (s_j == 0) mbar_wait(q_full, s_item & 1);
       mbar_wait(&k_full[s_slot], s_kvph);
       if (gi >= 2) mbar_wait(&s_free[sb], ((gi >> 1) - 1) & 1);
-      tc_fence_after();
-      if (elect_one()) {
-        const uint64_t kd = kd0 + (uint64_t)(s_slot * K16);
+      const uint64_t kd = kd0 + (uint64_t)(s_slot * K16);
 #pragma unroll
-        for (int c = 0; c < DC; ++c)
+      for (int c = 0; c < DC; ++c) {
+        if (s_j == 0) mbar_wait(&q_full[c], s_item & 1);   // the item's first S: chunk by chunk
+        tc_fence_after();
+        if (elect_one()) {
 #pragma unroll
           for (int k = 0; k < 4; ++k)
             tc_mma_2sm(tmem + S_COL + sb * KT, qd0 + (uint64_t)((c * 16384 + k * 32) >> 4),
                        kd + (uint64_t)((c * 8192 + k * 32) >> 4), idesc_s, (c | k) != 0);
+          // Q chunk c is free once the item's last S has used it
+          if (s_j == nT - 1) tc_commit_2sm_mc(&q_empty[c]);
+        }
+        __syncwarp();
+      }
+      if (elect_one()) {
         tc_commit_2sm_mc(&s_full[sb]);
         tc_commit_2sm_mc(&k_empty[s_slot]);
-        if (s_j == nT - 1) tc_commit_2sm_mc(q_empty);   // Q smem free once these finish
       }
       __syncwarp();
       if (++s_slot == NS) {
