@@ -174,7 +174,7 @@ def run_reference(args):
             "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": "C2 transformer layer (attention+FFN), paper dims",
-                       "model_dims": dict(PAPER), "mesh": list(mesh),
+                       "dims": dict(PAPER), "mesh": list(mesh),
                        "parallelism": "dp%dxmp%d" % mesh, "global_batch": PAPER["B"],
                        "seq_len": PAPER["S"],
                        "cpu_sample": "each step times a bounded sample of the workload, "
@@ -856,7 +856,7 @@ def main():
 
     if rank == 0:
         per_gpu = value / world
-        cfg = {"workload": wdesc, "model_dims": dims, "mesh": list(mesh),
+        cfg = {"workload": wdesc, "dims": dims, "mesh": list(mesh),
                "parallelism": ("dp%dxmp%d" % mesh) if args.config in ("c1", "c2", "c2train") else
                ("expert%d" % world if args.config == "c3" else "spatial%d" % world),
                "plan": "fast", "l2": "inputs larger than L2 (weights+activations)",

@@ -27,7 +27,7 @@ def test_reference_arm_json_line():
         assert k in d, k
     assert d["unit"] == "TFLOP/s" and d["higher_is_better"] is True and d["value"] > 0
     assert d["config"]["workload"].startswith("C2 transformer layer") and \
-        d["config"]["model_dims"] == bench.PAPER
+        d["config"]["dims"] == bench.PAPER
     cb = d["cpu_baseline"]
     assert cb["kind"] == "port" and cb["cores"] >= 1 and cb["value"] == d["value"]
     assert "oracle" in cb["sample"]
