@@ -429,7 +429,7 @@ class Executor:
             return
         mode = os.environ.get("SPMD_COMM_LANES", "critical")
         nxt = 0
-        npush = 0
+        npush = ncp = 0
         pids = {p.id for p in self.params}
         for st in self.steps:
             if not st.coll:
@@ -465,6 +465,15 @@ class Executor:
                 st.lane = 2 + (npush % 2 if os.environ.get("SPMD_EXPOSED_SPLIT", "1") != "0"
                                else 0)
                 npush += 1
+            elif mode == "critical" and st.ins.opcode == Op.COLLECTIVE_PERMUTE and \
+                    st.ins.id in self._peer_cp:
+                # halo exchanges: a conv layer's left and right slab permutes
+                # go out on lanes 2 and 3 at once (one lane ran them back to
+                # back, ~0.03 ms each per layer at C4 N=4:
+                # profiles/r2_timeline_c4_n4.log)
+                st.lane = 2 + (ncp % 2 if os.environ.get("SPMD_EXPOSED_SPLIT", "1") != "0"
+                               else 0)
+                ncp += 1
             elif mode == "critical" and eng not in (0, 3, 4):
                 st.lane = 2
         torch = _torch()
