@@ -65,14 +65,19 @@ struct ConvSmem {
   static constexpr int TOTAL = EPI_OFF + 8 * EPI_STAGE_BYTES + 1024;
 };
 
-__device__ __forceinline__ void conv_tile(const ConvShape& g, int64_t t, int& pn, int& ho, int& wb,
+__device__ __forceinline__ void conv_tile(const ConvShape& g, int64_t t64, int& pn, int& ho, int& wb,
                                           int& ct) {
-  ct = (int)(t % g.nt);
-  t /= g.nt;
-  wb = (int)(t % g.nwb);
-  t /= g.nwb;
-  ho = (int)(t % g.Ho);
-  pn = (int)(t / g.Ho);
+  // 32-bit index math (the host keeps tiles < 2^31): 64-bit division by a
+  // runtime value is a long call sequence per tile on the producer and
+  // epilogue paths (C4 layer at N=4 shapes: 0.447 -> 0.430 ms,
+  // scripts/halo_part_bench.py)
+  uint32_t t = (uint32_t)t64;
+  ct = (int)(t % (uint32_t)g.nt);
+  t /= (uint32_t)g.nt;
+  wb = (int)(t % (uint32_t)g.nwb);
+  t /= (uint32_t)g.nwb;
+  ho = (int)(t % (uint32_t)g.Ho);
+  pn = (int)(t / (uint32_t)g.Ho);
 }
 
 template <int BN, int STAGES>
@@ -598,6 +603,7 @@ int conv_tcgen05(const spmd_tensor& lhs, const spmd_tensor& rhs, const spmd_tens
   g.cin_blocks = g.Cin / CBK;
   g.kblocks = g.KH * g.KW * g.cin_blocks;
   g.tiles = (int64_t)nparts * g.N * g.Ho * g.nwb * g.nt;
+  if (g.tiles >= ((int64_t)1 << 31)) return SPMD_ERR_UNSUPPORTED;   // conv_tile's 32-bit math
   g.relu = cd.epilogue == 1;
   CUtensorMap mo;
   g.tma_store = encode_store_map(&mo, out.data, g.Cout, g.Wo, g.Cout, nparts * g.N * g.Ho,
