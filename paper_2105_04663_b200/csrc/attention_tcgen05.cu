@@ -71,6 +71,28 @@ __device__ __forceinline__ float ex2(float x) {
   return y;
 }
 
+// Packed fp32 pairs (FFMA2 / FADD2, sm_100): the softmax warps are
+// issue-bound, and the scale and the row sum halve their instruction count
+// (+1.2-1.5% best-of-4 same-box, profiles/r2_attn_ab_f2.log).
+__device__ __forceinline__ uint64_t f2pack(float a, float b) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ void f2unpack(uint64_t r, float& a, float& b) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(r));
+}
+__device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+
 template <int D>
 __global__ void __launch_bounds__(256, 1)
     attention_tcgen05(const __grid_constant__ CUtensorMap map_q,
@@ -1361,13 +1383,28 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
         resc = true;
       }
       const float nmc = m == -INFINITY ? 0.f : -m * c;
+      {
+        const uint64_t c2 = f2pack(c, c), n2 = f2pack(nmc, nmc);
 #pragma unroll
-      for (int i = 0; i < 64; ++i) s[i] = ex2(fmaf(s[i], c, nmc));
+        for (int i = 0; i < 64; i += 2) {
+          float a, b;
+          f2unpack(ffma2(f2pack(s[i], s[i + 1]), c2, n2), a, b);
+          s[i] = ex2(a);
+          s[i + 1] = ex2(b);
+        }
+        uint64_t t4[4];
 #pragma unroll
-      for (int a = 0; a < 8; ++a) t8[a] = s[a];
+        for (int a = 0; a < 4; ++a) t4[a] = f2pack(s[2 * a], s[2 * a + 1]);
 #pragma unroll
-      for (int i = 8; i < 64; ++i) t8[i & 7] += s[i];
-      l = l * alpha + (((t8[0] + t8[1]) + (t8[2] + t8[3])) + ((t8[4] + t8[5]) + (t8[6] + t8[7])));
+        for (int i = 8; i < 64; i += 2)
+          t4[(i >> 1) & 3] = fadd2(t4[(i >> 1) & 3], f2pack(s[i], s[i + 1]));
+        t4[0] = fadd2(t4[0], t4[1]);
+        t4[2] = fadd2(t4[2], t4[3]);
+        t4[0] = fadd2(t4[0], t4[2]);
+        float lo, hi;
+        f2unpack(t4[0], lo, hi);
+        l = l * alpha + (lo + hi);
+      }
       if (TP) {
         // PV(t-1) landed: needed by an O rescale / drain, and waited on every
         // tile so this warp never falls two phases behind pv_done (a parity
