@@ -118,6 +118,9 @@ int spmd_broadcast(spmd_tensor in, spmd_tensor out, const int32_t* broadcast_dim
                    int64_t nparts, void* stream);
 int spmd_transpose(spmd_tensor in, spmd_tensor out, const int32_t* perm,
                    int64_t nparts, void* stream);
+/* Transpose -> ReLU (numpy maximum(x, 0): -0 -> +0, NaN kept) in one pass. */
+int spmd_transpose_relu(spmd_tensor in, spmd_tensor out, const int32_t* perm, int64_t nparts,
+                        void* stream);
 int spmd_reverse(spmd_tensor in, spmd_tensor out, const int32_t* dims, int ndims,
                  int64_t nparts, void* stream);
 int spmd_pad(spmd_tensor in, spmd_tensor value, spmd_tensor out, const int64_t* low,

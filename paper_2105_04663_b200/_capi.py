@@ -73,6 +73,7 @@ _SIGNATURES = {
     "spmd_convert": ([_T, _T, _I64, _P], _I),
     "spmd_broadcast": ([_T, _T, _PI32, _I64, _P], _I),
     "spmd_transpose": ([_T, _T, _PI32, _I64, _P], _I),
+    "spmd_transpose_relu": ([_T, _T, _PI32, _I64, _P], _I),
     "spmd_reverse": ([_T, _T, _PI32, _I, _I64, _P], _I),
     "spmd_pad": ([_T, _T, _T, _PI64, _PI64, _PI64, _I64, _P], _I),
     "spmd_slice": ([_T, _T, _PI64, _PI64, _I64, _P], _I),

@@ -260,7 +260,23 @@ struct CopyArgs {
   // 1: every thread ends with __threadfence_system() -- the destination is a
   // peer's heap (NVLink stores) and a peer barrier follows (peer.cu)
   int fence_sys;
+  // ReLU on the copied elements' bits (fused Transpose -> ReLU): 1 IEEE
+  // float (f32 / bf16: negative or -0 -> +0, NaN kept, as UnaryF's vmax), 2
+  // signed int
+  int relu;
 };
+
+template <typename T>
+__device__ __forceinline__ T relu_bits(T b, int mode) {
+  constexpr int BITS = 8 * sizeof(T);
+  if (BITS != 16 && BITS != 32) return b;
+  const T sign = (T)((T)1 << (BITS - 1));
+  if (!(b & sign)) return b;
+  if (mode == 2) return (T)0;
+  const T mag = (T)(b & (T)~sign);
+  const T inf = BITS == 16 ? (T)0x7f80 : (T)0x7f800000u;
+  return mag > inf ? b : (T)0;          // NaN stays
+}
 
 int launch_copy(const void* src, void* dst, int dtype, CopyArgs a, int64_t nparts,
                 cudaStream_t s);

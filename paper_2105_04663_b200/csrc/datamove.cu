@@ -60,13 +60,19 @@ __global__ void strided_copy_kernel(const T* __restrict__ src, T* __restrict__ d
       if (a.dyn_on_dst) d0 += off; else so += off;
     }
     if (V == 1) {
-      dst[d0] = src[so];
+      dst[d0] = a.relu ? relu_bits<T>(src[so], a.relu) : src[so];
     } else if (SPLAT) {
       const T v = src[so];
       T f[V];
 #pragma unroll
       for (int j = 0; j < V; ++j) f[j] = v;
       *reinterpret_cast<uint4*>(dst + d0) = *reinterpret_cast<uint4*>(f);
+    } else if (a.relu) {
+      uint4 w = *reinterpret_cast<const uint4*>(src + so);
+      T* e = reinterpret_cast<T*>(&w);
+#pragma unroll
+      for (int j = 0; j < V; ++j) e[j] = relu_bits<T>(e[j], a.relu);
+      *reinterpret_cast<uint4*>(dst + d0) = w;
     } else {
       *reinterpret_cast<uint4*>(dst + d0) = *reinterpret_cast<const uint4*>(src + so);
     }
@@ -110,6 +116,14 @@ __global__ void __launch_bounds__(256) row_copy_kernel(const T* __restrict__ src
 #pragma unroll
     for (int u = 0; u < ROW_U; ++u)
       if (v0 + u * 256 < per_row) v[u] = __ldcs(s4 + v0 + u * 256);
+    if (a.relu) {
+#pragma unroll
+      for (int u = 0; u < ROW_U; ++u) {
+        T* e = reinterpret_cast<T*>(&v[u]);
+#pragma unroll
+        for (int j = 0; j < V; ++j) e[j] = relu_bits<T>(e[j], a.relu);
+      }
+    }
 #pragma unroll
     for (int u = 0; u < ROW_U; ++u)
       if (v0 + u * 256 < per_row) __stcs(d4 + v0 + u * 256, v[u]);
@@ -408,8 +422,8 @@ extern "C" int spmd_broadcast(spmd_tensor in, spmd_tensor out, const int32_t* bd
   return launch_copy(in.data, out.data, out.dtype, a, nparts, as_stream(stream));
 }
 
-extern "C" int spmd_transpose(spmd_tensor in, spmd_tensor out, const int32_t* perm,
-                              int64_t nparts, void* stream) {
+static int transpose_impl(const spmd_tensor& in, const spmd_tensor& out, const int32_t* perm,
+                          int relu, int64_t nparts, void* stream) {
   SPMD_CHECK_ARG(in.dtype == out.dtype && in.rank == out.rank, "transpose mismatch");
   int64_t ist[SPMD_MAX_RANK];
   contiguous_strides(in, ist);
@@ -420,7 +434,22 @@ extern "C" int spmd_transpose(spmd_tensor in, spmd_tensor out, const int32_t* pe
     a.sst[j] = ist[perm[j]];
   }
   a.spart = a.dpart = numel(in);
+  a.relu = relu;
   return launch_copy(in.data, out.data, out.dtype, a, nparts, as_stream(stream));
+}
+
+extern "C" int spmd_transpose(spmd_tensor in, spmd_tensor out, const int32_t* perm,
+                              int64_t nparts, void* stream) {
+  return transpose_impl(in, out, perm, 0, nparts, stream);
+}
+
+// Transpose -> ReLU in one pass (the MoE layer's reshard annotations: the
+// dispatched tokens and the expert outputs are transposed, then ReLU'd).
+extern "C" int spmd_transpose_relu(spmd_tensor in, spmd_tensor out, const int32_t* perm,
+                                   int64_t nparts, void* stream) {
+  SPMD_CHECK_ARG(in.dtype == SPMD_F32 || in.dtype == SPMD_BF16 || in.dtype == SPMD_S32,
+                 "transpose_relu: f32 / bf16 / s32");
+  return transpose_impl(in, out, perm, in.dtype == SPMD_S32 ? 2 : 1, nparts, stream);
 }
 
 extern "C" int spmd_reverse(spmd_tensor in, spmd_tensor out, const int32_t* dims, int ndims,

@@ -623,6 +623,7 @@ class Executor:
         return users
 
     def _plan_fusions(self):
+        import os
         users = self._users()
         outs = set(self.graph.outputs)
         by = self.by_id
@@ -692,6 +693,15 @@ class Executor:
                 relu = by[users[ins.id][0]]
                 self._fused_skip.add(ins.id)
                 self._fused[relu.id] = ("dot_relu" if ins.opcode == Op.DOT else "conv_relu", ins)
+            # transpose -> relu: one pass (the MoE layer's reshard annotations)
+            if ins.opcode == Op.TRANSPOSE and only_user(ins.id, Op.RELU) and \
+                    ins.shape.dtype in (DType.F32, DType.BF16, DType.S32) and \
+                    ins.id not in self._fused and ins.id not in self._fused_skip and \
+                    os.environ.get("SPMD_TRANSPOSE_RELU", "1") != "0":
+                relu = by[users[ins.id][0]]
+                if relu.id not in self._fused:
+                    self._fused_skip.add(ins.id)
+                    self._fused[relu.id] = ("transpose_relu", ins)
         self._plan_backward(users, outs, only_user, const_value)
         self._plan_halo_windows(users, outs)
         self._plan_halo_convs(users, outs)
@@ -1242,6 +1252,18 @@ class Executor:
             def run(env, s):
                 out = self._alloc(shp)
                 C.check(fn(desc(env[a], ash), desc(env[b], bsh), desc(out, shp), P, s), f[0])
+                return out
+            return run
+        if f is not None and f[0] == "transpose_relu":
+            tr = f[1]
+            src = tr.operands[0]
+            ssh = self._shape(src)
+            perm = C.i32_array(tr.attrs["permutation"])
+
+            def run(env, s):
+                out = self._alloc(shp)
+                C.check(lib.spmd_transpose_relu(desc(env[src], ssh), desc(out, shp), perm, P, s),
+                        "transpose_relu")
                 return out
             return run
         if f is not None and f[0] == "dot_relu":

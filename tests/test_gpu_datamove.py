@@ -175,3 +175,44 @@ def test_mask_range_matches_select_chain(inner):
         g = np.arange(n) + offs[p]
         keep = ((g >= low) & (g < high))[None, :, None]
         np.testing.assert_array_equal(got[p], np.where(keep, x[p], fills[p]))
+
+
+@pytest.mark.parametrize("dims,perm,dt", [
+    ((4, 6, 8, 16), (1, 0, 2, 3), "bf16"),      # the MoE annotation transposes: vector path
+    ((4, 6, 8, 16), (1, 0, 2, 3), "f32"),
+    ((5, 7, 3), (2, 0, 1), "f32"),              # last dim moves: scalar path
+    ((3, 4, 16400), (1, 0, 2), "bf16"),         # row-chunk kernel (2050 vectors per row)
+    ((6, 10), (1, 0), "s32"),
+])
+def test_transpose_relu_matches_numpy(dims, perm, dt):
+    """spmd_transpose_relu == numpy maximum(transpose(x), 0) bit for bit,
+    with -0.0, NaN, +-inf and (ints) INT_MIN in the data."""
+    import torch
+    from paper_2105_04663_b200 import _capi as C
+    from paper_2105_04663_b200.executor import desc
+    from paper_2105_04663_b200.ir import DType, Shape
+    rng = np.random.default_rng(len(dims) + sum(dims))
+    if dt == "s32":
+        x = rng.integers(-50, 50, dims).astype(np.int32)
+        x.flat[0] = np.iinfo(np.int32).min
+        t = torch.from_numpy(x).cuda()
+        dtype = DType.S32
+    else:
+        x = rng.standard_normal(dims).astype(np.float32)
+        x.flat[:4] = [-0.0, np.nan, -np.inf, np.inf]
+        t = torch.from_numpy(x).cuda()
+        if dt == "bf16":
+            t = t.bfloat16()
+            x = t.float().cpu().numpy()
+        dtype = DType.BF16 if dt == "bf16" else DType.F32
+    odims = tuple(dims[p] for p in perm)
+    out = torch.empty(odims, dtype=t.dtype, device="cuda")
+    C.check(C.lib().spmd_transpose_relu(desc(t, Shape(dims, dtype)), desc(out, Shape(odims, dtype)),
+                                        C.i32_array(perm), 1,
+                                        torch.cuda.current_stream().cuda_stream), "transpose_relu")
+    torch.cuda.synchronize()
+    want = np.maximum(np.transpose(x, perm), 0)
+    got = out.float().cpu().numpy() if dt == "bf16" else out.cpu().numpy()
+    np.testing.assert_array_equal(got, want.astype(got.dtype))
+    if dt != "s32":
+        assert not np.signbit(got[np.transpose(x, perm) == 0]).any()   # -0 -> +0
