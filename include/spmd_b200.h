@@ -221,6 +221,14 @@ int spmd_moe_dispatch(spmd_tensor x, spmd_tensor expert, spmd_tensor slot, spmd_
 /* y [B,E,C,M] bf16 -> out [B,S,M] (== Dot(combine_weights, y)) */
 int spmd_moe_combine(spmd_tensor y, spmd_tensor expert, spmd_tensor slot, spmd_tensor gate,
                      spmd_tensor out, int64_t nparts, void* stream);
+/* The same gathers with the MoE layer's Transpose(1,0,2,3) -> ReLU annotation
+ * chain folded in (workloads.moe_layer): flags bit 0 = the expert-side tensor
+ * is [E,B,C,M] (dispatch writes it, combine reads it), bit 1 = ReLU on the
+ * copied / read values (numpy maximum(x, 0)). */
+int spmd_moe_dispatch_ex(spmd_tensor x, spmd_tensor expert, spmd_tensor slot, spmd_tensor out,
+                         int flags, int64_t nparts, void* stream);
+int spmd_moe_combine_ex(spmd_tensor y, spmd_tensor expert, spmd_tensor slot, spmd_tensor gate,
+                        spmd_tensor out, int flags, int64_t nparts, void* stream);
 /* dense dispatch / combine masks [B,S,E,C] from a routing */
 int spmd_moe_masks(spmd_tensor expert, spmd_tensor slot, spmd_tensor gate,
                    spmd_tensor dispatch, spmd_tensor combine, int64_t nparts, void* stream);

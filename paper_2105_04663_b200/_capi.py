@@ -99,6 +99,8 @@ _SIGNATURES = {
     "spmd_moe_route": ([_T, _I, _T, _T, _T, _I64, _P], _I),
     "spmd_moe_dispatch": ([_T, _T, _T, _T, _I64, _P], _I),
     "spmd_moe_combine": ([_T, _T, _T, _T, _T, _I64, _P], _I),
+    "spmd_moe_dispatch_ex": ([_T, _T, _T, _T, _I, _I64, _P], _I),
+    "spmd_moe_combine_ex": ([_T, _T, _T, _T, _T, _I, _I64, _P], _I),
     "spmd_moe_masks": ([_T, _T, _T, _T, _T, _I64, _P], _I),
     "spmd_local_all_gather": ([_T, _T, _I, _PI32, _I, _I, _I64, _P], _I),
     "spmd_local_all_reduce": ([_T, _T, _I, _PI32, _I, _I, _I64, _P], _I),

@@ -100,11 +100,24 @@ __global__ void moe_route_kernel(const T* __restrict__ logits, int32_t* __restri
   }
 }
 
-// One warp per (token, choice) assignment a = t * K + c.
+// One warp per (token, choice) assignment a = t * K + c.  flags (the
+// executor folds the MoE layer's Transpose(1,0,2,3) -> ReLU chain into the
+// gather): MOE_EBCM writes [P][E][B][C][M] instead of [P][B][E][C][M],
+// MOE_RELU applies ReLU to the copied values.
+enum { MOE_EBCM = 1, MOE_RELU = 2 };
+
+__device__ __forceinline__ int64_t moe_row(int flags, int64_t row, int e, int sl, int B, int E,
+                                           int C) {
+  if (!(flags & MOE_EBCM)) return (row * E + e) * (int64_t)C + sl;
+  const int64_t p = row / B, b = row - p * B;
+  return ((p * E + e) * (int64_t)B + b) * C + sl;
+}
+
 template <int V>
 __global__ void moe_dispatch_kernel(const uint16_t* __restrict__ x, const int32_t* __restrict__ expert,
                                     const int32_t* __restrict__ slot, uint16_t* __restrict__ out,
-                                    int64_t assigns, int K, int S, int E, int C, int M) {
+                                    int64_t assigns, int K, int S, int B, int E, int C, int M,
+                                    int flags) {
   const int lane = threadIdx.x & 31;
   const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
   for (int64_t a = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); a < assigns;
@@ -115,7 +128,7 @@ __global__ void moe_dispatch_kernel(const uint16_t* __restrict__ x, const int32_
     const int64_t row = t / S;   // (partition, batch) row
     const int e = expert[a];
     const uint4* src = reinterpret_cast<const uint4*>(x + t * (int64_t)M);
-    uint4* dst = reinterpret_cast<uint4*>(out + ((row * E + e) * (int64_t)C + sl) * M);
+    uint4* dst = reinterpret_cast<uint4*>(out + moe_row(flags, row, e, sl, B, E, C) * M);
     // 4 independent 16-byte loads in flight per lane (one row is M/V vectors)
     const int nv = M / V;
     for (int i0 = lane; i0 < nv; i0 += 128) {
@@ -123,6 +136,14 @@ __global__ void moe_dispatch_kernel(const uint16_t* __restrict__ x, const int32_
 #pragma unroll
       for (int u = 0; u < 4; ++u)
         if (i0 + 32 * u < nv) v[u] = __ldcs(src + i0 + 32 * u);
+      if (flags & MOE_RELU) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          uint16_t* h = reinterpret_cast<uint16_t*>(&v[u]);
+#pragma unroll
+          for (int q = 0; q < 8; ++q) h[q] = relu_bits<uint16_t>(h[q], 1);
+        }
+      }
 #pragma unroll
       for (int u = 0; u < 4; ++u)
         if (i0 + 32 * u < nv) dst[i0 + 32 * u] = v[u];
@@ -137,8 +158,8 @@ __global__ void moe_dispatch_kernel(const uint16_t* __restrict__ x, const int32_
 // oracle's f64 Dot(combine, y) produces (one nonzero term per choice).
 __global__ void moe_combine_kernel(const bf16* __restrict__ y, const int32_t* __restrict__ expert,
                                    const int32_t* __restrict__ slot, const float* __restrict__ gate,
-                                   bf16* __restrict__ out, int64_t tokens, int K, int S, int E,
-                                   int C, int M) {
+                                   bf16* __restrict__ out, int64_t tokens, int K, int S, int B,
+                                   int E, int C, int M, int flags) {
   const int lane = threadIdx.x & 31;
   const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
   for (int64_t t = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); t < tokens;
@@ -151,7 +172,7 @@ __global__ void moe_combine_kernel(const bf16* __restrict__ y, const int32_t* __
       const int sl = slot[t * K + c];
       if (sl >= C) continue;
       src[n] = reinterpret_cast<const uint4*>(
-          y + ((row * E + expert[t * K + c]) * (int64_t)C + sl) * M);
+          y + moe_row(flags, row, expert[t * K + c], sl, B, E, C) * M);
       g[n++] = (double)__bfloat162float(__float2bfloat16_rn(gate[t * K + c]));
     }
     uint4* dst = reinterpret_cast<uint4*>(out + t * (int64_t)M);
@@ -159,6 +180,11 @@ __global__ void moe_combine_kernel(const bf16* __restrict__ y, const int32_t* __
       double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
       for (int j = 0; j < n; ++j) {
         uint4 v = __ldcs(src[j] + i);
+        if (flags & MOE_RELU) {
+          uint16_t* r = reinterpret_cast<uint16_t*>(&v);
+#pragma unroll
+          for (int q = 0; q < 8; ++q) r[q] = relu_bits<uint16_t>(r[q], 1);
+        }
         const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&v);
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
@@ -235,14 +261,17 @@ extern "C" int spmd_moe_route(spmd_tensor logits, int capacity, spmd_tensor expe
 }
 
 // x [P, B, S, M] bf16 -> out [P, B, E, C, M] bf16 (zero-filled empty slots).
-extern "C" int spmd_moe_dispatch(spmd_tensor x, spmd_tensor expert, spmd_tensor slot,
-                                 spmd_tensor out, int64_t nparts, void* stream) {
+// x [P, B, S, M] -> out [P, B, E, C, M] (flags & MOE_EBCM: [P, E, B, C, M]).
+extern "C" int spmd_moe_dispatch_ex(spmd_tensor x, spmd_tensor expert, spmd_tensor slot,
+                                    spmd_tensor out, int flags, int64_t nparts, void* stream) {
   SPMD_CHECK_ARG(x.dtype == SPMD_BF16 && out.dtype == SPMD_BF16 && x.rank == 3 && out.rank == 4,
-                 "moe dispatch expects bf16 x [B,S,M] -> [B,E,C,M]");
-  const int S = (int)x.dims[1], M = (int)x.dims[2];
-  const int E = (int)out.dims[1], C = (int)out.dims[2];
+                 "moe dispatch expects bf16 x [B,S,M] -> [B,E,C,M] / [E,B,C,M]");
+  SPMD_CHECK_ARG(flags >= 0 && flags <= 3, "moe dispatch flags");
+  const int ebcm = flags & MOE_EBCM;
+  const int B = (int)x.dims[0], S = (int)x.dims[1], M = (int)x.dims[2];
+  const int E = (int)out.dims[ebcm ? 0 : 1], C = (int)out.dims[2];
   const int K = routing_k(expert, 2);
-  SPMD_CHECK_ARG(out.dims[0] == x.dims[0] && out.dims[3] == M && M % 8 == 0 && K >= 1 &&
+  SPMD_CHECK_ARG(out.dims[ebcm ? 1 : 0] == B && out.dims[3] == M && M % 8 == 0 && K >= 1 &&
                      routing_k(slot, 2) == K,
                  "moe dispatch shape");
   cudaStream_t s = as_stream(stream);
@@ -251,28 +280,41 @@ extern "C" int spmd_moe_dispatch(spmd_tensor x, spmd_tensor expert, spmd_tensor 
   if (assigns == 0) return SPMD_OK;
   moe_dispatch_kernel<8><<<grid_for(assigns * 32, 256), 256, 0, s>>>(
       (const uint16_t*)x.data, (const int32_t*)expert.data, (const int32_t*)slot.data,
-      (uint16_t*)out.data, assigns, K, S, E, C, M);
+      (uint16_t*)out.data, assigns, K, S, B, E, C, M, flags);
   return launched(s);
 }
 
-// y [P, B, E, C, M] bf16 -> out [P, B, S, M] bf16.
-extern "C" int spmd_moe_combine(spmd_tensor y, spmd_tensor expert, spmd_tensor slot,
-                                spmd_tensor gate, spmd_tensor out, int64_t nparts, void* stream) {
+extern "C" int spmd_moe_dispatch(spmd_tensor x, spmd_tensor expert, spmd_tensor slot,
+                                 spmd_tensor out, int64_t nparts, void* stream) {
+  return spmd_moe_dispatch_ex(x, expert, slot, out, 0, nparts, stream);
+}
+
+// y [P, B, E, C, M] (flags & MOE_EBCM: [P, E, B, C, M]) bf16 -> out [P, B, S, M] bf16.
+extern "C" int spmd_moe_combine_ex(spmd_tensor y, spmd_tensor expert, spmd_tensor slot,
+                                   spmd_tensor gate, spmd_tensor out, int flags, int64_t nparts,
+                                   void* stream) {
   SPMD_CHECK_ARG(y.dtype == SPMD_BF16 && out.dtype == SPMD_BF16 && y.rank == 4 && out.rank == 3,
-                 "moe combine expects bf16 y [B,E,C,M] -> [B,S,M]");
-  const int S = (int)out.dims[1], M = (int)out.dims[2];
-  const int E = (int)y.dims[1], C = (int)y.dims[2];
+                 "moe combine expects bf16 y [B,E,C,M] / [E,B,C,M] -> [B,S,M]");
+  SPMD_CHECK_ARG(flags >= 0 && flags <= 3, "moe combine flags");
+  const int ebcm = flags & MOE_EBCM;
+  const int B = (int)out.dims[0], S = (int)out.dims[1], M = (int)out.dims[2];
+  const int E = (int)y.dims[ebcm ? 0 : 1], C = (int)y.dims[2];
   const int K = routing_k(expert, 2);
-  SPMD_CHECK_ARG(M % 8 == 0 && y.dims[3] == M && K >= 1 && routing_k(slot, 2) == K &&
-                     routing_k(gate, 2) == K,
+  SPMD_CHECK_ARG(M % 8 == 0 && y.dims[3] == M && y.dims[ebcm ? 1 : 0] == B && K >= 1 &&
+                     routing_k(slot, 2) == K && routing_k(gate, 2) == K,
                  "moe combine shape");
   const int64_t tokens = out.dims[0] * S * nparts;
   if (tokens == 0) return SPMD_OK;
   cudaStream_t s = as_stream(stream);
   moe_combine_kernel<<<grid_for(tokens * 32, 256), 256, 0, s>>>(
       (const bf16*)y.data, (const int32_t*)expert.data, (const int32_t*)slot.data,
-      (const float*)gate.data, (bf16*)out.data, tokens, K, S, E, C, M);
+      (const float*)gate.data, (bf16*)out.data, tokens, K, S, B, E, C, M, flags);
   return launched(s);
+}
+
+extern "C" int spmd_moe_combine(spmd_tensor y, spmd_tensor expert, spmd_tensor slot,
+                                spmd_tensor gate, spmd_tensor out, int64_t nparts, void* stream) {
+  return spmd_moe_combine_ex(y, expert, slot, gate, out, 0, nparts, stream);
 }
 
 // Dense masks [P, B, S, E, C] (dispatch = 1 at every kept choice, combine =

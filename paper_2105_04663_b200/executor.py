@@ -699,9 +699,33 @@ class Executor:
                     ins.id not in self._fused and ins.id not in self._fused_skip and \
                     os.environ.get("SPMD_TRANSPOSE_RELU", "1") != "0":
                 relu = by[users[ins.id][0]]
-                if relu.id not in self._fused:
+                src = self._fused.get(ins.operands[0])
+                if relu.id in self._fused:
+                    pass
+                elif src is not None and src[0] == "moe_dispatch" and len(src) == 3 and \
+                        tuple(ins.attrs["permutation"]) == (1, 0, 2, 3) and \
+                        only_user(ins.operands[0], Op.TRANSPOSE):
+                    # dispatch -> Transpose(1,0,2,3) -> ReLU: the gather writes
+                    # [E,B,C,M] rows with the ReLU applied (no extra pass)
+                    self._fused_skip.update((ins.operands[0], ins.id))
+                    del self._fused[ins.operands[0]]
+                    self._fused[relu.id] = ("moe_dispatch", src[1], src[2], 3)
+                else:
                     self._fused_skip.add(ins.id)
                     self._fused[relu.id] = ("transpose_relu", ins)
+        # Transpose(1,0,2,3) -> ReLU -> combine gather: the gather reads the
+        # [E,B,C,M] expert outputs and applies the ReLU itself
+        for cid, spec in list(self._fused.items()):
+            if spec[0] != "moe_combine" or len(spec) != 3:
+                continue
+            tr = self._fused.get(spec[1])
+            if tr is None or tr[0] != "transpose_relu" or spec[1] in outs or \
+                    tuple(tr[1].attrs["permutation"]) != (1, 0, 2, 3) or \
+                    len(users.get(spec[1], [])) != 1:
+                continue
+            self._fused_skip.add(spec[1])
+            del self._fused[spec[1]]
+            self._fused[cid] = ("moe_combine", tr[1].operands[0], spec[2], 3)
         self._plan_backward(users, outs, only_user, const_value)
         self._plan_halo_windows(users, outs)
         self._plan_halo_convs(users, outs)
@@ -1297,7 +1321,8 @@ class Executor:
                 return out
             return run
         if f is not None and f[0] in ("moe_dispatch", "moe_combine"):
-            _, x, ridx = f
+            x, ridx = f[1], f[2]
+            flags = f[3] if len(f) > 3 else 0     # moe.cu MOE_EBCM | MOE_RELU
             xsh = self._shape(x)
             r = self.routing[ridx]
             ish = Shape(tuple(r.expert.shape[1:]), DType.S32)
@@ -1306,12 +1331,12 @@ class Executor:
             def run(env, s):
                 out = self._alloc(shp)
                 if f[0] == "moe_dispatch":
-                    rc = lib.spmd_moe_dispatch(desc(env[x], xsh), desc(r.expert, ish),
-                                               desc(r.slot, ish), desc(out, shp), P, s)
+                    rc = lib.spmd_moe_dispatch_ex(desc(env[x], xsh), desc(r.expert, ish),
+                                                  desc(r.slot, ish), desc(out, shp), flags, P, s)
                 else:
-                    rc = lib.spmd_moe_combine(desc(env[x], xsh), desc(r.expert, ish),
-                                              desc(r.slot, ish), desc(r.gate, gsh),
-                                              desc(out, shp), P, s)
+                    rc = lib.spmd_moe_combine_ex(desc(env[x], xsh), desc(r.expert, ish),
+                                                 desc(r.slot, ish), desc(r.gate, gsh),
+                                                 desc(out, shp), flags, P, s)
                 C.check(rc, f[0])
                 return out
             return run

@@ -168,6 +168,10 @@ def test_executor_routing_equals_dense_masks(n, k):
                       routing={idx["dispatch"]: r, idx["combine"]: r})
     kinds = sorted(v[0] for v in routed._fused.values() if v[0].startswith("moe_"))
     assert kinds == ["moe_combine", "moe_dispatch"]
+    if n == 1:   # the Transpose(1,0,2,3) -> ReLU chains fold into both gathers
+        flags = {v[0]: (v[3] if len(v) > 3 else 0) for v in routed._fused.values()
+                 if v[0].startswith("moe_")}
+        assert flags == {"moe_dispatch": 3, "moe_combine": 3}, flags
     dense = Executor(prog, nparts=n, device=dev, fuse=True)
     a = routed.run(stacked)[0]
     b = dense.run(stacked)[0]
