@@ -159,6 +159,12 @@ typedef struct {
 } spmd_dot_dims;
 int spmd_dot(spmd_tensor lhs, spmd_tensor rhs, spmd_tensor out, const spmd_dot_dims* dd,
              int64_t nparts, void* stream);
+/* out = Dot(lhs, rhs) + resid (bf16; resid has the output's shape): the
+ * layer's residual Add (simulator.py:173-198) folded into the GEMM epilogue,
+ * one fp32 add before the single rounding.  SPMD_ERR_UNSUPPORTED when the
+ * wide tcgen05 GEMM does not apply (run spmd_dot and the Add instead). */
+int spmd_dot_add(spmd_tensor lhs, spmd_tensor rhs, spmd_tensor resid, spmd_tensor out,
+                 const spmd_dot_dims* dd, int64_t nparts, void* stream);
 
 typedef struct {
   int32_t lhs_batch, lhs_feature, rhs_in_feature, rhs_out_feature, out_batch, out_feature;

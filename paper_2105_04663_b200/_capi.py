@@ -84,6 +84,7 @@ _SIGNATURES = {
     "spmd_shift": ([_T, _T, _T, _I, _I64, _I64, _P], _I),
     "spmd_reduce": ([_T, _T, _T, _PI32, _I, _I, _I64, _P], _I),
     "spmd_dot": ([_T, _T, _T, ctypes.POINTER(SpmdDotDims), _I64, _P], _I),
+    "spmd_dot_add": ([_T, _T, _T, _T, ctypes.POINTER(SpmdDotDims), _I64, _P], _I),
     "spmd_convolution": ([_T, _T, _T, ctypes.POINTER(SpmdConvDims), _I64, _P], _I),
     "spmd_softmax_lastdim": ([_T, _T, _I64, _P], _I),
     "spmd_softmax_backward_lastdim": ([_T, _T, _T, _I64, _P], _I),

@@ -74,7 +74,7 @@ struct GemmScatter {
 // scattered dim is not the whole GEMM N).
 int dot_tcgen05(const spmd_tensor& lhs, const spmd_tensor& rhs, const spmd_tensor& out,
                 const spmd_dot_dims& dd, int64_t nparts, cudaStream_t s,
-                const GemmScatter* sc = nullptr);
+                const GemmScatter* sc = nullptr, const void* resid = nullptr);
 // Implemented in gemm_tf32x3.cu: large f32 Dots as a 3xTF32 tcgen05 GEMM;
 // SPMD_ERR_UNSUPPORTED for small / untileable ones (SIMT fp64 path then).
 int dot_tf32x3(const spmd_tensor& lhs, const spmd_tensor& rhs, const spmd_tensor& out,

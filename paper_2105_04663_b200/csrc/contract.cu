@@ -204,6 +204,22 @@ int conv_tcgen05(const spmd_tensor& lhs, const spmd_tensor& rhs, const spmd_tens
 
 using namespace spmd;
 
+// out = Dot(lhs, rhs) + resid (bf16, the Dot's output shape): the residual
+// add of a Transformer layer folded into the GEMM epilogue (one fp32 add
+// before the single rounding).  SPMD_ERR_UNSUPPORTED when the GEMM does not
+// take the wide tcgen05 kernel -- the caller then runs spmd_dot + the add.
+extern "C" int spmd_dot_add(spmd_tensor lhs, spmd_tensor rhs, spmd_tensor resid, spmd_tensor out,
+                            const spmd_dot_dims* dd, int64_t nparts, void* stream) {
+  SPMD_CHECK_ARG(lhs.dtype == SPMD_BF16 && rhs.dtype == SPMD_BF16 && out.dtype == SPMD_BF16 &&
+                     resid.dtype == SPMD_BF16 && numel(resid) == numel(out) &&
+                     resid.rank == out.rank,
+                 "dot_add expects bf16 operands and a residual of the output's shape");
+  for (int i = 0; i < out.rank; ++i)
+    SPMD_CHECK_ARG(resid.dims[i] == out.dims[i], "dot_add residual shape");
+  if (numel(out) * nparts == 0) return SPMD_OK;
+  return dot_tcgen05(lhs, rhs, out, *dd, nparts, as_stream(stream), nullptr, resid.data);
+}
+
 extern "C" int spmd_dot(spmd_tensor lhs, spmd_tensor rhs, spmd_tensor out, const spmd_dot_dims* dd,
                         int64_t nparts, void* stream) {
   SPMD_CHECK_ARG(lhs.dtype == rhs.dtype && lhs.dtype == out.dtype, "dot dtype mismatch");

@@ -61,6 +61,9 @@ struct GemmShape {
   int sc_rows;          // all-to-all (row-chunk) scatter, wide kernel only
   int64_t sc_rchunk;
   int sc_slot_base, sc_nslots;
+  // wide kernel, plain store epilogue: C = A.B + resid (same [nbat][M][N]
+  // layout as C), added in fp32 before the one rounding (spmd_dot_add)
+  const bf16* resid;
 };
 
 // Per-destination store maps of the reduce-scatter epilogue: rank j's heap as
@@ -588,6 +591,31 @@ __device__ __forceinline__ int64_t ring_take(int32_t* ids, uint64_t* rfull, uint
   return t;
 }
 
+// Lane `lane` of an epilogue warp holds row row0 + lane, columns [col, col + 32)
+// of the tile in r[] (fp32 bits): add the residual's bf16 values in fp32.
+__device__ __forceinline__ void add_resid_chunk(const GemmShape& g, int b, int row0, int col,
+                                                int lane, uint32_t (&r)[32]) {
+  const int row = row0 + lane;
+  if (row >= g.M) return;
+  const bf16* src = g.resid + (int64_t)b * g.out_batch_stride + (int64_t)row * g.N + col;
+  if (col + 32 <= g.N && (((uintptr_t)src) & 15) == 0) {
+    uint4 v[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) v[q] = __ldcs(reinterpret_cast<const uint4*>(src) + q);
+    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(v);
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const float2 f = __bfloat1622float2(h[i]);
+      r[2 * i] = __float_as_uint(__uint_as_float(r[2 * i]) + f.x);
+      r[2 * i + 1] = __float_as_uint(__uint_as_float(r[2 * i + 1]) + f.y);
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < 32; ++i)
+      if (col + i < g.N) r[i] = __float_as_uint(__uint_as_float(r[i]) + __bfloat162float(src[i]));
+  }
+}
+
 template <int STAGES>
 struct SmemW {
   static constexpr int A_BYTES = HALF * BK * 2;              // 16 KB
@@ -793,6 +821,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
           epi_store_chunk(&smaps.m[j], epi + (chunk++ & 1) * EPI_STAGE_BYTES, r, g.relu,
                           (int)(col - j * g.sc_chunk), row0, par * g.sc_par + g.sc_pos, lane);
         } else {
+          if (g.resid) add_resid_chunk(g, b, row0, col, lane, r);
           epi_store_chunk(&map_c, epi + (chunk++ & 1) * EPI_STAGE_BYTES, r, g.relu, col, row0,
                           b, lane, store_pol);
         }
@@ -1014,7 +1043,8 @@ int gemm_layout(const spmd_tensor& lhs, const spmd_tensor& rhs, const spmd_tenso
 }
 
 int dot_tcgen05(const spmd_tensor& lhs, const spmd_tensor& rhs, const spmd_tensor& out,
-                const spmd_dot_dims& dd, int64_t nparts, cudaStream_t s, const GemmScatter* sc) {
+                const spmd_dot_dims& dd, int64_t nparts, cudaStream_t s, const GemmScatter* sc,
+                const void* resid) {
   if (lhs.dtype != SPMD_BF16) return SPMD_ERR_UNSUPPORTED;
   GemmLayout lay;
   if (int rc = gemm_layout(lhs, rhs, out, dd, nparts, &lay)) return rc;
@@ -1030,6 +1060,8 @@ int dot_tcgen05(const spmd_tensor& lhs, const spmd_tensor& rhs, const spmd_tenso
   g.a_mn = a_mn;
   g.b_mn = b_mn;
   g.relu = dd.epilogue == 1;
+  g.resid = (const bf16*)resid;
+  if (resid && (sc || g.relu || (reinterpret_cast<uintptr_t>(resid) & 15))) return SPMD_ERR_UNSUPPORTED;
   const int group_opt = (int)option(OPT_GEMM_GROUP);   // 0: per-kernel default
   g.group = group_opt > 0 ? group_opt : 8;
   g.raster_n = (int)option(OPT_GEMM_RASTER_N);
@@ -1111,6 +1143,7 @@ int dot_tcgen05(const spmd_tensor& lhs, const spmd_tensor& rhs, const spmd_tenso
       return launch_gemm_2sm_wide<4>(ma, mb, mc, g, smaps, s);
     }
   }
+  if (g.resid) return SPMD_ERR_UNSUPPORTED;   // residual epilogue: wide kernel only
   if ((gemm_mode() >= 2 || sc) && (int64_t)g.M >= 256 && (int64_t)g.N >= 256) {
     // 2-CTA path: per-CTA boxes are 128 rows of A and 128 rows of B.
     bool ok2 = a_mn ? encode(&ma, lhs.data, va, 64, BK) : encode(&ma, lhs.data, va, BK, HALF);

@@ -380,7 +380,8 @@ class Executor:
         # 15.56-16.81 for as-soon-as-possible, profiles/r1_c2_n4_ab_wide_lanes_engines.log)
         depth = max(1, int(os.environ.get("SPMD_PREFETCH_DEPTH", "2")))
         heavy_ops = (Op.DOT, Op.CONVOLUTION)
-        heavy_fused = ("dot_relu", "conv_relu", "attention", "dot_rs", "dot_a2a", "halo_conv")
+        heavy_fused = ("dot_relu", "conv_relu", "attention", "dot_rs", "dot_a2a", "halo_conv",
+                       "dot_add")
 
         def heavy(st):
             f = self._fused.get(st.ins.id)
@@ -571,7 +572,7 @@ class Executor:
         # hidden gathers: copy engines (0), background SM pull (3) or NCCL (-1)
         hidden_mode = os.environ.get("SPMD_PEER_HIDDEN_ENGINE", "ce")
         heavy_ops = (Op.DOT, Op.CONVOLUTION)
-        heavy_fused = ("dot_relu", "conv_relu", "attention", "dot_rs", "dot_a2a")
+        heavy_fused = ("dot_relu", "conv_relu", "attention", "dot_rs", "dot_a2a", "dot_add")
         eng = {}
         order = self.steps
         for i, st in enumerate(order):
@@ -713,6 +714,22 @@ class Executor:
                 else:
                     self._fused_skip.add(ins.id)
                     self._fused[relu.id] = ("transpose_relu", ins)
+            # dot -> residual add: the add runs in the GEMM epilogue (fp32,
+            # one rounding); falls back to dot + add if the wide GEMM does
+            # not take it
+            if ins.opcode == Op.ADD and ins.shape.dtype == DType.BF16 and \
+                    ins.id not in self._fused and \
+                    os.environ.get("SPMD_DOT_ADD", "1") != "0":
+                for k in (0, 1):
+                    d, r = ins.operands[k], ins.operands[1 - k]
+                    dot = by[d]
+                    if dot.opcode == Op.DOT and dot.shape == ins.shape and \
+                            by[r].shape == ins.shape and d != r and \
+                            only_user(d, Op.ADD) and d not in self._fused and \
+                            d not in self._fused_skip:
+                        self._fused_skip.add(d)
+                        self._fused[ins.id] = ("dot_add", dot, r)
+                        break
         # Transpose(1,0,2,3) -> ReLU -> combine gather: the gather reads the
         # [E,B,C,M] expert outputs and applies the ReLU itself
         for cid, spec in list(self._fused.items()):
@@ -1229,6 +1246,8 @@ class Executor:
             return tuple(f[1]) + (f[3],) + ((mask[2], mask[3]) if mask is not None else ())
         if f[0] in ("moe_dispatch", "moe_combine", "moe_dispatch_a2a"):
             return (f[1],)
+        if f[0] == "dot_add":
+            return tuple(f[1].operands) + (f[2],)
         if f[0] == "halo_conv":
             _, conv, _, (_, pieces, _, start, mask), _ = f
             return tuple(pieces) + (start,) + ((mask[2],) if mask is not None else ()) + \
@@ -1276,6 +1295,27 @@ class Executor:
             def run(env, s):
                 out = self._alloc(shp)
                 C.check(fn(desc(env[a], ash), desc(env[b], bsh), desc(out, shp), P, s), f[0])
+                return out
+            return run
+        if f is not None and f[0] == "dot_add":
+            dot, res = f[1], f[2]
+            a, b = dot.operands
+            ash, bsh = self._shape(a), self._shape(b)
+            dd = self._dot_dims(dot)
+            ref = ctypes.byref(dd)
+
+            def run(env, s):
+                out = self._alloc(shp)
+                rc = lib.spmd_dot_add(desc(env[a], ash), desc(env[b], bsh), desc(env[res], shp),
+                                      desc(out, shp), ref, P, s)
+                if rc == C.ERR_UNSUPPORTED:
+                    # not a wide-GEMM shape: the Dot, then the Add in place
+                    C.check(lib.spmd_dot(desc(env[a], ash), desc(env[b], bsh), desc(out, shp),
+                                         ref, P, s), "dot")
+                    C.check(lib.spmd_binary(_BINARY[Op.ADD], 0, desc(out, shp),
+                                            desc(env[res], shp), desc(out, shp), P, s), "add")
+                else:
+                    C.check(rc, "dot_add")
                 return out
             return run
         if f is not None and f[0] == "transpose_relu":

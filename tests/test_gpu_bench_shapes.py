@@ -227,3 +227,33 @@ def test_c4_conv_at_paper_dims(taps, wres):
     ref = torch.relu(F.conv2d(x.float().permute(0, 3, 1, 2), w.float().permute(3, 2, 0, 1),
                               padding=1)).permute(0, 2, 3, 1)
     assert _err(out, ref) < BF16_TOL
+
+
+@pytest.mark.parametrize("M,N,K", [(16384, 8192, 65536 // 8), (2048, 1024, 512), (300, 520, 256)])
+def test_dot_add_epilogue(M, N, K):
+    """spmd_dot_add: C = A.B + R with the add in the wide GEMM's epilogue
+    (fp32, one rounding) vs fp32 torch; shapes the wide kernel does not take
+    report SPMD_ERR_UNSUPPORTED (the executor then runs Dot + Add)."""
+    import torch
+    from paper_2105_04663_b200 import _capi as C
+    from paper_2105_04663_b200.executor import desc
+    from paper_2105_04663_b200.ir import DType, Shape
+    g = torch.Generator(device="cuda").manual_seed(M + N + K)
+    a = torch.randn((M, K), generator=g, device="cuda").bfloat16()
+    b = (torch.randn((K, N), generator=g, device="cuda") / K ** 0.5).bfloat16()
+    r = torch.randn((M, N), generator=g, device="cuda").bfloat16()
+    out = torch.empty((M, N), dtype=torch.bfloat16, device="cuda")
+    dd = C.SpmdDotDims()
+    dd.n_contract = 1
+    dd.lhs_contracting[0], dd.rhs_contracting[0] = 1, 0
+    bf = DType.BF16
+    rc = C.lib().spmd_dot_add(desc(a, Shape((M, K), bf)), desc(b, Shape((K, N), bf)),
+                              desc(r, Shape((M, N), bf)), desc(out, Shape((M, N), bf)),
+                              ctypes.byref(dd), 1, torch.cuda.current_stream().cuda_stream)
+    if M < 256 or N < 512:
+        assert rc == C.ERR_UNSUPPORTED
+        return
+    C.check(rc, "dot_add")
+    torch.cuda.synchronize()
+    ref = a.float() @ b.float() + r.float()
+    assert _err(out, ref) < BF16_TOL
