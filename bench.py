@@ -347,15 +347,18 @@ class _Run:
 
 
 def _time_steps(run, steps, warmup, eager, barrier, world, dev):
-    """W-1 eager warm-up runs (materialise constants, NCCL sub-communicators,
-    kernel attributes), capture of the whole step into one CUDA graph
-    (compute + comm streams), one warm replay, then K timed replays between
-    barriers.  Returns (ms max over ranks, step fn, graph, outs, launches/step)."""
+    """W warm-up steps: one eager run (materialises constants, NCCL
+    sub-communicators, kernel attributes), capture of the whole step into one
+    CUDA graph (compute + comm streams), W-1 warm replays (the first replays
+    after another config ran in the process were measured slow: peer-heap
+    pages first touched over NVLink); then K timed replays between barriers.
+    Eager mode: W eager warm-up runs.  Returns (ms max over ranks, step fn,
+    graph, outs, launches/step)."""
     import torch
     import torch.distributed as dist
     ex, inputs = run.ex, run.inputs
     stream = torch.cuda.current_stream(dev)
-    for _ in range(max(1, warmup - 1)):
+    for _ in range(max(1, warmup - 1) if eager else 1):
         ex.run(inputs)
     torch.cuda.synchronize()
     ex.check_errors()
@@ -373,7 +376,8 @@ def _time_steps(run, steps, warmup, eager, barrier, world, dev):
         def step():
             graph.replay()
             return outs
-    step()
+    for _ in range(1 if eager else max(1, warmup - 1)):
+        step()
     torch.cuda.synchronize()
     barrier()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -485,8 +489,14 @@ def _extra_config(config, world, rank, dev, comm, barrier, steps, warmup, burst,
     """A compact summary of another BASELINE config, same harness: step time
     (CUDA-graph replay, max over ranks), TFLOP/s, MFU and the roofline of its
     dominant kernel."""
+    import time
     import torch
     run = _Run(config, world, rank, dev, comm)
+    # let the power controller recover from the previous config: right after
+    # the C2 layer the first C3 replays ran ~20% slow at N=4 (clock transient
+    # under the power cap; a 1 s pause removes it, scripts/extras_order.py)
+    torch.cuda.synchronize()
+    time.sleep(1.0)
     ms, _, graph, outs, launches = _time_steps(run, steps, warmup, False, barrier, world, dev)
     tf = run.flops / (ms * 1e-3) / 1e12
     roof = _top_kernel(run, dev, burst, sustained, peak_src, reps=10)
@@ -833,7 +843,8 @@ def main():
                                       "tflops": alt.flops / (ams * 1e-3) / 1e12}
             del alt, ag, ao
             torch.cuda.empty_cache()
-        for cfg in ("c1", "c3", "c4") if world in (1, 4) else ("c3", "c4"):
+        # C1 last: its 3xTF32 scratch pool keeps its memory (keep_pool_memory)
+        for cfg in ("c3", "c4", "c1") if world in (1, 4) else ("c3", "c4"):
             configs[cfg] = _extra_config(cfg, world, rank, dev, comm, barrier,
                                          max(5, args.steps // 2), args.warmup, burst, sustained,
                                          peak_src)
