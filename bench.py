@@ -489,7 +489,6 @@ def _extra_config(config, world, rank, dev, comm, barrier, steps, warmup, burst,
     """A compact summary of another BASELINE config, same harness: step time
     (CUDA-graph replay, max over ranks), TFLOP/s, MFU and the roofline of its
     dominant kernel."""
-    import time
     import torch
     run = _Run(config, world, rank, dev, comm)
     # let the power controller recover from the previous config: right after
@@ -837,6 +836,8 @@ def main():
             # BASELINE's 2x2 is the headline at N=4; the 1x4 mesh (no data
             # axis: no weight gathers) as the alternative layout
             alt = _Run("c2", world, rank, dev, comm, mesh=(1, 4))
+            torch.cuda.synchronize()
+            time.sleep(1.0)                  # see _extra_config
             ams, _, ag, ao, _ = _time_steps(alt, args.steps, args.warmup, False, barrier, world,
                                             dev)
             configs["c2_mesh_1x4"] = {"mesh": [1, 4], "ms_per_step": ams,
