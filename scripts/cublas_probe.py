@@ -1,3 +1,5 @@
+"""cuBLAS (torch.matmul) bf16 on the C2 FFN-in shape, launched for an ncu
+capture (the cuBLAS side of profiles/r2_cublas_ffn_ncu_raw.csv)."""
 import torch
 M,N,K=16384,65536,8192
 a=torch.randn(M,K,device="cuda",dtype=torch.bfloat16); b=torch.randn(K,N,device="cuda",dtype=torch.bfloat16)*0.01
