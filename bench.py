@@ -517,18 +517,19 @@ def _extra_config(config, world, rank, dev, comm, barrier, steps, warmup, burst,
 
 
 def _c5_hbm(dev, hbm, peak_src):
-    """C5's HBM-bound kernels at the 8-way uneven layout ([1001, 524288] f32
-    over 8 shards of ceil(1001/8) = 126 rows): the localize pad 1001 -> 1008
-    rows (partitioner.py:379-408), the dynamic-slice of one shard out of it,
-    and the select_range mask of the last shard (partitioner.py:236-247).
+    """C5's HBM-bound kernels at the 8-way uneven layout ([1001, D1] over 8
+    shards of ceil(1001/8) = 126 rows): the localize pad 1001 -> 1008 rows
+    (partitioner.py:379-408), the dynamic-slice of one shard out of it, and
+    the select_range mask of the last shard (partitioner.py:236-247) -- for
+    f32 and bf16 at D1 = 524288 and f32 at D1 = 65536.
     Achieved = bytes read + written / kernel time (CUDA events, 10 launches)."""
     import torch
     from paper_2105_04663_b200 import _capi as C
     from paper_2105_04663_b200.executor import desc
     from paper_2105_04663_b200.ir import DType, Shape
     lib, st = C.lib(), torch.cuda.current_stream(dev).cuda_stream
-    f32, s32 = DType.F32, DType.S32
-    D1, rows = 524288, 126
+    s32 = DType.S32
+    rows = 126
     sc = Shape((), s32)
 
     def timed(fn, reps=10):
@@ -544,32 +545,36 @@ def _c5_hbm(dev, hbm, peak_src):
         return e0.elapsed_time(e1) / reps
 
     res = {}
-    x = torch.randn((1, 1001, D1), device=dev)
-    y = torch.empty((1, 1008, D1), device=dev)
-    z = torch.zeros((1,), device=dev)
-    lo, hi, it = C.i64_array([0, 0]), C.i64_array([7, 0]), C.i64_array([0, 0])
-    ms = timed(lambda: C.check(lib.spmd_pad(desc(x, Shape((1001, D1), f32)),
-                                            desc(z, Shape((), f32)),
-                                            desc(y, Shape((1008, D1), f32)), lo, hi, it, 1, st),
-                               "pad"))
-    res["pad_1001_to_1008x524288_f32"] = (ms, (x.numel() + y.numel()) * 4)
-    s0 = torch.full((1,), rows * 7, dtype=torch.int32, device=dev)
-    s1 = torch.zeros((1,), dtype=torch.int32, device=dev)
-    y2 = torch.empty((1, rows, D1), device=dev)
-    starts = (C.SpmdTensor * 2)(desc(s0, sc), desc(s1, sc))
-    ms = timed(lambda: C.check(lib.spmd_dynamic_slice(desc(y, Shape((1008, D1), f32)), starts,
-                                                      desc(y2, Shape((rows, D1), f32)), 1, st),
-                               "dynamic_slice"))
-    res["dynamic_slice_1008_to_126x524288_f32"] = (ms, 2 * y2.numel() * 4)
-    off = torch.full((1,), 7 * rows, dtype=torch.int32, device=dev)
-    fill = torch.full((1,), float("-inf"), device=dev)
-    y3 = torch.empty_like(y2)
-    ms = timed(lambda: C.check(lib.spmd_mask_range(
-        desc(y2, Shape((rows, D1), f32)), desc(off, sc), desc(fill, Shape((), f32)),
-        desc(y3, Shape((rows, D1), f32)), 0, 0, 1001, 0, 1, st), "mask_range"))
-    res["mask_range_126x524288_f32"] = (ms, 2 * y2.numel() * 4)
-    del x, y, y2, y3
-    torch.cuda.empty_cache()
+    for D1, dt in ((524288, DType.F32), (524288, DType.BF16), (65536, DType.F32)):
+        tdt = torch.float32 if dt == DType.F32 else torch.bfloat16
+        es = 4 if dt == DType.F32 else 2
+        tag = "%dx%d_%s" % (rows, D1, dt.value)
+        x = torch.randn((1, 1001, D1), device=dev).to(tdt)
+        y = torch.empty((1, 1008, D1), device=dev, dtype=tdt)
+        z = torch.zeros((1,), device=dev, dtype=tdt)
+        lo, hi, it = C.i64_array([0, 0]), C.i64_array([7, 0]), C.i64_array([0, 0])
+        ms = timed(lambda: C.check(lib.spmd_pad(desc(x, Shape((1001, D1), dt)),
+                                                desc(z, Shape((), dt)),
+                                                desc(y, Shape((1008, D1), dt)), lo, hi, it, 1,
+                                                st), "pad"))
+        res["pad_1001_to_1008x%d_%s" % (D1, dt.value)] = (ms, (x.numel() + y.numel()) * es)
+        s0 = torch.full((1,), rows * 7, dtype=torch.int32, device=dev)
+        s1 = torch.zeros((1,), dtype=torch.int32, device=dev)
+        y2 = torch.empty((1, rows, D1), device=dev, dtype=tdt)
+        starts = (C.SpmdTensor * 2)(desc(s0, sc), desc(s1, sc))
+        ms = timed(lambda: C.check(lib.spmd_dynamic_slice(desc(y, Shape((1008, D1), dt)), starts,
+                                                          desc(y2, Shape((rows, D1), dt)), 1,
+                                                          st), "dynamic_slice"))
+        res["dynamic_slice_1008_to_" + tag] = (ms, 2 * y2.numel() * es)
+        off = torch.full((1,), 7 * rows, dtype=torch.int32, device=dev)
+        fill = torch.full((1,), float("-inf"), device=dev, dtype=tdt)
+        y3 = torch.empty_like(y2)
+        ms = timed(lambda: C.check(lib.spmd_mask_range(
+            desc(y2, Shape((rows, D1), dt)), desc(off, sc), desc(fill, Shape((), dt)),
+            desc(y3, Shape((rows, D1), dt)), 0, 0, 1001, 0, 1, st), "mask_range"))
+        res["mask_range_" + tag] = (ms, 2 * y2.numel() * es)
+        del x, y, y2, y3
+        torch.cuda.empty_cache()
     return {"bound": "hbm", "peak_gbs": hbm, "peak_source": peak_src + " copy bandwidth",
             "kernels": {k: {"ms": ms, "bytes": b, "gbs": b / (ms * 1e-3) / 1e9,
                             "frac": b / (ms * 1e-3) / 1e9 / hbm} for k, (ms, b) in res.items()}}
