@@ -159,6 +159,12 @@ typedef struct {
 } spmd_dot_dims;
 int spmd_dot(spmd_tensor lhs, spmd_tensor rhs, spmd_tensor out, const spmd_dot_dims* dd,
              int64_t nparts, void* stream);
+/* f32 Dot whose lhs comes as tf32 hi / lo halves (spmd_local_all_gather_split):
+ * the 3xTF32 GEMM without the lhs split pass; SPMD_ERR_UNSUPPORTED when the
+ * 3xTF32 path does not apply (lhs = hi + lo exactly; run spmd_dot). */
+int spmd_dot_f32_presplit(spmd_tensor lhs_hi, spmd_tensor lhs_lo, spmd_tensor rhs,
+                          spmd_tensor out, const spmd_dot_dims* dd, int64_t nparts,
+                          void* stream);
 /* out = Dot(lhs, rhs) + resid (bf16; resid has the output's shape): the
  * layer's residual Add (simulator.py:173-198) folded into the GEMM epilogue,
  * one fp32 add before the single rounding.  SPMD_ERR_UNSUPPORTED when the
@@ -245,6 +251,12 @@ int spmd_moe_masks(spmd_tensor expert, spmd_tensor slot, spmd_tensor gate,
  * results are bit-identical to the reference). */
 int spmd_local_all_gather(spmd_tensor in, spmd_tensor out, int dim, const int32_t* groups,
                           int ngroups, int gsize, int64_t nparts, void* stream);
+/* The same all-gather of an f32 operand written as its tf32 hi / lo halves
+ * (hi = tf32(x), lo = x - hi): feeds spmd_dot_f32_presplit, which then skips
+ * its split pass.  SPMD_ERR_UNSUPPORTED for runs too short for the row kernel. */
+int spmd_local_all_gather_split(spmd_tensor in, spmd_tensor hi, spmd_tensor lo, int dim,
+                                const int32_t* groups, int ngroups, int gsize, int64_t nparts,
+                                void* stream);
 int spmd_local_all_reduce(spmd_tensor in, spmd_tensor out, int kind, const int32_t* groups,
                           int ngroups, int gsize, int64_t nparts, void* stream);
 int spmd_local_reduce_scatter(spmd_tensor in, spmd_tensor out, int dim, int kind,

@@ -189,6 +189,52 @@ __global__ void __launch_bounds__(256) local_rows_kernel(const T* __restrict__ i
   }
 }
 
+// The all-gather of an f32 3xTF32 GEMM operand written as its tf32 hi / lo
+// halves (split_tf32) instead of f32: the GEMM then skips its split pass
+// (one HBM read + write of the gathered operand less).
+__global__ void __launch_bounds__(256) local_rows_split_kernel(const float* __restrict__ in,
+                                                               float* __restrict__ hi,
+                                                               float* __restrict__ lo,
+                                                               RowMove r, GroupTab g,
+                                                               int64_t chunks) {
+  const int64_t per_row = r.L / 4;
+  const int64_t rows = (int64_t)g.P * r.G * r.outer;
+  for (int64_t b = blockIdx.x; b < rows * chunks; b += gridDim.x) {
+    const int64_t row = b / chunks, chunk = b - row * chunks;
+    const int p = (int)(row / (r.G * r.outer));
+    int64_t q = row - (int64_t)p * r.G * r.outer;
+    const int j = (int)(q / r.outer);
+    q -= (int64_t)j * r.outer;
+    int64_t so = 0, d0 = (int64_t)p * r.n_out + (int64_t)j * r.dst_j;
+    for (int k = r.outer_rank - 1; k >= 0; --k) {
+      const int64_t c = q % r.oshape[k];
+      q /= r.oshape[k];
+      so += c * r.sstr[k];
+      d0 += c * r.dstr[k];
+    }
+    const int src = g.members[g.gid[p] * g.gsize + j];
+    const float4* s4 = reinterpret_cast<const float4*>(in + (int64_t)src * r.n_in + so);
+    float4* h4 = reinterpret_cast<float4*>(hi + d0);
+    float4* l4 = reinterpret_cast<float4*>(lo + d0);
+    const int64_t v0 = chunk * (256 * ROW_U) + threadIdx.x;
+    float4 v[ROW_U];
+#pragma unroll
+    for (int u = 0; u < ROW_U; ++u)
+      if (v0 + u * 256 < per_row) v[u] = __ldcs(s4 + v0 + u * 256);
+#pragma unroll
+    for (int u = 0; u < ROW_U; ++u) {
+      if (v0 + u * 256 >= per_row) continue;
+      float4 h, l;
+      split_tf32(v[u].x, h.x, l.x);
+      split_tf32(v[u].y, h.y, l.y);
+      split_tf32(v[u].z, h.z, l.z);
+      split_tf32(v[u].w, h.w, l.w);
+      h4[v0 + u * 256] = h;
+      l4[v0 + u * 256] = l;
+    }
+  }
+}
+
 // Row form of the move described by `a`, or false when the runs are too
 // short / misaligned for it (the element kernel then runs).
 static bool row_move(const spmd_tensor& in, const spmd_tensor& out, const MoveArgs& a,
@@ -323,6 +369,38 @@ extern "C" int spmd_local_all_gather(spmd_tensor in, spmd_tensor out, int dim,
   a.dim = dim;
   SPMD_DISPATCH_BYTES(in.dtype, T, return launch_move<T>(in, out, a, g, as_stream(stream)));
   return SPMD_OK;
+}
+
+// spmd_local_all_gather of an f32 tensor written as tf32 hi / lo halves (each
+// with the gathered shape), for spmd_dot_f32_presplit.  SPMD_ERR_UNSUPPORTED
+// when the runs are too short for the row kernel.
+extern "C" int spmd_local_all_gather_split(spmd_tensor in, spmd_tensor hi, spmd_tensor lo,
+                                           int dim, const int32_t* groups, int ngroups,
+                                           int gsize, int64_t nparts, void* stream) {
+  SPMD_CHECK_ARG(in.dtype == SPMD_F32 && hi.dtype == SPMD_F32 && lo.dtype == SPMD_F32 &&
+                     dim >= 0 && dim < in.rank && numel(hi) == numel(lo),
+                 "all-gather split expects f32");
+  SPMD_CHECK_ARG(hi.dims[dim] == in.dims[dim] * gsize, "all-gather output shape mismatch");
+  GroupTab g;
+  int rc = make_groups(groups, ngroups, gsize, nparts, g);
+  if (rc) return rc;
+  MoveArgs a;
+  memset(&a, 0, sizeof(a));
+  a.kind = K_AG;
+  a.in = view_of(in);
+  a.out = view_of(hi);
+  a.dim = dim;
+  RowMove r;
+  if (!row_move(in, hi, a, gsize, r) ||
+      ((reinterpret_cast<uintptr_t>(hi.data) | reinterpret_cast<uintptr_t>(lo.data)) & 15))
+    return SPMD_ERR_UNSUPPORTED;
+  if (numel(hi) * nparts == 0) return SPMD_OK;
+  cudaStream_t s = as_stream(stream);
+  const int64_t chunks = (r.L / 4 + 256 * ROW_U - 1) / (256 * ROW_U);
+  const int64_t rows = (int64_t)g.P * r.G * r.outer;
+  local_rows_split_kernel<<<row_grid(rows, chunks), 256, 0, s>>>(
+      (const float*)in.data, (float*)hi.data, (float*)lo.data, r, g, chunks);
+  return launched(s);
 }
 
 extern "C" int spmd_local_all_to_all(spmd_tensor in, spmd_tensor out, int split_dim,

@@ -77,8 +77,11 @@ int dot_tcgen05(const spmd_tensor& lhs, const spmd_tensor& rhs, const spmd_tenso
                 const GemmScatter* sc = nullptr, const void* resid = nullptr);
 // Implemented in gemm_tf32x3.cu: large f32 Dots as a 3xTF32 tcgen05 GEMM;
 // SPMD_ERR_UNSUPPORTED for small / untileable ones (SIMT fp64 path then).
+// lhs_hi / lhs_lo: the lhs already split (K-major, the lhs's own dense
+// layout; spmd_local_all_gather_split) -- only the rhs is split here.
 int dot_tf32x3(const spmd_tensor& lhs, const spmd_tensor& rhs, const spmd_tensor& out,
-               const spmd_dot_dims& dd, int64_t nparts, cudaStream_t s);
+               const spmd_dot_dims& dd, int64_t nparts, cudaStream_t s,
+               const float* lhs_hi = nullptr, const float* lhs_lo = nullptr);
 
 #define SPMD_CHECK_ARG(cond, msg)                  \
   do {                                             \
@@ -265,6 +268,16 @@ struct CopyArgs {
   // signed int
   int relu;
 };
+
+// 3xTF32 operand split: hi = x rounded to tf32, lo = x - hi (exact in f32;
+// 0 for non-finite x), so hi + lo == x.  Shared by the GEMM's split passes
+// and the loopback all-gather that writes the split directly.
+__device__ __forceinline__ void split_tf32(float v, float& h, float& l) {
+  uint32_t u;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(u) : "f"(v));
+  h = __uint_as_float(u);
+  l = isfinite(v) ? v - h : 0.f;
+}
 
 template <typename T>
 __device__ __forceinline__ T relu_bits(T b, int mode) {

@@ -204,6 +204,21 @@ int conv_tcgen05(const spmd_tensor& lhs, const spmd_tensor& rhs, const spmd_tens
 
 using namespace spmd;
 
+// f32 Dot whose lhs arrives already split into tf32 hi / lo halves (both
+// with the lhs's shape; spmd_local_all_gather_split): the 3xTF32 GEMM skips
+// the lhs split pass.  SPMD_ERR_UNSUPPORTED when the 3xTF32 path does not
+// apply (the caller then forms lhs = hi + lo -- exact -- and runs spmd_dot).
+extern "C" int spmd_dot_f32_presplit(spmd_tensor lhs_hi, spmd_tensor lhs_lo, spmd_tensor rhs,
+                                     spmd_tensor out, const spmd_dot_dims* dd, int64_t nparts,
+                                     void* stream) {
+  SPMD_CHECK_ARG(lhs_hi.dtype == SPMD_F32 && lhs_lo.dtype == SPMD_F32 && rhs.dtype == SPMD_F32 &&
+                     out.dtype == SPMD_F32 && numel(lhs_hi) == numel(lhs_lo),
+                 "dot_f32_presplit expects f32 hi / lo of one shape");
+  if (numel(out) * nparts == 0) return SPMD_OK;
+  return dot_tf32x3(lhs_hi, rhs, out, *dd, nparts, as_stream(stream), (const float*)lhs_hi.data,
+                    (const float*)lhs_lo.data);
+}
+
 // out = Dot(lhs, rhs) + resid (bf16, the Dot's output shape): the residual
 // add of a Transformer layer folded into the GEMM epilogue (one fp32 add
 // before the single rounding).  SPMD_ERR_UNSUPPORTED when the GEMM does not

@@ -76,12 +76,7 @@ __device__ __forceinline__ void ttile_coords(const TShape& g, int64_t t, int& b,
   n = rr / gs;
 }
 
-__device__ __forceinline__ void split1(float v, float& h, float& l) {
-  uint32_t u;
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(u) : "f"(v));
-  h = __uint_as_float(u);
-  l = isfinite(v) ? v - h : 0.f;
-}
+__device__ __forceinline__ void split1(float v, float& h, float& l) { split_tf32(v, h, l); }
 
 // K-major operand: elementwise split, 16-byte vectors (scalar tail / when
 // misaligned).
@@ -592,14 +587,19 @@ static void keep_pool_memory() {
 // f32 Dot -> 3xTF32 tcgen05 GEMM; SPMD_ERR_UNSUPPORTED when the layout or the
 // size does not qualify (the caller then runs the SIMT fp64 kernel).
 int dot_tf32x3(const spmd_tensor& lhs, const spmd_tensor& rhs, const spmd_tensor& out,
-               const spmd_dot_dims& dd, int64_t nparts, cudaStream_t s) {
+               const spmd_dot_dims& dd, int64_t nparts, cudaStream_t s, const float* lhs_hi,
+               const float* lhs_lo) {
   if (lhs.dtype != SPMD_F32 || !option(OPT_F32_DOT_TC) || dd.epilogue != 0)
     return SPMD_ERR_UNSUPPORTED;
   GemmLayout lay;
   if (gemm_layout(lhs, rhs, out, dd, nparts, &lay) != SPMD_OK) return SPMD_ERR_UNSUPPORTED;
   // small Dots (the parity-sized golden cases) stay on the exact fp64 path
   if (lay.M < 256 || lay.N < 256 || lay.K < 64) return SPMD_ERR_UNSUPPORTED;
-  const int64_t na = numel(lhs) * nparts, nb = numel(rhs) * nparts;
+  const bool presplit = lhs_hi != nullptr;
+  if (presplit && (lay.a_mn || !lhs_lo || ((reinterpret_cast<uintptr_t>(lhs_hi) |
+                                            reinterpret_cast<uintptr_t>(lhs_lo)) & 15)))
+    return SPMD_ERR_UNSUPPORTED;
+  const int64_t na = presplit ? 0 : numel(lhs) * nparts, nb = numel(rhs) * nparts;
   // each of the four split copies starts 16-byte aligned (vector stores, TMA)
   const int64_t na4 = (na + 3) & ~(int64_t)3, nb4 = (nb + 3) & ~(int64_t)3;
   keep_pool_memory();
@@ -612,7 +612,13 @@ int dot_tf32x3(const spmd_tensor& lhs, const spmd_tensor& rhs, const spmd_tensor
   // (the view covers a sub-box of it), so the same scratch sizes hold
   float *ah = scratch, *al = scratch + na4, *bh = scratch + 2 * na4, *bl = bh + nb4;
   OperandView va = lay.va, vb = lay.vb;
-  int rc = split_operand((const float*)lhs.data, na, &va, lay.a_mn, ah, al, s);
+  int rc = SPMD_OK;
+  if (presplit) {
+    ah = const_cast<float*>(lhs_hi);
+    al = const_cast<float*>(lhs_lo);
+  } else {
+    rc = split_operand((const float*)lhs.data, na, &va, lay.a_mn, ah, al, s);
+  }
   if (rc == SPMD_OK) rc = split_operand((const float*)rhs.data, nb, &vb, lay.b_mn, bh, bl, s);
   if (rc != SPMD_OK) {
     cudaFreeAsync(scratch, s);

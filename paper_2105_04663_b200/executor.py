@@ -714,6 +714,17 @@ class Executor:
                 else:
                     self._fused_skip.add(ins.id)
                     self._fused[relu.id] = ("transpose_relu", ins)
+            # loopback all-gather -> f32 Dot (its lhs): the gather writes the
+            # operand's tf32 hi / lo halves, the 3xTF32 GEMM skips its split
+            if ins.opcode == Op.ALL_GATHER and self.comm is None and \
+                    ins.shape.dtype == DType.F32 and only_user(ins.id, Op.DOT) and \
+                    ins.id not in self._fused_skip and \
+                    os.environ.get("SPMD_AG_SPLIT", "1") != "0":
+                dot = by[users[ins.id][0]]
+                if dot.operands[0] == ins.id and dot.operands[1] != ins.id and \
+                        dot.id not in self._fused and dot.id not in self._fused_skip:
+                    self._fused_skip.add(ins.id)
+                    self._fused[dot.id] = ("ag_split_dot", ins, dot)
             # dot -> residual add: the add runs in the GEMM epilogue (fp32,
             # one rounding); falls back to dot + add if the wide GEMM does
             # not take it
@@ -1246,6 +1257,8 @@ class Executor:
             return tuple(f[1]) + (f[3],) + ((mask[2], mask[3]) if mask is not None else ())
         if f[0] in ("moe_dispatch", "moe_combine", "moe_dispatch_a2a"):
             return (f[1],)
+        if f[0] == "ag_split_dot":
+            return (f[1].operands[0], f[2].operands[1])
         if f[0] == "dot_add":
             return tuple(f[1].operands) + (f[2],)
         if f[0] == "halo_conv":
@@ -1295,6 +1308,37 @@ class Executor:
             def run(env, s):
                 out = self._alloc(shp)
                 C.check(fn(desc(env[a], ash), desc(env[b], bsh), desc(out, shp), P, s), f[0])
+                return out
+            return run
+        if f is not None and f[0] == "ag_split_dot":
+            ag, dot = f[1], f[2]
+            x, rhs = ag.operands[0], dot.operands[1]
+            xsh, gsh, rsh = self._shape(x), ag.shape, self._shape(rhs)
+            groups, ng, gs = _groups_arg(ag.attrs["subgroups"])
+            dim = ag.attrs["dim"]
+            dd = self._dot_dims(dot)
+            ref = ctypes.byref(dd)
+
+            def run(env, s):
+                hi, lo, out = self._alloc(gsh), self._alloc(gsh), self._alloc(shp)
+                rc = lib.spmd_local_all_gather_split(desc(env[x], xsh), desc(hi, gsh),
+                                                     desc(lo, gsh), dim, groups, ng, gs, P, s)
+                if rc == C.ERR_UNSUPPORTED:      # short runs: plain gather + Dot
+                    C.check(lib.spmd_local_all_gather(desc(env[x], xsh), desc(hi, gsh), dim,
+                                                      groups, ng, gs, P, s), "all-gather")
+                    C.check(lib.spmd_dot(desc(hi, gsh), desc(env[rhs], rsh), desc(out, shp),
+                                         ref, P, s), "dot")
+                    return out
+                C.check(rc, "all-gather split")
+                rc = lib.spmd_dot_f32_presplit(desc(hi, gsh), desc(lo, gsh), desc(env[rhs], rsh),
+                                               desc(out, shp), ref, P, s)
+                if rc == C.ERR_UNSUPPORTED:      # hi + lo == x exactly: the plain Dot
+                    C.check(lib.spmd_binary(_BINARY[Op.ADD], 0, desc(hi, gsh), desc(lo, gsh),
+                                            desc(hi, gsh), P, s), "add")
+                    C.check(lib.spmd_dot(desc(hi, gsh), desc(env[rhs], rsh), desc(out, shp),
+                                         ref, P, s), "dot")
+                else:
+                    C.check(rc, "dot_f32_presplit")
                 return out
             return run
         if f is not None and f[0] == "dot_add":
