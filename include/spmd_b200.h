@@ -159,10 +159,14 @@ typedef struct {
 } spmd_dot_dims;
 int spmd_dot(spmd_tensor lhs, spmd_tensor rhs, spmd_tensor out, const spmd_dot_dims* dd,
              int64_t nparts, void* stream);
-/* f32 Dot whose lhs comes as tf32 hi / lo halves (spmd_local_all_gather_split):
- * the 3xTF32 GEMM without the lhs split pass; SPMD_ERR_UNSUPPORTED when the
- * 3xTF32 path does not apply (lhs = hi + lo exactly; run spmd_dot). */
-int spmd_dot_f32_presplit(spmd_tensor lhs_hi, spmd_tensor lhs_lo, spmd_tensor rhs,
+/* f32 Dot with operands given as their tf32 hi / lo halves
+ * (spmd_local_all_gather_split / _split_t; hi.data NULL = not pre-split, then
+ * the operand tensor's data is split here): the 3xTF32 GEMM without those
+ * split passes.  A pre-split MN-major rhs is in the K-major [batch][N][K]
+ * layout.  SPMD_ERR_UNSUPPORTED when the 3xTF32 path does not apply (operand =
+ * hi + lo exactly; run spmd_dot). */
+int spmd_dot_f32_presplit(spmd_tensor lhs, spmd_tensor lhs_hi, spmd_tensor lhs_lo,
+                          spmd_tensor rhs, spmd_tensor rhs_hi, spmd_tensor rhs_lo,
                           spmd_tensor out, const spmd_dot_dims* dd, int64_t nparts,
                           void* stream);
 /* out = Dot(lhs, rhs) + resid (bf16; resid has the output's shape): the
@@ -257,6 +261,13 @@ int spmd_local_all_gather(spmd_tensor in, spmd_tensor out, int dim, const int32_
 int spmd_local_all_gather_split(spmd_tensor in, spmd_tensor hi, spmd_tensor lo, int dim,
                                 const int32_t* groups, int ngroups, int gsize, int64_t nparts,
                                 void* stream);
+/* All-gather along dim 0 of an f32 [K_local, N] operand written as the tf32
+ * hi / lo halves of its K-major transpose [N, gsize * K_local] (the layout
+ * spmd_dot_f32_presplit takes for an MN-major rhs).  SPMD_ERR_UNSUPPORTED
+ * unless K_local % 64 == 0 and N % 4 == 0. */
+int spmd_local_all_gather_split_t(spmd_tensor in, spmd_tensor hi, spmd_tensor lo,
+                                  const int32_t* groups, int ngroups, int gsize, int64_t nparts,
+                                  void* stream);
 int spmd_local_all_reduce(spmd_tensor in, spmd_tensor out, int kind, const int32_t* groups,
                           int ngroups, int gsize, int64_t nparts, void* stream);
 int spmd_local_reduce_scatter(spmd_tensor in, spmd_tensor out, int dim, int kind,

@@ -105,7 +105,9 @@ _SIGNATURES = {
     "spmd_moe_masks": ([_T, _T, _T, _T, _T, _I64, _P], _I),
     "spmd_local_all_gather": ([_T, _T, _I, _PI32, _I, _I, _I64, _P], _I),
     "spmd_local_all_gather_split": ([_T, _T, _T, _I, _PI32, _I, _I, _I64, _P], _I),
-    "spmd_dot_f32_presplit": ([_T, _T, _T, _T, ctypes.POINTER(SpmdDotDims), _I64, _P], _I),
+    "spmd_local_all_gather_split_t": ([_T, _T, _T, _PI32, _I, _I, _I64, _P], _I),
+    "spmd_dot_f32_presplit": ([_T, _T, _T, _T, _T, _T, _T, ctypes.POINTER(SpmdDotDims), _I64,
+                               _P], _I),
     "spmd_local_all_reduce": ([_T, _T, _I, _PI32, _I, _I, _I64, _P], _I),
     "spmd_local_reduce_scatter": ([_T, _T, _I, _I, _PI32, _I, _I, _I64, _P], _I),
     "spmd_local_all_to_all": ([_T, _T, _I, _I, _PI32, _I, _I, _I64, _P], _I),

@@ -81,7 +81,8 @@ int dot_tcgen05(const spmd_tensor& lhs, const spmd_tensor& rhs, const spmd_tenso
 // layout; spmd_local_all_gather_split) -- only the rhs is split here.
 int dot_tf32x3(const spmd_tensor& lhs, const spmd_tensor& rhs, const spmd_tensor& out,
                const spmd_dot_dims& dd, int64_t nparts, cudaStream_t s,
-               const float* lhs_hi = nullptr, const float* lhs_lo = nullptr);
+               const float* lhs_hi = nullptr, const float* lhs_lo = nullptr,
+               const float* rhs_hi = nullptr, const float* rhs_lo = nullptr);
 
 #define SPMD_CHECK_ARG(cond, msg)                  \
   do {                                             \

@@ -204,19 +204,23 @@ int conv_tcgen05(const spmd_tensor& lhs, const spmd_tensor& rhs, const spmd_tens
 
 using namespace spmd;
 
-// f32 Dot whose lhs arrives already split into tf32 hi / lo halves (both
-// with the lhs's shape; spmd_local_all_gather_split): the 3xTF32 GEMM skips
-// the lhs split pass.  SPMD_ERR_UNSUPPORTED when the 3xTF32 path does not
-// apply (the caller then forms lhs = hi + lo -- exact -- and runs spmd_dot).
-extern "C" int spmd_dot_f32_presplit(spmd_tensor lhs_hi, spmd_tensor lhs_lo, spmd_tensor rhs,
+// f32 Dot with operands that arrive already split into their tf32 hi / lo
+// halves (spmd_local_all_gather_split / _split_t): `lhs` / `rhs` give the
+// shapes (their data is read only when that operand is not pre-split, i.e.
+// its hi.data is NULL); a pre-split lhs is in its own (K-major) layout, a
+// pre-split MN-major rhs in the dense K-major [batch][N][K] transpose.
+// SPMD_ERR_UNSUPPORTED when the 3xTF32 path does not apply (the caller then
+// forms the operands as hi + lo -- exact -- and runs spmd_dot).
+extern "C" int spmd_dot_f32_presplit(spmd_tensor lhs, spmd_tensor lhs_hi, spmd_tensor lhs_lo,
+                                     spmd_tensor rhs, spmd_tensor rhs_hi, spmd_tensor rhs_lo,
                                      spmd_tensor out, const spmd_dot_dims* dd, int64_t nparts,
                                      void* stream) {
-  SPMD_CHECK_ARG(lhs_hi.dtype == SPMD_F32 && lhs_lo.dtype == SPMD_F32 && rhs.dtype == SPMD_F32 &&
-                     out.dtype == SPMD_F32 && numel(lhs_hi) == numel(lhs_lo),
-                 "dot_f32_presplit expects f32 hi / lo of one shape");
+  SPMD_CHECK_ARG(lhs.dtype == SPMD_F32 && rhs.dtype == SPMD_F32 && out.dtype == SPMD_F32,
+                 "dot_f32_presplit expects f32");
   if (numel(out) * nparts == 0) return SPMD_OK;
-  return dot_tf32x3(lhs_hi, rhs, out, *dd, nparts, as_stream(stream), (const float*)lhs_hi.data,
-                    (const float*)lhs_lo.data);
+  return dot_tf32x3(lhs, rhs, out, *dd, nparts, as_stream(stream), (const float*)lhs_hi.data,
+                    (const float*)lhs_lo.data, (const float*)rhs_hi.data,
+                    (const float*)rhs_lo.data);
 }
 
 // out = Dot(lhs, rhs) + resid (bf16, the Dot's output shape): the residual

@@ -180,9 +180,73 @@ __global__ void __launch_bounds__(256) split_tf32_transpose_kernel(const float* 
   }
 }
 
+// Loopback all-gather along K of an MN-major [K_local][MN] operand fused with
+// its 3xTF32 split and transpose: partition p's output is the K-major hi / lo
+// [MN][gs * K_local] with K rows [j * K_local, (j + 1) * K_local) taken from
+// group member j's shard.  64 x 64 tiles as split_tf32_transpose_kernel.
+struct GatherK {
+  int64_t k_local, mn;
+  int gs;
+  int8_t src[SPMD_MAX_PARTS][8];   // [p][j]: partition holding K block j of p's gather
+};
+
+__global__ void __launch_bounds__(256) gather_split_transpose_kernel(const float* __restrict__ x,
+                                                                    GatherK g,
+                                                                    float* __restrict__ hi,
+                                                                    float* __restrict__ lo) {
+  __shared__ float tile[64][65];
+  const int p = blockIdx.z;
+  const int64_t K = g.k_local * g.gs;
+  const int64_t mn0 = (int64_t)blockIdx.x * 64, k0 = (int64_t)blockIdx.y * 64;
+  const int j = (int)(k0 / g.k_local);          // k_local % 64 == 0: one member per tile
+  const float* src = x + (int64_t)g.src[p][j] * g.k_local * g.mn + (k0 - j * g.k_local) * g.mn;
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int kk = ty + 16 * i;
+    const int64_t mn = mn0 + 4 * tx;
+    float4 f = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (mn + 3 < g.mn) f = __ldcs(reinterpret_cast<const float4*>(src + kk * g.mn + mn));
+    tile[kk][4 * tx] = f.x;
+    tile[kk][4 * tx + 1] = f.y;
+    tile[kk][4 * tx + 2] = f.z;
+    tile[kk][4 * tx + 3] = f.w;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int mm = ty + 16 * i;
+    const int64_t mn = mn0 + mm, k = k0 + 4 * tx;
+    if (mn >= g.mn) continue;
+    float4 h, l;
+    split_tf32(tile[4 * tx][mm], h.x, l.x);
+    split_tf32(tile[4 * tx + 1][mm], h.y, l.y);
+    split_tf32(tile[4 * tx + 2][mm], h.z, l.z);
+    split_tf32(tile[4 * tx + 3][mm], h.w, l.w);
+    const int64_t o = ((int64_t)p * g.mn + mn) * K + k;
+    *reinterpret_cast<float4*>(hi + o) = h;
+    *reinterpret_cast<float4*>(lo + o) = l;
+  }
+}
+
 // Split one operand into hi / lo K-major copies at `hi`, `lo` (each sized for
 // the operand's own layout when it is K-major, else dense [batch][MN][K]) and
 // rewrite `view` to describe them.
+// The dense K-major view [b2][b1][b0][MN][K] an MN-major operand is split
+// into (split_tf32_transpose_kernel's output layout).
+static OperandView kmajor_view(const OperandView& mnv) {
+  OperandView kv;
+  kv.size[0] = mnv.size[1], kv.stride[0] = 1;
+  kv.size[1] = mnv.size[0], kv.stride[1] = mnv.size[1];
+  int64_t st = mnv.size[0] * mnv.size[1];
+  for (int i = 0; i < 3; ++i) {
+    kv.size[2 + i] = mnv.size[2 + i];
+    kv.stride[2 + i] = mnv.size[2 + i] > 1 ? st : 8;
+    st *= mnv.size[2 + i];
+  }
+  return kv;
+}
+
 static int split_operand(const float* src, int64_t n, OperandView* view, int mn_major, float* hi,
                          float* lo, cudaStream_t s) {
   if (!mn_major) {
@@ -202,16 +266,7 @@ static int split_operand(const float* src, int64_t n, OperandView* view, int mn_
   if (nb > 65535) return SPMD_ERR_UNSUPPORTED;
   dim3 grid((unsigned)((v.mn + 63) / 64), (unsigned)((v.k + 63) / 64), (unsigned)nb);
   split_tf32_transpose_kernel<<<grid, 256, 0, s>>>(src, v, hi, lo);
-  // K-major dense view [b2][b1][b0][MN][K]
-  OperandView kv;
-  kv.size[0] = v.k, kv.stride[0] = 1;
-  kv.size[1] = v.mn, kv.stride[1] = v.k;
-  int64_t st = v.mn * v.k;
-  for (int i = 0; i < 3; ++i) {
-    kv.size[2 + i] = v.bsize[i];
-    kv.stride[2 + i] = v.bsize[i] > 1 ? st : 8;
-    st *= v.bsize[i];
-  }
+  OperandView kv = kmajor_view(*view);
   *view = kv;
   return launched(s);
 }
@@ -588,7 +643,7 @@ static void keep_pool_memory() {
 // size does not qualify (the caller then runs the SIMT fp64 kernel).
 int dot_tf32x3(const spmd_tensor& lhs, const spmd_tensor& rhs, const spmd_tensor& out,
                const spmd_dot_dims& dd, int64_t nparts, cudaStream_t s, const float* lhs_hi,
-               const float* lhs_lo) {
+               const float* lhs_lo, const float* rhs_hi, const float* rhs_lo) {
   if (lhs.dtype != SPMD_F32 || !option(OPT_F32_DOT_TC) || dd.epilogue != 0)
     return SPMD_ERR_UNSUPPORTED;
   GemmLayout lay;
@@ -599,7 +654,12 @@ int dot_tf32x3(const spmd_tensor& lhs, const spmd_tensor& rhs, const spmd_tensor
   if (presplit && (lay.a_mn || !lhs_lo || ((reinterpret_cast<uintptr_t>(lhs_hi) |
                                             reinterpret_cast<uintptr_t>(lhs_lo)) & 15)))
     return SPMD_ERR_UNSUPPORTED;
-  const int64_t na = presplit ? 0 : numel(lhs) * nparts, nb = numel(rhs) * nparts;
+  const bool presplit_b = rhs_hi != nullptr;
+  if (presplit_b && (!rhs_lo || ((reinterpret_cast<uintptr_t>(rhs_hi) |
+                                  reinterpret_cast<uintptr_t>(rhs_lo)) & 15)))
+    return SPMD_ERR_UNSUPPORTED;
+  const int64_t na = presplit ? 0 : numel(lhs) * nparts;
+  const int64_t nb = presplit_b ? 0 : numel(rhs) * nparts;
   // each of the four split copies starts 16-byte aligned (vector stores, TMA)
   const int64_t na4 = (na + 3) & ~(int64_t)3, nb4 = (nb + 3) & ~(int64_t)3;
   keep_pool_memory();
@@ -619,7 +679,15 @@ int dot_tf32x3(const spmd_tensor& lhs, const spmd_tensor& rhs, const spmd_tensor
   } else {
     rc = split_operand((const float*)lhs.data, na, &va, lay.a_mn, ah, al, s);
   }
-  if (rc == SPMD_OK) rc = split_operand((const float*)rhs.data, nb, &vb, lay.b_mn, bh, bl, s);
+  if (rc == SPMD_OK && presplit_b) {
+    // the K-major halves split_operand would have written (MN-major rhs:
+    // dense [batch][N][K]; K-major rhs: its own layout)
+    bh = const_cast<float*>(rhs_hi);
+    bl = const_cast<float*>(rhs_lo);
+    if (lay.b_mn) vb = kmajor_view(vb);
+  } else if (rc == SPMD_OK) {
+    rc = split_operand((const float*)rhs.data, nb, &vb, lay.b_mn, bh, bl, s);
+  }
   if (rc != SPMD_OK) {
     cudaFreeAsync(scratch, s);
     return rc;
@@ -681,3 +749,43 @@ int dot_tf32x3(const spmd_tensor& lhs, const spmd_tensor& rhs, const spmd_tensor
 }
 
 }  // namespace spmd
+
+using namespace spmd;
+
+// Loopback all-gather along dim 0 of an f32 [K_local, N] operand (per
+// partition) written as the tf32 hi / lo halves of its K-major transpose
+// [N, K] -- the rhs layout spmd_dot_f32_presplit takes for an MN-major rhs.
+// SPMD_ERR_UNSUPPORTED unless K_local % 64 == 0 and N % 4 == 0.
+extern "C" int spmd_local_all_gather_split_t(spmd_tensor in, spmd_tensor hi, spmd_tensor lo,
+                                             const int32_t* groups, int ngroups, int gsize,
+                                             int64_t nparts, void* stream) {
+  SPMD_CHECK_ARG(in.dtype == SPMD_F32 && hi.dtype == SPMD_F32 && lo.dtype == SPMD_F32 &&
+                     in.rank == 2 && hi.rank == 2 && lo.rank == 2,
+                 "all-gather split-transpose expects f32 [K_local, N] -> [N, K]");
+  const int64_t kl = in.dims[0], N = in.dims[1];
+  SPMD_CHECK_ARG(hi.dims[0] == N && hi.dims[1] == kl * gsize && lo.dims[0] == N &&
+                     lo.dims[1] == kl * gsize,
+                 "all-gather split-transpose output shape");
+  if (kl % 64 || N % 4 || gsize > 8 || nparts > SPMD_MAX_PARTS || nparts > 65535 ||
+      ngroups * gsize != nparts ||
+      ((reinterpret_cast<uintptr_t>(in.data) | reinterpret_cast<uintptr_t>(hi.data) |
+        reinterpret_cast<uintptr_t>(lo.data)) & 15))
+    return SPMD_ERR_UNSUPPORTED;
+  GatherK g;
+  memset(&g, -1, sizeof(g));
+  g.k_local = kl;
+  g.mn = N;
+  g.gs = gsize;
+  for (int i = 0; i < ngroups * gsize; ++i) {
+    const int d = groups[i];
+    SPMD_CHECK_ARG(d >= 0 && d < nparts, "subgroups do not partition the devices");
+    const int grp = i / gsize;
+    for (int j = 0; j < gsize; ++j) g.src[d][j] = (int8_t)groups[grp * gsize + j];
+  }
+  if (numel(hi) * nparts == 0) return SPMD_OK;
+  cudaStream_t s = as_stream(stream);
+  dim3 grid((unsigned)((N + 63) / 64), (unsigned)(kl * gsize / 64), (unsigned)nparts);
+  gather_split_transpose_kernel<<<grid, 256, 0, s>>>((const float*)in.data, g, (float*)hi.data,
+                                                     (float*)lo.data);
+  return launched(s);
+}

@@ -714,17 +714,29 @@ class Executor:
                 else:
                     self._fused_skip.add(ins.id)
                     self._fused[relu.id] = ("transpose_relu", ins)
-            # loopback all-gather -> f32 Dot (its lhs): the gather writes the
-            # operand's tf32 hi / lo halves, the 3xTF32 GEMM skips its split
-            if ins.opcode == Op.ALL_GATHER and self.comm is None and \
-                    ins.shape.dtype == DType.F32 and only_user(ins.id, Op.DOT) and \
-                    ins.id not in self._fused_skip and \
+            # loopback all-gathers -> f32 Dot: a gathered lhs (K-major) comes
+            # as tf32 hi / lo halves, a gathered 2-D rhs [K, N] (along K) as the
+            # halves of its K-major transpose; the 3xTF32 GEMM skips those
+            # split passes
+            if ins.opcode == Op.DOT and self.comm is None and ins.shape.dtype == DType.F32 and \
+                    ins.id not in self._fused and ins.id not in self._fused_skip and \
+                    ins.operands[0] != ins.operands[1] and \
                     os.environ.get("SPMD_AG_SPLIT", "1") != "0":
-                dot = by[users[ins.id][0]]
-                if dot.operands[0] == ins.id and dot.operands[1] != ins.id and \
-                        dot.id not in self._fused and dot.id not in self._fused_skip:
-                    self._fused_skip.add(ins.id)
-                    self._fused[dot.id] = ("ag_split_dot", ins, dot)
+                def gathered(vid):
+                    a = by[vid]
+                    return a if a.opcode == Op.ALL_GATHER and a.shape.dtype == DType.F32 and \
+                        only_user(vid, Op.DOT) and vid not in self._fused_skip else None
+                lag, rag = gathered(ins.operands[0]), gathered(ins.operands[1])
+                at = ins.attrs
+                if rag is not None and not (rag.shape.rank == 2 and rag.attrs["dim"] == 0 and
+                                            not at["rhs_batch"] and
+                                            tuple(at["rhs_contracting"]) == (0,)):
+                    rag = None
+                if lag is not None or rag is not None:
+                    for a in (lag, rag):
+                        if a is not None:
+                            self._fused_skip.add(a.id)
+                    self._fused[ins.id] = ("ag_split_dot", lag, rag, ins)
             # dot -> residual add: the add runs in the GEMM epilogue (fp32,
             # one rounding); falls back to dot + add if the wide GEMM does
             # not take it
@@ -1258,7 +1270,9 @@ class Executor:
         if f[0] in ("moe_dispatch", "moe_combine", "moe_dispatch_a2a"):
             return (f[1],)
         if f[0] == "ag_split_dot":
-            return (f[1].operands[0], f[2].operands[1])
+            lag, rag, dot = f[1], f[2], f[3]
+            return (lag.operands[0] if lag is not None else dot.operands[0],
+                    rag.operands[0] if rag is not None else dot.operands[1])
         if f[0] == "dot_add":
             return tuple(f[1].operands) + (f[2],)
         if f[0] == "halo_conv":
@@ -1311,36 +1325,7 @@ class Executor:
                 return out
             return run
         if f is not None and f[0] == "ag_split_dot":
-            ag, dot = f[1], f[2]
-            x, rhs = ag.operands[0], dot.operands[1]
-            xsh, gsh, rsh = self._shape(x), ag.shape, self._shape(rhs)
-            groups, ng, gs = _groups_arg(ag.attrs["subgroups"])
-            dim = ag.attrs["dim"]
-            dd = self._dot_dims(dot)
-            ref = ctypes.byref(dd)
-
-            def run(env, s):
-                hi, lo, out = self._alloc(gsh), self._alloc(gsh), self._alloc(shp)
-                rc = lib.spmd_local_all_gather_split(desc(env[x], xsh), desc(hi, gsh),
-                                                     desc(lo, gsh), dim, groups, ng, gs, P, s)
-                if rc == C.ERR_UNSUPPORTED:      # short runs: plain gather + Dot
-                    C.check(lib.spmd_local_all_gather(desc(env[x], xsh), desc(hi, gsh), dim,
-                                                      groups, ng, gs, P, s), "all-gather")
-                    C.check(lib.spmd_dot(desc(hi, gsh), desc(env[rhs], rsh), desc(out, shp),
-                                         ref, P, s), "dot")
-                    return out
-                C.check(rc, "all-gather split")
-                rc = lib.spmd_dot_f32_presplit(desc(hi, gsh), desc(lo, gsh), desc(env[rhs], rsh),
-                                               desc(out, shp), ref, P, s)
-                if rc == C.ERR_UNSUPPORTED:      # hi + lo == x exactly: the plain Dot
-                    C.check(lib.spmd_binary(_BINARY[Op.ADD], 0, desc(hi, gsh), desc(lo, gsh),
-                                            desc(hi, gsh), P, s), "add")
-                    C.check(lib.spmd_dot(desc(hi, gsh), desc(env[rhs], rsh), desc(out, shp),
-                                         ref, P, s), "dot")
-                else:
-                    C.check(rc, "dot_f32_presplit")
-                return out
-            return run
+            return self._ag_split_dot_step(f[1], f[2], f[3], shp)
         if f is not None and f[0] == "dot_add":
             dot, res = f[1], f[2]
             a, b = dot.operands
@@ -1674,6 +1659,92 @@ class Executor:
             out = self._alloc(shp)
             C.check(lib.spmd_dot(desc(env[a], ash), desc(env[b], bsh), desc(out, shp), ref, P, s),
                     "dot")
+            return out
+        return run
+
+    def _ag_split_dot_step(self, lag, rag, dot, shp):
+        """Loopback all-gather(s) -> f32 Dot (_plan_fusions): the gathers write
+        the operands' tf32 hi / lo halves (spmd_local_all_gather_split /
+        _split_t) and spmd_dot_f32_presplit skips those splits.  Any step
+        that does not apply falls back to the plain gather / Dot (hi + lo is
+        the gathered value exactly)."""
+        lib, P = self.lib, self.P
+        dd = self._dot_dims(dot)
+        ref = ctypes.byref(dd)
+        ash, bsh = self._shape(dot.operands[0]), self._shape(dot.operands[1])
+        a_src = lag.operands[0] if lag is not None else dot.operands[0]
+        b_src = rag.operands[0] if rag is not None else dot.operands[1]
+        a_ssh, b_ssh = self._shape(a_src), self._shape(b_src)
+        ga = _groups_arg(lag.attrs["subgroups"]) if lag is not None else None
+        gb = _groups_arg(rag.attrs["subgroups"]) if rag is not None else None
+        bt = Shape((bsh.dims[1], bsh.dims[0]), DType.F32) if rag is not None else None
+        t10 = C.i32_array((1, 0))
+
+        def gather(ag, gr, src, ssh, osh, env, s):
+            out = self._alloc(osh)
+            C.check(lib.spmd_local_all_gather(desc(env[src], ssh), desc(out, osh),
+                                              ag.attrs["dim"], gr[0], gr[1], gr[2], P, s),
+                    "all-gather")
+            return out
+
+        def shape_only(sh):
+            t = C.SpmdTensor()
+            t.dtype, t.rank = C.DTYPE_CODE[DType.F32], sh.rank
+            for i, d in enumerate(sh.dims):
+                t.dims[i] = d
+            return t
+
+        def run(env, s):
+            out = self._alloc(shp)
+            a_full = b_full = None
+            a_hl = b_hl = (C.SpmdTensor(), C.SpmdTensor())
+            # (the four halves stay referenced until the Dot is enqueued)
+            ahi = alo = bhi = blo = None
+            if lag is not None:
+                ahi, alo = self._alloc(ash), self._alloc(ash)
+                rc = lib.spmd_local_all_gather_split(desc(env[a_src], a_ssh), desc(ahi, ash),
+                                                     desc(alo, ash), lag.attrs["dim"], ga[0],
+                                                     ga[1], ga[2], P, s)
+                if rc == C.ERR_UNSUPPORTED:
+                    a_full = gather(lag, ga, a_src, a_ssh, ash, env, s)
+                else:
+                    C.check(rc, "all-gather split")
+                    a_hl = (desc(ahi, ash), desc(alo, ash))
+            else:
+                a_full = env[a_src]
+            if rag is not None:
+                bhi, blo = self._alloc(bt), self._alloc(bt)
+                rc = lib.spmd_local_all_gather_split_t(desc(env[b_src], b_ssh), desc(bhi, bt),
+                                                       desc(blo, bt), gb[0], gb[1], gb[2], P, s)
+                if rc == C.ERR_UNSUPPORTED:
+                    b_full = gather(rag, gb, b_src, b_ssh, bsh, env, s)
+                else:
+                    C.check(rc, "all-gather split-transpose")
+                    b_hl = (desc(bhi, bt), desc(blo, bt))
+            else:
+                b_full = env[b_src]
+            a_d = desc(a_full, ash) if a_full is not None else shape_only(ash)
+            b_d = desc(b_full, bsh) if b_full is not None else shape_only(bsh)
+            rc = lib.spmd_dot_f32_presplit(a_d, a_hl[0], a_hl[1], b_d, b_hl[0], b_hl[1],
+                                           desc(out, shp), ref, P, s)
+            if rc == C.ERR_UNSUPPORTED:
+                # rebuild the gathered operands exactly (hi + lo; the rhs
+                # halves are transposed) and run the plain Dot
+                if a_full is None:
+                    a_full = self._alloc(ash)
+                    C.check(lib.spmd_binary(_BINARY[Op.ADD], 0, a_hl[0], a_hl[1],
+                                            desc(a_full, ash), P, s), "add")
+                if b_full is None:
+                    t = self._alloc(bt)
+                    C.check(lib.spmd_binary(_BINARY[Op.ADD], 0, b_hl[0], b_hl[1], desc(t, bt),
+                                            P, s), "add")
+                    b_full = self._alloc(bsh)
+                    C.check(lib.spmd_transpose(desc(t, bt), desc(b_full, bsh), t10, P, s),
+                            "transpose")
+                C.check(lib.spmd_dot(desc(a_full, ash), desc(b_full, bsh), desc(out, shp), ref,
+                                     P, s), "dot")
+            else:
+                C.check(rc, "dot_f32_presplit")
             return out
         return run
 

@@ -115,3 +115,43 @@ def test_local_all_reduce_bf16_max_exact():
     from paper_2105_04663_b200.ir import DType, Op, ReduceKind
     _run(Op.ALL_REDUCE, {"kind": ReduceKind.MAX, "subgroups": GROUPS4[0]},
          _inputs((2, 8192), DType.BF16), (2, 8192), DType.BF16)
+
+
+@pytest.mark.parametrize("groups", [((0, 1), (2, 3)), ((0, 2), (1, 3))])
+def test_local_all_gather_split_halves(groups):
+    """spmd_local_all_gather_split / _split_t: hi + lo == the gathered value
+    exactly, hi is the tf32 rounding of it; _split_t writes the K-major
+    transpose."""
+    import torch
+    from paper_2105_04663_b200 import _capi as C
+    from paper_2105_04663_b200.executor import desc
+    from paper_2105_04663_b200.ir import DType, Shape
+    P, f32 = 4, DType.F32
+    g = torch.Generator(device="cuda").manual_seed(9)
+    flat = [d for grp in groups for d in grp]
+    st = torch.cuda.current_stream().cuda_stream
+    # lhs: [2, 3, 2048] per partition gathered along the last dim
+    x = torch.randn((P, 2, 3, 2048), generator=g, device="cuda")
+    hi = torch.empty((P, 2, 3, 4096), device="cuda")
+    lo = torch.empty_like(hi)
+    C.check(C.lib().spmd_local_all_gather_split(desc(x, Shape((2, 3, 2048), f32)),
+                                                desc(hi, Shape((2, 3, 4096), f32)),
+                                                desc(lo, Shape((2, 3, 4096), f32)), 2,
+                                                C.i32_array(flat), len(groups), 2, P, st), "split")
+    # rhs: [K_local=128, N=96] per partition gathered along K, K-major transpose out
+    w = torch.randn((P, 128, 96), generator=g, device="cuda")
+    thi = torch.empty((P, 96, 256), device="cuda")
+    tlo = torch.empty_like(thi)
+    C.check(C.lib().spmd_local_all_gather_split_t(desc(w, Shape((128, 96), f32)),
+                                                  desc(thi, Shape((96, 256), f32)),
+                                                  desc(tlo, Shape((96, 256), f32)),
+                                                  C.i32_array(flat), len(groups), 2, P, st),
+            "split_t")
+    torch.cuda.synchronize()
+    for p in range(P):
+        grp = next(gr for gr in groups if p in gr)
+        full = torch.cat([x[m] for m in grp], dim=-1)
+        assert torch.equal(hi[p] + lo[p], full)
+        assert torch.equal(hi[p], (hi[p].view(torch.int32) & ~0x1FFF).view(torch.float32))
+        wfull = torch.cat([w[m] for m in grp], dim=0).t()
+        assert torch.equal(thi[p] + tlo[p], wfull)
