@@ -341,6 +341,13 @@ int64_t spmd_comm_fused_half(spmd_comm* comm);
 int spmd_dot_reduce_scatter(spmd_comm* comm, spmd_tensor lhs, spmd_tensor rhs, spmd_tensor out,
                             const spmd_dot_dims* dims, int dim, const int32_t* groups,
                             int ngroups, int gsize, void* stream);
+/* ... with the layer's residual Add (simulator.py:173-198) folded into the
+ * reduce: out = reduce_scatter(dot(lhs, rhs)) + resid, rounded as the unfused
+ * pair (bit-identical to spmd_dot_reduce_scatter followed by the Add). */
+int spmd_dot_reduce_scatter_add(spmd_comm* comm, spmd_tensor lhs, spmd_tensor rhs,
+                                spmd_tensor resid, spmd_tensor out, const spmd_dot_dims* dims,
+                                int dim, const int32_t* groups, int ngroups, int gsize,
+                                void* stream);
 /* out = all-to-all(split 1, concat 0)(dot(lhs, rhs)) for a dot with one
  * batch dim (output dim 0): the expert FFN-out einsum + GShard combine
  * all-to-all (C3).  The GEMM epilogue stores each output row chunk into the

@@ -128,6 +128,8 @@ _SIGNATURES = {
     "spmd_comm_fused_half": ([_P], _I64),
     "spmd_dot_reduce_scatter": ([_P, _T, _T, _T, ctypes.POINTER(SpmdDotDims), _I, _PI32, _I, _I,
                                  _P], _I),
+    "spmd_dot_reduce_scatter_add": ([_P, _T, _T, _T, _T, ctypes.POINTER(SpmdDotDims), _I, _PI32,
+                                     _I, _I, _P], _I),
     "spmd_dot_all_to_all": ([_P, _T, _T, _T, ctypes.POINTER(SpmdDotDims), _I, _I, _PI32, _I, _I,
                              _P], _I),
     "spmd_moe_dispatch_all_to_all": ([_P, _T, _T, _T, _T, _T, _PI32, _I, _I, _P], _I),

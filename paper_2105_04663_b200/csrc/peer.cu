@@ -85,7 +85,8 @@ __global__ void peer_barrier_kernel(uint32_t* ctrl, PeerFlags pf, int nranks, in
 // out[i] = sum_j slot_j[i] (fp32 accumulation in group-position order).
 __global__ void peer_slot_reduce_kernel(const bf16* __restrict__ data, bf16* __restrict__ out,
                                         const uint32_t* ctrl, int G, int64_t slot,
-                                        int64_t par_slots, int64_t nvec) {
+                                        int64_t par_slots, int64_t nvec,
+                                        const bf16* __restrict__ resid) {
   const int64_t par = (int64_t)(*(volatile const uint32_t*)ctrl & 1);
   const bf16* base = data + par * par_slots * slot;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nvec;
@@ -105,6 +106,17 @@ __global__ void peer_slot_reduce_kernel(const bf16* __restrict__ data, bf16* __r
     __nv_bfloat162* oh = reinterpret_cast<__nv_bfloat162*>(&o);
 #pragma unroll
     for (int q = 0; q < 4; ++q) oh[q] = __floats2bfloat162_rn(acc[2 * q], acc[2 * q + 1]);
+    if (resid) {
+      // the layer's residual Add, with the unfused path's roundings (the
+      // reduce-scatter result in bf16, then the Add in f32 and one rounding)
+      const uint4 rw = __ldcs(reinterpret_cast<const uint4*>(resid) + i);
+      const __nv_bfloat162* rh = reinterpret_cast<const __nv_bfloat162*>(&rw);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const float2 a = __bfloat1622float2(oh[q]), b = __bfloat1622float2(rh[q]);
+        oh[q] = __floats2bfloat162_rn(a.x + b.x, a.y + b.y);
+      }
+    }
     reinterpret_cast<uint4*>(out)[i] = o;
   }
 }
@@ -266,10 +278,10 @@ extern "C" int spmd_comm_reserve_fused(spmd_comm* c, int64_t half_bytes) {
 
 extern "C" int64_t spmd_comm_fused_half(spmd_comm* c) { return c ? c->fused_half : 0; }
 
-extern "C" int spmd_dot_reduce_scatter(spmd_comm* c, spmd_tensor lhs, spmd_tensor rhs,
-                                       spmd_tensor out, const spmd_dot_dims* dd, int dim,
-                                       const int32_t* groups, int ngroups, int gsize,
-                                       void* stream) {
+static int dot_reduce_scatter(spmd_comm* c, spmd_tensor lhs, spmd_tensor rhs,
+                              const bf16* resid, spmd_tensor out, const spmd_dot_dims* dd,
+                              int dim, const int32_t* groups, int ngroups, int gsize,
+                              void* stream) {
   SPMD_CHECK_ARG(c && dd, "dot_reduce_scatter arguments");
   SPMD_CHECK_ARG(lhs.dtype == SPMD_BF16 && rhs.dtype == SPMD_BF16 && out.dtype == SPMD_BF16,
                  "dot_reduce_scatter is bf16");
@@ -312,8 +324,30 @@ extern "C" int spmd_dot_reduce_scatter(spmd_comm* c, spmd_tensor lhs, spmd_tenso
   const int64_t nvec = slot / 8;
   peer_slot_reduce_kernel<<<grid_for(nvec, 256), 256, 0, s>>>(
       (const bf16*)(c->heap + CTRL_BYTES), (bf16*)out.data, (const uint32_t*)c->heap, gsize, slot,
-      par_slots, nvec);
+      par_slots, nvec, resid);
   return launched(s);
+}
+
+extern "C" int spmd_dot_reduce_scatter(spmd_comm* c, spmd_tensor lhs, spmd_tensor rhs,
+                                       spmd_tensor out, const spmd_dot_dims* dd, int dim,
+                                       const int32_t* groups, int ngroups, int gsize,
+                                       void* stream) {
+  return dot_reduce_scatter(c, lhs, rhs, nullptr, out, dd, dim, groups, ngroups, gsize, stream);
+}
+
+// The same with the layer's residual Add folded into the slot reduce:
+// out = reduce_scatter(dot) + resid (resid has out's shape), rounded exactly
+// as the unfused reduce-scatter followed by the Add.
+extern "C" int spmd_dot_reduce_scatter_add(spmd_comm* c, spmd_tensor lhs, spmd_tensor rhs,
+                                           spmd_tensor resid, spmd_tensor out,
+                                           const spmd_dot_dims* dd, int dim,
+                                           const int32_t* groups, int ngroups, int gsize,
+                                           void* stream) {
+  SPMD_CHECK_ARG(resid.dtype == SPMD_BF16 && numel(resid) == numel(out) &&
+                     (reinterpret_cast<uintptr_t>(resid.data) & 15) == 0,
+                 "dot_reduce_scatter_add residual");
+  return dot_reduce_scatter(c, lhs, rhs, (const bf16*)resid.data, out, dd, dim, groups, ngroups,
+                            gsize, stream);
 }
 
 // All-gather through the peer heap: stage my shard at `heap_offset`, barrier,

@@ -381,7 +381,7 @@ class Executor:
         depth = max(1, int(os.environ.get("SPMD_PREFETCH_DEPTH", "2")))
         heavy_ops = (Op.DOT, Op.CONVOLUTION)
         heavy_fused = ("dot_relu", "conv_relu", "attention", "dot_rs", "dot_a2a", "halo_conv",
-                       "dot_add")
+                       "dot_add", "dot_rs_add")
 
         def heavy(st):
             f = self._fused.get(st.ins.id)
@@ -502,7 +502,7 @@ class Executor:
         import os
         half = 0
         for spec in self._fused.values():
-            if spec[0] == "dot_rs":
+            if spec[0] in ("dot_rs", "dot_rs_add"):
                 rs = spec[2]
                 half = max(half, rs.shape.num_elements * len(rs.attrs["subgroups"][0]) *
                            rs.shape.dtype.itemsize)
@@ -572,7 +572,8 @@ class Executor:
         # hidden gathers: copy engines (0), background SM pull (3) or NCCL (-1)
         hidden_mode = os.environ.get("SPMD_PEER_HIDDEN_ENGINE", "ce")
         heavy_ops = (Op.DOT, Op.CONVOLUTION)
-        heavy_fused = ("dot_relu", "conv_relu", "attention", "dot_rs", "dot_a2a", "dot_add")
+        heavy_fused = ("dot_relu", "conv_relu", "attention", "dot_rs", "dot_a2a", "dot_add",
+                       "dot_rs_add")
         eng = {}
         order = self.steps
         for i, st in enumerate(order):
@@ -771,7 +772,31 @@ class Executor:
         self._plan_halo_convs(users, outs)
         self._plan_attention(users, outs)
         self._plan_dot_reduce_scatter(users, outs)
+        self._plan_rs_residual_adds(users, outs)
         self._plan_slice_permutes(users, outs)
+
+    def _plan_rs_residual_adds(self, users, outs):
+        """Fused dot -> reduce-scatter whose only user is the layer's residual
+        Add: the add runs in the reduce-scatter's slot reduce
+        (spmd_dot_reduce_scatter_add, same roundings as unfused).
+        SPMD_RS_ADD=0 disables it."""
+        import os
+        if os.environ.get("SPMD_RS_ADD", "1") == "0":
+            return
+        by = self.by_id
+        for add in self.graph.instructions:
+            if add.opcode != Op.ADD or add.shape.dtype != DType.BF16 or add.id in self._fused:
+                continue
+            for k in (0, 1):
+                rsid, r = add.operands[k], add.operands[1 - k]
+                spec = self._fused.get(rsid)
+                if spec is None or spec[0] != "dot_rs" or rsid in outs or r == rsid or \
+                        len(users.get(rsid, [])) != 1 or by[r].shape != add.shape:
+                    continue
+                del self._fused[rsid]
+                self._fused_skip.add(rsid)
+                self._fused[add.id] = ("dot_rs_add", spec[1], spec[2], r)
+                break
 
     def _plan_backward(self, users, outs, only_user, const_value):
         """Training-step backward chains (workloads.transformer_train_step):
@@ -1269,6 +1294,8 @@ class Executor:
             return tuple(f[1]) + (f[3],) + ((mask[2], mask[3]) if mask is not None else ())
         if f[0] in ("moe_dispatch", "moe_combine", "moe_dispatch_a2a"):
             return (f[1],)
+        if f[0] == "dot_rs_add":
+            return tuple(f[1].operands) + (f[3],)
         if f[0] == "ag_split_dot":
             lag, rag, dot = f[1], f[2], f[3]
             return (lag.operands[0] if lag is not None else dot.operands[0],
@@ -1365,6 +1392,8 @@ class Executor:
             return self._conv_step(f[1], epilogue=1)
         if f is not None and f[0] == "halo_conv":
             return self._halo_conv_step(*f[1:])
+        if f is not None and f[0] == "dot_rs_add":
+            return self._dot_rs_step(f[1], f[2], resid=f[3])
         if f is not None and f[0] == "dot_rs":
             return self._dot_rs_step(f[1], f[2])
         if f is not None and f[0] == "dot_a2a":
@@ -1776,7 +1805,7 @@ class Executor:
             return out
         return run
 
-    def _dot_rs_step(self, dot, rs):
+    def _dot_rs_step(self, dot, rs, resid=None):
         lib, comm = self.lib, self.comm
         a, b = dot.operands
         ash, bsh, shp = self._shape(a), self._shape(b), rs.shape
@@ -1787,9 +1816,16 @@ class Executor:
 
         def run(env, s):
             out = self._alloc(shp)
-            C.check(lib.spmd_dot_reduce_scatter(comm.handle, desc(env[a], ash), desc(env[b], bsh),
-                                                desc(out, shp), ref, dim, groups, ng, gs, s),
-                    "dot_reduce_scatter")
+            if resid is None:
+                C.check(lib.spmd_dot_reduce_scatter(comm.handle, desc(env[a], ash),
+                                                    desc(env[b], bsh), desc(out, shp), ref, dim,
+                                                    groups, ng, gs, s), "dot_reduce_scatter")
+            else:
+                C.check(lib.spmd_dot_reduce_scatter_add(comm.handle, desc(env[a], ash),
+                                                        desc(env[b], bsh),
+                                                        desc(env[resid], shp), desc(out, shp),
+                                                        ref, dim, groups, ng, gs, s),
+                        "dot_reduce_scatter_add")
             return out
         return run
 

@@ -143,7 +143,7 @@ def layer(comm, rank, world, dev, mesh, dims, fused_rs, env=None):
             t = torch.from_numpy(np.ascontiguousarray(piece, dtype=np.float32)).to(dev)
         stacked.append(t.to(torch.bfloat16).reshape((1,) + p.shape.dims))
     ex = Executor(prog, nparts=1, device=dev, comm=comm, partition_base=rank, fuse=True)
-    n_rs = sum(1 for v in ex._fused.values() if v[0] == "dot_rs")
+    n_rs = sum(1 for v in ex._fused.values() if v[0] in ("dot_rs", "dot_rs_add"))
     return ex, stacked, n_rs
 
 
@@ -206,7 +206,7 @@ def main():
             t = torch.from_numpy(np.ascontiguousarray(piece, dtype=np.float32)).to(dev)
             txs.append(t.to(torch.bfloat16).reshape((1,) + p.shape.dims))
         tex = Executor(tprog, nparts=1, device=dev, comm=comm, partition_base=rank, fuse=True)
-        n_fused = sum(1 for v in tex._fused.values() if v[0] == "dot_rs")
+        n_fused = sum(1 for v in tex._fused.values() if v[0] in ("dot_rs", "dot_rs_add"))
         res[fusedflag] = ([o.float() for o in tex.run(txs)], n_fused)
     torch.cuda.synchronize()
     terr = max(rel(a, b) for a, b in zip(res[True][0], res[False][0]))

@@ -53,15 +53,17 @@ def _layer(mesh, **env):
 @pytest.mark.parametrize("mesh", [(1, 2), (2, 2), (1, 4), (2, 4)])
 def test_dot_reduce_scatter_fusion_matches_the_two_output_projections(mesh):
     ex, comm = _layer(mesh)
-    rs = {k: v for k, v in ex._fused.items() if v[0] == "dot_rs"}
+    rs = {k: v for k, v in ex._fused.items() if v[0] in ("dot_rs", "dot_rs_add")}
     assert len(rs) == 2   # attention out-projection and FFN-out (2-D finalized)
-    for rid, (_, dot, r) in rs.items():
+    for rid, (kind, dot, r, *resid) in rs.items():
         assert r.opcode == Op.REDUCE_SCATTER and dot.opcode == Op.DOT
         assert r.attrs["dim"] == dot.shape.rank - 1 and r.operands[0] == dot.id
         assert dot.id in ex._fused_skip
         step = next(s for s in ex.steps if s.ins.id == rid)
         assert not step.coll   # runs on the compute stream
-        assert step.ops == dot.operands
+        # both are the layer's residual adds: the add runs in the RS reduce
+        assert kind == "dot_rs_add" and r.id in ex._fused_skip
+        assert step.ops == tuple(dot.operands) + tuple(resid)
     # other fusions still planned
     kinds = {v[0] for v in ex._fused.values()}
     assert {"softmax", "attention", "dot_relu"} <= kinds
@@ -69,7 +71,7 @@ def test_dot_reduce_scatter_fusion_matches_the_two_output_projections(mesh):
 
 def test_peer_fusion_can_be_disabled():
     ex, _ = _layer((2, 2), SPMD_PEER_FUSION="0", SPMD_PEER_AG="0")
-    assert not any(v[0] == "dot_rs" for v in ex._fused.values())
+    assert not any(v[0] in ("dot_rs", "dot_rs_add") for v in ex._fused.values())
     assert ex._peer_ag == {} and ex._peer_engine == {}
     assert sum(1 for s in ex.steps if s.coll and s.ins.opcode == Op.REDUCE_SCATTER) == 2
 
@@ -80,7 +82,7 @@ def test_no_peer_fusion_without_a_communicator():
     ann, _ = propagate(g)
     prog = partition(ann, 4, plan="fast")
     ex = Executor(prog, nparts=4, device="cpu", fuse=True, overlap=False)
-    assert not any(v[0] == "dot_rs" for v in ex._fused.values())
+    assert not any(v[0] in ("dot_rs", "dot_rs_add") for v in ex._fused.values())
     assert ex._peer_ag == {}
 
 
@@ -88,7 +90,8 @@ def test_no_peer_fusion_without_a_communicator():
 def test_peer_heap_layout_is_disjoint_and_aligned(mesh):
     ex, comm = _layer(mesh)
     rs_bytes = max(2 * r.shape.num_elements * len(r.attrs["subgroups"][0]) * 2
-                   for _, _, r in (v for v in ex._fused.values() if v[0] == "dot_rs"))
+                   for _, _, r, *_ in (v for v in ex._fused.values()
+                                       if v[0] in ("dot_rs", "dot_rs_add")))
     spans = []
     for aid, off in ex._peer_ag.items():
         ins = ex.by_id[aid]
@@ -122,7 +125,7 @@ def test_engine_policy_under_overlap():
             between = ex.steps[i + 1:first_use]
             hidden = any(not s.coll and (s.ins.opcode == Op.DOT or
                                          (ex._fused.get(s.ins.id) or ("",))[0] in
-                                         ("dot_relu", "attention", "dot_rs"))
+                                         ("dot_relu", "attention", "dot_rs", "dot_rs_add"))
                          for s in between)
             assert e == (0 if hidden else (1 if gs <= 2 else -1)), (mesh, aid)
         # the weight gathers of the later projections are hidden, the first
@@ -143,7 +146,7 @@ def test_training_step_gradient_reduce_scatters_all_fuse(mesh):
     ex = Executor(prog, nparts=1, device="cpu", comm=comm, partition_base=0, fuse=True,
                   overlap=False)
     rs = [i for i in prog.graph.instructions if i.opcode == Op.REDUCE_SCATTER]
-    fused = {k: v for k, v in ex._fused.items() if v[0] == "dot_rs"}
+    fused = {k: v for k, v in ex._fused.items() if v[0] in ("dot_rs", "dot_rs_add")}
     assert len(rs) == 12 and len(fused) == 12
     dims = {v[2].attrs["dim"] for v in fused.values()}
     assert 0 in dims and any(d > 0 for d in dims)
@@ -162,7 +165,7 @@ def _check_fused_parity_layout(ex, comm):
     assert H > 0 and ex._fused_half == H
     sizes = set()
     for kind, *spec in ex._fused.values():
-        if kind == "dot_rs":
+        if kind in ("dot_rs", "dot_rs_add"):
             rs = spec[1]
             u, n = rs.shape.nbytes, len(rs.attrs["subgroups"][0])
         elif kind == "dot_a2a":
