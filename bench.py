@@ -861,6 +861,11 @@ def main():
     # ---- reshard GB/s (config C5) at N > 1 ----
     reshard = None
     if world > 1 and args.config == "c2":
+        # settle after the tensor-core configs: run straight after C1 the
+        # all-to-all measured 549 GB/s/GPU at N=4, 650 on its own
+        # (scripts/reshard_probe.py, profiles/r2_reshard_probe_n4.log)
+        torch.cuda.synchronize()
+        time.sleep(1.0)
         reshard = _reshard(world, rank, dev, comm, barrier)
 
     cpu = None
