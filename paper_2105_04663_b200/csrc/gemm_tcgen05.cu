@@ -730,7 +730,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
     }
   } else if (warp == 1 && lane == 0 && leader) {
     // ---------------- MMA issuer (leader CTA only) ----------------
+    // Descriptors are precomputed and advanced by constant offsets (the
+    // 14-bit start field is addr >> 4; smem < 256 KB never carries out of
+    // it).  Running the loop on the whole warp with one elected issuer (the
+    // conv kernel's scheme, where a UMMA is only 64 tensor cycles) measured
+    // no gain here (UMMA 256x256x16 = 128 cycles): -9% .. +2% per shape,
+    // C2 step within noise (profiles/r2_gemm_ab_mmawarp.log).
     const uint32_t idesc = make_idesc(BM2, WHALF_N, g.a_mn, g.b_mn);
+    const uint32_t s0 = smem_u32(smem);
+    const uint64_t a0 = g.a_mn ? make_desc(s0, BK * 128, 1024) : make_desc(s0, 16, 1024);
+    const uint64_t b0 = g.b_mn ? make_desc(s0 + L::A_BYTES, BK * 128, 1024)
+                               : make_desc(s0 + L::A_BYTES, 16, 1024);
+    const uint32_t ka = g.a_mn ? (2048 >> 4) : (32 >> 4), kb16 = g.b_mn ? (2048 >> 4) : (32 >> 4);
+    constexpr uint32_t STAGE16 = L::STAGE_BYTES >> 4, BJ16 = (HALF * BK * 2) >> 4;
     int s = 0;
     uint32_t ph = 0;
     uint32_t acc_ph = 0;
@@ -745,21 +757,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
       for (int kb = 0; kb < kblocks; ++kb) {
         mbar_wait(&full[s], ph);
         tc_fence_after();
-        const uint32_t sa = smem_u32(smem + s * L::STAGE_BYTES);
-        const uint32_t sb = sa + L::A_BYTES;
+        {
+          const uint64_t ad = a0 + (uint64_t)(s * STAGE16), bd = b0 + (uint64_t)(s * STAGE16);
 #pragma unroll
-        for (int k = 0; k < BK / 16; ++k) {
-          const uint64_t ad = g.a_mn ? make_desc(sa + k * 2048, BK * 128, 1024)
-                                     : make_desc(sa + k * 32, 16, 1024);
+          for (int k = 0; k < BK / 16; ++k) {
 #pragma unroll
-          for (int j = 0; j < 2; ++j) {
-            const uint32_t sbj = sb + j * (HALF * BK * 2);
-            const uint64_t bd = g.b_mn ? make_desc(sbj + k * 2048, BK * 128, 1024)
-                                       : make_desc(sbj + k * 32, 16, 1024);
-            tc_mma_2sm(tmem + j * WHALF_N, ad, bd, idesc, (kb | k) != 0);
+            for (int j = 0; j < 2; ++j)
+              tc_mma_2sm(tmem + j * WHALF_N, ad + (uint64_t)(k * ka),
+                         bd + (uint64_t)(j * BJ16 + k * kb16), idesc, (kb | k) != 0);
           }
+          tc_commit_2sm_mc(&empty[s]);
         }
-        tc_commit_2sm_mc(&empty[s]);
         if (++s == STAGES) {
           s = 0;
           ph ^= 1;
