@@ -32,6 +32,7 @@ from typing import Mapping, Optional, Sequence
 import numpy as np
 
 from . import _capi as C
+from . import knobs as _knobs
 from .ir import (COLLECTIVES, ELEMENTWISE_BINARY, ELEMENTWISE_UNARY,
                  CompareDirection, DType, Graph, Instruction, Op, ReduceKind,
                  Shape, np_dtype)
@@ -207,9 +208,12 @@ class Executor:
     def __init__(self, program, nparts: Optional[int] = None, device=None,
                  comm: Optional[NcclComm] = None, partition_base: int = 0,
                  fuse: bool = False, overlap: Optional[bool] = None,
-                 routing: Optional[Mapping[int, "Routing"]] = None):
+                 routing: Optional[Mapping[int, "Routing"]] = None,
+                 knobs: Optional[Mapping[str, object]] = None):
         torch = _torch()
         self.lib = C.lib()
+        # plan knobs (knobs.py): environment / overrides, read once here
+        self._knobs = _knobs.resolve(knobs)
         # Collectives on a dedicated stream, hoisted to issue as soon as
         # their operands exist (weight all-gathers prefetch under GEMMs).
         self.overlap = (comm is not None) if overlap is None else overlap
@@ -236,8 +240,7 @@ class Executor:
         self.comm_streams = []
         if self.overlap:
             self.steps = self._hoist_collectives(self.steps)
-            import os
-            prio = int(os.environ.get("SPMD_COMM_PRIORITY", "0"))
+            prio = int(self._knob("SPMD_COMM_PRIORITY"))
             self.comm_stream = torch.cuda.Stream(device=self.device, priority=prio)
             self.comm_streams = [self.comm_stream]
         if comm is not None:
@@ -265,6 +268,9 @@ class Executor:
         self._assign_lanes()
         self._lane_of = {st.cuda_stream: k + 1 for k, st in enumerate(self.comm_streams)}
 
+
+    def _knob(self, name: str) -> str:
+        return self._knobs[name]
     def _plan_staged_gathers(self) -> dict:
         """Peer all-gathers of parameters (the weight gathers, GSPMD's
         2-D-finalized weight AG over X) -> pre-staged copy-engine pulls
@@ -275,20 +281,19 @@ class Executor:
         step end keeps the slots until every member has pulled.
         Returns {all-gather id: parameter index}.  SPMD_PEER_STAGE=0
         disables it."""
-        import os
-        if not self.comm_streams or os.environ.get("SPMD_PEER_STAGE", "1") == "0":
+        if not self.comm_streams or self._knob("SPMD_PEER_STAGE") == "0":
             return {}
         pids = [p.id for p in self.params]
         staged = {}
-        wide = os.environ.get("SPMD_PEER_STAGE_WIDE", "1") == "1"
+        wide = self._knob("SPMD_PEER_STAGE_WIDE") == "1"
         # exposed parameter gathers: pushed from the parameter itself
         # (peer_push_kernel, 661 / 677 GB/s per GPU at N=2 / 4 vs 463 / 342
         # for staged pulls: profiles/r2_bench_n{2,4}_final.log) unless
         # SPMD_PEER_AG_PUSH_PARAMS=0
-        push_params = os.environ.get("SPMD_PEER_AG_PUSH", "1") != "0" and \
-            os.environ.get("SPMD_PEER_AG_PUSH_PARAMS", "1") != "0"
+        push_params = self._knob("SPMD_PEER_AG_PUSH") != "0" and \
+            self._knob("SPMD_PEER_AG_PUSH_PARAMS") != "0"
         # activation staging measured slower (profiles/r1_c2_n4_ab_stage_act.log)
-        act = os.environ.get("SPMD_PEER_STAGE_ACT", "0") == "1"
+        act = self._knob("SPMD_PEER_STAGE_ACT") == "1"
         for aid in self._peer_ag:
             src = self.by_id[self.by_id[aid].operands[0]]
             if src.opcode != Op.PARAMETER:
@@ -316,9 +321,8 @@ class Executor:
         step's first x / weight gathers -- get a push landing zone after the
         heap regions _peer_bytes laid out; every member pushes its shard
         straight from the parameter (spmd_peer_push_all_gather)."""
-        import os
-        if os.environ.get("SPMD_PEER_AG_PUSH", "1") == "0" or \
-                os.environ.get("SPMD_PEER_AG_PUSH_PARAMS", "1") == "0":
+        if self._knob("SPMD_PEER_AG_PUSH") == "0" or \
+                self._knob("SPMD_PEER_AG_PUSH_PARAMS") == "0":
             return
         pids = {p.id for p in self.params}
         off = self._peer_bytes_used
@@ -335,8 +339,7 @@ class Executor:
     def _stage_phases(self) -> list:
         """Staging order: exposed gathers' shards, then the rest
         (SPMD_STAGE_PHASES=1: one phase)."""
-        import os
-        if os.environ.get("SPMD_STAGE_PHASES", "2") == "1":
+        if self._knob("SPMD_STAGE_PHASES") == "1":
             return [list(self._staged)]
         first = [a for a in self._staged if a in self._staged_exposed]
         rest = [a for a in self._staged if a not in self._staged_exposed]
@@ -354,11 +357,10 @@ class Executor:
         them (default 2; 0 when the weight gathers are pre-staged and need
         no kernel, since a reserved pair costs a GEMM whose tile count is a
         multiple of 74 pairs up to one extra tile round)."""
-        import os
         if not self.comm_streams or self.comm is None or \
                 not any(st.coll for st in self.steps):
             return 0
-        reserve = int(os.environ.get("SPMD_COMM_SMS", "0" if self._staged else "2"))
+        reserve = int((self._knob("SPMD_COMM_SMS") or ("0" if self._staged else "2")))
         if reserve <= 0:
             return 0
         sms = _torch().cuda.get_device_properties(self.device).multi_processor_count
@@ -373,12 +375,11 @@ class Executor:
         2x2 the first critical gather took 0.50 instead of ~0.17 ms,
         profiles/r1_timeline_c2_n4_wide.log).  SPMD_PREFETCH=asap keeps the
         hoisted order."""
-        import os
-        if os.environ.get("SPMD_PREFETCH", "jit") == "asap":
+        if self._knob("SPMD_PREFETCH") == "asap":
             return steps
         # GEMMs ahead: 2 measured best at C2 2x2 (15.28 ms vs 15.76 for 1 and
         # 15.56-16.81 for as-soon-as-possible, profiles/r1_c2_n4_ab_wide_lanes_engines.log)
-        depth = max(1, int(os.environ.get("SPMD_PREFETCH_DEPTH", "2")))
+        depth = max(1, int(self._knob("SPMD_PREFETCH_DEPTH")))
         heavy_ops = (Op.DOT, Op.CONVOLUTION)
         heavy_fused = ("dot_relu", "conv_relu", "attention", "dot_rs", "dot_a2a", "halo_conv",
                        "dot_add", "dot_rs_add")
@@ -425,10 +426,9 @@ class Executor:
         (profiles/r1_timeline_c2_n4_wide.log).  SPMD_COMM_LANES=1: one lane;
         =2: alternate all peer gathers (measured slower); default "critical".
         """
-        import os
         if not self.comm_streams:
             return
-        mode = os.environ.get("SPMD_COMM_LANES", "critical")
+        mode = self._knob("SPMD_COMM_LANES")
         nxt = 0
         npush = ncp = 0
         pids = {p.id for p in self.params}
@@ -450,10 +450,10 @@ class Executor:
                 # profiles/r2_timeline_c2_2x2.log).  SPMD_STAGE_PHASES=1:
                 # alternate lanes 2 and 1 (round 1)
                 k = self._staged_exposed.index(st.ins.id) % 2
-                if os.environ.get("SPMD_STAGE_PHASES", "2") == "1":
+                if self._knob("SPMD_STAGE_PHASES") == "1":
                     st.lane = 2 - k
                 else:
-                    st.lane = 2 + (k if os.environ.get("SPMD_EXPOSED_SPLIT", "1") != "0" else 0)
+                    st.lane = 2 + (k if self._knob("SPMD_EXPOSED_SPLIT") != "0" else 0)
             elif mode == "critical" and eng in (1, -1) and st.ins.id in self._peer_agp and \
                     self.by_id[st.ins.id].operands[0] in pids:
                 # exposed parameter gathers on the push engine (the step's
@@ -463,7 +463,7 @@ class Executor:
                 # concurrent: first GEMM 0.12 ms earlier in the eager
                 # timeline, r2_timeline_c2_n4_lanes.log; graph-replayed step
                 # within noise, 13.67 vs 13.71 ms: r2_ab_exposed_split_push.log)
-                st.lane = 2 + (npush % 2 if os.environ.get("SPMD_EXPOSED_SPLIT", "1") != "0"
+                st.lane = 2 + (npush % 2 if self._knob("SPMD_EXPOSED_SPLIT") != "0"
                                else 0)
                 npush += 1
             elif mode == "critical" and st.ins.opcode == Op.COLLECTIVE_PERMUTE and \
@@ -472,7 +472,7 @@ class Executor:
                 # go out on lanes 2 and 3 at once (one lane ran them back to
                 # back, ~0.03 ms each per layer at C4 N=4:
                 # profiles/r2_timeline_c4_n4.log)
-                st.lane = 2 + (ncp % 2 if os.environ.get("SPMD_EXPOSED_SPLIT", "1") != "0"
+                st.lane = 2 + (ncp % 2 if self._knob("SPMD_EXPOSED_SPLIT") != "0"
                                else 0)
                 ncp += 1
             elif mode == "critical" and eng not in (0, 3, 4):
@@ -499,7 +499,6 @@ class Executor:
         uses the same parity stride: peer.cu fused_parity), then one staging
         slot per peer all-gather and one landing slot per peer permute
         (offsets recorded in ``self._peer_ag`` / ``self._peer_cp``)."""
-        import os
         half = 0
         for spec in self._fused.values():
             if spec[0] in ("dot_rs", "dot_rs_add"):
@@ -515,7 +514,7 @@ class Executor:
         self._fused_half = half
         off = 3 * half
         self._peer_ag = {}
-        if os.environ.get("SPMD_PEER_AG", "1") != "0":
+        if self._knob("SPMD_PEER_AG") != "0":
             for ins in self.graph.instructions:
                 if ins.opcode == Op.ALL_GATHER and ins.id not in self._fused_skip:
                     self._peer_ag[ins.id] = off
@@ -530,7 +529,7 @@ class Executor:
         # (parameter gathers left on the critical path get theirs later,
         # _add_param_push_zones, once the engines are planned)
         self._peer_agp = {}
-        if os.environ.get("SPMD_PEER_AG_PUSH", "1") != "0":
+        if self._knob("SPMD_PEER_AG_PUSH") != "0":
             pids = {p.id for p in self.params}
             for ins in self.graph.instructions:
                 if ins.opcode == Op.ALL_GATHER and ins.id not in self._fused_skip and \
@@ -542,7 +541,7 @@ class Executor:
         # pushes its piece there (spmd_peer_all_to_all), and the zone is the
         # value the consumers read
         self._peer_a2a = {}
-        if os.environ.get("SPMD_PEER_A2A", "1") != "0":
+        if self._knob("SPMD_PEER_A2A") != "0":
             for ins in self.graph.instructions:
                 if ins.opcode == Op.ALL_TO_ALL and ins.id not in self._fused_skip and \
                         ins.id not in self._fused:
@@ -551,7 +550,7 @@ class Executor:
         # collective-permutes (halo exchanges, pipeline shifts): one landing
         # slot each, written by the source rank's copy engine
         self._peer_cp = {}
-        if os.environ.get("SPMD_PEER_CP", "1") != "0":
+        if self._knob("SPMD_PEER_CP") != "0":
             for ins in self.graph.instructions:
                 if ins.opcode == Op.COLLECTIVE_PERMUTE and ins.id not in self._fused_skip:
                     self._peer_cp[ins.id] = off
@@ -567,10 +566,9 @@ class Executor:
         groups, where its NVLink-multicast all-gather out-runs point-to-point
         pulls (profiles/r1_peer_ag_bench_n4.jsonl).  SPMD_PEER_AG_ENGINE=ce|sm
         forces one."""
-        import os
-        force = os.environ.get("SPMD_PEER_AG_ENGINE", "auto")
+        force = self._knob("SPMD_PEER_AG_ENGINE")
         # hidden gathers: copy engines (0), background SM pull (3) or NCCL (-1)
-        hidden_mode = os.environ.get("SPMD_PEER_HIDDEN_ENGINE", "ce")
+        hidden_mode = self._knob("SPMD_PEER_HIDDEN_ENGINE")
         heavy_ops = (Op.DOT, Op.CONVOLUTION)
         heavy_fused = ("dot_relu", "conv_relu", "attention", "dot_rs", "dot_a2a", "dot_add",
                        "dot_rs_add")
@@ -625,7 +623,6 @@ class Executor:
         return users
 
     def _plan_fusions(self):
-        import os
         users = self._users()
         outs = set(self.graph.outputs)
         by = self.by_id
@@ -699,7 +696,7 @@ class Executor:
             if ins.opcode == Op.TRANSPOSE and only_user(ins.id, Op.RELU) and \
                     ins.shape.dtype in (DType.F32, DType.BF16, DType.S32) and \
                     ins.id not in self._fused and ins.id not in self._fused_skip and \
-                    os.environ.get("SPMD_TRANSPOSE_RELU", "1") != "0":
+                    self._knob("SPMD_TRANSPOSE_RELU") != "0":
                 relu = by[users[ins.id][0]]
                 src = self._fused.get(ins.operands[0])
                 if relu.id in self._fused:
@@ -722,7 +719,7 @@ class Executor:
             if ins.opcode == Op.DOT and self.comm is None and ins.shape.dtype == DType.F32 and \
                     ins.id not in self._fused and ins.id not in self._fused_skip and \
                     ins.operands[0] != ins.operands[1] and \
-                    os.environ.get("SPMD_AG_SPLIT", "1") != "0":
+                    self._knob("SPMD_AG_SPLIT") != "0":
                 def gathered(vid):
                     a = by[vid]
                     return a if a.opcode == Op.ALL_GATHER and a.shape.dtype == DType.F32 and \
@@ -743,7 +740,7 @@ class Executor:
             # not take it
             if ins.opcode == Op.ADD and ins.shape.dtype == DType.BF16 and \
                     ins.id not in self._fused and \
-                    os.environ.get("SPMD_DOT_ADD", "1") != "0":
+                    self._knob("SPMD_DOT_ADD") != "0":
                 for k in (0, 1):
                     d, r = ins.operands[k], ins.operands[1 - k]
                     dot = by[d]
@@ -780,8 +777,7 @@ class Executor:
         Add: the add runs in the reduce-scatter's slot reduce
         (spmd_dot_reduce_scatter_add, same roundings as unfused).
         SPMD_RS_ADD=0 disables it."""
-        import os
-        if os.environ.get("SPMD_RS_ADD", "1") == "0":
+        if self._knob("SPMD_RS_ADD") == "0":
             return
         by = self.by_id
         for add in self.graph.instructions:
@@ -809,8 +805,7 @@ class Executor:
           epilogue and the mask reads ``relu(h) > 0`` (the same predicate,
           NaN included) so ``h`` is never written.
         SPMD_BWD_FUSION=0 disables both."""
-        import os
-        if os.environ.get("SPMD_BWD_FUSION", "1") == "0":
+        if self._knob("SPMD_BWD_FUSION") == "0":
             return
         by = self.by_id
 
@@ -878,8 +873,7 @@ class Executor:
         (formatting.py:54-182 exchange_and_slice).  With a multi-process
         communicator the peer permute writes the slab rows straight from the
         sliced tensor (spmd_peer_slice_collective_permute)."""
-        import os
-        if self.comm is None or self.P != 1 or os.environ.get("SPMD_PEER_CP", "1") == "0":
+        if self.comm is None or self.P != 1 or self._knob("SPMD_PEER_CP") == "0":
             return
         by = self.by_id
         for cp in self.graph.instructions:
@@ -920,8 +914,7 @@ class Executor:
         window buffer; unpack bytes 0 when fused into the conv
         loader).  Needs a zero mask fill (masked rows load as TMA zeros).
         SPMD_HALO_CONV=0 disables it."""
-        import os
-        if os.environ.get("SPMD_HALO_CONV", "1") == "0":
+        if self._knob("SPMD_HALO_CONV") == "0":
             return
         by = self.by_id
         for ds_id, spec in list(self._fused.items()):
@@ -977,8 +970,7 @@ class Executor:
         """Dot whose only user is a sum reduce-scatter of its last dim (the
         rhs free dim) -> one GEMM with a peer-store epilogue (peer.cu).  Only
         with a multi-process communicator; SPMD_PEER_FUSION=0 disables."""
-        import os
-        if self.comm is None or os.environ.get("SPMD_PEER_FUSION", "1") == "0":
+        if self.comm is None or self._knob("SPMD_PEER_FUSION") == "0":
             return
         by = self.by_id
         for rs in self.graph.instructions:
@@ -1064,8 +1056,7 @@ class Executor:
         """Dot(q,k) -> fused softmax -> Dot(probs, v) with the Transformer
         layouts q/k/v [B,S|T,N,D], logits [B,N,S,T], ctx [B,N,S,D] -> one
         flash-attention kernel (tcgen05; no logits in HBM)."""
-        import os
-        if os.environ.get("SPMD_FUSED_ATTENTION", "1") == "0":
+        if self._knob("SPMD_FUSED_ATTENTION") == "0":
             return
         by = self.by_id
         for div_id, spec in list(self._fused.items()):
