@@ -2145,40 +2145,82 @@ class Executor:
             C.check(self.lib.spmd_peer_barrier(self.comm.handle, self._lane_of[st.cuda_stream],
                                                compute.cuda_stream), "peer_barrier")
 
-    def timeline(self, inputs) -> list[dict]:
-        """Eager run with CUDA events around every step on the stream it is
-        issued to; returns [{id, op, stream, start_ms, end_ms}] relative to
-        the first event (diagnostics: compute-stream gaps = exposed comm)."""
+    def timeline(self, inputs, graph: bool = False, replays: int = 5) -> list[dict]:
+        """Run with CUDA events around every step on the stream it is issued
+        to; returns [{id, op, stream, start_ms, end_ms}] relative to the
+        first event (diagnostics: compute-stream gaps = exposed comm).
+        ``graph``: the events become external event-record nodes of a
+        captured CUDA graph (cudaEventRecordExternal) and the times are those
+        of the last of ``replays`` back-to-back replays -- the timed step of
+        bench.py, not the eager run."""
         torch = _torch()
         marks = []
         orig = [s.fn for s in self.steps]
         compute = torch.cuda.current_stream(self.device)
+        if graph:
+            rt = ctypes.CDLL("libcudart.so.12")
+
+            def event():
+                e = ctypes.c_void_p()
+                assert rt.cudaEventCreate(ctypes.byref(e)) == 0
+                return e
+
+            def record(e, st):
+                assert rt.cudaEventRecordWithFlags(e, ctypes.c_void_p(st.cuda_stream), 1) == 0
+
+            def elapsed(a, b):
+                ms = ctypes.c_float()
+                assert rt.cudaEventElapsedTime(ctypes.byref(ms), a, b) == 0
+                return ms.value
+        else:
+            def event():
+                return torch.cuda.Event(enable_timing=True)
+
+            def record(e, st):
+                e.record(st)
+
+            def elapsed(a, b):
+                return a.elapsed_time(b)
 
         def wrap(step, fn):
             def run(env, s):
-                st = self.comm_streams[step.lane - 1] if (step.coll and step.lane) else compute
-                e0 = torch.cuda.Event(enable_timing=True)
-                e1 = torch.cuda.Event(enable_timing=True)
-                e0.record(st)
+                cur = torch.cuda.current_stream(self.device)
+                st = self.comm_streams[step.lane - 1] if (step.coll and step.lane) else cur
+                e0, e1 = event(), event()
+                record(e0, st)
                 out = fn(env, s)
-                e1.record(st)
+                record(e1, st)
                 marks.append((step.ins.id, step.ins.opcode.value,
-                              f"comm{step.lane}" if st is not compute else "compute", e0, e1))
+                              f"comm{step.lane}" if st is not cur else "compute", e0, e1))
                 return out
             return run
 
+        if graph:
+            self.run(inputs)
+            torch.cuda.synchronize(self.device)
         for s, f in zip(self.steps, orig):
             s.fn = wrap(s, f)
         try:
-            t0 = torch.cuda.Event(enable_timing=True)
-            t0.record(compute)
-            self.run(inputs)
+            t0 = event()
+            if graph:
+                g = torch.cuda.CUDAGraph()
+                cap = torch.cuda.Stream(device=self.device)
+                cap.wait_stream(compute)
+                with torch.cuda.graph(g, stream=cap):
+                    record(t0, cap)
+                    self.run(inputs)
+                torch.cuda.synchronize(self.device)
+                for _ in range(replays):
+                    g.replay()
+            else:
+                record(t0, compute)
+                self.run(inputs)
             torch.cuda.synchronize(self.device)
         finally:
             for s, f in zip(self.steps, orig):
                 s.fn = f
-        return [{"id": i, "op": o, "stream": st, "start_ms": t0.elapsed_time(a),
-                 "end_ms": t0.elapsed_time(b)} for i, o, st, a, b in marks]
+        return [{"id": i, "op": o, "stream": st, "start_ms": elapsed(t0, a),
+                 "end_ms": elapsed(t0, b)} for i, o, st, a, b in marks]
 
     def capture(self, inputs):
         """Capture one execution into a CUDA graph (after an eager warm-up
