@@ -189,6 +189,26 @@ def main():
                 failed.append(f"layer_small{lm}:{eng}")
             del ex1, ex0, x1, x0
 
+    # residual Add inside the reduce-scatter's slot reduce (dot_rs_add) vs
+    # the reduce-scatter then the Add: same roundings, so bit-identical
+    for lm in meshes:
+        ex1, x1, n1 = layer(comm, rank, world, dev, lm, small, True, {"SPMD_RS_ADD": "1"})
+        ex0, x0, _ = layer(comm, rank, world, dev, lm, small, True, {"SPMD_RS_ADD": "0"})
+        n_add = sum(1 for v in ex1._fused.values() if v[0] == "dot_rs_add")
+        a = ex1.run(x1)[0]
+        b = ex0.run(x0)[0]
+        torch.cuda.synchronize()
+        same = bool(torch.equal(a, b))
+        alls = [None] * world
+        dist.all_gather_object(alls, same)
+        if rank == 0:
+            print(json.dumps({"section": "rs_add_bitwise", "mesh": lm, "dot_rs_add": n_add,
+                              "bit_identical_all_ranks": all(alls)}), flush=True)
+        if not (all(alls) and n_add == 2):
+            failed.append(f"rs_add_bitwise{lm}")
+        os.environ.pop("SPMD_RS_ADD", None)
+        del ex1, ex0, x1, x0
+
     # training step (forward + backward): all weight-gradient reduce-scatters
     # fused (row and column splits) vs NCCL
     from paper_2105_04663_b200.workloads import train_step_inputs, transformer_train_step
