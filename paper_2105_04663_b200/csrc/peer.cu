@@ -679,29 +679,59 @@ struct PushArgs {
 };
 
 template <typename T, int V>
+__device__ __forceinline__ void push_offsets(const PushArgs& a, int j, int64_t v, int64_t& so,
+                                             int64_t& d0) {
+  int64_t r = v * V;
+  so = a.sbase[j];
+  d0 = a.dbase;
+#pragma unroll
+  for (int k = SPMD_MAX_RANK - 1; k >= 0; --k) {
+    if (k < a.rank) {
+      const int64_t ck = r % a.shape[k];
+      r /= a.shape[k];
+      so += ck * a.sst[k];
+      d0 += ck * a.dst[k];
+    }
+  }
+}
+
+// U vectors per thread per chunk (chunk = 256 * U vectors of one piece):
+// the U loads are all issued before the U NVLink stores.
+template <typename T, int V, int U>
 __global__ void __launch_bounds__(256) peer_push_kernel(const T* __restrict__ src, PushArgs a) {
   const int64_t per = a.n / V;                       // vectors per piece
-  const int64_t chunks = (per + 255) / 256;           // 256-vector chunks per piece
+  const int64_t chunks = (per + 256 * U - 1) / (256 * U);
   const int64_t total = chunks * a.G;
   for (int64_t c = blockIdx.x; c < total; c += gridDim.x) {
     const int j = (int)(c % a.G);
-    const int64_t v = (c / a.G) * 256 + threadIdx.x;
-    if (v >= per) continue;
-    int64_t r = v * V, so = a.sbase[j], d0 = a.dbase;
-#pragma unroll
-    for (int k = SPMD_MAX_RANK - 1; k >= 0; --k) {
-      if (k < a.rank) {
-        const int64_t ck = r % a.shape[k];
-        r /= a.shape[k];
-        so += ck * a.sst[k];
-        d0 += ck * a.dst[k];
-      }
-    }
+    const int64_t v0 = (c / a.G) * (256 * U) + threadIdx.x;
     T* dst = reinterpret_cast<T*>(a.out[j]);
-    if (V == 1)
-      dst[d0] = src[so];
-    else
-      *reinterpret_cast<uint4*>(dst + d0) = __ldcs(reinterpret_cast<const uint4*>(src + so));
+    if (V == 1) {
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t v = v0 + u * 256;
+        if (v >= per) break;
+        int64_t so, d0;
+        push_offsets<T, V>(a, j, v, so, d0);
+        dst[d0] = src[so];
+      }
+    } else {
+      uint4 val[U];
+      int64_t dof[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t v = v0 + u * 256;
+        dof[u] = -1;
+        if (v < per) {
+          int64_t so;
+          push_offsets<T, V>(a, j, v, so, dof[u]);
+          val[u] = __ldcs(reinterpret_cast<const uint4*>(src + so));
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (dof[u] >= 0) *reinterpret_cast<uint4*>(dst + dof[u]) = val[u];
+    }
   }
   __threadfence_system();   // peer stores visible before the barrier signal
 }
@@ -752,14 +782,22 @@ static int peer_push(spmd_comm* c, const spmd_tensor& in, const spmd_tensor& zon
   for (int k = 0; vec && k < r - 1; ++k) vec = a.sst[k] % V == 0 && a.dst[k] % V == 0;
   for (int j = 0; vec && j < gsize; ++j) vec = a.sbase[j] % V == 0;
   const int64_t vecs = vec ? a.n / V : a.n;
-  int64_t grid = ((vecs + 255) / 256) * gsize;
-  if (grid > 148LL * 16) grid = 148LL * 16;
+  // 4 vectors per thread per chunk (loads before stores).  Grid cap by size
+  // (scripts/push_size_probe.py, profiles/r2_push_ilp*_probe.log): 8 blocks
+  // per SM for pushes under 256 MB (33.5 MB piece 0.069 vs 0.083 ms with 16;
+  // the C2 2x2 step-start pair 0.154 vs 0.182), 16 above (536 MB piece:
+  // 669 vs 650 GB/s).
+  constexpr int PU = 4;
+  int64_t grid = ((vecs + 256 * PU - 1) / (256 * PU)) * gsize;
+  const int64_t cap = a.n * elem_size(in.dtype) * gsize >= (256LL << 20) ? 148LL * 16 : 148LL * 8;
+  if (grid > cap) grid = cap;
   if (grid < 1) grid = 1;
   SPMD_DISPATCH_BYTES(in.dtype, T, {
     if (vec)
-      peer_push_kernel<T, 16 / sizeof(T)><<<(unsigned)grid, 256, 0, s>>>((const T*)in.data, a);
+      peer_push_kernel<T, 16 / sizeof(T), PU><<<(unsigned)grid, 256, 0, s>>>((const T*)in.data,
+                                                                              a);
     else
-      peer_push_kernel<T, 1><<<(unsigned)grid, 256, 0, s>>>((const T*)in.data, a);
+      peer_push_kernel<T, 1, PU><<<(unsigned)grid, 256, 0, s>>>((const T*)in.data, a);
   });
   return launched(s);
 }
